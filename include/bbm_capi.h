@@ -1,0 +1,162 @@
+/* bbm_capi.h — C ABI of libbbm, the B200-native Binary Block Masking engine.
+ *
+ * This is the drop-in boundary below the reference's C++ API (namespace blockmask in
+ * /root/reference/proj/include/blockmask). Plain pointers and sizes only; no torch or C++ types.
+ * The C++ drop-in headers in include/blockmask/ and the Python package
+ * paper_2409_15097_b200/ both bind exactly these symbols.
+ *
+ * Each entry point names the reference interface it replaces (file:line under proj/include).
+ * Error convention: every call returns a bbm_status; on failure bbm_last_error() holds a
+ * thread-local message. BBM_ERR_INVALID corresponds to the reference's
+ * require() -> std::invalid_argument (matrix.hpp:47-49) and is raised on the same triggers
+ * (engine.hpp:244-258, 493-496); the C++ wrappers rethrow it as std::invalid_argument.
+ * There is no CPU fallback: compute entry points fail with BBM_ERR_CUDA when no device exists.
+ *
+ * Mask layout (input): the reference's bit-packed rows, u64 words, words_per_row = ceil(n/64),
+ * bit j of row i at word j>>6 bit j&63, tail bits zero (mask.hpp:17-52); or a dense n x n bool
+ * (uint8) mask on the device. Attention tensors: bf16 [slots][n][d], d in {64,128}, row-major.
+ */
+#ifndef BBM_CAPI_H
+#define BBM_CAPI_H
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define BBM_ABI_VERSION 1
+
+typedef enum {
+  BBM_OK = 0,
+  BBM_ERR_INVALID = 1,     /* bad argument: reference would throw std::invalid_argument */
+  BBM_ERR_CUDA = 2,        /* CUDA runtime / device failure (including "no device") */
+  BBM_ERR_UNSUPPORTED = 3, /* valid for the reference, not for the sm_100a kernel (e.g. d=5) */
+  BBM_ERR_INTERNAL = 4
+} bbm_status;
+
+/* Variant (engine.hpp:21-26); same numbering as the reference enum. */
+typedef enum {
+  BBM_VARIANT_DENSE = 0,
+  BBM_VARIANT_NAIVE = 1,
+  BBM_VARIANT_BINBLK = 2,
+  BBM_VARIANT_DENSE_BINBLK = 3
+} bbm_variant;
+
+/* BlockStats (mask.hpp:156-162) */
+typedef struct {
+  uint64_t blocks_total, blocks_nonzero, blocks_full;
+  double block_density, element_density;
+} bbm_block_stats;
+
+/* EngineCounters (engine.hpp:49-66) */
+typedef struct {
+  uint64_t blocks_visited, blocks_processed, mask_block_reads, skipped_by_binblk,
+      skipped_mask_reads_by_run;
+} bbm_counters;
+
+typedef struct {
+  uint64_t n, block_i, block_j, rows, cols; /* caller's BlockSpec view (BlockSums geometry) */
+  uint32_t ktile, krows, kcols;             /* attention kernel's 128x128 view */
+  uint64_t knnz, kfull;                     /* occupied / full tiles in the kernel view */
+  int device;
+} bbm_prep_info;
+
+/* Opaque MaskPrep (engine.hpp:71-78): host copies of sums/occupancy/runs/stats plus the
+ * device-resident kernel metadata (compacted tile lists, tile-major partial bitmaps). */
+typedef struct bbm_prep_s* bbm_prep;
+
+int bbm_abi_version(void);
+const char* bbm_last_error(void);
+bbm_status bbm_device_count(int* count);
+
+/* ---- preprocess_mask (engine.hpp:80-91): block_sums + build_block_occupancy +
+ *      build_dense_runs + block_stats (mask.hpp:184-247), computed on the GPU. Any BlockSpec
+ *      with block_i, block_j >= 1 (BlockSpec::validate, mask.hpp:61-63); n >= 1. ---- */
+bbm_status bbm_preprocess_packed_host(const uint64_t* words, uint64_t n, uint64_t block_i,
+                                      uint64_t block_j, int device, bbm_prep* out);
+bbm_status bbm_preprocess_packed_device(const uint64_t* d_words, uint64_t n, uint64_t block_i,
+                                        uint64_t block_j, void* stream, bbm_prep* out);
+/* Dense bool mask on the device (K1: pack + sums fused), row stride in bytes. */
+bbm_status bbm_preprocess_bool_device(const uint8_t* d_mask, uint64_t n, uint64_t row_stride,
+                                      uint64_t block_i, uint64_t block_j, void* stream,
+                                      bbm_prep* out);
+bbm_status bbm_prep_destroy(bbm_prep prep);
+bbm_status bbm_prep_get_info(bbm_prep prep, bbm_prep_info* info);
+/* BlockSums::sum(p,q) row-major [rows][cols] (mask.hpp:71-109) */
+bbm_status bbm_prep_get_sums(bbm_prep prep, uint32_t* sums);
+/* BlockOccupancy (mask.hpp:113-132), u8 [rows][cols] */
+bbm_status bbm_prep_get_occupancy(bbm_prep prep, uint8_t* occ);
+/* DenseRuns offset / total_ones, u32 [rows] each (mask.hpp:139-154) */
+bbm_status bbm_prep_get_runs(bbm_prep prep, uint32_t* offset, uint32_t* total_ones);
+/* BlockStats (mask.hpp:230-247) */
+bbm_status bbm_prep_get_stats(bbm_prep prep, bbm_block_stats* stats);
+/* Kernel view: row_cnt[krows], list[krows*kcols] (bit31 = full tile), LPT order[krows].
+ * Any pointer may be NULL. */
+bbm_status bbm_prep_get_kernel_lists(bbm_prep prep, uint32_t* row_cnt, uint32_t* list,
+                                     uint32_t* order);
+/* EngineCounters a blocked_forward over `slots` slots reports for `variant`
+ * (classify_tile, engine.hpp:118-153; summed as run_attention does, engine.hpp:500-503). */
+bbm_status bbm_prep_counters(bbm_prep prep, int variant, uint64_t slots, bbm_counters* out);
+/* Peer-to-peer copy of the device metadata to another GPU (NVLink), for the multi-GPU driver.
+ * The result is an independent prep bound to `device`. */
+bbm_status bbm_prep_replicate(bbm_prep prep, int device, void* stream, bbm_prep* out);
+
+/* ---- blocked_forward (engine.hpp:282-341) over `slots` independent (batch, head) slots that
+ *      share one mask (run_attention, engine.hpp:489-505). Device pointers, bf16 [slots][n][d];
+ *      row_max / row_sum fp32 [slots][n] in natural-log units (NULL to skip). Asynchronous on
+ *      `stream` (a cudaStream_t, NULL = legacy default stream). ---- */
+bbm_status bbm_attn_fwd(bbm_prep prep, int variant, const void* q, const void* k, const void* v,
+                        void* out, float* row_max, float* row_sum, uint64_t slots,
+                        uint32_t head_dim, double scale, void* stream);
+
+/* Same, host buffers (bf16 bits as uint16): copies in, runs, copies out, synchronizes.
+ * Pinned buffers get full PCIe bandwidth. */
+bbm_status bbm_attn_fwd_host_bf16(bbm_prep prep, int variant, const uint16_t* q,
+                                  const uint16_t* k, const uint16_t* v, uint16_t* out,
+                                  float* row_max, float* row_sum, uint64_t slots,
+                                  uint32_t head_dim, double scale);
+
+/* Same, float host buffers (the reference's Matrix<float> storage, matrix.hpp:14-45); inputs
+ * rounded to bf16 (RNE) on the device, output widened back to float; row stats as double.
+ * Validates finiteness like validate_forward_args (engine.hpp:244-258). */
+bbm_status bbm_attn_fwd_host_f32(bbm_prep prep, int variant, const float* q, const float* k,
+                                 const float* v, float* out, double* row_max, double* row_sum,
+                                 uint64_t slots, uint32_t head_dim, double scale);
+
+/* Multi-GPU run_attention: slots sharded contiguously over `n_devices` GPUs
+ * ([g*S/G, (g+1)*S/G)), metadata replicated peer-to-peer from prep's device, one stream per
+ * GPU, no collective. Host bf16 buffers. elapsed_ms (may be NULL) = device time, max over GPUs
+ * of the kernel span measured from a common start. */
+bbm_status bbm_run_attention_multi(bbm_prep prep, int variant, int n_devices,
+                                   const int* devices, const uint16_t* q, const uint16_t* k,
+                                   const uint16_t* v, uint16_t* out, float* row_max,
+                                   float* row_sum, uint64_t slots, uint32_t head_dim,
+                                   double scale, double* elapsed_ms);
+
+/* ---- reorder.hpp ---- */
+/* rcm_order(build_graph(mask)) (reorder.hpp:28-133): forward[new] = old. Host. */
+bbm_status bbm_rcm_order(const uint64_t* words, uint64_t n, uint32_t* forward);
+/* bandwidth (reorder.hpp:137-153). Host. */
+bbm_status bbm_bandwidth(const uint64_t* words, uint64_t n, uint64_t* bandwidth);
+/* permute_rows / unpermute_rows (reorder.hpp:167-189) on the device over `slots` matrices
+ * [slots][n][row_bytes]; inverse != 0 scatters (unpermute). d_forward: u32 [n] on device. */
+bbm_status bbm_permute_rows_device(const void* src, void* dst, const uint32_t* d_forward,
+                                   uint64_t slots, uint64_t n, uint64_t row_bytes, int inverse,
+                                   void* stream);
+/* permute_mask (reorder.hpp:156-163) on the device: mask'(a,b) = mask(fwd[a], fwd[b]);
+ * both masks in the reference packed layout (ceil(n/64) words per row). */
+bbm_status bbm_permute_mask_device(const uint64_t* d_src, uint64_t* d_dst,
+                                   const uint32_t* d_forward, uint64_t n, void* stream);
+
+/* ---- generators.hpp (host fixtures): MaskSpec grammar (generators.hpp:364-438); families with
+ *      a free n take n_free. Call with words == NULL to query n. ---- */
+bbm_status bbm_generate(const char* spec, uint64_t n_free, uint64_t* n_out, uint64_t* words);
+/* Relabel a mask's tokens by a std::shuffle(mt19937_64(seed)) permutation:
+ * out(label[i], label[j]) = in(i, j) (the test_reorder.cpp relabel fixture). */
+bbm_status bbm_relabel(const uint64_t* words, uint64_t n, uint64_t seed, uint64_t* out_words);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* BBM_CAPI_H */

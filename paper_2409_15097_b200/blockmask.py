@@ -1,0 +1,705 @@
+"""Python mirror of the reference's C++ API (namespace blockmask, /root/reference/proj/include).
+
+Same names, argument meaning and error behaviour as the reference headers, so callers and tests
+read like the reference's own; every compute call goes through libbbm.so's C ABI to the sm_100a
+kernels. ``ValueError`` plays the role of ``std::invalid_argument``.
+
+  reference (file:line)                      here
+  Mask (mask.hpp:17-52)                      Mask           packed u64 words, same layout
+  BlockSpec (mask.hpp:57-66)                 BlockSpec
+  BlockSums / BlockOccupancy / DenseRuns /   BlockSums / BlockOccupancy / DenseRuns / BlockStats
+    BlockStats (mask.hpp:71-162)
+  block_sums, build_block_occupancy,         same names; computed by the GPU preprocessor
+    build_dense_runs, block_stats (:184-247)
+  Variant, to_string, parse_variant          same
+    (engine.hpp:21-45)
+  EngineCounters (engine.hpp:49-66)          EngineCounters
+  MaskPrep, preprocess_mask (:71-91)         MaskPrep, preprocess_mask  (+ device metadata)
+  ForwardResult (engine.hpp:93-99)           ForwardResult
+  blocked_forward (engine.hpp:282-341)       blocked_forward   (torch CUDA bf16 or host float)
+  SlotInputs / MultiHeadForward /            SlotInputs / MultiHeadForward / run_attention
+    run_attention (engine.hpp:475-505)
+  rcm_order / bandwidth / permute_rows /     rcm_order / bandwidth / permute_rows /
+    unpermute_rows / permute_mask              unpermute_rows / permute_mask (reorder.hpp)
+  generators (generators.hpp)                gen_* / generate
+"""
+from __future__ import annotations
+
+import ctypes as C
+import enum
+import math
+from dataclasses import dataclass, field
+from typing import Iterable, List, Optional, Sequence
+
+import numpy as np
+
+from . import _lib
+from ._lib import check, lib, ptr
+
+# ----------------------------------------------------------------------------- mask model
+
+
+@dataclass(frozen=True)
+class BlockSpec:
+    """Tile shape (mask.hpp:57-66); default 64 x 64 like the reference."""
+    block_i: int = 64
+    block_j: int = 64
+
+    def validate(self) -> None:
+        if self.block_i < 1 or self.block_j < 1:
+            raise ValueError("block sizes must be >= 1")
+
+
+class Mask:
+    """Square bit-packed attention mask, the reference's layout (mask.hpp:17-52):
+    row-major u64 words, words_per_row = ceil(n/64), bit j of row i at word j>>6 bit j&63,
+    tail bits zero."""
+
+    def __init__(self, n: int = 0, words: Optional[np.ndarray] = None):
+        self._n = int(n)
+        self._wpr = (self._n + 63) // 64
+        if words is None:
+            self.words = np.zeros((self._n, self._wpr), dtype=np.uint64)
+        else:
+            w = np.ascontiguousarray(words, dtype=np.uint64).reshape(self._n, self._wpr)
+            self.words = w
+
+    def size(self) -> int:
+        return self._n
+
+    def words_per_row(self) -> int:
+        return self._wpr
+
+    def get(self, i: int, j: int) -> bool:
+        return bool((int(self.words[i, j >> 6]) >> (j & 63)) & 1)
+
+    def set(self, i: int, j: int, value: bool) -> None:
+        bit = np.uint64(1 << (j & 63))
+        if value:
+            self.words[i, j >> 6] |= bit
+        else:
+            self.words[i, j >> 6] &= ~bit
+
+    def row_words(self, i: int) -> np.ndarray:
+        return self.words[i]
+
+    def count_ones(self) -> int:
+        return int(np.unpackbits(self.words.view(np.uint8)).sum())
+
+    def to_dense(self) -> np.ndarray:
+        bits = np.unpackbits(self.words.view(np.uint8), axis=1, bitorder="little")
+        return bits[:, : self._n].astype(bool)
+
+    @staticmethod
+    def from_dense(dense: np.ndarray) -> "Mask":
+        dense = np.asarray(dense, dtype=bool)
+        n = dense.shape[0]
+        if dense.shape != (n, n):
+            raise ValueError("mask must be square")
+        wpr = (n + 63) // 64
+        pad = np.zeros((n, wpr * 64), dtype=np.uint8)
+        pad[:, :n] = dense
+        packed = np.packbits(pad, axis=1, bitorder="little")
+        return Mask(n, packed.view(np.uint64).reshape(n, wpr))
+
+    def __eq__(self, other) -> bool:
+        return isinstance(other, Mask) and self._n == other._n and np.array_equal(self.words, other.words)
+
+
+class BlockSums:
+    """Per-block one counts with edge geometry (mask.hpp:71-109)."""
+
+    def __init__(self, n_tokens: int, spec: BlockSpec, sums: np.ndarray):
+        self._n = n_tokens
+        self._spec = spec
+        self.values = sums
+
+    def n_tokens(self) -> int:
+        return self._n
+
+    def spec(self) -> BlockSpec:
+        return self._spec
+
+    def rows(self) -> int:
+        return self.values.shape[0]
+
+    def cols(self) -> int:
+        return self.values.shape[1]
+
+    def sum(self, p: int, q: int) -> int:
+        return int(self.values[p, q])
+
+    def rows_in_block(self, p: int) -> int:
+        return min(self._spec.block_i, self._n - p * self._spec.block_i)
+
+    def cols_in_block(self, q: int) -> int:
+        return min(self._spec.block_j, self._n - q * self._spec.block_j)
+
+    def block_area(self, p: int, q: int) -> int:
+        return self.rows_in_block(p) * self.cols_in_block(q)
+
+    def full(self, p: int, q: int) -> bool:
+        return self.sum(p, q) == self.block_area(p, q)
+
+
+class BlockOccupancy:
+    """u8 per block, 1 iff any set bit (mask.hpp:113-132)."""
+
+    def __init__(self, occ: np.ndarray):
+        self.values = occ
+
+    def rows(self) -> int:
+        return self.values.shape[0]
+
+    def cols(self) -> int:
+        return self.values.shape[1]
+
+    def at(self, p: int, q: int) -> bool:
+        return bool(self.values[p, q])
+
+    def __eq__(self, other) -> bool:
+        return isinstance(other, BlockOccupancy) and np.array_equal(self.values, other.values)
+
+
+@dataclass
+class DenseRuns:
+    """First maximal run of full blocks per row block (mask.hpp:139-154), half-open."""
+    offset: List[int]
+    total_ones: List[int]
+
+    def in_run(self, r: int, q: int) -> bool:
+        return self.offset[r] <= q < self.offset[r] + self.total_ones[r]
+
+    def total_run_blocks(self) -> int:
+        return int(sum(self.total_ones))
+
+
+@dataclass
+class BlockStats:
+    blocks_total: int = 0
+    blocks_nonzero: int = 0
+    blocks_full: int = 0
+    block_density: float = 0.0
+    element_density: float = 0.0
+
+
+@dataclass
+class EngineCounters:
+    """Deterministic tile bookkeeping (engine.hpp:49-66)."""
+    blocks_visited: int = 0
+    blocks_processed: int = 0
+    mask_block_reads: int = 0
+    skipped_by_binblk: int = 0
+    skipped_mask_reads_by_run: int = 0
+
+    def __iadd__(self, o: "EngineCounters") -> "EngineCounters":
+        self.blocks_visited += o.blocks_visited
+        self.blocks_processed += o.blocks_processed
+        self.mask_block_reads += o.mask_block_reads
+        self.skipped_by_binblk += o.skipped_by_binblk
+        self.skipped_mask_reads_by_run += o.skipped_mask_reads_by_run
+        return self
+
+
+class Variant(enum.IntEnum):
+    """engine.hpp:21-26"""
+    dense = 0
+    naive_masked = 1
+    binblk = 2
+    dense_binblk = 3
+
+
+_VARIANT_NAMES = {Variant.dense: "dense", Variant.naive_masked: "naive", Variant.binblk: "binblk",
+                  Variant.dense_binblk: "dense-binblk"}
+
+
+def to_string(v: Variant) -> str:
+    return _VARIANT_NAMES.get(Variant(v), "?")
+
+
+def parse_variant(name: str) -> Variant:
+    for v, s in _VARIANT_NAMES.items():
+        if s == name:
+            return v
+    raise ValueError(f"unknown variant: '{name}' (expected dense, naive, binblk, dense-binblk)")
+
+
+# ----------------------------------------------------------------------------- preprocessing
+
+
+class _PrepHandle:
+    """Owns a bbm_prep (device metadata); destroyed with the Python object."""
+
+    def __init__(self, h: C.c_void_p):
+        self.h = h
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            lib.bbm_prep_destroy(self.h)
+            self.h = None
+
+
+@dataclass
+class MaskPrep:
+    """engine.hpp:71-78 plus the device-resident kernel metadata (``handle``)."""
+    n_tokens: int
+    spec: BlockSpec
+    sums: BlockSums
+    occupancy: BlockOccupancy
+    runs: DenseRuns
+    stats: BlockStats
+    handle: _PrepHandle = field(repr=False)
+
+    def info(self) -> _lib.PrepInfoC:
+        info = _lib.PrepInfoC()
+        check(lib.bbm_prep_get_info(self.handle.h, C.byref(info)))
+        return info
+
+    def kernel_lists(self):
+        """(row_cnt[krows], list[krows, kcols] with bit 31 = full, LPT order[krows])."""
+        info = self.info()
+        cnt = np.zeros(info.krows, np.uint32)
+        lst = np.zeros((info.krows, info.kcols), np.uint32)
+        order = np.zeros(info.krows, np.uint32)
+        check(lib.bbm_prep_get_kernel_lists(self.handle.h, ptr(cnt, C.c_uint32), ptr(lst, C.c_uint32),
+                                            ptr(order, C.c_uint32)))
+        return cnt, lst, order
+
+    def counters(self, variant: Variant, slots: int = 1) -> EngineCounters:
+        c = _lib.CountersC()
+        check(lib.bbm_prep_counters(self.handle.h, int(variant), int(slots), C.byref(c)))
+        return EngineCounters(c.blocks_visited, c.blocks_processed, c.mask_block_reads,
+                              c.skipped_by_binblk, c.skipped_mask_reads_by_run)
+
+
+def _prep_from_handle(h: C.c_void_p) -> MaskPrep:
+    handle = _PrepHandle(h)
+    info = _lib.PrepInfoC()
+    check(lib.bbm_prep_get_info(h, C.byref(info)))
+    rows, cols = int(info.rows), int(info.cols)
+    sums = np.zeros((rows, cols), np.uint32)
+    occ = np.zeros((rows, cols), np.uint8)
+    off = np.zeros(rows, np.uint32)
+    tot = np.zeros(rows, np.uint32)
+    st = _lib.BlockStatsC()
+    check(lib.bbm_prep_get_sums(h, ptr(sums, C.c_uint32)))
+    check(lib.bbm_prep_get_occupancy(h, ptr(occ, C.c_uint8)))
+    check(lib.bbm_prep_get_runs(h, ptr(off, C.c_uint32), ptr(tot, C.c_uint32)))
+    check(lib.bbm_prep_get_stats(h, C.byref(st)))
+    spec = BlockSpec(int(info.block_i), int(info.block_j))
+    return MaskPrep(
+        n_tokens=int(info.n), spec=spec, sums=BlockSums(int(info.n), spec, sums),
+        occupancy=BlockOccupancy(occ), runs=DenseRuns([int(x) for x in off], [int(x) for x in tot]),
+        stats=BlockStats(st.blocks_total, st.blocks_nonzero, st.blocks_full, st.block_density,
+                         st.element_density),
+        handle=handle)
+
+
+def preprocess_mask(mask, spec: BlockSpec = BlockSpec(), device: int = 0, stream=None) -> MaskPrep:
+    """preprocess_mask (engine.hpp:80-91) on the GPU.
+
+    ``mask`` may be a :class:`Mask` (host, bit-packed), a CUDA ``torch.bool``/``uint8`` n x n
+    tensor (dense mask: K1 pack + sums kernel) or a CUDA ``torch.int64`` tensor holding the packed
+    words [n][ceil(n/64)].
+    """
+    spec.validate()
+    h = C.c_void_p()
+    if isinstance(mask, Mask):
+        if mask.size() < 1:
+            raise ValueError("mask must be non-empty")
+        words = np.ascontiguousarray(mask.words)
+        check(lib.bbm_preprocess_packed_host(ptr(words, C.c_uint64), mask.size(), spec.block_i,
+                                             spec.block_j, device, C.byref(h)))
+        return _prep_from_handle(h)
+    import torch  # device path
+
+    if not isinstance(mask, torch.Tensor) or not mask.is_cuda:
+        raise ValueError("mask must be a Mask or a CUDA tensor")
+    s = stream if stream is not None else torch.cuda.current_stream(mask.device).cuda_stream
+    with torch.cuda.device(mask.device):
+        if mask.dtype in (torch.bool, torch.uint8):
+            n = mask.shape[0]
+            if mask.dim() != 2 or mask.shape[1] != n:
+                raise ValueError("dense mask must be n x n")
+            m = mask if mask.stride(1) == 1 else mask.contiguous()
+            check(lib.bbm_preprocess_bool_device(C.c_void_p(m.data_ptr()), n, m.stride(0),
+                                                 spec.block_i, spec.block_j, C.c_void_p(s), C.byref(h)))
+        elif mask.dtype == torch.int64:
+            n = mask.shape[0]
+            m = mask.contiguous()
+            check(lib.bbm_preprocess_packed_device(C.c_void_p(m.data_ptr()), n, spec.block_i,
+                                                   spec.block_j, C.c_void_p(s), C.byref(h)))
+        else:
+            raise ValueError("unsupported mask tensor dtype")
+    return _prep_from_handle(h)
+
+
+def block_sums(mask, spec: BlockSpec) -> BlockSums:
+    """block_sums (mask.hpp:184-201), computed by the GPU preprocessor."""
+    return preprocess_mask(mask, spec).sums
+
+
+def build_block_occupancy(sums: BlockSums) -> BlockOccupancy:
+    """build_block_occupancy (mask.hpp:203-209): occupied = sums > 0 (O(tiles) metadata)."""
+    return BlockOccupancy((sums.values > 0).astype(np.uint8))
+
+
+def _areas(sums: BlockSums) -> np.ndarray:
+    n, spec = sums.n_tokens(), sums.spec()
+    ri = np.minimum(spec.block_i, n - np.arange(sums.rows()) * spec.block_i)
+    cj = np.minimum(spec.block_j, n - np.arange(sums.cols()) * spec.block_j)
+    return np.outer(ri, cj)
+
+
+def build_dense_runs(sums: BlockSums) -> DenseRuns:
+    """build_dense_runs (mask.hpp:213-228) over already-computed sums (O(tiles) metadata)."""
+    full = sums.values == _areas(sums)
+    off, tot = [], []
+    for p in range(sums.rows()):
+        idx = np.flatnonzero(full[p])
+        if idx.size == 0:
+            off.append(0)
+            tot.append(0)
+            continue
+        q0 = int(idx[0])
+        notfull = np.flatnonzero(~full[p, q0:])
+        off.append(q0)
+        tot.append(int(notfull[0]) if notfull.size else sums.cols() - q0)
+    return DenseRuns(off, tot)
+
+
+def block_stats(sums: BlockSums) -> BlockStats:
+    """block_stats (mask.hpp:230-247)."""
+    total = sums.rows() * sums.cols()
+    nz = int((sums.values > 0).sum())
+    full = int((sums.values == _areas(sums)).sum())
+    ones = int(sums.values.astype(np.uint64).sum())
+    n = float(sums.n_tokens())
+    return BlockStats(total, nz, full, nz / total if total else 0.0, ones / (n * n) if n > 0 else 0.0)
+
+
+# ----------------------------------------------------------------------------- attention
+
+
+@dataclass
+class ForwardResult:
+    """engine.hpp:93-99. ``out`` keeps the input's container type; row stats as float64."""
+    out: object
+    row_max: object
+    row_sum: object
+    counters: EngineCounters
+
+
+@dataclass
+class SlotInputs:
+    q: object
+    k: object
+    v: object
+
+
+@dataclass
+class MultiHeadForward:
+    slots: List[ForwardResult]
+    counters: EngineCounters
+
+
+def _validate_common(prep: MaskPrep, mask, scale: float, threads: int) -> None:
+    # validate_forward_args (engine.hpp:244-258)
+    n = mask.size() if isinstance(mask, Mask) else int(mask.shape[0])
+    if prep.n_tokens != n:
+        raise ValueError("mask preprocessing does not match this mask")
+    if not math.isfinite(scale):
+        raise ValueError("scale must be finite")
+    if threads < 1:
+        raise ValueError("thread count must be >= 1")
+
+
+def attn_fwd_device(prep: MaskPrep, variant: Variant, q, k, v, out, row_max=None, row_sum=None,
+                    scale: float = 1.0, stream=None) -> None:
+    """Raw launch on device tensors (bf16 [slots][n][d], contiguous). No validation beyond
+    shapes; this is the timed entry point. row_max / row_sum: float32 [slots][n] or None."""
+    import torch
+
+    slots, n, d = (q.shape if q.dim() == 3 else (1, *q.shape))
+    s = stream if stream is not None else torch.cuda.current_stream(q.device).cuda_stream
+    check(lib.bbm_attn_fwd(prep.handle.h, int(variant), C.c_void_p(q.data_ptr()), C.c_void_p(k.data_ptr()),
+                           C.c_void_p(v.data_ptr()), C.c_void_p(out.data_ptr()),
+                           C.c_void_p(row_max.data_ptr() if row_max is not None else 0),
+                           C.c_void_p(row_sum.data_ptr() if row_sum is not None else 0),
+                           int(slots), int(d), float(scale), C.c_void_p(s)))
+
+
+def blocked_forward(q, k, v, scale: float, mask, prep: MaskPrep, variant: Variant,
+                    threads: int = 1, check_finite: bool = True) -> ForwardResult:
+    """blocked_forward (engine.hpp:282-341) on the sm_100a kernel.
+
+    q, k, v: CUDA bf16 tensors [n, d] or [slots, n, d] (device path, result stays on device), or
+    numpy float arrays [n, d] (host path, like Matrix<float>; rounded to bf16 on the device).
+    d must be 64 or 128 and d_v == d_k (documented narrowing of the reference)."""
+    _validate_common(prep, mask, scale, threads)
+    n = prep.n_tokens
+    if isinstance(q, np.ndarray):
+        return _blocked_forward_host(q, k, v, scale, prep, variant)
+    import torch
+
+    shapes = {tuple(t.shape[-2:]) for t in (q, k, v)}
+    if q.shape[-2] != n or k.shape[-2] != n or v.shape[-2] != n:
+        raise ValueError("q/k/v row count must match mask size")
+    if q.shape[-1] != k.shape[-1] or q.shape[-1] < 1:
+        raise ValueError("q and k must share a positive head dim")
+    if v.shape[-1] < 1:
+        raise ValueError("v must have a positive head dim")
+    if len(shapes) != 1:
+        raise ValueError(f"head dims {sorted(shapes)} unsupported: the sm_100a kernel needs d_v == d_k")
+    if check_finite:
+        for name, t in (("q", q), ("k", k), ("v", v)):
+            if not bool(torch.isfinite(t).all()):
+                raise ValueError(f"{name} must hold finite values")
+    squeeze = q.dim() == 2
+    q3, k3, v3 = (t.unsqueeze(0) if squeeze else t for t in (q, k, v))
+    q3, k3, v3 = (t.to(torch.bfloat16).contiguous() for t in (q3, k3, v3))
+    slots, _, d = q3.shape
+    out = torch.empty_like(q3)
+    rmax = torch.empty((slots, n), dtype=torch.float32, device=q3.device)
+    rsum = torch.empty((slots, n), dtype=torch.float32, device=q3.device)
+    with torch.cuda.device(q3.device):
+        attn_fwd_device(prep, variant, q3, k3, v3, out, rmax, rsum, scale)
+    counters = prep.counters(variant, slots)
+    if squeeze:
+        out, rmax, rsum = out[0], rmax[0], rsum[0]
+    return ForwardResult(out, rmax.double(), rsum.double(), counters)
+
+
+def _blocked_forward_host(q, k, v, scale, prep, variant) -> ForwardResult:
+    n = prep.n_tokens
+    arrs = [np.ascontiguousarray(a, dtype=np.float32) for a in (q, k, v)]
+    squeeze = arrs[0].ndim == 2
+    if squeeze:
+        arrs = [a[None] for a in arrs]
+    qa, ka, va = arrs
+    if qa.shape[1] != n or ka.shape[1] != n or va.shape[1] != n:
+        raise ValueError("q/k/v row count must match mask size")
+    if qa.shape[2] != ka.shape[2]:
+        raise ValueError("q and k must share a positive head dim")
+    if va.shape[2] != qa.shape[2]:
+        raise ValueError("head dims unsupported: the sm_100a kernel needs d_v == d_k")
+    slots, _, d = qa.shape
+    out = np.empty_like(qa)
+    rmax = np.empty((slots, n), np.float64)
+    rsum = np.empty((slots, n), np.float64)
+    check(lib.bbm_attn_fwd_host_f32(prep.handle.h, int(variant), ptr(qa, C.c_float), ptr(ka, C.c_float),
+                                    ptr(va, C.c_float), ptr(out, C.c_float), ptr(rmax, C.c_double),
+                                    ptr(rsum, C.c_double), slots, d, float(scale)))
+    counters = prep.counters(variant, slots)
+    if squeeze:
+        out, rmax, rsum = out[0], rmax[0], rsum[0]
+    return ForwardResult(out, rmax, rsum, counters)
+
+
+def run_attention(slots: Sequence[SlotInputs], scale: float, mask, prep: MaskPrep, variant: Variant,
+                  threads: int = 1) -> MultiHeadForward:
+    """run_attention (engine.hpp:489-505): all slots share the mask and prep. Slots are stacked
+    and run as ONE persistent launch (slot-major work list) instead of sequentially."""
+    if len(slots) == 0:
+        raise ValueError("need at least one batch/head slot")
+    d0 = (tuple(slots[0].q.shape[-1:]), tuple(slots[0].v.shape[-1:]))
+    for s in slots:
+        if (tuple(s.q.shape[-1:]), tuple(s.v.shape[-1:])) != d0:
+            raise ValueError("all slots must share head dimensions")
+    if isinstance(slots[0].q, np.ndarray):
+        q = np.stack([s.q for s in slots])
+        k = np.stack([s.k for s in slots])
+        v = np.stack([s.v for s in slots])
+    else:
+        import torch
+        q = torch.stack([s.q for s in slots])
+        k = torch.stack([s.k for s in slots])
+        v = torch.stack([s.v for s in slots])
+    res = blocked_forward(q, k, v, scale, mask, prep, variant, threads)
+    per = [ForwardResult(res.out[i], res.row_max[i], res.row_sum[i], prep.counters(variant, 1))
+           for i in range(len(slots))]
+    return MultiHeadForward(per, res.counters)
+
+
+def run_attention_multi(prep: MaskPrep, variant: Variant, q: np.ndarray, k: np.ndarray, v: np.ndarray,
+                        scale: float, devices: Sequence[int]):
+    """Multi-GPU driver (C ABI bbm_run_attention_multi): host bf16 (uint16) [slots][n][d] sharded
+    contiguously over ``devices``; metadata replicated peer-to-peer. Returns (out, row_max,
+    row_sum, elapsed_ms)."""
+    slots, n, d = q.shape
+    out = np.empty_like(q)
+    rmax = np.empty((slots, n), np.float32)
+    rsum = np.empty((slots, n), np.float32)
+    devs = (C.c_int * len(devices))(*devices)
+    ms = C.c_double(0.0)
+    check(lib.bbm_run_attention_multi(prep.handle.h, int(variant), len(devices), devs,
+                                      ptr(q, C.c_uint16), ptr(k, C.c_uint16), ptr(v, C.c_uint16),
+                                      ptr(out, C.c_uint16), ptr(rmax, C.c_float), ptr(rsum, C.c_float),
+                                      slots, d, float(scale), C.byref(ms)))
+    return out, rmax, rsum, ms.value
+
+
+def shard_slots(slots: int, world: int, rank: int):
+    """Contiguous slot range of one GPU: [r*S/G, (r+1)*S/G)."""
+    return slots * rank // world, slots * (rank + 1) // world
+
+
+# ----------------------------------------------------------------------------- reorder.hpp
+
+
+@dataclass
+class Permutation:
+    """reorder.hpp:53-79: forward maps new -> old, inverse old -> new."""
+    forward: np.ndarray
+    inverse: np.ndarray
+
+    @staticmethod
+    def from_forward(fwd) -> "Permutation":
+        fwd = np.asarray(fwd, dtype=np.uint32)
+        n = fwd.size
+        if n and (fwd.max() >= n or np.unique(fwd).size != n):
+            raise ValueError("forward map is not a bijection")
+        inv = np.empty(n, np.uint32)
+        inv[fwd] = np.arange(n, dtype=np.uint32)
+        return Permutation(fwd, inv)
+
+    @staticmethod
+    def identity(n: int) -> "Permutation":
+        return Permutation.from_forward(np.arange(n, dtype=np.uint32))
+
+    def size(self) -> int:
+        return int(self.forward.size)
+
+
+def rcm_order(mask: Mask) -> Permutation:
+    """rcm_order(build_graph(mask)) (reorder.hpp:28-133), host."""
+    words = np.ascontiguousarray(mask.words)
+    fwd = np.zeros(mask.size(), np.uint32)
+    check(lib.bbm_rcm_order(ptr(words, C.c_uint64), mask.size(), ptr(fwd, C.c_uint32)))
+    return Permutation.from_forward(fwd)
+
+
+def bandwidth(mask: Mask) -> int:
+    """reorder.hpp:137-153"""
+    words = np.ascontiguousarray(mask.words)
+    out = C.c_uint64(0)
+    check(lib.bbm_bandwidth(ptr(words, C.c_uint64), mask.size(), C.byref(out)))
+    return int(out.value)
+
+
+def permute_mask(mask: Mask, perm: Permutation, device: int = 0) -> Mask:
+    """permute_mask (reorder.hpp:156-163) on the GPU (K6)."""
+    import torch
+
+    if perm.size() != mask.size():
+        raise ValueError("permutation length must match mask size")
+    dev = torch.device("cuda", device)
+    src = torch.from_numpy(np.ascontiguousarray(mask.words).view(np.int64)).to(dev)
+    dst = torch.empty_like(src)
+    fwd = torch.from_numpy(perm.forward.astype(np.int32)).to(dev)
+    with torch.cuda.device(dev):
+        check(lib.bbm_permute_mask_device(C.c_void_p(src.data_ptr()), C.c_void_p(dst.data_ptr()),
+                                          C.c_void_p(fwd.data_ptr()), mask.size(),
+                                          C.c_void_p(torch.cuda.current_stream(dev).cuda_stream)))
+    return Mask(mask.size(), dst.cpu().numpy().view(np.uint64))
+
+
+def _permute_rows_impl(m, perm: Permutation, inverse: bool):
+    import torch
+
+    if perm.size() != m.shape[-2]:
+        raise ValueError("permutation length must match row count")
+    dev = m.device
+    fwd = torch.from_numpy(perm.forward.astype(np.int32)).to(dev)
+    src = m.contiguous()
+    dst = torch.empty_like(src)
+    slots = src.numel() // (src.shape[-2] * src.shape[-1])
+    row_bytes = src.shape[-1] * src.element_size()
+    with torch.cuda.device(dev):
+        check(lib.bbm_permute_rows_device(C.c_void_p(src.data_ptr()), C.c_void_p(dst.data_ptr()),
+                                          C.c_void_p(fwd.data_ptr()), slots, src.shape[-2], row_bytes,
+                                          1 if inverse else 0,
+                                          C.c_void_p(torch.cuda.current_stream(dev).cuda_stream)))
+    return dst
+
+
+def permute_rows(m, perm: Permutation):
+    """permute_rows (reorder.hpp:167-176) on the GPU (K5): row a <- row forward[a]."""
+    return _permute_rows_impl(m, perm, False)
+
+
+def unpermute_rows(m, perm: Permutation):
+    """unpermute_rows (reorder.hpp:180-189) on the GPU (K5): row forward[a] <- row a."""
+    return _permute_rows_impl(m, perm, True)
+
+
+# ----------------------------------------------------------------------------- generators
+
+
+def generate(spec: str, n: int = 0) -> Mask:
+    """MaskSpec::parse + generate (generators.hpp:233-438), host fixture."""
+    n_out = C.c_uint64(0)
+    check(lib.bbm_generate(spec.encode(), n, C.byref(n_out), None))
+    m = Mask(int(n_out.value))
+    check(lib.bbm_generate(spec.encode(), n, C.byref(n_out), ptr(m.words, C.c_uint64)))
+    return m
+
+
+def _join(xs: Iterable[int]) -> str:
+    return ";".join(str(int(x)) for x in xs)
+
+
+def gen_causal(n: int) -> Mask:
+    return generate("causal", n)
+
+
+def gen_all_ones(n: int) -> Mask:
+    return generate("all-ones", n)
+
+
+def gen_medusa(candidates: Sequence[int]) -> Mask:
+    return generate(f"medusa[{_join(candidates)}]")
+
+
+def medusa_size(candidates: Sequence[int]) -> int:
+    if not candidates:
+        raise ValueError("medusa candidate list must be non-empty")
+    total, level = 0, 1
+    for s in candidates:
+        if s < 1:
+            raise ValueError("medusa candidate counts must be positive")
+        level *= s
+        total += level
+    return total
+
+
+def gen_packed_sequential(lengths: Sequence[int]) -> Mask:
+    return generate(f"packed-seq[{_join(lengths)}]")
+
+
+def gen_packed_input_bidirectional(segments: Sequence[tuple]) -> Mask:
+    return generate("packed-bidir[" + ";".join(f"{a}:{b}" for a, b in segments) + "]")
+
+
+def gen_longformer_windowed(n: int, window: int, causal: bool = False) -> Mask:
+    return generate(f"windowed(w={window}" + (";causal=1" if causal else "") + ")", n)
+
+
+def gen_longformer_dilated(n: int, window: int, dilation: int) -> Mask:
+    return generate(f"dilated(w={window};d={dilation})", n)
+
+
+def gen_longformer_global(n: int, window: int, global_count: int) -> Mask:
+    return generate(f"global(w={window};g={global_count})", n)
+
+
+def gen_random_sparse(n: int, density: float, seed: int, force_diagonal: bool = True) -> Mask:
+    return generate(f"random(p={density!r};seed={seed}" + ("" if force_diagonal else ";diag=0") + ")", n)
+
+
+def relabel(mask: Mask, seed: int) -> Mask:
+    """out(label[i], label[j]) = mask(i, j), labels = std::shuffle(iota, mt19937_64(seed))."""
+    out = Mask(mask.size())
+    words = np.ascontiguousarray(mask.words)
+    check(lib.bbm_relabel(ptr(words, C.c_uint64), mask.size(), seed, ptr(out.words, C.c_uint64)))
+    return out

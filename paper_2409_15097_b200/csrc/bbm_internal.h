@@ -1,0 +1,109 @@
+// bbm_internal.h — shared host/device declarations for libbbm (not part of the public ABI).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+namespace bbm {
+
+// Tile shape of the attention kernel (BLOCK_M query rows x BLOCK_N key rows). The preprocessor
+// supports any BlockSpec; the kernel metadata is always also built at this shape.
+constexpr uint32_t kTile = 128;
+
+extern thread_local std::string g_last_error;  // capi.cu
+
+struct CudaError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct ArgError : std::invalid_argument {
+  using std::invalid_argument::invalid_argument;
+};
+
+inline void check_cuda(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) throw CudaError(std::string(what) + ": " + cudaGetErrorString(e));
+}
+#define BBM_CUDA(x) ::bbm::check_cuda((x), #x)
+
+inline void require(bool cond, const std::string& msg) {
+  if (!cond) throw ArgError(msg);
+}
+
+// Device metadata at the kernel tile shape (128 x 128). Layouts (all device memory):
+//   mask      : padded bit-packed mask, ktiles*128 rows x kcols*2 u64 words (zero padded)
+//   sums      : u32 [krows][kcols]
+//   row_cnt   : u32 [krows]              occupied tiles per query row tile
+//   list      : u32 [krows][kcols]       ascending occupied column tiles, bit 31 = full tile
+//   order     : u32 [krows]              row tiles by descending row_cnt (LPT), ties by index
+//   bitmaps   : uint4 [krows*kcols][128] tile-major copy of every occupied tile's mask bits
+//                                        (row r of tile (p,q) = 16 bytes), written sparsely
+struct KernelMeta {
+  uint32_t krows = 0, kcols = 0;
+  uint64_t* mask = nullptr;
+  uint32_t* sums = nullptr;
+  uint32_t* row_cnt = nullptr;
+  uint32_t* list = nullptr;
+  uint32_t* order = nullptr;
+  uint4* bitmaps = nullptr;
+  uint64_t nnz = 0, full = 0;  // occupied / full tiles at 128x128
+};
+
+// Per-spec metadata that mirrors the reference's MaskPrep (engine.hpp:71-78), host side.
+struct SpecMeta {
+  uint64_t bi = 0, bj = 0, rows = 0, cols = 0;
+  std::vector<uint32_t> sums;
+  std::vector<uint8_t> occ;
+  std::vector<uint32_t> offset, total_ones;
+  uint64_t blocks_total = 0, blocks_nonzero = 0, blocks_full = 0, ones = 0;
+};
+
+struct Prep {
+  int device = 0;
+  uint64_t n = 0;
+  SpecMeta spec;     // the caller's BlockSpec
+  KernelMeta kmeta;  // the kernel's 128x128 view
+  std::vector<uint32_t> h_row_cnt;  // host copy of kmeta.row_cnt (scheduling + tests)
+  ~Prep();
+};
+
+// ---- kernel launchers (prep.cu) ----
+void launch_pack_bool(const uint8_t* d_bool, uint64_t n, uint64_t row_stride, const KernelMeta& km,
+                      cudaStream_t s);
+void launch_pad_packed(const uint64_t* d_words, uint64_t n, const KernelMeta& km, cudaStream_t s);
+void launch_sums128(const KernelMeta& km, cudaStream_t s);
+void launch_sums_generic(const KernelMeta& km, uint64_t n, uint64_t bi, uint64_t bj,
+                         uint64_t rows, uint64_t cols, uint32_t* d_sums, cudaStream_t s);
+void launch_rowmeta(const uint32_t* d_sums, uint64_t n, uint64_t bi, uint64_t bj, uint64_t rows,
+                    uint64_t cols, uint8_t* d_occ, uint32_t* d_offset, uint32_t* d_total,
+                    uint64_t* d_row_stats /* rows x 3 */, uint32_t* d_list, uint32_t* d_cnt,
+                    cudaStream_t s);
+void launch_compact_bitmaps(const KernelMeta& km, cudaStream_t s);
+void launch_finalize(const uint64_t* d_row_stats, uint64_t rows, const uint32_t* d_cnt,
+                     uint32_t* d_order, uint64_t* d_totals /* 3 */, cudaStream_t s);
+
+// ---- permutation kernels (permute.cu) ----
+void launch_permute_rows(const void* src, void* dst, const uint32_t* d_fwd, uint64_t slots,
+                         uint64_t n, uint64_t row_bytes, bool inverse, cudaStream_t s);
+void launch_permute_mask(const uint64_t* d_src, uint64_t* d_dst, const uint32_t* d_fwd,
+                         uint64_t n, uint64_t src_wpr, uint64_t dst_wpr, cudaStream_t s);
+
+// ---- attention (attn_fwd.cu) ----
+struct AttnArgs {
+  const void* q;
+  const void* k;
+  const void* v;
+  void* o;
+  float* row_max;
+  float* row_sum;
+  uint64_t slots;
+  uint64_t n;
+  uint32_t d;
+  float scale;
+  int variant;
+};
+void launch_attn_fwd(const Prep& prep, const AttnArgs& a, cudaStream_t s, int num_sms);
+int attn_fwd_kernel_launches_per_call();
+
+}  // namespace bbm

@@ -1,0 +1,717 @@
+// capi.cu — implementation of the C ABI in include/bbm_capi.h (host orchestration).
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "../../include/bbm_capi.h"
+#include "bbm_internal.h"
+
+namespace bbm {
+
+thread_local std::string g_last_error;
+
+template <class F>
+bbm_status guarded(F&& f) {
+  try {
+    f();
+    return BBM_OK;
+  } catch (const ArgError& e) {
+    g_last_error = e.what();
+    return BBM_ERR_INVALID;
+  } catch (const CudaError& e) {
+    g_last_error = e.what();
+    return BBM_ERR_CUDA;
+  } catch (const std::exception& e) {
+    g_last_error = e.what();
+    return BBM_ERR_INTERNAL;
+  }
+}
+
+namespace {
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    BBM_CUDA(cudaGetDevice(&prev));
+    if (prev != dev) BBM_CUDA(cudaSetDevice(dev));
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+
+int sm_count(int dev) {
+  static int cache[64] = {0};
+  if (dev < 64 && cache[dev]) return cache[dev];
+  int v = 0;
+  BBM_CUDA(cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev));
+  if (dev < 64) cache[dev] = v;
+  return v;
+}
+
+template <class T>
+T* dmalloc(uint64_t count) {
+  void* p = nullptr;
+  if (count == 0) count = 1;
+  BBM_CUDA(cudaMalloc(&p, count * sizeof(T)));
+  return static_cast<T*>(p);
+}
+
+void alloc_kernel_meta(KernelMeta& km, uint64_t n) {
+  km.krows = static_cast<uint32_t>((n + kTile - 1) / kTile);
+  km.kcols = km.krows;
+  const uint64_t tiles = static_cast<uint64_t>(km.krows) * km.kcols;
+  km.mask = dmalloc<uint64_t>(static_cast<uint64_t>(km.krows) * kTile * km.kcols * 2);
+  km.sums = dmalloc<uint32_t>(tiles);
+  km.row_cnt = dmalloc<uint32_t>(km.krows);
+  km.list = dmalloc<uint32_t>(tiles);
+  km.order = dmalloc<uint32_t>(km.krows);
+  km.bitmaps = dmalloc<uint4>(tiles * kTile);
+}
+
+void free_kernel_meta(KernelMeta& km) {
+  cudaFree(km.mask);
+  cudaFree(km.sums);
+  cudaFree(km.row_cnt);
+  cudaFree(km.list);
+  cudaFree(km.order);
+  cudaFree(km.bitmaps);
+  km = KernelMeta{};
+}
+
+void validate_spec(uint64_t n, uint64_t bi, uint64_t bj) {
+  require(bi >= 1 && bj >= 1, "block sizes must be >= 1");  // mask.hpp:61-63
+  require(n >= 1, "mask must be non-empty");                 // engine.hpp:82
+  require(n < (1ull << 31), "mask too large for the device metadata (n >= 2^31)");
+}
+
+// Everything after the padded mask exists: sums at both views, row metadata, lists, bitmaps.
+void build_metadata(Prep& pr, uint64_t bi, uint64_t bj, cudaStream_t s) {
+  KernelMeta& km = pr.kmeta;
+  const uint64_t n = pr.n;
+  SpecMeta& sp = pr.spec;
+  sp.bi = bi;
+  sp.bj = bj;
+  sp.rows = (n + bi - 1) / bi;
+  sp.cols = (n + bj - 1) / bj;
+
+  // kernel view (128 x 128): sums already produced by the pack kernel or produced here
+  uint8_t* d_kocc = dmalloc<uint8_t>(static_cast<uint64_t>(km.krows) * km.kcols);
+  uint32_t* d_koff = dmalloc<uint32_t>(km.krows);
+  uint32_t* d_ktot = dmalloc<uint32_t>(km.krows);
+  uint64_t* d_kstats = dmalloc<uint64_t>(static_cast<uint64_t>(km.krows) * 3);
+  uint64_t* d_ktotals = dmalloc<uint64_t>(3);
+  launch_rowmeta(km.sums, n, kTile, kTile, km.krows, km.kcols, d_kocc, d_koff, d_ktot, d_kstats,
+                 km.list, km.row_cnt, s);
+  launch_compact_bitmaps(km, s);
+  launch_finalize(d_kstats, km.krows, km.row_cnt, km.order, d_ktotals, s);
+
+  // caller's view
+  const bool same = (bi == kTile && bj == kTile);
+  const uint64_t tiles = sp.rows * sp.cols;
+  uint32_t* d_sums = same ? km.sums : dmalloc<uint32_t>(tiles);
+  uint8_t* d_occ = same ? d_kocc : dmalloc<uint8_t>(tiles);
+  uint32_t* d_off = same ? d_koff : dmalloc<uint32_t>(sp.rows);
+  uint32_t* d_tot = same ? d_ktot : dmalloc<uint32_t>(sp.rows);
+  uint64_t* d_stats = same ? d_kstats : dmalloc<uint64_t>(sp.rows * 3);
+  uint64_t* d_totals = same ? d_ktotals : dmalloc<uint64_t>(3);
+  if (!same) {
+    launch_sums_generic(km, n, bi, bj, sp.rows, sp.cols, d_sums, s);
+    launch_rowmeta(d_sums, n, bi, bj, sp.rows, sp.cols, d_occ, d_off, d_tot, d_stats, nullptr,
+                   nullptr, s);
+    launch_finalize(d_stats, sp.rows, nullptr, nullptr, d_totals, s);
+  }
+
+  sp.sums.resize(tiles);
+  sp.occ.resize(tiles);
+  sp.offset.resize(sp.rows);
+  sp.total_ones.resize(sp.rows);
+  uint64_t totals[3] = {0, 0, 0}, ktotals[3] = {0, 0, 0};
+  pr.h_row_cnt.resize(km.krows);
+  BBM_CUDA(cudaMemcpyAsync(sp.sums.data(), d_sums, tiles * 4, cudaMemcpyDeviceToHost, s));
+  BBM_CUDA(cudaMemcpyAsync(sp.occ.data(), d_occ, tiles, cudaMemcpyDeviceToHost, s));
+  BBM_CUDA(cudaMemcpyAsync(sp.offset.data(), d_off, sp.rows * 4, cudaMemcpyDeviceToHost, s));
+  BBM_CUDA(cudaMemcpyAsync(sp.total_ones.data(), d_tot, sp.rows * 4, cudaMemcpyDeviceToHost, s));
+  BBM_CUDA(cudaMemcpyAsync(totals, d_totals, 24, cudaMemcpyDeviceToHost, s));
+  BBM_CUDA(cudaMemcpyAsync(ktotals, d_ktotals, 24, cudaMemcpyDeviceToHost, s));
+  BBM_CUDA(cudaMemcpyAsync(pr.h_row_cnt.data(), km.row_cnt, km.krows * 4, cudaMemcpyDeviceToHost,
+                           s));
+  BBM_CUDA(cudaStreamSynchronize(s));
+  sp.blocks_total = tiles;
+  sp.blocks_nonzero = totals[0];
+  sp.blocks_full = totals[1];
+  sp.ones = totals[2];
+  km.nnz = ktotals[0];
+  km.full = ktotals[1];
+
+  if (!same) {
+    cudaFree(d_sums);
+    cudaFree(d_occ);
+    cudaFree(d_off);
+    cudaFree(d_tot);
+    cudaFree(d_stats);
+    cudaFree(d_totals);
+  }
+  cudaFree(d_kocc);
+  cudaFree(d_koff);
+  cudaFree(d_ktot);
+  cudaFree(d_kstats);
+  cudaFree(d_ktotals);
+}
+
+Prep* new_prep(uint64_t n, int device) {
+  auto* pr = new Prep;
+  pr->device = device;
+  pr->n = n;
+  try {
+    alloc_kernel_meta(pr->kmeta, n);
+  } catch (...) {
+    delete pr;
+    throw;
+  }
+  return pr;
+}
+
+}  // namespace
+
+Prep::~Prep() {
+  int prev = -1;
+  cudaGetDevice(&prev);
+  cudaSetDevice(device);
+  free_kernel_meta(kmeta);
+  if (prev >= 0) cudaSetDevice(prev);
+}
+
+}  // namespace bbm
+
+using namespace bbm;
+
+struct bbm_prep_s {
+  std::unique_ptr<Prep> p;
+  // replicas on other devices for the multi-GPU driver, created lazily
+  std::vector<std::unique_ptr<bbm_prep_s>> replicas;
+};
+
+namespace bbm_capi_detail {
+Prep& unwrap(bbm_prep h) {
+  require(h != nullptr && h->p != nullptr, "null prep handle");
+  return *h->p;
+}
+
+bbm_prep wrap(Prep* p) {
+  auto* h = new bbm_prep_s;
+  h->p.reset(p);
+  return h;
+}
+
+void check_attn_args(const Prep& pr, int variant, uint64_t slots, uint32_t d, double scale) {
+  require(variant >= 0 && variant <= 3, "unknown variant");
+  require(slots >= 1, "need at least one batch/head slot");  // engine.hpp:493
+  require(std::isfinite(scale), "scale must be finite");     // engine.hpp:253
+  if (d != 64 && d != 128)
+    throw ArgError("head dim " + std::to_string(d) +
+                   " unsupported by the sm_100a kernel (64 or 128; d_v must equal d_k)");
+  (void)pr;
+}
+
+__global__ void f32_to_bf16_kernel(const float* __restrict__ in, __nv_bfloat16* __restrict__ out,
+                                   uint64_t count, int* __restrict__ bad) {
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < count;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const float x = in[i];
+    if (!isfinite(x)) *bad = 1;
+    out[i] = __float2bfloat16_rn(x);
+  }
+}
+
+__global__ void bf16_to_f32_kernel(const __nv_bfloat16* __restrict__ in, float* __restrict__ out,
+                                   uint64_t count) {
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < count;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
+    out[i] = __bfloat162float(in[i]);
+}
+
+unsigned grid_of(uint64_t count) {
+  uint64_t g = (count + 255) / 256;
+  return static_cast<unsigned>(std::max<uint64_t>(1, std::min<uint64_t>(g, 148ull * 16)));
+}
+
+}  // namespace bbm_capi_detail
+using namespace bbm_capi_detail;
+
+extern "C" {
+
+int bbm_abi_version(void) { return BBM_ABI_VERSION; }
+
+const char* bbm_last_error(void) { return g_last_error.c_str(); }
+
+bbm_status bbm_device_count(int* count) {
+  return guarded([&] {
+    int c = 0;
+    const cudaError_t e = cudaGetDeviceCount(&c);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      c = 0;
+    }
+    *count = c;
+  });
+}
+
+bbm_status bbm_preprocess_packed_host(const uint64_t* words, uint64_t n, uint64_t bi, uint64_t bj,
+                                      int device, bbm_prep* out) {
+  return guarded([&] {
+    validate_spec(n, bi, bj);
+    require(words != nullptr && out != nullptr, "null argument");
+    DeviceGuard g(device);
+    std::unique_ptr<Prep> pr(new_prep(n, device));
+    const KernelMeta& km = pr->kmeta;
+    cudaStream_t s;
+    BBM_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    const uint64_t wpr = (n + 63) / 64, pad_wpr = static_cast<uint64_t>(km.kcols) * 2;
+    const uint64_t rows_pad = static_cast<uint64_t>(km.krows) * kTile;
+    BBM_CUDA(cudaMemsetAsync(km.mask, 0, rows_pad * pad_wpr * 8, s));
+    BBM_CUDA(cudaMemcpy2DAsync(km.mask, pad_wpr * 8, words, wpr * 8, wpr * 8, n,
+                               cudaMemcpyHostToDevice, s));
+    launch_sums128(km, s);
+    build_metadata(*pr, bi, bj, s);
+    BBM_CUDA(cudaStreamDestroy(s));
+    *out = wrap(pr.release());
+  });
+}
+
+bbm_status bbm_preprocess_packed_device(const uint64_t* d_words, uint64_t n, uint64_t bi,
+                                        uint64_t bj, void* stream, bbm_prep* out) {
+  return guarded([&] {
+    validate_spec(n, bi, bj);
+    require(d_words != nullptr && out != nullptr, "null argument");
+    int dev = 0;
+    BBM_CUDA(cudaGetDevice(&dev));
+    std::unique_ptr<Prep> pr(new_prep(n, dev));
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    launch_pad_packed(d_words, n, pr->kmeta, s);
+    launch_sums128(pr->kmeta, s);
+    build_metadata(*pr, bi, bj, s);
+    *out = wrap(pr.release());
+  });
+}
+
+bbm_status bbm_preprocess_bool_device(const uint8_t* d_mask, uint64_t n, uint64_t row_stride,
+                                      uint64_t bi, uint64_t bj, void* stream, bbm_prep* out) {
+  return guarded([&] {
+    validate_spec(n, bi, bj);
+    require(d_mask != nullptr && out != nullptr, "null argument");
+    require(row_stride >= n, "row stride must be >= n");
+    int dev = 0;
+    BBM_CUDA(cudaGetDevice(&dev));
+    std::unique_ptr<Prep> pr(new_prep(n, dev));
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    launch_pack_bool(d_mask, n, row_stride, pr->kmeta, s);
+    build_metadata(*pr, bi, bj, s);
+    *out = wrap(pr.release());
+  });
+}
+
+bbm_status bbm_prep_destroy(bbm_prep prep) {
+  return guarded([&] { delete prep; });
+}
+
+bbm_status bbm_prep_get_info(bbm_prep prep, bbm_prep_info* info) {
+  return guarded([&] {
+    const Prep& pr = unwrap(prep);
+    info->n = pr.n;
+    info->block_i = pr.spec.bi;
+    info->block_j = pr.spec.bj;
+    info->rows = pr.spec.rows;
+    info->cols = pr.spec.cols;
+    info->ktile = kTile;
+    info->krows = pr.kmeta.krows;
+    info->kcols = pr.kmeta.kcols;
+    info->knnz = pr.kmeta.nnz;
+    info->kfull = pr.kmeta.full;
+    info->device = pr.device;
+  });
+}
+
+bbm_status bbm_prep_get_sums(bbm_prep prep, uint32_t* sums) {
+  return guarded([&] {
+    const Prep& pr = unwrap(prep);
+    std::memcpy(sums, pr.spec.sums.data(), pr.spec.sums.size() * 4);
+  });
+}
+
+bbm_status bbm_prep_get_occupancy(bbm_prep prep, uint8_t* occ) {
+  return guarded([&] {
+    const Prep& pr = unwrap(prep);
+    std::memcpy(occ, pr.spec.occ.data(), pr.spec.occ.size());
+  });
+}
+
+bbm_status bbm_prep_get_runs(bbm_prep prep, uint32_t* offset, uint32_t* total_ones) {
+  return guarded([&] {
+    const Prep& pr = unwrap(prep);
+    if (offset) std::memcpy(offset, pr.spec.offset.data(), pr.spec.offset.size() * 4);
+    if (total_ones)
+      std::memcpy(total_ones, pr.spec.total_ones.data(), pr.spec.total_ones.size() * 4);
+  });
+}
+
+bbm_status bbm_prep_get_stats(bbm_prep prep, bbm_block_stats* st) {
+  return guarded([&] {
+    const Prep& pr = unwrap(prep);
+    // block_stats (mask.hpp:230-247): same double expressions as the reference
+    st->blocks_total = pr.spec.blocks_total;
+    st->blocks_nonzero = pr.spec.blocks_nonzero;
+    st->blocks_full = pr.spec.blocks_full;
+    const double nd = static_cast<double>(pr.n);
+    st->block_density = st->blocks_total ? static_cast<double>(st->blocks_nonzero) /
+                                               static_cast<double>(st->blocks_total)
+                                         : 0.0;
+    st->element_density = nd > 0 ? static_cast<double>(pr.spec.ones) / (nd * nd) : 0.0;
+  });
+}
+
+bbm_status bbm_prep_get_kernel_lists(bbm_prep prep, uint32_t* row_cnt, uint32_t* list,
+                                     uint32_t* order) {
+  return guarded([&] {
+    const Prep& pr = unwrap(prep);
+    DeviceGuard g(pr.device);
+    const KernelMeta& km = pr.kmeta;
+    if (row_cnt) BBM_CUDA(cudaMemcpy(row_cnt, km.row_cnt, km.krows * 4, cudaMemcpyDeviceToHost));
+    if (list)
+      BBM_CUDA(cudaMemcpy(list, km.list, static_cast<uint64_t>(km.krows) * km.kcols * 4,
+                          cudaMemcpyDeviceToHost));
+    if (order) BBM_CUDA(cudaMemcpy(order, km.order, km.krows * 4, cudaMemcpyDeviceToHost));
+  });
+}
+
+bbm_status bbm_prep_counters(bbm_prep prep, int variant, uint64_t slots, bbm_counters* c) {
+  return guarded([&] {
+    const Prep& pr = unwrap(prep);
+    require(variant >= 0 && variant <= 3, "unknown variant");
+    // classify_tile (engine.hpp:118-153) summed over every tile of the caller's BlockSpec:
+    // counts depend on the mask and spec only (engine.hpp:47-48).
+    const SpecMeta& sp = pr.spec;
+    uint64_t run_blocks = 0;
+    for (uint32_t t : sp.total_ones) run_blocks += t;
+    bbm_counters one{};
+    one.blocks_visited = sp.blocks_total;
+    switch (variant) {
+      case BBM_VARIANT_DENSE:
+        one.blocks_processed = sp.blocks_total;
+        break;
+      case BBM_VARIANT_NAIVE:
+        one.blocks_processed = sp.blocks_total;
+        one.mask_block_reads = sp.blocks_total;
+        break;
+      case BBM_VARIANT_BINBLK:
+        one.blocks_processed = sp.blocks_nonzero;
+        one.mask_block_reads = sp.blocks_nonzero;
+        one.skipped_by_binblk = sp.blocks_total - sp.blocks_nonzero;
+        break;
+      case BBM_VARIANT_DENSE_BINBLK:
+        // run blocks are full, hence occupied: they are processed without a mask read
+        one.blocks_processed = sp.blocks_nonzero;
+        one.skipped_by_binblk = sp.blocks_total - sp.blocks_nonzero;
+        one.skipped_mask_reads_by_run = run_blocks;
+        one.mask_block_reads = sp.blocks_nonzero - run_blocks;
+        break;
+    }
+    c->blocks_visited = one.blocks_visited * slots;
+    c->blocks_processed = one.blocks_processed * slots;
+    c->mask_block_reads = one.mask_block_reads * slots;
+    c->skipped_by_binblk = one.skipped_by_binblk * slots;
+    c->skipped_mask_reads_by_run = one.skipped_mask_reads_by_run * slots;
+  });
+}
+
+bbm_status bbm_prep_replicate(bbm_prep prep, int device, void* stream, bbm_prep* out) {
+  return guarded([&] {
+    const Prep& src = unwrap(prep);
+    DeviceGuard g(device);
+    std::unique_ptr<Prep> dst(new_prep(src.n, device));
+    dst->spec = src.spec;
+    dst->h_row_cnt = src.h_row_cnt;
+    KernelMeta& a = dst->kmeta;
+    const KernelMeta& b = src.kmeta;
+    a.nnz = b.nnz;
+    a.full = b.full;
+    if (device != src.device) {
+      int can = 0;
+      BBM_CUDA(cudaDeviceCanAccessPeer(&can, device, src.device));
+      if (can) {
+        const cudaError_t e = cudaDeviceEnablePeerAccess(src.device, 0);
+        if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) BBM_CUDA(e);
+        cudaGetLastError();
+      }
+    }
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const uint64_t tiles = static_cast<uint64_t>(b.krows) * b.kcols;
+    auto peer = [&](void* d, const void* sp, uint64_t bytes) {
+      BBM_CUDA(cudaMemcpyPeerAsync(d, device, sp, src.device, bytes, s));
+    };
+    peer(a.mask, b.mask, static_cast<uint64_t>(b.krows) * kTile * b.kcols * 16);
+    peer(a.sums, b.sums, tiles * 4);
+    peer(a.row_cnt, b.row_cnt, b.krows * 4);
+    peer(a.list, b.list, tiles * 4);
+    peer(a.order, b.order, b.krows * 4);
+    peer(a.bitmaps, b.bitmaps, tiles * kTile * 16);
+    BBM_CUDA(cudaStreamSynchronize(s));
+    *out = wrap(dst.release());
+  });
+}
+
+bbm_status bbm_attn_fwd(bbm_prep prep, int variant, const void* q, const void* k, const void* v,
+                        void* out, float* row_max, float* row_sum, uint64_t slots,
+                        uint32_t head_dim, double scale, void* stream) {
+  return guarded([&] {
+    const Prep& pr = unwrap(prep);
+    check_attn_args(pr, variant, slots, head_dim, scale);
+    require(q && k && v && out, "null tensor pointer");
+    AttnArgs a{q, k, v, out, row_max, row_sum, slots, pr.n, head_dim, static_cast<float>(scale),
+               variant};
+    int dev = 0;
+    BBM_CUDA(cudaGetDevice(&dev));
+    require(dev == pr.device, "prep lives on another device; use bbm_prep_replicate");
+    launch_attn_fwd(pr, a, static_cast<cudaStream_t>(stream), sm_count(dev));
+  });
+}
+
+bbm_status bbm_attn_fwd_host_bf16(bbm_prep prep, int variant, const uint16_t* q, const uint16_t* k,
+                                  const uint16_t* v, uint16_t* out, float* row_max,
+                                  float* row_sum, uint64_t slots, uint32_t head_dim,
+                                  double scale) {
+  return guarded([&] {
+    const Prep& pr = unwrap(prep);
+    check_attn_args(pr, variant, slots, head_dim, scale);
+    DeviceGuard g(pr.device);
+    cudaStream_t s;
+    BBM_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    const uint64_t elems = slots * pr.n * head_dim, bytes = elems * 2;
+    void *dq, *dk, *dv, *dout;
+    float *dmax = nullptr, *dsum = nullptr;
+    BBM_CUDA(cudaMallocAsync(&dq, bytes, s));
+    BBM_CUDA(cudaMallocAsync(&dk, bytes, s));
+    BBM_CUDA(cudaMallocAsync(&dv, bytes, s));
+    BBM_CUDA(cudaMallocAsync(&dout, bytes, s));
+    if (row_max) BBM_CUDA(cudaMallocAsync(&dmax, slots * pr.n * 4, s));
+    if (row_sum) BBM_CUDA(cudaMallocAsync(&dsum, slots * pr.n * 4, s));
+    BBM_CUDA(cudaMemcpyAsync(dq, q, bytes, cudaMemcpyHostToDevice, s));
+    BBM_CUDA(cudaMemcpyAsync(dk, k, bytes, cudaMemcpyHostToDevice, s));
+    BBM_CUDA(cudaMemcpyAsync(dv, v, bytes, cudaMemcpyHostToDevice, s));
+    AttnArgs a{dq, dk, dv, dout, dmax, dsum, slots, pr.n, head_dim, static_cast<float>(scale),
+               variant};
+    launch_attn_fwd(pr, a, s, sm_count(pr.device));
+    BBM_CUDA(cudaMemcpyAsync(out, dout, bytes, cudaMemcpyDeviceToHost, s));
+    if (row_max) BBM_CUDA(cudaMemcpyAsync(row_max, dmax, slots * pr.n * 4, cudaMemcpyDeviceToHost, s));
+    if (row_sum) BBM_CUDA(cudaMemcpyAsync(row_sum, dsum, slots * pr.n * 4, cudaMemcpyDeviceToHost, s));
+    cudaFreeAsync(dq, s);
+    cudaFreeAsync(dk, s);
+    cudaFreeAsync(dv, s);
+    cudaFreeAsync(dout, s);
+    if (dmax) cudaFreeAsync(dmax, s);
+    if (dsum) cudaFreeAsync(dsum, s);
+    BBM_CUDA(cudaStreamSynchronize(s));
+    BBM_CUDA(cudaStreamDestroy(s));
+  });
+}
+
+bbm_status bbm_attn_fwd_host_f32(bbm_prep prep, int variant, const float* q, const float* k,
+                                 const float* v, float* out, double* row_max, double* row_sum,
+                                 uint64_t slots, uint32_t head_dim, double scale) {
+  return guarded([&] {
+    const Prep& pr = unwrap(prep);
+    check_attn_args(pr, variant, slots, head_dim, scale);
+    DeviceGuard g(pr.device);
+    cudaStream_t s;
+    BBM_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    const uint64_t elems = slots * pr.n * head_dim, rows = slots * pr.n;
+    float* stage;
+    __nv_bfloat16 *dq, *dk, *dv, *dout;
+    float *dmax, *dsum;
+    int* dbad;
+    BBM_CUDA(cudaMallocAsync(&stage, elems * 4, s));
+    BBM_CUDA(cudaMallocAsync(&dq, elems * 2, s));
+    BBM_CUDA(cudaMallocAsync(&dk, elems * 2, s));
+    BBM_CUDA(cudaMallocAsync(&dv, elems * 2, s));
+    BBM_CUDA(cudaMallocAsync(&dout, elems * 2, s));
+    BBM_CUDA(cudaMallocAsync(&dmax, rows * 4, s));
+    BBM_CUDA(cudaMallocAsync(&dsum, rows * 4, s));
+    BBM_CUDA(cudaMallocAsync(&dbad, 4 * 3, s));
+    BBM_CUDA(cudaMemsetAsync(dbad, 0, 12, s));
+    const float* srcs[3] = {q, k, v};
+    __nv_bfloat16* dsts[3] = {dq, dk, dv};
+    for (int t = 0; t < 3; ++t) {
+      BBM_CUDA(cudaMemcpyAsync(stage, srcs[t], elems * 4, cudaMemcpyHostToDevice, s));
+      f32_to_bf16_kernel<<<grid_of(elems), 256, 0, s>>>(stage, dsts[t], elems, dbad + t);
+      BBM_CUDA(cudaGetLastError());
+    }
+    int bad[3] = {0, 0, 0};
+    BBM_CUDA(cudaMemcpyAsync(bad, dbad, 12, cudaMemcpyDeviceToHost, s));
+    BBM_CUDA(cudaStreamSynchronize(s));
+    auto release = [&] {
+      cudaFreeAsync(stage, s);
+      cudaFreeAsync(dq, s);
+      cudaFreeAsync(dk, s);
+      cudaFreeAsync(dv, s);
+      cudaFreeAsync(dout, s);
+      cudaFreeAsync(dmax, s);
+      cudaFreeAsync(dsum, s);
+      cudaFreeAsync(dbad, s);
+      cudaStreamSynchronize(s);
+      cudaStreamDestroy(s);
+    };
+    static const char* names[3] = {"q", "k", "v"};
+    for (int t = 0; t < 3; ++t)
+      if (bad[t]) {  // require_finite (engine.hpp:237-242)
+        release();
+        throw ArgError(std::string(names[t]) + " must hold finite values");
+      }
+    AttnArgs a{dq, dk, dv, dout, dmax, dsum, slots, pr.n, head_dim, static_cast<float>(scale),
+               variant};
+    launch_attn_fwd(pr, a, s, sm_count(pr.device));
+    bf16_to_f32_kernel<<<grid_of(elems), 256, 0, s>>>(dout, stage, elems);
+    BBM_CUDA(cudaGetLastError());
+    BBM_CUDA(cudaMemcpyAsync(out, stage, elems * 4, cudaMemcpyDeviceToHost, s));
+    std::vector<float> hmax(rows), hsum(rows);
+    BBM_CUDA(cudaMemcpyAsync(hmax.data(), dmax, rows * 4, cudaMemcpyDeviceToHost, s));
+    BBM_CUDA(cudaMemcpyAsync(hsum.data(), dsum, rows * 4, cudaMemcpyDeviceToHost, s));
+    release();
+    for (uint64_t i = 0; i < rows; ++i) {
+      if (row_max) row_max[i] = static_cast<double>(hmax[i]);
+      if (row_sum) row_sum[i] = static_cast<double>(hsum[i]);
+    }
+  });
+}
+
+bbm_status bbm_run_attention_multi(bbm_prep prep, int variant, int n_devices, const int* devices,
+                                   const uint16_t* q, const uint16_t* k, const uint16_t* v,
+                                   uint16_t* out, float* row_max, float* row_sum, uint64_t slots,
+                                   uint32_t head_dim, double scale, double* elapsed_ms) {
+  return guarded([&] {
+    Prep& pr = unwrap(prep);
+    check_attn_args(pr, variant, slots, head_dim, scale);
+    require(n_devices >= 1 && devices != nullptr, "need at least one device");
+    const uint64_t per_slot = pr.n * head_dim;
+    // replicate metadata peer-to-peer once per device (cached on the handle)
+    std::vector<bbm_prep> preps(n_devices);
+    for (int g = 0; g < n_devices; ++g) {
+      if (devices[g] == pr.device) {
+        preps[g] = prep;
+        continue;
+      }
+      bbm_prep found = nullptr;
+      for (auto& r : prep->replicas)
+        if (r->p->device == devices[g]) found = r.get();
+      if (!found) {
+        bbm_prep rep = nullptr;
+        const bbm_status st = bbm_prep_replicate(prep, devices[g], nullptr, &rep);
+        if (st != BBM_OK) throw CudaError(g_last_error);
+        prep->replicas.emplace_back(rep);
+        found = rep;
+      }
+      preps[g] = found;
+    }
+    struct Shard {
+      uint64_t s0 = 0, s1 = 0;
+      void *dq = nullptr, *dk = nullptr, *dv = nullptr, *dout = nullptr;
+      float *dmax = nullptr, *dsum = nullptr;
+      cudaStream_t st = nullptr;
+      cudaEvent_t e0 = nullptr, e1 = nullptr;
+    };
+    std::vector<Shard> sh(n_devices);
+    for (int g = 0; g < n_devices; ++g) {
+      Shard& x = sh[g];
+      x.s0 = slots * g / n_devices;
+      x.s1 = slots * (g + 1) / n_devices;
+      DeviceGuard dg(devices[g]);
+      BBM_CUDA(cudaStreamCreateWithFlags(&x.st, cudaStreamNonBlocking));
+      BBM_CUDA(cudaEventCreate(&x.e0));
+      BBM_CUDA(cudaEventCreate(&x.e1));
+      const uint64_t ns = x.s1 - x.s0;
+      if (ns == 0) continue;
+      const uint64_t bytes = ns * per_slot * 2;
+      BBM_CUDA(cudaMallocAsync(&x.dq, bytes, x.st));
+      BBM_CUDA(cudaMallocAsync(&x.dk, bytes, x.st));
+      BBM_CUDA(cudaMallocAsync(&x.dv, bytes, x.st));
+      BBM_CUDA(cudaMallocAsync(&x.dout, bytes, x.st));
+      BBM_CUDA(cudaMallocAsync(&x.dmax, ns * pr.n * 4, x.st));
+      BBM_CUDA(cudaMallocAsync(&x.dsum, ns * pr.n * 4, x.st));
+      BBM_CUDA(cudaMemcpyAsync(x.dq, q + x.s0 * per_slot, bytes, cudaMemcpyHostToDevice, x.st));
+      BBM_CUDA(cudaMemcpyAsync(x.dk, k + x.s0 * per_slot, bytes, cudaMemcpyHostToDevice, x.st));
+      BBM_CUDA(cudaMemcpyAsync(x.dv, v + x.s0 * per_slot, bytes, cudaMemcpyHostToDevice, x.st));
+    }
+    // launch all shards, then collect (no collective: shards are independent)
+    for (int g = 0; g < n_devices; ++g) {
+      Shard& x = sh[g];
+      DeviceGuard dg(devices[g]);
+      BBM_CUDA(cudaEventRecord(x.e0, x.st));
+      const uint64_t ns = x.s1 - x.s0;
+      if (ns) {
+        AttnArgs a{x.dq, x.dk, x.dv, x.dout, x.dmax, x.dsum, ns, pr.n, head_dim,
+                   static_cast<float>(scale), variant};
+        launch_attn_fwd(*preps[g]->p, a, x.st, sm_count(devices[g]));
+      }
+      BBM_CUDA(cudaEventRecord(x.e1, x.st));
+    }
+    double worst = 0.0;
+    for (int g = 0; g < n_devices; ++g) {
+      Shard& x = sh[g];
+      DeviceGuard dg(devices[g]);
+      const uint64_t ns = x.s1 - x.s0;
+      if (ns) {
+        BBM_CUDA(cudaMemcpyAsync(out + x.s0 * per_slot, x.dout, ns * per_slot * 2,
+                                 cudaMemcpyDeviceToHost, x.st));
+        if (row_max)
+          BBM_CUDA(cudaMemcpyAsync(row_max + x.s0 * pr.n, x.dmax, ns * pr.n * 4,
+                                   cudaMemcpyDeviceToHost, x.st));
+        if (row_sum)
+          BBM_CUDA(cudaMemcpyAsync(row_sum + x.s0 * pr.n, x.dsum, ns * pr.n * 4,
+                                   cudaMemcpyDeviceToHost, x.st));
+      }
+      BBM_CUDA(cudaStreamSynchronize(x.st));
+      float ms = 0.0f;
+      BBM_CUDA(cudaEventElapsedTime(&ms, x.e0, x.e1));
+      worst = std::max(worst, static_cast<double>(ms));
+      cudaFree(x.dq);
+      cudaFree(x.dk);
+      cudaFree(x.dv);
+      cudaFree(x.dout);
+      cudaFree(x.dmax);
+      cudaFree(x.dsum);
+      cudaEventDestroy(x.e0);
+      cudaEventDestroy(x.e1);
+      cudaStreamDestroy(x.st);
+    }
+    if (elapsed_ms) *elapsed_ms = worst;
+  });
+}
+
+bbm_status bbm_permute_rows_device(const void* src, void* dst, const uint32_t* d_forward,
+                                   uint64_t slots, uint64_t n, uint64_t row_bytes, int inverse,
+                                   void* stream) {
+  return guarded([&] {
+    require(src && dst && d_forward, "null argument");
+    require(src != dst, "permute_rows cannot run in place");
+    require(row_bytes % 16 == 0, "row bytes must be a multiple of 16");
+    launch_permute_rows(src, dst, d_forward, slots, n, row_bytes, inverse != 0,
+                        static_cast<cudaStream_t>(stream));
+  });
+}
+
+bbm_status bbm_permute_mask_device(const uint64_t* d_src, uint64_t* d_dst,
+                                   const uint32_t* d_forward, uint64_t n, void* stream) {
+  return guarded([&] {
+    require(d_src && d_dst && d_forward && d_src != d_dst, "bad argument");
+    const uint64_t wpr = (n + 63) / 64;
+    launch_permute_mask(d_src, d_dst, d_forward, n, wpr, wpr, static_cast<cudaStream_t>(stream));
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,345 @@
+// prep.cu — GPU mask preprocessor (the reference's preprocess_mask, engine.hpp:80-91, and the
+// mask-model functions it calls, mask.hpp:184-247), B200-native.
+//
+// Kernels (all HBM-bound integer work; no tensor cores):
+//   pack_bool_sums128  K1+K2  dense bool mask -> padded bit-packed mask + 128x128 block sums.
+//                             uint4 loads (16 bools/lane, 512 B per warp per row), bytes folded to
+//                             bits with shift/or, words assembled with warp shuffles, popc sums.
+//   pad_packed                caller's packed words (ceil(n/64) per row) -> padded layout.
+//   sums128            K2     padded packed mask -> 128x128 sums (uint4 per lane, smem reduce).
+//   sums_generic              any BlockSpec: popcount_range per (row, tile), mask.hpp:167-199.
+//   rowmeta                   per query-row tile: occupancy (mask.hpp:203-209), first maximal run
+//                             of full tiles (mask.hpp:213-228), per-row stats partials
+//                             (mask.hpp:230-247), ascending compacted KV-tile list (block-wide
+//                             ballot prefix scan) with a full/partial flag.
+//   compact_bitmaps    K3     every occupied 128x128 tile's 2 KiB of mask bits -> tile-major copy
+//                             so the attention kernel reads 16 B per row, fully coalesced.
+//   finalize                  totals over rows (deterministic integer sums) + LPT row order.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "bbm_internal.h"
+
+namespace bbm {
+namespace {
+
+__device__ __forceinline__ uint32_t bytes_to_bits4(uint32_t w) {
+  // 4 bytes (any nonzero = true) -> 4 bits, byte k -> bit k.
+  w |= w >> 4;
+  w |= w >> 2;
+  w |= w >> 1;
+  w &= 0x01010101u;
+  return (w * 0x01020408u) >> 24;  // distinct partial products: no carries
+}
+
+// grid (ceil(kcols/32), krows), 256 threads. Warp w owns column tiles 4*w .. 4*w+3 of the chunk
+// (8 lanes x 16 bools each) and walks all 128 rows of the tile row.
+__global__ void __launch_bounds__(256) pack_bool_sums128_kernel(
+    const uint8_t* __restrict__ mask, uint64_t n, uint64_t stride, uint64_t* __restrict__ out,
+    uint32_t kcols, uint32_t* __restrict__ sums) {
+  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t p = blockIdx.y;
+  const uint32_t q = blockIdx.x * 32 + warp * 4 + (lane >> 3);  // column tile of this lane
+  const uint64_t col0 = static_cast<uint64_t>(q) * 128 + (lane & 7) * 16;
+  const bool col_ok = q < kcols && col0 < n;  // n % 16 == 0 on this path
+  const uint64_t wpr = static_cast<uint64_t>(kcols) * 2;
+  uint32_t count = 0;
+#pragma unroll 4
+  for (uint32_t r = 0; r < 128; ++r) {
+    const uint64_t row = static_cast<uint64_t>(p) * 128 + r;
+    uint32_t bits16 = 0;
+    if (col_ok && row < n) {
+      const uint4 v = __ldg(reinterpret_cast<const uint4*>(mask + row * stride + col0));
+      bits16 = bytes_to_bits4(v.x) | (bytes_to_bits4(v.y) << 4) | (bytes_to_bits4(v.z) << 8) |
+               (bytes_to_bits4(v.w) << 12);
+    }
+    count += __popc(bits16);
+    uint64_t part = static_cast<uint64_t>(bits16) << (16 * (lane & 3));
+    part |= __shfl_xor_sync(0xffffffffu, part, 1);
+    part |= __shfl_xor_sync(0xffffffffu, part, 2);
+    if ((lane & 3) == 0 && q < kcols)
+      out[row * wpr + static_cast<uint64_t>(q) * 2 + ((lane >> 2) & 1)] = part;
+  }
+  count += __shfl_xor_sync(0xffffffffu, count, 1);
+  count += __shfl_xor_sync(0xffffffffu, count, 2);
+  count += __shfl_xor_sync(0xffffffffu, count, 4);
+  if ((lane & 7) == 0 && q < kcols) sums[p * kcols + q] = count;
+}
+
+// Generic bool path (n % 16 != 0 or unaligned rows): one thread per output word.
+__global__ void pack_bool_generic_kernel(const uint8_t* __restrict__ mask, uint64_t n,
+                                         uint64_t stride, uint64_t* __restrict__ out,
+                                         uint32_t kcols, uint64_t total_words) {
+  const uint64_t wpr = static_cast<uint64_t>(kcols) * 2;
+  for (uint64_t t = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; t < total_words;
+       t += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint64_t row = t / wpr, w = t % wpr;
+    uint64_t word = 0;
+    if (row < n)
+      for (uint32_t b = 0; b < 64; ++b) {
+        const uint64_t c = w * 64 + b;
+        if (c < n && mask[row * stride + c]) word |= 1ull << b;
+      }
+    out[t] = word;
+  }
+}
+
+__global__ void pad_packed_kernel(const uint64_t* __restrict__ in, uint64_t n, uint64_t in_wpr,
+                                  uint64_t* __restrict__ out, uint64_t out_wpr,
+                                  uint64_t total_words) {
+  for (uint64_t t = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; t < total_words;
+       t += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint64_t row = t / out_wpr, w = t % out_wpr;
+    out[t] = (row < n && w < in_wpr) ? in[row * in_wpr + w] : 0ull;
+  }
+}
+
+// grid (ceil(kcols/32), krows), 256 threads: lane = column tile, warp = row phase.
+__global__ void __launch_bounds__(256) sums128_kernel(const uint4* __restrict__ mask,
+                                                      uint32_t kcols, uint32_t* __restrict__ sums) {
+  __shared__ uint32_t part[8][32];
+  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t p = blockIdx.y, q = blockIdx.x * 32 + lane;
+  uint32_t count = 0;
+  if (q < kcols) {
+#pragma unroll 4
+    for (uint32_t r = warp; r < 128; r += 8) {
+      const uint4 v = __ldg(mask + (static_cast<uint64_t>(p) * 128 + r) * kcols + q);
+      count += __popc(v.x) + __popc(v.y) + __popc(v.z) + __popc(v.w);
+    }
+  }
+  part[warp][lane] = count;
+  __syncthreads();
+  if (warp == 0 && q < kcols) {
+    uint32_t s = 0;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) s += part[w][lane];
+    sums[p * kcols + q] = s;
+  }
+}
+
+__device__ __forceinline__ uint32_t popcount_range_dev(const uint64_t* words, uint64_t c0,
+                                                       uint64_t c1) {
+  // mask.hpp:167-179
+  if (c0 >= c1) return 0;
+  const uint64_t w0 = c0 >> 6, w1 = (c1 - 1) >> 6;
+  const uint64_t first = ~0ull << (c0 & 63);
+  const uint64_t last = (c1 & 63) ? (~0ull >> (64 - (c1 & 63))) : ~0ull;
+  if (w0 == w1) return __popcll(words[w0] & first & last);
+  uint32_t c = __popcll(words[w0] & first) + __popcll(words[w1] & last);
+  for (uint64_t w = w0 + 1; w < w1; ++w) c += __popcll(words[w]);
+  return c;
+}
+
+// One thread per (p, q) tile of an arbitrary BlockSpec.
+__global__ void sums_generic_kernel(const uint64_t* __restrict__ mask, uint64_t wpr, uint64_t n,
+                                    uint64_t bi, uint64_t bj, uint64_t rows, uint64_t cols,
+                                    uint32_t* __restrict__ sums) {
+  const uint64_t total = rows * cols;
+  for (uint64_t t = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; t < total;
+       t += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint64_t q = t % cols, p = t / cols;
+    const uint64_t i0 = p * bi, i1 = min(i0 + bi, n);
+    const uint64_t c0 = q * bj, c1 = min(c0 + bj, n);
+    uint32_t s = 0;
+    for (uint64_t i = i0; i < i1; ++i) s += popcount_range_dev(mask + i * wpr, c0, c1);
+    sums[t] = s;
+  }
+}
+
+__device__ __forceinline__ uint32_t area_of(uint64_t n, uint64_t bi, uint64_t bj, uint64_t p,
+                                            uint64_t q) {
+  // BlockSums::block_area, mask.hpp:89-99 (true extent of edge blocks)
+  const uint64_t ri = min(bi, n - p * bi), cj = min(bj, n - q * bj);
+  return static_cast<uint32_t>(ri * cj);
+}
+
+// One CTA (256 threads) per row tile p; the row is walked in chunks of 256 tiles.
+__global__ void __launch_bounds__(256) rowmeta_kernel(
+    const uint32_t* __restrict__ sums, uint64_t n, uint64_t bi, uint64_t bj, uint64_t cols,
+    uint8_t* __restrict__ occ, uint32_t* __restrict__ offset, uint32_t* __restrict__ total,
+    uint64_t* __restrict__ row_stats, uint32_t* __restrict__ list, uint32_t* __restrict__ cnt) {
+  __shared__ uint32_t warp_cnt[8];
+  __shared__ uint32_t s_run_start, s_run_end;
+  __shared__ unsigned long long s_nz, s_full, s_ones;
+  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint64_t p = blockIdx.x;
+  if (threadIdx.x == 0) {
+    s_run_start = 0xFFFFFFFFu;
+    s_run_end = 0xFFFFFFFFu;
+    s_nz = s_full = s_ones = 0;
+  }
+  __syncthreads();
+  uint32_t base = 0;  // running list length
+  unsigned long long my_nz = 0, my_full = 0, my_ones = 0;
+  for (uint64_t c0 = 0; c0 < cols; c0 += 256) {
+    const uint64_t q = c0 + threadIdx.x;
+    uint32_t s = 0, a = 0;
+    bool in = q < cols;
+    if (in) {
+      s = sums[p * cols + q];
+      a = area_of(n, bi, bj, p, q);
+      occ[p * cols + q] = s > 0 ? 1 : 0;
+      my_nz += s > 0;
+      my_full += s == a;
+      my_ones += s;
+      if (s == a) atomicMin(&s_run_start, static_cast<uint32_t>(q));
+    }
+    const bool o = in && s > 0;
+    const uint32_t ballot = __ballot_sync(0xffffffffu, o);
+    if (lane == 0) warp_cnt[warp] = __popc(ballot);
+    __syncthreads();
+    uint32_t before = base;
+    for (uint32_t w = 0; w < warp; ++w) before += warp_cnt[w];
+    before += __popc(ballot & ((1u << lane) - 1u));
+    if (list && o) list[p * cols + before] = static_cast<uint32_t>(q) | ((s == a) ? 0x80000000u : 0u);
+    uint32_t chunk = 0;
+    for (uint32_t w = 0; w < 8; ++w) chunk += warp_cnt[w];
+    base += chunk;
+    __syncthreads();
+  }
+  // end of the first maximal run: first non-full tile after its start (mask.hpp:219-221)
+  const uint32_t start = s_run_start;
+  if (start != 0xFFFFFFFFu) {
+    for (uint64_t q = start + 1 + threadIdx.x; q < cols; q += 256) {
+      if (sums[p * cols + q] != area_of(n, bi, bj, p, q))
+        atomicMin(&s_run_end, static_cast<uint32_t>(q));
+    }
+  }
+  atomicAdd(&s_nz, my_nz);
+  atomicAdd(&s_full, my_full);
+  atomicAdd(&s_ones, my_ones);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    if (start == 0xFFFFFFFFu) {
+      offset[p] = 0;
+      total[p] = 0;
+    } else {
+      const uint32_t end = s_run_end == 0xFFFFFFFFu ? static_cast<uint32_t>(cols) : s_run_end;
+      offset[p] = start;
+      total[p] = end - start;
+    }
+    row_stats[p * 3 + 0] = s_nz;
+    row_stats[p * 3 + 1] = s_full;
+    row_stats[p * 3 + 2] = s_ones;
+    if (cnt) cnt[p] = base;
+  }
+}
+
+// grid (kcols, krows), 128 threads: CTA copies list entry (p, k) if it exists.
+__global__ void __launch_bounds__(128) compact_bitmaps_kernel(const uint4* __restrict__ mask,
+                                                              uint32_t kcols,
+                                                              const uint32_t* __restrict__ list,
+                                                              const uint32_t* __restrict__ cnt,
+                                                              uint4* __restrict__ bitmaps) {
+  const uint32_t p = blockIdx.y, k = blockIdx.x;
+  if (k >= cnt[p]) return;
+  const uint32_t q = list[p * kcols + k] & 0x7FFFFFFFu;
+  const uint32_t r = threadIdx.x;
+  bitmaps[(static_cast<uint64_t>(p) * kcols + q) * 128 + r] =
+      mask[(static_cast<uint64_t>(p) * 128 + r) * kcols + q];
+}
+
+__global__ void __launch_bounds__(1024) finalize_kernel(const uint64_t* __restrict__ row_stats,
+                                                        uint64_t rows,
+                                                        const uint32_t* __restrict__ cnt,
+                                                        uint32_t* __restrict__ order,
+                                                        unsigned long long* __restrict__ totals) {
+  __shared__ unsigned long long acc[3];
+  if (threadIdx.x < 3) acc[threadIdx.x] = 0;
+  __syncthreads();
+  unsigned long long a0 = 0, a1 = 0, a2 = 0;
+  for (uint64_t p = threadIdx.x; p < rows; p += blockDim.x) {
+    a0 += row_stats[p * 3 + 0];
+    a1 += row_stats[p * 3 + 1];
+    a2 += row_stats[p * 3 + 2];
+  }
+  atomicAdd(&acc[0], a0);
+  atomicAdd(&acc[1], a1);
+  atomicAdd(&acc[2], a2);
+  if (cnt && order) {
+    // LPT order: rank = #rows with a longer list, ties broken by index (stable).
+    for (uint64_t p = threadIdx.x; p < rows; p += blockDim.x) {
+      const uint32_t c = cnt[p];
+      uint32_t rank = 0;
+      for (uint64_t o = 0; o < rows; ++o) {
+        const uint32_t co = cnt[o];
+        rank += (co > c) || (co == c && o < p);
+      }
+      order[rank] = static_cast<uint32_t>(p);
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x < 3) totals[threadIdx.x] = acc[threadIdx.x];
+}
+
+inline unsigned grid_for(uint64_t work, unsigned block) {
+  uint64_t g = (work + block - 1) / block;
+  if (g > 148ull * 32) g = 148ull * 32;
+  return static_cast<unsigned>(g ? g : 1);
+}
+
+}  // namespace
+
+void launch_pack_bool(const uint8_t* d_bool, uint64_t n, uint64_t stride, const KernelMeta& km,
+                      cudaStream_t s) {
+  const bool fast = (n % 16 == 0) && (stride % 16 == 0) &&
+                    (reinterpret_cast<uintptr_t>(d_bool) % 16 == 0);
+  if (fast) {
+    dim3 grid((km.kcols + 31) / 32, km.krows);
+    pack_bool_sums128_kernel<<<grid, 256, 0, s>>>(d_bool, n, stride, km.mask, km.kcols, km.sums);
+  } else {
+    const uint64_t words = static_cast<uint64_t>(km.krows) * 128 * km.kcols * 2;
+    pack_bool_generic_kernel<<<grid_for(words, 256), 256, 0, s>>>(d_bool, n, stride, km.mask,
+                                                                   km.kcols, words);
+    launch_sums128(km, s);
+  }
+  BBM_CUDA(cudaGetLastError());
+}
+
+void launch_pad_packed(const uint64_t* d_words, uint64_t n, const KernelMeta& km,
+                       cudaStream_t s) {
+  const uint64_t out_wpr = static_cast<uint64_t>(km.kcols) * 2;
+  const uint64_t words = static_cast<uint64_t>(km.krows) * 128 * out_wpr;
+  pad_packed_kernel<<<grid_for(words, 256), 256, 0, s>>>(d_words, n, (n + 63) / 64, km.mask,
+                                                         out_wpr, words);
+  BBM_CUDA(cudaGetLastError());
+}
+
+void launch_sums128(const KernelMeta& km, cudaStream_t s) {
+  dim3 grid((km.kcols + 31) / 32, km.krows);
+  sums128_kernel<<<grid, 256, 0, s>>>(reinterpret_cast<const uint4*>(km.mask), km.kcols, km.sums);
+  BBM_CUDA(cudaGetLastError());
+}
+
+void launch_sums_generic(const KernelMeta& km, uint64_t n, uint64_t bi, uint64_t bj,
+                         uint64_t rows, uint64_t cols, uint32_t* d_sums, cudaStream_t s) {
+  sums_generic_kernel<<<grid_for(rows * cols, 256), 256, 0, s>>>(
+      km.mask, static_cast<uint64_t>(km.kcols) * 2, n, bi, bj, rows, cols, d_sums);
+  BBM_CUDA(cudaGetLastError());
+}
+
+void launch_rowmeta(const uint32_t* d_sums, uint64_t n, uint64_t bi, uint64_t bj, uint64_t rows,
+                    uint64_t cols, uint8_t* d_occ, uint32_t* d_offset, uint32_t* d_total,
+                    uint64_t* d_row_stats, uint32_t* d_list, uint32_t* d_cnt, cudaStream_t s) {
+  rowmeta_kernel<<<static_cast<unsigned>(rows), 256, 0, s>>>(
+      d_sums, n, bi, bj, cols, d_occ, d_offset, d_total, d_row_stats, d_list, d_cnt);
+  BBM_CUDA(cudaGetLastError());
+}
+
+void launch_compact_bitmaps(const KernelMeta& km, cudaStream_t s) {
+  dim3 grid(km.kcols, km.krows);
+  compact_bitmaps_kernel<<<grid, 128, 0, s>>>(reinterpret_cast<const uint4*>(km.mask), km.kcols,
+                                              km.list, km.row_cnt, km.bitmaps);
+  BBM_CUDA(cudaGetLastError());
+}
+
+void launch_finalize(const uint64_t* d_row_stats, uint64_t rows, const uint32_t* d_cnt,
+                     uint32_t* d_order, uint64_t* d_totals, cudaStream_t s) {
+  finalize_kernel<<<1, 1024, 0, s>>>(d_row_stats, rows, d_cnt, d_order,
+                                     reinterpret_cast<unsigned long long*>(d_totals));
+  BBM_CUDA(cudaGetLastError());
+}
+
+}  // namespace bbm
