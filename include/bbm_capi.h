@@ -81,6 +81,13 @@ bbm_status bbm_preprocess_packed_device(const uint64_t* d_words, uint64_t n, uin
 bbm_status bbm_preprocess_bool_device(const uint8_t* d_mask, uint64_t n, uint64_t row_stride,
                                       uint64_t block_i, uint64_t block_j, void* stream,
                                       bbm_prep* out);
+/* Rebuild the KERNEL view (128x128 sums, tile lists, LPT order, partial-tile bitmaps) of an
+ * existing prep from a new mask of the same n, fully asynchronously on `stream` (no host
+ * copies, no allocation): the per-batch path when every batch packs different sequences. The
+ * caller-spec host metadata (sums/occupancy/runs/stats getters) is NOT refreshed. */
+bbm_status bbm_prep_update_bool_device(bbm_prep prep, const uint8_t* d_mask, uint64_t row_stride,
+                                       void* stream);
+bbm_status bbm_prep_update_packed_device(bbm_prep prep, const uint64_t* d_words, void* stream);
 bbm_status bbm_prep_destroy(bbm_prep prep);
 bbm_status bbm_prep_get_info(bbm_prep prep, bbm_prep_info* info);
 /* BlockSums::sum(p,q) row-major [rows][cols] (mask.hpp:71-109) */

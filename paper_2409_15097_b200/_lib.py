@@ -56,6 +56,8 @@ SIGNATURES = {
     "bbm_preprocess_packed_host": (C.c_int, [u64p, C.c_uint64, C.c_uint64, C.c_uint64, C.c_int, C.POINTER(vp)]),
     "bbm_preprocess_packed_device": (C.c_int, [vp, C.c_uint64, C.c_uint64, C.c_uint64, vp, C.POINTER(vp)]),
     "bbm_preprocess_bool_device": (C.c_int, [vp, C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint64, vp, C.POINTER(vp)]),
+    "bbm_prep_update_bool_device": (C.c_int, [vp, vp, C.c_uint64, vp]),
+    "bbm_prep_update_packed_device": (C.c_int, [vp, vp, vp]),
     "bbm_prep_destroy": (C.c_int, [vp]),
     "bbm_prep_get_info": (C.c_int, [vp, C.POINTER(PrepInfoC)]),
     "bbm_prep_get_sums": (C.c_int, [vp, u32p]),

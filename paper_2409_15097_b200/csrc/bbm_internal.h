@@ -48,6 +48,12 @@ struct KernelMeta {
   uint32_t* order = nullptr;
   uint4* bitmaps = nullptr;
   uint64_t nnz = 0, full = 0;  // occupied / full tiles at 128x128
+  // persistent scratch of the per-row pass (so rebuilds allocate nothing)
+  uint8_t* occ = nullptr;
+  uint32_t* run_off = nullptr;
+  uint32_t* run_len = nullptr;
+  uint64_t* row_stats = nullptr;
+  uint64_t* totals = nullptr;
 };
 
 // Per-spec metadata that mirrors the reference's MaskPrep (engine.hpp:71-78), host side.

@@ -74,6 +74,19 @@ void alloc_kernel_meta(KernelMeta& km, uint64_t n) {
   km.list = dmalloc<uint32_t>(tiles);
   km.order = dmalloc<uint32_t>(km.krows);
   km.bitmaps = dmalloc<uint4>(tiles * kTile);
+  km.occ = dmalloc<uint8_t>(tiles);
+  km.run_off = dmalloc<uint32_t>(km.krows);
+  km.run_len = dmalloc<uint32_t>(km.krows);
+  km.row_stats = dmalloc<uint64_t>(static_cast<uint64_t>(km.krows) * 3);
+  km.totals = dmalloc<uint64_t>(3);
+}
+
+// Kernel view from km.sums (already built): lists, bitmaps, LPT order. Async, no allocation.
+void build_kernel_view(const KernelMeta& km, uint64_t n, cudaStream_t s) {
+  launch_rowmeta(km.sums, n, kTile, kTile, km.krows, km.kcols, km.occ, km.run_off, km.run_len,
+                 km.row_stats, km.list, km.row_cnt, s);
+  launch_compact_bitmaps(km, s);
+  launch_finalize(km.row_stats, km.krows, km.row_cnt, km.order, km.totals, s);
 }
 
 void free_kernel_meta(KernelMeta& km) {
@@ -83,6 +96,11 @@ void free_kernel_meta(KernelMeta& km) {
   cudaFree(km.list);
   cudaFree(km.order);
   cudaFree(km.bitmaps);
+  cudaFree(km.occ);
+  cudaFree(km.run_off);
+  cudaFree(km.run_len);
+  cudaFree(km.row_stats);
+  cudaFree(km.totals);
   km = KernelMeta{};
 }
 
@@ -102,16 +120,13 @@ void build_metadata(Prep& pr, uint64_t bi, uint64_t bj, cudaStream_t s) {
   sp.rows = (n + bi - 1) / bi;
   sp.cols = (n + bj - 1) / bj;
 
-  // kernel view (128 x 128): sums already produced by the pack kernel or produced here
-  uint8_t* d_kocc = dmalloc<uint8_t>(static_cast<uint64_t>(km.krows) * km.kcols);
-  uint32_t* d_koff = dmalloc<uint32_t>(km.krows);
-  uint32_t* d_ktot = dmalloc<uint32_t>(km.krows);
-  uint64_t* d_kstats = dmalloc<uint64_t>(static_cast<uint64_t>(km.krows) * 3);
-  uint64_t* d_ktotals = dmalloc<uint64_t>(3);
-  launch_rowmeta(km.sums, n, kTile, kTile, km.krows, km.kcols, d_kocc, d_koff, d_ktot, d_kstats,
-                 km.list, km.row_cnt, s);
-  launch_compact_bitmaps(km, s);
-  launch_finalize(d_kstats, km.krows, km.row_cnt, km.order, d_ktotals, s);
+  // kernel view (128 x 128): sums already produced by the pack kernel or the sums kernel
+  build_kernel_view(km, n, s);
+  uint8_t* d_kocc = km.occ;
+  uint32_t* d_koff = km.run_off;
+  uint32_t* d_ktot = km.run_len;
+  uint64_t* d_kstats = km.row_stats;
+  uint64_t* d_ktotals = km.totals;
 
   // caller's view
   const bool same = (bi == kTile && bj == kTile);
@@ -159,11 +174,6 @@ void build_metadata(Prep& pr, uint64_t bi, uint64_t bj, cudaStream_t s) {
     cudaFree(d_stats);
     cudaFree(d_totals);
   }
-  cudaFree(d_kocc);
-  cudaFree(d_koff);
-  cudaFree(d_ktot);
-  cudaFree(d_kstats);
-  cudaFree(d_ktotals);
 }
 
 Prep* new_prep(uint64_t n, int device) {
@@ -315,6 +325,28 @@ bbm_status bbm_preprocess_bool_device(const uint8_t* d_mask, uint64_t n, uint64_
     launch_pack_bool(d_mask, n, row_stride, pr->kmeta, s);
     build_metadata(*pr, bi, bj, s);
     *out = wrap(pr.release());
+  });
+}
+
+bbm_status bbm_prep_update_bool_device(bbm_prep prep, const uint8_t* d_mask, uint64_t row_stride,
+                                       void* stream) {
+  return guarded([&] {
+    Prep& pr = unwrap(prep);
+    require(d_mask != nullptr && row_stride >= pr.n, "bad mask argument");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    launch_pack_bool(d_mask, pr.n, row_stride, pr.kmeta, s);
+    build_kernel_view(pr.kmeta, pr.n, s);
+  });
+}
+
+bbm_status bbm_prep_update_packed_device(bbm_prep prep, const uint64_t* d_words, void* stream) {
+  return guarded([&] {
+    Prep& pr = unwrap(prep);
+    require(d_words != nullptr, "bad mask argument");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    launch_pad_packed(d_words, pr.n, pr.kmeta, s);
+    launch_sums128(pr.kmeta, s);
+    build_kernel_view(pr.kmeta, pr.n, s);
   });
 }
 
