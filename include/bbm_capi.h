@@ -141,6 +141,12 @@ bbm_status bbm_run_attention_multi(bbm_prep prep, int variant, int n_devices,
                                    float* row_sum, uint64_t slots, uint32_t head_dim,
                                    double scale, double* elapsed_ms);
 
+/* ---- tracing (no reference counterpart; the reference only has steady_clock timings,
+ *      bench.hpp:155-159): every attention launch made after this call records per-role events
+ *      (TMA issue, MMA issue, softmax waits/arrivals; clock64 cycles) for CTAs [0, ctas) into
+ *      d_buffer (device, ctas * 8192 u64). NULL disables. Format in attn_fwd.cu (trace_ev). ---- */
+bbm_status bbm_set_trace(void* d_buffer, uint32_t ctas);
+
 /* ---- reorder.hpp ---- */
 /* rcm_order(build_graph(mask)) (reorder.hpp:28-133): forward[new] = old. Host. */
 bbm_status bbm_rcm_order(const uint64_t* words, uint64_t n, uint32_t* forward);

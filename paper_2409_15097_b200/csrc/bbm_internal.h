@@ -109,6 +109,13 @@ struct AttnArgs {
   float scale;
   int variant;
 };
+// Process-wide kernel event trace (bbm_set_trace): device buffer of ctas * 8192 u64 events.
+struct TraceConfig {
+  void* buffer = nullptr;
+  uint32_t ctas = 0;
+};
+extern TraceConfig g_trace;
+
 void launch_attn_fwd(const Prep& prep, const AttnArgs& a, cudaStream_t s, int num_sms);
 int attn_fwd_kernel_launches_per_call();
 

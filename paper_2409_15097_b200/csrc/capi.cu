@@ -16,6 +16,7 @@
 namespace bbm {
 
 thread_local std::string g_last_error;
+TraceConfig g_trace;
 
 template <class F>
 bbm_status guarded(F&& f) {
@@ -722,6 +723,13 @@ bbm_status bbm_run_attention_multi(bbm_prep prep, int variant, int n_devices, co
       cudaStreamDestroy(x.st);
     }
     if (elapsed_ms) *elapsed_ms = worst;
+  });
+}
+
+bbm_status bbm_set_trace(void* d_buffer, uint32_t ctas) {
+  return guarded([&] {
+    g_trace.buffer = d_buffer;
+    g_trace.ctas = d_buffer ? ctas : 0;
   });
 }
 
