@@ -70,9 +70,9 @@ constexpr uint32_t kTraceCap = 8192;  // events per traced CTA
 //        MMA 10 S_j issued, 11 PV_j issued;
 //        softmax 20 s_full wait begin, 21 s_full wait end, 22 p_full arrive, 23 o_full wait end,
 //        24 epilogue done.
-__device__ __forceinline__ void trace_ev(const FwdParams& p, uint32_t* counter, uint32_t code,
-                                         uint32_t stream, uint32_t aux) {
-  if (p.trace == nullptr || blockIdx.x >= p.trace_ctas) return;
+__device__ __forceinline__ void trace_ev(bool on, const FwdParams& p, uint32_t* counter,
+                                         uint32_t code, uint32_t stream, uint32_t aux) {
+  if (!on) return;
   const uint32_t i = atomicAdd(counter, 1u);
   if (i >= kTraceCap) return;
   const uint64_t t = static_cast<uint64_t>(clock64()) & ((1ull << 40) - 1);
@@ -236,6 +236,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   }
   const MetaView mv{ctl->order, ctl->cnt, p.order, p.row_cnt, staged};
+  const bool tracing = p.trace != nullptr && blockIdx.x < p.trace_ctas;
 
   if (threadIdx.x == 0) {
     ctl->trace_count = 0;
@@ -284,7 +285,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (uint32_t b = 0; b < C::kBoxes; ++b)
           tma_load_3d(myring + r * C::kTileBytes + b * kBoxBytes, tm, full, b * 64, q * 128, slot,
                       pol_kv);
-        trace_ev(p, &ctl->trace_count, code, s, j);
+        trace_ev(tracing, p, &ctl->trace_count, code, s, j);
         if (++r == C::kRing) { r = 0; rph ^= 1; }
       };
       Item it;
@@ -297,7 +298,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (uint32_t b = 0; b < C::kBoxes; ++b)
           tma_load_3d(sq + s * C::kTileBytes + b * kBoxBytes, &tm_q, &bar_q_full[s], b * 64,
                       it.rt * 128, it.slot, pol_q);
-        trace_ev(p, &ctl->trace_count, 1, s, t);
+        trace_ev(tracing, p, &ctl->trace_count, 1, s, t);
         for (uint32_t j = 0; j < it.nt; ++j) {
           const uint32_t nxt = (j + 1 < it.nt) ? entry_of<MODE>(p, it.rt, j + 1) : 0;
           const uint32_t q = cur & 0x7FFFFFFFu;
@@ -338,7 +339,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (++r == C::kRing) { r = 0; rph ^= 1; }
           if (j + 1 == it.nt) tc_commit(&bar_q_empty[s]);
           tc_commit(&bar_s_full[s]);
-          trace_ev(p, &ctl->trace_count, 10, s, j);
+          trace_ev(tracing, p, &ctl->trace_count, 10, s, j);
           // O += P_j V_j
           mbar_wait(&bar_p_full[s], pph);
           pph ^= 1;
@@ -352,7 +353,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           tc_commit(&ctl->ring_empty[s][r]);
           if (++r == C::kRing) { r = 0; rph ^= 1; }
           if (j + 1 == it.nt) tc_commit(&bar_o_full[s]);
-          trace_ev(p, &ctl->trace_count, 11, s, j);
+          trace_ev(tracing, p, &ctl->trace_count, 11, s, j);
         }
       }
     }
@@ -383,7 +384,23 @@ __global__ void __launch_bounds__(kThreads, 1)
       bool pend;  // finished item waiting for its epilogue
       Item eit;   // item of the pending epilogue
       float e_m_run, e_m_true, e_l;
+      uint2 nbits;      // this half's mask bits of tile j, loaded a turn ahead
+      uint32_t nentry;  // list entry of tile j (dense_binblk: the full flag), a turn ahead
     } st[2];
+
+    // loads for tile j of the current item, issued one engine turn before they are needed; the
+    // bitmap address depends only on (row tile, list position), never on a loaded value
+    auto prefetch = [&](Stream& x) {
+      if (!x.live) return;
+      const uint64_t grow = static_cast<uint64_t>(x.it.rt) * 128 + row;
+      if constexpr (MODE == kModeNaive)
+        x.nbits = __ldg(reinterpret_cast<const uint2*>(p.mask + grow * p.kcols + x.j) + half);
+      else if constexpr (MODE != kModeDense)
+        x.nbits = __ldg(reinterpret_cast<const uint2*>(
+                            p.bitmaps + (static_cast<uint64_t>(x.it.rt) * p.kcols + x.j) * 128 + row) +
+                        half);
+      if constexpr (MODE == kModeDenseBinblk) x.nentry = entry_of<MODE>(p, x.it.rt, x.j);
+    };
 
     // zero rows / stats for items without any tile (fully masked row tiles)
     auto zero_item = [&](const Item& it) {
@@ -422,6 +439,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       st[s].s_phase = st[s].o_phase = 0;
       st[s].pend = false;
       next_item(st[s]);
+      prefetch(st[s]);
     }
     uint32_t step = 0;  // parity selects the max-exchange buffer
 
@@ -438,7 +456,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           mbar_wait(&bar_o_full[s], x.o_phase);
           x.o_phase ^= 1;
           tc_fence_after();
-          if (tracer) trace_ev(p, &ctl->trace_count, 23, s, x.eit.t);
+          if (tracer) trace_ev(tracing, p, &ctl->trace_count, 23, s, x.eit.t);
           // total row sum = both halves' partial sums
           ctl->xchg[step & 1][half][row] = x.e_l;
           named_bar_sync(1, 256);
@@ -484,42 +502,33 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (p.row_sum)
               p.row_sum[si] = l_tot > 0.0f ? l_tot * fast_exp2(x.e_m_run - x.e_m_true) : 0.0f;
           }
-          if (tracer) trace_ev(p, &ctl->trace_count, 24, s, x.eit.t);
+          if (tracer) trace_ev(tracing, p, &ctl->trace_count, 24, s, x.eit.t);
         }
         if (!x.live) continue;
 
         // ---------------- one tile of this stream
         const uint32_t j = x.j;
-        const uint32_t entry = entry_of<MODE>(p, x.it.rt, j);
-        const uint32_t q = entry & 0x7FFFFFFFu;
-        const uint64_t grow = static_cast<uint64_t>(x.it.rt) * 128 + row;
         bool masked;
-        if constexpr (MODE == kModeDense) masked = false;
-        else if constexpr (MODE == kModeDenseBinblk) masked = (entry & 0x80000000u) == 0;
-        else masked = true;
-        uint2 bits = make_uint2(0xFFFFFFFFu, 0xFFFFFFFFu);  // this half's 64 columns
-        if (masked) {
-          const uint4* src;
-          if constexpr (MODE == kModeNaive) src = p.mask + grow * p.kcols + q;
-          else src = p.bitmaps + (static_cast<uint64_t>(x.it.rt) * p.kcols + q) * 128 + row;
-          bits = __ldg(reinterpret_cast<const uint2*>(src) + half);
+        uint2 bits = x.nbits;
+        if constexpr (MODE == kModeDense) {
+          // only the ragged right edge needs a column bound (no bitmap in this mode)
+          masked = ragged && j == last_q;
+          if (masked) {
+            const int v = static_cast<int>(kv_valid_last) - static_cast<int>(half * 64);
+            bits.x = v >= 32 ? 0xFFFFFFFFu : (v <= 0 ? 0u : ((1u << v) - 1u));
+            bits.y = v >= 64 ? 0xFFFFFFFFu : (v <= 32 ? 0u : ((1u << (v - 32)) - 1u));
+          }
+        } else if constexpr (MODE == kModeDenseBinblk) {
+          masked = (x.nentry & 0x80000000u) == 0;  // full tiles skip the mask bits
+        } else {
+          masked = true;  // bitmaps carry zeros beyond n, so ragged edges need nothing extra
         }
-        if (ragged && q == last_q) {
-          // columns >= n do not exist (TMA zero-filled rows of K/V): never visible
-          const int v = static_cast<int>(kv_valid_last) - static_cast<int>(half * 64);
-          const uint32_t w0 = v >= 32 ? 0xFFFFFFFFu : (v <= 0 ? 0u : ((1u << v) - 1u));
-          const uint32_t w1 = v >= 64 ? 0xFFFFFFFFu : (v <= 32 ? 0u : ((1u << (v - 32)) - 1u));
-          bits.x &= w0;
-          bits.y &= w1;
-          masked = true;
-        }
-        masked = __any_sync(0xffffffffu, masked);  // warp-uniform code path
 
-        if (tracer) trace_ev(p, &ctl->trace_count, 20, s, j);
+        if (tracer) trace_ev(tracing, p, &ctl->trace_count, 20, s, j);
         mbar_wait(&bar_s_full[s], x.s_phase);
         x.s_phase ^= 1;
         tc_fence_after();
-        if (tracer) trace_ev(p, &ctl->trace_count, 21, s, j);
+        if (tracer) trace_ev(tracing, p, &ctl->trace_count, 21, s, j);
 
         uint32_t a0[32], a1[32];
         tmem_ld32(ts + half * 64, a0);
@@ -581,7 +590,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         tmem_st_wait();
         tc_fence_before();
         mbar_arrive(&bar_p_full[s]);
-        if (tracer) trace_ev(p, &ctl->trace_count, 22, s, j);
+        if (tracer) trace_ev(tracing, p, &ctl->trace_count, 22, s, j);
 
         if (++x.j == x.it.nt) {  // item done: epilogue on this stream's next turn
           x.pend = true;
@@ -591,6 +600,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           x.e_l = x.l;
           next_item(x);
         }
+        prefetch(x);
       }
     }
   }

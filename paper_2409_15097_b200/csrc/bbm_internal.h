@@ -36,9 +36,11 @@ inline void require(bool cond, const std::string& msg) {
 //   sums      : u32 [krows][kcols]
 //   row_cnt   : u32 [krows]              occupied tiles per query row tile
 //   list      : u32 [krows][kcols]       ascending occupied column tiles, bit 31 = full tile
+//                                        (never set on a ragged right-edge tile)
 //   order     : u32 [krows]              row tiles by descending row_cnt (LPT), ties by index
-//   bitmaps   : uint4 [krows*kcols][128] tile-major copy of every occupied tile's mask bits
-//                                        (row r of tile (p,q) = 16 bytes), written sparsely
+//   bitmaps   : uint4 [krows*kcols][128] tile-major copy of every occupied tile's mask bits at
+//                                        its LIST position: row r of list entry (p,k) at
+//                                        (p*kcols + k)*128 + r (16 bytes), written sparsely
 struct KernelMeta {
   uint32_t krows = 0, kcols = 0;
   uint64_t* mask = nullptr;

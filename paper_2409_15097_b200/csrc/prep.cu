@@ -13,7 +13,8 @@
 //                             (mask.hpp:230-247), ascending compacted KV-tile list (block-wide
 //                             ballot prefix scan) with a full/partial flag.
 //   compact_bitmaps    K3     every occupied 128x128 tile's 2 KiB of mask bits -> tile-major copy
-//                             so the attention kernel reads 16 B per row, fully coalesced.
+//                             at its list position, so the attention kernel reads 16 B per row,
+//                             fully coalesced, at an address known before the list entry.
 //   finalize                  totals over rows (deterministic integer sums) + LPT row order.
 #include <cuda_runtime.h>
 
@@ -160,6 +161,8 @@ __global__ void __launch_bounds__(256) rowmeta_kernel(
     const uint32_t* __restrict__ sums, uint64_t n, uint64_t bi, uint64_t bj, uint64_t cols,
     uint8_t* __restrict__ occ, uint32_t* __restrict__ offset, uint32_t* __restrict__ total,
     uint64_t* __restrict__ row_stats, uint32_t* __restrict__ list, uint32_t* __restrict__ cnt) {
+  // Kernel view only (list != nullptr): a tile narrower than bj (ragged right edge) is never
+  // flagged full, so the attention kernel always applies its bitmap, whose bits beyond n are 0.
   __shared__ uint32_t warp_cnt[8];
   __shared__ uint32_t s_run_start, s_run_end;
   __shared__ unsigned long long s_nz, s_full, s_ones;
@@ -193,7 +196,8 @@ __global__ void __launch_bounds__(256) rowmeta_kernel(
     uint32_t before = base;
     for (uint32_t w = 0; w < warp; ++w) before += warp_cnt[w];
     before += __popc(ballot & ((1u << lane) - 1u));
-    if (list && o) list[p * cols + before] = static_cast<uint32_t>(q) | ((s == a) ? 0x80000000u : 0u);
+    const bool flag_full = s == a && (q + 1) * bj <= n;
+    if (list && o) list[p * cols + before] = static_cast<uint32_t>(q) | (flag_full ? 0x80000000u : 0u);
     uint32_t chunk = 0;
     for (uint32_t w = 0; w < 8; ++w) chunk += warp_cnt[w];
     base += chunk;
@@ -227,7 +231,9 @@ __global__ void __launch_bounds__(256) rowmeta_kernel(
   }
 }
 
-// grid (kcols, krows), 128 threads: CTA copies list entry (p, k) if it exists.
+// grid (kcols, krows), 128 threads: CTA copies the mask bits of list entry (p, k) (if it exists)
+// to bitmap slot (p, k) — indexed by LIST POSITION, so the attention kernel can compute the
+// address of tile j's bits without first loading the list entry.
 __global__ void __launch_bounds__(128) compact_bitmaps_kernel(const uint4* __restrict__ mask,
                                                               uint32_t kcols,
                                                               const uint32_t* __restrict__ list,
@@ -237,7 +243,7 @@ __global__ void __launch_bounds__(128) compact_bitmaps_kernel(const uint4* __res
   if (k >= cnt[p]) return;
   const uint32_t q = list[p * kcols + k] & 0x7FFFFFFFu;
   const uint32_t r = threadIdx.x;
-  bitmaps[(static_cast<uint64_t>(p) * kcols + q) * 128 + r] =
+  bitmaps[(static_cast<uint64_t>(p) * kcols + k) * 128 + r] =
       mask[(static_cast<uint64_t>(p) * 128 + r) * kcols + q];
 }
 

@@ -69,7 +69,9 @@ def expected_kernel_lists(words, n):
     lists = []
     for p in range(kr):
         qs = np.flatnonzero(sums[p] > 0)
-        lists.append([int(q) | (0x80000000 if sums[p, q] == area[p, q] else 0) for q in qs])
+        # full flag (bit 31) is never set on a ragged right-edge tile (the kernel masks it)
+        lists.append([int(q) | (0x80000000 if sums[p, q] == area[p, q] and (q + 1) * 128 <= n else 0)
+                      for q in qs])
     order = sorted(range(kr), key=lambda p: (-int(cnt[p]), p))
     return cnt, lists, order
 
