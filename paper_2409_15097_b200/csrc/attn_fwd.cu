@@ -6,32 +6,39 @@
 // (engine.hpp:311), with an online softmax whose fully-masked rows are exact no-ops
 // (engine.hpp:206-235) and fully-masked output rows written as zeros (engine.hpp:330-332).
 //
-// Structure: one persistent CTA per SM (384 threads) running TWO fully independent query-tile
-// streams that share the tensor core — while softmax warpgroup A turns S_A into P_A, the tensor
-// core runs stream B's MMAs, and vice versa. Each stream walks its own work items (slot, row
-// tile), so row tiles with different KV lists pair up freely (block-sparse masks give every row
-// its own list; FA-style shared KV loops do not apply). Every role blocks in hardware
-// (mbarrier try_wait) on exactly the event it needs; nothing polls.
-//   warps 0, 1   TMA producer of stream A / B: Q tile per item, then K_j, V_j into the stream's
-//                K/V ring (128B-swizzled 64-column boxes).
-//   warps 2, 3   MMA issuer of stream A / B (one thread each; tcgen05.commit tracks the issuing
-//                thread's ops, so the two streams never wait on each other's MMAs):
-//                S = Q K^T (SS, both K-major) into TMEM, O += P V (TS: P read straight from
-//                TMEM, V MN-major). Warp 2 also owns the TMEM allocation (512 columns:
-//                S_A, S_B at [0,256), O_A, O_B at [256,512)).
-//   warps 4-7    softmax + correction + epilogue of stream A (TMEM lane = query row); the
-//                epilogue stages bf16 O in swizzled shared memory and writes it with TMA stores
-//   warps 8-11   same for stream B
+// Work: a (slot, row unit) item, where a row unit is a row tile's whole KV list or — for rows
+// longer than the launch's unit length L — one balanced chunk of it (split-KV). Chunks write
+// unnormalized partials (O, running max, sum) to a workspace and the last chunk to finish
+// combines them. Items are claimed dynamically (one global atomic per item) in slot-major order,
+// longest units first inside a slot.
+//
+// Structure: one persistent CTA per SM (384 threads) running TWO independent item streams that
+// share the tensor core; every role blocks in hardware (mbarrier try_wait) on what it needs.
+//   warps 0, 1   producer of stream A / B: claims items, publishes them through the stream's
+//                shared-memory item queue, loads the Q tile and K_j, V_j into the stream's K/V
+//                ring (TMA, 128B-swizzled 64-column boxes).
+//   warps 2, 3   MMA issuer of stream A / B (one thread; tcgen05.commit tracks the issuing
+//                thread's ops, so the streams never wait on each other's MMAs):
+//                S = Q K^T (SS, both K-major) into TMEM, O += P V (TS: P read from TMEM,
+//                V MN-major). Warp 2 owns the TMEM allocation (512 columns: S_A, S_B at
+//                [0,256), O_A, O_B at [256,512)).
+//   warps 4-11   ONE softmax engine serving the streams in turn (A, B, A, ...): while it turns
+//                S_A into P_A the tensor core runs stream B's MMAs, and vice versa. Warps 4-7
+//                own S columns [0,64) and O columns [0,D/2), warps 8-11 the other halves; the
+//                halves exchange their partial row max through shared memory once per tile.
+//                The epilogue stages bf16 O in 128B-swizzled shared memory for TMA stores.
 // Numerics: scores are scaled into the log2 domain; the running max is only raised when it grows
 // by more than 2^8 (stale-max trick; exact after the final O/l), P is rounded to bf16 for the
-// MMA and written over S in TMEM, l accumulates in fp32. Partial tiles read 16 B of mask bits
-// per row (coalesced, tile-major); full tiles read none.
+// MMA and written over S in TMEM, l accumulates in fp32. Partial tiles read 8 B of mask bits per
+// row and half (coalesced, list-position tile-major, prefetched a turn ahead); full tiles read
+// none under dense_binblk.
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
 #include <cstdint>
+#include <vector>
 
 #include "bbm_internal.h"
 #include "bbm_ptx.cuh"
@@ -44,17 +51,25 @@ using namespace ptx;
 
 enum Mode : int { kModeBinblk = 0, kModeDenseBinblk = 1, kModeDense = 2, kModeNaive = 3 };
 
+constexpr uint32_t kNoSplit = 0xFFFFFFFFu;
+constexpr uint32_t kEnd = 0xFFFFFFFFu;
+
 struct FwdParams {
   uint64_t n;
   uint32_t slots;
   uint32_t krows, kcols;
-  uint32_t total_items;
-  float sl2;  // scale * log2(e)
+  uint32_t units;        // row units per slot
+  uint32_t total_items;  // slots * units
+  float sl2;             // scale * log2(e)
   const uint32_t* list;
-  const uint32_t* row_cnt;
-  const uint32_t* order;
   const uint4* bitmaps;
-  const uint4* mask;  // padded packed mask, kcols uint4 per row
+  const uint4* mask;        // padded packed mask, kcols uint4 per row
+  const uint4* unit_desc;   // [units] {row tile, j0, tiles, split (kNoSplit | row << 8 | chunk)}
+  const uint2* split_info;  // [split rows] {chunks, first workspace chunk}
+  uint32_t split_rows, split_chunks;
+  float* ws;             // [slots][split_chunks][128 * (D + 3)] partial O | m_run | m_true | l
+  uint32_t* split_ctr;   // [slots][split_rows] finished chunks (reset by the combiner)
+  uint32_t* work_ctr;    // [2] next item, finished CTAs (reset by the last CTA)
   __nv_bfloat16* out;
   float* row_max;
   float* row_sum;
@@ -64,6 +79,7 @@ struct FwdParams {
 
 constexpr uint32_t kThreads = 384;
 constexpr uint32_t kTraceCap = 8192;  // events per traced CTA
+constexpr uint32_t kQueue = 4;        // item queue depth per stream
 
 // Trace event: [63:24] clock64 low 40 bits | [23:16] code | [15] stream | [14:0] aux.
 // Codes: producer 1 Q issued (aux = item), 2 K_j issued, 3 V_j issued;
@@ -79,20 +95,23 @@ __device__ __forceinline__ void trace_ev(bool on, const FwdParams& p, uint32_t* 
   p.trace[static_cast<uint64_t>(blockIdx.x) * kTraceCap + i] =
       (t << 24) | (static_cast<uint64_t>(code & 0xFF) << 16) | ((stream & 1u) << 15) | (aux & 0x7FFF);
 }
+
 constexpr uint32_t kBoxBytes = 128 * 64 * 2;  // 128 rows x 64 bf16, one 128B-swizzle box
 constexpr float kRescaleThreshold = 8.0f;     // log2 units
 constexpr float kLn2 = 0.69314718055994530942f;
-
-constexpr uint32_t kMetaRows = 256;  // row tiles whose order / count are staged in smem
 
 template <int D>
 struct Cfg {
   static constexpr uint32_t kBoxes = D / 64;
   static constexpr uint32_t kTileBytes = kBoxes * kBoxBytes;  // one 128 x D bf16 tile
   static constexpr uint32_t kRing = (D == 64) ? 5 : 2;        // K/V ring slots per stream
-  static constexpr uint32_t kStageBytes = kBoxBytes;          // epilogue staging per stream
+  static constexpr uint32_t kStageBytes = kBoxBytes;          // epilogue staging (two buffers)
   static constexpr uint32_t kTmemCols = 512;
   static constexpr uint32_t kOCol = 256;
+};
+
+struct ItemDesc {
+  uint32_t t, slot, rt, j0, nt, split;
 };
 
 // Everything that is not a tile lives behind the tiles in the same dynamic allocation (no static
@@ -101,11 +120,12 @@ template <uint32_t kRing>
 struct SmemCtl {
   uint64_t q_full[2], q_empty[2], s_full[2], p_full[2], o_full[2];
   uint64_t ring_full[2][kRing], ring_empty[2][kRing];
+  uint64_t item_full[2][kQueue], item_empty[2][kQueue];
+  ItemDesc items[2][kQueue];
   uint32_t tmem_base;
   uint32_t trace_count;
+  uint32_t bcast;
   float xchg[2][2][128];  // [exchange parity][half][row]: partial row max / row sum
-  uint16_t cnt[kMetaRows];   // row_cnt, staged when krows <= kMetaRows
-  uint8_t order[kMetaRows];  // LPT order (row tile < 256), staged likewise
 };
 
 template <int D>
@@ -115,54 +135,27 @@ constexpr uint32_t smem_bytes() {
 }
 
 template <int MODE>
-__device__ __forceinline__ uint32_t tiles_of(const FwdParams& p, const uint32_t* cnt,
-                                             uint32_t row_tile) {
-  if constexpr (MODE == kModeDense || MODE == kModeNaive) return p.kcols;
-  else return cnt[row_tile];
-}
-
-template <int MODE>
 __device__ __forceinline__ uint32_t entry_of(const FwdParams& p, uint32_t row_tile, uint32_t j) {
   if constexpr (MODE == kModeDense || MODE == kModeNaive) return j;
   else return p.list[static_cast<uint64_t>(row_tile) * p.kcols + j];
 }
 
-// Work item t -> (slot, row tile): slot-major (K/V reuse across a slot's row tiles stays in L2),
-// row tiles in LPT order inside a slot.
-struct Item {
-  uint32_t t, slot, rt, nt;
-};
-
-// Row order / counts come from the smem copies when krows <= kMetaRows, else from global.
-struct MetaView {
-  const uint8_t* order_s;
-  const uint16_t* cnt_s;
-  const uint32_t* order_g;
-  const uint32_t* cnt_g;
-  bool staged;
-};
-
-template <int MODE>
-__device__ __forceinline__ Item make_item(const FwdParams& p, const MetaView& mv, uint32_t t) {
-  Item it;
-  it.t = t;
-  it.slot = t / p.krows;
-  const uint32_t k = t - it.slot * p.krows;
-  it.rt = mv.staged ? mv.order_s[k] : mv.order_g[k];
-  if constexpr (MODE == kModeDense || MODE == kModeNaive) it.nt = p.kcols;
-  else it.nt = mv.staged ? mv.cnt_s[it.rt] : mv.cnt_g[it.rt];
-  return it;
-}
-
-// Next item with work (nt > 0) of a stream whose items are t0, t0 + stride, ...
-template <int MODE>
-__device__ __forceinline__ bool next_busy_item(const FwdParams& p, const MetaView& mv, uint32_t& t,
-                                               uint32_t stride, Item& it) {
-  for (; t < p.total_items; t += stride) {
-    it = make_item<MODE>(p, mv, t);
-    if (it.nt > 0) return true;
+__device__ __forceinline__ ItemDesc decode_item(const FwdParams& p, uint32_t t) {
+  ItemDesc d;
+  d.t = t;
+  if (t >= p.total_items) {
+    d.t = kEnd;
+    d.slot = d.rt = d.j0 = d.nt = 0;
+    d.split = kNoSplit;
+    return d;
   }
-  return false;
+  d.slot = t / p.units;
+  const uint4 u = p.unit_desc[t - d.slot * p.units];
+  d.rt = u.x;
+  d.j0 = u.y;
+  d.nt = u.z;
+  d.split = u.w;
+  return d;
 }
 
 // Masked max of 32 raw scores of one row chunk (negated first when the scale is negative).
@@ -207,6 +200,20 @@ __device__ __forceinline__ void chunk_exp(const uint32_t (&r)[32], uint32_t mw, 
   }
 }
 
+// 32 fp32 -> 4 x 16 B of bf16 into a 128B-swizzled staging row
+__device__ __forceinline__ void stage_chunk32(uint8_t* rowp, uint32_t row, uint32_t chunk0,
+                                              const float* v, float inv) {
+#pragma unroll
+  for (uint32_t c = 0; c < 4; ++c) {
+    uint4 w;
+    w.x = pack_bf16x2(v[c * 8 + 0] * inv, v[c * 8 + 1] * inv);
+    w.y = pack_bf16x2(v[c * 8 + 2] * inv, v[c * 8 + 3] * inv);
+    w.z = pack_bf16x2(v[c * 8 + 4] * inv, v[c * 8 + 5] * inv);
+    w.w = pack_bf16x2(v[c * 8 + 6] * inv, v[c * 8 + 7] * inv);
+    *reinterpret_cast<uint4*>(rowp + (((chunk0 + c) ^ (row & 7)) << 4)) = w;
+  }
+}
+
 template <int D, int MODE>
 __global__ void __launch_bounds__(kThreads, 1)
     attn_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
@@ -214,44 +221,32 @@ __global__ void __launch_bounds__(kThreads, 1)
                     const FwdParams p) {
   using C = Cfg<D>;
   extern __shared__ __align__(1024) uint8_t smem[];
-  uint8_t* sq = smem;                      // [2][tile]     Q of each stream
-  uint8_t* ring = sq + 2 * C::kTileBytes;  // [2][kRing][tile] K/V ring of each stream
+  uint8_t* sq = smem;                                    // [2][tile]          Q of each stream
+  uint8_t* ring = sq + 2 * C::kTileBytes;                // [2][kRing][tile]   K/V ring per stream
   uint8_t* stage = ring + 2 * C::kRing * C::kTileBytes;  // [2][128 x 64 bf16] epilogue staging
   auto* ctl = reinterpret_cast<SmemCtl<C::kRing>*>(stage + 2 * C::kStageBytes);
-  uint64_t* bar_q_full = ctl->q_full;
-  uint64_t* bar_q_empty = ctl->q_empty;
-  uint64_t* bar_s_full = ctl->s_full;
-  uint64_t* bar_p_full = ctl->p_full;
-  uint64_t* bar_o_full = ctl->o_full;
 
   const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint32_t stride = 2 * gridDim.x;  // items of stream s: 2*blockIdx.x + s + k*stride
   if ((smem_u32(smem) & 1023u) != 0) __trap();  // 128B-swizzle atoms need 1024-byte alignment
-
-  const bool staged = p.krows <= kMetaRows;
-  if (staged) {
-    for (uint32_t i = threadIdx.x; i < p.krows; i += blockDim.x) {
-      ctl->order[i] = static_cast<uint8_t>(p.order[i]);
-      ctl->cnt[i] = static_cast<uint16_t>(p.row_cnt[i]);
-    }
-  }
-  const MetaView mv{ctl->order, ctl->cnt, p.order, p.row_cnt, staged};
   const bool tracing = p.trace != nullptr && blockIdx.x < p.trace_ctas;
 
   if (threadIdx.x == 0) {
     ctl->trace_count = 0;
     for (int s = 0; s < 2; ++s) {
-      mbar_init(&bar_q_full[s], 1);
-      mbar_init(&bar_q_empty[s], 1);
-      mbar_init(&bar_s_full[s], 1);
-      mbar_init(&bar_p_full[s], 256);
-      mbar_init(&bar_o_full[s], 1);
-    }
-    for (int s = 0; s < 2; ++s)
+      mbar_init(&ctl->q_full[s], 1);
+      mbar_init(&ctl->q_empty[s], 1);
+      mbar_init(&ctl->s_full[s], 1);
+      mbar_init(&ctl->p_full[s], 256);
+      mbar_init(&ctl->o_full[s], 1);
       for (uint32_t r = 0; r < C::kRing; ++r) {
         mbar_init(&ctl->ring_full[s][r], 1);
         mbar_init(&ctl->ring_empty[s][r], 1);
       }
+      for (uint32_t r = 0; r < kQueue; ++r) {
+        mbar_init(&ctl->item_full[s][r], 1);
+        mbar_init(&ctl->item_empty[s][r], 2);  // MMA issuer + softmax engine
+      }
+    }
     fence_barrier_init();
   }
   if (warp == 0 && lane == 0) {
@@ -270,12 +265,12 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t tmem = ctl->tmem_base;
 
   if (warp < 2) {
-    // ------------------------------------------------------------------ TMA producer (stream = warp)
+    // ------------------------------------------------------------------ producer (stream = warp)
     if (lane == 0) {
       const int s = static_cast<int>(warp);
       const uint64_t pol_q = policy_evict_first();
       const uint64_t pol_kv = policy_evict_last();
-      uint32_t r = 0, rph = 1, qph = 1;
+      uint32_t r = 0, rph = 1, qph = 1, qi = 0, qiph = 1;
       uint8_t* myring = ring + s * C::kRing * C::kTileBytes;
       auto load_tile = [&](const CUtensorMap* tm, uint32_t q, uint32_t slot, uint32_t code,
                            uint32_t j) {
@@ -288,22 +283,28 @@ __global__ void __launch_bounds__(kThreads, 1)
         trace_ev(tracing, p, &ctl->trace_count, code, s, j);
         if (++r == C::kRing) { r = 0; rph ^= 1; }
       };
-      Item it;
-      for (uint32_t t = 2 * blockIdx.x + s; next_busy_item<MODE>(p, mv, t, stride, it); t += stride) {
+      for (;;) {
+        const ItemDesc d = decode_item(p, atomicAdd(&p.work_ctr[0], 1u));
+        mbar_wait(&ctl->item_empty[s][qi], qiph);
+        ctl->items[s][qi] = d;
+        mbar_arrive(&ctl->item_full[s][qi]);  // release: the descriptor is visible to waiters
+        if (++qi == kQueue) { qi = 0; qiph ^= 1; }
+        if (d.t == kEnd) break;
+        if (d.nt == 0) continue;
         // list entries one tile ahead so the TMA issue never waits on an L2 load
-        uint32_t cur = entry_of<MODE>(p, it.rt, 0);
-        mbar_wait(&bar_q_empty[s], qph);
+        uint32_t cur = entry_of<MODE>(p, d.rt, d.j0);
+        mbar_wait(&ctl->q_empty[s], qph);
         qph ^= 1;
-        mbar_arrive_expect_tx(&bar_q_full[s], C::kTileBytes);
+        mbar_arrive_expect_tx(&ctl->q_full[s], C::kTileBytes);
         for (uint32_t b = 0; b < C::kBoxes; ++b)
-          tma_load_3d(sq + s * C::kTileBytes + b * kBoxBytes, &tm_q, &bar_q_full[s], b * 64,
-                      it.rt * 128, it.slot, pol_q);
-        trace_ev(tracing, p, &ctl->trace_count, 1, s, t);
-        for (uint32_t j = 0; j < it.nt; ++j) {
-          const uint32_t nxt = (j + 1 < it.nt) ? entry_of<MODE>(p, it.rt, j + 1) : 0;
+          tma_load_3d(sq + s * C::kTileBytes + b * kBoxBytes, &tm_q, &ctl->q_full[s], b * 64,
+                      d.rt * 128, d.slot, pol_q);
+        trace_ev(tracing, p, &ctl->trace_count, 1, s, d.t);
+        for (uint32_t j = 0; j < d.nt; ++j) {
+          const uint32_t nxt = (j + 1 < d.nt) ? entry_of<MODE>(p, d.rt, d.j0 + j + 1) : 0;
           const uint32_t q = cur & 0x7FFFFFFFu;
-          load_tile(&tm_k, q, it.slot, 2, j);
-          load_tile(&tm_v, q, it.slot, 3, j);
+          load_tile(&tm_k, q, d.slot, 2, j);
+          load_tile(&tm_v, q, d.slot, 3, j);
           cur = nxt;
         }
       }
@@ -319,12 +320,17 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t qbase = smem_u32(sq) + s * C::kTileBytes;
       const uint32_t rbase = smem_u32(ring) + s * C::kRing * C::kTileBytes;
       const uint32_t tmem_s = tmem + s * 128, tmem_o = tmem + C::kOCol + s * 128;
-      uint32_t r = 0, rph = 0, qph = 0, pph = 0;
-      Item it;
-      for (uint32_t t = 2 * blockIdx.x + s; next_busy_item<MODE>(p, mv, t, stride, it); t += stride) {
-        mbar_wait(&bar_q_full[s], qph);
+      uint32_t r = 0, rph = 0, qph = 0, pph = 0, qi = 0, qiph = 0;
+      for (;;) {
+        mbar_wait(&ctl->item_full[s][qi], qiph);
+        const ItemDesc d = ctl->items[s][qi];
+        mbar_arrive(&ctl->item_empty[s][qi]);
+        if (++qi == kQueue) { qi = 0; qiph ^= 1; }
+        if (d.t == kEnd) break;
+        if (d.nt == 0) continue;
+        mbar_wait(&ctl->q_full[s], qph);
         qph ^= 1;
-        for (uint32_t j = 0; j < it.nt; ++j) {
+        for (uint32_t j = 0; j < d.nt; ++j) {
           // S_j = Q K_j^T
           mbar_wait(&ctl->ring_full[s][r], rph);
           tc_fence_after();
@@ -337,11 +343,11 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
           tc_commit(&ctl->ring_empty[s][r]);
           if (++r == C::kRing) { r = 0; rph ^= 1; }
-          if (j + 1 == it.nt) tc_commit(&bar_q_empty[s]);
-          tc_commit(&bar_s_full[s]);
+          if (j + 1 == d.nt) tc_commit(&ctl->q_empty[s]);
+          tc_commit(&ctl->s_full[s]);
           trace_ev(tracing, p, &ctl->trace_count, 10, s, j);
           // O += P_j V_j
-          mbar_wait(&bar_p_full[s], pph);
+          mbar_wait(&ctl->p_full[s], pph);
           pph ^= 1;
           mbar_wait(&ctl->ring_full[s][r], rph);
           tc_fence_after();
@@ -352,17 +358,13 @@ __global__ void __launch_bounds__(kThreads, 1)
                     idesc_o, (j > 0 || kk > 0) ? 1u : 0u);
           tc_commit(&ctl->ring_empty[s][r]);
           if (++r == C::kRing) { r = 0; rph ^= 1; }
-          if (j + 1 == it.nt) tc_commit(&bar_o_full[s]);
+          if (j + 1 == d.nt) tc_commit(&ctl->o_full[s]);
           trace_ev(tracing, p, &ctl->trace_count, 11, s, j);
         }
       }
     }
   } else if (warp >= 4) {
     // ------------------------------------------------------------------ softmax engine
-    // ONE engine of 8 warps serves both streams in turn (A, B, A, B, ...): while it turns S_A
-    // into P_A the tensor core runs stream B's MMAs, and vice versa. Warps 4-7 own S/O columns
-    // [0, 64) / [0, D/2), warps 8-11 the other half; the two halves exchange their partial row
-    // max through shared memory once per tile, so both hold identical softmax state.
     const uint32_t half = (warp >= 8) ? 1u : 0u;
     const uint32_t quad = warp & 3;
     const uint32_t row = quad * 32 + lane;
@@ -377,71 +379,104 @@ __global__ void __launch_bounds__(kThreads, 1)
     constexpr uint32_t kHalfO = D / 2;  // O columns per half
 
     struct Stream {
-      uint32_t t, j, s_phase, o_phase;
-      Item it;
+      uint32_t j, s_phase, o_phase, qi, qiph;
+      ItemDesc it;
       float m_run, m_true, l;
-      bool live;  // has an item with tiles in progress
-      bool pend;  // finished item waiting for its epilogue
-      Item eit;   // item of the pending epilogue
+      bool live;   // an item with tiles is in progress
+      bool ended;  // the producer published kEnd
+      bool pend;   // finished item waiting for its epilogue
+      ItemDesc eit;  // item of the pending epilogue
       float e_m_run, e_m_true, e_l;
       uint2 nbits;      // this half's mask bits of tile j, loaded a turn ahead
       uint32_t nentry;  // list entry of tile j (dense_binblk: the full flag), a turn ahead
     } st[2];
 
-    // loads for tile j of the current item, issued one engine turn before they are needed; the
-    // bitmap address depends only on (row tile, list position), never on a loaded value
-    auto prefetch = [&](Stream& x) {
-      if (!x.live) return;
-      const uint64_t grow = static_cast<uint64_t>(x.it.rt) * 128 + row;
-      if constexpr (MODE == kModeNaive)
-        x.nbits = __ldg(reinterpret_cast<const uint2*>(p.mask + grow * p.kcols + x.j) + half);
-      else if constexpr (MODE != kModeDense)
-        x.nbits = __ldg(reinterpret_cast<const uint2*>(
-                            p.bitmaps + (static_cast<uint64_t>(x.it.rt) * p.kcols + x.j) * 128 + row) +
-                        half);
-      if constexpr (MODE == kModeDenseBinblk) x.nentry = entry_of<MODE>(p, x.it.rt, x.j);
-    };
+    uint32_t step = 0;  // parity selects the exchange buffer
 
+    auto write_stats = [&](const ItemDesc& it, float m_true2, float m_run2, float l_tot) {
+      const uint64_t grow = static_cast<uint64_t>(it.rt) * 128 + row;
+      if (half == 0 && grow < p.n) {
+        const uint64_t si = static_cast<uint64_t>(it.slot) * p.n + grow;
+        if (p.row_max) p.row_max[si] = m_true2 == -INFINITY ? -INFINITY : m_true2 * kLn2;
+        if (p.row_sum) p.row_sum[si] = l_tot > 0.0f ? l_tot * exp2f(m_run2 - m_true2) : 0.0f;
+      }
+    };
     // zero rows / stats for items without any tile (fully masked row tiles)
-    auto zero_item = [&](const Item& it) {
+    auto zero_item = [&](const ItemDesc& it) {
       const uint64_t grow = static_cast<uint64_t>(it.rt) * 128 + row;
       if (grow >= p.n) return;
       uint4* dst = reinterpret_cast<uint4*>(p.out + (static_cast<uint64_t>(it.slot) * p.n + grow) * D +
                                             half * kHalfO);
       for (uint32_t v = 0; v < kHalfO / 8; ++v) dst[v] = make_uint4(0, 0, 0, 0);
-      if (half == 0) {
-        const uint64_t si = static_cast<uint64_t>(it.slot) * p.n + grow;
-        if (p.row_max) p.row_max[si] = -INFINITY;
-        if (p.row_sum) p.row_sum[si] = 0.0f;
+      write_stats(it, -INFINITY, -INFINITY, 0.0f);
+    };
+    // TMA-store the staged O tile of item `it` (called by every engine thread)
+    auto store_staged = [&](const ItemDesc& it) {
+      fence_proxy_async_smem();
+      named_bar_sync(1, 256);
+      if (leader) {
+        tma_store_3d(&tm_o, stage, 0, it.rt * 128, it.slot);
+        if (D == 128) tma_store_3d(&tm_o, stage + C::kStageBytes, 64, it.rt * 128, it.slot);
+        bulk_commit_group();
       }
     };
-    // advance stream x to its next item that has tiles (writing zero items on the way)
-    auto next_item = [&](Stream& x) {
+    auto stage_wait_free = [&]() {
+      if (leader) bulk_wait_group_read<0>();  // staging buffers free again
+      named_bar_sync(1, 256);
+    };
+    // D=128: half h stages columns [64h, 64h+64) in buffer h; D=64: both halves share buffer 0,
+    // 32 columns (4 chunks) each
+    uint8_t* stg_row = stage + (D == 128 ? half * C::kStageBytes : 0) + row * 128;
+
+    // loads for tile j of the current item, issued one engine turn before they are needed; the
+    // bitmap address depends only on (row tile, list position), never on a loaded value
+    auto prefetch = [&](Stream& x) {
+      if (!x.live) return;
+      const uint32_t jj = x.it.j0 + x.j;
+      const uint64_t grow = static_cast<uint64_t>(x.it.rt) * 128 + row;
+      if constexpr (MODE == kModeNaive)
+        x.nbits = __ldg(reinterpret_cast<const uint2*>(p.mask + grow * p.kcols + jj) + half);
+      else if constexpr (MODE != kModeDense)
+        x.nbits = __ldg(reinterpret_cast<const uint2*>(
+                            p.bitmaps + (static_cast<uint64_t>(x.it.rt) * p.kcols + jj) * 128 + row) +
+                        half);
+      if constexpr (MODE == kModeDenseBinblk) x.nentry = entry_of<MODE>(p, x.it.rt, jj);
+    };
+    // pull this stream's next item with tiles from its queue (writing zero items on the way)
+    auto next_item = [&](Stream& x, int s) {
       x.live = false;
-      for (; x.t < p.total_items; x.t += stride) {
-        const Item it = make_item<MODE>(p, mv, x.t);
-        if (it.nt == 0) {
-          zero_item(it);
+      while (!x.ended) {
+        mbar_wait(&ctl->item_full[s][x.qi], x.qiph);
+        const ItemDesc d = ctl->items[s][x.qi];
+        named_bar_sync(1, 256);  // every engine thread has read the descriptor
+        if (leader) mbar_arrive(&ctl->item_empty[s][x.qi]);
+        if (++x.qi == kQueue) { x.qi = 0; x.qiph ^= 1; }
+        if (d.t == kEnd) {
+          x.ended = true;
+          break;
+        }
+        if (d.nt == 0) {
+          zero_item(d);
           continue;
         }
-        x.it = it;
+        x.it = d;
         x.j = 0;
         x.m_run = -INFINITY;
         x.m_true = -INFINITY;
         x.l = 0.0f;
         x.live = true;
-        x.t += stride;
         break;
       }
+      prefetch(x);
     };
     for (int s = 0; s < 2; ++s) {
-      st[s].t = 2 * blockIdx.x + s;
       st[s].s_phase = st[s].o_phase = 0;
+      st[s].qi = 0;
+      st[s].qiph = 0;
       st[s].pend = false;
-      next_item(st[s]);
-      prefetch(st[s]);
+      st[s].ended = false;
+      next_item(st[s], s);
     }
-    uint32_t step = 0;  // parity selects the max-exchange buffer
 
     while (st[0].live || st[0].pend || st[1].live || st[1].pend) {
 #pragma unroll
@@ -453,54 +488,106 @@ __global__ void __launch_bounds__(kThreads, 1)
         // while the engine served the other stream)
         if (x.pend) {
           x.pend = false;
-          mbar_wait(&bar_o_full[s], x.o_phase);
+          mbar_wait(&ctl->o_full[s], x.o_phase);
           x.o_phase ^= 1;
           tc_fence_after();
           if (tracer) trace_ev(tracing, p, &ctl->trace_count, 23, s, x.eit.t);
-          // total row sum = both halves' partial sums
+          // total row sum of this unit = both halves' partial sums
           ctl->xchg[step & 1][half][row] = x.e_l;
           named_bar_sync(1, 256);
-          const float l_tot = x.e_l + ctl->xchg[step & 1][half ^ 1][row];
+          const float l_unit = x.e_l + ctl->xchg[step & 1][half ^ 1][row];
           ++step;
-          const float inv = l_tot > 0.0f ? 1.0f / l_tot : 0.0f;
-          if (leader) bulk_wait_group_read<0>();  // staging buffers free again
-          named_bar_sync(1, 256);
-          // D=128: half h stages columns [64h, 64h+64) in buffer h; D=64: both halves share
-          // buffer 0, 32 columns (4 chunks) each
-          uint8_t* stg = stage + (D == 128 ? half * C::kStageBytes : 0);
-          uint8_t* rowp = stg + row * 128;
+          if (x.eit.split == kNoSplit) {
+            const float inv = l_unit > 0.0f ? 1.0f / l_unit : 0.0f;
+            stage_wait_free();
 #pragma unroll
-          for (uint32_t c32 = 0; c32 < kHalfO / 32; ++c32) {
-            uint32_t o[32];
-            tmem_ld32(to + half * kHalfO + c32 * 32, o);
-            tmem_ld_wait();
-#pragma unroll
-            for (uint32_t c = 0; c < 4; ++c) {
-              const uint32_t chunk = (D == 128 ? c32 * 4 : half * 4) + c;
-              uint4 w;
-              w.x = pack_bf16x2(__uint_as_float(o[c * 8 + 0]) * inv, __uint_as_float(o[c * 8 + 1]) * inv);
-              w.y = pack_bf16x2(__uint_as_float(o[c * 8 + 2]) * inv, __uint_as_float(o[c * 8 + 3]) * inv);
-              w.z = pack_bf16x2(__uint_as_float(o[c * 8 + 4]) * inv, __uint_as_float(o[c * 8 + 5]) * inv);
-              w.w = pack_bf16x2(__uint_as_float(o[c * 8 + 6]) * inv, __uint_as_float(o[c * 8 + 7]) * inv);
-              *reinterpret_cast<uint4*>(rowp + ((chunk ^ (row & 7)) << 4)) = w;
+            for (uint32_t c32 = 0; c32 < kHalfO / 32; ++c32) {
+              uint32_t o[32];
+              tmem_ld32(to + half * kHalfO + c32 * 32, o);
+              tmem_ld_wait();
+              stage_chunk32(stg_row, row, D == 128 ? c32 * 4 : half * 4,
+                            reinterpret_cast<const float*>(o), inv);
             }
-          }
-          // O TMEM of this stream may now be overwritten (its next first PV waits for this
-          // engine's next p_full arrival on this stream, which comes later)
-          tc_fence_before();
-          fence_proxy_async_smem();
-          named_bar_sync(1, 256);
-          if (leader) {
-            tma_store_3d(&tm_o, stage, 0, x.eit.rt * 128, x.eit.slot);
-            if (D == 128) tma_store_3d(&tm_o, stage + C::kStageBytes, 64, x.eit.rt * 128, x.eit.slot);
-            bulk_commit_group();
-          }
-          const uint64_t grow = static_cast<uint64_t>(x.eit.rt) * 128 + row;
-          if (half == 0 && grow < p.n) {
-            const uint64_t si = static_cast<uint64_t>(x.eit.slot) * p.n + grow;
-            if (p.row_max) p.row_max[si] = x.e_m_true == -INFINITY ? -INFINITY : x.e_m_true * kLn2;
-            if (p.row_sum)
-              p.row_sum[si] = l_tot > 0.0f ? l_tot * fast_exp2(x.e_m_run - x.e_m_true) : 0.0f;
+            // O TMEM of this stream may be overwritten from here on (its next first PV waits
+            // for this engine's next p_full arrival on this stream)
+            tc_fence_before();
+            store_staged(x.eit);
+            write_stats(x.eit, x.e_m_true, x.e_m_run, l_unit);
+          } else {
+            // ---- split-KV chunk: publish the unnormalized partial, the last chunk combines
+            const uint32_t srow = x.eit.split >> 8, chunk = x.eit.split & 0xFF;
+            const uint2 si = p.split_info[srow];  // {chunks, first workspace chunk}
+            const uint64_t blk = static_cast<uint64_t>(128) * (D + 3);
+            float* wsb =
+                p.ws + (static_cast<uint64_t>(x.eit.slot) * p.split_chunks + si.y + chunk) * blk;
+#pragma unroll
+            for (uint32_t c32 = 0; c32 < kHalfO / 32; ++c32) {
+              uint32_t o[32];
+              tmem_ld32(to + half * kHalfO + c32 * 32, o);
+              tmem_ld_wait();
+              uint4* dst = reinterpret_cast<uint4*>(wsb + row * D + half * kHalfO + c32 * 32);
+#pragma unroll
+              for (uint32_t v = 0; v < 8; ++v)
+                dst[v] = make_uint4(o[v * 4], o[v * 4 + 1], o[v * 4 + 2], o[v * 4 + 3]);
+            }
+            tc_fence_before();
+            if (half == 0) {
+              wsb[128 * D + row] = x.e_m_run;
+              wsb[128 * D + 128 + row] = x.e_m_true;
+              wsb[128 * D + 256 + row] = l_unit;
+            }
+            __threadfence();
+            named_bar_sync(1, 256);
+            uint32_t* ctr = p.split_ctr + static_cast<uint64_t>(x.eit.slot) * p.split_rows + srow;
+            if (leader) ctl->bcast = atomicAdd(ctr, 1u);
+            named_bar_sync(1, 256);
+            const uint32_t done_before = ctl->bcast;
+            if (done_before + 1 == si.x) {
+              // last chunk: combine every chunk's partial for this row tile
+              __threadfence();
+              const float* base =
+                  p.ws + (static_cast<uint64_t>(x.eit.slot) * p.split_chunks + si.y) * blk;
+              float mrun = -INFINITY, mtrue = -INFINITY;
+              for (uint32_t c = 0; c < si.x; ++c) {
+                const float* b = base + c * blk + 128 * D;
+                if (__ldcg(b + 256 + row) > 0.0f) mrun = fmaxf(mrun, __ldcg(b + row));
+                mtrue = fmaxf(mtrue, __ldcg(b + 128 + row));
+              }
+              float ltot = 0.0f;
+              for (uint32_t c = 0; c < si.x; ++c) {
+                const float* b = base + c * blk + 128 * D;
+                const float lc = __ldcg(b + 256 + row);
+                if (lc > 0.0f) ltot += lc * exp2f(__ldcg(b + row) - mrun);
+              }
+              const float inv = ltot > 0.0f ? 1.0f / ltot : 0.0f;
+              stage_wait_free();
+              if (leader) *ctr = 0;  // every engine thread has read the count: reset for reuse
+#pragma unroll 1
+              for (uint32_t c32 = 0; c32 < kHalfO / 32; ++c32) {
+                float acc[32];
+#pragma unroll
+                for (uint32_t i = 0; i < 32; ++i) acc[i] = 0.0f;
+                for (uint32_t c = 0; c < si.x; ++c) {
+                  const float* b = base + c * blk;
+                  const float lc = __ldcg(b + 128 * D + 256 + row);
+                  if (!(lc > 0.0f)) continue;
+                  const float w = exp2f(__ldcg(b + 128 * D + row) - mrun);
+                  const float4* src =
+                      reinterpret_cast<const float4*>(b + row * D + half * kHalfO + c32 * 32);
+#pragma unroll
+                  for (uint32_t v = 0; v < 8; ++v) {
+                    const float4 f = __ldcg(src + v);
+                    acc[v * 4 + 0] += w * f.x;
+                    acc[v * 4 + 1] += w * f.y;
+                    acc[v * 4 + 2] += w * f.z;
+                    acc[v * 4 + 3] += w * f.w;
+                  }
+                }
+                stage_chunk32(stg_row, row, D == 128 ? c32 * 4 : half * 4, acc, inv);
+              }
+              store_staged(x.eit);
+              write_stats(x.eit, mtrue, mrun, ltot);
+            }
           }
           if (tracer) trace_ev(tracing, p, &ctl->trace_count, 24, s, x.eit.t);
         }
@@ -512,7 +599,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         uint2 bits = x.nbits;
         if constexpr (MODE == kModeDense) {
           // only the ragged right edge needs a column bound (no bitmap in this mode)
-          masked = ragged && j == last_q;
+          masked = ragged && x.it.j0 + j == last_q;
           if (masked) {
             const int v = static_cast<int>(kv_valid_last) - static_cast<int>(half * 64);
             bits.x = v >= 32 ? 0xFFFFFFFFu : (v <= 0 ? 0u : ((1u << v) - 1u));
@@ -525,7 +612,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
 
         if (tracer) trace_ev(tracing, p, &ctl->trace_count, 20, s, j);
-        mbar_wait(&bar_s_full[s], x.s_phase);
+        mbar_wait(&ctl->s_full[s], x.s_phase);
         x.s_phase ^= 1;
         tc_fence_after();
         if (tracer) trace_ev(tracing, p, &ctl->trace_count, 21, s, j);
@@ -542,15 +629,16 @@ __global__ void __launch_bounds__(kThreads, 1)
           pmax = neg ? fmaxf(chunk_max<false, true>(a0, 0), chunk_max<false, true>(a1, 0))
                      : fmaxf(chunk_max<false, false>(a0, 0), chunk_max<false, false>(a1, 0));
         }
-        // exchange with the other half (double-buffered by step parity); after this barrier
-        // every S read of this tile has completed, so P may overwrite S columns [0, 64)
+        // exchange with the other half (double-buffered by parity); after this barrier every S
+        // read of this tile has completed, so P may overwrite S columns [0, 64)
         ctl->xchg[step & 1][half][row] = pmax;
         named_bar_sync(1, 256);
         float tmax = fmaxf(pmax, ctl->xchg[step & 1][half ^ 1][row]);
         ++step;
         tmax = tmax == -INFINITY ? -INFINITY : tmax * abs_sl2;  // log2 domain
         x.m_true = fmaxf(x.m_true, tmax);
-        const bool need = tmax > x.m_run + kRescaleThreshold || (x.m_run == -INFINITY && tmax > -INFINITY);
+        const bool need =
+            tmax > x.m_run + kRescaleThreshold || (x.m_run == -INFINITY && tmax > -INFINITY);
         const bool rescale_o = need && j > 0 && x.m_run > -INFINITY;
         float factor = 1.0f;
         if (need) {
@@ -589,7 +677,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         x.l += f2_lo(lacc) + f2_hi(lacc);
         tmem_st_wait();
         tc_fence_before();
-        mbar_arrive(&bar_p_full[s]);
+        mbar_arrive(&ctl->p_full[s]);
         if (tracer) trace_ev(tracing, p, &ctl->trace_count, 22, s, j);
 
         if (++x.j == x.it.nt) {  // item done: epilogue on this stream's next turn
@@ -598,23 +686,104 @@ __global__ void __launch_bounds__(kThreads, 1)
           x.e_m_run = x.m_run;
           x.e_m_true = x.m_true;
           x.e_l = x.l;
-          next_item(x);
+          next_item(x, s);
+        } else {
+          prefetch(x);
         }
-        prefetch(x);
       }
     }
+    if (leader) bulk_wait_group<0>();  // O stores landed
   }
 
-  if (warp == 4 && lane == 0) bulk_wait_group<0>();  // O stores landed
   tc_fence_before();
   __syncthreads();
   if (warp == 2) tmem_dealloc<C::kTmemCols>(tmem);
+  // the last CTA out resets the work counter for the next launch (stream-ordered)
+  if (threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(&p.work_ctr[1], 1u) == gridDim.x - 1) {
+      p.work_ctr[0] = 0;
+      p.work_ctr[1] = 0;
+      __threadfence();
+    }
+  }
+}
+
+// ------------------------------------------------------------------ host side
+
+// Row units for a launch: row tiles longer than L are split into balanced chunks. With dynamic
+// longest-first claiming the makespan is about (average work per stream + longest unit), so L is
+// half a stream's average share (at least 16 tiles: combining partials is not free).
+struct UnitBuild {
+  std::vector<uint4> desc;
+  std::vector<uint2> split_info;
+  uint32_t split_chunks = 0;
+};
+
+UnitBuild build_units(const std::vector<uint32_t>& row_tiles, uint64_t slots, int streams) {
+  uint64_t total = 0;
+  for (uint32_t c : row_tiles) total += c;
+  total *= slots;
+  const uint64_t per_stream = total / static_cast<uint64_t>(std::max(1, streams));
+  const uint32_t L = static_cast<uint32_t>(std::max<uint64_t>(16, (per_stream + 1) / 2));
+  UnitBuild ub;
+  struct U {
+    uint32_t rt, j0, nt, split;
+  };
+  std::vector<U> units;
+  for (uint32_t p = 0; p < row_tiles.size(); ++p) {
+    const uint32_t nt = row_tiles[p];
+    if (nt <= L) {
+      units.push_back({p, 0, nt, kNoSplit});
+      continue;
+    }
+    const uint32_t k = std::min<uint32_t>((nt + L - 1) / L, 255);
+    const uint32_t srow = static_cast<uint32_t>(ub.split_info.size());
+    ub.split_info.push_back(make_uint2(k, ub.split_chunks));
+    ub.split_chunks += k;
+    uint32_t j0 = 0;
+    for (uint32_t c = 0; c < k; ++c) {
+      const uint32_t len = nt / k + (c < nt % k ? 1 : 0);
+      units.push_back({p, j0, len, (srow << 8) | c});
+      j0 += len;
+    }
+  }
+  std::stable_sort(units.begin(), units.end(), [](const U& a, const U& b) { return a.nt > b.nt; });
+  for (const U& u : units) ub.desc.push_back(make_uint4(u.rt, u.j0, u.nt, u.split));
+  return ub;
 }
 
 template <int D, int MODE>
 void launch_impl(const Prep& prep, const AttnArgs& a, cudaStream_t s, int num_sms) {
   static_assert(smem_bytes<D>() <= 232448, "exceeds the 227 KB opt-in shared memory");
   const KernelMeta& km = prep.kmeta;
+  constexpr bool kAllTiles = (MODE == kModeDense || MODE == kModeNaive);
+  const uint32_t grid = std::min<uint32_t>(
+      static_cast<uint32_t>(std::max<uint64_t>(1, (a.slots * km.krows + 1) / 2)),
+      static_cast<uint32_t>(num_sms));
+  const LaunchPlan& plan = prep.plan_for(kAllTiles, a.slots, 2 * grid, [&]() {
+    std::vector<uint32_t> rows(km.krows);
+    for (uint32_t p = 0; p < km.krows; ++p) rows[p] = kAllTiles ? km.kcols : prep.h_row_cnt[p];
+    const UnitBuild ub = build_units(rows, a.slots, static_cast<int>(2 * grid));
+    LaunchPlan lp;
+    lp.units = static_cast<uint32_t>(ub.desc.size());
+    lp.split_rows = static_cast<uint32_t>(ub.split_info.size());
+    lp.split_chunks = ub.split_chunks;
+    lp.slots = a.slots;
+    BBM_CUDA(cudaMalloc(&lp.unit_desc, std::max<size_t>(1, ub.desc.size()) * sizeof(uint4)));
+    BBM_CUDA(cudaMemcpy(lp.unit_desc, ub.desc.data(), ub.desc.size() * sizeof(uint4),
+                        cudaMemcpyHostToDevice));
+    BBM_CUDA(cudaMalloc(&lp.split_info, std::max<size_t>(1, ub.split_info.size()) * sizeof(uint2)));
+    if (!ub.split_info.empty())
+      BBM_CUDA(cudaMemcpy(lp.split_info, ub.split_info.data(),
+                          ub.split_info.size() * sizeof(uint2), cudaMemcpyHostToDevice));
+    const size_t nctr = std::max<size_t>(1, a.slots * lp.split_rows);
+    BBM_CUDA(cudaMalloc(&lp.split_ctr, nctr * sizeof(uint32_t)));
+    BBM_CUDA(cudaMemset(lp.split_ctr, 0, nctr * sizeof(uint32_t)));
+    return lp;
+  });
+  float* ws = prep.workspace_for(static_cast<size_t>(a.slots) * plan.split_chunks * 128 * (D + 3));
+
   const CUtensorMap tq = make_tmap_bf16_3d(a.q, D, a.n, a.slots, 64, 128);
   const CUtensorMap tk = make_tmap_bf16_3d(a.k, D, a.n, a.slots, 64, 128);
   const CUtensorMap tv = make_tmap_bf16_3d(a.v, D, a.n, a.slots, 64, 128);
@@ -624,13 +793,19 @@ void launch_impl(const Prep& prep, const AttnArgs& a, cudaStream_t s, int num_sm
   p.slots = static_cast<uint32_t>(a.slots);
   p.krows = km.krows;
   p.kcols = km.kcols;
-  p.total_items = static_cast<uint32_t>(a.slots * km.krows);
+  p.units = plan.units;
+  p.total_items = static_cast<uint32_t>(a.slots * plan.units);
   p.sl2 = a.scale * 1.4426950408889634f;
   p.list = km.list;
-  p.row_cnt = km.row_cnt;
-  p.order = km.order;
   p.bitmaps = km.bitmaps;
   p.mask = reinterpret_cast<const uint4*>(km.mask);
+  p.unit_desc = plan.unit_desc;
+  p.split_info = plan.split_info;
+  p.split_rows = plan.split_rows;
+  p.split_chunks = plan.split_chunks;
+  p.ws = ws;
+  p.split_ctr = plan.split_ctr;
+  p.work_ctr = prep.work_ctr;
   p.out = static_cast<__nv_bfloat16*>(a.o);
   p.row_max = a.row_max;
   p.row_sum = a.row_sum;
@@ -642,9 +817,6 @@ void launch_impl(const Prep& prep, const AttnArgs& a, cudaStream_t s, int num_sm
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes<D>()));
     attr_set = true;
   }
-  // two item streams per CTA, at most one CTA per SM (the kernel owns the SM's whole TMEM)
-  const uint32_t grid =
-      std::min<uint32_t>((p.total_items + 1) / 2, static_cast<uint32_t>(num_sms));
   attn_fwd_kernel<D, MODE><<<grid, kThreads, smem_bytes<D>(), s>>>(tq, tk, tv, to, p);
   BBM_CUDA(cudaGetLastError());
 }
@@ -665,6 +837,7 @@ void launch_d(const Prep& prep, const AttnArgs& a, cudaStream_t s, int num_sms) 
 void launch_attn_fwd(const Prep& prep, const AttnArgs& a, cudaStream_t s, int num_sms) {
   require(a.slots >= 1, "need at least one batch/head slot");
   require(a.n == prep.n, "mask preprocessing does not match this problem");
+  require(a.slots < (1ull << 24), "too many slots for one launch");
   if (a.slots * prep.kmeta.krows == 0) return;
   if (a.d == 64) launch_d<64>(prep, a, s, num_sms);
   else if (a.d == 128) launch_d<128>(prep, a, s, num_sms);

@@ -3,8 +3,10 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <map>
 #include <stdexcept>
 #include <string>
+#include <tuple>
 #include <vector>
 
 namespace bbm {
@@ -67,12 +69,45 @@ struct SpecMeta {
   uint64_t blocks_total = 0, blocks_nonzero = 0, blocks_full = 0, ones = 0;
 };
 
+// Work decomposition of one attention launch shape (mode class x slots x streams): row units
+// (whole row tiles, or balanced chunks of long ones = split-KV), device-resident.
+struct LaunchPlan {
+  uint32_t units = 0, split_rows = 0, split_chunks = 0;
+  uint64_t slots = 0;
+  uint4* unit_desc = nullptr;    // [units] {row tile, j0, tiles, split | kNoSplit}
+  uint2* split_info = nullptr;   // [split_rows] {chunks, first workspace chunk}
+  uint32_t* split_ctr = nullptr; // [slots][split_rows] finished-chunk counters
+};
+
 struct Prep {
   int device = 0;
   uint64_t n = 0;
   SpecMeta spec;     // the caller's BlockSpec
   KernelMeta kmeta;  // the kernel's 128x128 view
   std::vector<uint32_t> h_row_cnt;  // host copy of kmeta.row_cnt (scheduling + tests)
+  uint32_t* work_ctr = nullptr;     // device [2]: dynamic item counter, finished CTAs
+  // launch plans and the split-KV workspace are built on first use (not thread-safe: one
+  // launch at a time per prep, like the reference's single-threaded callers)
+  mutable std::map<std::tuple<bool, uint64_t, uint32_t>, LaunchPlan> plans;
+  mutable float* workspace = nullptr;
+  mutable size_t workspace_floats = 0;
+
+  template <class F>
+  const LaunchPlan& plan_for(bool all_tiles, uint64_t slots, uint32_t streams, F make) const {
+    const auto key = std::make_tuple(all_tiles, slots, streams);
+    auto it = plans.find(key);
+    if (it == plans.end()) it = plans.emplace(key, make()).first;
+    return it->second;
+  }
+  float* workspace_for(size_t floats) const {
+    if (floats > workspace_floats) {
+      cudaFree(workspace);
+      workspace = nullptr;
+      check_cuda(cudaMalloc(&workspace, floats * sizeof(float)), "cudaMalloc(split workspace)");
+      workspace_floats = floats;
+    }
+    return workspace;
+  }
   ~Prep();
 };
 

@@ -183,6 +183,8 @@ Prep* new_prep(uint64_t n, int device) {
   pr->n = n;
   try {
     alloc_kernel_meta(pr->kmeta, n);
+    pr->work_ctr = dmalloc<uint32_t>(2);
+    BBM_CUDA(cudaMemset(pr->work_ctr, 0, 2 * sizeof(uint32_t)));
   } catch (...) {
     delete pr;
     throw;
@@ -197,6 +199,13 @@ Prep::~Prep() {
   cudaGetDevice(&prev);
   cudaSetDevice(device);
   free_kernel_meta(kmeta);
+  cudaFree(work_ctr);
+  cudaFree(workspace);
+  for (auto& kv : plans) {
+    cudaFree(kv.second.unit_desc);
+    cudaFree(kv.second.split_info);
+    cudaFree(kv.second.split_ctr);
+  }
   if (prev >= 0) cudaSetDevice(prev);
 }
 
