@@ -86,8 +86,10 @@ constexpr uint32_t kQueue = 4;        // item queue depth per stream
 //        MMA 10 S_j issued, 11 PV_j issued;
 //        softmax 20 s_full wait begin, 21 s_full wait end, 22 p_full arrive, 23 o_full wait end,
 //        24 epilogue done.
+template <bool kTrace>
 __device__ __forceinline__ void trace_ev(bool on, const FwdParams& p, uint32_t* counter,
                                          uint32_t code, uint32_t stream, uint32_t aux) {
+  if constexpr (!kTrace) return;
   if (!on) return;
   const uint32_t i = atomicAdd(counter, 1u);
   if (i >= kTraceCap) return;
@@ -158,21 +160,23 @@ __device__ __forceinline__ ItemDesc decode_item(const FwdParams& p, uint32_t t) 
   return d;
 }
 
-// Masked max of 32 raw scores of one row chunk (negated first when the scale is negative).
-template <bool kMasked, bool kNeg>
-__device__ __forceinline__ float chunk_max(const uint32_t (&r)[32], uint32_t mw) {
+// Replace the scores of invisible keys by a sentinel in place: -inf (or +inf when the scale is
+// negative, so that scale * sentinel = -inf). The max and exp passes then need no selects.
+__device__ __forceinline__ void apply_mask(uint32_t (&r)[32], uint32_t mw, uint32_t sentinel) {
+#pragma unroll
+  for (uint32_t i = 0; i < 32; ++i) r[i] = ((mw >> i) & 1u) ? r[i] : sentinel;
+}
+
+// Max of 32 (already masked) raw scores of one row chunk; of the negated scores when the scale
+// is negative (FMNMX takes negated operands for free).
+template <bool kNeg>
+__device__ __forceinline__ float chunk_max(const uint32_t (&r)[32]) {
   float m0 = -INFINITY, m1 = -INFINITY;
 #pragma unroll
   for (uint32_t i = 0; i < 32; i += 4) {
     float a = __uint_as_float(r[i]), b = __uint_as_float(r[i + 1]);
     float c = __uint_as_float(r[i + 2]), d = __uint_as_float(r[i + 3]);
     if constexpr (kNeg) { a = -a; b = -b; c = -c; d = -d; }
-    if constexpr (kMasked) {
-      a = ((mw >> i) & 1u) ? a : -INFINITY;
-      b = ((mw >> (i + 1)) & 1u) ? b : -INFINITY;
-      c = ((mw >> (i + 2)) & 1u) ? c : -INFINITY;
-      d = ((mw >> (i + 3)) & 1u) ? d : -INFINITY;
-    }
     m0 = fmax3(m0, a, b);
     m1 = fmax3(m1, c, d);
   }
@@ -214,7 +218,7 @@ __device__ __forceinline__ void stage_chunk32(uint8_t* rowp, uint32_t row, uint3
   }
 }
 
-template <int D, int MODE>
+template <int D, int MODE, bool kTrace>
 __global__ void __launch_bounds__(kThreads, 1)
     attn_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                     const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_o,
@@ -228,7 +232,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if ((smem_u32(smem) & 1023u) != 0) __trap();  // 128B-swizzle atoms need 1024-byte alignment
-  const bool tracing = p.trace != nullptr && blockIdx.x < p.trace_ctas;
+  const bool tracing = kTrace && blockIdx.x < p.trace_ctas;
 
   if (threadIdx.x == 0) {
     ctl->trace_count = 0;
@@ -280,7 +284,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (uint32_t b = 0; b < C::kBoxes; ++b)
           tma_load_3d(myring + r * C::kTileBytes + b * kBoxBytes, tm, full, b * 64, q * 128, slot,
                       pol_kv);
-        trace_ev(tracing, p, &ctl->trace_count, code, s, j);
+        trace_ev<kTrace>(tracing, p, &ctl->trace_count, code, s, j);
         if (++r == C::kRing) { r = 0; rph ^= 1; }
       };
       for (;;) {
@@ -299,7 +303,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (uint32_t b = 0; b < C::kBoxes; ++b)
           tma_load_3d(sq + s * C::kTileBytes + b * kBoxBytes, &tm_q, &ctl->q_full[s], b * 64,
                       d.rt * 128, d.slot, pol_q);
-        trace_ev(tracing, p, &ctl->trace_count, 1, s, d.t);
+        trace_ev<kTrace>(tracing, p, &ctl->trace_count, 1, s, d.t);
         for (uint32_t j = 0; j < d.nt; ++j) {
           const uint32_t nxt = (j + 1 < d.nt) ? entry_of<MODE>(p, d.rt, d.j0 + j + 1) : 0;
           const uint32_t q = cur & 0x7FFFFFFFu;
@@ -345,7 +349,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (++r == C::kRing) { r = 0; rph ^= 1; }
           if (j + 1 == d.nt) tc_commit(&ctl->q_empty[s]);
           tc_commit(&ctl->s_full[s]);
-          trace_ev(tracing, p, &ctl->trace_count, 10, s, j);
+          trace_ev<kTrace>(tracing, p, &ctl->trace_count, 10, s, j);
           // O += P_j V_j
           mbar_wait(&ctl->p_full[s], pph);
           pph ^= 1;
@@ -359,7 +363,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           tc_commit(&ctl->ring_empty[s][r]);
           if (++r == C::kRing) { r = 0; rph ^= 1; }
           if (j + 1 == d.nt) tc_commit(&ctl->o_full[s]);
-          trace_ev(tracing, p, &ctl->trace_count, 11, s, j);
+          trace_ev<kTrace>(tracing, p, &ctl->trace_count, 11, s, j);
         }
       }
     }
@@ -375,7 +379,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t last_q = p.kcols - 1;
     const uint32_t kv_valid_last = static_cast<uint32_t>(p.n - static_cast<uint64_t>(last_q) * 128);
     const bool neg = p.sl2 < 0.0f;
+    const bool zero_scale = p.sl2 == 0.0f;
     const float abs_sl2 = fabsf(p.sl2);
+    // masked scores: -inf, or +inf with a negative scale; with a zero scale the sentinel only
+    // has to drop out of the max (the exp pass selects explicitly)
+    const uint32_t sentinel = neg ? 0x7F800000u : 0xFF800000u;
     constexpr uint32_t kHalfO = D / 2;  // O columns per half
 
     struct Stream {
@@ -491,7 +499,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           mbar_wait(&ctl->o_full[s], x.o_phase);
           x.o_phase ^= 1;
           tc_fence_after();
-          if (tracer) trace_ev(tracing, p, &ctl->trace_count, 23, s, x.eit.t);
+          if (tracer) trace_ev<kTrace>(tracing, p, &ctl->trace_count, 23, s, x.eit.t);
           // total row sum of this unit = both halves' partial sums
           ctl->xchg[step & 1][half][row] = x.e_l;
           named_bar_sync(1, 256);
@@ -589,7 +597,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               write_stats(x.eit, mtrue, mrun, ltot);
             }
           }
-          if (tracer) trace_ev(tracing, p, &ctl->trace_count, 24, s, x.eit.t);
+          if (tracer) trace_ev<kTrace>(tracing, p, &ctl->trace_count, 24, s, x.eit.t);
         }
         if (!x.live) continue;
 
@@ -611,24 +619,22 @@ __global__ void __launch_bounds__(kThreads, 1)
           masked = true;  // bitmaps carry zeros beyond n, so ragged edges need nothing extra
         }
 
-        if (tracer) trace_ev(tracing, p, &ctl->trace_count, 20, s, j);
+        if (tracer) trace_ev<kTrace>(tracing, p, &ctl->trace_count, 20, s, j);
         mbar_wait(&ctl->s_full[s], x.s_phase);
         x.s_phase ^= 1;
         tc_fence_after();
-        if (tracer) trace_ev(tracing, p, &ctl->trace_count, 21, s, j);
+        if (tracer) trace_ev<kTrace>(tracing, p, &ctl->trace_count, 21, s, j);
 
         uint32_t a0[32], a1[32];
         tmem_ld32(ts + half * 64, a0);
         tmem_ld32(ts + half * 64 + 32, a1);
         tmem_ld_wait();
-        float pmax;
         if (masked) {
-          pmax = neg ? fmaxf(chunk_max<true, true>(a0, bits.x), chunk_max<true, true>(a1, bits.y))
-                     : fmaxf(chunk_max<true, false>(a0, bits.x), chunk_max<true, false>(a1, bits.y));
-        } else {
-          pmax = neg ? fmaxf(chunk_max<false, true>(a0, 0), chunk_max<false, true>(a1, 0))
-                     : fmaxf(chunk_max<false, false>(a0, 0), chunk_max<false, false>(a1, 0));
+          apply_mask(a0, bits.x, sentinel);
+          apply_mask(a1, bits.y, sentinel);
         }
+        const float pmax = neg ? fmaxf(chunk_max<true>(a0), chunk_max<true>(a1))
+                               : fmaxf(chunk_max<false>(a0), chunk_max<false>(a1));
         // exchange with the other half (double-buffered by parity); after this barrier every S
         // read of this tile has completed, so P may overwrite S columns [0, 64)
         ctl->xchg[step & 1][half][row] = pmax;
@@ -662,8 +668,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         uint32_t pk[16];
         uint64_t lacc = 0;
         const uint64_t sl2x2 = f2_pack(p.sl2, p.sl2), nm2 = f2_pack(-m_use, -m_use);
-        // this half's 64 columns -> 32 packed P columns at [32 * half, 32 * half + 32)
-        if (masked) {
+        // this half's 64 columns -> 32 packed P columns at [32 * half, 32 * half + 32); masked
+        // scores already hold the sentinel, except with a zero scale (inf * 0 = NaN), which
+        // keeps the select inside the exp pass
+        if (masked && zero_scale) {
           chunk_exp<true>(a0, bits.x, sl2x2, nm2, pk, lacc);
           tmem_st16(ts + half * 32, pk);
           chunk_exp<true>(a1, bits.y, sl2x2, nm2, pk, lacc);
@@ -678,7 +686,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         tmem_st_wait();
         tc_fence_before();
         mbar_arrive(&ctl->p_full[s]);
-        if (tracer) trace_ev(tracing, p, &ctl->trace_count, 22, s, j);
+        if (tracer) trace_ev<kTrace>(tracing, p, &ctl->trace_count, 22, s, j);
 
         if (++x.j == x.it.nt) {  // item done: epilogue on this stream's next turn
           x.pend = true;
@@ -758,9 +766,10 @@ void launch_impl(const Prep& prep, const AttnArgs& a, cudaStream_t s, int num_sm
   static_assert(smem_bytes<D>() <= 232448, "exceeds the 227 KB opt-in shared memory");
   const KernelMeta& km = prep.kmeta;
   constexpr bool kAllTiles = (MODE == kModeDense || MODE == kModeNaive);
+  // one CTA per SM; when work items are scarce, at most one CTA per item (a CTA's engine
+  // serializes its two streams' tiles, so spreading scarce items over more SMs wins)
   const uint32_t grid = std::min<uint32_t>(
-      static_cast<uint32_t>(std::max<uint64_t>(1, (a.slots * km.krows + 1) / 2)),
-      static_cast<uint32_t>(num_sms));
+      static_cast<uint32_t>(std::max<uint64_t>(1, a.slots * km.krows)), static_cast<uint32_t>(num_sms));
   const LaunchPlan& plan = prep.plan_for(kAllTiles, a.slots, 2 * grid, [&]() {
     std::vector<uint32_t> rows(km.krows);
     for (uint32_t p = 0; p < km.krows; ++p) rows[p] = kAllTiles ? km.kcols : prep.h_row_cnt[p];
@@ -813,11 +822,16 @@ void launch_impl(const Prep& prep, const AttnArgs& a, cudaStream_t s, int num_sm
   p.trace_ctas = g_trace.ctas;
   static bool attr_set = false;  // per (D, MODE) instantiation
   if (!attr_set) {
-    BBM_CUDA(cudaFuncSetAttribute(attn_fwd_kernel<D, MODE>,
+    BBM_CUDA(cudaFuncSetAttribute(attn_fwd_kernel<D, MODE, false>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes<D>()));
+    BBM_CUDA(cudaFuncSetAttribute(attn_fwd_kernel<D, MODE, true>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes<D>()));
     attr_set = true;
   }
-  attn_fwd_kernel<D, MODE><<<grid, kThreads, smem_bytes<D>(), s>>>(tq, tk, tv, to, p);
+  if (p.trace)  // event-tracing build of the same kernel (bbm_set_trace)
+    attn_fwd_kernel<D, MODE, true><<<grid, kThreads, smem_bytes<D>(), s>>>(tq, tk, tv, to, p);
+  else
+    attn_fwd_kernel<D, MODE, false><<<grid, kThreads, smem_bytes<D>(), s>>>(tq, tk, tv, to, p);
   BBM_CUDA(cudaGetLastError());
 }
 
