@@ -198,7 +198,11 @@ __device__ __forceinline__ void chunk_exp(const uint32_t (&r)[32], uint32_t mw, 
       x0 = ((mw >> i) & 1u) ? x0 : -INFINITY;
       x1 = ((mw >> (i + 1)) & 1u) ? x1 : -INFINITY;
     }
+#ifdef BBM_ABLATE_NO_MUFU
+    const float e0 = x0 * 0.5f + 1.0f, e1 = x1 * 0.5f + 1.0f;
+#else
     const float e0 = fast_exp2(x0), e1 = fast_exp2(x1);
+#endif
     lacc = fadd2(lacc, f2_pack(e0, e1));
     pk[i / 2] = pack_bf16x2(e0, e1);
   }
@@ -637,9 +641,13 @@ __global__ void __launch_bounds__(kThreads, 1)
                                : fmaxf(chunk_max<false>(a0), chunk_max<false>(a1));
         // exchange with the other half (double-buffered by parity); after this barrier every S
         // read of this tile has completed, so P may overwrite S columns [0, 64)
+#ifdef BBM_ABLATE_NO_XCHG
+        float tmax = pmax;
+#else
         ctl->xchg[step & 1][half][row] = pmax;
         named_bar_sync(1, 256);
         float tmax = fmaxf(pmax, ctl->xchg[step & 1][half ^ 1][row]);
+#endif
         ++step;
         tmax = tmax == -INFINITY ? -INFINITY : tmax * abs_sl2;  // log2 domain
         x.m_true = fmaxf(x.m_true, tmax);

@@ -1,0 +1,105 @@
+// mma_rate_probe.cu — achievable tcgen05.mma rate on this part, per mode (measurement tool).
+//
+// 148 CTAs (one per SM), one thread issues `iters` groups of 8 MMAs (K = 8 x 16 = 128) with
+// M=128, N in {128, 256}: SS (A and B from shared memory) or TS (A from TMEM); clock64 around
+// the loop after a commit/wait. Prints cycles per 128x128x16 MMA-equivalent (ideal: 64).
+#include <cstdio>
+#include <cstdlib>
+
+#include "../paper_2409_15097_b200/csrc/bbm_ptx.cuh"
+
+using namespace bbm::ptx;
+
+template <int MODE, int N, bool kTma>  // MODE 0 = SS, 1 = TS; kTma: concurrent bulk copies
+__global__ void __launch_bounds__(128, 1) rate_kernel(int iters, unsigned long long* out,
+                                                      const uint8_t* gsrc, volatile int* stop) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  __shared__ uint64_t bar, tbar;
+  __shared__ uint32_t tbase;
+  __shared__ volatile int done;
+  const int warp = threadIdx.x / 32;
+  if (threadIdx.x == 0) {
+    mbar_init(&bar, 1);
+    mbar_init(&tbar, 1);
+    done = 0;
+    fence_barrier_init();
+  }
+  if (warp == 0) {
+    tmem_alloc<512>(&tbase);
+    tmem_relinquish();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tbase;
+  if (threadIdx.x == 0) {
+    const uint32_t a = smem_u32(smem), b = a + 32768;
+    constexpr uint32_t idesc = make_idesc_bf16(128, N, false, false);
+    long long t0 = clock64();
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+      for (int kk = 0; kk < 8; ++kk) {
+        const uint32_t off = (kk / 4) * 16384 + (kk % 4) * 32;
+        if (MODE == 0)
+          umma_ss(tmem, make_sdesc_sw128(a + off, 16, 1024), make_sdesc_sw128(b + off, 16, 1024),
+                  idesc, kk > 0 || it > 0);
+        else
+          umma_ts(tmem, tmem + 256 + kk * 8, make_sdesc_sw128(b + off, 16, 1024), idesc,
+                  kk > 0 || it > 0);
+      }
+    }
+    tc_commit(&bar);
+    mbar_wait(&bar, 0);
+    long long t1 = clock64();
+    if (blockIdx.x == 0) out[0] = static_cast<unsigned long long>(t1 - t0);
+    done = 1;
+  }
+  if (kTma && threadIdx.x == 32) {
+    // 32 KB bulk copies global -> shared (region [128K, 160K)) back to back, ~1 in flight
+    uint32_t ph = 0;
+    const uint32_t dst = smem_u32(smem) + 131072;
+    uint64_t n = 0;
+    while (!done) {
+      mbar_arrive_expect_tx(&tbar, 32768);
+      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                   :: "r"(dst), "l"(gsrc + (n++ % 64) * 32768), "r"(32768), "r"(smem_u32(&tbar)) : "memory");
+      mbar_wait(&tbar, ph);
+      ph ^= 1;
+    }
+    if (blockIdx.x == 0) out[1] = n;
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) tmem_dealloc<512>(tmem);
+}
+
+template <int MODE, int N, bool kTma>
+void run(const char* name) {
+  unsigned long long* d;
+  cudaMalloc(&d, 16);
+  uint8_t* g;
+  cudaMalloc(&g, 64 * 32768);
+  const int smem = 2 * 65536 + 32768 + 1024;
+  cudaFuncSetAttribute(rate_kernel<MODE, N, kTma>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  const int iters = 2000;
+  rate_kernel<MODE, N, kTma><<<148, 128, smem>>>(iters, d, g, nullptr);
+  rate_kernel<MODE, N, kTma><<<148, 128, smem>>>(iters, d, g, nullptr);
+  cudaError_t e = cudaDeviceSynchronize();
+  unsigned long long res[2] = {0, 0};
+  cudaMemcpy(res, d, 16, cudaMemcpyDeviceToHost);
+  const double per = double(res[0]) / (iters * 8.0 * (N / 128.0));
+  std::printf("%-12s N=%3d tma=%d: %s  %.1f cycles per 128x128x16 (ideal 64); bulk copies %llu (%.1f B/cycle)\n",
+              name, N, int(kTma), e == cudaSuccess ? "ok" : cudaGetErrorString(e), per, res[1],
+              res[1] * 32768.0 / double(res[0]));
+  cudaFree(d);
+  cudaFree(g);
+}
+
+int main() {
+  run<0, 128, false>("SS");
+  run<1, 128, false>("TS");
+  run<0, 128, true>("SS+bulk");
+  run<1, 128, true>("TS+bulk");
+  run<0, 256, true>("SS+bulk");
+  return 0;
+}
