@@ -12,25 +12,26 @@
 // combines them. Items are claimed dynamically (one global atomic per item) in slot-major order,
 // longest units first inside a slot.
 //
-// Structure: one persistent CTA per SM (384 threads) running TWO independent item streams that
-// share the tensor core; every role blocks in hardware (mbarrier try_wait) on what it needs.
-//   warps 0, 1   producer of stream A / B: claims items, publishes them through the stream's
-//                shared-memory item queue, loads the Q tile and K_j, V_j into the stream's K/V
-//                ring (TMA, 128B-swizzled 64-column boxes).
-//   warps 2, 3   MMA issuer of stream A / B (one thread; tcgen05.commit tracks the issuing
-//                thread's ops, so the streams never wait on each other's MMAs):
-//                S = Q K^T (SS, both K-major) into TMEM, O += P V (TS: P read from TMEM,
-//                V MN-major). Warp 2 owns the TMEM allocation (512 columns: S_A, S_B at
-//                [0,256), O_A, O_B at [256,512)).
-//   warps 4-11   ONE softmax engine serving the streams in turn (A, B, A, ...): while it turns
-//                S_A into P_A the tensor core runs stream B's MMAs, and vice versa. Warps 4-7
-//                own S columns [0,64) and O columns [0,D/2), warps 8-11 the other halves; the
-//                halves exchange their partial row max through shared memory once per tile.
-//                The epilogue stages bf16 O in 128B-swizzled shared memory for TMA stores.
+// Structure: one persistent CTA per SM (384 threads), one stream of items (the tile sequence of
+// consecutive items is treated as one sequence k = 0, 1, 2, ...). tcgen05.mma issue is nearly
+// synchronous (the MMA queue holds ~6 instructions), so the score accumulator is DOUBLE-BUFFERED
+// in TMEM: S_{k+2} is computed while the softmax engine turns S_k into P_k, and the engine never
+// waits on the tensor core in steady state.
+//   warp 0       producer: claims items, publishes them through a shared-memory item queue,
+//                loads Q (double-buffered across items) and K_k, V_k into a K/V ring (TMA,
+//                128B-swizzled 64-column boxes).
+//   warp 1       MMA issuer (one thread): S_k = Q K_k^T (SS, both K-major) into TMEM buffer
+//                k % 2, O += P_k V_k (TS: P read from TMEM, V MN-major). Issue order
+//                S_0, S_1, PV_0, S_2, PV_1, S_3, ... (S_{k+2} reuses P_k's columns, after PV_k).
+//   warp 2       TMEM allocator (512 columns: S buffers at [0,128) and [128,256), O at 256).
+//   warps 4-11   softmax engine: warps 4-7 own S columns [0,64) and O columns [0,D/2), warps
+//                8-11 the other halves; the halves exchange their partial row max through shared
+//                memory once per tile. The epilogue stages bf16 O in 128B-swizzled shared memory
+//                for TMA stores.
 // Numerics: scores are scaled into the log2 domain; the running max is only raised when it grows
 // by more than 2^8 (stale-max trick; exact after the final O/l), P is rounded to bf16 for the
 // MMA and written over S in TMEM, l accumulates in fp32. Partial tiles read 8 B of mask bits per
-// row and half (coalesced, list-position tile-major, prefetched a turn ahead); full tiles read
+// row and half (coalesced, list-position tile-major, prefetched a tile ahead); full tiles read
 // none under dense_binblk.
 #include <cuda.h>
 #include <cuda_bf16.h>
@@ -79,11 +80,11 @@ struct FwdParams {
 
 constexpr uint32_t kThreads = 384;
 constexpr uint32_t kTraceCap = 8192;  // events per traced CTA
-constexpr uint32_t kQueue = 4;        // item queue depth per stream
+constexpr uint32_t kQueue = 4;        // item queue depth (>= 3 items open at the MMA issuer)
 
 // Trace event: [63:24] clock64 low 40 bits | [23:16] code | [15] stream | [14:0] aux.
-// Codes: producer 1 Q issued (aux = item), 2 K_j issued, 3 V_j issued;
-//        MMA 10 S_j issued, 11 PV_j issued;
+// Codes: producer 1 Q issued (aux = item), 2 K_k issued, 3 V_k issued;
+//        MMA 10 S_k issued, 11 PV_k issued;
 //        softmax 20 s_full wait begin, 21 s_full wait end, 22 p_full arrive, 23 o_full wait end,
 //        24 epilogue done.
 template <bool kTrace>
@@ -106,7 +107,7 @@ template <int D>
 struct Cfg {
   static constexpr uint32_t kBoxes = D / 64;
   static constexpr uint32_t kTileBytes = kBoxes * kBoxBytes;  // one 128 x D bf16 tile
-  static constexpr uint32_t kRing = (D == 64) ? 5 : 2;        // K/V ring slots per stream
+  static constexpr uint32_t kRing = (D == 64) ? 10 : 4;       // K/V ring slots
   static constexpr uint32_t kStageBytes = kBoxBytes;          // epilogue staging (two buffers)
   static constexpr uint32_t kTmemCols = 512;
   static constexpr uint32_t kOCol = 256;
@@ -120,10 +121,10 @@ struct ItemDesc {
 // smem, so the dynamic base is the 1024-byte aligned start of the CTA's window).
 template <uint32_t kRing>
 struct SmemCtl {
-  uint64_t q_full[2], q_empty[2], s_full[2], p_full[2], o_full[2];
-  uint64_t ring_full[2][kRing], ring_empty[2][kRing];
-  uint64_t item_full[2][kQueue], item_empty[2][kQueue];
-  ItemDesc items[2][kQueue];
+  uint64_t q_full[2], q_empty[2], s_full[2], p_full[2], o_full, pv_done;
+  uint64_t ring_full[kRing], ring_empty[kRing];
+  uint64_t item_full[kQueue], item_empty[kQueue];
+  ItemDesc items[kQueue];
   uint32_t tmem_base;
   uint32_t trace_count;
   uint32_t bcast;
@@ -132,7 +133,7 @@ struct SmemCtl {
 
 template <int D>
 constexpr uint32_t smem_bytes() {
-  return Cfg<D>::kTileBytes * (2 + 2 * Cfg<D>::kRing) + 2 * Cfg<D>::kStageBytes +
+  return Cfg<D>::kTileBytes * (2 + Cfg<D>::kRing) + 2 * Cfg<D>::kStageBytes +
          sizeof(SmemCtl<Cfg<D>::kRing>);
 }
 
@@ -198,7 +199,7 @@ __device__ __forceinline__ void chunk_exp(const uint32_t (&r)[32], uint32_t mw, 
       x0 = ((mw >> i) & 1u) ? x0 : -INFINITY;
       x1 = ((mw >> (i + 1)) & 1u) ? x1 : -INFINITY;
     }
-#ifdef BBM_ABLATE_NO_MUFU
+#ifdef BBM_ABLATE_NO_MUFU  // timing experiments only (tools/ablate.sh): wrong results
     const float e0 = x0 * 0.5f + 1.0f, e1 = x1 * 0.5f + 1.0f;
 #else
     const float e0 = fast_exp2(x0), e1 = fast_exp2(x1);
@@ -229,9 +230,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                     const FwdParams p) {
   using C = Cfg<D>;
   extern __shared__ __align__(1024) uint8_t smem[];
-  uint8_t* sq = smem;                                    // [2][tile]          Q of each stream
-  uint8_t* ring = sq + 2 * C::kTileBytes;                // [2][kRing][tile]   K/V ring per stream
-  uint8_t* stage = ring + 2 * C::kRing * C::kTileBytes;  // [2][128 x 64 bf16] epilogue staging
+  uint8_t* sq = smem;                              // [2][tile]          Q, double-buffered
+  uint8_t* ring = sq + 2 * C::kTileBytes;          // [kRing][tile]      K/V ring
+  uint8_t* stage = ring + C::kRing * C::kTileBytes;  // [2][128 x 64 bf16] epilogue staging
   auto* ctl = reinterpret_cast<SmemCtl<C::kRing>*>(stage + 2 * C::kStageBytes);
 
   const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -240,20 +241,21 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   if (threadIdx.x == 0) {
     ctl->trace_count = 0;
-    for (int s = 0; s < 2; ++s) {
-      mbar_init(&ctl->q_full[s], 1);
-      mbar_init(&ctl->q_empty[s], 1);
-      mbar_init(&ctl->s_full[s], 1);
-      mbar_init(&ctl->p_full[s], 256);
-      mbar_init(&ctl->o_full[s], 1);
-      for (uint32_t r = 0; r < C::kRing; ++r) {
-        mbar_init(&ctl->ring_full[s][r], 1);
-        mbar_init(&ctl->ring_empty[s][r], 1);
-      }
-      for (uint32_t r = 0; r < kQueue; ++r) {
-        mbar_init(&ctl->item_full[s][r], 1);
-        mbar_init(&ctl->item_empty[s][r], 2);  // MMA issuer + softmax engine
-      }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&ctl->q_full[b], 1);
+      mbar_init(&ctl->q_empty[b], 1);
+      mbar_init(&ctl->s_full[b], 1);
+      mbar_init(&ctl->p_full[b], 256);
+    }
+    mbar_init(&ctl->o_full, 1);
+    mbar_init(&ctl->pv_done, 1);
+    for (uint32_t r = 0; r < C::kRing; ++r) {
+      mbar_init(&ctl->ring_full[r], 1);
+      mbar_init(&ctl->ring_empty[r], 1);
+    }
+    for (uint32_t r = 0; r < kQueue; ++r) {
+      mbar_init(&ctl->item_full[r], 1);
+      mbar_init(&ctl->item_empty[r], 2);  // MMA issuer + softmax engine
     }
     fence_barrier_init();
   }
@@ -272,42 +274,42 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_after();
   const uint32_t tmem = ctl->tmem_base;
 
-  if (warp < 2) {
-    // ------------------------------------------------------------------ producer (stream = warp)
+  if (warp == 0) {
+    // ------------------------------------------------------------------ producer
     if (lane == 0) {
-      const int s = static_cast<int>(warp);
       const uint64_t pol_q = policy_evict_first();
       const uint64_t pol_kv = policy_evict_last();
-      uint32_t r = 0, rph = 1, qph = 1, qi = 0, qiph = 1;
-      uint8_t* myring = ring + s * C::kRing * C::kTileBytes;
+      uint32_t r = 0, rph = 1, qi = 0, qiph = 1, qb = 0;
+      uint32_t qph[2] = {1, 1};
       auto load_tile = [&](const CUtensorMap* tm, uint32_t q, uint32_t slot, uint32_t code,
                            uint32_t j) {
-        mbar_wait(&ctl->ring_empty[s][r], rph);
-        uint64_t* full = &ctl->ring_full[s][r];
+        mbar_wait(&ctl->ring_empty[r], rph);
+        uint64_t* full = &ctl->ring_full[r];
         mbar_arrive_expect_tx(full, C::kTileBytes);
         for (uint32_t b = 0; b < C::kBoxes; ++b)
-          tma_load_3d(myring + r * C::kTileBytes + b * kBoxBytes, tm, full, b * 64, q * 128, slot,
+          tma_load_3d(ring + r * C::kTileBytes + b * kBoxBytes, tm, full, b * 64, q * 128, slot,
                       pol_kv);
-        trace_ev<kTrace>(tracing, p, &ctl->trace_count, code, s, j);
+        trace_ev<kTrace>(tracing, p, &ctl->trace_count, code, 0, j);
         if (++r == C::kRing) { r = 0; rph ^= 1; }
       };
       for (;;) {
         const ItemDesc d = decode_item(p, atomicAdd(&p.work_ctr[0], 1u));
-        mbar_wait(&ctl->item_empty[s][qi], qiph);
-        ctl->items[s][qi] = d;
-        mbar_arrive(&ctl->item_full[s][qi]);  // release: the descriptor is visible to waiters
+        mbar_wait(&ctl->item_empty[qi], qiph);
+        ctl->items[qi] = d;
+        mbar_arrive(&ctl->item_full[qi]);  // release: the descriptor is visible to waiters
         if (++qi == kQueue) { qi = 0; qiph ^= 1; }
         if (d.t == kEnd) break;
         if (d.nt == 0) continue;
         // list entries one tile ahead so the TMA issue never waits on an L2 load
         uint32_t cur = entry_of<MODE>(p, d.rt, d.j0);
-        mbar_wait(&ctl->q_empty[s], qph);
-        qph ^= 1;
-        mbar_arrive_expect_tx(&ctl->q_full[s], C::kTileBytes);
+        mbar_wait(&ctl->q_empty[qb], qph[qb]);
+        qph[qb] ^= 1;
+        mbar_arrive_expect_tx(&ctl->q_full[qb], C::kTileBytes);
         for (uint32_t b = 0; b < C::kBoxes; ++b)
-          tma_load_3d(sq + s * C::kTileBytes + b * kBoxBytes, &tm_q, &ctl->q_full[s], b * 64,
+          tma_load_3d(sq + qb * C::kTileBytes + b * kBoxBytes, &tm_q, &ctl->q_full[qb], b * 64,
                       d.rt * 128, d.slot, pol_q);
-        trace_ev<kTrace>(tracing, p, &ctl->trace_count, 1, s, d.t);
+        trace_ev<kTrace>(tracing, p, &ctl->trace_count, 1, 0, d.t);
+        qb ^= 1;
         for (uint32_t j = 0; j < d.nt; ++j) {
           const uint32_t nxt = (j + 1 < d.nt) ? entry_of<MODE>(p, d.rt, d.j0 + j + 1) : 0;
           const uint32_t q = cur & 0x7FFFFFFFu;
@@ -317,58 +319,109 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
     }
-  } else if (warp < 4) {
-    // ------------------------------------------------------------------ MMA issuer (stream = warp-2)
-    // Op sequence S_0, PV_0, S_1, PV_1, ...: S_{j+1} overwrites the TMEM columns P_j lives in,
-    // so it is issued after PV_j (tcgen05.mma executes in issue order).
+  } else if (warp == 1) {
+    // ------------------------------------------------------------------ MMA issuer
+    // Two cursors over the tile sequence: the S cursor runs two tiles ahead of the PV cursor.
+    // Ring slots: K_k at 2k, V_k at 2k+1 (mod kRing) — consumed in order S_k ... PV_k.
     if (lane == 0) {
-      const int s = static_cast<int>(warp) - 2;
       constexpr uint32_t idesc_s = make_idesc_bf16(128, 128, false, false);
       constexpr uint32_t idesc_o = make_idesc_bf16(128, D, false, true);
-      const uint32_t qbase = smem_u32(sq) + s * C::kTileBytes;
-      const uint32_t rbase = smem_u32(ring) + s * C::kRing * C::kTileBytes;
-      const uint32_t tmem_s = tmem + s * 128, tmem_o = tmem + C::kOCol + s * 128;
-      uint32_t r = 0, rph = 0, qph = 0, pph = 0, qi = 0, qiph = 0;
-      for (;;) {
-        mbar_wait(&ctl->item_full[s][qi], qiph);
-        const ItemDesc d = ctl->items[s][qi];
-        mbar_arrive(&ctl->item_empty[s][qi]);
-        if (++qi == kQueue) { qi = 0; qiph ^= 1; }
-        if (d.t == kEnd) break;
-        if (d.nt == 0) continue;
-        mbar_wait(&ctl->q_full[s], qph);
-        qph ^= 1;
-        for (uint32_t j = 0; j < d.nt; ++j) {
-          // S_j = Q K_j^T
-          mbar_wait(&ctl->ring_full[s][r], rph);
-          tc_fence_after();
-          const uint32_t kbase = rbase + r * C::kTileBytes;
-#pragma unroll
-          for (uint32_t kk = 0; kk < D / 16; ++kk) {
-            const uint32_t off = (kk / 4) * kBoxBytes + (kk % 4) * 32;
-            umma_ss(tmem_s, make_sdesc_sw128(qbase + off, 16, 1024),
-                    make_sdesc_sw128(kbase + off, 16, 1024), idesc_s, kk > 0);
+      const uint32_t qaddr = smem_u32(sq), raddr = smem_u32(ring);
+      const uint32_t tmem_o = tmem + C::kOCol;
+      // S cursor
+      uint32_t sq_i = 0, s_j = 0, s_qb = 0, s_k = 0;
+      uint32_t s_qph[2] = {0, 0};
+      bool s_need_item = true, s_done = false;
+      ItemDesc s_it{};
+      uint32_t s_qi_ph = 0;  // item_full phase for the S cursor's queue index
+      // PV cursor
+      uint32_t pq_i = 0, p_j = 0, p_k = 0;
+      uint32_t p_ph[2] = {0, 0};
+      ItemDesc p_it{};
+      bool p_need_item = true;
+      uint32_t p_qi_ph = 0;
+
+      // advance the S cursor to the next tile; returns false when the sequence ended
+      auto s_next_tile = [&]() -> bool {
+        while (s_need_item) {
+          if (s_done) return false;
+          mbar_wait(&ctl->item_full[sq_i], s_qi_ph);
+          s_it = ctl->items[sq_i];
+          if (++sq_i == kQueue) { sq_i = 0; s_qi_ph ^= 1; }
+          if (s_it.t == kEnd) {
+            s_done = true;
+            return false;
           }
-          tc_commit(&ctl->ring_empty[s][r]);
-          if (++r == C::kRing) { r = 0; rph ^= 1; }
-          if (j + 1 == d.nt) tc_commit(&ctl->q_empty[s]);
-          tc_commit(&ctl->s_full[s]);
-          trace_ev<kTrace>(tracing, p, &ctl->trace_count, 10, s, j);
-          // O += P_j V_j
-          mbar_wait(&ctl->p_full[s], pph);
-          pph ^= 1;
-          mbar_wait(&ctl->ring_full[s][r], rph);
-          tc_fence_after();
-          const uint32_t vbase = rbase + r * C::kTileBytes;
-#pragma unroll
-          for (uint32_t kk = 0; kk < 128 / 16; ++kk)
-            umma_ts(tmem_o, tmem_s + kk * 8, make_sdesc_sw128(vbase + kk * 2048, kBoxBytes, 1024),
-                    idesc_o, (j > 0 || kk > 0) ? 1u : 0u);
-          tc_commit(&ctl->ring_empty[s][r]);
-          if (++r == C::kRing) { r = 0; rph ^= 1; }
-          if (j + 1 == d.nt) tc_commit(&ctl->o_full[s]);
-          trace_ev<kTrace>(tracing, p, &ctl->trace_count, 11, s, j);
+          if (s_it.nt == 0) continue;
+          s_need_item = false;
+          s_j = 0;
         }
+        return true;
+      };
+      auto issue_s = [&]() {
+        const uint32_t buf = s_k & 1;
+        if (s_j == 0) {
+          mbar_wait(&ctl->q_full[s_qb], s_qph[s_qb]);
+          s_qph[s_qb] ^= 1;
+        }
+        const uint32_t slot = (2 * s_k) % C::kRing;
+        mbar_wait(&ctl->ring_full[slot], ((2 * s_k) / C::kRing) & 1);
+        tc_fence_after();
+        const uint32_t qbase = qaddr + s_qb * C::kTileBytes, kbase = raddr + slot * C::kTileBytes;
+#pragma unroll
+        for (uint32_t kk = 0; kk < D / 16; ++kk) {
+          const uint32_t off = (kk / 4) * kBoxBytes + (kk % 4) * 32;
+          umma_ss(tmem + buf * 128, make_sdesc_sw128(qbase + off, 16, 1024),
+                  make_sdesc_sw128(kbase + off, 16, 1024), idesc_s, kk > 0);
+        }
+        tc_commit(&ctl->ring_empty[slot]);
+        tc_commit(&ctl->s_full[buf]);
+        trace_ev<kTrace>(tracing, p, &ctl->trace_count, 10, buf, s_j);
+        if (++s_j == s_it.nt) {
+          tc_commit(&ctl->q_empty[s_qb]);
+          s_qb ^= 1;
+          s_need_item = true;
+        }
+        ++s_k;
+      };
+      // S lookahead of two tiles
+      for (int w = 0; w < 2; ++w)
+        if (s_next_tile()) issue_s();
+      for (;;) {
+        // PV cursor: item of tile p_k
+        while (p_need_item) {
+          mbar_wait(&ctl->item_full[pq_i], p_qi_ph);
+          p_it = ctl->items[pq_i];
+          mbar_arrive(&ctl->item_empty[pq_i]);  // released by the PV cursor (the last user)
+          if (++pq_i == kQueue) { pq_i = 0; p_qi_ph ^= 1; }
+          if (p_it.t == kEnd) break;
+          if (p_it.nt == 0) continue;
+          p_need_item = false;
+          p_j = 0;
+        }
+        if (p_need_item) break;  // end of the sequence
+        const uint32_t buf = p_k & 1;
+        mbar_wait(&ctl->p_full[buf], p_ph[buf]);
+        p_ph[buf] ^= 1;
+        const uint32_t slot = (2 * p_k + 1) % C::kRing;
+        mbar_wait(&ctl->ring_full[slot], ((2 * p_k + 1) / C::kRing) & 1);
+        tc_fence_after();
+        const uint32_t vbase = raddr + slot * C::kTileBytes;
+#pragma unroll
+        for (uint32_t kk = 0; kk < 128 / 16; ++kk)
+          umma_ts(tmem_o, tmem + buf * 128 + kk * 8,
+                  make_sdesc_sw128(vbase + kk * 2048, kBoxBytes, 1024), idesc_o,
+                  (p_j > 0 || kk > 0) ? 1u : 0u);
+        tc_commit(&ctl->ring_empty[slot]);
+        tc_commit(&ctl->pv_done);
+        trace_ev<kTrace>(tracing, p, &ctl->trace_count, 11, buf, p_j);
+        if (++p_j == p_it.nt) {
+          tc_commit(&ctl->o_full);
+          p_need_item = true;
+        }
+        ++p_k;
+        // S_{k+2} goes into the buffer PV_k just read (in issue order after PV_k)
+        if (s_next_tile()) issue_s();
       }
     }
   } else if (warp >= 4) {
@@ -379,31 +432,24 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t lane_off = (quad * 32) << 16;
     const bool leader = (warp == 4 && lane == 0);
     const bool tracer = (quad == 0 && lane == 0 && half == 0);
-    const bool ragged = (p.n % 128) != 0;
-    const uint32_t last_q = p.kcols - 1;
-    const uint32_t kv_valid_last = static_cast<uint32_t>(p.n - static_cast<uint64_t>(last_q) * 128);
     const bool neg = p.sl2 < 0.0f;
     const bool zero_scale = p.sl2 == 0.0f;
     const float abs_sl2 = fabsf(p.sl2);
+    const bool ragged = (p.n % 128) != 0;
+    const uint32_t last_q = p.kcols - 1;
+    const uint32_t kv_valid_last = static_cast<uint32_t>(p.n - static_cast<uint64_t>(last_q) * 128);
     // masked scores: -inf, or +inf with a negative scale; with a zero scale the sentinel only
     // has to drop out of the max (the exp pass selects explicitly)
     const uint32_t sentinel = neg ? 0x7F800000u : 0xFF800000u;
     constexpr uint32_t kHalfO = D / 2;  // O columns per half
-
-    struct Stream {
-      uint32_t j, s_phase, o_phase, qi, qiph;
-      ItemDesc it;
-      float m_run, m_true, l;
-      bool live;   // an item with tiles is in progress
-      bool ended;  // the producer published kEnd
-      bool pend;   // finished item waiting for its epilogue
-      ItemDesc eit;  // item of the pending epilogue
-      float e_m_run, e_m_true, e_l;
-      uint2 nbits;      // this half's mask bits of tile j, loaded a turn ahead
-      uint32_t nentry;  // list entry of tile j (dense_binblk: the full flag), a turn ahead
-    } st[2];
+    const uint32_t to = tmem + C::kOCol + lane_off;
 
     uint32_t step = 0;  // parity selects the exchange buffer
+    uint32_t k = 0;     // global tile index (S buffer k % 2)
+    uint2 nbits = make_uint2(0xFFFFFFFFu, 0xFFFFFFFFu);  // mask bits of the next tile
+    uint32_t nentry = 0;                                // its list entry (dense_binblk)
+    bool have_next_bits = false;                        // prefetched for the next item
+    uint32_t s_ph[2] = {0, 0}, o_ph = 0, qi = 0, qiph = 0;
 
     auto write_stats = [&](const ItemDesc& it, float m_true2, float m_run2, float l_tot) {
       const uint64_t grow = static_cast<uint64_t>(it.rt) * 128 + row;
@@ -432,202 +478,74 @@ __global__ void __launch_bounds__(kThreads, 1)
         bulk_commit_group();
       }
     };
-    auto stage_wait_free = [&]() {
-      if (leader) bulk_wait_group_read<0>();  // staging buffers free again
-      named_bar_sync(1, 256);
-    };
     // D=128: half h stages columns [64h, 64h+64) in buffer h; D=64: both halves share buffer 0,
     // 32 columns (4 chunks) each
     uint8_t* stg_row = stage + (D == 128 ? half * C::kStageBytes : 0) + row * 128;
 
-    // loads for tile j of the current item, issued one engine turn before they are needed; the
-    // bitmap address depends only on (row tile, list position), never on a loaded value
-    auto prefetch = [&](Stream& x) {
-      if (!x.live) return;
-      const uint32_t jj = x.it.j0 + x.j;
-      const uint64_t grow = static_cast<uint64_t>(x.it.rt) * 128 + row;
+    // mask bits (and, for dense_binblk, the list entry) of tile jj of item `it`; the bitmap
+    // address depends only on (row tile, list position), never on a loaded value
+    auto load_bits = [&](const ItemDesc& it, uint32_t jj, uint2& bits, uint32_t& entry) {
+      const uint64_t grow = static_cast<uint64_t>(it.rt) * 128 + row;
       if constexpr (MODE == kModeNaive)
-        x.nbits = __ldg(reinterpret_cast<const uint2*>(p.mask + grow * p.kcols + jj) + half);
+        bits = __ldg(reinterpret_cast<const uint2*>(p.mask + grow * p.kcols + jj) + half);
       else if constexpr (MODE != kModeDense)
-        x.nbits = __ldg(reinterpret_cast<const uint2*>(
-                            p.bitmaps + (static_cast<uint64_t>(x.it.rt) * p.kcols + jj) * 128 + row) +
-                        half);
-      if constexpr (MODE == kModeDenseBinblk) x.nentry = entry_of<MODE>(p, x.it.rt, jj);
+        bits = __ldg(reinterpret_cast<const uint2*>(
+                         p.bitmaps + (static_cast<uint64_t>(it.rt) * p.kcols + jj) * 128 + row) +
+                     half);
+      if constexpr (MODE == kModeDenseBinblk) entry = entry_of<MODE>(p, it.rt, jj);
     };
-    // pull this stream's next item with tiles from its queue (writing zero items on the way)
-    auto next_item = [&](Stream& x, int s) {
-      x.live = false;
-      while (!x.ended) {
-        mbar_wait(&ctl->item_full[s][x.qi], x.qiph);
-        const ItemDesc d = ctl->items[s][x.qi];
-        named_bar_sync(1, 256);  // every engine thread has read the descriptor
-        if (leader) mbar_arrive(&ctl->item_empty[s][x.qi]);
-        if (++x.qi == kQueue) { x.qi = 0; x.qiph ^= 1; }
-        if (d.t == kEnd) {
-          x.ended = true;
-          break;
-        }
-        if (d.nt == 0) {
-          zero_item(d);
-          continue;
-        }
-        x.it = d;
-        x.j = 0;
-        x.m_run = -INFINITY;
-        x.m_true = -INFINITY;
-        x.l = 0.0f;
-        x.live = true;
-        break;
+
+    for (;;) {
+      // ---------------- next item (items without tiles are written as zeros right away)
+      mbar_wait(&ctl->item_full[qi], qiph);
+      const ItemDesc it = ctl->items[qi];
+      named_bar_sync(1, 256);  // every engine thread has read the descriptor
+      if (leader) mbar_arrive(&ctl->item_empty[qi]);
+      if (++qi == kQueue) { qi = 0; qiph ^= 1; }
+      if (it.t == kEnd) break;
+      if (it.nt == 0) {
+        zero_item(it);
+        continue;
       }
-      prefetch(x);
-    };
-    for (int s = 0; s < 2; ++s) {
-      st[s].s_phase = st[s].o_phase = 0;
-      st[s].qi = 0;
-      st[s].qiph = 0;
-      st[s].pend = false;
-      st[s].ended = false;
-      next_item(st[s], s);
-    }
+      float m_run = -INFINITY, m_true = -INFINITY, l = 0.0f;
+      if (!have_next_bits) load_bits(it, it.j0, nbits, nentry);  // else prefetched last item
+      have_next_bits = false;
 
-    while (st[0].live || st[0].pend || st[1].live || st[1].pend) {
-#pragma unroll
-      for (int s = 0; s < 2; ++s) {
-        Stream& x = st[s];
-        const uint32_t ts = tmem + s * 128 + lane_off;
-        const uint32_t to = tmem + C::kOCol + s * 128 + lane_off;
-        // ---------------- deferred epilogue of this stream's previous item (its last PV ran
-        // while the engine served the other stream)
-        if (x.pend) {
-          x.pend = false;
-          mbar_wait(&ctl->o_full[s], x.o_phase);
-          x.o_phase ^= 1;
-          tc_fence_after();
-          if (tracer) trace_ev<kTrace>(tracing, p, &ctl->trace_count, 23, s, x.eit.t);
-          // total row sum of this unit = both halves' partial sums
-          ctl->xchg[step & 1][half][row] = x.e_l;
-          named_bar_sync(1, 256);
-          const float l_unit = x.e_l + ctl->xchg[step & 1][half ^ 1][row];
-          ++step;
-          if (x.eit.split == kNoSplit) {
-            const float inv = l_unit > 0.0f ? 1.0f / l_unit : 0.0f;
-            stage_wait_free();
-#pragma unroll
-            for (uint32_t c32 = 0; c32 < kHalfO / 32; ++c32) {
-              uint32_t o[32];
-              tmem_ld32(to + half * kHalfO + c32 * 32, o);
-              tmem_ld_wait();
-              stage_chunk32(stg_row, row, D == 128 ? c32 * 4 : half * 4,
-                            reinterpret_cast<const float*>(o), inv);
-            }
-            // O TMEM of this stream may be overwritten from here on (its next first PV waits
-            // for this engine's next p_full arrival on this stream)
-            tc_fence_before();
-            store_staged(x.eit);
-            write_stats(x.eit, x.e_m_true, x.e_m_run, l_unit);
-          } else {
-            // ---- split-KV chunk: publish the unnormalized partial, the last chunk combines
-            const uint32_t srow = x.eit.split >> 8, chunk = x.eit.split & 0xFF;
-            const uint2 si = p.split_info[srow];  // {chunks, first workspace chunk}
-            const uint64_t blk = static_cast<uint64_t>(128) * (D + 3);
-            float* wsb =
-                p.ws + (static_cast<uint64_t>(x.eit.slot) * p.split_chunks + si.y + chunk) * blk;
-#pragma unroll
-            for (uint32_t c32 = 0; c32 < kHalfO / 32; ++c32) {
-              uint32_t o[32];
-              tmem_ld32(to + half * kHalfO + c32 * 32, o);
-              tmem_ld_wait();
-              uint4* dst = reinterpret_cast<uint4*>(wsb + row * D + half * kHalfO + c32 * 32);
-#pragma unroll
-              for (uint32_t v = 0; v < 8; ++v)
-                dst[v] = make_uint4(o[v * 4], o[v * 4 + 1], o[v * 4 + 2], o[v * 4 + 3]);
-            }
-            tc_fence_before();
-            if (half == 0) {
-              wsb[128 * D + row] = x.e_m_run;
-              wsb[128 * D + 128 + row] = x.e_m_true;
-              wsb[128 * D + 256 + row] = l_unit;
-            }
-            __threadfence();
-            named_bar_sync(1, 256);
-            uint32_t* ctr = p.split_ctr + static_cast<uint64_t>(x.eit.slot) * p.split_rows + srow;
-            if (leader) ctl->bcast = atomicAdd(ctr, 1u);
-            named_bar_sync(1, 256);
-            const uint32_t done_before = ctl->bcast;
-            if (done_before + 1 == si.x) {
-              // last chunk: combine every chunk's partial for this row tile
-              __threadfence();
-              const float* base =
-                  p.ws + (static_cast<uint64_t>(x.eit.slot) * p.split_chunks + si.y) * blk;
-              float mrun = -INFINITY, mtrue = -INFINITY;
-              for (uint32_t c = 0; c < si.x; ++c) {
-                const float* b = base + c * blk + 128 * D;
-                if (__ldcg(b + 256 + row) > 0.0f) mrun = fmaxf(mrun, __ldcg(b + row));
-                mtrue = fmaxf(mtrue, __ldcg(b + 128 + row));
-              }
-              float ltot = 0.0f;
-              for (uint32_t c = 0; c < si.x; ++c) {
-                const float* b = base + c * blk + 128 * D;
-                const float lc = __ldcg(b + 256 + row);
-                if (lc > 0.0f) ltot += lc * exp2f(__ldcg(b + row) - mrun);
-              }
-              const float inv = ltot > 0.0f ? 1.0f / ltot : 0.0f;
-              stage_wait_free();
-              if (leader) *ctr = 0;  // every engine thread has read the count: reset for reuse
-#pragma unroll 1
-              for (uint32_t c32 = 0; c32 < kHalfO / 32; ++c32) {
-                float acc[32];
-#pragma unroll
-                for (uint32_t i = 0; i < 32; ++i) acc[i] = 0.0f;
-                for (uint32_t c = 0; c < si.x; ++c) {
-                  const float* b = base + c * blk;
-                  const float lc = __ldcg(b + 128 * D + 256 + row);
-                  if (!(lc > 0.0f)) continue;
-                  const float w = exp2f(__ldcg(b + 128 * D + row) - mrun);
-                  const float4* src =
-                      reinterpret_cast<const float4*>(b + row * D + half * kHalfO + c32 * 32);
-#pragma unroll
-                  for (uint32_t v = 0; v < 8; ++v) {
-                    const float4 f = __ldcg(src + v);
-                    acc[v * 4 + 0] += w * f.x;
-                    acc[v * 4 + 1] += w * f.y;
-                    acc[v * 4 + 2] += w * f.z;
-                    acc[v * 4 + 3] += w * f.w;
-                  }
-                }
-                stage_chunk32(stg_row, row, D == 128 ? c32 * 4 : half * 4, acc, inv);
-              }
-              store_staged(x.eit);
-              write_stats(x.eit, mtrue, mrun, ltot);
-            }
-          }
-          if (tracer) trace_ev<kTrace>(tracing, p, &ctl->trace_count, 24, s, x.eit.t);
-        }
-        if (!x.live) continue;
-
-        // ---------------- one tile of this stream
-        const uint32_t j = x.j;
+      for (uint32_t j = 0; j < it.nt; ++j, ++k) {
+        const uint32_t buf = k & 1;
+        const uint32_t ts = tmem + buf * 128 + lane_off;
         bool masked;
-        uint2 bits = x.nbits;
+        uint2 bits = nbits;
         if constexpr (MODE == kModeDense) {
           // only the ragged right edge needs a column bound (no bitmap in this mode)
-          masked = ragged && x.it.j0 + j == last_q;
+          masked = ragged && it.j0 + j == last_q;
           if (masked) {
             const int v = static_cast<int>(kv_valid_last) - static_cast<int>(half * 64);
             bits.x = v >= 32 ? 0xFFFFFFFFu : (v <= 0 ? 0u : ((1u << v) - 1u));
             bits.y = v >= 64 ? 0xFFFFFFFFu : (v <= 32 ? 0u : ((1u << (v - 32)) - 1u));
           }
         } else if constexpr (MODE == kModeDenseBinblk) {
-          masked = (x.nentry & 0x80000000u) == 0;  // full tiles skip the mask bits
+          masked = (nentry & 0x80000000u) == 0;  // full tiles skip the mask bits
         } else {
           masked = true;  // bitmaps carry zeros beyond n, so ragged edges need nothing extra
         }
+        if (j + 1 < it.nt) {
+          load_bits(it, it.j0 + j + 1, nbits, nentry);  // a tile ahead
+        } else if (mbar_test(&ctl->item_full[qi], qiph)) {
+          // last tile: if the next item is already published, prefetch its first tile's bits
+          // (the descriptor is read again, and released, at the top of the item loop)
+          const ItemDesc nx = ctl->items[qi];
+          if (nx.t != kEnd) {
+            load_bits(nx, nx.j0, nbits, nentry);
+            have_next_bits = true;
+          }
+        }
 
-        if (tracer) trace_ev<kTrace>(tracing, p, &ctl->trace_count, 20, s, j);
-        mbar_wait(&ctl->s_full[s], x.s_phase);
-        x.s_phase ^= 1;
+        if (tracer) trace_ev<kTrace>(tracing, p, &ctl->trace_count, 20, buf, j);
+        mbar_wait(&ctl->s_full[buf], s_ph[buf]);
+        s_ph[buf] ^= 1;
         tc_fence_after();
-        if (tracer) trace_ev<kTrace>(tracing, p, &ctl->trace_count, 21, s, j);
+        if (tracer) trace_ev<kTrace>(tracing, p, &ctl->trace_count, 21, buf, j);
 
         uint32_t a0[32], a1[32];
         tmem_ld32(ts + half * 64, a0);
@@ -641,7 +559,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                                : fmaxf(chunk_max<false>(a0), chunk_max<false>(a1));
         // exchange with the other half (double-buffered by parity); after this barrier every S
         // read of this tile has completed, so P may overwrite S columns [0, 64)
-#ifdef BBM_ABLATE_NO_XCHG
+#ifdef BBM_ABLATE_NO_XCHG  // timing experiments only: wrong results
         float tmax = pmax;
 #else
         ctl->xchg[step & 1][half][row] = pmax;
@@ -650,16 +568,18 @@ __global__ void __launch_bounds__(kThreads, 1)
 #endif
         ++step;
         tmax = tmax == -INFINITY ? -INFINITY : tmax * abs_sl2;  // log2 domain
-        x.m_true = fmaxf(x.m_true, tmax);
-        const bool need =
-            tmax > x.m_run + kRescaleThreshold || (x.m_run == -INFINITY && tmax > -INFINITY);
-        const bool rescale_o = need && j > 0 && x.m_run > -INFINITY;
+        m_true = fmaxf(m_true, tmax);
+        const bool need = tmax > m_run + kRescaleThreshold || (m_run == -INFINITY && tmax > -INFINITY);
+        const bool rescale_o = need && j > 0 && m_run > -INFINITY;
         float factor = 1.0f;
         if (need) {
-          if (x.m_run > -INFINITY) factor = fast_exp2(x.m_run - tmax);
-          x.m_run = tmax;
+          if (m_run > -INFINITY) factor = fast_exp2(m_run - tmax);
+          m_run = tmax;
         }
         if (__any_sync(0xffffffffu, rescale_o)) {
+          // O must be quiescent: PV_{k-1} (the last one issued) has to complete first
+          mbar_wait(&ctl->pv_done, (k - 1) & 1);
+          tc_fence_after();
           const float f = rescale_o ? factor : 1.0f;
 #pragma unroll 1
           for (uint32_t c = 0; c < kHalfO / 32; ++c) {
@@ -671,8 +591,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             tmem_st32(to + half * kHalfO + c * 32, o);
           }
         }
-        x.l *= factor;
-        const float m_use = x.m_run == -INFINITY ? 0.0f : x.m_run;
+        l *= factor;
+        const float m_use = m_run == -INFINITY ? 0.0f : m_run;
         uint32_t pk[16];
         uint64_t lacc = 0;
         const uint64_t sl2x2 = f2_pack(p.sl2, p.sl2), nm2 = f2_pack(-m_use, -m_use);
@@ -690,23 +610,112 @@ __global__ void __launch_bounds__(kThreads, 1)
           chunk_exp<false>(a1, 0, sl2x2, nm2, pk, lacc);
           tmem_st16(ts + half * 32 + 16, pk);
         }
-        x.l += f2_lo(lacc) + f2_hi(lacc);
+        l += f2_lo(lacc) + f2_hi(lacc);
         tmem_st_wait();
         tc_fence_before();
-        mbar_arrive(&ctl->p_full[s]);
-        if (tracer) trace_ev<kTrace>(tracing, p, &ctl->trace_count, 22, s, j);
+        mbar_arrive(&ctl->p_full[buf]);
+        if (tracer) trace_ev<kTrace>(tracing, p, &ctl->trace_count, 22, buf, j);
+      }
 
-        if (++x.j == x.it.nt) {  // item done: epilogue on this stream's next turn
-          x.pend = true;
-          x.eit = x.it;
-          x.e_m_run = x.m_run;
-          x.e_m_true = x.m_true;
-          x.e_l = x.l;
-          next_item(x, s);
-        } else {
-          prefetch(x);
+      // ---------------- epilogue: the item's last PV completes while the row sums are combined
+      ctl->xchg[step & 1][half][row] = l;
+      if (leader) bulk_wait_group_read<0>();  // staging buffers free again
+      mbar_wait(&ctl->o_full, o_ph);
+      o_ph ^= 1;
+      tc_fence_after();
+      named_bar_sync(1, 256);
+      const float l_unit = l + ctl->xchg[step & 1][half ^ 1][row];
+      ++step;
+      if (tracer) trace_ev<kTrace>(tracing, p, &ctl->trace_count, 23, 0, it.t);
+      if (it.split == kNoSplit) {
+        const float inv = l_unit > 0.0f ? 1.0f / l_unit : 0.0f;
+#pragma unroll
+        for (uint32_t c32 = 0; c32 < kHalfO / 32; ++c32) {
+          uint32_t o[32];
+          tmem_ld32(to + half * kHalfO + c32 * 32, o);
+          tmem_ld_wait();
+          stage_chunk32(stg_row, row, D == 128 ? c32 * 4 : half * 4,
+                        reinterpret_cast<const float*>(o), inv);
+        }
+        // O may be overwritten from here on: the next item's first PV waits for this engine's
+        // next p_full arrival, which comes after these loads completed
+        tc_fence_before();
+        store_staged(it);
+        write_stats(it, m_true, m_run, l_unit);
+      } else {
+        // ---- split-KV chunk: publish the unnormalized partial, the last chunk combines
+        const uint32_t srow = it.split >> 8, chunk = it.split & 0xFF;
+        const uint2 si = p.split_info[srow];  // {chunks, first workspace chunk}
+        const uint64_t blk = static_cast<uint64_t>(128) * (D + 3);
+        float* wsb = p.ws + (static_cast<uint64_t>(it.slot) * p.split_chunks + si.y + chunk) * blk;
+#pragma unroll
+        for (uint32_t c32 = 0; c32 < kHalfO / 32; ++c32) {
+          uint32_t o[32];
+          tmem_ld32(to + half * kHalfO + c32 * 32, o);
+          tmem_ld_wait();
+          uint4* dst = reinterpret_cast<uint4*>(wsb + row * D + half * kHalfO + c32 * 32);
+#pragma unroll
+          for (uint32_t v = 0; v < 8; ++v)
+            dst[v] = make_uint4(o[v * 4], o[v * 4 + 1], o[v * 4 + 2], o[v * 4 + 3]);
+        }
+        tc_fence_before();
+        if (half == 0) {
+          wsb[128 * D + row] = m_run;
+          wsb[128 * D + 128 + row] = m_true;
+          wsb[128 * D + 256 + row] = l_unit;
+        }
+        __threadfence();
+        named_bar_sync(1, 256);
+        uint32_t* ctr = p.split_ctr + static_cast<uint64_t>(it.slot) * p.split_rows + srow;
+        if (leader) ctl->bcast = atomicAdd(ctr, 1u);
+        named_bar_sync(1, 256);
+        const uint32_t done_before = ctl->bcast;
+        if (done_before + 1 == si.x) {
+          // last chunk: combine every chunk's partial for this row tile
+          __threadfence();
+          const float* base = p.ws + (static_cast<uint64_t>(it.slot) * p.split_chunks + si.y) * blk;
+          float mrun = -INFINITY, mtrue = -INFINITY;
+          for (uint32_t c = 0; c < si.x; ++c) {
+            const float* b = base + c * blk + 128 * D;
+            if (__ldcg(b + 256 + row) > 0.0f) mrun = fmaxf(mrun, __ldcg(b + row));
+            mtrue = fmaxf(mtrue, __ldcg(b + 128 + row));
+          }
+          float ltot = 0.0f;
+          for (uint32_t c = 0; c < si.x; ++c) {
+            const float* b = base + c * blk + 128 * D;
+            const float lc = __ldcg(b + 256 + row);
+            if (lc > 0.0f) ltot += lc * exp2f(__ldcg(b + row) - mrun);
+          }
+          const float inv = ltot > 0.0f ? 1.0f / ltot : 0.0f;
+          named_bar_sync(1, 256);  // every engine thread has read the count
+          if (leader) *ctr = 0;    // ready for the next launch
+#pragma unroll 1
+          for (uint32_t c32 = 0; c32 < kHalfO / 32; ++c32) {
+            float acc[32];
+#pragma unroll
+            for (uint32_t i = 0; i < 32; ++i) acc[i] = 0.0f;
+            for (uint32_t c = 0; c < si.x; ++c) {
+              const float* b = base + c * blk;
+              const float lc = __ldcg(b + 128 * D + 256 + row);
+              if (!(lc > 0.0f)) continue;
+              const float w = exp2f(__ldcg(b + 128 * D + row) - mrun);
+              const float4* src = reinterpret_cast<const float4*>(b + row * D + half * kHalfO + c32 * 32);
+#pragma unroll
+              for (uint32_t v = 0; v < 8; ++v) {
+                const float4 f = __ldcg(src + v);
+                acc[v * 4 + 0] += w * f.x;
+                acc[v * 4 + 1] += w * f.y;
+                acc[v * 4 + 2] += w * f.z;
+                acc[v * 4 + 3] += w * f.w;
+              }
+            }
+            stage_chunk32(stg_row, row, D == 128 ? c32 * 4 : half * 4, acc, inv);
+          }
+          store_staged(it);
+          write_stats(it, mtrue, mrun, ltot);
         }
       }
+      if (tracer) trace_ev<kTrace>(tracing, p, &ctl->trace_count, 24, 0, it.t);
     }
     if (leader) bulk_wait_group<0>();  // O stores landed
   }
@@ -725,23 +734,43 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
+// Fully masked row tiles (no tile in the list): zero output rows, row_max = -inf, row_sum = 0
+// (engine.hpp:330-332). One CTA per (slot, empty row tile), 128 threads = rows.
+template <int D>
+__global__ void __launch_bounds__(128) zero_rows_kernel(const uint32_t* __restrict__ rows,
+                                                        uint32_t n_rows, uint64_t n,
+                                                        __nv_bfloat16* __restrict__ out,
+                                                        float* __restrict__ row_max,
+                                                        float* __restrict__ row_sum) {
+  const uint32_t slot = blockIdx.x / n_rows;
+  const uint64_t grow = static_cast<uint64_t>(rows[blockIdx.x % n_rows]) * 128 + threadIdx.x;
+  if (grow >= n) return;
+  uint4* dst = reinterpret_cast<uint4*>(out + (static_cast<uint64_t>(slot) * n + grow) * D);
+#pragma unroll
+  for (uint32_t v = 0; v < D / 8; ++v) dst[v] = make_uint4(0, 0, 0, 0);
+  const uint64_t si = static_cast<uint64_t>(slot) * n + grow;
+  if (row_max) row_max[si] = -INFINITY;
+  if (row_sum) row_sum[si] = 0.0f;
+}
+
 // ------------------------------------------------------------------ host side
 
 // Row units for a launch: row tiles longer than L are split into balanced chunks. With dynamic
-// longest-first claiming the makespan is about (average work per stream + longest unit), so L is
-// half a stream's average share (at least 16 tiles: combining partials is not free).
+// longest-first claiming the makespan is about (average work per CTA + longest unit), so L is
+// half a CTA's average share (at least 16 tiles: combining partials is not free).
 struct UnitBuild {
   std::vector<uint4> desc;
   std::vector<uint2> split_info;
+  std::vector<uint32_t> empty_rows;  // row tiles without any tile: zeroed by zero_rows_kernel
   uint32_t split_chunks = 0;
 };
 
-UnitBuild build_units(const std::vector<uint32_t>& row_tiles, uint64_t slots, int streams) {
+UnitBuild build_units(const std::vector<uint32_t>& row_tiles, uint64_t slots, int workers) {
   uint64_t total = 0;
   for (uint32_t c : row_tiles) total += c;
   total *= slots;
-  const uint64_t per_stream = total / static_cast<uint64_t>(std::max(1, streams));
-  const uint32_t L = static_cast<uint32_t>(std::max<uint64_t>(16, (per_stream + 1) / 2));
+  const uint64_t per_worker = total / static_cast<uint64_t>(std::max(1, workers));
+  const uint32_t L = static_cast<uint32_t>(std::max<uint64_t>(16, (per_worker + 1) / 2));
   UnitBuild ub;
   struct U {
     uint32_t rt, j0, nt, split;
@@ -749,6 +778,10 @@ UnitBuild build_units(const std::vector<uint32_t>& row_tiles, uint64_t slots, in
   std::vector<U> units;
   for (uint32_t p = 0; p < row_tiles.size(); ++p) {
     const uint32_t nt = row_tiles[p];
+    if (nt == 0) {  // never enters the work queue (every queued item has >= 1 tile)
+      ub.empty_rows.push_back(p);
+      continue;
+    }
     if (nt <= L) {
       units.push_back({p, 0, nt, kNoSplit});
       continue;
@@ -774,14 +807,13 @@ void launch_impl(const Prep& prep, const AttnArgs& a, cudaStream_t s, int num_sm
   static_assert(smem_bytes<D>() <= 232448, "exceeds the 227 KB opt-in shared memory");
   const KernelMeta& km = prep.kmeta;
   constexpr bool kAllTiles = (MODE == kModeDense || MODE == kModeNaive);
-  // one CTA per SM; when work items are scarce, at most one CTA per item (a CTA's engine
-  // serializes its two streams' tiles, so spreading scarce items over more SMs wins)
+  // one CTA per SM; when work items are scarce, at most one CTA per item
   const uint32_t grid = std::min<uint32_t>(
       static_cast<uint32_t>(std::max<uint64_t>(1, a.slots * km.krows)), static_cast<uint32_t>(num_sms));
-  const LaunchPlan& plan = prep.plan_for(kAllTiles, a.slots, 2 * grid, [&]() {
+  const LaunchPlan& plan = prep.plan_for(kAllTiles, a.slots, grid, [&]() {
     std::vector<uint32_t> rows(km.krows);
     for (uint32_t p = 0; p < km.krows; ++p) rows[p] = kAllTiles ? km.kcols : prep.h_row_cnt[p];
-    const UnitBuild ub = build_units(rows, a.slots, static_cast<int>(2 * grid));
+    const UnitBuild ub = build_units(rows, a.slots, static_cast<int>(grid));
     LaunchPlan lp;
     lp.units = static_cast<uint32_t>(ub.desc.size());
     lp.split_rows = static_cast<uint32_t>(ub.split_info.size());
@@ -794,6 +826,12 @@ void launch_impl(const Prep& prep, const AttnArgs& a, cudaStream_t s, int num_sm
     if (!ub.split_info.empty())
       BBM_CUDA(cudaMemcpy(lp.split_info, ub.split_info.data(),
                           ub.split_info.size() * sizeof(uint2), cudaMemcpyHostToDevice));
+    lp.empty_rows = static_cast<uint32_t>(ub.empty_rows.size());
+    if (lp.empty_rows) {
+      BBM_CUDA(cudaMalloc(&lp.empty_list, ub.empty_rows.size() * sizeof(uint32_t)));
+      BBM_CUDA(cudaMemcpy(lp.empty_list, ub.empty_rows.data(),
+                          ub.empty_rows.size() * sizeof(uint32_t), cudaMemcpyHostToDevice));
+    }
     const size_t nctr = std::max<size_t>(1, a.slots * lp.split_rows);
     BBM_CUDA(cudaMalloc(&lp.split_ctr, nctr * sizeof(uint32_t)));
     BBM_CUDA(cudaMemset(lp.split_ctr, 0, nctr * sizeof(uint32_t)));
@@ -836,6 +874,12 @@ void launch_impl(const Prep& prep, const AttnArgs& a, cudaStream_t s, int num_sm
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes<D>()));
     attr_set = true;
   }
+  if (plan.empty_rows) {
+    zero_rows_kernel<D><<<static_cast<unsigned>(a.slots * plan.empty_rows), 128, 0, s>>>(
+        plan.empty_list, plan.empty_rows, a.n, p.out, p.row_max, p.row_sum);
+    BBM_CUDA(cudaGetLastError());
+  }
+  if (p.total_items == 0) return;
   if (p.trace)  // event-tracing build of the same kernel (bbm_set_trace)
     attn_fwd_kernel<D, MODE, true><<<grid, kThreads, smem_bytes<D>(), s>>>(tq, tk, tv, to, p);
   else

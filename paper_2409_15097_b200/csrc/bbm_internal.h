@@ -77,6 +77,8 @@ struct LaunchPlan {
   uint4* unit_desc = nullptr;    // [units] {row tile, j0, tiles, split | kNoSplit}
   uint2* split_info = nullptr;   // [split_rows] {chunks, first workspace chunk}
   uint32_t* split_ctr = nullptr; // [slots][split_rows] finished-chunk counters
+  uint32_t empty_rows = 0;         // row tiles without tiles (zeroed by a small kernel)
+  uint32_t* empty_list = nullptr;
 };
 
 struct Prep {

@@ -205,6 +205,7 @@ Prep::~Prep() {
     cudaFree(kv.second.unit_desc);
     cudaFree(kv.second.split_info);
     cudaFree(kv.second.split_ctr);
+    cudaFree(kv.second.empty_list);
   }
   if (prev >= 0) cudaSetDevice(prev);
 }

@@ -10,8 +10,8 @@
 
 using namespace bbm::ptx;
 
-template <int MODE, int N, bool kTma>  // MODE 0 = SS, 1 = TS; kTma: concurrent bulk copies
-__global__ void __launch_bounds__(128, 1) rate_kernel(int iters, unsigned long long* out,
+template <int MODE, int N, bool kTma, int kLdWarps = 0>  // MODE 0 = SS, 1 = TS
+__global__ void __launch_bounds__(384, 1) rate_kernel(int iters, unsigned long long* out,
                                                       const uint8_t* gsrc, volatile int* stop) {
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ uint64_t bar, tbar;
@@ -68,27 +68,47 @@ __global__ void __launch_bounds__(128, 1) rate_kernel(int iters, unsigned long l
     }
     if (blockIdx.x == 0) out[1] = n;
   }
+  if (kLdWarps > 0 && warp >= 4 && warp < 4 + kLdWarps) {
+    // TMEM readers like the softmax engine: 64 columns of the second S buffer per pass, plus a
+    // 16-column store back, in a loop until the MMA thread is done
+    const uint32_t lane_off = ((warp & 3) * 32) << 16;
+    const uint32_t half = (warp >= 8) ? 1 : 0;
+    uint64_t passes = 0;
+    while (!done) {
+      uint32_t a0[32], a1[32];
+      tmem_ld32(tmem + 384 + lane_off + half * 64, a0);
+      tmem_ld32(tmem + 384 + lane_off + half * 64 + 32, a1);
+      tmem_ld_wait();
+      uint32_t pk[16];
+#pragma unroll
+      for (int i = 0; i < 16; ++i) pk[i] = a0[2 * i] ^ a1[2 * i + 1];
+      tmem_st16(tmem + 384 + lane_off + half * 32, pk);
+      tmem_st_wait();
+      ++passes;
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 128) out[1] = passes;
+  }
   tc_fence_before();
   __syncthreads();
   if (warp == 0) tmem_dealloc<512>(tmem);
 }
 
-template <int MODE, int N, bool kTma>
+template <int MODE, int N, bool kTma, int kLdWarps = 0>
 void run(const char* name) {
   unsigned long long* d;
   cudaMalloc(&d, 16);
   uint8_t* g;
   cudaMalloc(&g, 64 * 32768);
   const int smem = 2 * 65536 + 32768 + 1024;
-  cudaFuncSetAttribute(rate_kernel<MODE, N, kTma>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaFuncSetAttribute(rate_kernel<MODE, N, kTma, kLdWarps>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   const int iters = 2000;
-  rate_kernel<MODE, N, kTma><<<148, 128, smem>>>(iters, d, g, nullptr);
-  rate_kernel<MODE, N, kTma><<<148, 128, smem>>>(iters, d, g, nullptr);
+  rate_kernel<MODE, N, kTma, kLdWarps><<<148, 384, smem>>>(iters, d, g, nullptr);
+  rate_kernel<MODE, N, kTma, kLdWarps><<<148, 384, smem>>>(iters, d, g, nullptr);
   cudaError_t e = cudaDeviceSynchronize();
   unsigned long long res[2] = {0, 0};
   cudaMemcpy(res, d, 16, cudaMemcpyDeviceToHost);
   const double per = double(res[0]) / (iters * 8.0 * (N / 128.0));
-  std::printf("%-12s N=%3d tma=%d: %s  %.1f cycles per 128x128x16 (ideal 64); bulk copies %llu (%.1f B/cycle)\n",
+  std::printf("%-12s N=%3d tma=%d: %s  %.1f cycles per 128x128x16 (ideal 64); side count %llu (%.1f B/cycle if bulk)\n",
               name, N, int(kTma), e == cudaSuccess ? "ok" : cudaGetErrorString(e), per, res[1],
               res[1] * 32768.0 / double(res[0]));
   cudaFree(d);
@@ -99,7 +119,8 @@ int main() {
   run<0, 128, false>("SS");
   run<1, 128, false>("TS");
   run<0, 128, true>("SS+bulk");
-  run<1, 128, true>("TS+bulk");
-  run<0, 256, true>("SS+bulk");
+  run<0, 128, false, 4>("SS+4ldwarps");
+  run<0, 128, false, 8>("SS+8ldwarps");
+  run<1, 128, false, 8>("TS+8ldwarps");
   return 0;
 }
