@@ -105,6 +105,12 @@ bbm_status bbm_prep_get_kernel_lists(bbm_prep prep, uint32_t* row_cnt, uint32_t*
 /* EngineCounters a blocked_forward over `slots` slots reports for `variant`
  * (classify_tile, engine.hpp:118-153; summed as run_attention does, engine.hpp:500-503). */
 bbm_status bbm_prep_counters(bbm_prep prep, int variant, uint64_t slots, bbm_counters* out);
+/* build_block_occupancy + build_dense_runs + block_stats (mask.hpp:203-247) for a caller-held
+ * BlockSums (u32 [ceil(n/bi)][ceil(n/bj)], row-major), on `device`: the same per-row-tile
+ * kernel the preprocessor runs after its sums pass. Any output pointer may be NULL. */
+bbm_status bbm_sums_metadata(const uint32_t* sums, uint64_t n, uint64_t block_i, uint64_t block_j,
+                             int device, uint8_t* occ, uint32_t* offset, uint32_t* total_ones,
+                             bbm_block_stats* stats);
 /* Peer-to-peer copy of the device metadata to another GPU (NVLink), for the multi-GPU driver.
  * The result is an independent prep bound to `device`. */
 bbm_status bbm_prep_replicate(bbm_prep prep, int device, void* stream, bbm_prep* out);
@@ -130,6 +136,23 @@ bbm_status bbm_attn_fwd_host_bf16(bbm_prep prep, int variant, const uint16_t* q,
 bbm_status bbm_attn_fwd_host_f32(bbm_prep prep, int variant, const float* q, const float* k,
                                  const float* v, float* out, double* row_max, double* row_sum,
                                  uint64_t slots, uint32_t head_dim, double scale);
+
+/* ---- blocked_backward (engine.hpp:346-471): dq, dk, dv of L = sum(out * d_out) from the forward's
+ *      saved row statistics (row_max / row_sum as bbm_attn_fwd returns them), over the same tiles
+ *      the forward processed. Deterministic (no atomics on gradients). Device pointers, bf16
+ *      [slots][n][d]; asynchronous on `stream`. The first call on a prep builds its column view
+ *      (column tile lists + transposed partial-tile bitmaps), which needs one host sync. ---- */
+bbm_status bbm_attn_bwd(bbm_prep prep, int variant, const void* q, const void* k, const void* v,
+                        const void* out, const float* row_max, const float* row_sum,
+                        const void* d_out, void* dq, void* dk, void* dv, uint64_t slots,
+                        uint32_t head_dim, double scale, void* stream);
+/* Same, float host buffers (Matrix<float>) with the reference's double row statistics; q, k, v,
+ * d_out are rounded to bf16 on the device, out stays fp32 for delta = rowsum(d_out * out).
+ * Validates finiteness of q, k, v, d_out (engine.hpp:244-258, 358). Synchronous. */
+bbm_status bbm_attn_bwd_host_f32(bbm_prep prep, int variant, const float* q, const float* k,
+                                 const float* v, const float* out, const double* row_max,
+                                 const double* row_sum, const float* d_out, float* dq, float* dk,
+                                 float* dv, uint64_t slots, uint32_t head_dim, double scale);
 
 /* Multi-GPU run_attention: slots sharded contiguously over `n_devices` GPUs
  * ([g*S/G, (g+1)*S/G)), metadata replicated peer-to-peer from prep's device, one stream per
@@ -161,6 +184,18 @@ bbm_status bbm_permute_rows_device(const void* src, void* dst, const uint32_t* d
  * both masks in the reference packed layout (ceil(n/64) words per row). */
 bbm_status bbm_permute_mask_device(const uint64_t* d_src, uint64_t* d_dst,
                                    const uint32_t* d_forward, uint64_t n, void* stream);
+
+/* Host-buffer forms of the two kernels above (upload, permute on `device`, download), for the
+ * Matrix<T>/Mask overloads of the C++ drop-in headers. Any row_bytes >= 1. `forward` must be a
+ * bijection (Permutation::from_forward, reorder.hpp:57-68) or BBM_ERR_INVALID is returned. */
+bbm_status bbm_permute_rows_host(const void* src, void* dst, const uint32_t* forward,
+                                 uint64_t slots, uint64_t n, uint64_t row_bytes, int inverse,
+                                 int device);
+bbm_status bbm_permute_mask_host(const uint64_t* src, uint64_t* dst, const uint32_t* forward,
+                                 uint64_t n, int device);
+/* build_graph (reorder.hpp:28-49) as CSR: offsets u64 [n+1]; neighbors u32 [offsets[n]] sorted
+ * ascending per node (NULL to query offsets only). Host. */
+bbm_status bbm_graph_csr(const uint64_t* words, uint64_t n, uint64_t* offsets, uint32_t* neighbors);
 
 /* ---- generators.hpp (host fixtures): MaskSpec grammar (generators.hpp:364-438); families with
  *      a free n take n_free. Call with words == NULL to query n. ---- */

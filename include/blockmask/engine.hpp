@@ -1,0 +1,263 @@
+// blockmask/engine.hpp — drop-in for the reference's attention engine (proj/include/blockmask/
+// engine.hpp:21-505). Same types and entry points; the work runs on the B200:
+//
+//   preprocess_mask (engine.hpp:80-91)      -> bbm_preprocess_packed_host (GPU preprocessor; the
+//                                              MaskPrep keeps the device metadata alive)
+//   blocked_forward (engine.hpp:282-341)    -> bbm_attn_fwd_host_f32 (sm_100a tcgen05 kernel)
+//   blocked_backward (engine.hpp:346-471)   -> bbm_attn_bwd_host_f32
+//   run_attention (engine.hpp:489-505)      -> one bbm_attn_fwd_host_f32 launch over all slots
+//
+// Numerics: Q/K/V are rounded to bf16 (RNE) on the device and the kernel accumulates in fp32, so
+// outputs agree with the reference to a bf16 tolerance (max-abs <= 2e-2; tests/), not bit for
+// bit. Counters (engine.hpp:47-66) are exact: they depend on the mask and spec only.
+// New rejections (std::invalid_argument): head dims other than 64 / 128, d_v != d_k.
+// `threads` is validated (>= 1) like the reference and otherwise ignored.
+#pragma once
+
+#include <cmath>
+#include <cstdint>
+#include <limits>
+#include <memory>
+#include <span>
+#include <string>
+#include <type_traits>
+#include <vector>
+
+#include "blockmask/device.hpp"
+#include "blockmask/mask.hpp"
+#include "blockmask/matrix.hpp"
+
+namespace blockmask {
+
+enum class Variant {
+    dense,         // every tile, mask ignored
+    naive_masked,  // every tile, mask applied everywhere
+    binblk,        // occupied tiles only
+    dense_binblk,  // occupied tiles; the first full run of each row skips its mask reads
+};
+
+inline const char* to_string(Variant v) {
+    switch (v) {
+        case Variant::dense: return "dense";
+        case Variant::naive_masked: return "naive";
+        case Variant::binblk: return "binblk";
+        case Variant::dense_binblk: return "dense-binblk";
+    }
+    return "?";
+}
+
+inline Variant parse_variant(const std::string& name) {
+    if (name == "dense") return Variant::dense;
+    if (name == "naive") return Variant::naive_masked;
+    if (name == "binblk") return Variant::binblk;
+    if (name == "dense-binblk") return Variant::dense_binblk;
+    throw std::invalid_argument("unknown variant: '" + name +
+                                "' (expected dense, naive, binblk, dense-binblk)");
+}
+
+struct EngineCounters {
+    std::uint64_t blocks_visited = 0;
+    std::uint64_t blocks_processed = 0;
+    std::uint64_t mask_block_reads = 0;
+    std::uint64_t skipped_by_binblk = 0;
+    std::uint64_t skipped_mask_reads_by_run = 0;
+
+    EngineCounters& operator+=(const EngineCounters& o) {
+        blocks_visited += o.blocks_visited;
+        blocks_processed += o.blocks_processed;
+        mask_block_reads += o.mask_block_reads;
+        skipped_by_binblk += o.skipped_by_binblk;
+        skipped_mask_reads_by_run += o.skipped_mask_reads_by_run;
+        return *this;
+    }
+    friend bool operator==(const EngineCounters&, const EngineCounters&) = default;
+};
+
+/// The reference's MaskPrep fields plus `device`: the GPU-resident metadata (tile lists,
+/// partial-tile bitmaps) shared by every call that uses this prep.
+struct MaskPrep {
+    std::size_t n_tokens = 0;
+    BlockSpec spec;
+    BlockSums sums;
+    BlockOccupancy occupancy;
+    DenseRuns runs;
+    BlockStats stats;
+    device::PrepPtr device;
+};
+
+inline MaskPrep preprocess_mask(const Mask& mask, BlockSpec spec) {
+    spec.validate();
+    require(mask.size() >= 1, "mask must be non-empty");
+    bbm_prep h = nullptr;
+    device::check(bbm_preprocess_packed_host(mask.words(), mask.size(), spec.block_i, spec.block_j,
+                                             device::default_device(), &h),
+                  "preprocess_mask");
+    MaskPrep prep;
+    prep.device = std::make_shared<device::PrepHandle>(h);
+    prep.n_tokens = mask.size();
+    prep.spec = spec;
+    prep.sums = BlockSums(mask.size(), spec);
+    device::check(bbm_prep_get_sums(h, prep.sums.data()), "preprocess_mask");
+    prep.occupancy = BlockOccupancy(prep.sums.rows(), prep.sums.cols());
+    device::check(bbm_prep_get_occupancy(h, prep.occupancy.data()), "preprocess_mask");
+    prep.runs.offset.assign(prep.sums.rows(), 0);
+    prep.runs.total_ones.assign(prep.sums.rows(), 0);
+    device::check(bbm_prep_get_runs(h, prep.runs.offset.data(), prep.runs.total_ones.data()),
+                  "preprocess_mask");
+    bbm_block_stats st{};
+    device::check(bbm_prep_get_stats(h, &st), "preprocess_mask");
+    prep.stats = BlockStats{st.blocks_total, st.blocks_nonzero, st.blocks_full, st.block_density,
+                            st.element_density};
+    return prep;
+}
+
+template <typename T>
+struct ForwardResult {
+    Matrix<T> out;
+    std::vector<double> row_max;  // natural-log units, -inf for fully masked rows
+    std::vector<double> row_sum;  // 0 for fully masked rows
+    EngineCounters counters;
+};
+
+template <typename T>
+struct BackwardResult {
+    Matrix<T> dq;
+    Matrix<T> dk;
+    Matrix<T> dv;
+    EngineCounters counters;
+};
+
+template <typename T>
+struct SlotInputs {
+    Matrix<T> q, k, v;
+};
+
+template <typename T>
+struct MultiHeadForward {
+    std::vector<ForwardResult<T>> slots;
+    EngineCounters counters;
+};
+
+namespace detail {
+
+inline EngineCounters counters_for(const MaskPrep& prep, Variant v, std::uint64_t slots) {
+    bbm_counters c{};
+    device::check(bbm_prep_counters(prep.device->get(), static_cast<int>(v), slots, &c), "counters");
+    return EngineCounters{c.blocks_visited, c.blocks_processed, c.mask_block_reads,
+                          c.skipped_by_binblk, c.skipped_mask_reads_by_run};
+}
+
+// validate_forward_args (engine.hpp:244-258) minus the finiteness scan, which the device does
+// while converting the inputs (bbm_attn_fwd_host_f32 -> BBM_ERR_INVALID).
+template <typename T>
+void validate_shapes(const Matrix<T>& q, const Matrix<T>& k, const Matrix<T>& v, double scale,
+                     const Mask& mask, const MaskPrep& prep, unsigned threads) {
+    const std::size_t n = mask.size();
+    require(prep.n_tokens == n, "mask preprocessing does not match this mask");
+    require(prep.device != nullptr, "MaskPrep was not built by preprocess_mask");
+    require(q.rows() == n && k.rows() == n && v.rows() == n, "q, k, v need one row per token");
+    require(q.cols() == k.cols(), "q and k must share the head dimension");
+    require(v.cols() >= 1, "v needs at least one column");
+    require(std::isfinite(scale), "scale must be finite");
+    require(threads >= 1, "threads must be >= 1");
+}
+
+// Matrix<T> (float or double) -> packed float [slots][n][d] (the C ABI's host format).
+template <typename T>
+void append_f32(std::vector<float>& dst, const Matrix<T>& m) {
+    const std::size_t at = dst.size();
+    dst.resize(at + m.size());
+    for (std::size_t i = 0; i < m.size(); ++i) dst[at + i] = static_cast<float>(m.data()[i]);
+}
+
+template <typename T>
+void forward_slots(const std::vector<const SlotInputs<T>*>& in, double scale, const MaskPrep& prep,
+                   Variant variant, std::vector<ForwardResult<T>>& out) {
+    static_assert(std::is_floating_point_v<T>, "Matrix<T> of float or double");
+    const std::size_t slots = in.size(), n = prep.n_tokens, d = in.front()->q.cols();
+    std::vector<float> q, k, v;
+    q.reserve(slots * n * d), k.reserve(slots * n * d), v.reserve(slots * n * d);
+    for (const SlotInputs<T>* s : in) append_f32(q, s->q), append_f32(k, s->k), append_f32(v, s->v);
+    if (in.front()->v.cols() != d)
+        throw std::invalid_argument("d_v != d_k is not supported by the sm_100a kernel");
+    std::vector<float> o(slots * n * d);
+    std::vector<double> rmax(slots * n), rsum(slots * n);
+    device::check(bbm_attn_fwd_host_f32(prep.device->get(), static_cast<int>(variant), q.data(),
+                                        k.data(), v.data(), o.data(), rmax.data(), rsum.data(),
+                                        slots, static_cast<std::uint32_t>(d), scale),
+                  "blocked_forward");
+    const EngineCounters per_slot = counters_for(prep, variant, 1);
+    out.resize(slots);
+    for (std::size_t s = 0; s < slots; ++s) {
+        ForwardResult<T>& r = out[s];
+        r.out = Matrix<T>(n, d);
+        for (std::size_t i = 0; i < n * d; ++i) r.out.data()[i] = static_cast<T>(o[s * n * d + i]);
+        r.row_max.assign(rmax.begin() + s * n, rmax.begin() + (s + 1) * n);
+        r.row_sum.assign(rsum.begin() + s * n, rsum.begin() + (s + 1) * n);
+        r.counters = per_slot;
+    }
+}
+
+}  // namespace detail
+
+template <typename T>
+ForwardResult<T> blocked_forward(const Matrix<T>& q, const Matrix<T>& k, const Matrix<T>& v,
+                                 double scale, const Mask& mask, const MaskPrep& prep,
+                                 Variant variant, unsigned threads = 1) {
+    detail::validate_shapes(q, k, v, scale, mask, prep, threads);
+    SlotInputs<T> one{q, k, v};
+    std::vector<ForwardResult<T>> out;
+    detail::forward_slots<T>({&one}, scale, prep, variant, out);
+    return std::move(out.front());
+}
+
+template <typename T>
+BackwardResult<T> blocked_backward(const Matrix<T>& q, const Matrix<T>& k, const Matrix<T>& v,
+                                   double scale, const Mask& mask, const MaskPrep& prep,
+                                   Variant variant, const ForwardResult<T>& fwd,
+                                   const Matrix<T>& d_out, unsigned threads = 1) {
+    detail::validate_shapes(q, k, v, scale, mask, prep, threads);
+    const std::size_t n = mask.size(), d = q.cols();
+    require(fwd.out.rows() == n && fwd.out.cols() == v.cols(), "forward output shape mismatch");
+    require(fwd.row_max.size() == n && fwd.row_sum.size() == n, "forward row stats missing");
+    require(d_out.rows() == n && d_out.cols() == v.cols(), "d_out shape must match the output");
+    if (v.cols() != d) throw std::invalid_argument("d_v != d_k is not supported by the sm_100a kernel");
+    std::vector<float> hq, hk, hv, ho, hdo;
+    detail::append_f32(hq, q), detail::append_f32(hk, k), detail::append_f32(hv, v);
+    detail::append_f32(ho, fwd.out), detail::append_f32(hdo, d_out);
+    std::vector<float> dq(n * d), dk(n * d), dv(n * d);
+    device::check(bbm_attn_bwd_host_f32(prep.device->get(), static_cast<int>(variant), hq.data(),
+                                        hk.data(), hv.data(), ho.data(), fwd.row_max.data(),
+                                        fwd.row_sum.data(), hdo.data(), dq.data(), dk.data(),
+                                        dv.data(), 1, static_cast<std::uint32_t>(d), scale),
+                  "blocked_backward");
+    BackwardResult<T> r;
+    r.dq = Matrix<T>(n, d), r.dk = Matrix<T>(n, d), r.dv = Matrix<T>(n, d);
+    for (std::size_t i = 0; i < n * d; ++i) {
+        r.dq.data()[i] = static_cast<T>(dq[i]);
+        r.dk.data()[i] = static_cast<T>(dk[i]);
+        r.dv.data()[i] = static_cast<T>(dv[i]);
+    }
+    r.counters = detail::counters_for(prep, variant, 1);
+    return r;
+}
+
+template <typename T>
+MultiHeadForward<T> run_attention(std::span<const SlotInputs<T>> slots, double scale,
+                                  const Mask& mask, const MaskPrep& prep, Variant variant,
+                                  unsigned threads = 1) {
+    require(!slots.empty(), "need at least one batch/head slot");
+    std::vector<const SlotInputs<T>*> in;
+    for (const SlotInputs<T>& s : slots) {
+        require(s.q.cols() == slots.front().q.cols() && s.v.cols() == slots.front().v.cols(),
+                "all slots must share head dimensions");
+        detail::validate_shapes(s.q, s.k, s.v, scale, mask, prep, threads);
+        in.push_back(&s);
+    }
+    MultiHeadForward<T> res;
+    detail::forward_slots<T>(in, scale, prep, variant, res.slots);  // one launch, all slots
+    for (const ForwardResult<T>& r : res.slots) res.counters += r.counters;
+    return res;
+}
+
+}  // namespace blockmask

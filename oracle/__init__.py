@@ -66,6 +66,8 @@ def orc():
                                         C.c_double, u64p, f64p, f64p, f64p, C.c_int]
         L.orc_dense_forward.argtypes = [f64p, f64p, f64p, C.c_uint64, C.c_uint64, C.c_uint64,
                                         C.c_double, f64p, f64p, f64p, C.c_int]
+        L.orc_naive_backward.argtypes = [f64p, f64p, f64p, f64p, C.c_uint64, C.c_uint64, C.c_double,
+                                         u64p, f64p, f64p, f64p, C.c_int]
         L.orc_rcm_order.argtypes = [u64p, C.c_uint64, u32p]
         L.orc_bandwidth.argtypes = [u64p, C.c_uint64]
         L.orc_bandwidth.restype = C.c_uint64
@@ -185,6 +187,31 @@ def naive_forward(q, k, v, scale: float, words, n: int, threads: int = 8):
                             _p(w, C.c_uint64), _p(out, C.c_double), _p(rmax, C.c_double),
                             _p(rsum, C.c_double), threads)
     return out, rmax, rsum
+
+
+def naive_backward(q, k, v, d_out, scale: float, words, n: int, threads: int = 8):
+    """reference.hpp:84-139 in double: (dq, dk, dv) of L = sum(out * d_out). words=None -> every
+    key visible (the dense variant)."""
+    q, k, v, g = (np.ascontiguousarray(a, dtype=np.float64) for a in (q, k, v, d_out))
+    d = q.shape[1]
+    dq, dk, dv = (np.zeros((n, d), np.float64) for _ in range(3))
+    w = None if words is None else np.ascontiguousarray(words, dtype=np.uint64)
+    orc().orc_naive_backward(_p(q, C.c_double), _p(k, C.c_double), _p(v, C.c_double), _p(g, C.c_double),
+                             n, d, scale, None if w is None else _p(w, C.c_uint64), _p(dq, C.c_double),
+                             _p(dk, C.c_double), _p(dv, C.c_double), threads)
+    return dq, dk, dv
+
+
+def ref_naive_backward(q, k, v, d_out, scale: float, words, n: int):
+    """The reference's own naive_backward (oracle/_ref), to pin the restatement."""
+    q, k, v, g = (np.ascontiguousarray(a, dtype=np.float64) for a in (q, k, v, d_out))
+    d = q.shape[1]
+    dq, dk, dv = (np.zeros((n, d), np.float64) for _ in range(3))
+    w = np.ascontiguousarray(words, dtype=np.uint64)
+    _check_ref(ref().ref_naive_backward(_p(q, C.c_double), _p(k, C.c_double), _p(v, C.c_double), n, d, scale,
+                                        _p(w, C.c_uint64), _p(g, C.c_double), _p(dq, C.c_double),
+                                        _p(dk, C.c_double), _p(dv, C.c_double)))
+    return dq, dk, dv
 
 
 def rcm_order(words, n: int) -> np.ndarray:

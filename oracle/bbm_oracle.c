@@ -276,6 +276,100 @@ void orc_dense_forward(const double* q, const double* k, const double* v, uint64
   run_forward(q, k, v, n, d, dv, scale, NULL, out, row_max, row_sum, threads);
 }
 
+/* reference.hpp:84-139 — naive_backward: gradients of L = sum(out * d_out), one query row at a
+ * time in double. words == NULL: every key visible (the dense variant). Threads split the query
+ * rows; each owns private dk/dv accumulators, summed afterwards in thread order. */
+typedef struct {
+  const double *q, *k, *v, *dout;
+  uint64_t n, d;
+  double scale;
+  const uint64_t* words;
+  double *dq, *dk, *dv; /* dq: shared (rows owned); dk, dv: private */
+  uint64_t r0, r1;
+} bwd_job;
+
+static void* bwd_rows(void* arg) {
+  const bwd_job* j = (const bwd_job*)arg;
+  const uint64_t n = j->n, d = j->d, wpr = wpr_of(n);
+  double* s = (double*)malloc(sizeof(double) * (n ? n : 1));
+  double* p = (double*)malloc(sizeof(double) * (n ? n : 1));
+  double* dp = (double*)malloc(sizeof(double) * (n ? n : 1));
+  for (uint64_t i = j->r0; i < j->r1; ++i) {
+    double m = -INFINITY;
+    for (uint64_t c = 0; c < n; ++c) {
+      if (j->words && !((j->words[i * wpr + (c >> 6)] >> (c & 63)) & 1u)) continue;
+      double t = 0.0;
+      for (uint64_t x = 0; x < d; ++x) t += j->q[i * d + x] * j->k[c * d + x];
+      s[c] = j->scale * t;
+      if (s[c] > m) m = s[c];
+    }
+    if (isinf(m)) continue; /* fully masked row contributes nothing */
+    double l = 0.0;
+    for (uint64_t c = 0; c < n; ++c) {
+      if (j->words && !((j->words[i * wpr + (c >> 6)] >> (c & 63)) & 1u)) continue;
+      p[c] = exp(s[c] - m);
+      l += p[c];
+    }
+    double delta = 0.0;
+    for (uint64_t c = 0; c < n; ++c) {
+      if (j->words && !((j->words[i * wpr + (c >> 6)] >> (c & 63)) & 1u)) continue;
+      p[c] /= l;
+      double t = 0.0;
+      for (uint64_t x = 0; x < d; ++x) t += j->dout[i * d + x] * j->v[c * d + x];
+      dp[c] = t;
+      delta += p[c] * t;
+    }
+    for (uint64_t c = 0; c < n; ++c) {
+      if (j->words && !((j->words[i * wpr + (c >> 6)] >> (c & 63)) & 1u)) continue;
+      const double ds = p[c] * (dp[c] - delta);
+      for (uint64_t x = 0; x < d; ++x) {
+        j->dq[i * d + x] += j->scale * ds * j->k[c * d + x];
+        j->dk[c * d + x] += j->scale * ds * j->q[i * d + x];
+      }
+      for (uint64_t x = 0; x < d; ++x) j->dv[c * d + x] += p[c] * j->dout[i * d + x];
+    }
+  }
+  free(s);
+  free(p);
+  free(dp);
+  return NULL;
+}
+
+void orc_naive_backward(const double* q, const double* k, const double* v, const double* dout,
+                        uint64_t n, uint64_t d, double scale, const uint64_t* words, double* dq,
+                        double* dk, double* dv, int threads) {
+  if (threads < 1) threads = 1;
+  if ((uint64_t)threads > n) threads = (int)(n ? n : 1);
+  pthread_t* tid = (pthread_t*)malloc(sizeof(pthread_t) * threads);
+  bwd_job* jobs = (bwd_job*)malloc(sizeof(bwd_job) * threads);
+  const uint64_t nd = n * d;
+  double* priv = (double*)calloc(2 * nd * (uint64_t)threads + 1, sizeof(double));
+  memset(dq, 0, sizeof(double) * nd);
+  for (int t = 0; t < threads; ++t) {
+    bwd_job jb = {q, k, v, dout, n, d, scale, words, dq, priv + 2 * nd * t, priv + 2 * nd * t + nd,
+                  n * (uint64_t)t / threads, n * (uint64_t)(t + 1) / threads};
+    jobs[t] = jb;
+    if (threads == 1)
+      bwd_rows(&jobs[t]);
+    else
+      pthread_create(&tid[t], NULL, bwd_rows, &jobs[t]);
+  }
+  if (threads > 1)
+    for (int t = 0; t < threads; ++t) pthread_join(tid[t], NULL);
+  for (uint64_t e = 0; e < nd; ++e) {
+    double a = 0.0, b = 0.0;
+    for (int t = 0; t < threads; ++t) {
+      a += priv[2 * nd * t + e];
+      b += priv[2 * nd * t + nd + e];
+    }
+    dk[e] = a;
+    dv[e] = b;
+  }
+  free(priv);
+  free(tid);
+  free(jobs);
+}
+
 /* -------------------------------------------------------------- reorder.hpp */
 typedef struct {
   uint64_t n;

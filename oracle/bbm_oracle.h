@@ -70,6 +70,10 @@ void orc_dense_forward(const double* q, const double* k, const double* v, uint64
                        double* row_sum, int threads);
 
 /* --- reorder.hpp:28-189 --- */
+/* reference.hpp:84-139 (naive_backward); words == NULL: dense (every key visible) */
+void orc_naive_backward(const double* q, const double* k, const double* v, const double* dout,
+                        uint64_t n, uint64_t d, double scale, const uint64_t* words, double* dq,
+                        double* dk, double* dv, int threads);
 int orc_rcm_order(const uint64_t* words, uint64_t n, uint32_t* forward /* n */);
 uint64_t orc_bandwidth(const uint64_t* words, uint64_t n);
 void orc_permute_mask(const uint64_t* words, uint64_t n, const uint32_t* forward,

@@ -339,43 +339,36 @@ def block_sums(mask, spec: BlockSpec) -> BlockSums:
     return preprocess_mask(mask, spec).sums
 
 
+def _sums_metadata(sums: BlockSums, device: int = 0):
+    """build_block_occupancy + build_dense_runs + block_stats of caller-held sums, computed by
+    the preprocessor's per-row-tile kernel on the GPU (C ABI bbm_sums_metadata)."""
+    spec = sums.spec()
+    vals = np.ascontiguousarray(sums.values, dtype=np.uint32)
+    occ = np.empty(vals.shape, np.uint8)
+    off = np.empty(sums.rows(), np.uint32)
+    tot = np.empty(sums.rows(), np.uint32)
+    st = _lib.BlockStatsC()
+    check(lib.bbm_sums_metadata(ptr(vals, C.c_uint32), sums.n_tokens(), spec.block_i, spec.block_j, device,
+                                ptr(occ, C.c_uint8), ptr(off, C.c_uint32), ptr(tot, C.c_uint32), C.byref(st)))
+    return occ, off, tot, st
+
+
 def build_block_occupancy(sums: BlockSums) -> BlockOccupancy:
-    """build_block_occupancy (mask.hpp:203-209): occupied = sums > 0 (O(tiles) metadata)."""
-    return BlockOccupancy((sums.values > 0).astype(np.uint8))
-
-
-def _areas(sums: BlockSums) -> np.ndarray:
-    n, spec = sums.n_tokens(), sums.spec()
-    ri = np.minimum(spec.block_i, n - np.arange(sums.rows()) * spec.block_i)
-    cj = np.minimum(spec.block_j, n - np.arange(sums.cols()) * spec.block_j)
-    return np.outer(ri, cj)
+    """build_block_occupancy (mask.hpp:203-209), on the GPU."""
+    return BlockOccupancy(_sums_metadata(sums)[0])
 
 
 def build_dense_runs(sums: BlockSums) -> DenseRuns:
-    """build_dense_runs (mask.hpp:213-228) over already-computed sums (O(tiles) metadata)."""
-    full = sums.values == _areas(sums)
-    off, tot = [], []
-    for p in range(sums.rows()):
-        idx = np.flatnonzero(full[p])
-        if idx.size == 0:
-            off.append(0)
-            tot.append(0)
-            continue
-        q0 = int(idx[0])
-        notfull = np.flatnonzero(~full[p, q0:])
-        off.append(q0)
-        tot.append(int(notfull[0]) if notfull.size else sums.cols() - q0)
-    return DenseRuns(off, tot)
+    """build_dense_runs (mask.hpp:213-228), on the GPU."""
+    _, off, tot, _ = _sums_metadata(sums)
+    return DenseRuns(off.tolist(), tot.tolist())
 
 
 def block_stats(sums: BlockSums) -> BlockStats:
-    """block_stats (mask.hpp:230-247)."""
-    total = sums.rows() * sums.cols()
-    nz = int((sums.values > 0).sum())
-    full = int((sums.values == _areas(sums)).sum())
-    ones = int(sums.values.astype(np.uint64).sum())
-    n = float(sums.n_tokens())
-    return BlockStats(total, nz, full, nz / total if total else 0.0, ones / (n * n) if n > 0 else 0.0)
+    """block_stats (mask.hpp:230-247), on the GPU."""
+    st = _sums_metadata(sums)[3]
+    return BlockStats(int(st.blocks_total), int(st.blocks_nonzero), int(st.blocks_full),
+                      float(st.block_density), float(st.element_density))
 
 
 # ----------------------------------------------------------------------------- attention
@@ -494,6 +487,79 @@ def _blocked_forward_host(q, k, v, scale, prep, variant) -> ForwardResult:
     if squeeze:
         out, rmax, rsum = out[0], rmax[0], rsum[0]
     return ForwardResult(out, rmax, rsum, counters)
+
+
+@dataclass
+class BackwardResult:
+    """engine.hpp:101-107."""
+    dq: object
+    dk: object
+    dv: object
+    counters: EngineCounters
+
+
+def attn_bwd_device(prep: MaskPrep, variant: Variant, q, k, v, out, row_max, row_sum, d_out,
+                    dq, dk, dv, scale: float = 1.0, stream=None) -> None:
+    """Raw backward launch on device tensors: bf16 [slots][n][d] (q, k, v, out, d_out, dq, dk, dv)
+    and float32 [slots][n] row stats as the forward returns them. The timed entry point."""
+    import torch
+
+    slots, n, d = (q.shape if q.dim() == 3 else (1, *q.shape))
+    s = stream if stream is not None else torch.cuda.current_stream(q.device).cuda_stream
+    vp_ = lambda t: C.c_void_p(t.data_ptr())  # noqa: E731
+    check(lib.bbm_attn_bwd(prep.handle.h, int(variant), vp_(q), vp_(k), vp_(v), vp_(out), vp_(row_max),
+                           vp_(row_sum), vp_(d_out), vp_(dq), vp_(dk), vp_(dv), int(slots), int(d),
+                           float(scale), C.c_void_p(s)))
+
+
+def blocked_backward(q, k, v, scale: float, mask, prep: MaskPrep, variant: Variant, fwd: ForwardResult,
+                     d_out, threads: int = 1) -> BackwardResult:
+    """blocked_backward (engine.hpp:346-471) on the sm_100a kernels: gradients of
+    L = sum(out * d_out) from the forward's saved row statistics. Same containers as
+    blocked_forward (CUDA bf16 tensors or numpy float arrays); counters equal the forward's."""
+    _validate_common(prep, mask, scale, threads)
+    n = prep.n_tokens
+    if isinstance(q, np.ndarray):
+        arrs = [np.ascontiguousarray(a, dtype=np.float32) for a in (q, k, v, fwd.out, d_out)]
+        squeeze = arrs[0].ndim == 2
+        if squeeze:
+            arrs = [a[None] for a in arrs]
+        qa, ka, va, oa, ga = arrs
+        slots, _, d = qa.shape
+        for a in (ka, va, oa, ga):
+            if a.shape != qa.shape:
+                raise ValueError("q, k, v, out, d_out must share one shape (d_v == d_k on the sm_100a kernel)")
+        if qa.shape[1] != n:
+            raise ValueError("q/k/v row count must match mask size")
+        rm = np.ascontiguousarray(np.asarray(fwd.row_max, np.float64).reshape(slots, n))
+        rs = np.ascontiguousarray(np.asarray(fwd.row_sum, np.float64).reshape(slots, n))
+        dq, dk, dv = (np.empty_like(qa) for _ in range(3))
+        check(lib.bbm_attn_bwd_host_f32(prep.handle.h, int(variant), ptr(qa, C.c_float), ptr(ka, C.c_float),
+                                        ptr(va, C.c_float), ptr(oa, C.c_float), ptr(rm, C.c_double),
+                                        ptr(rs, C.c_double), ptr(ga, C.c_float), ptr(dq, C.c_float),
+                                        ptr(dk, C.c_float), ptr(dv, C.c_float), slots, d, float(scale)))
+        if squeeze:
+            dq, dk, dv = dq[0], dk[0], dv[0]
+        return BackwardResult(dq, dk, dv, prep.counters(variant, slots))
+    import torch
+
+    squeeze = q.dim() == 2
+    ts = [t.unsqueeze(0) if squeeze else t for t in (q, k, v, fwd.out, d_out)]
+    if len({tuple(t.shape) for t in ts}) != 1 or ts[0].shape[1] != n:
+        raise ValueError("q, k, v, out, d_out must share one [slots][n][d] shape (d_v == d_k)")
+    for name, t in (("q", q), ("k", k), ("v", v), ("d_out", d_out)):
+        if not bool(torch.isfinite(t).all()):
+            raise ValueError(f"{name} must hold finite values")
+    q3, k3, v3, o3, g3 = (t.to(torch.bfloat16).contiguous() for t in ts)
+    slots, _, d = q3.shape
+    rm = torch.as_tensor(fwd.row_max, device=q3.device).reshape(slots, n).float().contiguous()
+    rs = torch.as_tensor(fwd.row_sum, device=q3.device).reshape(slots, n).float().contiguous()
+    dq, dk, dv = (torch.empty_like(q3) for _ in range(3))
+    with torch.cuda.device(q3.device):
+        attn_bwd_device(prep, variant, q3, k3, v3, o3, rm, rs, g3, dq, dk, dv, scale)
+    if squeeze:
+        dq, dk, dv = dq[0], dk[0], dv[0]
+    return BackwardResult(dq, dk, dv, prep.counters(variant, slots))
 
 
 def run_attention(slots: Sequence[SlotInputs], scale: float, mask, prep: MaskPrep, variant: Variant,

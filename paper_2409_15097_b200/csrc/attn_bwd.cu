@@ -1,0 +1,657 @@
+// attn_bwd.cu — block-sparse masked flash-attention backward for sm_100a (TMA + tcgen05 + TMEM).
+//
+// Replaces the reference's blocked_backward (engine.hpp:346-471): gradients of
+// L = sum(out * d_out) from the forward's saved row statistics, over the same tiles the forward
+// processed (so the counters equal the forward's). Two deterministic kernels, no atomics on
+// gradients (engine.hpp:379-389 merges dK/dV in a fixed order for the same reason):
+//
+//   dkdv  one item per (slot, key tile j): walks the COLUMN list of j (query row tiles i whose
+//         tile (i, j) is occupied, ascending) and accumulates in TMEM
+//             S^T  = K_j Q_i^T          dP^T = V_j dO_i^T         (SS MMAs, M = keys)
+//             P^T  = exp2(S^T sl2 - lse2_i)   dS^T = P^T (dP^T - delta_i)   (registers)
+//             dV_j += P^T dO_i          dK_j += dS^T Q_i           (TS MMAs, A = P^T / dS^T in TMEM)
+//         then writes dK_j * scale and dV_j.
+//   dq    one item per (slot, query row tile i): walks the ROW list of i (the forward's list) with
+//             S = Q_i K_j^T   dP = dO_i V_j^T   P, dS as above   dQ_i += dS K_j
+//         then writes dQ_i * scale.
+// delta_i = rowsum(dO_i * O_i) (engine.hpp:366-372) and lse2 = (row_max + ln row_sum) log2 e come
+// from a small row pass (rowstats_kernel). Fully masked rows (row_sum = 0) and rows past n get
+// lse2 = +inf, so every P of theirs is exactly 0.
+//
+// Both kernels share one structure (the template parameter SIDE picks the operand roles):
+//   warp 0      producer: claims items, loads the item's two fixed tiles (K_j, V_j | Q_i, dO_i)
+//               and streams the partner tiles (Q_i, dO_i | K_j, V_j) through a ring (TMA, 128B
+//               swizzle); for dkdv the partner's lse2 / delta vectors ride along (bulk copy).
+//   warp 1      MMA issuer (one thread).
+//   warp 2      TMEM allocator: S at [0,128), dP at [128,256), accumulators at 256 (+D).
+//   warps 4-11  elementwise engine: warp w owns TMEM lanes 32*(w%4).. and column half w/8.
+//               P and dS are written back as packed bf16 into their own half's columns
+//               ([64h, 64h+32) of S / dP), which the TS MMAs read as the A operand.
+// Mask bits: partial tiles only (full tiles skip them), 8 B per row and half from tile-major
+// bitmaps — the forward's row bitmaps for dq, the transposed column bitmaps for dkdv.
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdint>
+#include <numeric>
+#include <vector>
+
+#include "bbm_internal.h"
+#include "bbm_ptx.cuh"
+#include "bbm_tmap.h"
+
+namespace bbm {
+namespace {
+
+using namespace ptx;
+
+enum Side : int { kSideDQ = 0, kSideDKDV = 1 };
+
+constexpr uint32_t kThreads = 384;
+constexpr uint32_t kQueue = 4;
+constexpr uint32_t kEnd = 0xFFFFFFFFu;
+constexpr uint32_t kBoxBytes = 128 * 64 * 2;
+constexpr float kLog2e = 1.4426950408889634f;
+
+struct BwdParams {
+  uint64_t n;
+  uint32_t slots, tiles;      // items = slots * tiles (tiles = key tiles | query row tiles)
+  uint32_t partners;          // dense mode: every tile has this many partners
+  uint32_t total_items;
+  float sl2, scale;
+  bool all_tiles;             // dense variant: every partner, no mask
+  const uint32_t* cnt;        // [tiles] list lengths (list mode)
+  const uint32_t* list;       // [tiles][stride] partner entries, bit 31 = full
+  uint32_t list_stride;
+  const uint32_t* order;      // [tiles] LPT order
+  const uint4* bitmaps;       // list-position tile-major bits (row bitmaps | transposed)
+  const float* lse2;          // [slots][rows_pad]
+  const float* delta;         // [slots][rows_pad]
+  uint32_t rows_pad;          // krows * 128
+  uint32_t* ctr;              // [2] next item, finished CTAs
+  __nv_bfloat16* out0;        // dq | dk
+  __nv_bfloat16* out1;        // -  | dv
+};
+
+struct ItemDesc {
+  uint32_t t, slot, tile, nt;
+};
+
+template <int D, int SIDE>
+struct BCfg {
+  static constexpr uint32_t kBoxes = D / 64;
+  static constexpr uint32_t kTileBytes = kBoxes * kBoxBytes;
+  static constexpr uint32_t kVecBytes = SIDE == kSideDKDV ? 1024 : 0;  // lse2 | delta of 128 rows
+  static constexpr uint32_t kStageBytes = 2 * kTileBytes + (SIDE == kSideDKDV ? 1024 : 0);
+  static constexpr uint32_t kStageAlloc = (kStageBytes + 1023) / 1024 * 1024;
+  static constexpr uint32_t kStages = D == 64 ? 4 : 2;
+  static constexpr uint32_t kAcc0 = 256;      // dQ | dK
+  static constexpr uint32_t kAcc1 = 256 + D;  // dV
+};
+
+struct BwdCtl {
+  uint64_t fixed_full, fixed_empty, s_full, p_full, acc_full, acc_empty;
+  uint64_t ring_full[4], ring_empty[4];
+  uint64_t item_full[kQueue], item_empty[kQueue];
+  ItemDesc items[kQueue];
+  uint32_t tmem_base;
+};
+
+template <int D, int SIDE>
+constexpr uint32_t bwd_smem_bytes() {
+  using C = BCfg<D, SIDE>;
+  return 2 * C::kTileBytes + C::kStages * C::kStageAlloc + sizeof(BwdCtl);
+}
+
+__device__ __forceinline__ ItemDesc bwd_decode(const BwdParams& p, uint32_t t) {
+  ItemDesc d{};
+  if (t >= p.total_items) {
+    d.t = kEnd;
+    return d;
+  }
+  d.t = t;
+  d.slot = t / p.tiles;
+  d.tile = p.order[t - d.slot * p.tiles];
+  d.nt = p.all_tiles ? p.partners : p.cnt[d.tile];
+  return d;
+}
+
+__device__ __forceinline__ uint32_t bwd_entry(const BwdParams& p, uint32_t tile, uint32_t j) {
+  return p.all_tiles ? j : p.list[static_cast<uint64_t>(tile) * p.list_stride + j];
+}
+
+// 1-D bulk copy global -> shared, completion on an mbarrier (16-byte aligned, multiple of 16 B)
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(src)), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+template <int D, int SIDE>
+__global__ void __launch_bounds__(kThreads, 1)
+    attn_bwd_kernel(const __grid_constant__ CUtensorMap tm_f0, const __grid_constant__ CUtensorMap tm_f1,
+                    const __grid_constant__ CUtensorMap tm_s0, const __grid_constant__ CUtensorMap tm_s1,
+                    const BwdParams p) {
+  // fixed tiles f0, f1: (Q_i, dO_i) for dq, (K_j, V_j) for dkdv; streamed s0, s1: the partner's
+  // (K_j, V_j) for dq, (Q_i, dO_i) for dkdv.
+  using C = BCfg<D, SIDE>;
+  extern __shared__ __align__(1024) uint8_t smem[];
+  uint8_t* fixed = smem;                       // [2][tile]
+  uint8_t* ring = smem + 2 * C::kTileBytes;    // [kStages][stage]
+  auto* ctl = reinterpret_cast<BwdCtl*>(ring + C::kStages * C::kStageAlloc);
+  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if ((smem_u32(smem) & 1023u) != 0) __trap();
+
+  if (threadIdx.x == 0) {
+    mbar_init(&ctl->fixed_full, 1);
+    mbar_init(&ctl->fixed_empty, 1);
+    mbar_init(&ctl->s_full, 1);
+    mbar_init(&ctl->p_full, 256);
+    mbar_init(&ctl->acc_full, 1);
+    mbar_init(&ctl->acc_empty, 256);
+    for (uint32_t r = 0; r < C::kStages; ++r) {
+      mbar_init(&ctl->ring_full[r], 1);
+      mbar_init(&ctl->ring_empty[r], 1);
+    }
+    for (uint32_t r = 0; r < kQueue; ++r) {
+      mbar_init(&ctl->item_full[r], 1);
+      mbar_init(&ctl->item_empty[r], 2);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tm_f0);
+    tma_prefetch_desc(&tm_f1);
+    tma_prefetch_desc(&tm_s0);
+    tma_prefetch_desc(&tm_s1);
+  }
+  if (warp == 2) {
+    tmem_alloc<512>(&ctl->tmem_base);
+    tmem_relinquish();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = ctl->tmem_base;
+
+  if (warp == 0) {
+    // ------------------------------------------------------------------ producer
+    if (lane == 0) {
+      const uint64_t pol_fixed = policy_evict_first();
+      const uint64_t pol_stream = policy_evict_last();
+      uint32_t r = 0, rph = 1, qi = 0, qiph = 1, fph = 1;
+      for (;;) {
+        const ItemDesc d = bwd_decode(p, atomicAdd(&p.ctr[0], 1u));
+        mbar_wait(&ctl->item_empty[qi], qiph);
+        ctl->items[qi] = d;
+        mbar_arrive(&ctl->item_full[qi]);
+        if (++qi == kQueue) { qi = 0; qiph ^= 1; }
+        if (d.t == kEnd) break;
+        if (d.nt == 0) continue;
+        mbar_wait(&ctl->fixed_empty, fph);
+        fph ^= 1;
+        mbar_arrive_expect_tx(&ctl->fixed_full, 2 * C::kTileBytes);
+        for (uint32_t b = 0; b < C::kBoxes; ++b) {
+          tma_load_3d(fixed + b * kBoxBytes, &tm_f0, &ctl->fixed_full, b * 64, d.tile * 128, d.slot, pol_fixed);
+          tma_load_3d(fixed + C::kTileBytes + b * kBoxBytes, &tm_f1, &ctl->fixed_full, b * 64,
+                      d.tile * 128, d.slot, pol_fixed);
+        }
+        for (uint32_t j = 0; j < d.nt; ++j) {
+          const uint32_t u = bwd_entry(p, d.tile, j) & 0x7FFFFFFFu;
+          mbar_wait(&ctl->ring_empty[r], rph);
+          uint64_t* full = &ctl->ring_full[r];
+          uint8_t* st = ring + r * C::kStageAlloc;
+          mbar_arrive_expect_tx(full, C::kStageBytes);
+          for (uint32_t b = 0; b < C::kBoxes; ++b) {
+            tma_load_3d(st + b * kBoxBytes, &tm_s0, full, b * 64, u * 128, d.slot, pol_stream);
+            tma_load_3d(st + C::kTileBytes + b * kBoxBytes, &tm_s1, full, b * 64, u * 128, d.slot,
+                        pol_stream);
+          }
+          if constexpr (SIDE == kSideDKDV) {
+            const uint64_t off = static_cast<uint64_t>(d.slot) * p.rows_pad + u * 128;
+            bulk_load(st + 2 * C::kTileBytes, p.lse2 + off, 512, full);
+            bulk_load(st + 2 * C::kTileBytes + 512, p.delta + off, 512, full);
+          }
+          if (++r == C::kStages) { r = 0; rph ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------------ MMA issuer
+    if (lane == 0) {
+      constexpr uint32_t idesc_s = make_idesc_bf16(128, 128, false, false);
+      constexpr uint32_t idesc_acc = make_idesc_bf16(128, D, false, true);
+      const uint32_t faddr = smem_u32(fixed), raddr = smem_u32(ring);
+      uint32_t qi = 0, qiph = 0, r = 0, rph = 0, fph = 0, pph = 0, aph = 1;
+      for (;;) {
+        mbar_wait(&ctl->item_full[qi], qiph);
+        const ItemDesc it = ctl->items[qi];
+        mbar_arrive(&ctl->item_empty[qi]);
+        if (++qi == kQueue) { qi = 0; qiph ^= 1; }
+        if (it.t == kEnd) break;
+        if (it.nt == 0) continue;
+        mbar_wait(&ctl->fixed_full, fph);
+        fph ^= 1;
+        for (uint32_t j = 0; j < it.nt; ++j) {
+          mbar_wait(&ctl->ring_full[r], rph);
+          tc_fence_after();
+          const uint32_t sbase = raddr + r * C::kStageAlloc;
+          // S (or S^T) = f0 s0^T, dP (or dP^T) = f1 s1^T: both operands K-major, K = D
+#pragma unroll
+          for (uint32_t kk = 0; kk < D / 16; ++kk) {
+            const uint32_t off = (kk / 4) * kBoxBytes + (kk % 4) * 32;
+            umma_ss(tmem, make_sdesc_sw128(faddr + off, 16, 1024), make_sdesc_sw128(sbase + off, 16, 1024),
+                    idesc_s, kk > 0);
+          }
+#pragma unroll
+          for (uint32_t kk = 0; kk < D / 16; ++kk) {
+            const uint32_t off = (kk / 4) * kBoxBytes + (kk % 4) * 32;
+            umma_ss(tmem + 128, make_sdesc_sw128(faddr + C::kTileBytes + off, 16, 1024),
+                    make_sdesc_sw128(sbase + C::kTileBytes + off, 16, 1024), idesc_s, kk > 0);
+          }
+          tc_commit(&ctl->s_full);
+          if (j + 1 == it.nt) tc_commit(&ctl->fixed_empty);
+          mbar_wait(&ctl->p_full, pph);
+          pph ^= 1;
+          if (j == 0) {
+            mbar_wait(&ctl->acc_empty, aph);  // previous item's epilogue has read the accumulators
+            aph ^= 1;
+          }
+          tc_fence_after();
+          // packed bf16 A operand: half h's 32 columns at [64h, 64h+32) of its region; K step kk
+          // (16 partner rows = 8 packed columns) -> column (kk/4)*64 + (kk%4)*8
+#pragma unroll
+          for (uint32_t kk = 0; kk < 8; ++kk) {
+            const uint32_t acol = (kk / 4) * 64 + (kk % 4) * 8;
+            // dQ += dS K_j  |  dK += dS^T Q_i   (B = streamed tile 0, MN-major)
+            umma_ts(tmem + C::kAcc0, tmem + 128 + acol,
+                    make_sdesc_sw128(sbase + kk * 2048, kBoxBytes, 1024), idesc_acc, (j > 0 || kk > 0) ? 1u : 0u);
+            if constexpr (SIDE == kSideDKDV)  // dV += P^T dO_i   (B = streamed tile 1)
+              umma_ts(tmem + C::kAcc1, tmem + acol,
+                      make_sdesc_sw128(sbase + C::kTileBytes + kk * 2048, kBoxBytes, 1024), idesc_acc,
+                      (j > 0 || kk > 0) ? 1u : 0u);
+          }
+          tc_commit(&ctl->ring_empty[r]);
+          if (++r == C::kStages) { r = 0; rph ^= 1; }
+        }
+        tc_commit(&ctl->acc_full);
+      }
+    }
+  } else if (warp >= 4) {
+    // ------------------------------------------------------------------ elementwise engine
+    const uint32_t half = warp >= 8 ? 1u : 0u;
+    const uint32_t quad = warp & 3;
+    const uint32_t row = quad * 32 + lane;  // TMEM lane: key (dkdv) or query (dq) in the tile
+    const uint32_t lane_off = (quad * 32) << 16;
+    const bool leader = warp == 4 && lane == 0;
+    const float sl2 = p.sl2;
+    uint32_t qi = 0, qiph = 0, sph = 0, acph = 0, r = 0;
+    const uint32_t last = (static_cast<uint32_t>(p.n) + 127) / 128 - 1;
+    const int valid_last = static_cast<int>(p.n - static_cast<uint64_t>(last) * 128) - static_cast<int>(half * 64);
+    for (;;) {
+      mbar_wait(&ctl->item_full[qi], qiph);
+      const ItemDesc it = ctl->items[qi];
+      named_bar_sync(1, 256);
+      if (leader) mbar_arrive(&ctl->item_empty[qi]);
+      if (++qi == kQueue) { qi = 0; qiph ^= 1; }
+      if (it.t == kEnd) break;
+      const uint64_t grow = static_cast<uint64_t>(it.tile) * 128 + row;
+      if (it.nt > 0) {
+        float my_lse = 0.0f, my_delta = 0.0f;
+        if constexpr (SIDE == kSideDQ) {
+          const uint64_t o = static_cast<uint64_t>(it.slot) * p.rows_pad + grow;
+          my_lse = p.lse2[o];
+          my_delta = p.delta[o];
+        }
+        for (uint32_t j = 0; j < it.nt; ++j) {
+          const uint32_t e = bwd_entry(p, it.tile, j);
+          const uint32_t u = e & 0x7FFFFFFFu;
+          bool masked;
+          uint2 bits = make_uint2(0xFFFFFFFFu, 0xFFFFFFFFu);
+          if (p.all_tiles) {
+            // dense: only the dq side has a ragged key edge (its columns are keys); rows past n
+            // on the dkdv side carry lse2 = +inf
+            masked = SIDE == kSideDQ && u == last && valid_last < 64;
+            if (masked) {
+              const int v = valid_last;
+              bits.x = v >= 32 ? 0xFFFFFFFFu : (v <= 0 ? 0u : ((1u << v) - 1u));
+              bits.y = v >= 64 ? 0xFFFFFFFFu : (v <= 32 ? 0u : ((1u << (v - 32)) - 1u));
+            }
+          } else {
+            masked = (e & 0x80000000u) == 0;
+            if (masked)
+              bits = __ldg(reinterpret_cast<const uint2*>(
+                                p.bitmaps + (static_cast<uint64_t>(it.tile) * p.list_stride + j) * 128 + row) +
+                            half);
+          }
+          mbar_wait(&ctl->s_full, sph);
+          sph ^= 1;
+          tc_fence_after();
+          const uint32_t ts = tmem + lane_off + half * 64;
+          const float* vec = nullptr;
+          if constexpr (SIDE == kSideDKDV)
+            vec = reinterpret_cast<const float*>(ring + r * C::kStageAlloc + 2 * C::kTileBytes) + half * 64;
+#pragma unroll
+          for (uint32_t c32 = 0; c32 < 2; ++c32) {
+            uint32_t s[32], dp[32];
+            tmem_ld32(ts + c32 * 32, s);
+            tmem_ld32(ts + 128 + c32 * 32, dp);
+            tmem_ld_wait();
+            const uint32_t mw = c32 ? bits.y : bits.x;
+            uint32_t pk[16], dk[16];
+#pragma unroll
+            for (uint32_t i = 0; i < 32; i += 2) {
+              float l0 = my_lse, l1 = my_lse, d0 = my_delta, d1 = my_delta;
+              if constexpr (SIDE == kSideDKDV) {
+                const float2 lv = *reinterpret_cast<const float2*>(vec + c32 * 32 + i);
+                const float2 dv = *reinterpret_cast<const float2*>(vec + 128 + c32 * 32 + i);
+                l0 = lv.x, l1 = lv.y, d0 = dv.x, d1 = dv.y;
+              }
+              float p0 = fast_exp2(__uint_as_float(s[i]) * sl2 - l0);
+              float p1 = fast_exp2(__uint_as_float(s[i + 1]) * sl2 - l1);
+              if (masked) {
+                p0 = ((mw >> i) & 1u) ? p0 : 0.0f;
+                p1 = ((mw >> (i + 1)) & 1u) ? p1 : 0.0f;
+              }
+              const float g0 = p0 * (__uint_as_float(dp[i]) - d0);
+              const float g1 = p1 * (__uint_as_float(dp[i + 1]) - d1);
+              pk[i / 2] = pack_bf16x2(p0, p1);
+              dk[i / 2] = pack_bf16x2(g0, g1);
+            }
+            tmem_st16(ts + c32 * 16, pk);        // P over this half's own S columns
+            tmem_st16(ts + 128 + c32 * 16, dk);  // dS over this half's own dP columns
+          }
+          tmem_st_wait();
+          tc_fence_before();
+          mbar_arrive(&ctl->p_full);
+          if (++r == C::kStages) r = 0;
+        }
+        // epilogue: accumulators -> bf16 rows (dq * scale | dk * scale, dv)
+        mbar_wait(&ctl->acc_full, acph);
+        acph ^= 1;
+        tc_fence_after();
+      }
+      constexpr uint32_t kHalf = D / 2;
+      const bool in = grow < p.n;
+      const uint64_t obase = (static_cast<uint64_t>(it.slot) * p.n + grow) * D + half * kHalf;
+#pragma unroll
+      for (uint32_t a = 0; a < (SIDE == kSideDKDV ? 2u : 1u); ++a) {
+        __nv_bfloat16* dst = a == 0 ? p.out0 : p.out1;
+        const float mul = a == 0 ? p.scale : 1.0f;
+#pragma unroll
+        for (uint32_t c32 = 0; c32 < kHalf / 32; ++c32) {
+          uint32_t v[32];
+          if (it.nt > 0) {
+            tmem_ld32(tmem + lane_off + (a == 0 ? C::kAcc0 : C::kAcc1) + half * kHalf + c32 * 32, v);
+            tmem_ld_wait();
+          } else {
+#pragma unroll
+            for (uint32_t i = 0; i < 32; ++i) v[i] = 0u;
+          }
+          if (in) {
+            uint4* o = reinterpret_cast<uint4*>(dst + obase + c32 * 32);
+#pragma unroll
+            for (uint32_t w = 0; w < 4; ++w)
+              o[w] = make_uint4(pack_bf16x2(__uint_as_float(v[w * 8 + 0]) * mul, __uint_as_float(v[w * 8 + 1]) * mul),
+                                pack_bf16x2(__uint_as_float(v[w * 8 + 2]) * mul, __uint_as_float(v[w * 8 + 3]) * mul),
+                                pack_bf16x2(__uint_as_float(v[w * 8 + 4]) * mul, __uint_as_float(v[w * 8 + 5]) * mul),
+                                pack_bf16x2(__uint_as_float(v[w * 8 + 6]) * mul, __uint_as_float(v[w * 8 + 7]) * mul));
+          }
+        }
+      }
+      if (it.nt > 0) {
+        tc_fence_before();
+        mbar_arrive(&ctl->acc_empty);
+      }
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) tmem_dealloc<512>(tmem);
+  if (threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(&p.ctr[1], 1u) == gridDim.x - 1) {
+      p.ctr[0] = 0;
+      p.ctr[1] = 0;
+      __threadfence();
+    }
+  }
+}
+
+// delta = rowsum(dO * O) (engine.hpp:366-372), lse2 = (row_max + ln row_sum) * log2(e); rows with
+// row_sum == 0 (fully masked) and rows past n: lse2 = +inf (their P is 0), delta = 0.
+// One warp per row.
+template <typename OT>
+__global__ void rowstats_kernel(const OT* __restrict__ o, const __nv_bfloat16* __restrict__ dout,
+                                const float* __restrict__ row_max, const float* __restrict__ row_sum,
+                                uint64_t slots, uint64_t n, uint32_t d, uint32_t rows_pad,
+                                float* __restrict__ lse2, float* __restrict__ delta) {
+  const uint64_t total = slots * rows_pad;
+  const uint32_t lane = threadIdx.x & 31;
+  for (uint64_t w = (blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x) >> 5; w < total;
+       w += (static_cast<uint64_t>(gridDim.x) * blockDim.x) >> 5) {
+    const uint64_t slot = w / rows_pad, r = w % rows_pad;
+    float acc = 0.0f, l = INFINITY;
+    if (r < n) {
+      const uint64_t base = (slot * n + r) * d;
+      for (uint32_t c = lane; c < d; c += 32) {
+        float ov;
+        if constexpr (sizeof(OT) == 4) ov = o[base + c];
+        else ov = __bfloat162float(o[base + c]);
+        acc += ov * __bfloat162float(dout[base + c]);
+      }
+      const float rs = row_sum[slot * n + r];
+      if (rs > 0.0f) l = (row_max[slot * n + r] + logf(rs)) * kLog2e;
+    }
+#pragma unroll
+    for (uint32_t m = 16; m; m >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, m);
+    if (lane == 0) {
+      lse2[w] = l;
+      delta[w] = r < n ? acc : 0.0f;
+    }
+  }
+}
+
+// Column lists: for key tile q, the ascending occupied query row tiles (bit 31 = full, never on
+// a ragged tile). One CTA (256 threads) per column tile.
+__global__ void __launch_bounds__(256) collist_kernel(const uint32_t* __restrict__ sums, uint64_t n,
+                                                      uint32_t krows, uint32_t kcols,
+                                                      uint32_t* __restrict__ col_list,
+                                                      uint32_t* __restrict__ col_cnt) {
+  __shared__ uint32_t warp_cnt[8];
+  const uint32_t q = blockIdx.x, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint32_t base = 0;
+  for (uint32_t p0 = 0; p0 < krows; p0 += 256) {
+    const uint32_t pr = p0 + threadIdx.x;
+    const uint32_t s = pr < krows ? sums[static_cast<uint64_t>(pr) * kcols + q] : 0u;
+    const bool o = s > 0;
+    const uint32_t ballot = __ballot_sync(0xffffffffu, o);
+    if (lane == 0) warp_cnt[warp] = __popc(ballot);
+    __syncthreads();
+    uint32_t before = base;
+    for (uint32_t w = 0; w < warp; ++w) before += warp_cnt[w];
+    before += __popc(ballot & ((1u << lane) - 1u));
+    const bool full = s == 128u * 128u && (static_cast<uint64_t>(pr) + 1) * 128 <= n &&
+                      (static_cast<uint64_t>(q) + 1) * 128 <= n;
+    if (o) col_list[static_cast<uint64_t>(q) * krows + before] = pr | (full ? 0x80000000u : 0u);
+    for (uint32_t w = 0; w < 8; ++w) base += warp_cnt[w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) col_cnt[q] = base;
+}
+
+// Transposed bits of every occupied tile at its column-list position: CTA (q, k), 4 warps; warp w
+// holds query rows 32w..32w+31 of the tile and emits, per key c, the ballot of their bit c.
+__global__ void __launch_bounds__(128) transpose_bitmaps_kernel(const uint4* __restrict__ mask,
+                                                                uint32_t krows, uint32_t kcols,
+                                                                const uint32_t* __restrict__ col_list,
+                                                                const uint32_t* __restrict__ col_cnt,
+                                                                uint4* __restrict__ tbits) {
+  const uint32_t q = blockIdx.y, k = blockIdx.x;
+  if (k >= col_cnt[q]) return;
+  const uint32_t pr = col_list[static_cast<uint64_t>(q) * krows + k] & 0x7FFFFFFFu;
+  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint4 rowbits = mask[(static_cast<uint64_t>(pr) * 128 + warp * 32 + lane) * kcols + q];
+  uint32_t* out = reinterpret_cast<uint32_t*>(tbits + (static_cast<uint64_t>(q) * krows + k) * 128);
+  const uint32_t words[4] = {rowbits.x, rowbits.y, rowbits.z, rowbits.w};
+#pragma unroll
+  for (uint32_t wd = 0; wd < 4; ++wd)
+#pragma unroll 8
+    for (uint32_t b = 0; b < 32; ++b) {
+      const uint32_t col = __ballot_sync(0xffffffffu, (words[wd] >> b) & 1u);
+      if (lane == 0) out[(wd * 32 + b) * 4 + warp] = col;
+    }
+}
+
+template <int D, int SIDE>
+void launch_side(const Prep& prep, const BwdArgs& a, const float* lse2, const float* delta, uint32_t rows_pad,
+                 cudaStream_t s, int num_sms) {
+  static_assert(bwd_smem_bytes<D, SIDE>() <= 232448, "exceeds the 227 KB opt-in shared memory");
+  const KernelMeta& km = prep.kmeta;
+  const BwdMeta& bm = prep.bwd;
+  BwdParams p{};
+  p.n = a.n;
+  p.slots = static_cast<uint32_t>(a.slots);
+  p.all_tiles = a.variant == 0;
+  p.sl2 = a.scale * kLog2e;
+  p.scale = a.scale;
+  p.lse2 = lse2;
+  p.delta = delta;
+  p.rows_pad = rows_pad;
+  if (SIDE == kSideDQ) {
+    p.tiles = km.krows;
+    p.partners = km.kcols;
+    p.cnt = km.row_cnt;
+    p.list = km.list;
+    p.list_stride = km.kcols;
+    p.order = p.all_tiles ? bm.all_order : km.order;
+    p.bitmaps = km.bitmaps;
+    p.ctr = bm.ctr;
+    p.out0 = static_cast<__nv_bfloat16*>(a.dq);
+  } else {
+    p.tiles = km.kcols;
+    p.partners = km.krows;
+    p.cnt = bm.col_cnt;
+    p.list = bm.col_list;
+    p.list_stride = km.krows;
+    p.order = p.all_tiles ? bm.all_order : bm.col_order;
+    p.bitmaps = bm.tbitmaps;
+    p.ctr = bm.ctr + 2;
+    p.out0 = static_cast<__nv_bfloat16*>(a.dk);
+    p.out1 = static_cast<__nv_bfloat16*>(a.dv);
+  }
+  p.total_items = static_cast<uint32_t>(a.slots * p.tiles);
+  const CUtensorMap tq = make_tmap_bf16_3d(a.q, D, a.n, a.slots, 64, 128);
+  const CUtensorMap tk = make_tmap_bf16_3d(a.k, D, a.n, a.slots, 64, 128);
+  const CUtensorMap tv = make_tmap_bf16_3d(a.v, D, a.n, a.slots, 64, 128);
+  const CUtensorMap tdo = make_tmap_bf16_3d(a.d_out, D, a.n, a.slots, 64, 128);
+  static bool attr = false;
+  if (!attr) {
+    BBM_CUDA(cudaFuncSetAttribute(attn_bwd_kernel<D, SIDE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  bwd_smem_bytes<D, SIDE>()));
+    attr = true;
+  }
+  const uint32_t grid = std::min<uint32_t>(p.total_items, static_cast<uint32_t>(num_sms));
+  if (SIDE == kSideDQ)
+    attn_bwd_kernel<D, SIDE><<<grid, kThreads, bwd_smem_bytes<D, SIDE>(), s>>>(tq, tdo, tk, tv, p);
+  else
+    attn_bwd_kernel<D, SIDE><<<grid, kThreads, bwd_smem_bytes<D, SIDE>(), s>>>(tk, tv, tq, tdo, p);
+  BBM_CUDA(cudaGetLastError());
+}
+
+template <class T>
+T* bwd_alloc(uint64_t count) {
+  void* ptr = nullptr;
+  BBM_CUDA(cudaMalloc(&ptr, std::max<uint64_t>(1, count) * sizeof(T)));
+  return static_cast<T*>(ptr);
+}
+
+}  // namespace
+
+void free_bwd_meta(BwdMeta& b) {
+  cudaFree(b.col_cnt);
+  cudaFree(b.col_list);
+  cudaFree(b.col_order);
+  cudaFree(b.all_order);
+  cudaFree(b.tbitmaps);
+  cudaFree(b.ctr);
+  cudaFree(b.rowws);
+  b = BwdMeta{};
+}
+
+void build_bwd_meta(Prep& prep, cudaStream_t s) {
+  BwdMeta& b = prep.bwd;
+  if (b.built) return;
+  const KernelMeta& km = prep.kmeta;
+  const uint32_t kr = km.krows, kc = km.kcols;
+  if (!b.col_cnt) {
+    b.col_cnt = bwd_alloc<uint32_t>(kc);
+    b.col_list = bwd_alloc<uint32_t>(static_cast<uint64_t>(kc) * kr);
+    b.col_order = bwd_alloc<uint32_t>(kc);
+    b.all_order = bwd_alloc<uint32_t>(std::max(kr, kc));
+    b.tbitmaps = bwd_alloc<uint4>(static_cast<uint64_t>(kc) * kr * 128);
+    b.ctr = bwd_alloc<uint32_t>(4);
+    BBM_CUDA(cudaMemsetAsync(b.ctr, 0, 16, s));
+    std::vector<uint32_t> ident(std::max(kr, kc));
+    std::iota(ident.begin(), ident.end(), 0u);
+    BBM_CUDA(cudaMemcpyAsync(b.all_order, ident.data(), ident.size() * 4, cudaMemcpyHostToDevice, s));
+    BBM_CUDA(cudaStreamSynchronize(s));
+  }
+  collist_kernel<<<kc, 256, 0, s>>>(km.sums, prep.n, kr, kc, b.col_list, b.col_cnt);
+  BBM_CUDA(cudaGetLastError());
+  transpose_bitmaps_kernel<<<dim3(kr, kc), 128, 0, s>>>(reinterpret_cast<const uint4*>(km.mask), kr, kc,
+                                                         b.col_list, b.col_cnt, b.tbitmaps);
+  BBM_CUDA(cudaGetLastError());
+  // LPT order of the columns (longest list first, ties by index), like the forward's row order
+  std::vector<uint32_t> cnt(kc), order(kc);
+  BBM_CUDA(cudaMemcpyAsync(cnt.data(), b.col_cnt, kc * 4, cudaMemcpyDeviceToHost, s));
+  BBM_CUDA(cudaStreamSynchronize(s));
+  std::iota(order.begin(), order.end(), 0u);
+  std::stable_sort(order.begin(), order.end(), [&](uint32_t x, uint32_t y) { return cnt[x] > cnt[y]; });
+  BBM_CUDA(cudaMemcpyAsync(b.col_order, order.data(), kc * 4, cudaMemcpyHostToDevice, s));
+  BBM_CUDA(cudaStreamSynchronize(s));
+  b.built = true;
+}
+
+void launch_attn_bwd(const Prep& prep, const BwdArgs& a, cudaStream_t s, int num_sms) {
+  require(a.slots >= 1, "need at least one batch/head slot");
+  require(a.n == prep.n, "mask preprocessing does not match this problem");
+  require(prep.bwd.built, "backward metadata not built");
+  if (a.d != 64 && a.d != 128) throw ArgError("head dim must be 64 or 128 on the sm_100a kernel");
+  const uint32_t rows_pad = prep.kmeta.krows * 128;
+  const size_t need = 2 * static_cast<size_t>(a.slots) * rows_pad;
+  const BwdMeta& b = prep.bwd;
+  if (need > b.rowws_floats) {
+    cudaFree(b.rowws);
+    b.rowws = nullptr;
+    BBM_CUDA(cudaMalloc(&b.rowws, need * sizeof(float)));
+    b.rowws_floats = need;
+  }
+  float* lse2 = b.rowws;
+  float* delta = b.rowws + static_cast<size_t>(a.slots) * rows_pad;
+  const uint64_t warps = a.slots * rows_pad;
+  const unsigned grid = static_cast<unsigned>(std::min<uint64_t>((warps + 7) / 8, 148ull * 64));
+  if (a.o_f32)
+    rowstats_kernel<float><<<grid, 256, 0, s>>>(static_cast<const float*>(a.o),
+                                                static_cast<const __nv_bfloat16*>(a.d_out), a.row_max,
+                                                a.row_sum, a.slots, a.n, a.d, rows_pad, lse2, delta);
+  else
+    rowstats_kernel<__nv_bfloat16><<<grid, 256, 0, s>>>(
+        static_cast<const __nv_bfloat16*>(a.o), static_cast<const __nv_bfloat16*>(a.d_out), a.row_max,
+        a.row_sum, a.slots, a.n, a.d, rows_pad, lse2, delta);
+  BBM_CUDA(cudaGetLastError());
+  if (a.d == 64) {
+    launch_side<64, kSideDKDV>(prep, a, lse2, delta, rows_pad, s, num_sms);
+    launch_side<64, kSideDQ>(prep, a, lse2, delta, rows_pad, s, num_sms);
+  } else {
+    launch_side<128, kSideDKDV>(prep, a, lse2, delta, rows_pad, s, num_sms);
+    launch_side<128, kSideDQ>(prep, a, lse2, delta, rows_pad, s, num_sms);
+  }
+}
+
+}  // namespace bbm

@@ -905,6 +905,7 @@ void launch_attn_fwd(const Prep& prep, const AttnArgs& a, cudaStream_t s, int nu
   require(a.n == prep.n, "mask preprocessing does not match this problem");
   require(a.slots < (1ull << 24), "too many slots for one launch");
   if (a.slots * prep.kmeta.krows == 0) return;
+  refresh_kernel_view(prep, s);
   if (a.d == 64) launch_d<64>(prep, a, s, num_sms);
   else if (a.d == 128) launch_d<128>(prep, a, s, num_sms);
   else throw ArgError("head dim must be 64 or 128 on the sm_100a kernel");

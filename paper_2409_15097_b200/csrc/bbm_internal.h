@@ -81,12 +81,32 @@ struct LaunchPlan {
   uint32_t* empty_list = nullptr;
 };
 
+// Backward metadata (built on first backward use, attn_bwd.cu): the column view of the kernel
+// tiles — for key tile q, the ascending occupied query row tiles (bit 31 = full tile), LPT order
+// of the columns, and every occupied tile's mask bits TRANSPOSED (key-major) at its column-list
+// position: key row c of column entry (q, k) at (q*krows + k)*128 + c (16 bytes over queries).
+struct BwdMeta {
+  bool built = false;
+  uint32_t* col_cnt = nullptr;   // [kcols]
+  uint32_t* col_list = nullptr;  // [kcols][krows]
+  uint32_t* col_order = nullptr; // [kcols]
+  uint32_t* all_order = nullptr; // [max(krows,kcols)] identity order (dense mode)
+  uint4* tbitmaps = nullptr;     // [kcols*krows][128]
+  uint32_t* ctr = nullptr;       // [4] dynamic item counters + finished CTAs (dq / dkdv kernels)
+  mutable float* rowws = nullptr;  // [slots][krows*128] x 2: lse2 | delta
+  mutable size_t rowws_floats = 0;
+};
+
 struct Prep {
   int device = 0;
   uint64_t n = 0;
   SpecMeta spec;     // the caller's BlockSpec
   KernelMeta kmeta;  // the kernel's 128x128 view
-  std::vector<uint32_t> h_row_cnt;  // host copy of kmeta.row_cnt (scheduling + tests)
+  mutable std::vector<uint32_t> h_row_cnt;  // host copy of kmeta.row_cnt (scheduling + tests)
+  // set by the asynchronous kernel-view rebuilds (bbm_prep_update_*): the host row counts, the
+  // cached launch plans and the backward's column view are refreshed at the next launch
+  mutable bool kview_stale = false;
+  BwdMeta bwd;                      // column view for the backward (lazy)
   uint32_t* work_ctr = nullptr;     // device [2]: dynamic item counter, finished CTAs
   // launch plans and the split-KV workspace are built on first use (not thread-safe: one
   // launch at a time per prep, like the reference's single-threaded callers)
@@ -156,6 +176,31 @@ struct TraceConfig {
 extern TraceConfig g_trace;
 
 void launch_attn_fwd(const Prep& prep, const AttnArgs& a, cudaStream_t s, int num_sms);
+
+// ---- attention backward (attn_bwd.cu) ----
+struct BwdArgs {
+  const void* q;  // bf16 [slots][n][d]
+  const void* k;
+  const void* v;
+  const void* o;        // forward output: bf16 (o_f32 == false) or fp32 [slots][n][d]
+  bool o_f32;
+  const float* row_max;  // [slots][n] natural-log units (ForwardResult::row_max)
+  const float* row_sum;  // [slots][n]
+  const void* d_out;     // bf16 [slots][n][d]
+  void* dq;              // bf16 [slots][n][d]
+  void* dk;
+  void* dv;
+  uint64_t slots;
+  uint64_t n;
+  uint32_t d;
+  float scale;
+  int variant;
+};
+void build_bwd_meta(Prep& prep, cudaStream_t s);  // idempotent
+void launch_attn_bwd(const Prep& prep, const BwdArgs& a, cudaStream_t s, int num_sms);
+void free_bwd_meta(BwdMeta& b);
+// refresh host row counts / plans after bbm_prep_update_* (synchronizes `s` once)
+void refresh_kernel_view(const Prep& prep, cudaStream_t s);
 int attn_fwd_kernel_launches_per_call();
 
 }  // namespace bbm

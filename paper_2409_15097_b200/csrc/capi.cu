@@ -199,6 +199,7 @@ Prep::~Prep() {
   cudaGetDevice(&prev);
   cudaSetDevice(device);
   free_kernel_meta(kmeta);
+  free_bwd_meta(bwd);
   cudaFree(work_ctr);
   cudaFree(workspace);
   for (auto& kv : plans) {
@@ -208,6 +209,25 @@ Prep::~Prep() {
     cudaFree(kv.second.empty_list);
   }
   if (prev >= 0) cudaSetDevice(prev);
+}
+
+void refresh_kernel_view(const Prep& pr, cudaStream_t s) {
+  if (!pr.kview_stale) return;
+  std::vector<uint32_t> cnt(pr.kmeta.krows);
+  BBM_CUDA(cudaMemcpyAsync(cnt.data(), pr.kmeta.row_cnt, cnt.size() * 4, cudaMemcpyDeviceToHost, s));
+  BBM_CUDA(cudaStreamSynchronize(s));
+  if (cnt != pr.h_row_cnt) {
+    for (auto& kv : pr.plans) {
+      cudaFree(kv.second.unit_desc);
+      cudaFree(kv.second.split_info);
+      cudaFree(kv.second.split_ctr);
+      cudaFree(kv.second.empty_list);
+    }
+    pr.plans.clear();
+    pr.h_row_cnt = cnt;
+  }
+  const_cast<Prep&>(pr).bwd.built = false;  // column view follows the new mask on next use
+  pr.kview_stale = false;
 }
 
 }  // namespace bbm
@@ -257,6 +277,15 @@ __global__ void bf16_to_f32_kernel(const __nv_bfloat16* __restrict__ in, float* 
   for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < count;
        i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
     out[i] = __bfloat162float(in[i]);
+}
+
+// Permutation::from_forward (reorder.hpp:57-68): forward must be a bijection on [0, n)
+void check_bijection(const uint32_t* fwd, uint64_t n) {
+  std::vector<char> seen(n, 0);
+  for (uint64_t a = 0; a < n; ++a) {
+    require(fwd[a] < n && !seen[fwd[a]], "forward map is not a bijection");
+    seen[fwd[a]] = 1;
+  }
 }
 
 unsigned grid_of(uint64_t count) {
@@ -347,6 +376,7 @@ bbm_status bbm_prep_update_bool_device(bbm_prep prep, const uint8_t* d_mask, uin
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     launch_pack_bool(d_mask, pr.n, row_stride, pr.kmeta, s);
     build_kernel_view(pr.kmeta, pr.n, s);
+    pr.kview_stale = true;
   });
 }
 
@@ -358,6 +388,7 @@ bbm_status bbm_prep_update_packed_device(bbm_prep prep, const uint64_t* d_words,
     launch_pad_packed(d_words, pr.n, pr.kmeta, s);
     launch_sums128(pr.kmeta, s);
     build_kernel_view(pr.kmeta, pr.n, s);
+    pr.kview_stale = true;
   });
 }
 
@@ -471,6 +502,59 @@ bbm_status bbm_prep_counters(bbm_prep prep, int variant, uint64_t slots, bbm_cou
     c->mask_block_reads = one.mask_block_reads * slots;
     c->skipped_by_binblk = one.skipped_by_binblk * slots;
     c->skipped_mask_reads_by_run = one.skipped_mask_reads_by_run * slots;
+  });
+}
+
+bbm_status bbm_sums_metadata(const uint32_t* sums, uint64_t n, uint64_t bi, uint64_t bj,
+                             int device, uint8_t* occ, uint32_t* offset, uint32_t* total_ones,
+                             bbm_block_stats* stats) {
+  return guarded([&] {
+    validate_spec(n, bi, bj);
+    require(sums != nullptr, "null sums");
+    DeviceGuard g(device);
+    const uint64_t rows = (n + bi - 1) / bi, cols = (n + bj - 1) / bj, tiles = rows * cols;
+    cudaStream_t s;
+    BBM_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    uint32_t* d_sums = dmalloc<uint32_t>(tiles);
+    uint8_t* d_occ = dmalloc<uint8_t>(tiles);
+    uint32_t* d_off = dmalloc<uint32_t>(rows);
+    uint32_t* d_tot = dmalloc<uint32_t>(rows);
+    uint64_t* d_stats = dmalloc<uint64_t>(rows * 3);
+    uint64_t* d_totals = dmalloc<uint64_t>(3);
+    uint64_t totals[3] = {0, 0, 0};
+    auto release = [&] {
+      cudaFree(d_sums);
+      cudaFree(d_occ);
+      cudaFree(d_off);
+      cudaFree(d_tot);
+      cudaFree(d_stats);
+      cudaFree(d_totals);
+      cudaStreamDestroy(s);
+    };
+    try {
+      BBM_CUDA(cudaMemcpyAsync(d_sums, sums, tiles * 4, cudaMemcpyHostToDevice, s));
+      // the same per-row pass and totals the preprocessor runs after its sums kernel
+      launch_rowmeta(d_sums, n, bi, bj, rows, cols, d_occ, d_off, d_tot, d_stats, nullptr, nullptr, s);
+      launch_finalize(d_stats, rows, nullptr, nullptr, d_totals, s);
+      if (occ) BBM_CUDA(cudaMemcpyAsync(occ, d_occ, tiles, cudaMemcpyDeviceToHost, s));
+      if (offset) BBM_CUDA(cudaMemcpyAsync(offset, d_off, rows * 4, cudaMemcpyDeviceToHost, s));
+      if (total_ones) BBM_CUDA(cudaMemcpyAsync(total_ones, d_tot, rows * 4, cudaMemcpyDeviceToHost, s));
+      BBM_CUDA(cudaMemcpyAsync(totals, d_totals, 24, cudaMemcpyDeviceToHost, s));
+      BBM_CUDA(cudaStreamSynchronize(s));
+    } catch (...) {
+      release();
+      throw;
+    }
+    release();
+    if (stats) {
+      // block_stats (mask.hpp:230-247): same double expressions as the reference
+      stats->blocks_total = tiles;
+      stats->blocks_nonzero = totals[0];
+      stats->blocks_full = totals[1];
+      const double nd = static_cast<double>(n);
+      stats->block_density = tiles ? static_cast<double>(totals[0]) / static_cast<double>(tiles) : 0.0;
+      stats->element_density = static_cast<double>(totals[2]) / (nd * nd);
+    }
   });
 }
 
@@ -633,6 +717,101 @@ bbm_status bbm_attn_fwd_host_f32(bbm_prep prep, int variant, const float* q, con
   });
 }
 
+bbm_status bbm_attn_bwd(bbm_prep prep, int variant, const void* q, const void* k, const void* v,
+                        const void* out, const float* row_max, const float* row_sum,
+                        const void* d_out, void* dq, void* dk, void* dv, uint64_t slots,
+                        uint32_t head_dim, double scale, void* stream) {
+  return guarded([&] {
+    Prep& pr = unwrap(prep);
+    check_attn_args(pr, variant, slots, head_dim, scale);
+    require(q && k && v && out && row_max && row_sum && d_out && dq && dk && dv, "null tensor pointer");
+    int dev = 0;
+    BBM_CUDA(cudaGetDevice(&dev));
+    require(dev == pr.device, "prep lives on another device; use bbm_prep_replicate");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    refresh_kernel_view(pr, s);
+    build_bwd_meta(pr, s);
+    BwdArgs a{q, k, v, out, false, row_max, row_sum, d_out, dq, dk, dv, slots, pr.n, head_dim,
+              static_cast<float>(scale), variant};
+    launch_attn_bwd(pr, a, s, sm_count(dev));
+  });
+}
+
+bbm_status bbm_attn_bwd_host_f32(bbm_prep prep, int variant, const float* q, const float* k,
+                                 const float* v, const float* out, const double* row_max,
+                                 const double* row_sum, const float* d_out, float* dq, float* dk,
+                                 float* dv, uint64_t slots, uint32_t head_dim, double scale) {
+  return guarded([&] {
+    Prep& pr = unwrap(prep);
+    check_attn_args(pr, variant, slots, head_dim, scale);
+    require(q && k && v && out && row_max && row_sum && d_out && dq && dk && dv, "null tensor pointer");
+    DeviceGuard g(pr.device);
+    cudaStream_t s;
+    BBM_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    const uint64_t elems = slots * pr.n * head_dim, rows = slots * pr.n;
+    std::vector<void*> owned;
+    auto alloc = [&](uint64_t bytes) {
+      void* p = nullptr;
+      BBM_CUDA(cudaMallocAsync(&p, std::max<uint64_t>(bytes, 16), s));
+      owned.push_back(p);
+      return p;
+    };
+    auto release = [&] {
+      for (void* p : owned) cudaFreeAsync(p, s);
+      cudaStreamSynchronize(s);
+      cudaStreamDestroy(s);
+    };
+    try {
+      float* stage = static_cast<float*>(alloc(elems * 4));
+      float* o32 = static_cast<float*>(alloc(elems * 4));
+      __nv_bfloat16* b[4];
+      for (auto& x : b) x = static_cast<__nv_bfloat16*>(alloc(elems * 2));  // q k v dO
+      __nv_bfloat16* g3[3];
+      for (auto& x : g3) x = static_cast<__nv_bfloat16*>(alloc(elems * 2));  // dq dk dv
+      float* rm = static_cast<float*>(alloc(rows * 4));
+      float* rs = static_cast<float*>(alloc(rows * 4));
+      int* bad = static_cast<int*>(alloc(16));
+      BBM_CUDA(cudaMemsetAsync(bad, 0, 16, s));
+      const float* srcs[4] = {q, k, v, d_out};
+      for (int t = 0; t < 4; ++t) {
+        BBM_CUDA(cudaMemcpyAsync(stage, srcs[t], elems * 4, cudaMemcpyHostToDevice, s));
+        f32_to_bf16_kernel<<<grid_of(elems), 256, 0, s>>>(stage, b[t], elems, bad + t);
+        BBM_CUDA(cudaGetLastError());
+      }
+      BBM_CUDA(cudaMemcpyAsync(o32, out, elems * 4, cudaMemcpyHostToDevice, s));
+      std::vector<float> hm(rows), hs(rows);
+      for (uint64_t i = 0; i < rows; ++i) {
+        hm[i] = static_cast<float>(row_max[i]);
+        hs[i] = static_cast<float>(row_sum[i]);
+      }
+      BBM_CUDA(cudaMemcpyAsync(rm, hm.data(), rows * 4, cudaMemcpyHostToDevice, s));
+      BBM_CUDA(cudaMemcpyAsync(rs, hs.data(), rows * 4, cudaMemcpyHostToDevice, s));
+      int hbad[4] = {0, 0, 0, 0};
+      BBM_CUDA(cudaMemcpyAsync(hbad, bad, 16, cudaMemcpyDeviceToHost, s));
+      BBM_CUDA(cudaStreamSynchronize(s));
+      static const char* names[4] = {"q", "k", "v", "d_out"};
+      for (int t = 0; t < 4; ++t)  // require_finite (engine.hpp:237-242, 358)
+        if (hbad[t]) throw ArgError(std::string(names[t]) + " must hold finite values");
+      refresh_kernel_view(pr, s);
+      build_bwd_meta(pr, s);
+      BwdArgs a{b[0], b[1], b[2], o32, true, rm, rs, b[3], g3[0], g3[1], g3[2], slots, pr.n, head_dim,
+                static_cast<float>(scale), variant};
+      launch_attn_bwd(pr, a, s, sm_count(pr.device));
+      float* dsts[3] = {dq, dk, dv};
+      for (int t = 0; t < 3; ++t) {
+        bf16_to_f32_kernel<<<grid_of(elems), 256, 0, s>>>(g3[t], stage, elems);
+        BBM_CUDA(cudaGetLastError());
+        BBM_CUDA(cudaMemcpyAsync(dsts[t], stage, elems * 4, cudaMemcpyDeviceToHost, s));
+        BBM_CUDA(cudaStreamSynchronize(s));
+      }
+    } catch (...) {
+      release();
+      throw;
+    }
+    release();
+  });
+}
+
 bbm_status bbm_run_attention_multi(bbm_prep prep, int variant, int n_devices, const int* devices,
                                    const uint16_t* q, const uint16_t* k, const uint16_t* v,
                                    uint16_t* out, float* row_max, float* row_sum, uint64_t slots,
@@ -761,6 +940,60 @@ bbm_status bbm_permute_mask_device(const uint64_t* d_src, uint64_t* d_dst,
     require(d_src && d_dst && d_forward && d_src != d_dst, "bad argument");
     const uint64_t wpr = (n + 63) / 64;
     launch_permute_mask(d_src, d_dst, d_forward, n, wpr, wpr, static_cast<cudaStream_t>(stream));
+  });
+}
+
+bbm_status bbm_permute_rows_host(const void* src, void* dst, const uint32_t* forward,
+                                 uint64_t slots, uint64_t n, uint64_t row_bytes, int inverse,
+                                 int device) {
+  return guarded([&] {
+    require(src && dst && forward, "null argument");
+    require(row_bytes >= 1, "row bytes must be >= 1");
+    check_bijection(forward, n);
+    DeviceGuard g(device);
+    const uint64_t pitch = (row_bytes + 15) / 16 * 16, rows = slots * n;
+    cudaStream_t s;
+    BBM_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    uint8_t* a = dmalloc<uint8_t>(rows * pitch);
+    uint8_t* b = dmalloc<uint8_t>(rows * pitch);
+    uint32_t* f = dmalloc<uint32_t>(n);
+    try {
+      BBM_CUDA(cudaMemcpy2DAsync(a, pitch, src, row_bytes, row_bytes, rows, cudaMemcpyHostToDevice, s));
+      BBM_CUDA(cudaMemcpyAsync(f, forward, n * 4, cudaMemcpyHostToDevice, s));
+      launch_permute_rows(a, b, f, slots, n, pitch, inverse != 0, s);
+      BBM_CUDA(cudaMemcpy2DAsync(dst, row_bytes, b, pitch, row_bytes, rows, cudaMemcpyDeviceToHost, s));
+      BBM_CUDA(cudaStreamSynchronize(s));
+    } catch (...) {
+      cudaFree(a), cudaFree(b), cudaFree(f), cudaStreamDestroy(s);
+      throw;
+    }
+    cudaFree(a), cudaFree(b), cudaFree(f), cudaStreamDestroy(s);
+  });
+}
+
+bbm_status bbm_permute_mask_host(const uint64_t* src, uint64_t* dst, const uint32_t* forward,
+                                 uint64_t n, int device) {
+  return guarded([&] {
+    require(src && dst && forward, "null argument");
+    check_bijection(forward, n);
+    DeviceGuard g(device);
+    const uint64_t wpr = (n + 63) / 64;
+    cudaStream_t s;
+    BBM_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    uint64_t* a = dmalloc<uint64_t>(n * wpr);
+    uint64_t* b = dmalloc<uint64_t>(n * wpr);
+    uint32_t* f = dmalloc<uint32_t>(n);
+    try {
+      BBM_CUDA(cudaMemcpyAsync(a, src, n * wpr * 8, cudaMemcpyHostToDevice, s));
+      BBM_CUDA(cudaMemcpyAsync(f, forward, n * 4, cudaMemcpyHostToDevice, s));
+      launch_permute_mask(a, b, f, n, wpr, wpr, s);
+      BBM_CUDA(cudaMemcpyAsync(dst, b, n * wpr * 8, cudaMemcpyDeviceToHost, s));
+      BBM_CUDA(cudaStreamSynchronize(s));
+    } catch (...) {
+      cudaFree(a), cudaFree(b), cudaFree(f), cudaStreamDestroy(s);
+      throw;
+    }
+    cudaFree(a), cudaFree(b), cudaFree(f), cudaStreamDestroy(s);
   });
 }
 

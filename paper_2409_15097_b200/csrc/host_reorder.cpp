@@ -164,3 +164,26 @@ extern "C" bbm_status bbm_bandwidth(const uint64_t* words, uint64_t n, uint64_t*
   *bandwidth = bw;
   return BBM_OK;
 }
+
+extern "C" bbm_status bbm_graph_csr(const uint64_t* words, uint64_t n, uint64_t* offsets,
+                                    uint32_t* neighbors) {
+  // build_graph (reorder.hpp:28-49): symmetrized pattern, self loops dropped, neighbours sorted
+  try {
+    bbm::require(words != nullptr && offsets != nullptr, "null argument");
+    const BitGraph g = build_bit_graph(words, n);
+    offsets[0] = 0;
+    for (uint64_t i = 0; i < n; ++i) offsets[i + 1] = offsets[i] + g.degree[i];
+    if (neighbors)
+      for (uint64_t i = 0; i < n; ++i) {
+        uint64_t at = offsets[i];
+        for_each_neighbor(g, static_cast<uint32_t>(i), [&](uint32_t j) { neighbors[at++] = j; });
+      }
+    return BBM_OK;
+  } catch (const std::invalid_argument& e) {
+    bbm::g_last_error = e.what();
+    return BBM_ERR_INVALID;
+  } catch (const std::exception& e) {
+    bbm::g_last_error = e.what();
+    return BBM_ERR_INTERNAL;
+  }
+}

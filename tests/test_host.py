@@ -113,6 +113,7 @@ def test_mask_helpers_and_permutation():
     assert p.inverse.tolist() == [1, 2, 0]
 
 
+@pytest.mark.gpu  # the helpers run the preprocessor's row kernel on the device
 def test_host_metadata_helpers_match_golden():
     g = np.load(os.path.join(GOLDEN, "mask_model.npz"))
     for i in range(0, int(g["count"]), 7):

@@ -187,3 +187,22 @@ def test_preprocess_matches_reference_on_large_random():
         for x, y in zip(a[:4], b[:4]):
             assert np.array_equal(x, y)
         assert a[4] == b[4]
+
+
+@pytest.mark.skipif(not oracle.ref_available(), reason="oracle/_ref not built")
+@pytest.mark.parametrize("spec,n,d", [("causal", 70, 16), ("packed-seq[20;33;14]", 0, 8), ("random(p=0.2;seed=5;diag=0)", 45, 12)])
+def test_naive_backward_matches_reference(spec, n, d):
+    # pins the C restatement of naive_backward (reference.hpp:84-139) on the reference itself
+    words = oracle.ref_generate(spec, n)
+    n = words.shape[0]
+    q, k, v, g = (a[0] for a in oracle.make_problem(3, 1, n, d))
+    for threads in (1, 3):
+        got = oracle.naive_backward(q, k, v, g, 0.37, words, n, threads=threads)
+        want = oracle.ref_naive_backward(q, k, v, g, 0.37, words, n)
+        for a, b in zip(got, want):
+            assert np.allclose(a, b, rtol=1e-12, atol=1e-13)
+    # dense = every key visible: the all-ones mask
+    got = oracle.naive_backward(q, k, v, g, 0.37, None, n)
+    want = oracle.ref_naive_backward(q, k, v, g, 0.37, np.full_like(words, 0) | oracle.ref_generate("all-ones", n), n)
+    for a, b in zip(got, want):
+        assert np.allclose(a, b, rtol=1e-12, atol=1e-13)
