@@ -240,18 +240,18 @@ __global__ void __launch_bounds__(kThreads, 1)
           mbar_wait(&ctl->ring_full[r], rph);
           tc_fence_after();
           const uint32_t sbase = raddr + r * C::kStageAlloc;
+          const uint64_t f0 = make_sdesc_sw128(faddr, 16, 1024), f1 = make_sdesc_sw128(faddr + C::kTileBytes, 16, 1024);
+          const uint64_t s0 = make_sdesc_sw128(sbase, 16, 1024), s1 = make_sdesc_sw128(sbase + C::kTileBytes, 16, 1024);
           // S (or S^T) = f0 s0^T, dP (or dP^T) = f1 s1^T: both operands K-major, K = D
 #pragma unroll
           for (uint32_t kk = 0; kk < D / 16; ++kk) {
             const uint32_t off = (kk / 4) * kBoxBytes + (kk % 4) * 32;
-            umma_ss(tmem, make_sdesc_sw128(faddr + off, 16, 1024), make_sdesc_sw128(sbase + off, 16, 1024),
-                    idesc_s, kk > 0);
+            umma_ss(tmem, sdesc_advance(f0, off), sdesc_advance(s0, off), idesc_s, kk > 0);
           }
 #pragma unroll
           for (uint32_t kk = 0; kk < D / 16; ++kk) {
             const uint32_t off = (kk / 4) * kBoxBytes + (kk % 4) * 32;
-            umma_ss(tmem + 128, make_sdesc_sw128(faddr + C::kTileBytes + off, 16, 1024),
-                    make_sdesc_sw128(sbase + C::kTileBytes + off, 16, 1024), idesc_s, kk > 0);
+            umma_ss(tmem + 128, sdesc_advance(f1, off), sdesc_advance(s1, off), idesc_s, kk > 0);
           }
           tc_commit(&ctl->s_full);
           if (j + 1 == it.nt) tc_commit(&ctl->fixed_empty);
@@ -264,15 +264,16 @@ __global__ void __launch_bounds__(kThreads, 1)
           tc_fence_after();
           // packed bf16 A operand: half h's 32 columns at [64h, 64h+32) of its region; K step kk
           // (16 partner rows = 8 packed columns) -> column (kk/4)*64 + (kk%4)*8
+          const uint64_t b0 = make_sdesc_sw128(sbase, kBoxBytes, 1024);
+          const uint64_t b1 = make_sdesc_sw128(sbase + C::kTileBytes, kBoxBytes, 1024);
 #pragma unroll
           for (uint32_t kk = 0; kk < 8; ++kk) {
             const uint32_t acol = (kk / 4) * 64 + (kk % 4) * 8;
             // dQ += dS K_j  |  dK += dS^T Q_i   (B = streamed tile 0, MN-major)
-            umma_ts(tmem + C::kAcc0, tmem + 128 + acol,
-                    make_sdesc_sw128(sbase + kk * 2048, kBoxBytes, 1024), idesc_acc, (j > 0 || kk > 0) ? 1u : 0u);
+            umma_ts(tmem + C::kAcc0, tmem + 128 + acol, sdesc_advance(b0, kk * 2048), idesc_acc,
+                    (j > 0 || kk > 0) ? 1u : 0u);
             if constexpr (SIDE == kSideDKDV)  // dV += P^T dO_i   (B = streamed tile 1)
-              umma_ts(tmem + C::kAcc1, tmem + acol,
-                      make_sdesc_sw128(sbase + C::kTileBytes + kk * 2048, kBoxBytes, 1024), idesc_acc,
+              umma_ts(tmem + C::kAcc1, tmem + acol, sdesc_advance(b1, kk * 2048), idesc_acc,
                       (j > 0 || kk > 0) ? 1u : 0u);
           }
           tc_commit(&ctl->ring_empty[r]);

@@ -84,7 +84,7 @@ constexpr uint32_t kQueue = 4;        // item queue depth (>= 3 items open at th
 
 // Trace event: [63:24] clock64 low 40 bits | [23:16] code | [15] stream | [14:0] aux.
 // Codes: producer 1 Q issued (aux = item), 2 K_k issued, 3 V_k issued;
-//        MMA 10 S_k issued, 11 PV_k issued;
+//        MMA 10 S_k issued, 11 PV_k issued, 12 V_k landed, 13 K_k landed, 14 P_k seen;
 //        softmax 20 s_full wait begin, 21 s_full wait end, 22 p_full arrive, 23 o_full wait end,
 //        24 epilogue done.
 template <bool kTrace>
@@ -276,53 +276,96 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   if (warp == 0) {
     // ------------------------------------------------------------------ producer
+    // Loads follow the MMA issuer's consumption order S_0, S_1, PV_0, S_2, PV_1, ..., i.e.
+    // K_0, K_1, V_0, K_2, V_1, K_3, ...: a K cursor runs two tiles ahead of a V cursor, so a load
+    // only ever waits for the ring slot freed kRing positions earlier in that same order.
     if (lane == 0) {
       const uint64_t pol_q = policy_evict_first();
       const uint64_t pol_kv = policy_evict_last();
-      uint32_t r = 0, rph = 1, qi = 0, qiph = 1, qb = 0;
+      uint32_t qi = 0, qiph = 1, qb = 0;
       uint32_t qph[2] = {1, 1};
-      auto load_tile = [&](const CUtensorMap* tm, uint32_t q, uint32_t slot, uint32_t code,
+      ItemDesc pit[kQueue];  // items claimed by the K cursor, replayed by the V cursor
+      uint32_t pw = 0, pr = 0;
+      auto load_tile = [&](const CUtensorMap* tm, uint32_t seq, uint32_t q, uint32_t slot, uint32_t code,
                            uint32_t j) {
-        mbar_wait(&ctl->ring_empty[r], rph);
+        const uint32_t r = seq % C::kRing;
+        mbar_wait(&ctl->ring_empty[r], ((seq / C::kRing) & 1) ^ 1);
         uint64_t* full = &ctl->ring_full[r];
         mbar_arrive_expect_tx(full, C::kTileBytes);
         for (uint32_t b = 0; b < C::kBoxes; ++b)
-          tma_load_3d(ring + r * C::kTileBytes + b * kBoxBytes, tm, full, b * 64, q * 128, slot,
-                      pol_kv);
+          tma_load_3d(ring + r * C::kTileBytes + b * kBoxBytes, tm, full, b * 64, q * 128, slot, pol_kv);
         trace_ev<kTrace>(tracing, p, &ctl->trace_count, code, 0, j);
-        if (++r == C::kRing) { r = 0; rph ^= 1; }
       };
-      for (;;) {
-        const ItemDesc d = decode_item(p, atomicAdd(&p.work_ctr[0], 1u));
-        mbar_wait(&ctl->item_empty[qi], qiph);
-        ctl->items[qi] = d;
-        mbar_arrive(&ctl->item_full[qi]);  // release: the descriptor is visible to waiters
-        if (++qi == kQueue) { qi = 0; qiph ^= 1; }
-        if (d.t == kEnd) break;
-        if (d.nt == 0) continue;
-        // list entries one tile ahead so the TMA issue never waits on an L2 load
-        uint32_t cur = entry_of<MODE>(p, d.rt, d.j0);
-        mbar_wait(&ctl->q_empty[qb], qph[qb]);
-        qph[qb] ^= 1;
-        mbar_arrive_expect_tx(&ctl->q_full[qb], C::kTileBytes);
-        for (uint32_t b = 0; b < C::kBoxes; ++b)
-          tma_load_3d(sq + qb * C::kTileBytes + b * kBoxBytes, &tm_q, &ctl->q_full[qb], b * 64,
-                      d.rt * 128, d.slot, pol_q);
-        trace_ev<kTrace>(tracing, p, &ctl->trace_count, 1, 0, d.t);
-        qb ^= 1;
-        for (uint32_t j = 0; j < d.nt; ++j) {
-          const uint32_t nxt = (j + 1 < d.nt) ? entry_of<MODE>(p, d.rt, d.j0 + j + 1) : 0;
-          const uint32_t q = cur & 0x7FFFFFFFu;
-          load_tile(&tm_k, q, d.slot, 2, j);
-          load_tile(&tm_v, q, d.slot, 3, j);
-          cur = nxt;
+      // K cursor (claims and publishes items, loads Q)
+      ItemDesc kit{};
+      uint32_t kj = 0, kk = 0, kentry = 0;
+      bool k_need = true, k_done = false;
+      auto k_next = [&]() -> bool {
+        while (k_need) {
+          if (k_done) return false;
+          const ItemDesc d = decode_item(p, atomicAdd(&p.work_ctr[0], 1u));
+          mbar_wait(&ctl->item_empty[qi], qiph);
+          ctl->items[qi] = d;
+          mbar_arrive(&ctl->item_full[qi]);  // release: the descriptor is visible to waiters
+          if (++qi == kQueue) { qi = 0; qiph ^= 1; }
+          if (d.t == kEnd) {
+            k_done = true;
+            return false;
+          }
+          if (d.nt == 0) continue;
+          pit[pw++ % kQueue] = d;
+          kentry = entry_of<MODE>(p, d.rt, d.j0);
+          mbar_wait(&ctl->q_empty[qb], qph[qb]);
+          qph[qb] ^= 1;
+          mbar_arrive_expect_tx(&ctl->q_full[qb], C::kTileBytes);
+          for (uint32_t b = 0; b < C::kBoxes; ++b)
+            tma_load_3d(sq + qb * C::kTileBytes + b * kBoxBytes, &tm_q, &ctl->q_full[qb], b * 64,
+                        d.rt * 128, d.slot, pol_q);
+          trace_ev<kTrace>(tracing, p, &ctl->trace_count, 1, 0, d.t);
+          qb ^= 1;
+          kit = d;
+          kj = 0;
+          k_need = false;
         }
-      }
+        return true;
+      };
+      auto issue_k = [&]() {
+        const uint32_t cur = kentry;
+        // the next list entry is fetched now, a full issue step before it is needed
+        if (kj + 1 < kit.nt) kentry = entry_of<MODE>(p, kit.rt, kit.j0 + kj + 1);
+        load_tile(&tm_k, kk == 0 ? 0u : 2 * kk - 1, cur & 0x7FFFFFFFu, kit.slot, 2, kj);
+        ++kk;
+        if (++kj == kit.nt) k_need = true;
+      };
+      // V cursor
+      ItemDesc vit{};
+      uint32_t vj = 0, vk = 0, ventry = 0;
+      bool v_need = true;
+      auto issue_v = [&]() -> bool {
+        if (v_need) {
+          if (pr == pw) return false;
+          vit = pit[pr++ % kQueue];
+          vj = 0;
+          ventry = entry_of<MODE>(p, vit.rt, vit.j0);
+          v_need = false;
+        }
+        const uint32_t cur = ventry;
+        if (vj + 1 < vit.nt) ventry = entry_of<MODE>(p, vit.rt, vit.j0 + vj + 1);
+        load_tile(&tm_v, 2 * vk + 2, cur & 0x7FFFFFFFu, vit.slot, 3, vj);
+        ++vk;
+        if (++vj == vit.nt) v_need = true;
+        return true;
+      };
+      for (int w = 0; w < 2; ++w)
+        if (k_next()) issue_k();
+      while (issue_v())
+        if (k_next()) issue_k();
     }
   } else if (warp == 1) {
     // ------------------------------------------------------------------ MMA issuer
     // Two cursors over the tile sequence: the S cursor runs two tiles ahead of the PV cursor.
-    // Ring slots: K_k at 2k, V_k at 2k+1 (mod kRing) — consumed in order S_k ... PV_k.
+    // Ring slots follow the load order K_0, K_1, V_0, K_2, V_1, ...: K_k at position
+    // max(0, 2k-1), V_k at 2k+2 (mod kRing).
     if (lane == 0) {
       constexpr uint32_t idesc_s = make_idesc_bf16(128, 128, false, false);
       constexpr uint32_t idesc_o = make_idesc_bf16(128, D, false, true);
@@ -364,15 +407,17 @@ __global__ void __launch_bounds__(kThreads, 1)
           mbar_wait(&ctl->q_full[s_qb], s_qph[s_qb]);
           s_qph[s_qb] ^= 1;
         }
-        const uint32_t slot = (2 * s_k) % C::kRing;
-        mbar_wait(&ctl->ring_full[slot], ((2 * s_k) / C::kRing) & 1);
+        const uint32_t kseq = s_k == 0 ? 0u : 2 * s_k - 1;  // load order K_0, K_1, V_0, K_2, V_1, ...
+        const uint32_t slot = kseq % C::kRing;
+        mbar_wait(&ctl->ring_full[slot], (kseq / C::kRing) & 1);
+        trace_ev<kTrace>(tracing, p, &ctl->trace_count, 13, buf, s_j);
         tc_fence_after();
-        const uint32_t qbase = qaddr + s_qb * C::kTileBytes, kbase = raddr + slot * C::kTileBytes;
+        const uint64_t qdesc = make_sdesc_sw128(qaddr + s_qb * C::kTileBytes, 16, 1024);
+        const uint64_t kdesc = make_sdesc_sw128(raddr + slot * C::kTileBytes, 16, 1024);
 #pragma unroll
         for (uint32_t kk = 0; kk < D / 16; ++kk) {
           const uint32_t off = (kk / 4) * kBoxBytes + (kk % 4) * 32;
-          umma_ss(tmem + buf * 128, make_sdesc_sw128(qbase + off, 16, 1024),
-                  make_sdesc_sw128(kbase + off, 16, 1024), idesc_s, kk > 0);
+          umma_ss(tmem + buf * 128, sdesc_advance(qdesc, off), sdesc_advance(kdesc, off), idesc_s, kk > 0);
         }
         tc_commit(&ctl->ring_empty[slot]);
         tc_commit(&ctl->s_full[buf]);
@@ -403,14 +448,17 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t buf = p_k & 1;
         mbar_wait(&ctl->p_full[buf], p_ph[buf]);
         p_ph[buf] ^= 1;
-        const uint32_t slot = (2 * p_k + 1) % C::kRing;
-        mbar_wait(&ctl->ring_full[slot], ((2 * p_k + 1) / C::kRing) & 1);
+        trace_ev<kTrace>(tracing, p, &ctl->trace_count, 14, buf, p_j);
+        const uint32_t vseq = 2 * p_k + 2;
+        const uint32_t slot = vseq % C::kRing;
+        mbar_wait(&ctl->ring_full[slot], (vseq / C::kRing) & 1);
+        trace_ev<kTrace>(tracing, p, &ctl->trace_count, 12, buf, p_j);
         tc_fence_after();
-        const uint32_t vbase = raddr + slot * C::kTileBytes;
+        const uint64_t vdesc = make_sdesc_sw128(raddr + slot * C::kTileBytes, kBoxBytes, 1024);
+        const uint32_t pcol = tmem + buf * 128;
 #pragma unroll
         for (uint32_t kk = 0; kk < 128 / 16; ++kk)
-          umma_ts(tmem_o, tmem + buf * 128 + kk * 8,
-                  make_sdesc_sw128(vbase + kk * 2048, kBoxBytes, 1024), idesc_o,
+          umma_ts(tmem_o, pcol + kk * 8, sdesc_advance(vdesc, kk * 2048), idesc_o,
                   (p_j > 0 || kk > 0) ? 1u : 0u);
         tc_commit(&ctl->ring_empty[slot]);
         tc_commit(&ctl->pv_done);

@@ -97,6 +97,17 @@ struct BwdMeta {
   mutable size_t rowws_floats = 0;
 };
 
+// Host-buffer pipeline of one prep's device (host_io.cu): persistent device buffers (grow-only)
+// and three streams, so a host-buffer call overlaps H2D of slot chunk c+1, the kernel on chunk c
+// and D2H of chunk c-1 instead of running copy -> kernel -> copy serially.
+struct HostPipe {
+  cudaStream_t h2d = nullptr, comp = nullptr, d2h = nullptr;
+  std::vector<cudaEvent_t> ev_in, ev_out;
+  uint8_t* buf = nullptr;
+  size_t cap = 0;
+  ~HostPipe();
+};
+
 struct Prep {
   int device = 0;
   uint64_t n = 0;
@@ -113,6 +124,7 @@ struct Prep {
   mutable std::map<std::tuple<bool, uint64_t, uint32_t>, LaunchPlan> plans;
   mutable float* workspace = nullptr;
   mutable size_t workspace_floats = 0;
+  mutable HostPipe* pipe = nullptr;  // host-buffer pipeline (lazy, host_io.cu)
 
   template <class F>
   const LaunchPlan& plan_for(bool all_tiles, uint64_t slots, uint32_t streams, F make) const {
@@ -202,5 +214,12 @@ void free_bwd_meta(BwdMeta& b);
 // refresh host row counts / plans after bbm_prep_update_* (synchronizes `s` once)
 void refresh_kernel_view(const Prep& prep, cudaStream_t s);
 int attn_fwd_kernel_launches_per_call();
+
+// host-buffer forward through the prep's pipeline (host_io.cu): bf16 host q/k/v/out (pinned for
+// full PCIe bandwidth), optional fp32 row stats; synchronous. Returns the device-side span in ms
+// (first H2D issued -> last D2H done) when `span_ms` is non-null.
+void run_fwd_host_pipelined(const Prep& prep, int variant, const uint16_t* q, const uint16_t* k,
+                            const uint16_t* v, uint16_t* out, float* row_max, float* row_sum,
+                            uint64_t slots, uint32_t d, float scale, int num_sms, double* span_ms);
 
 }  // namespace bbm

@@ -203,6 +203,13 @@ __device__ __forceinline__ uint64_t make_sdesc_sw128(uint32_t smem_addr, uint32_
   return d;
 }
 
+// The same descriptor advanced by `bytes` (a multiple of 16): the start address is the low field,
+// and every operand of a CTA lies below 256 KB of shared memory, so a plain add never carries out
+// of it. Hoisting the base descriptor out of the K loop leaves one add per MMA issue.
+__device__ __forceinline__ uint64_t sdesc_advance(uint64_t desc, uint32_t bytes) {
+  return desc + static_cast<uint64_t>(bytes >> 4);
+}
+
 // kind::f16 instruction descriptor: bf16 x bf16 -> f32.
 __host__ __device__ constexpr uint32_t make_idesc_bf16(uint32_t M, uint32_t N, bool a_mn_major,
                                                        bool b_mn_major) {

@@ -198,6 +198,7 @@ Prep::~Prep() {
   int prev = -1;
   cudaGetDevice(&prev);
   cudaSetDevice(device);
+  delete pipe;
   free_kernel_meta(kmeta);
   free_bwd_meta(bwd);
   cudaFree(work_ctr);
@@ -617,35 +618,10 @@ bbm_status bbm_attn_fwd_host_bf16(bbm_prep prep, int variant, const uint16_t* q,
   return guarded([&] {
     const Prep& pr = unwrap(prep);
     check_attn_args(pr, variant, slots, head_dim, scale);
+    require(q && k && v && out, "null tensor pointer");
     DeviceGuard g(pr.device);
-    cudaStream_t s;
-    BBM_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
-    const uint64_t elems = slots * pr.n * head_dim, bytes = elems * 2;
-    void *dq, *dk, *dv, *dout;
-    float *dmax = nullptr, *dsum = nullptr;
-    BBM_CUDA(cudaMallocAsync(&dq, bytes, s));
-    BBM_CUDA(cudaMallocAsync(&dk, bytes, s));
-    BBM_CUDA(cudaMallocAsync(&dv, bytes, s));
-    BBM_CUDA(cudaMallocAsync(&dout, bytes, s));
-    if (row_max) BBM_CUDA(cudaMallocAsync(&dmax, slots * pr.n * 4, s));
-    if (row_sum) BBM_CUDA(cudaMallocAsync(&dsum, slots * pr.n * 4, s));
-    BBM_CUDA(cudaMemcpyAsync(dq, q, bytes, cudaMemcpyHostToDevice, s));
-    BBM_CUDA(cudaMemcpyAsync(dk, k, bytes, cudaMemcpyHostToDevice, s));
-    BBM_CUDA(cudaMemcpyAsync(dv, v, bytes, cudaMemcpyHostToDevice, s));
-    AttnArgs a{dq, dk, dv, dout, dmax, dsum, slots, pr.n, head_dim, static_cast<float>(scale),
-               variant};
-    launch_attn_fwd(pr, a, s, sm_count(pr.device));
-    BBM_CUDA(cudaMemcpyAsync(out, dout, bytes, cudaMemcpyDeviceToHost, s));
-    if (row_max) BBM_CUDA(cudaMemcpyAsync(row_max, dmax, slots * pr.n * 4, cudaMemcpyDeviceToHost, s));
-    if (row_sum) BBM_CUDA(cudaMemcpyAsync(row_sum, dsum, slots * pr.n * 4, cudaMemcpyDeviceToHost, s));
-    cudaFreeAsync(dq, s);
-    cudaFreeAsync(dk, s);
-    cudaFreeAsync(dv, s);
-    cudaFreeAsync(dout, s);
-    if (dmax) cudaFreeAsync(dmax, s);
-    if (dsum) cudaFreeAsync(dsum, s);
-    BBM_CUDA(cudaStreamSynchronize(s));
-    BBM_CUDA(cudaStreamDestroy(s));
+    run_fwd_host_pipelined(pr, variant, q, k, v, out, row_max, row_sum, slots, head_dim,
+                           static_cast<float>(scale), sm_count(pr.device), nullptr);
   });
 }
 
@@ -840,77 +816,31 @@ bbm_status bbm_run_attention_multi(bbm_prep prep, int variant, int n_devices, co
       }
       preps[g] = found;
     }
-    struct Shard {
-      uint64_t s0 = 0, s1 = 0;
-      void *dq = nullptr, *dk = nullptr, *dv = nullptr, *dout = nullptr;
-      float *dmax = nullptr, *dsum = nullptr;
-      cudaStream_t st = nullptr;
-      cudaEvent_t e0 = nullptr, e1 = nullptr;
-    };
-    std::vector<Shard> sh(n_devices);
-    for (int g = 0; g < n_devices; ++g) {
-      Shard& x = sh[g];
-      x.s0 = slots * g / n_devices;
-      x.s1 = slots * (g + 1) / n_devices;
-      DeviceGuard dg(devices[g]);
-      BBM_CUDA(cudaStreamCreateWithFlags(&x.st, cudaStreamNonBlocking));
-      BBM_CUDA(cudaEventCreate(&x.e0));
-      BBM_CUDA(cudaEventCreate(&x.e1));
-      const uint64_t ns = x.s1 - x.s0;
-      if (ns == 0) continue;
-      const uint64_t bytes = ns * per_slot * 2;
-      BBM_CUDA(cudaMallocAsync(&x.dq, bytes, x.st));
-      BBM_CUDA(cudaMallocAsync(&x.dk, bytes, x.st));
-      BBM_CUDA(cudaMallocAsync(&x.dv, bytes, x.st));
-      BBM_CUDA(cudaMallocAsync(&x.dout, bytes, x.st));
-      BBM_CUDA(cudaMallocAsync(&x.dmax, ns * pr.n * 4, x.st));
-      BBM_CUDA(cudaMallocAsync(&x.dsum, ns * pr.n * 4, x.st));
-      BBM_CUDA(cudaMemcpyAsync(x.dq, q + x.s0 * per_slot, bytes, cudaMemcpyHostToDevice, x.st));
-      BBM_CUDA(cudaMemcpyAsync(x.dk, k + x.s0 * per_slot, bytes, cudaMemcpyHostToDevice, x.st));
-      BBM_CUDA(cudaMemcpyAsync(x.dv, v + x.s0 * per_slot, bytes, cudaMemcpyHostToDevice, x.st));
-    }
-    // launch all shards, then collect (no collective: shards are independent)
-    for (int g = 0; g < n_devices; ++g) {
-      Shard& x = sh[g];
-      DeviceGuard dg(devices[g]);
-      BBM_CUDA(cudaEventRecord(x.e0, x.st));
-      const uint64_t ns = x.s1 - x.s0;
-      if (ns) {
-        AttnArgs a{x.dq, x.dk, x.dv, x.dout, x.dmax, x.dsum, ns, pr.n, head_dim,
-                   static_cast<float>(scale), variant};
-        launch_attn_fwd(*preps[g]->p, a, x.st, sm_count(devices[g]));
-      }
-      BBM_CUDA(cudaEventRecord(x.e1, x.st));
-    }
-    double worst = 0.0;
-    for (int g = 0; g < n_devices; ++g) {
-      Shard& x = sh[g];
-      DeviceGuard dg(devices[g]);
-      const uint64_t ns = x.s1 - x.s0;
-      if (ns) {
-        BBM_CUDA(cudaMemcpyAsync(out + x.s0 * per_slot, x.dout, ns * per_slot * 2,
-                                 cudaMemcpyDeviceToHost, x.st));
-        if (row_max)
-          BBM_CUDA(cudaMemcpyAsync(row_max + x.s0 * pr.n, x.dmax, ns * pr.n * 4,
-                                   cudaMemcpyDeviceToHost, x.st));
-        if (row_sum)
-          BBM_CUDA(cudaMemcpyAsync(row_sum + x.s0 * pr.n, x.dsum, ns * pr.n * 4,
-                                   cudaMemcpyDeviceToHost, x.st));
-      }
-      BBM_CUDA(cudaStreamSynchronize(x.st));
-      float ms = 0.0f;
-      BBM_CUDA(cudaEventElapsedTime(&ms, x.e0, x.e1));
-      worst = std::max(worst, static_cast<double>(ms));
-      cudaFree(x.dq);
-      cudaFree(x.dk);
-      cudaFree(x.dv);
-      cudaFree(x.dout);
-      cudaFree(x.dmax);
-      cudaFree(x.dsum);
-      cudaEventDestroy(x.e0);
-      cudaEventDestroy(x.e1);
-      cudaStreamDestroy(x.st);
-    }
+    // one host thread per GPU drives that GPU's copy/compute pipeline over its contiguous slot
+    // range; shards share nothing (no collective), the span is max over GPUs of each device's
+    // first-H2D -> last-D2H time
+    std::vector<double> span(n_devices, 0.0);
+    std::vector<std::string> err(n_devices);
+    std::vector<std::thread> th;
+    for (int g = 0; g < n_devices; ++g)
+      th.emplace_back([&, g] {
+        try {
+          const uint64_t s0 = slots * g / n_devices, s1 = slots * (g + 1) / n_devices;
+          if (s1 == s0) return;
+          DeviceGuard dg(devices[g]);
+          run_fwd_host_pipelined(*preps[g]->p, variant, q + s0 * per_slot, k + s0 * per_slot,
+                                 v + s0 * per_slot, out + s0 * per_slot,
+                                 row_max ? row_max + s0 * pr.n : nullptr,
+                                 row_sum ? row_sum + s0 * pr.n : nullptr, s1 - s0, head_dim,
+                                 static_cast<float>(scale), sm_count(devices[g]), &span[g]);
+        } catch (const std::exception& e) {
+          err[g] = e.what();
+        }
+      });
+    for (auto& t : th) t.join();
+    for (int g = 0; g < n_devices; ++g)
+      if (!err[g].empty()) throw CudaError("device " + std::to_string(devices[g]) + ": " + err[g]);
+    const double worst = *std::max_element(span.begin(), span.end());
     if (elapsed_ms) *elapsed_ms = worst;
   });
 }

@@ -10,7 +10,7 @@
 
 using namespace bbm::ptx;
 
-template <int MODE, int N, bool kTma, int kLdWarps = 0>  // MODE 0 = SS, 1 = TS
+template <int MODE, int N, bool kTma, int kLdWarps = 0, int kMufu = 0>  // MODE 0 = SS, 1 = TS
 __global__ void __launch_bounds__(384, 1) rate_kernel(int iters, unsigned long long* out,
                                                       const uint8_t* gsrc, volatile int* stop) {
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -82,6 +82,15 @@ __global__ void __launch_bounds__(384, 1) rate_kernel(int iters, unsigned long l
       uint32_t pk[16];
 #pragma unroll
       for (int i = 0; i < 16; ++i) pk[i] = a0[2 * i] ^ a1[2 * i + 1];
+      if (kMufu) {  // the softmax engine's exp2 load on the XU pipe
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+          float x = __uint_as_float(a0[i] & 0x3fffffffu), y = __uint_as_float(a1[i] & 0x3fffffffu);
+          asm volatile("ex2.approx.ftz.f32 %0, %0;" : "+f"(x));
+          asm volatile("ex2.approx.ftz.f32 %0, %0;" : "+f"(y));
+          pk[i / 2] ^= __float_as_uint(x) ^ __float_as_uint(y);
+        }
+      }
       tmem_st16(tmem + 384 + lane_off + half * 32, pk);
       tmem_st_wait();
       ++passes;
@@ -93,17 +102,17 @@ __global__ void __launch_bounds__(384, 1) rate_kernel(int iters, unsigned long l
   if (warp == 0) tmem_dealloc<512>(tmem);
 }
 
-template <int MODE, int N, bool kTma, int kLdWarps = 0>
+template <int MODE, int N, bool kTma, int kLdWarps = 0, int kMufu = 0>
 void run(const char* name) {
   unsigned long long* d;
   cudaMalloc(&d, 16);
   uint8_t* g;
   cudaMalloc(&g, 64 * 32768);
   const int smem = 2 * 65536 + 32768 + 1024;
-  cudaFuncSetAttribute(rate_kernel<MODE, N, kTma, kLdWarps>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaFuncSetAttribute(rate_kernel<MODE, N, kTma, kLdWarps, kMufu>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   const int iters = 2000;
-  rate_kernel<MODE, N, kTma, kLdWarps><<<148, 384, smem>>>(iters, d, g, nullptr);
-  rate_kernel<MODE, N, kTma, kLdWarps><<<148, 384, smem>>>(iters, d, g, nullptr);
+  rate_kernel<MODE, N, kTma, kLdWarps, kMufu><<<148, 384, smem>>>(iters, d, g, nullptr);
+  rate_kernel<MODE, N, kTma, kLdWarps, kMufu><<<148, 384, smem>>>(iters, d, g, nullptr);
   cudaError_t e = cudaDeviceSynchronize();
   unsigned long long res[2] = {0, 0};
   cudaMemcpy(res, d, 16, cudaMemcpyDeviceToHost);
@@ -122,5 +131,7 @@ int main() {
   run<0, 128, false, 4>("SS+4ldwarps");
   run<0, 128, false, 8>("SS+8ldwarps");
   run<1, 128, false, 8>("TS+8ldwarps");
+  run<0, 128, false, 8, 1>("SS+8ld+mufu");
+  run<1, 128, false, 8, 1>("TS+8ld+mufu");
   return 0;
 }

@@ -17,7 +17,7 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
-NAMES = {1: "P:Q", 2: "P:K", 3: "P:V", 10: "M:S", 11: "M:PV", 20: "X:swait", 21: "X:sready",
+NAMES = {1: "P:Q", 2: "P:K", 3: "P:V", 10: "M:S", 11: "M:PV", 12: "M:Vready", 13: "M:Kready", 14: "M:Pseen", 20: "X:swait", 21: "X:sready",
          22: "X:pready", 23: "X:oready", 24: "X:epi_done"}
 
 
@@ -73,6 +73,16 @@ def main():
                 per["softmax compute (S ready -> P ready)"].append(t - last[(s, 21)])
             if code == 11 and (s, 22) in last:
                 per["P ready -> PV issued"].append(t - last[(s, 22)])
+            if code == 14 and (s, 22) in last:
+                per["  P ready -> MMA sees P"].append(t - last[(s, 22)])
+            if code == 12 and (s, 14) in last:
+                per["  MMA sees P -> V landed"].append(t - last[(s, 14)])
+            if code == 11 and (s, 12) in last:
+                per["  V landed -> PV issued"].append(t - last[(s, 12)])
+            if code == 13 and (s, 11) in last:
+                per["  PV issued -> K landed"].append(t - last[(s, 11)])
+            if code == 10 and (s, 13) in last:
+                per["  K landed -> S issued"].append(t - last[(s, 13)])
             if code == 10 and (s, 11) in last:
                 per["PV issued -> next S issued"].append(t - last[(s, 11)])
             if code == 23 and (s, 22) in last:
