@@ -100,6 +100,19 @@ def executed_flops(prep, slots: int, d: int, variant: int) -> float:
     return 4.0 * area * d * slots
 
 
+def max_over_ranks(value: float, device=None) -> float:
+    """Max of a per-rank float over the default process group (the contract's max-over-ranks
+    device time); identity when torch.distributed is not initialised."""
+    import torch
+    import torch.distributed as dist
+
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
+        return float(value)
+    t = torch.tensor([float(value)], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
 def load_peaks():
     path = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(path):
@@ -256,6 +269,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--profile", action="store_true", help="minimal run for ncu (no extras)")
+    ap.add_argument("--pass", dest="which", default="fwd", choices=["fwd", "bwd"],
+                    help="fwd: the BASELINE metric; bwd: blocked_backward over the same tiles")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
 
@@ -301,6 +316,24 @@ def main():
     def step(var=variant):
         bbm.attn_fwd_device(prep, var, q, k, v, out, rmax, rsum, scale, stream.cuda_stream)
 
+    if args.which == "bwd":
+        # blocked_backward (engine.hpp:346-471) from this forward's output and row statistics;
+        # FLOPs counted the standard way (5 GEMMs per executed tile = 2.5x the forward's),
+        # although the two deterministic kernels recompute S and dP (7 GEMMs)
+        d_out = (torch.rand((slots, n, d), generator=g, device=dev) * 2 - 1).to(torch.bfloat16)
+        grads = [torch.empty_like(q) for _ in range(3)]
+        fwd_outs = {}
+        for var in {int(variant), 0}:
+            o_, m_, l_ = torch.empty_like(q), torch.empty_like(rmax), torch.empty_like(rsum)
+            bbm.attn_fwd_device(prep, var, q, k, v, o_, m_, l_, scale, stream.cuda_stream)
+            fwd_outs[var] = (o_, m_, l_)
+        flops *= 2.5
+        dense_flops *= 2.5
+
+        def step(var=variant):  # noqa: F811
+            o_, m_, l_ = fwd_outs[int(var)]
+            bbm.attn_bwd_device(prep, var, q, k, v, o_, m_, l_, d_out, *grads, scale, stream.cuda_stream)
+
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
@@ -334,10 +367,7 @@ def main():
     sampler.stop()
     elapsed_ms = start_all.elapsed_time(end_all)
     launch_ms = [a.elapsed_time(b) for a, b in ev]
-    if world > 1:
-        tt = torch.tensor([elapsed_ms], device=dev, dtype=torch.float64)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        elapsed_ms = float(tt.item())
+    elapsed_ms = max_over_ranks(elapsed_ms, dev)
     ms_step = elapsed_ms / args.steps
     value = world * flops / (ms_step * 1e-3) / 1e12
     if args.profile:
@@ -389,6 +419,8 @@ def main():
                                     "speedup_vs_dense": dense_ms / ms_step,
                                     "ideal_speedup_by_tiles": dense_flops / flops}
         # preprocessor: per-batch rebuild of the kernel metadata from the dense bool mask
+        if args.which == "bwd":
+            args.no_e2e = args.no_cpu_baseline = True
         for _ in range(3):
             prep_update(prep, dense_mask, stream)
         torch.cuda.synchronize()
@@ -423,7 +455,8 @@ def main():
 
     if rank == 0:
         line = {
-            "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
+            "metric": METRIC if args.which == "fwd" else METRIC.replace("fwd", "bwd (5-GEMM FLOPs)"),
+            "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic (uniform[-1,1) bf16 inputs)",
             "config": {"workload": desc, "variant": args.variant, "batch": B, "heads": H, "seq_len": n,
