@@ -14,16 +14,16 @@
 //
 // Structure: one persistent CTA per SM (384 threads), one stream of items (the tile sequence of
 // consecutive items is treated as one sequence k = 0, 1, 2, ...). tcgen05.mma issue is nearly
-// synchronous (the MMA queue holds ~6 instructions), so the score accumulator is DOUBLE-BUFFERED
-// in TMEM: S_{k+2} is computed while the softmax engine turns S_k into P_k, and the engine never
-// waits on the tensor core in steady state.
+// synchronous, so the score accumulator is TRIPLE-BUFFERED in TMEM: S_{k+1} and S_{k+2} are
+// computed while the softmax engine turns S_k into P_k, and the engine never waits on the tensor
+// core in steady state.
 //   warp 0       producer: claims items, publishes them through a shared-memory item queue,
 //                loads Q (double-buffered across items) and K_k, V_k into a K/V ring (TMA,
 //                128B-swizzled 64-column boxes).
-//   warp 1       MMA issuer (one thread): S_k = Q K_k^T (SS, both K-major) into TMEM buffer
-//                k % 2, O += P_k V_k (TS: P read from TMEM, V MN-major). Issue order
-//                S_0, S_1, PV_0, S_2, PV_1, S_3, ... (S_{k+2} reuses P_k's columns, after PV_k).
-//   warp 2       TMEM allocator (512 columns: S buffers at [0,128) and [128,256), O at 256).
+//   warps 1, 3   MMA issuers (one thread each): warp 1 S_k = Q K_k^T (SS, both K-major) into
+//                TMEM buffer k % 3 once PV_{k-3} has completed (S_{k+3} reuses P_k's columns);
+//                warp 3 O += P_k V_k (TS: P read from TMEM, V MN-major).
+//   warp 2       TMEM allocator (512 columns: S buffers at 0, 128, 256; O at 384).
 //   warps 4-11   softmax engine: warps 4-7 own S columns [0,64) and O columns [0,D/2), warps
 //                8-11 the other halves; the halves exchange their partial row max through shared
 //                memory once per tile. The epilogue stages bf16 O in 128B-swizzled shared memory
@@ -80,7 +80,7 @@ struct FwdParams {
 
 constexpr uint32_t kThreads = 384;
 constexpr uint32_t kTraceCap = 8192;  // events per traced CTA
-constexpr uint32_t kQueue = 4;        // item queue depth (>= 3 items open at the MMA issuer)
+constexpr uint32_t kQueue = 8;        // item queue depth (items open between the producer and the PV issuer)
 
 // Trace event: [63:24] clock64 low 40 bits | [23:16] code | [15] stream | [14:0] aux.
 // Codes: producer 1 Q issued (aux = item), 2 K_k issued, 3 V_k issued;
@@ -100,6 +100,20 @@ __device__ __forceinline__ void trace_ev(bool on, const FwdParams& p, uint32_t* 
 }
 
 constexpr uint32_t kBoxBytes = 128 * 64 * 2;  // 128 rows x 64 bf16, one 128B-swizzle box
+
+// S buffers in TMEM: S_{k+kSBufs} is issued once PV_k (the last reader of P_k, written over S_k)
+// has completed, so the S issuer runs kSBufs tiles ahead of the PV issuer and the softmax engine
+// always finds its next S computed (3 x 128 columns + O at 384: the whole 512-column allocation
+// at D = 128).
+constexpr uint32_t kSBufs = 3;
+// Ring positions in the load order K_0 .. K_{kSBufs-1}, V_0, K_kSBufs, V_1, ...: the order the
+// two MMA issuers consume them in, so a load only waits for the slot freed kRing positions
+// earlier in that same order.
+__host__ __device__ constexpr uint32_t kseq_of(uint32_t k) {
+  return k < kSBufs ? k : 2 * k - (kSBufs - 1);
+}
+__host__ __device__ constexpr uint32_t vseq_of(uint32_t k) { return 2 * k + kSBufs; }
+static_assert(kseq_of(kSBufs) == vseq_of(0) + 1 && vseq_of(1) == kseq_of(kSBufs) + 1, "interleave");
 constexpr float kRescaleThreshold = 8.0f;     // log2 units
 constexpr float kLn2 = 0.69314718055994530942f;
 
@@ -110,7 +124,7 @@ struct Cfg {
   static constexpr uint32_t kRing = (D == 64) ? 10 : 4;       // K/V ring slots
   static constexpr uint32_t kStageBytes = kBoxBytes;          // epilogue staging (two buffers)
   static constexpr uint32_t kTmemCols = 512;
-  static constexpr uint32_t kOCol = 256;
+  static constexpr uint32_t kOCol = kSBufs * 128;
 };
 
 struct ItemDesc {
@@ -121,7 +135,7 @@ struct ItemDesc {
 // smem, so the dynamic base is the 1024-byte aligned start of the CTA's window).
 template <uint32_t kRing>
 struct SmemCtl {
-  uint64_t q_full[2], q_empty[2], s_full[2], p_full[2], o_full, pv_done;
+  uint64_t q_full[2], q_empty[2], s_full[kSBufs], p_full[kSBufs], o_full, pv_done[kSBufs];
   uint64_t ring_full[kRing], ring_empty[kRing];
   uint64_t item_full[kQueue], item_empty[kQueue];
   ItemDesc items[kQueue];
@@ -184,6 +198,14 @@ __device__ __forceinline__ float chunk_max(const uint32_t (&r)[32]) {
   return fmaxf(m0, m1);
 }
 
+// Which of the 16 exponential pairs of a chunk run as a polynomial on the FMA pipe instead of
+// MUFU ex2 (bit i = pair i): 6 of 16 balances the XU pipe (8 cycles per warp instruction) against
+// the extra issue slots of the polynomial (~10 instructions per pair).
+#ifndef BBM_POLY_PAIRS
+#define BBM_POLY_PAIRS 0x0707u
+#endif
+constexpr uint32_t kPolyPairs = BBM_POLY_PAIRS;
+
 // P chunk: 32 scores -> 16 packed bf16x2; accumulates the fp32 sum of the unrounded
 // exponentials into the packed pair `lacc`. Scale/shift and the sum run two lanes per
 // instruction (FFMA2 / FADD2).
@@ -199,11 +221,13 @@ __device__ __forceinline__ void chunk_exp(const uint32_t (&r)[32], uint32_t mw, 
       x0 = ((mw >> i) & 1u) ? x0 : -INFINITY;
       x1 = ((mw >> (i + 1)) & 1u) ? x1 : -INFINITY;
     }
-#ifdef BBM_ABLATE_NO_MUFU  // timing experiments only (tools/ablate.sh): wrong results
-    const float e0 = x0 * 0.5f + 1.0f, e1 = x1 * 0.5f + 1.0f;
-#else
-    const float e0 = fast_exp2(x0), e1 = fast_exp2(x1);
-#endif
+    float e0, e1;
+    if ((kPolyPairs >> ((i / 2) & 15)) & 1u) {
+      exp2_poly2(x0, x1, e0, e1);  // this pair on the FMA pipe
+    } else {
+      e0 = fast_exp2(x0);  // MUFU
+      e1 = fast_exp2(x1);
+    }
     lacc = fadd2(lacc, f2_pack(e0, e1));
     pk[i / 2] = pack_bf16x2(e0, e1);
   }
@@ -244,18 +268,20 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int b = 0; b < 2; ++b) {
       mbar_init(&ctl->q_full[b], 1);
       mbar_init(&ctl->q_empty[b], 1);
+    }
+    for (uint32_t b = 0; b < kSBufs; ++b) {
       mbar_init(&ctl->s_full[b], 1);
       mbar_init(&ctl->p_full[b], 256);
+      mbar_init(&ctl->pv_done[b], 1);
     }
     mbar_init(&ctl->o_full, 1);
-    mbar_init(&ctl->pv_done, 1);
     for (uint32_t r = 0; r < C::kRing; ++r) {
       mbar_init(&ctl->ring_full[r], 1);
       mbar_init(&ctl->ring_empty[r], 1);
     }
     for (uint32_t r = 0; r < kQueue; ++r) {
       mbar_init(&ctl->item_full[r], 1);
-      mbar_init(&ctl->item_empty[r], 2);  // MMA issuer + softmax engine
+      mbar_init(&ctl->item_empty[r], 3);  // S issuer + PV issuer + softmax engine
     }
     fence_barrier_init();
   }
@@ -276,9 +302,9 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   if (warp == 0) {
     // ------------------------------------------------------------------ producer
-    // Loads follow the MMA issuer's consumption order S_0, S_1, PV_0, S_2, PV_1, ..., i.e.
-    // K_0, K_1, V_0, K_2, V_1, K_3, ...: a K cursor runs two tiles ahead of a V cursor, so a load
-    // only ever waits for the ring slot freed kRing positions earlier in that same order.
+    // Loads follow the MMA issuers' consumption order (kseq_of / vseq_of): a K cursor runs kSBufs
+    // tiles ahead of a V cursor, so a load only ever waits for the ring slot freed kRing
+    // positions earlier in that same order.
     if (lane == 0) {
       const uint64_t pol_q = policy_evict_first();
       const uint64_t pol_kv = policy_evict_last();
@@ -333,7 +359,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t cur = kentry;
         // the next list entry is fetched now, a full issue step before it is needed
         if (kj + 1 < kit.nt) kentry = entry_of<MODE>(p, kit.rt, kit.j0 + kj + 1);
-        load_tile(&tm_k, kk == 0 ? 0u : 2 * kk - 1, cur & 0x7FFFFFFFu, kit.slot, 2, kj);
+        load_tile(&tm_k, kseq_of(kk), cur & 0x7FFFFFFFu, kit.slot, 2, kj);
         ++kk;
         if (++kj == kit.nt) k_need = true;
       };
@@ -351,125 +377,90 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         const uint32_t cur = ventry;
         if (vj + 1 < vit.nt) ventry = entry_of<MODE>(p, vit.rt, vit.j0 + vj + 1);
-        load_tile(&tm_v, 2 * vk + 2, cur & 0x7FFFFFFFu, vit.slot, 3, vj);
+        load_tile(&tm_v, vseq_of(vk), cur & 0x7FFFFFFFu, vit.slot, 3, vj);
         ++vk;
         if (++vj == vit.nt) v_need = true;
         return true;
       };
-      for (int w = 0; w < 2; ++w)
+      for (uint32_t w = 0; w < kSBufs; ++w)
         if (k_next()) issue_k();
       while (issue_v())
         if (k_next()) issue_k();
     }
-  } else if (warp == 1) {
-    // ------------------------------------------------------------------ MMA issuer
-    // Two cursors over the tile sequence: the S cursor runs two tiles ahead of the PV cursor.
-    // Ring slots follow the load order K_0, K_1, V_0, K_2, V_1, ...: K_k at position
-    // max(0, 2k-1), V_k at 2k+2 (mod kRing).
+  } else if (warp == 1 || warp == 3) {
+    // ------------------------------------------------------------------ MMA issuers
+    // tcgen05.mma issue is nearly synchronous (~56 cycles per 128x128x16 MMA from an idle pipe,
+    // tools/mma_latency_probe.cu), so one issuing thread competing for issue slots with two
+    // softmax warps on its SMSP cannot keep the tensor pipe fed. Two issuers, each walking the
+    // same tile sequence k = 0, 1, 2, ...:
+    //   warp 1: S_k = Q K_k^T into TMEM buffer k % 3 (SS), once PV_{k-3} (the last reader of
+    //           that buffer's P) has completed;
+    //   warp 3: O += P_k V_k (TS, P read from TMEM) once the softmax engine has written P_k.
+    // Ring slots follow the load order: K_k at kseq_of(k), V_k at vseq_of(k) (mod kRing).
     if (lane == 0) {
+      const bool s_side = warp == 1;
       constexpr uint32_t idesc_s = make_idesc_bf16(128, 128, false, false);
       constexpr uint32_t idesc_o = make_idesc_bf16(128, D, false, true);
       const uint32_t qaddr = smem_u32(sq), raddr = smem_u32(ring);
       const uint32_t tmem_o = tmem + C::kOCol;
-      // S cursor
-      uint32_t sq_i = 0, s_j = 0, s_qb = 0, s_k = 0;
-      uint32_t s_qph[2] = {0, 0};
-      bool s_need_item = true, s_done = false;
-      ItemDesc s_it{};
-      uint32_t s_qi_ph = 0;  // item_full phase for the S cursor's queue index
-      // PV cursor
-      uint32_t pq_i = 0, p_j = 0, p_k = 0;
-      uint32_t p_ph[2] = {0, 0};
-      ItemDesc p_it{};
-      bool p_need_item = true;
-      uint32_t p_qi_ph = 0;
-
-      // advance the S cursor to the next tile; returns false when the sequence ended
-      auto s_next_tile = [&]() -> bool {
-        while (s_need_item) {
-          if (s_done) return false;
-          mbar_wait(&ctl->item_full[sq_i], s_qi_ph);
-          s_it = ctl->items[sq_i];
-          if (++sq_i == kQueue) { sq_i = 0; s_qi_ph ^= 1; }
-          if (s_it.t == kEnd) {
-            s_done = true;
-            return false;
-          }
-          if (s_it.nt == 0) continue;
-          s_need_item = false;
-          s_j = 0;
-        }
-        return true;
-      };
-      auto issue_s = [&]() {
-        const uint32_t buf = s_k & 1;
-        if (s_j == 0) {
-          mbar_wait(&ctl->q_full[s_qb], s_qph[s_qb]);
-          s_qph[s_qb] ^= 1;
-        }
-        const uint32_t kseq = s_k == 0 ? 0u : 2 * s_k - 1;  // load order K_0, K_1, V_0, K_2, V_1, ...
-        const uint32_t slot = kseq % C::kRing;
-        mbar_wait(&ctl->ring_full[slot], (kseq / C::kRing) & 1);
-        trace_ev<kTrace>(tracing, p, &ctl->trace_count, 13, buf, s_j);
-        tc_fence_after();
-        const uint64_t qdesc = make_sdesc_sw128(qaddr + s_qb * C::kTileBytes, 16, 1024);
-        const uint64_t kdesc = make_sdesc_sw128(raddr + slot * C::kTileBytes, 16, 1024);
-#pragma unroll
-        for (uint32_t kk = 0; kk < D / 16; ++kk) {
-          const uint32_t off = (kk / 4) * kBoxBytes + (kk % 4) * 32;
-          umma_ss(tmem + buf * 128, sdesc_advance(qdesc, off), sdesc_advance(kdesc, off), idesc_s, kk > 0);
-        }
-        tc_commit(&ctl->ring_empty[slot]);
-        tc_commit(&ctl->s_full[buf]);
-        trace_ev<kTrace>(tracing, p, &ctl->trace_count, 10, buf, s_j);
-        if (++s_j == s_it.nt) {
-          tc_commit(&ctl->q_empty[s_qb]);
-          s_qb ^= 1;
-          s_need_item = true;
-        }
-        ++s_k;
-      };
-      // S lookahead of two tiles
-      for (int w = 0; w < 2; ++w)
-        if (s_next_tile()) issue_s();
+      uint32_t qi = 0, qiph = 0, k = 0, qb = 0;
+      uint32_t q_ph[2] = {0, 0}, p_ph[kSBufs] = {};
       for (;;) {
-        // PV cursor: item of tile p_k
-        while (p_need_item) {
-          mbar_wait(&ctl->item_full[pq_i], p_qi_ph);
-          p_it = ctl->items[pq_i];
-          mbar_arrive(&ctl->item_empty[pq_i]);  // released by the PV cursor (the last user)
-          if (++pq_i == kQueue) { pq_i = 0; p_qi_ph ^= 1; }
-          if (p_it.t == kEnd) break;
-          if (p_it.nt == 0) continue;
-          p_need_item = false;
-          p_j = 0;
-        }
-        if (p_need_item) break;  // end of the sequence
-        const uint32_t buf = p_k & 1;
-        mbar_wait(&ctl->p_full[buf], p_ph[buf]);
-        p_ph[buf] ^= 1;
-        trace_ev<kTrace>(tracing, p, &ctl->trace_count, 14, buf, p_j);
-        const uint32_t vseq = 2 * p_k + 2;
-        const uint32_t slot = vseq % C::kRing;
-        mbar_wait(&ctl->ring_full[slot], (vseq / C::kRing) & 1);
-        trace_ev<kTrace>(tracing, p, &ctl->trace_count, 12, buf, p_j);
-        tc_fence_after();
-        const uint64_t vdesc = make_sdesc_sw128(raddr + slot * C::kTileBytes, kBoxBytes, 1024);
-        const uint32_t pcol = tmem + buf * 128;
+        mbar_wait(&ctl->item_full[qi], qiph);
+        const ItemDesc it = ctl->items[qi];
+        mbar_arrive(&ctl->item_empty[qi]);
+        if (++qi == kQueue) { qi = 0; qiph ^= 1; }
+        if (it.t == kEnd) break;
+        if (it.nt == 0) continue;
+        for (uint32_t j = 0; j < it.nt; ++j, ++k) {
+          const uint32_t buf = k % kSBufs;
+          if (s_side) {
+            if (k >= kSBufs) mbar_wait(&ctl->pv_done[buf], ((k - kSBufs) / kSBufs) & 1);
+            if (j == 0) {
+              mbar_wait(&ctl->q_full[qb], q_ph[qb]);
+              q_ph[qb] ^= 1;
+            }
+            const uint32_t kseq = kseq_of(k);
+            const uint32_t slot = kseq % C::kRing;
+            mbar_wait(&ctl->ring_full[slot], (kseq / C::kRing) & 1);
+            trace_ev<kTrace>(tracing, p, &ctl->trace_count, 13, buf, j);
+            tc_fence_after();
+            const uint64_t qdesc = make_sdesc_sw128(qaddr + qb * C::kTileBytes, 16, 1024);
+            const uint64_t kdesc = make_sdesc_sw128(raddr + slot * C::kTileBytes, 16, 1024);
 #pragma unroll
-        for (uint32_t kk = 0; kk < 128 / 16; ++kk)
-          umma_ts(tmem_o, pcol + kk * 8, sdesc_advance(vdesc, kk * 2048), idesc_o,
-                  (p_j > 0 || kk > 0) ? 1u : 0u);
-        tc_commit(&ctl->ring_empty[slot]);
-        tc_commit(&ctl->pv_done);
-        trace_ev<kTrace>(tracing, p, &ctl->trace_count, 11, buf, p_j);
-        if (++p_j == p_it.nt) {
-          tc_commit(&ctl->o_full);
-          p_need_item = true;
+            for (uint32_t kk = 0; kk < D / 16; ++kk) {
+              const uint32_t off = (kk / 4) * kBoxBytes + (kk % 4) * 32;
+              umma_ss(tmem + buf * 128, sdesc_advance(qdesc, off), sdesc_advance(kdesc, off), idesc_s,
+                      kk > 0);
+            }
+            tc_commit(&ctl->ring_empty[slot]);
+            tc_commit(&ctl->s_full[buf]);
+            trace_ev<kTrace>(tracing, p, &ctl->trace_count, 10, buf, j);
+            if (j + 1 == it.nt) {
+              tc_commit(&ctl->q_empty[qb]);
+              qb ^= 1;
+            }
+          } else {
+            mbar_wait(&ctl->p_full[buf], p_ph[buf]);
+            p_ph[buf] ^= 1;
+            trace_ev<kTrace>(tracing, p, &ctl->trace_count, 14, buf, j);
+            const uint32_t vseq = vseq_of(k);
+            const uint32_t slot = vseq % C::kRing;
+            mbar_wait(&ctl->ring_full[slot], (vseq / C::kRing) & 1);
+            trace_ev<kTrace>(tracing, p, &ctl->trace_count, 12, buf, j);
+            tc_fence_after();
+            const uint64_t vdesc = make_sdesc_sw128(raddr + slot * C::kTileBytes, kBoxBytes, 1024);
+            const uint32_t pcol = tmem + buf * 128;
+#pragma unroll
+            for (uint32_t kk = 0; kk < 128 / 16; ++kk)
+              umma_ts(tmem_o, pcol + kk * 8, sdesc_advance(vdesc, kk * 2048), idesc_o,
+                      (j > 0 || kk > 0) ? 1u : 0u);
+            tc_commit(&ctl->ring_empty[slot]);
+            tc_commit(&ctl->pv_done[buf]);
+            trace_ev<kTrace>(tracing, p, &ctl->trace_count, 11, buf, j);
+            if (j + 1 == it.nt) tc_commit(&ctl->o_full);
+          }
         }
-        ++p_k;
-        // S_{k+2} goes into the buffer PV_k just read (in issue order after PV_k)
-        if (s_next_tile()) issue_s();
       }
     }
   } else if (warp >= 4) {
@@ -493,11 +484,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t to = tmem + C::kOCol + lane_off;
 
     uint32_t step = 0;  // parity selects the exchange buffer
-    uint32_t k = 0;     // global tile index (S buffer k % 2)
+    uint32_t k = 0;     // global tile index (S buffer k % kSBufs)
     uint2 nbits = make_uint2(0xFFFFFFFFu, 0xFFFFFFFFu);  // mask bits of the next tile
     uint32_t nentry = 0;                                // its list entry (dense_binblk)
     bool have_next_bits = false;                        // prefetched for the next item
-    uint32_t s_ph[2] = {0, 0}, o_ph = 0, qi = 0, qiph = 0;
+    uint32_t s_ph[kSBufs] = {}, o_ph = 0, qi = 0, qiph = 0;
 
     auto write_stats = [&](const ItemDesc& it, float m_true2, float m_run2, float l_tot) {
       const uint64_t grow = static_cast<uint64_t>(it.rt) * 128 + row;
@@ -560,7 +551,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       have_next_bits = false;
 
       for (uint32_t j = 0; j < it.nt; ++j, ++k) {
-        const uint32_t buf = k & 1;
+        const uint32_t buf = k % kSBufs;
         const uint32_t ts = tmem + buf * 128 + lane_off;
         bool masked;
         uint2 bits = nbits;
@@ -626,7 +617,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         if (__any_sync(0xffffffffu, rescale_o)) {
           // O must be quiescent: PV_{k-1} (the last one issued) has to complete first
-          mbar_wait(&ctl->pv_done, (k - 1) & 1);
+          mbar_wait(&ctl->pv_done[(k - 1) % kSBufs], ((k - 1) / kSBufs) & 1);
           tc_fence_after();
           const float f = rescale_o ? factor : 1.0f;
 #pragma unroll 1

@@ -298,6 +298,31 @@ __device__ __forceinline__ uint64_t fadd2(uint64_t a, uint64_t b) {
   asm("add.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
   return d;
 }
+__device__ __forceinline__ uint64_t fadd2_rm(uint64_t a, uint64_t b) {  // round toward -inf
+  uint64_t d;
+  asm("add.rm.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+
+// 2^x for two lanes on the FMA pipe (no MUFU), FA4-style: j = floor(x) via the 1.5*2^23 magic
+// add rounded toward -inf, f = x - j in [0,1), 2^f by a cubic with p(0) = 1 exactly (max relative
+// error 8.6e-5, far below the bf16 rounding of P), exponent added as an integer. x is clamped at
+// -127, where the result is exactly +0 (so masked -inf scores still give 0).
+__device__ __forceinline__ void exp2_poly2(float x0, float x1, float& e0, float& e1) {
+  constexpr float kMagic = 12582912.0f;  // 1.5 * 2^23
+  const uint64_t x = f2_pack(fmaxf(x0, -127.0f), fmaxf(x1, -127.0f));
+  const uint64_t magic = f2_pack(kMagic, kMagic);
+  const uint64_t t = fadd2_rm(x, magic);                          // floor(x) in the low bits
+  const uint64_t nj = ffma2(t, f2_pack(-1.0f, -1.0f), magic);     // -floor(x), exact
+  const uint64_t fr = fadd2(x, nj);                               // x - floor(x)
+  uint64_t pv = ffma2(fr, f2_pack(0.07706641f, 0.07706641f), f2_pack(0.2276457f, 0.2276457f));
+  pv = ffma2(pv, fr, f2_pack(0.69511664f, 0.69511664f));
+  pv = ffma2(pv, fr, f2_pack(1.0f, 1.0f));
+  const uint32_t tl = static_cast<uint32_t>(t), th = static_cast<uint32_t>(t >> 32);
+  e0 = __uint_as_float(static_cast<uint32_t>(pv) + (tl << 23));
+  e1 = __uint_as_float(static_cast<uint32_t>(pv >> 32) + (th << 23));
+}
+
 __device__ __forceinline__ float fmax3(float a, float b, float c) {
   float d;
   asm("max.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));

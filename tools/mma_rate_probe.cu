@@ -68,6 +68,23 @@ __global__ void __launch_bounds__(384, 1) rate_kernel(int iters, unsigned long l
     }
     if (blockIdx.x == 0) out[1] = n;
   }
+  if (kMufu == 2 && warp >= 4) {
+    // issue-slot hogs: independent FFMA2 chains (no TMEM, no MUFU), like a busy softmax engine
+    uint64_t a = 0x3f8000003f800000ull, b = a, c = a, d = a;
+    const uint64_t m = 0x3f7ff0003f7ff000ull;
+    uint64_t passes = 0;
+    while (!done) {
+#pragma unroll
+      for (int i = 0; i < 64; ++i) {
+        asm volatile("fma.rn.f32x2 %0, %0, %1, %1;" : "+l"(a) : "l"(m));
+        asm volatile("fma.rn.f32x2 %0, %0, %1, %1;" : "+l"(b) : "l"(m));
+        asm volatile("fma.rn.f32x2 %0, %0, %1, %1;" : "+l"(c) : "l"(m));
+        asm volatile("fma.rn.f32x2 %0, %0, %1, %1;" : "+l"(d) : "l"(m));
+      }
+      ++passes;
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 128) out[1] = passes + (a ^ b ^ c ^ d) % 2;
+  }
   if (kLdWarps > 0 && warp >= 4 && warp < 4 + kLdWarps) {
     // TMEM readers like the softmax engine: 64 columns of the second S buffer per pass, plus a
     // 16-column store back, in a loop until the MMA thread is done
@@ -133,5 +150,7 @@ int main() {
   run<1, 128, false, 8>("TS+8ldwarps");
   run<0, 128, false, 8, 1>("SS+8ld+mufu");
   run<1, 128, false, 8, 1>("TS+8ld+mufu");
+  run<0, 128, false, 0, 2>("SS+8fma-hogs");
+  run<1, 128, false, 0, 2>("TS+8fma-hogs");
   return 0;
 }
