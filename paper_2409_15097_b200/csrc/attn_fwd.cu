@@ -102,10 +102,9 @@ __device__ __forceinline__ void trace_ev(bool on, const FwdParams& p, uint32_t* 
 constexpr uint32_t kBoxBytes = 128 * 64 * 2;  // 128 rows x 64 bf16, one 128B-swizzle box
 
 // S buffers in TMEM: S_{k+kSBufs} is issued once PV_k (the last reader of P_k, written over S_k)
-// has completed, so the S issuer runs kSBufs tiles ahead of the PV issuer and the softmax engine
-// always finds its next S computed (3 x 128 columns + O at 384: the whole 512-column allocation
-// at D = 128).
-constexpr uint32_t kSBufs = 3;
+// has completed, so the S issuer runs kSBufs tiles ahead of the PV issuer. TMEM at D = 128:
+// S at 0 and 128, two O accumulators at 256 and 384 (the whole 512-column allocation).
+constexpr uint32_t kSBufs = 2;
 // Ring positions in the load order K_0 .. K_{kSBufs-1}, V_0, K_kSBufs, V_1, ...: the order the
 // two MMA issuers consume them in, so a load only waits for the slot freed kRing positions
 // earlier in that same order.
@@ -135,7 +134,7 @@ struct ItemDesc {
 // smem, so the dynamic base is the 1024-byte aligned start of the CTA's window).
 template <uint32_t kRing>
 struct SmemCtl {
-  uint64_t q_full[2], q_empty[2], s_full[kSBufs], p_full[kSBufs], o_full, pv_done[kSBufs];
+  uint64_t q_full[2], q_empty[2], s_full[kSBufs], p_full[kSBufs], o_full[2], o_empty[2], pv_done[kSBufs];
   uint64_t ring_full[kRing], ring_empty[kRing];
   uint64_t item_full[kQueue], item_empty[kQueue];
   ItemDesc items[kQueue];
@@ -274,7 +273,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&ctl->p_full[b], 256);
       mbar_init(&ctl->pv_done[b], 1);
     }
-    mbar_init(&ctl->o_full, 1);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&ctl->o_full[b], 1);
+      mbar_init(&ctl->o_empty[b], 256);
+    }
     for (uint32_t r = 0; r < C::kRing; ++r) {
       mbar_init(&ctl->ring_full[r], 1);
       mbar_init(&ctl->ring_empty[r], 1);
@@ -402,9 +404,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       constexpr uint32_t idesc_s = make_idesc_bf16(128, 128, false, false);
       constexpr uint32_t idesc_o = make_idesc_bf16(128, D, false, true);
       const uint32_t qaddr = smem_u32(sq), raddr = smem_u32(ring);
-      const uint32_t tmem_o = tmem + C::kOCol;
-      uint32_t qi = 0, qiph = 0, k = 0, qb = 0;
-      uint32_t q_ph[2] = {0, 0}, p_ph[kSBufs] = {};
+      uint32_t qi = 0, qiph = 0, k = 0, qb = 0, items = 0;
+      uint32_t q_ph[2] = {0, 0}, p_ph[kSBufs] = {}, oe_ph[2] = {1, 1};
       for (;;) {
         mbar_wait(&ctl->item_full[qi], qiph);
         const ItemDesc it = ctl->items[qi];
@@ -412,6 +413,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (++qi == kQueue) { qi = 0; qiph ^= 1; }
         if (it.t == kEnd) break;
         if (it.nt == 0) continue;
+        // items alternate between the two O accumulators; an item's first PV waits until the
+        // engine has read out the item two back (its deferred epilogue)
+        const uint32_t ob = items++ & 1;
+        const uint32_t tmem_o = tmem + C::kOCol + ob * D;
         for (uint32_t j = 0; j < it.nt; ++j, ++k) {
           const uint32_t buf = k % kSBufs;
           if (s_side) {
@@ -444,6 +449,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             mbar_wait(&ctl->p_full[buf], p_ph[buf]);
             p_ph[buf] ^= 1;
             trace_ev<kTrace>(tracing, p, &ctl->trace_count, 14, buf, j);
+            if (j == 0) {
+              mbar_wait(&ctl->o_empty[ob], oe_ph[ob]);
+              oe_ph[ob] ^= 1;
+            }
             const uint32_t vseq = vseq_of(k);
             const uint32_t slot = vseq % C::kRing;
             mbar_wait(&ctl->ring_full[slot], (vseq / C::kRing) & 1);
@@ -458,7 +467,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             tc_commit(&ctl->ring_empty[slot]);
             tc_commit(&ctl->pv_done[buf]);
             trace_ev<kTrace>(tracing, p, &ctl->trace_count, 11, buf, j);
-            if (j + 1 == it.nt) tc_commit(&ctl->o_full);
+            if (j + 1 == it.nt) tc_commit(&ctl->o_full[ob]);
           }
         }
       }
@@ -481,14 +490,26 @@ __global__ void __launch_bounds__(kThreads, 1)
     // has to drop out of the max (the exp pass selects explicitly)
     const uint32_t sentinel = neg ? 0x7F800000u : 0xFF800000u;
     constexpr uint32_t kHalfO = D / 2;  // O columns per half
-    const uint32_t to = tmem + C::kOCol + lane_off;
+    const uint32_t to_base = tmem + C::kOCol + lane_off;
 
     uint32_t step = 0;  // parity selects the exchange buffer
     uint32_t k = 0;     // global tile index (S buffer k % kSBufs)
     uint2 nbits = make_uint2(0xFFFFFFFFu, 0xFFFFFFFFu);  // mask bits of the next tile
     uint32_t nentry = 0;                                // its list entry (dense_binblk)
     bool have_next_bits = false;                        // prefetched for the next item
-    uint32_t s_ph[kSBufs] = {}, o_ph = 0, qi = 0, qiph = 0;
+    uint32_t s_ph[kSBufs] = {}, qi = 0, qiph = 0, items = 0;
+    uint32_t o_ph[2] = {0, 0};
+    // The epilogue of an item is DEFERRED until the next item's first tile has been handed to
+    // the tensor core: the engine never idles while the item's last PV drains (the two items use
+    // different O accumulators). At most one epilogue is pending at a time.
+    struct Pending {
+      ItemDesc it;
+      float l_unit, m_run, m_true;
+      uint32_t ob;
+      bool valid;
+    };
+    Pending pend{};
+    pend.valid = false;
 
     auto write_stats = [&](const ItemDesc& it, float m_true2, float m_run2, float l_tot) {
       const uint64_t grow = static_cast<uint64_t>(it.rt) * 128 + row;
@@ -534,6 +555,108 @@ __global__ void __launch_bounds__(kThreads, 1)
       if constexpr (MODE == kModeDenseBinblk) entry = entry_of<MODE>(p, it.rt, jj);
     };
 
+    auto finish = [&](const Pending& pd) {
+      const ItemDesc& it = pd.it;
+      const float l_unit = pd.l_unit, m_run = pd.m_run, m_true = pd.m_true;
+      const uint32_t to = to_base + pd.ob * D;
+      if (leader) bulk_wait_group_read<0>();  // staging buffers free again
+      mbar_wait(&ctl->o_full[pd.ob], o_ph[pd.ob]);
+      o_ph[pd.ob] ^= 1;
+      tc_fence_after();
+      named_bar_sync(1, 256);
+      if (tracer) trace_ev<kTrace>(tracing, p, &ctl->trace_count, 23, 0, it.t);
+      if (it.split == kNoSplit) {
+        const float inv = l_unit > 0.0f ? 1.0f / l_unit : 0.0f;
+#pragma unroll
+        for (uint32_t c32 = 0; c32 < kHalfO / 32; ++c32) {
+          uint32_t o[32];
+          tmem_ld32(to + half * kHalfO + c32 * 32, o);
+          tmem_ld_wait();
+          stage_chunk32(stg_row, row, D == 128 ? c32 * 4 : half * 4,
+                        reinterpret_cast<const float*>(o), inv);
+        }
+        tc_fence_before();
+        mbar_arrive(&ctl->o_empty[pd.ob]);  // the accumulator may be overwritten from here on
+        store_staged(it);
+        write_stats(it, m_true, m_run, l_unit);
+      } else {
+        // ---- split-KV chunk: publish the unnormalized partial, the last chunk combines
+        const uint32_t srow = it.split >> 8, chunk = it.split & 0xFF;
+        const uint2 si = p.split_info[srow];  // {chunks, first workspace chunk}
+        const uint64_t blk = static_cast<uint64_t>(128) * (D + 3);
+        float* wsb = p.ws + (static_cast<uint64_t>(it.slot) * p.split_chunks + si.y + chunk) * blk;
+#pragma unroll
+        for (uint32_t c32 = 0; c32 < kHalfO / 32; ++c32) {
+          uint32_t o[32];
+          tmem_ld32(to + half * kHalfO + c32 * 32, o);
+          tmem_ld_wait();
+          uint4* dst = reinterpret_cast<uint4*>(wsb + row * D + half * kHalfO + c32 * 32);
+#pragma unroll
+          for (uint32_t v = 0; v < 8; ++v)
+            dst[v] = make_uint4(o[v * 4], o[v * 4 + 1], o[v * 4 + 2], o[v * 4 + 3]);
+        }
+        tc_fence_before();
+        mbar_arrive(&ctl->o_empty[pd.ob]);
+        if (half == 0) {
+          wsb[128 * D + row] = m_run;
+          wsb[128 * D + 128 + row] = m_true;
+          wsb[128 * D + 256 + row] = l_unit;
+        }
+        __threadfence();
+        named_bar_sync(1, 256);
+        uint32_t* ctr = p.split_ctr + static_cast<uint64_t>(it.slot) * p.split_rows + srow;
+        if (leader) ctl->bcast = atomicAdd(ctr, 1u);
+        named_bar_sync(1, 256);
+        const uint32_t done_before = ctl->bcast;
+        if (done_before + 1 == si.x) {
+          // last chunk: combine every chunk's partial for this row tile
+          __threadfence();
+          const float* base = p.ws + (static_cast<uint64_t>(it.slot) * p.split_chunks + si.y) * blk;
+          float mrun = -INFINITY, mtrue = -INFINITY;
+          for (uint32_t c = 0; c < si.x; ++c) {
+            const float* b = base + c * blk + 128 * D;
+            if (__ldcg(b + 256 + row) > 0.0f) mrun = fmaxf(mrun, __ldcg(b + row));
+            mtrue = fmaxf(mtrue, __ldcg(b + 128 + row));
+          }
+          float ltot = 0.0f;
+          for (uint32_t c = 0; c < si.x; ++c) {
+            const float* b = base + c * blk + 128 * D;
+            const float lc = __ldcg(b + 256 + row);
+            if (lc > 0.0f) ltot += lc * exp2f(__ldcg(b + row) - mrun);
+          }
+          const float inv = ltot > 0.0f ? 1.0f / ltot : 0.0f;
+          named_bar_sync(1, 256);  // every engine thread has read the count
+          if (leader) *ctr = 0;    // ready for the next launch
+#pragma unroll 1
+          for (uint32_t c32 = 0; c32 < kHalfO / 32; ++c32) {
+            float acc[32];
+#pragma unroll
+            for (uint32_t i = 0; i < 32; ++i) acc[i] = 0.0f;
+            for (uint32_t c = 0; c < si.x; ++c) {
+              const float* b = base + c * blk;
+              const float lc = __ldcg(b + 128 * D + 256 + row);
+              if (!(lc > 0.0f)) continue;
+              const float w = exp2f(__ldcg(b + 128 * D + row) - mrun);
+              const float4* src = reinterpret_cast<const float4*>(b + row * D + half * kHalfO + c32 * 32);
+#pragma unroll
+              for (uint32_t v = 0; v < 8; ++v) {
+                const float4 f = __ldcg(src + v);
+                acc[v * 4 + 0] += w * f.x;
+                acc[v * 4 + 1] += w * f.y;
+                acc[v * 4 + 2] += w * f.z;
+                acc[v * 4 + 3] += w * f.w;
+              }
+            }
+            stage_chunk32(stg_row, row, D == 128 ? c32 * 4 : half * 4, acc, inv);
+          }
+          store_staged(it);
+          write_stats(it, mtrue, mrun, ltot);
+        }
+      }
+      if (tracer) trace_ev<kTrace>(tracing, p, &ctl->trace_count, 24, 0, it.t);
+      pend.valid = false;
+    };
+
     for (;;) {
       // ---------------- next item (items without tiles are written as zeros right away)
       mbar_wait(&ctl->item_full[qi], qiph);
@@ -547,6 +670,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         continue;
       }
       float m_run = -INFINITY, m_true = -INFINITY, l = 0.0f;
+      const uint32_t ob = items++ & 1;  // this item's O accumulator (same sequence as the PV issuer)
+      const uint32_t to = to_base + ob * D;
       if (!have_next_bits) load_bits(it, it.j0, nbits, nentry);  // else prefetched last item
       have_next_bits = false;
 
@@ -654,108 +779,21 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc_fence_before();
         mbar_arrive(&ctl->p_full[buf]);
         if (tracer) trace_ev<kTrace>(tracing, p, &ctl->trace_count, 22, buf, j);
+        if (j == 0 && pend.valid) finish(pend);  // the previous item's last PV has drained meanwhile
       }
 
-      // ---------------- epilogue: the item's last PV completes while the row sums are combined
+      // ---------------- item end: combine the halves' row sums now; the O readout is deferred
       ctl->xchg[step & 1][half][row] = l;
-      if (leader) bulk_wait_group_read<0>();  // staging buffers free again
-      mbar_wait(&ctl->o_full, o_ph);
-      o_ph ^= 1;
-      tc_fence_after();
       named_bar_sync(1, 256);
-      const float l_unit = l + ctl->xchg[step & 1][half ^ 1][row];
+      pend.l_unit = l + ctl->xchg[step & 1][half ^ 1][row];
       ++step;
-      if (tracer) trace_ev<kTrace>(tracing, p, &ctl->trace_count, 23, 0, it.t);
-      if (it.split == kNoSplit) {
-        const float inv = l_unit > 0.0f ? 1.0f / l_unit : 0.0f;
-#pragma unroll
-        for (uint32_t c32 = 0; c32 < kHalfO / 32; ++c32) {
-          uint32_t o[32];
-          tmem_ld32(to + half * kHalfO + c32 * 32, o);
-          tmem_ld_wait();
-          stage_chunk32(stg_row, row, D == 128 ? c32 * 4 : half * 4,
-                        reinterpret_cast<const float*>(o), inv);
-        }
-        // O may be overwritten from here on: the next item's first PV waits for this engine's
-        // next p_full arrival, which comes after these loads completed
-        tc_fence_before();
-        store_staged(it);
-        write_stats(it, m_true, m_run, l_unit);
-      } else {
-        // ---- split-KV chunk: publish the unnormalized partial, the last chunk combines
-        const uint32_t srow = it.split >> 8, chunk = it.split & 0xFF;
-        const uint2 si = p.split_info[srow];  // {chunks, first workspace chunk}
-        const uint64_t blk = static_cast<uint64_t>(128) * (D + 3);
-        float* wsb = p.ws + (static_cast<uint64_t>(it.slot) * p.split_chunks + si.y + chunk) * blk;
-#pragma unroll
-        for (uint32_t c32 = 0; c32 < kHalfO / 32; ++c32) {
-          uint32_t o[32];
-          tmem_ld32(to + half * kHalfO + c32 * 32, o);
-          tmem_ld_wait();
-          uint4* dst = reinterpret_cast<uint4*>(wsb + row * D + half * kHalfO + c32 * 32);
-#pragma unroll
-          for (uint32_t v = 0; v < 8; ++v)
-            dst[v] = make_uint4(o[v * 4], o[v * 4 + 1], o[v * 4 + 2], o[v * 4 + 3]);
-        }
-        tc_fence_before();
-        if (half == 0) {
-          wsb[128 * D + row] = m_run;
-          wsb[128 * D + 128 + row] = m_true;
-          wsb[128 * D + 256 + row] = l_unit;
-        }
-        __threadfence();
-        named_bar_sync(1, 256);
-        uint32_t* ctr = p.split_ctr + static_cast<uint64_t>(it.slot) * p.split_rows + srow;
-        if (leader) ctl->bcast = atomicAdd(ctr, 1u);
-        named_bar_sync(1, 256);
-        const uint32_t done_before = ctl->bcast;
-        if (done_before + 1 == si.x) {
-          // last chunk: combine every chunk's partial for this row tile
-          __threadfence();
-          const float* base = p.ws + (static_cast<uint64_t>(it.slot) * p.split_chunks + si.y) * blk;
-          float mrun = -INFINITY, mtrue = -INFINITY;
-          for (uint32_t c = 0; c < si.x; ++c) {
-            const float* b = base + c * blk + 128 * D;
-            if (__ldcg(b + 256 + row) > 0.0f) mrun = fmaxf(mrun, __ldcg(b + row));
-            mtrue = fmaxf(mtrue, __ldcg(b + 128 + row));
-          }
-          float ltot = 0.0f;
-          for (uint32_t c = 0; c < si.x; ++c) {
-            const float* b = base + c * blk + 128 * D;
-            const float lc = __ldcg(b + 256 + row);
-            if (lc > 0.0f) ltot += lc * exp2f(__ldcg(b + row) - mrun);
-          }
-          const float inv = ltot > 0.0f ? 1.0f / ltot : 0.0f;
-          named_bar_sync(1, 256);  // every engine thread has read the count
-          if (leader) *ctr = 0;    // ready for the next launch
-#pragma unroll 1
-          for (uint32_t c32 = 0; c32 < kHalfO / 32; ++c32) {
-            float acc[32];
-#pragma unroll
-            for (uint32_t i = 0; i < 32; ++i) acc[i] = 0.0f;
-            for (uint32_t c = 0; c < si.x; ++c) {
-              const float* b = base + c * blk;
-              const float lc = __ldcg(b + 128 * D + 256 + row);
-              if (!(lc > 0.0f)) continue;
-              const float w = exp2f(__ldcg(b + 128 * D + row) - mrun);
-              const float4* src = reinterpret_cast<const float4*>(b + row * D + half * kHalfO + c32 * 32);
-#pragma unroll
-              for (uint32_t v = 0; v < 8; ++v) {
-                const float4 f = __ldcg(src + v);
-                acc[v * 4 + 0] += w * f.x;
-                acc[v * 4 + 1] += w * f.y;
-                acc[v * 4 + 2] += w * f.z;
-                acc[v * 4 + 3] += w * f.w;
-              }
-            }
-            stage_chunk32(stg_row, row, D == 128 ? c32 * 4 : half * 4, acc, inv);
-          }
-          store_staged(it);
-          write_stats(it, mtrue, mrun, ltot);
-        }
-      }
-      if (tracer) trace_ev<kTrace>(tracing, p, &ctl->trace_count, 24, 0, it.t);
+      pend.it = it;
+      pend.m_run = m_run;
+      pend.m_true = m_true;
+      pend.ob = ob;
+      pend.valid = true;
     }
+    if (pend.valid) finish(pend);
     if (leader) bulk_wait_group<0>();  // O stores landed
   }
 
