@@ -1,26 +1,34 @@
 #!/bin/bash
-# Build timing-only ablations of libbbm (numerically WRONG by design) into ablate/, then
-#   gpurun -- ./ablate/run.sh
-# Each variant removes one piece of the softmax engine to show what bounds the kernel.
+# Build timing-only ablations of libbbm into abl_bin/ (git-ignored, travels with gpurun), then
+#   gpurun -- bash abl_bin/run.sh
+# Each variant removes or changes one piece of the softmax engine to show what bounds the kernel.
+# NO_XCHG / NO_MUFU give numerically WRONG results by design; POLY_* are exact-enough variants.
 set -e
 ROOT=$(cd "$(dirname "$0")/.." && pwd)
-mkdir -p "$ROOT/ablate"
-for v in NO_MUFU NO_XCHG; do
+mkdir -p "$ROOT/abl_bin"
+VARIANTS="${VARIANTS:-NO_XCHG POLY_NONE POLY_HALF}"
+for v in $VARIANTS; do
+  case $v in
+    NO_XCHG) FL="-DBBM_ABLATE_NO_XCHG" ;;
+    POLY_NONE) FL="-DBBM_POLY_PAIRS=0x0000u" ;;
+    POLY_HALF) FL="-DBBM_POLY_PAIRS=0x5555u" ;;
+    POLY_ALL) FL="-DBBM_POLY_PAIRS=0xFFFFu" ;;
+  esac
   rm -rf /tmp/abl_$v && mkdir -p /tmp/abl_$v
   cp -r "$ROOT/paper_2409_15097_b200" "$ROOT/include" /tmp/abl_$v/
-  (cd /tmp/abl_$v/paper_2409_15097_b200/csrc && sed -i "s|^NVFLAGS := |NVFLAGS := -DBBM_ABLATE_$v |; s|^BUILD := .*|BUILD := /tmp/abl_obj_$v|" Makefile && make -j8 >/dev/null)
-  cp /tmp/abl_$v/paper_2409_15097_b200/libbbm.so "$ROOT/ablate/libbbm_$v.so"
+  (cd /tmp/abl_$v/paper_2409_15097_b200/csrc && sed -i "s|^NVFLAGS := |NVFLAGS := $FL |; s|^BUILD := .*|BUILD := /tmp/abl_obj_$v|" Makefile && make -j8 >/dev/null)
+  cp /tmp/abl_$v/paper_2409_15097_b200/libbbm.so "$ROOT/abl_bin/libbbm_$v.so"
 done
-cat > "$ROOT/ablate/run.sh" <<'EOS'
+cat > "$ROOT/abl_bin/run.sh" <<EOS
 #!/bin/bash
-set -e
+mkdir -p gpurun_out
 cp paper_2409_15097_b200/libbbm.so /tmp/libbbm_real.so
-for v in NO_MUFU NO_XCHG; do
-  cp ablate/libbbm_$v.so paper_2409_15097_b200/libbbm.so
-  for var in binblk dense; do
-    echo -n "$v "; python bench.py --config c2 --variant $var --steps 10 --warmup 3 --no-cpu-baseline --no-e2e 2>&1 | tail -1 | python3 tools/bench_summary.py
+for v in base $VARIANTS; do
+  if [ \$v = base ]; then cp /tmp/libbbm_real.so paper_2409_15097_b200/libbbm.so; else cp abl_bin/libbbm_\$v.so paper_2409_15097_b200/libbbm.so; fi
+  for spec in "c2 binblk" "c2 dense" "c4 dense-binblk"; do set -- \$spec
+    echo -n "\$v "; python bench.py --config \$1 --variant \$2 --steps 10 --warmup 3 --no-cpu-baseline --no-e2e 2>&1 | tail -1 | python3 tools/bench_summary.py
   done
-done
+done > gpurun_out/ablate.txt 2>&1
 cp /tmp/libbbm_real.so paper_2409_15097_b200/libbbm.so
 EOS
-chmod +x "$ROOT/ablate/run.sh"
+chmod +x "$ROOT/abl_bin/run.sh"
