@@ -80,9 +80,29 @@ __device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {
   return ok != 0;
 }
 
+// try_wait with a suspend-time hint: the warp sleeps in hardware until the phase completes (or
+// the hint elapses) instead of spinning, so waiting roles do not steal issue slots from the
+// softmax warps sharing their SMSP.
+__device__ __forceinline__ bool mbar_try_wait_sleep(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred P;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P, [%1], %2, %3;\n\t"
+      "selp.u32 %0, 1, 0, P;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity), "r"(0x989680u)
+      : "memory");
+  return ok != 0;
+}
+
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+#ifdef BBM_SPIN_WAIT
   while (!mbar_try_wait(bar, parity)) {
   }
+#else
+  while (!mbar_try_wait_sleep(bar, parity)) {
+  }
+#endif
 }
 
 // ---------------------------------------------------------------- TMA
