@@ -32,7 +32,14 @@ typedef enum {
   BBM_ERR_INVALID = 1,     /* bad argument: reference would throw std::invalid_argument */
   BBM_ERR_CUDA = 2,        /* CUDA runtime / device failure (including "no device") */
   BBM_ERR_UNSUPPORTED = 3, /* valid for the reference, not for the sm_100a kernel (e.g. d=5) */
-  BBM_ERR_INTERNAL = 4
+  BBM_ERR_INTERNAL = 4,
+  /* MaskIoError kinds (mask_io.hpp:24-42) from the mask-file entry points */
+  BBM_ERR_IO_FAILURE = 10,
+  BBM_ERR_IO_BAD_MAGIC = 11,
+  BBM_ERR_IO_BAD_VERSION = 12,
+  BBM_ERR_IO_DIMENSION_OVERFLOW = 13,
+  BBM_ERR_IO_TRUNCATED = 14,
+  BBM_ERR_IO_TRAILING_DATA = 15
 } bbm_status;
 
 /* Variant (engine.hpp:21-26); same numbering as the reference enum. */
@@ -197,9 +204,29 @@ bbm_status bbm_permute_mask_host(const uint64_t* src, uint64_t* dst, const uint3
  * ascending per node (NULL to query offsets only). Host. */
 bbm_status bbm_graph_csr(const uint64_t* words, uint64_t n, uint64_t* offsets, uint32_t* neighbors);
 
+/* ---- mask_io.hpp: BBMK mask files and BBLK occupancy sidecars (mask_io.hpp:14-207), same
+ *      byte layout, 4M-token cap and error kinds (BBM_ERR_IO_*). Host, except
+ *      bbm_preprocess_mask_file, which uploads the file's byte rows as-is and unpacks them on
+ *      the device straight into the preprocessor (read_mask + preprocess_mask). ---- */
+bbm_status bbm_write_mask_file(const char* path, const uint64_t* words, uint64_t n);
+/* words == NULL: query n only. Else words receives n * ceil(n/64) u64 (the Mask layout). */
+bbm_status bbm_read_mask_file(const char* path, uint64_t* n, uint64_t* words);
+/* occ: u8 [ceil(n/bi)][ceil(n/bj)] (BlockOccupancy) */
+bbm_status bbm_write_occupancy_file(const char* path, const uint8_t* occ, uint64_t n_tokens,
+                                    uint64_t block_i, uint64_t block_j);
+/* occ == NULL: query n_tokens / block sizes only. */
+bbm_status bbm_read_occupancy_file(const char* path, uint64_t* n_tokens, uint64_t* block_i,
+                                   uint64_t* block_j, uint8_t* occ);
+bbm_status bbm_preprocess_mask_file(const char* path, uint64_t block_i, uint64_t block_j,
+                                    int device, bbm_prep* out);
+
 /* ---- generators.hpp (host fixtures): MaskSpec grammar (generators.hpp:364-438); families with
  *      a free n take n_free. Call with words == NULL to query n. ---- */
 bbm_status bbm_generate(const char* spec, uint64_t n_free, uint64_t* n_out, uint64_t* words);
+/* make_problem's input stream (bench.hpp:320-337, rng.hpp:15-42): per slot q, k, v, d_out
+ * (n x d each, uniform [-1,1) from one mt19937_64(seed), drawn in that order), as float. Host. */
+bbm_status bbm_make_problem(uint64_t seed, uint64_t slots, uint64_t n, uint64_t d, float* q,
+                            float* k, float* v, float* d_out);
 /* Relabel a mask's tokens by a std::shuffle(mt19937_64(seed)) permutation:
  * out(label[i], label[j]) = in(i, j) (the test_reorder.cpp relabel fixture). */
 bbm_status bbm_relabel(const uint64_t* words, uint64_t n, uint64_t seed, uint64_t* out_words);

@@ -85,18 +85,16 @@ struct MaskPrep {
     device::PrepPtr device;
 };
 
-inline MaskPrep preprocess_mask(const Mask& mask, BlockSpec spec) {
-    spec.validate();
-    require(mask.size() >= 1, "mask must be non-empty");
-    bbm_prep h = nullptr;
-    device::check(bbm_preprocess_packed_host(mask.words(), mask.size(), spec.block_i, spec.block_j,
-                                             device::default_device(), &h),
-                  "preprocess_mask");
+namespace detail {
+/// MaskPrep around a device handle: the host fields are read back from libbbm.
+inline MaskPrep prep_from_handle(bbm_prep h, BlockSpec spec) {
     MaskPrep prep;
     prep.device = std::make_shared<device::PrepHandle>(h);
-    prep.n_tokens = mask.size();
+    bbm_prep_info info{};
+    device::check(bbm_prep_get_info(h, &info), "preprocess_mask");
+    prep.n_tokens = info.n;
     prep.spec = spec;
-    prep.sums = BlockSums(mask.size(), spec);
+    prep.sums = BlockSums(info.n, spec);
     device::check(bbm_prep_get_sums(h, prep.sums.data()), "preprocess_mask");
     prep.occupancy = BlockOccupancy(prep.sums.rows(), prep.sums.cols());
     device::check(bbm_prep_get_occupancy(h, prep.occupancy.data()), "preprocess_mask");
@@ -109,6 +107,17 @@ inline MaskPrep preprocess_mask(const Mask& mask, BlockSpec spec) {
     prep.stats = BlockStats{st.blocks_total, st.blocks_nonzero, st.blocks_full, st.block_density,
                             st.element_density};
     return prep;
+}
+}  // namespace detail
+
+inline MaskPrep preprocess_mask(const Mask& mask, BlockSpec spec) {
+    spec.validate();
+    require(mask.size() >= 1, "mask must be non-empty");
+    bbm_prep h = nullptr;
+    device::check(bbm_preprocess_packed_host(mask.words(), mask.size(), spec.block_i, spec.block_j,
+                                             device::default_device(), &h),
+                  "preprocess_mask");
+    return detail::prep_from_handle(h, spec);
 }
 
 template <typename T>

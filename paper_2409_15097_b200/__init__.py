@@ -8,6 +8,8 @@ sm_100a kernels. Importing fails loudly if the library was not built: there is n
 from . import _lib  # noqa: F401  (raises ImportError when libbbm.so is missing)
 from .blockmask import *  # noqa: F401,F403
 from .blockmask import (BackwardResult, attn_bwd_device, blocked_backward)  # noqa: F401
+from .blockmask import (MaskIoError, OccupancyFile, preprocess_mask_file, read_mask, read_occupancy,  # noqa: F401
+                        write_mask, write_occupancy)
 from .blockmask import (BlockOccupancy, BlockSpec, BlockStats, BlockSums, DenseRuns, EngineCounters,
                         ForwardResult, Mask, MaskPrep, MultiHeadForward, Permutation, SlotInputs,
                         Variant, attn_fwd_device, bandwidth, block_stats, block_sums,

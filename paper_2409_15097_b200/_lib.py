@@ -27,6 +27,9 @@ f64p = C.POINTER(C.c_double)
 vp = C.c_void_p
 
 BBM_OK, BBM_ERR_INVALID, BBM_ERR_CUDA, BBM_ERR_UNSUPPORTED, BBM_ERR_INTERNAL = range(5)
+# MaskIoError kinds (mask_io.hpp:24-42)
+IO_KINDS = {10: "io_failure", 11: "bad_magic", 12: "bad_version", 13: "dimension_overflow",
+            14: "truncated", 15: "trailing_data"}
 
 
 class BlockStatsC(C.Structure):
@@ -84,6 +87,12 @@ SIGNATURES = {
     "bbm_permute_mask_device": (C.c_int, [vp, vp, vp, C.c_uint64, vp]),
     "bbm_generate": (C.c_int, [C.c_char_p, C.c_uint64, u64p, u64p]),
     "bbm_relabel": (C.c_int, [u64p, C.c_uint64, C.c_uint64, u64p]),
+    "bbm_write_mask_file": (C.c_int, [C.c_char_p, u64p, C.c_uint64]),
+    "bbm_read_mask_file": (C.c_int, [C.c_char_p, u64p, u64p]),
+    "bbm_write_occupancy_file": (C.c_int, [C.c_char_p, u8p, C.c_uint64, C.c_uint64, C.c_uint64]),
+    "bbm_read_occupancy_file": (C.c_int, [C.c_char_p, u64p, u64p, u64p, u8p]),
+    "bbm_preprocess_mask_file": (C.c_int, [C.c_char_p, C.c_uint64, C.c_uint64, C.c_int, C.POINTER(vp)]),
+    "bbm_make_problem": (C.c_int, [C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint64, f32p, f32p, f32p, f32p]),
 }
 
 for _name, (_res, _args) in SIGNATURES.items():
@@ -96,11 +105,21 @@ class BbmError(RuntimeError):
     """CUDA / internal failure inside libbbm."""
 
 
+class MaskIoError(RuntimeError):
+    """mask_io.hpp:24-42: a mask / occupancy file problem; ``kind`` names which."""
+
+    def __init__(self, kind: str, msg: str):
+        super().__init__(msg)
+        self.kind = kind
+
+
 def check(status: int) -> None:
     """Map a bbm_status to the reference's error convention (matrix.hpp:47-49)."""
     if status == BBM_OK:
         return
     msg = lib.bbm_last_error().decode(errors="replace")
+    if status in IO_KINDS:
+        raise MaskIoError(IO_KINDS[status], msg)
     if status in (BBM_ERR_INVALID, BBM_ERR_UNSUPPORTED):
         raise ValueError(msg)  # the Python spelling of std::invalid_argument
     raise BbmError(msg)

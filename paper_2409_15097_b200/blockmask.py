@@ -769,3 +769,56 @@ def relabel(mask: Mask, seed: int) -> Mask:
     words = np.ascontiguousarray(mask.words)
     check(lib.bbm_relabel(ptr(words, C.c_uint64), mask.size(), seed, ptr(out.words, C.c_uint64)))
     return out
+
+
+# ----------------------------------------------------------------------------- mask_io.hpp
+
+MaskIoError = _lib.MaskIoError
+
+
+def write_mask(mask: Mask, path: str) -> None:
+    """write_mask (mask_io.hpp:134-144): "BBMK", version 1, n (u64 LE), ceil(n/8)-byte rows."""
+    check(lib.bbm_write_mask_file(str(path).encode(), ptr(mask.words, C.c_uint64), mask.size()))
+
+
+def read_mask(path: str) -> Mask:
+    """read_mask (mask_io.hpp:146-162); raises MaskIoError with the reference's kinds."""
+    n = C.c_uint64(0)
+    check(lib.bbm_read_mask_file(str(path).encode(), C.byref(n), None))
+    m = Mask(int(n.value))
+    check(lib.bbm_read_mask_file(str(path).encode(), C.byref(n), ptr(m.words, C.c_uint64)))
+    return m
+
+
+@dataclass
+class OccupancyFile:
+    """mask_io.hpp:164-168."""
+    n_tokens: int
+    spec: BlockSpec
+    occupancy: BlockOccupancy
+
+
+def write_occupancy(occ: BlockOccupancy, n_tokens: int, spec: BlockSpec, path: str) -> None:
+    """write_occupancy (mask_io.hpp:170-181): the "BBLK" sidecar."""
+    vals = np.ascontiguousarray(occ.values, dtype=np.uint8)
+    check(lib.bbm_write_occupancy_file(str(path).encode(), ptr(vals, C.c_uint8), n_tokens, spec.block_i,
+                                       spec.block_j))
+
+
+def read_occupancy(path: str) -> OccupancyFile:
+    """read_occupancy (mask_io.hpp:183-207)."""
+    n, bi, bj = C.c_uint64(0), C.c_uint64(0), C.c_uint64(0)
+    check(lib.bbm_read_occupancy_file(str(path).encode(), C.byref(n), C.byref(bi), C.byref(bj), None))
+    rows, cols = -(-n.value // bi.value), -(-n.value // bj.value)
+    occ = np.zeros((rows, cols), np.uint8)
+    check(lib.bbm_read_occupancy_file(str(path).encode(), C.byref(n), C.byref(bi), C.byref(bj),
+                                      ptr(occ, C.c_uint8)))
+    return OccupancyFile(int(n.value), BlockSpec(int(bi.value), int(bj.value)), BlockOccupancy(occ))
+
+
+def preprocess_mask_file(path: str, spec: BlockSpec = BlockSpec(), device: int = 0) -> MaskPrep:
+    """read_mask + preprocess_mask with the file's byte rows unpacked on the device."""
+    spec.validate()
+    h = C.c_void_p()
+    check(lib.bbm_preprocess_mask_file(str(path).encode(), spec.block_i, spec.block_j, device, C.byref(h)))
+    return _prep_from_handle(h)

@@ -160,6 +160,10 @@ void launch_compact_bitmaps(const KernelMeta& km, cudaStream_t s);
 void launch_finalize(const uint64_t* d_row_stats, uint64_t rows, const uint32_t* d_cnt,
                      uint32_t* d_order, uint64_t* d_totals /* 3 */, cudaStream_t s);
 
+// ---- mask files (mask_io.cu) ----
+void launch_bbmk_unpack(const uint8_t* d_payload, uint64_t n, uint64_t* d_words, uint64_t wpr,
+                        uint64_t rows_out, cudaStream_t s);
+
 // ---- permutation kernels (permute.cu) ----
 void launch_permute_rows(const void* src, void* dst, const uint32_t* d_fwd, uint64_t slots,
                          uint64_t n, uint64_t row_bytes, bool inverse, cudaStream_t s);

@@ -335,3 +335,19 @@ extern "C" bbm_status bbm_relabel(const uint64_t* words, uint64_t n, uint64_t se
       }
   });
 }
+
+// make_problem's input stream (bench.hpp:320-337, rng.hpp:15-42): per slot q, k, v and d_out,
+// each n x d entries uniform in [-1, 1) from one std::mt19937_64(seed), in that order; stored as
+// float (the reference's Matrix<float>; its double variant draws the identical doubles).
+extern "C" bbm_status bbm_make_problem(uint64_t seed, uint64_t slots, uint64_t n, uint64_t d,
+                                       float* q, float* k, float* v, float* d_out) {
+  return guard([&] {
+    require(q && k && v && d_out, "null argument");
+    std::mt19937_64 gen(seed);
+    const uint64_t per = n * d;
+    for (uint64_t s = 0; s < slots; ++s)
+      for (float* dst : {q, k, v, d_out})
+        for (uint64_t i = 0; i < per; ++i)
+          dst[s * per + i] = static_cast<float>(2.0 * (static_cast<double>(gen() >> 11) * 0x1.0p-53) - 1.0);
+  });
+}

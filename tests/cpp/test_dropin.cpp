@@ -21,6 +21,7 @@
 #include "blockmask/engine.hpp"
 #include "blockmask/generators.hpp"
 #include "blockmask/mask.hpp"
+#include "blockmask/mask_io.hpp"
 #include "blockmask/reorder.hpp"
 
 using namespace blockmask;
@@ -197,6 +198,29 @@ int main() {
   run("BlockModel.InvalidSpecsRejected (test_mask_model.cpp:191-195)", [] {
     EXPECT_THROW_INVALID(BlockSpec({0, 4}).validate());
     EXPECT_THROW_INVALID(block_sums(gen_causal(4), BlockSpec{0, 2}));
+  });
+
+  run("MaskIo.RoundTripErrorsAndDevicePath (test_mask_model.cpp:224-323)", [] {
+    const std::filesystem::path dir = std::filesystem::temp_directory_path();
+    const Mask mask = gen_random_sparse(77, 0.2, 3, false);
+    const auto path = dir / "bbm_dropin.bbmk";
+    write_mask(mask, path);
+    EXPECT(std::filesystem::file_size(path) == 13 + 77 * 10);
+    EXPECT(read_mask(path) == mask);
+    bool kinded = false;
+    try {
+      read_mask(dir / "bbm_dropin_missing.bbmk");
+    } catch (const MaskIoError& e) {
+      kinded = e.kind() == MaskIoError::Kind::io_failure;
+    }
+    EXPECT(kinded);
+    const MaskPrep a = preprocess_mask_file(path, BlockSpec{16, 8});
+    const MaskPrep b = preprocess_mask(mask, BlockSpec{16, 8});
+    EXPECT(a.occupancy == b.occupancy && a.runs == b.runs && a.stats.blocks_nonzero == b.stats.blocks_nonzero);
+    const auto occ_path = dir / "bbm_dropin.bblk";
+    write_occupancy(b.occupancy, 77, BlockSpec{16, 8}, occ_path);
+    const OccupancyFile f = read_occupancy(occ_path);
+    EXPECT(f.n_tokens == 77 && f.spec == (BlockSpec{16, 8}) && f.occupancy == b.occupancy);
   });
 
   // ---------------------------------------------------------------- engine
