@@ -86,7 +86,7 @@ constexpr uint32_t kQueue = 8;        // item queue depth (items open between th
 // Codes: producer 1 Q issued (aux = item), 2 K_k issued, 3 V_k issued;
 //        MMA 10 S_k issued, 11 PV_k issued, 12 V_k landed, 13 K_k landed, 14 P_k seen;
 //        softmax 20 s_full wait begin, 21 s_full wait end, 22 p_full arrive, 23 o_full wait end,
-//        24 epilogue done.
+//        24 epilogue done, 25 S in registers, 26 row max exchanged, 27 P computed.
 template <bool kTrace>
 __device__ __forceinline__ void trace_ev(bool on, const FwdParams& p, uint32_t* counter,
                                          uint32_t code, uint32_t stream, uint32_t aux) {
@@ -715,6 +715,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         tmem_ld32(ts + half * 64, a0);
         tmem_ld32(ts + half * 64 + 32, a1);
         tmem_ld_wait();
+        if (tracer) trace_ev<kTrace>(tracing, p, &ctl->trace_count, 25, buf, j);
         if (masked) {
           apply_mask(a0, bits.x, sentinel);
           apply_mask(a1, bits.y, sentinel);
@@ -731,6 +732,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         float tmax = fmaxf(pmax, ctl->xchg[step & 1][half ^ 1][row]);
 #endif
         ++step;
+        if (tracer) trace_ev<kTrace>(tracing, p, &ctl->trace_count, 26, buf, j);
         tmax = tmax == -INFINITY ? -INFINITY : tmax * abs_sl2;  // log2 domain
         m_true = fmaxf(m_true, tmax);
         const bool need = tmax > m_run + kRescaleThreshold || (m_run == -INFINITY && tmax > -INFINITY);
@@ -775,6 +777,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           tmem_st16(ts + half * 32 + 16, pk);
         }
         l += f2_lo(lacc) + f2_hi(lacc);
+        if (tracer) trace_ev<kTrace>(tracing, p, &ctl->trace_count, 27, buf, j);
         tmem_st_wait();
         tc_fence_before();
         mbar_arrive(&ctl->p_full[buf]);

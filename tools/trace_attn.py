@@ -17,7 +17,7 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
-NAMES = {1: "P:Q", 2: "P:K", 3: "P:V", 10: "M:S", 11: "M:PV", 12: "M:Vready", 13: "M:Kready", 14: "M:Pseen", 20: "X:swait", 21: "X:sready",
+NAMES = {1: "P:Q", 2: "P:K", 3: "P:V", 10: "M:S", 11: "M:PV", 12: "M:Vready", 13: "M:Kready", 14: "M:Pseen", 25: "X:sregs", 26: "X:maxed", 27: "X:pcomp", 20: "X:swait", 21: "X:sready",
          22: "X:pready", 23: "X:oready", 24: "X:epi_done"}
 
 
@@ -58,7 +58,7 @@ def main():
         evs.sort()
         t0 = evs[0][0]
         for t, code, s, aux in evs:
-            lines.append(f"cta{c} {t - t0:9d} s{s} {NAMES.get(code, code):10s} {aux}")
+            lines.append(f"cta{c} {t - t0:9d} s{s} {str(NAMES.get(code, code)):10s} {aux}")
         # per stream stage latencies
         per = collections.defaultdict(list)
         last = {}
@@ -69,6 +69,14 @@ def main():
                 per["S issue -> softmax has S"].append(t - last[(s, 10)])
             if code == 21 and (s, 20) in last:
                 per["softmax waited for S"].append(t - last[(s, 20)])
+            if code == 25 and (s, 21) in last:
+                per["  S ready -> S in registers"].append(t - last[(s, 21)])
+            if code == 26 and (s, 25) in last:
+                per["  S in registers -> row max exchanged"].append(t - last[(s, 25)])
+            if code == 27 and (s, 26) in last:
+                per["  max exchanged -> P computed"].append(t - last[(s, 26)])
+            if code == 22 and (s, 27) in last:
+                per["  P computed -> P stored + arrive"].append(t - last[(s, 27)])
             if code == 22 and (s, 21) in last:
                 per["softmax compute (S ready -> P ready)"].append(t - last[(s, 21)])
             if code == 11 and (s, 22) in last:
