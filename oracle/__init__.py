@@ -68,6 +68,8 @@ def orc():
                                         C.c_double, f64p, f64p, f64p, C.c_int]
         L.orc_naive_backward.argtypes = [f64p, f64p, f64p, f64p, C.c_uint64, C.c_uint64, C.c_double,
                                          u64p, f64p, f64p, f64p, C.c_int]
+        L.orc_naive_rows.argtypes = [f64p, f64p, f64p, f64p, C.c_uint64, C.c_uint64, C.c_double, u64p,
+                                     u64p, C.c_uint64, f64p, f64p, f64p, f64p]
         L.orc_rcm_order.argtypes = [u64p, C.c_uint64, u32p]
         L.orc_bandwidth.argtypes = [u64p, C.c_uint64]
         L.orc_bandwidth.restype = C.c_uint64
@@ -200,6 +202,26 @@ def naive_backward(q, k, v, d_out, scale: float, words, n: int, threads: int = 8
                              n, d, scale, None if w is None else _p(w, C.c_uint64), _p(dq, C.c_double),
                              _p(dk, C.c_double), _p(dv, C.c_double), threads)
     return dq, dk, dv
+
+
+def naive_rows(q, k, v, scale: float, words, n: int, rows, d_out=None):
+    """Forward (out, row_max, row_sum) and, with d_out, dq of the listed query rows only
+    (reference.hpp:42-139 restated per row); q, k, v, d_out [n][d]. words=None: dense."""
+    q, k, v = (np.ascontiguousarray(a, dtype=np.float64) for a in (q, k, v))
+    g = None if d_out is None else np.ascontiguousarray(d_out, dtype=np.float64)
+    r = np.ascontiguousarray(rows, dtype=np.uint64)
+    d = q.shape[1]
+    out = np.zeros((r.size, d), np.float64)
+    rmax = np.zeros(r.size, np.float64)
+    rsum = np.zeros(r.size, np.float64)
+    dq = None if g is None else np.zeros((r.size, d), np.float64)
+    w = None if words is None else np.ascontiguousarray(words, dtype=np.uint64)
+    orc().orc_naive_rows(_p(q, C.c_double), _p(k, C.c_double), _p(v, C.c_double),
+                         None if g is None else _p(g, C.c_double), n, d, scale,
+                         None if w is None else _p(w, C.c_uint64), _p(r, C.c_uint64), r.size,
+                         _p(out, C.c_double), _p(rmax, C.c_double), _p(rsum, C.c_double),
+                         None if dq is None else _p(dq, C.c_double))
+    return out, rmax, rsum, dq
 
 
 def ref_naive_backward(q, k, v, d_out, scale: float, words, n: int):

@@ -370,6 +370,65 @@ void orc_naive_backward(const double* q, const double* k, const double* v, const
   free(jobs);
 }
 
+/* reference.hpp:42-81 (forward) and the dq half of reference.hpp:84-139 (backward) for a LIST
+ * of query rows only — each row needs nothing but its own softmax, so full-size problems can be
+ * spot-checked row by row. Outputs are indexed by list position: out [nrows][d], row_max /
+ * row_sum [nrows], dq [nrows][d] (skipped when dout == NULL). words == NULL: every key visible. */
+void orc_naive_rows(const double* q, const double* k, const double* v, const double* dout,
+                    uint64_t n, uint64_t d, double scale, const uint64_t* words,
+                    const uint64_t* rows, uint64_t nrows, double* out, double* row_max,
+                    double* row_sum, double* dq) {
+  const uint64_t wpr = wpr_of(n);
+  double* s = (double*)malloc(sizeof(double) * (n ? n : 1));
+  double* dp = (double*)malloc(sizeof(double) * (n ? n : 1));
+  for (uint64_t r = 0; r < nrows; ++r) {
+    const uint64_t i = rows[r];
+    double m = -INFINITY;
+    for (uint64_t c = 0; c < n; ++c) {
+      if (words && !((words[i * wpr + (c >> 6)] >> (c & 63)) & 1u)) continue;
+      double t = 0.0;
+      for (uint64_t x = 0; x < d; ++x) t += q[i * d + x] * k[c * d + x];
+      s[c] = scale * t;
+      if (s[c] > m) m = s[c];
+    }
+    row_max[r] = m;
+    for (uint64_t x = 0; x < d; ++x) out[r * d + x] = 0.0;
+    if (dq)
+      for (uint64_t x = 0; x < d; ++x) dq[r * d + x] = 0.0;
+    if (isinf(m)) { /* no visible key: zero output, nothing flows back */
+      row_sum[r] = 0.0;
+      continue;
+    }
+    double l = 0.0;
+    for (uint64_t c = 0; c < n; ++c) {
+      if (words && !((words[i * wpr + (c >> 6)] >> (c & 63)) & 1u)) continue;
+      const double p = exp(s[c] - m);
+      s[c] = p;
+      l += p;
+      for (uint64_t x = 0; x < d; ++x) out[r * d + x] += p * v[c * d + x];
+    }
+    row_sum[r] = l;
+    for (uint64_t x = 0; x < d; ++x) out[r * d + x] /= l;
+    if (!dq) continue;
+    double delta = 0.0;
+    for (uint64_t c = 0; c < n; ++c) {
+      if (words && !((words[i * wpr + (c >> 6)] >> (c & 63)) & 1u)) continue;
+      s[c] /= l;
+      double t = 0.0;
+      for (uint64_t x = 0; x < d; ++x) t += dout[i * d + x] * v[c * d + x];
+      dp[c] = t;
+      delta += s[c] * t;
+    }
+    for (uint64_t c = 0; c < n; ++c) {
+      if (words && !((words[i * wpr + (c >> 6)] >> (c & 63)) & 1u)) continue;
+      const double ds = s[c] * (dp[c] - delta);
+      for (uint64_t x = 0; x < d; ++x) dq[r * d + x] += scale * ds * k[c * d + x];
+    }
+  }
+  free(s);
+  free(dp);
+}
+
 /* -------------------------------------------------------------- reorder.hpp */
 typedef struct {
   uint64_t n;

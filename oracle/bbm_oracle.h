@@ -74,6 +74,11 @@ void orc_dense_forward(const double* q, const double* k, const double* v, uint64
 void orc_naive_backward(const double* q, const double* k, const double* v, const double* dout,
                         uint64_t n, uint64_t d, double scale, const uint64_t* words, double* dq,
                         double* dk, double* dv, int threads);
+/* forward (+ dq) of a list of query rows only (reference.hpp:42-139 restated per row) */
+void orc_naive_rows(const double* q, const double* k, const double* v, const double* dout,
+                    uint64_t n, uint64_t d, double scale, const uint64_t* words,
+                    const uint64_t* rows, uint64_t nrows, double* out, double* row_max,
+                    double* row_sum, double* dq);
 int orc_rcm_order(const uint64_t* words, uint64_t n, uint32_t* forward /* n */);
 uint64_t orc_bandwidth(const uint64_t* words, uint64_t n);
 void orc_permute_mask(const uint64_t* words, uint64_t n, const uint32_t* forward,

@@ -206,3 +206,17 @@ def test_naive_backward_matches_reference(spec, n, d):
     want = oracle.ref_naive_backward(q, k, v, g, 0.37, np.full_like(words, 0) | oracle.ref_generate("all-ones", n), n)
     for a, b in zip(got, want):
         assert np.allclose(a, b, rtol=1e-12, atol=1e-13)
+
+
+def test_naive_rows_equals_full_oracle():
+    # the row-sampled oracle is the full one restricted to the listed rows
+    words = oracle.ref_generate("global(w=9;g=2)", 70)
+    n = words.shape[0]
+    q, k, v, g = (a[0] for a in oracle.make_problem(4, 1, n, 16))
+    rows = [0, 1, 5, 33, 69]
+    out, rmax, rsum, dq = oracle.naive_rows(q, k, v, 0.3, words, n, rows, d_out=g)
+    o2, m2, l2 = oracle.naive_forward(q, k, v, 0.3, words, n, threads=1)
+    dq2, _, _ = oracle.naive_backward(q, k, v, g, 0.3, words, n, threads=1)
+    assert np.allclose(out, o2[rows], rtol=1e-13, atol=1e-14)
+    assert np.allclose(rmax, m2[rows]) and np.allclose(rsum, l2[rows], rtol=1e-13)
+    assert np.allclose(dq, dq2[rows], rtol=1e-12, atol=1e-13)
