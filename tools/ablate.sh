@@ -13,6 +13,10 @@ for v in $VARIANTS; do
     POLY_NONE) FL="-DBBM_POLY_PAIRS=0x0000u" ;;
     POLY_HALF) FL="-DBBM_POLY_PAIRS=0x5555u" ;;
     POLY_ALL) FL="-DBBM_POLY_PAIRS=0xFFFFu" ;;
+    POLY_4) FL="-DBBM_POLY_PAIRS=0x0303u" ;;
+    DEG2_6) FL="-DBBM_POLY_DEG2" ;;
+    DEG2_8) FL="-DBBM_POLY_DEG2 -DBBM_POLY_PAIRS=0x0F0Fu" ;;
+    DEG2_4) FL="-DBBM_POLY_DEG2 -DBBM_POLY_PAIRS=0x0303u" ;;
   esac
   rm -rf /tmp/abl_$v && mkdir -p /tmp/abl_$v
   cp -r "$ROOT/paper_2409_15097_b200" "$ROOT/include" /tmp/abl_$v/
