@@ -837,7 +837,17 @@ __global__ void __launch_bounds__(128) zero_rows_kernel(const uint32_t* __restri
 
 // Row units for a launch: row tiles longer than L are split into balanced chunks. With dynamic
 // longest-first claiming the makespan is about (average work per CTA + longest unit), so L is
-// half a CTA's average share (at least 16 tiles: combining partials is not free).
+// half a CTA's average share, and at least 16 tiles: combining partials goes through global
+// memory and costs more than a few tiles (splitting a tiny launch further measured slower).
+//
+// The masked variants split IN KEY SPACE, at boundaries set by the occupied tiles only: chunk c
+// of a row holds the same occupied tiles, in the same order, whether the variant walks the
+// compacted list (binblk, dense_binblk) or every tile of the key range (naive, whose extra tiles
+// are fully masked and change nothing). Their partials and the combine are then identical, so
+// the masked variants agree bit for bit at every size (test_engine.cpp:112-134). The dense
+// variant ignores the mask and splits by position.
+enum PlanClass : int { kPlanDense = 0, kPlanNaive = 1, kPlanList = 2 };
+
 struct UnitBuild {
   std::vector<uint4> desc;
   std::vector<uint2> split_info;
@@ -845,36 +855,49 @@ struct UnitBuild {
   uint32_t split_chunks = 0;
 };
 
-UnitBuild build_units(const std::vector<uint32_t>& row_tiles, uint64_t slots, int workers) {
+// cnt[p]: occupied tiles of row tile p; list: their ascending key tiles ([p * kcols + k]).
+UnitBuild build_units(int cls, uint32_t kcols, const std::vector<uint32_t>& cnt,
+                      const std::vector<uint32_t>& list, uint64_t slots, int workers) {
+  const uint32_t krows = static_cast<uint32_t>(cnt.size());
   uint64_t total = 0;
-  for (uint32_t c : row_tiles) total += c;
+  for (uint32_t p = 0; p < krows; ++p) total += cls == kPlanDense ? kcols : cnt[p];
   total *= slots;
-  const uint64_t per_worker = total / static_cast<uint64_t>(std::max(1, workers));
-  const uint32_t L = static_cast<uint32_t>(std::max<uint64_t>(16, (per_worker + 1) / 2));
+  const uint64_t w = static_cast<uint64_t>(std::max(1, workers));
+  const uint32_t L = static_cast<uint32_t>(std::max<uint64_t>(16, (total / w + 1) / 2));
   UnitBuild ub;
   struct U {
     uint32_t rt, j0, nt, split;
   };
   std::vector<U> units;
-  for (uint32_t p = 0; p < row_tiles.size(); ++p) {
-    const uint32_t nt = row_tiles[p];
-    if (nt == 0) {  // never enters the work queue (every queued item has >= 1 tile)
+  for (uint32_t p = 0; p < krows; ++p) {
+    const uint32_t occ = cls == kPlanDense ? kcols : cnt[p];
+    const uint32_t walk = cls == kPlanList ? cnt[p] : kcols;  // tiles the kernel walks
+    if (walk == 0) {  // never enters the work queue (every queued item has >= 1 tile)
       ub.empty_rows.push_back(p);
       continue;
     }
-    if (nt <= L) {
-      units.push_back({p, 0, nt, kNoSplit});
+    if (occ <= L) {
+      units.push_back({p, 0, walk, kNoSplit});
       continue;
     }
-    const uint32_t k = std::min<uint32_t>((nt + L - 1) / L, 255);
+    const uint32_t k = std::min<uint32_t>((occ + L - 1) / L, 255);
     const uint32_t srow = static_cast<uint32_t>(ub.split_info.size());
     ub.split_info.push_back(make_uint2(k, ub.split_chunks));
     ub.split_chunks += k;
-    uint32_t j0 = 0;
+    // chunk c: occupied tiles [o0, o1) of the row; key range from its first occupied tile up to
+    // the next chunk's (the first chunk from key 0, the last to the end of the row)
+    auto first_occ = [&](uint32_t c) { return (occ / k) * c + std::min(c, occ % k); };
+    auto key_of = [&](uint32_t o) {
+      return cls == kPlanDense ? o : (list[static_cast<uint64_t>(p) * kcols + o] & 0x7FFFFFFFu);
+    };
     for (uint32_t c = 0; c < k; ++c) {
-      const uint32_t len = nt / k + (c < nt % k ? 1 : 0);
-      units.push_back({p, j0, len, (srow << 8) | c});
-      j0 += len;
+      const uint32_t o0 = first_occ(c), o1 = first_occ(c + 1);
+      if (cls == kPlanNaive) {
+        const uint32_t kv0 = c == 0 ? 0 : key_of(o0), kv1 = c + 1 == k ? kcols : key_of(o1);
+        units.push_back({p, kv0, kv1 - kv0, (srow << 8) | c});
+      } else {
+        units.push_back({p, o0, o1 - o0, (srow << 8) | c});  // list positions (dense: positions)
+      }
     }
   }
   std::stable_sort(units.begin(), units.end(), [](const U& a, const U& b) { return a.nt > b.nt; });
@@ -886,14 +909,14 @@ template <int D, int MODE>
 void launch_impl(const Prep& prep, const AttnArgs& a, cudaStream_t s, int num_sms) {
   static_assert(smem_bytes<D>() <= 232448, "exceeds the 227 KB opt-in shared memory");
   const KernelMeta& km = prep.kmeta;
-  constexpr bool kAllTiles = (MODE == kModeDense || MODE == kModeNaive);
-  // one CTA per SM; when work items are scarce, at most one CTA per item
-  const uint32_t grid = std::min<uint32_t>(
-      static_cast<uint32_t>(std::max<uint64_t>(1, a.slots * km.krows)), static_cast<uint32_t>(num_sms));
-  const LaunchPlan& plan = prep.plan_for(kAllTiles, a.slots, grid, [&]() {
-    std::vector<uint32_t> rows(km.krows);
-    for (uint32_t p = 0; p < km.krows; ++p) rows[p] = kAllTiles ? km.kcols : prep.h_row_cnt[p];
-    const UnitBuild ub = build_units(rows, a.slots, static_cast<int>(grid));
+  constexpr int kCls = MODE == kModeDense ? kPlanDense : (MODE == kModeNaive ? kPlanNaive : kPlanList);
+  const LaunchPlan& plan = prep.plan_for(kCls, a.slots, static_cast<uint32_t>(num_sms), [&]() {
+    std::vector<uint32_t> list;
+    if (kCls != kPlanDense) {  // the occupied key tiles set the masked variants' split points
+      list.resize(static_cast<size_t>(km.krows) * km.kcols);
+      BBM_CUDA(cudaMemcpy(list.data(), km.list, list.size() * 4, cudaMemcpyDeviceToHost));
+    }
+    const UnitBuild ub = build_units(kCls, km.kcols, prep.h_row_cnt, list, a.slots, num_sms);
     LaunchPlan lp;
     lp.units = static_cast<uint32_t>(ub.desc.size());
     lp.split_rows = static_cast<uint32_t>(ub.split_info.size());
@@ -917,6 +940,9 @@ void launch_impl(const Prep& prep, const AttnArgs& a, cudaStream_t s, int num_sm
     BBM_CUDA(cudaMemset(lp.split_ctr, 0, nctr * sizeof(uint32_t)));
     return lp;
   });
+  // one CTA per SM; when work items are scarce, at most one CTA per item
+  const uint32_t grid = static_cast<uint32_t>(
+      std::max<uint64_t>(1, std::min<uint64_t>(a.slots * plan.units, static_cast<uint64_t>(num_sms))));
   float* ws = prep.workspace_for(static_cast<size_t>(a.slots) * plan.split_chunks * 128 * (D + 3));
 
   const CUtensorMap tq = make_tmap_bf16_3d(a.q, D, a.n, a.slots, 64, 128);

@@ -69,7 +69,7 @@ struct SpecMeta {
   uint64_t blocks_total = 0, blocks_nonzero = 0, blocks_full = 0, ones = 0;
 };
 
-// Work decomposition of one attention launch shape (mode class x slots x streams): row units
+// Work decomposition of one attention launch shape (plan class x slots x SMs): row units
 // (whole row tiles, or balanced chunks of long ones = split-KV), device-resident.
 struct LaunchPlan {
   uint32_t units = 0, split_rows = 0, split_chunks = 0;
@@ -121,14 +121,14 @@ struct Prep {
   uint32_t* work_ctr = nullptr;     // device [2]: dynamic item counter, finished CTAs
   // launch plans and the split-KV workspace are built on first use (not thread-safe: one
   // launch at a time per prep, like the reference's single-threaded callers)
-  mutable std::map<std::tuple<bool, uint64_t, uint32_t>, LaunchPlan> plans;
+  mutable std::map<std::tuple<int, uint64_t, uint32_t>, LaunchPlan> plans;
   mutable float* workspace = nullptr;
   mutable size_t workspace_floats = 0;
   mutable HostPipe* pipe = nullptr;  // host-buffer pipeline (lazy, host_io.cu)
 
   template <class F>
-  const LaunchPlan& plan_for(bool all_tiles, uint64_t slots, uint32_t streams, F make) const {
-    const auto key = std::make_tuple(all_tiles, slots, streams);
+  const LaunchPlan& plan_for(int plan_class, uint64_t slots, uint32_t workers, F make) const {
+    const auto key = std::make_tuple(plan_class, slots, workers);
     auto it = plans.find(key);
     if (it == plans.end()) it = plans.emplace(key, make()).first;
     return it->second;

@@ -217,7 +217,7 @@ void refresh_kernel_view(const Prep& pr, cudaStream_t s) {
   std::vector<uint32_t> cnt(pr.kmeta.krows);
   BBM_CUDA(cudaMemcpyAsync(cnt.data(), pr.kmeta.row_cnt, cnt.size() * 4, cudaMemcpyDeviceToHost, s));
   BBM_CUDA(cudaStreamSynchronize(s));
-  if (cnt != pr.h_row_cnt) {
+  {  // plans depend on the counts and (masked split points) on the lists: rebuild them
     for (auto& kv : pr.plans) {
       cudaFree(kv.second.unit_desc);
       cudaFree(kv.second.split_info);

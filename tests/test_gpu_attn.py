@@ -312,3 +312,18 @@ def test_split_kv_long_rows_match_oracle(cuda, spec, n, d):
     first = run_gpu(mask, q, k, v, scale, bbm.Variant.binblk, cuda, prep=prep)
     again = run_gpu(mask, q, k, v, scale, bbm.Variant.binblk, cuda, prep=prep)
     assert np.array_equal(again[0], first[0])
+
+
+@pytest.mark.parametrize("spec,n,d", [("global(w=64;g=100)", 4096, 64), ("causal", 1024, 64),
+                                      ("packed-seq[700;1200;900;1296]", 0, 128)])
+def test_masked_variants_bitwise_identical_with_split_rows(cuda, spec, n, d):
+    # long rows are split into key-range chunks at boundaries set by the occupied tiles, so the
+    # masked variants stay bit-identical even when rows are split (test_engine.cpp:112-134)
+    mask = bbm.generate(spec, n)
+    n = mask.size()
+    q, k, v = problem(21, 3, n, d)
+    prep = bbm.preprocess_mask(mask, bbm.BlockSpec(128, 128))
+    outs = [run_gpu(mask, q, k, v, d ** -0.5, var, cuda, prep=prep) for var in MASKED]
+    for o in outs[1:]:
+        assert np.array_equal(o[0], outs[0][0]) and np.array_equal(o[1], outs[0][1]) and np.array_equal(o[2], outs[0][2])
+    check_against_oracle(mask, q, k, v, d ** -0.5, *outs[1][:3], bbm.Variant.binblk, slots_to_check=[0])
