@@ -551,12 +551,11 @@ void launch_side(const Prep& prep, const BwdArgs& a, const float* lse2, const fl
   const CUtensorMap tk = make_tmap_bf16_3d(a.k, D, a.n, a.slots, 64, 128);
   const CUtensorMap tv = make_tmap_bf16_3d(a.v, D, a.n, a.slots, 64, 128);
   const CUtensorMap tdo = make_tmap_bf16_3d(a.d_out, D, a.n, a.slots, 64, 128);
-  static bool attr = false;
-  if (!attr) {
+  static std::atomic<uint64_t> attr_devices{0};
+  once_per_device(attr_devices, [] {
     BBM_CUDA(cudaFuncSetAttribute(attn_bwd_kernel<D, SIDE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   bwd_smem_bytes<D, SIDE>()));
-    attr = true;
-  }
+  });
   const uint32_t grid = std::min<uint32_t>(p.total_items, static_cast<uint32_t>(num_sms));
   if (SIDE == kSideDQ)
     attn_bwd_kernel<D, SIDE><<<grid, kThreads, bwd_smem_bytes<D, SIDE>(), s>>>(tq, tdo, tk, tv, p);

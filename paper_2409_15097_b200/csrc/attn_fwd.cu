@@ -972,14 +972,13 @@ void launch_impl(const Prep& prep, const AttnArgs& a, cudaStream_t s, int num_sm
   p.row_sum = a.row_sum;
   p.trace = static_cast<uint64_t*>(g_trace.buffer);
   p.trace_ctas = g_trace.ctas;
-  static bool attr_set = false;  // per (D, MODE) instantiation
-  if (!attr_set) {
+  static std::atomic<uint64_t> attr_devices{0};  // per (D, MODE) instantiation
+  once_per_device(attr_devices, [] {
     BBM_CUDA(cudaFuncSetAttribute(attn_fwd_kernel<D, MODE, false>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes<D>()));
     BBM_CUDA(cudaFuncSetAttribute(attn_fwd_kernel<D, MODE, true>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes<D>()));
-    attr_set = true;
-  }
+  });
   if (plan.empty_rows) {
     zero_rows_kernel<D><<<static_cast<unsigned>(a.slots * plan.empty_rows), 128, 0, s>>>(
         plan.empty_list, plan.empty_rows, a.n, p.out, p.row_max, p.row_sum);

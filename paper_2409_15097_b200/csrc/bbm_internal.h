@@ -2,6 +2,7 @@
 #pragma once
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cstdint>
 #include <map>
 #include <stdexcept>
@@ -31,6 +32,19 @@ inline void check_cuda(cudaError_t e, const char* what) {
 
 inline void require(bool cond, const std::string& msg) {
   if (!cond) throw ArgError(msg);
+}
+
+// Kernel attributes (e.g. the opt-in shared memory size) belong to a device context: set them
+// once per (kernel, device). `done` is a per-kernel bitmask of devices (threads of the
+// multi-GPU driver launch on different devices concurrently).
+template <class Set>
+void once_per_device(std::atomic<uint64_t>& done, Set&& set) {
+  int dev = 0;
+  check_cuda(cudaGetDevice(&dev), "cudaGetDevice");
+  const uint64_t bit = uint64_t{1} << (dev & 63);
+  if (done.load(std::memory_order_acquire) & bit) return;
+  set();
+  done.fetch_or(bit, std::memory_order_release);
 }
 
 // Device metadata at the kernel tile shape (128 x 128). Layouts (all device memory):

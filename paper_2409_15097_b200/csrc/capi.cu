@@ -49,11 +49,14 @@ struct DeviceGuard {
 };
 
 int sm_count(int dev) {
-  static int cache[64] = {0};
-  if (dev < 64 && cache[dev]) return cache[dev];
+  static std::atomic<int> cache[64] = {};  // read by the multi-GPU driver's threads
+  if (dev >= 0 && dev < 64) {
+    const int c = cache[dev].load(std::memory_order_relaxed);
+    if (c) return c;
+  }
   int v = 0;
   BBM_CUDA(cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev));
-  if (dev < 64) cache[dev] = v;
+  if (dev >= 0 && dev < 64) cache[dev].store(v, std::memory_order_relaxed);
   return v;
 }
 
