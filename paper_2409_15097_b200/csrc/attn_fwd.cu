@@ -567,6 +567,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (tracer) trace_ev<kTrace>(tracing, p, &ctl->trace_count, 23, 0, it.t);
       if (it.split == kNoSplit) {
         const float inv = l_unit > 0.0f ? 1.0f / l_unit : 0.0f;
+#ifdef BBM_ABLATE_NO_EPI  // timing experiments only (tools/ablate.sh): O is never written
+        if (false)
+#endif
 #pragma unroll
         for (uint32_t c32 = 0; c32 < kHalfO / 32; ++c32) {
           uint32_t o[32];
@@ -577,7 +580,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         tc_fence_before();
         mbar_arrive(&ctl->o_empty[pd.ob]);  // the accumulator may be overwritten from here on
+#ifndef BBM_ABLATE_NO_EPI
         store_staged(it);
+#endif
         write_stats(it, m_true, m_run, l_unit);
       } else {
         // ---- split-KV chunk: publish the unnormalized partial, the last chunk combines

@@ -10,6 +10,7 @@ VARIANTS="${VARIANTS:-NO_XCHG POLY_NONE POLY_HALF}"
 for v in $VARIANTS; do
   case $v in
     NO_XCHG) FL="-DBBM_ABLATE_NO_XCHG" ;;
+    NO_EPI) FL="-DBBM_ABLATE_NO_EPI" ;;
     POLY_NONE) FL="-DBBM_POLY_PAIRS=0x0000u" ;;
     POLY_HALF) FL="-DBBM_POLY_PAIRS=0x5555u" ;;
     POLY_ALL) FL="-DBBM_POLY_PAIRS=0xFFFFu" ;;
