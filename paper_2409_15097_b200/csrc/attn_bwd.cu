@@ -92,7 +92,7 @@ struct BCfg {
 };
 
 struct BwdCtl {
-  uint64_t fixed_full, fixed_empty, s_full, p_full, acc_full, acc_empty;
+  uint64_t fixed_full, fixed_empty, s_full[2], p_full[2], acc_full, acc_empty;
   uint64_t ring_full[4], ring_empty[4];
   uint64_t item_full[kQueue], item_empty[kQueue];
   ItemDesc items[kQueue];
@@ -149,8 +149,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (threadIdx.x == 0) {
     mbar_init(&ctl->fixed_full, 1);
     mbar_init(&ctl->fixed_empty, 1);
-    mbar_init(&ctl->s_full, 1);
-    mbar_init(&ctl->p_full, 256);
+    for (int h = 0; h < 2; ++h) {
+      mbar_init(&ctl->s_full[h], 1);
+      mbar_init(&ctl->p_full[h], 128);  // the four softmax warps of half h
+    }
     mbar_init(&ctl->acc_full, 1);
     mbar_init(&ctl->acc_empty, 256);
     for (uint32_t r = 0; r < C::kStages; ++r) {
@@ -222,11 +224,51 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else if (warp == 1) {
     // ------------------------------------------------------------------ MMA issuer
+    // Each tile's work is split by partner-row halves h (TMEM columns [64h, 64h+64) of S and dP,
+    // owned by softmax warps 4-7 / 8-11): S_h, dP_h (N = 64) and the accumulate MMAs over K-steps
+    // of half h. Issue order  SdP_0(j) SdP_1(j) | acc_0(j) SdP_0(j+1) | acc_1(j) SdP_1(j+1) | ...
+    // so one half's elementwise pass overlaps the other half's MMAs, and a half's next scores
+    // overwrite its P / dS columns only after its accumulate MMAs (in-order execution).
     if (lane == 0) {
-      constexpr uint32_t idesc_s = make_idesc_bf16(128, 128, false, false);
+      constexpr uint32_t idesc_s = make_idesc_bf16(128, 64, false, false);
       constexpr uint32_t idesc_acc = make_idesc_bf16(128, D, false, true);
       const uint32_t faddr = smem_u32(fixed), raddr = smem_u32(ring);
-      uint32_t qi = 0, qiph = 0, r = 0, rph = 0, fph = 0, pph = 0, aph = 1;
+      const uint64_t f0 = make_sdesc_sw128(faddr, 16, 1024), f1 = make_sdesc_sw128(faddr + C::kTileBytes, 16, 1024);
+      uint32_t qi = 0, qiph = 0, r = 0, rph = 0, fph = 0, aph = 1;
+      uint32_t pph[2] = {0, 0};
+      // S_h = f0 s0[64h..]^T, dP_h = f1 s1[64h..]^T: both K-major, K = D, N = 64 partner rows
+      auto issue_sdp = [&](uint32_t h, uint32_t stage) {
+        const uint32_t sbase = raddr + stage * C::kStageAlloc + h * 8192;
+        const uint64_t s0 = make_sdesc_sw128(sbase, 16, 1024), s1 = make_sdesc_sw128(sbase + C::kTileBytes, 16, 1024);
+#pragma unroll
+        for (uint32_t kk = 0; kk < D / 16; ++kk) {
+          const uint32_t off = (kk / 4) * kBoxBytes + (kk % 4) * 32;
+          umma_ss(tmem + h * 64, sdesc_advance(f0, off), sdesc_advance(s0, off), idesc_s, kk > 0);
+        }
+#pragma unroll
+        for (uint32_t kk = 0; kk < D / 16; ++kk) {
+          const uint32_t off = (kk / 4) * kBoxBytes + (kk % 4) * 32;
+          umma_ss(tmem + 128 + h * 64, sdesc_advance(f1, off), sdesc_advance(s1, off), idesc_s, kk > 0);
+        }
+        tc_commit(&ctl->s_full[h]);
+      };
+      // accumulate MMAs of half h: K steps 4h..4h+3 (partner rows 64h..64h+63). Packed bf16 A
+      // operand: half h's 32 columns at [64h, 64h+32) of its region -> column (kk/4)*64 + (kk%4)*8
+      auto issue_acc = [&](uint32_t h, uint32_t stage, uint32_t j) {
+        const uint32_t sbase = raddr + stage * C::kStageAlloc;
+        const uint64_t b0 = make_sdesc_sw128(sbase, kBoxBytes, 1024);
+        const uint64_t b1 = make_sdesc_sw128(sbase + C::kTileBytes, kBoxBytes, 1024);
+#pragma unroll
+        for (uint32_t q = 0; q < 4; ++q) {
+          const uint32_t kk = 4 * h + q;
+          const uint32_t acol = (kk / 4) * 64 + (kk % 4) * 8;
+          const uint32_t acc = (j > 0 || kk > 0) ? 1u : 0u;
+          // dQ += dS K_j  |  dK += dS^T Q_i   (B = streamed tile 0, MN-major)
+          umma_ts(tmem + C::kAcc0, tmem + 128 + acol, sdesc_advance(b0, kk * 2048), idesc_acc, acc);
+          if constexpr (SIDE == kSideDKDV)  // dV += P^T dO_i   (B = streamed tile 1)
+            umma_ts(tmem + C::kAcc1, tmem + acol, sdesc_advance(b1, kk * 2048), idesc_acc, acc);
+        }
+      };
       for (;;) {
         mbar_wait(&ctl->item_full[qi], qiph);
         const ItemDesc it = ctl->items[qi];
@@ -236,48 +278,35 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (it.nt == 0) continue;
         mbar_wait(&ctl->fixed_full, fph);
         fph ^= 1;
+        mbar_wait(&ctl->ring_full[r], rph);
+        tc_fence_after();
+        issue_sdp(0, r);
+        issue_sdp(1, r);
+        if (it.nt == 1) tc_commit(&ctl->fixed_empty);
         for (uint32_t j = 0; j < it.nt; ++j) {
-          mbar_wait(&ctl->ring_full[r], rph);
-          tc_fence_after();
-          const uint32_t sbase = raddr + r * C::kStageAlloc;
-          const uint64_t f0 = make_sdesc_sw128(faddr, 16, 1024), f1 = make_sdesc_sw128(faddr + C::kTileBytes, 16, 1024);
-          const uint64_t s0 = make_sdesc_sw128(sbase, 16, 1024), s1 = make_sdesc_sw128(sbase + C::kTileBytes, 16, 1024);
-          // S (or S^T) = f0 s0^T, dP (or dP^T) = f1 s1^T: both operands K-major, K = D
-#pragma unroll
-          for (uint32_t kk = 0; kk < D / 16; ++kk) {
-            const uint32_t off = (kk / 4) * kBoxBytes + (kk % 4) * 32;
-            umma_ss(tmem, sdesc_advance(f0, off), sdesc_advance(s0, off), idesc_s, kk > 0);
+          const uint32_t rn = r + 1 == C::kStages ? 0 : r + 1;
+          const uint32_t rnph = r + 1 == C::kStages ? rph ^ 1 : rph;
+          for (uint32_t h = 0; h < 2; ++h) {
+            mbar_wait(&ctl->p_full[h], pph[h]);
+            pph[h] ^= 1;
+            if (j == 0 && h == 0) {
+              mbar_wait(&ctl->acc_empty, aph);  // previous item's epilogue has read the accumulators
+              aph ^= 1;
+            }
+            tc_fence_after();
+            issue_acc(h, r, j);
+            if (h == 1) tc_commit(&ctl->ring_empty[r]);  // both halves of tile j consumed
+            if (j + 1 < it.nt) {
+              if (h == 0) {
+                mbar_wait(&ctl->ring_full[rn], rnph);
+                tc_fence_after();
+              }
+              issue_sdp(h, rn);
+              if (h == 1 && j + 2 == it.nt) tc_commit(&ctl->fixed_empty);
+            }
           }
-#pragma unroll
-          for (uint32_t kk = 0; kk < D / 16; ++kk) {
-            const uint32_t off = (kk / 4) * kBoxBytes + (kk % 4) * 32;
-            umma_ss(tmem + 128, sdesc_advance(f1, off), sdesc_advance(s1, off), idesc_s, kk > 0);
-          }
-          tc_commit(&ctl->s_full);
-          if (j + 1 == it.nt) tc_commit(&ctl->fixed_empty);
-          mbar_wait(&ctl->p_full, pph);
-          pph ^= 1;
-          if (j == 0) {
-            mbar_wait(&ctl->acc_empty, aph);  // previous item's epilogue has read the accumulators
-            aph ^= 1;
-          }
-          tc_fence_after();
-          // packed bf16 A operand: half h's 32 columns at [64h, 64h+32) of its region; K step kk
-          // (16 partner rows = 8 packed columns) -> column (kk/4)*64 + (kk%4)*8
-          const uint64_t b0 = make_sdesc_sw128(sbase, kBoxBytes, 1024);
-          const uint64_t b1 = make_sdesc_sw128(sbase + C::kTileBytes, kBoxBytes, 1024);
-#pragma unroll
-          for (uint32_t kk = 0; kk < 8; ++kk) {
-            const uint32_t acol = (kk / 4) * 64 + (kk % 4) * 8;
-            // dQ += dS K_j  |  dK += dS^T Q_i   (B = streamed tile 0, MN-major)
-            umma_ts(tmem + C::kAcc0, tmem + 128 + acol, sdesc_advance(b0, kk * 2048), idesc_acc,
-                    (j > 0 || kk > 0) ? 1u : 0u);
-            if constexpr (SIDE == kSideDKDV)  // dV += P^T dO_i   (B = streamed tile 1)
-              umma_ts(tmem + C::kAcc1, tmem + acol, sdesc_advance(b1, kk * 2048), idesc_acc,
-                      (j > 0 || kk > 0) ? 1u : 0u);
-          }
-          tc_commit(&ctl->ring_empty[r]);
-          if (++r == C::kStages) { r = 0; rph ^= 1; }
+          r = rn;
+          rph = rnph;
         }
         tc_commit(&ctl->acc_full);
       }
@@ -329,7 +358,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                                 p.bitmaps + (static_cast<uint64_t>(it.tile) * p.list_stride + j) * 128 + row) +
                             half);
           }
-          mbar_wait(&ctl->s_full, sph);
+          mbar_wait(&ctl->s_full[half], sph);
           sph ^= 1;
           tc_fence_after();
           const uint32_t ts = tmem + lane_off + half * 64;
@@ -368,7 +397,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
           tmem_st_wait();
           tc_fence_before();
-          mbar_arrive(&ctl->p_full);
+          mbar_arrive(&ctl->p_full[half]);
           if (++r == C::kStages) r = 0;
         }
         // epilogue: accumulators -> bf16 rows (dq * scale | dk * scale, dv)
