@@ -45,6 +45,9 @@ def alpaca_lengths(total: int, seed: int = 7, lo: int = 64, span: int = 449):
     return out
 
 
+RCM_PERM = {}  # config -> RCM permutation (new -> old) of its reordered mask
+
+
 def make_config(name: str):
     """BASELINE.json configs -> (mask, B, H, d, description). C2 is the headline workload."""
     import paper_2409_15097_b200 as bbm
@@ -76,6 +79,7 @@ def make_config(name: str):
         base = bbm.gen_longformer_windowed(32768, 164)
         shuffled = bbm.relabel(base, 3)
         perm = bbm.rcm_order(shuffled)
+        RCM_PERM["c5"] = perm
         return (bbm.permute_mask(shuffled, perm), 4, 32, 128,
                 "C5 1% band (w=164) relabelled by mt19937_64(3), RCM-reordered, N=32768 B=4 H=32 d=128")
     raise SystemExit(f"unknown config {name}")
@@ -437,6 +441,9 @@ def main():
         # e2e: the same forward through the host-buffer C ABI call, H2D + D2H inside the region
         if not args.no_e2e:
             extras["e2e"] = e2e_measure(prep, variant, q, k, v, slots, n, d, scale, flops, args.steps)
+            if args.config in RCM_PERM:  # the whole reordered pipeline from original-order buffers
+                extras["e2e_rcm"] = e2e_measure(prep, variant, q, k, v, slots, n, d, scale, flops, args.steps,
+                                                forward=RCM_PERM[args.config].forward)
         if not args.no_cpu_baseline and world == 1:
             try:
                 threads = os.cpu_count() or 1
@@ -481,9 +488,11 @@ def prep_update(prep, dense_mask, stream):
                                                      dense_mask.stride(0), C.c_void_p(stream.cuda_stream)))
 
 
-def e2e_measure(prep, variant, q, k, v, slots, n, d, scale, flops, steps):
+def e2e_measure(prep, variant, q, k, v, slots, n, d, scale, flops, steps, forward=None):
     """bbm_attn_fwd_host_bf16 with pinned host buffers: H2D of Q/K/V, the kernel, D2H of O and the
-    row statistics, all inside the timed call."""
+    row statistics, all inside the timed call. With `forward` (an RCM permutation), the
+    reordered pipeline bbm_attn_fwd_rcm_host_bf16 instead: original-order buffers, the device
+    gathers / scatters rows around the kernel."""
     import ctypes as C
 
     import torch
@@ -495,9 +504,20 @@ def e2e_measure(prep, variant, q, k, v, slots, n, d, scale, flops, steps):
     hmax = torch.empty((slots, n), dtype=torch.float32).pin_memory()
     hsum = torch.empty((slots, n), dtype=torch.float32).pin_memory()
 
+    import numpy as np
+
+    fwd = None if forward is None else np.ascontiguousarray(forward, dtype=np.uint32)
+
     def call():
         u16 = C.POINTER(C.c_uint16)
         f32 = C.POINTER(C.c_float)
+        if fwd is not None:
+            _lib.check(_lib.lib.bbm_attn_fwd_rcm_host_bf16(
+                prep.handle.h, int(variant), fwd.ctypes.data_as(C.POINTER(C.c_uint32)),
+                C.cast(hq.data_ptr(), u16), C.cast(hk.data_ptr(), u16), C.cast(hv.data_ptr(), u16),
+                C.cast(ho.data_ptr(), u16), C.cast(hmax.data_ptr(), f32), C.cast(hsum.data_ptr(), f32),
+                slots, d, scale))
+            return
         _lib.check(_lib.lib.bbm_attn_fwd_host_bf16(
             prep.handle.h, int(variant), C.cast(hq.data_ptr(), u16), C.cast(hk.data_ptr(), u16),
             C.cast(hv.data_ptr(), u16), C.cast(ho.data_ptr(), u16), C.cast(hmax.data_ptr(), f32),
@@ -513,7 +533,8 @@ def e2e_measure(prep, variant, q, k, v, slots, n, d, scale, flops, steps):
     d2h = slots * n * d * 2 + 2 * slots * n * 4
     return {"value": flops / (ms * 1e-3) / 1e12, "unit": "TFLOP/s", "ms_per_step": ms,
             "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-            "path": "bbm_attn_fwd_host_bf16 (C ABI, pinned host buffers, synchronous)"}
+            "path": ("bbm_attn_fwd_rcm_host_bf16 (original token order; device gather/scatter)" if fwd is not None
+                     else "bbm_attn_fwd_host_bf16") + " (C ABI, pinned host buffers, synchronous)"}
 
 
 if __name__ == "__main__":

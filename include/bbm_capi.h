@@ -137,6 +137,16 @@ bbm_status bbm_attn_fwd_host_bf16(bbm_prep prep, int variant, const uint16_t* q,
                                   float* row_max, float* row_sum, uint64_t slots,
                                   uint32_t head_dim, double scale);
 
+/* The reordered pipeline end to end (bench.hpp:448-467 with reorder.hpp:156-189 on the device):
+ * q/k/v/out/row stats in the ORIGINAL token order, `prep` built from permute_mask(mask, perm),
+ * `forward` = perm.forward (new -> old, host u32 [n]). Rows are gathered into the reordered
+ * layout, attended with the reordered mask, and O / row stats scattered back, on the device,
+ * pipelined with the PCIe copies. Equals the attention with the original mask (equivariance). */
+bbm_status bbm_attn_fwd_rcm_host_bf16(bbm_prep prep, int variant, const uint32_t* forward,
+                                      const uint16_t* q, const uint16_t* k, const uint16_t* v,
+                                      uint16_t* out, float* row_max, float* row_sum, uint64_t slots,
+                                      uint32_t head_dim, double scale);
+
 /* Same, float host buffers (the reference's Matrix<float> storage, matrix.hpp:14-45); inputs
  * rounded to bf16 (RNE) on the device, output widened back to float; row stats as double.
  * Validates finiteness like validate_forward_args (engine.hpp:244-258). */

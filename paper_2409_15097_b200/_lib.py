@@ -78,6 +78,7 @@ SIGNATURES = {
     "bbm_graph_csr": (C.c_int, [u64p, C.c_uint64, u64p, u32p]),
     "bbm_attn_fwd": (C.c_int, [vp, C.c_int, vp, vp, vp, vp, vp, vp, C.c_uint64, C.c_uint32, C.c_double, vp]),
     "bbm_attn_fwd_host_bf16": (C.c_int, [vp, C.c_int, u16p, u16p, u16p, u16p, f32p, f32p, C.c_uint64, C.c_uint32, C.c_double]),
+    "bbm_attn_fwd_rcm_host_bf16": (C.c_int, [vp, C.c_int, u32p, u16p, u16p, u16p, u16p, f32p, f32p, C.c_uint64, C.c_uint32, C.c_double]),
     "bbm_attn_fwd_host_f32": (C.c_int, [vp, C.c_int, f32p, f32p, f32p, f32p, f64p, f64p, C.c_uint64, C.c_uint32, C.c_double]),
     "bbm_run_attention_multi": (C.c_int, [vp, C.c_int, C.c_int, C.POINTER(C.c_int), u16p, u16p, u16p, u16p, f32p, f32p, C.c_uint64, C.c_uint32, C.c_double, f64p]),
     "bbm_set_trace": (C.c_int, [vp, C.c_uint32]),

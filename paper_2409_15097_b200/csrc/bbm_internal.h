@@ -239,5 +239,10 @@ int attn_fwd_kernel_launches_per_call();
 void run_fwd_host_pipelined(const Prep& prep, int variant, const uint16_t* q, const uint16_t* k,
                             const uint16_t* v, uint16_t* out, float* row_max, float* row_sum,
                             uint64_t slots, uint32_t d, float scale, int num_sms, double* span_ms);
+// the RCM path end to end: original-order host buffers, prep built from the permuted mask
+void run_fwd_host_rcm(const Prep& prep, int variant, const uint32_t* forward, const uint16_t* q,
+                      const uint16_t* k, const uint16_t* v, uint16_t* out, float* row_max,
+                      float* row_sum, uint64_t slots, uint32_t d, float scale, int num_sms,
+                      double* span_ms);
 
 }  // namespace bbm

@@ -628,6 +628,21 @@ bbm_status bbm_attn_fwd_host_bf16(bbm_prep prep, int variant, const uint16_t* q,
   });
 }
 
+bbm_status bbm_attn_fwd_rcm_host_bf16(bbm_prep prep, int variant, const uint32_t* forward,
+                                      const uint16_t* q, const uint16_t* k, const uint16_t* v,
+                                      uint16_t* out, float* row_max, float* row_sum, uint64_t slots,
+                                      uint32_t head_dim, double scale) {
+  return guarded([&] {
+    const Prep& pr = unwrap(prep);
+    check_attn_args(pr, variant, slots, head_dim, scale);
+    require(q && k && v && out && forward, "null argument");
+    check_bijection(forward, pr.n);
+    DeviceGuard g(pr.device);
+    run_fwd_host_rcm(pr, variant, forward, q, k, v, out, row_max, row_sum, slots, head_dim,
+                     static_cast<float>(scale), sm_count(pr.device), nullptr);
+  });
+}
+
 bbm_status bbm_attn_fwd_host_f32(bbm_prep prep, int variant, const float* q, const float* k,
                                  const float* v, float* out, double* row_max, double* row_sum,
                                  uint64_t slots, uint32_t head_dim, double scale) {

@@ -327,3 +327,50 @@ def test_masked_variants_bitwise_identical_with_split_rows(cuda, spec, n, d):
     for o in outs[1:]:
         assert np.array_equal(o[0], outs[0][0]) and np.array_equal(o[1], outs[0][1]) and np.array_equal(o[2], outs[0][2])
     check_against_oracle(mask, q, k, v, d ** -0.5, *outs[1][:3], bbm.Variant.binblk, slots_to_check=[0])
+
+
+def test_rcm_host_pipeline_equals_explicit_permutation(cuda):
+    # bbm_attn_fwd_rcm_host_bf16: original-order inputs through the device-side permutation
+    # equal the explicit host permutation + forward on the reordered mask + host unpermutation
+    # (bit for bit: the same kernel runs on the same reordered data), and the attention with the
+    # original mask (equivariance, test_reorder.cpp:202-216) to the bf16 tolerance
+    import ctypes as C
+
+    from paper_2409_15097_b200 import _lib
+
+    base = bbm.gen_longformer_windowed(1000, 7)
+    shuffled = bbm.relabel(base, 3)
+    perm = bbm.rcm_order(shuffled)
+    pmask = bbm.permute_mask(shuffled, perm)
+    slots, n, d = 5, 1000, 128
+    q, k, v = problem(31, slots, n, d)
+    to_u16 = lambda a: (np.ascontiguousarray(a, np.float32).view(np.uint32) >> 16).astype(np.uint16)  # noqa: E731
+    hq, hk, hv = (to_u16(a) for a in (q, k, v))  # inputs are already bf16-exact
+    prep = bbm.preprocess_mask(pmask, bbm.BlockSpec(128, 128))
+    out = np.empty_like(hq)
+    rmax = np.empty((slots, n), np.float32)
+    rsum = np.empty((slots, n), np.float32)
+    fwd = np.ascontiguousarray(perm.forward, dtype=np.uint32)
+    u16, f32 = C.POINTER(C.c_uint16), C.POINTER(C.c_float)
+    _lib.check(_lib.lib.bbm_attn_fwd_rcm_host_bf16(
+        prep.handle.h, int(bbm.Variant.binblk), fwd.ctypes.data_as(C.POINTER(C.c_uint32)),
+        hq.ctypes.data_as(u16), hk.ctypes.data_as(u16), hv.ctypes.data_as(u16), out.ctypes.data_as(u16),
+        rmax.ctypes.data_as(f32), rsum.ctypes.data_as(f32), slots, d, d ** -0.5))
+    # explicit: permute on the host, plain host-buffer forward, unpermute on the host
+    pq, pk, pv = (np.ascontiguousarray(a[:, fwd]) for a in (hq, hk, hv))
+    pout = np.empty_like(pq)
+    pmax = np.empty((slots, n), np.float32)
+    psum = np.empty((slots, n), np.float32)
+    _lib.check(_lib.lib.bbm_attn_fwd_host_bf16(
+        prep.handle.h, int(bbm.Variant.binblk), pq.ctypes.data_as(u16), pk.ctypes.data_as(u16),
+        pv.ctypes.data_as(u16), pout.ctypes.data_as(u16), pmax.ctypes.data_as(f32), psum.ctypes.data_as(f32),
+        slots, d, d ** -0.5))
+    want = np.empty_like(pout)
+    want[:, fwd] = pout
+    assert np.array_equal(out, want)
+    wmax = np.empty_like(pmax)
+    wmax[:, fwd] = pmax
+    assert np.array_equal(rmax, wmax)
+    got = (out.astype(np.uint32) << 16).view(np.float32)
+    check_against_oracle(shuffled, q, k, v, d ** -0.5, got, rmax.astype(np.float64),
+                         rsum.astype(np.float64), bbm.Variant.binblk, slots_to_check=[0, 4])
