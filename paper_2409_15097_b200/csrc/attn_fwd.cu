@@ -78,7 +78,15 @@ struct FwdParams {
   uint32_t trace_ctas;   // CTAs that record
 };
 
-constexpr uint32_t kThreads = 384;
+// Softmax engine split: kParts warps per TMEM lane quadrant, each owning 128/kParts score
+// columns and D/kParts output columns of its 32 rows.
+#ifndef BBM_PARTS128
+#define BBM_PARTS128 2
+#endif
+template <int D>
+constexpr uint32_t kParts = D == 128 ? BBM_PARTS128 : 2;
+template <int D>
+constexpr uint32_t kThreadsOf = 128 + 128 * kParts<D>;
 constexpr uint32_t kTraceCap = 8192;  // events per traced CTA
 constexpr uint32_t kQueue = 8;        // item queue depth (items open between the producer and the PV issuer)
 
@@ -120,7 +128,7 @@ template <int D>
 struct Cfg {
   static constexpr uint32_t kBoxes = D / 64;
   static constexpr uint32_t kTileBytes = kBoxes * kBoxBytes;  // one 128 x D bf16 tile
-  static constexpr uint32_t kRing = (D == 64) ? 10 : 4;       // K/V ring slots
+  static constexpr uint32_t kRing = (D == 64) ? 10 : (BBM_PARTS128 > 2 ? 3 : 4);  // K/V ring slots
   static constexpr uint32_t kStageBytes = kBoxBytes;          // epilogue staging (two buffers)
   static constexpr uint32_t kTmemCols = 512;
   static constexpr uint32_t kOCol = kSBufs * 128;
@@ -132,7 +140,7 @@ struct ItemDesc {
 
 // Everything that is not a tile lives behind the tiles in the same dynamic allocation (no static
 // smem, so the dynamic base is the 1024-byte aligned start of the CTA's window).
-template <uint32_t kRing>
+template <uint32_t kRing, uint32_t kXP>
 struct SmemCtl {
   uint64_t q_full[2], q_empty[2], s_full[kSBufs], p_full[kSBufs], o_full[2], o_empty[2], pv_done[kSBufs];
   uint64_t ring_full[kRing], ring_empty[kRing];
@@ -141,13 +149,13 @@ struct SmemCtl {
   uint32_t tmem_base;
   uint32_t trace_count;
   uint32_t bcast;
-  float xchg[2][2][128];  // [exchange parity][half][row]: partial row max / row sum
+  float xchg[2][kXP][128];  // [exchange parity][part][row]: partial row max / row sum
 };
 
 template <int D>
 constexpr uint32_t smem_bytes() {
   return Cfg<D>::kTileBytes * (2 + Cfg<D>::kRing) + 2 * Cfg<D>::kStageBytes +
-         sizeof(SmemCtl<Cfg<D>::kRing>);
+         sizeof(SmemCtl<Cfg<D>::kRing, kParts<D>>);
 }
 
 template <int MODE>
@@ -247,7 +255,7 @@ __device__ __forceinline__ void stage_chunk32(uint8_t* rowp, uint32_t row, uint3
 }
 
 template <int D, int MODE, bool kTrace>
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(kThreadsOf<D>, 1)
     attn_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                     const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_o,
                     const FwdParams p) {
@@ -256,7 +264,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint8_t* sq = smem;                              // [2][tile]          Q, double-buffered
   uint8_t* ring = sq + 2 * C::kTileBytes;          // [kRing][tile]      K/V ring
   uint8_t* stage = ring + C::kRing * C::kTileBytes;  // [2][128 x 64 bf16] epilogue staging
-  auto* ctl = reinterpret_cast<SmemCtl<C::kRing>*>(stage + 2 * C::kStageBytes);
+  auto* ctl = reinterpret_cast<SmemCtl<C::kRing, kParts<D>>*>(stage + 2 * C::kStageBytes);
 
   const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if ((smem_u32(smem) & 1023u) != 0) __trap();  // 128B-swizzle atoms need 1024-byte alignment
@@ -270,12 +278,12 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (uint32_t b = 0; b < kSBufs; ++b) {
       mbar_init(&ctl->s_full[b], 1);
-      mbar_init(&ctl->p_full[b], 256);
+      mbar_init(&ctl->p_full[b], 128 * kParts<D>);
       mbar_init(&ctl->pv_done[b], 1);
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&ctl->o_full[b], 1);
-      mbar_init(&ctl->o_empty[b], 256);
+      mbar_init(&ctl->o_empty[b], 128 * kParts<D>);
     }
     for (uint32_t r = 0; r < C::kRing; ++r) {
       mbar_init(&ctl->ring_full[r], 1);
@@ -474,7 +482,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else if (warp >= 4) {
     // ------------------------------------------------------------------ softmax engine
-    const uint32_t half = (warp >= 8) ? 1u : 0u;
+    constexpr uint32_t kP = kParts<D>;
+    constexpr uint32_t kSC = 128 / kP;        // score columns per part
+    constexpr uint32_t kEng = 128 * kP;       // engine threads
+    const uint32_t half = (warp - 4) >> 2;    // this thread's part
     const uint32_t quad = warp & 3;
     const uint32_t row = quad * 32 + lane;
     const uint32_t lane_off = (quad * 32) << 16;
@@ -489,7 +500,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     // masked scores: -inf, or +inf with a negative scale; with a zero scale the sentinel only
     // has to drop out of the max (the exp pass selects explicitly)
     const uint32_t sentinel = neg ? 0x7F800000u : 0xFF800000u;
-    constexpr uint32_t kHalfO = D / 2;  // O columns per half
+    constexpr uint32_t kHalfO = D / kP;  // O columns per part
     const uint32_t to_base = tmem + C::kOCol + lane_off;
 
     uint32_t step = 0;  // parity selects the exchange buffer
@@ -531,7 +542,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     // TMA-store the staged O tile of item `it` (called by every engine thread)
     auto store_staged = [&](const ItemDesc& it) {
       fence_proxy_async_smem();
-      named_bar_sync(1, 256);
+      named_bar_sync(1, kEng);
       if (leader) {
         tma_store_3d(&tm_o, stage, 0, it.rt * 128, it.slot);
         if (D == 128) tma_store_3d(&tm_o, stage + C::kStageBytes, 64, it.rt * 128, it.slot);
@@ -540,18 +551,22 @@ __global__ void __launch_bounds__(kThreads, 1)
     };
     // D=128: half h stages columns [64h, 64h+64) in buffer h; D=64: both halves share buffer 0,
     // 32 columns (4 chunks) each
-    uint8_t* stg_row = stage + (D == 128 ? half * C::kStageBytes : 0) + row * 128;
+    // staged output column c goes to box c / 64, 16-byte chunk (c % 64) / 8 of the row
+    auto stg_row_of = [&](uint32_t c) { return stage + (c / 64) * C::kStageBytes + row * 128; };
+    auto stg_chunk_of = [&](uint32_t c) { return (c % 64) / 8; };
 
     // mask bits (and, for dense_binblk, the list entry) of tile jj of item `it`; the bitmap
     // address depends only on (row tile, list position), never on a loaded value
     auto load_bits = [&](const ItemDesc& it, uint32_t jj, uint2& bits, uint32_t& entry) {
       const uint64_t grow = static_cast<uint64_t>(it.rt) * 128 + row;
       if constexpr (MODE == kModeNaive)
-        bits = __ldg(reinterpret_cast<const uint2*>(p.mask + grow * p.kcols + jj) + half);
-      else if constexpr (MODE != kModeDense)
-        bits = __ldg(reinterpret_cast<const uint2*>(
-                         p.bitmaps + (static_cast<uint64_t>(it.rt) * p.kcols + jj) * 128 + row) +
-                     half);
+        bits = kSC == 64 ? __ldg(reinterpret_cast<const uint2*>(p.mask + grow * p.kcols + jj) + half)
+                         : make_uint2(__ldg(reinterpret_cast<const uint32_t*>(p.mask + grow * p.kcols + jj) + half), 0u);
+      else if constexpr (MODE != kModeDense) {
+        const uint4* bp = p.bitmaps + (static_cast<uint64_t>(it.rt) * p.kcols + jj) * 128 + row;
+        bits = kSC == 64 ? __ldg(reinterpret_cast<const uint2*>(bp) + half)
+                         : make_uint2(__ldg(reinterpret_cast<const uint32_t*>(bp) + half), 0u);
+      }
       if constexpr (MODE == kModeDenseBinblk) entry = entry_of<MODE>(p, it.rt, jj);
     };
 
@@ -563,7 +578,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_wait(&ctl->o_full[pd.ob], o_ph[pd.ob]);
       o_ph[pd.ob] ^= 1;
       tc_fence_after();
-      named_bar_sync(1, 256);
+      named_bar_sync(1, kEng);
       if (tracer) trace_ev<kTrace>(tracing, p, &ctl->trace_count, 23, 0, it.t);
       if (it.split == kNoSplit) {
         const float inv = l_unit > 0.0f ? 1.0f / l_unit : 0.0f;
@@ -575,7 +590,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           uint32_t o[32];
           tmem_ld32(to + half * kHalfO + c32 * 32, o);
           tmem_ld_wait();
-          stage_chunk32(stg_row, row, D == 128 ? c32 * 4 : half * 4,
+          stage_chunk32(stg_row_of(half * kHalfO + c32 * 32), row, stg_chunk_of(half * kHalfO + c32 * 32),
                         reinterpret_cast<const float*>(o), inv);
         }
         tc_fence_before();
@@ -608,10 +623,10 @@ __global__ void __launch_bounds__(kThreads, 1)
           wsb[128 * D + 256 + row] = l_unit;
         }
         __threadfence();
-        named_bar_sync(1, 256);
+        named_bar_sync(1, kEng);
         uint32_t* ctr = p.split_ctr + static_cast<uint64_t>(it.slot) * p.split_rows + srow;
         if (leader) ctl->bcast = atomicAdd(ctr, 1u);
-        named_bar_sync(1, 256);
+        named_bar_sync(1, kEng);
         const uint32_t done_before = ctl->bcast;
         if (done_before + 1 == si.x) {
           // last chunk: combine every chunk's partial for this row tile
@@ -630,7 +645,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (lc > 0.0f) ltot += lc * exp2f(__ldcg(b + row) - mrun);
           }
           const float inv = ltot > 0.0f ? 1.0f / ltot : 0.0f;
-          named_bar_sync(1, 256);  // every engine thread has read the count
+          named_bar_sync(1, kEng);  // every engine thread has read the count
           if (leader) *ctr = 0;    // ready for the next launch
 #pragma unroll 1
           for (uint32_t c32 = 0; c32 < kHalfO / 32; ++c32) {
@@ -652,7 +667,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 acc[v * 4 + 3] += w * f.w;
               }
             }
-            stage_chunk32(stg_row, row, D == 128 ? c32 * 4 : half * 4, acc, inv);
+            stage_chunk32(stg_row_of(half * kHalfO + c32 * 32), row, stg_chunk_of(half * kHalfO + c32 * 32), acc, inv);
           }
           store_staged(it);
           write_stats(it, mtrue, mrun, ltot);
@@ -666,7 +681,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       // ---------------- next item (items without tiles are written as zeros right away)
       mbar_wait(&ctl->item_full[qi], qiph);
       const ItemDesc it = ctl->items[qi];
-      named_bar_sync(1, 256);  // every engine thread has read the descriptor
+      named_bar_sync(1, kEng);  // every engine thread has read the descriptor
       if (leader) mbar_arrive(&ctl->item_empty[qi]);
       if (++qi == kQueue) { qi = 0; qiph ^= 1; }
       if (it.t == kEnd) break;
@@ -689,7 +704,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           // only the ragged right edge needs a column bound (no bitmap in this mode)
           masked = ragged && it.j0 + j == last_q;
           if (masked) {
-            const int v = static_cast<int>(kv_valid_last) - static_cast<int>(half * 64);
+            const int v = static_cast<int>(kv_valid_last) - static_cast<int>(half * kSC);
             bits.x = v >= 32 ? 0xFFFFFFFFu : (v <= 0 ? 0u : ((1u << v) - 1u));
             bits.y = v >= 64 ? 0xFFFFFFFFu : (v <= 32 ? 0u : ((1u << (v - 32)) - 1u));
           }
@@ -717,24 +732,26 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (tracer) trace_ev<kTrace>(tracing, p, &ctl->trace_count, 21, buf, j);
 
         uint32_t a0[32], a1[32];
-        tmem_ld32(ts + half * 64, a0);
-        tmem_ld32(ts + half * 64 + 32, a1);
+        tmem_ld32(ts + half * kSC, a0);
+        if constexpr (kSC == 64) tmem_ld32(ts + half * kSC + 32, a1);
         tmem_ld_wait();
         if (tracer) trace_ev<kTrace>(tracing, p, &ctl->trace_count, 25, buf, j);
         if (masked) {
           apply_mask(a0, bits.x, sentinel);
-          apply_mask(a1, bits.y, sentinel);
+          if constexpr (kSC == 64) apply_mask(a1, bits.y, sentinel);
         }
-        const float pmax = neg ? fmaxf(chunk_max<true>(a0), chunk_max<true>(a1))
-                               : fmaxf(chunk_max<false>(a0), chunk_max<false>(a1));
+        float pmax = neg ? chunk_max<true>(a0) : chunk_max<false>(a0);
+        if constexpr (kSC == 64) pmax = fmaxf(pmax, neg ? chunk_max<true>(a1) : chunk_max<false>(a1));
         // exchange with the other half (double-buffered by parity); after this barrier every S
         // read of this tile has completed, so P may overwrite S columns [0, 64)
 #ifdef BBM_ABLATE_NO_XCHG  // timing experiments only: wrong results
         float tmax = pmax;
 #else
         ctl->xchg[step & 1][half][row] = pmax;
-        named_bar_sync(1, 256);
-        float tmax = fmaxf(pmax, ctl->xchg[step & 1][half ^ 1][row]);
+        named_bar_sync(1, kEng);
+        float tmax = pmax;
+#pragma unroll
+        for (uint32_t o = 1; o < kP; ++o) tmax = fmaxf(tmax, ctl->xchg[step & 1][(half + o) % kP][row]);
 #endif
         ++step;
         if (tracer) trace_ev<kTrace>(tracing, p, &ctl->trace_count, 26, buf, j);
@@ -772,14 +789,18 @@ __global__ void __launch_bounds__(kThreads, 1)
         // keeps the select inside the exp pass
         if (masked && zero_scale) {
           chunk_exp<true>(a0, bits.x, sl2x2, nm2, pk, lacc);
-          tmem_st16(ts + half * 32, pk);
-          chunk_exp<true>(a1, bits.y, sl2x2, nm2, pk, lacc);
-          tmem_st16(ts + half * 32 + 16, pk);
+          tmem_st16(ts + half * (kSC / 2), pk);
+          if constexpr (kSC == 64) {
+            chunk_exp<true>(a1, bits.y, sl2x2, nm2, pk, lacc);
+            tmem_st16(ts + half * (kSC / 2) + 16, pk);
+          }
         } else {
           chunk_exp<false>(a0, 0, sl2x2, nm2, pk, lacc);
-          tmem_st16(ts + half * 32, pk);
-          chunk_exp<false>(a1, 0, sl2x2, nm2, pk, lacc);
-          tmem_st16(ts + half * 32 + 16, pk);
+          tmem_st16(ts + half * (kSC / 2), pk);
+          if constexpr (kSC == 64) {
+            chunk_exp<false>(a1, 0, sl2x2, nm2, pk, lacc);
+            tmem_st16(ts + half * (kSC / 2) + 16, pk);
+          }
         }
         l += f2_lo(lacc) + f2_hi(lacc);
         if (tracer) trace_ev<kTrace>(tracing, p, &ctl->trace_count, 27, buf, j);
@@ -792,8 +813,10 @@ __global__ void __launch_bounds__(kThreads, 1)
 
       // ---------------- item end: combine the halves' row sums now; the O readout is deferred
       ctl->xchg[step & 1][half][row] = l;
-      named_bar_sync(1, 256);
-      pend.l_unit = l + ctl->xchg[step & 1][half ^ 1][row];
+      named_bar_sync(1, kEng);
+      pend.l_unit = l;
+#pragma unroll
+      for (uint32_t o = 1; o < kP; ++o) pend.l_unit += ctl->xchg[step & 1][(half + o) % kP][row];
       ++step;
       pend.it = it;
       pend.m_run = m_run;
@@ -991,9 +1014,9 @@ void launch_impl(const Prep& prep, const AttnArgs& a, cudaStream_t s, int num_sm
   }
   if (p.total_items == 0) return;
   if (p.trace)  // event-tracing build of the same kernel (bbm_set_trace)
-    attn_fwd_kernel<D, MODE, true><<<grid, kThreads, smem_bytes<D>(), s>>>(tq, tk, tv, to, p);
+    attn_fwd_kernel<D, MODE, true><<<grid, kThreadsOf<D>, smem_bytes<D>(), s>>>(tq, tk, tv, to, p);
   else
-    attn_fwd_kernel<D, MODE, false><<<grid, kThreads, smem_bytes<D>(), s>>>(tq, tk, tv, to, p);
+    attn_fwd_kernel<D, MODE, false><<<grid, kThreadsOf<D>, smem_bytes<D>(), s>>>(tq, tk, tv, to, p);
   BBM_CUDA(cudaGetLastError());
 }
 
