@@ -731,6 +731,22 @@ __global__ void __launch_bounds__(kThreadsOf<D>, 1)
         tc_fence_after();
         if (tracer) trace_ev<kTrace>(tracing, p, &ctl->trace_count, 21, buf, j);
 
+#ifdef BBM_ABLATE_FAST_ENGINE  // timing experiments only: P = 0, no softmax work (MMA-side ceiling)
+        if (true) {
+          uint32_t z[16];
+#pragma unroll
+          for (uint32_t i = 0; i < 16; ++i) z[i] = 0u;
+          tmem_st16(ts + half * (kSC / 2), z);
+          if constexpr (kSC == 64) tmem_st16(ts + half * (kSC / 2) + 16, z);
+          l = 1.0f;
+          m_run = m_true = 0.0f;
+          tmem_st_wait();
+          tc_fence_before();
+          mbar_arrive(&ctl->p_full[buf]);
+          if (j == 0 && pend.valid) finish(pend);
+          continue;
+        }
+#endif
         uint32_t a0[32], a1[32];
         tmem_ld32(ts + half * kSC, a0);
         if constexpr (kSC == 64) tmem_ld32(ts + half * kSC + 32, a1);

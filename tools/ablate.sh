@@ -12,6 +12,7 @@ for v in $VARIANTS; do
     NO_XCHG) FL="-DBBM_ABLATE_NO_XCHG" ;;
     NO_EPI) FL="-DBBM_ABLATE_NO_EPI" ;;
     PARTS4) FL="-DBBM_PARTS128=4" ;;
+    FAST_ENGINE) FL="-DBBM_ABLATE_FAST_ENGINE" ;;
     POLY_NONE) FL="-DBBM_POLY_PAIRS=0x0000u" ;;
     POLY_HALF) FL="-DBBM_POLY_PAIRS=0x5555u" ;;
     POLY_ALL) FL="-DBBM_POLY_PAIRS=0xFFFFu" ;;
