@@ -235,7 +235,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t faddr = smem_u32(fixed), raddr = smem_u32(ring);
       const uint64_t f0 = make_sdesc_sw128(faddr, 16, 1024), f1 = make_sdesc_sw128(faddr + C::kTileBytes, 16, 1024);
       uint32_t qi = 0, qiph = 0, r = 0, rph = 0, fph = 0, aph = 1;
-      uint32_t pph[2] = {0, 0};
+      PhaseBits pph{0u};
       // S_h = f0 s0[64h..]^T, dP_h = f1 s1[64h..]^T: both K-major, K = D, N = 64 partner rows
       auto issue_sdp = [&](uint32_t h, uint32_t stage) {
         const uint32_t sbase = raddr + stage * C::kStageAlloc + h * 8192;
@@ -288,7 +288,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           const uint32_t rnph = r + 1 == C::kStages ? rph ^ 1 : rph;
           for (uint32_t h = 0; h < 2; ++h) {
             mbar_wait(&ctl->p_full[h], pph[h]);
-            pph[h] ^= 1;
+            pph.flip(h);
             if (j == 0 && h == 0) {
               mbar_wait(&ctl->acc_empty, aph);  // previous item's epilogue has read the accumulators
               aph ^= 1;

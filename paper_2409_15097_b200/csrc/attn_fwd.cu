@@ -319,7 +319,7 @@ __global__ void __launch_bounds__(kThreadsOf<D>, 1)
       const uint64_t pol_q = policy_evict_first();
       const uint64_t pol_kv = policy_evict_last();
       uint32_t qi = 0, qiph = 1, qb = 0;
-      uint32_t qph[2] = {1, 1};
+      PhaseBits qph{0x3u};
       ItemDesc pit[kQueue];  // items claimed by the K cursor, replayed by the V cursor
       uint32_t pw = 0, pr = 0;
       auto load_tile = [&](const CUtensorMap* tm, uint32_t seq, uint32_t q, uint32_t slot, uint32_t code,
@@ -352,7 +352,7 @@ __global__ void __launch_bounds__(kThreadsOf<D>, 1)
           pit[pw++ % kQueue] = d;
           kentry = entry_of<MODE>(p, d.rt, d.j0);
           mbar_wait(&ctl->q_empty[qb], qph[qb]);
-          qph[qb] ^= 1;
+          qph.flip(qb);
           mbar_arrive_expect_tx(&ctl->q_full[qb], C::kTileBytes);
           for (uint32_t b = 0; b < C::kBoxes; ++b)
             tma_load_3d(sq + qb * C::kTileBytes + b * kBoxBytes, &tm_q, &ctl->q_full[qb], b * 64,
@@ -413,7 +413,7 @@ __global__ void __launch_bounds__(kThreadsOf<D>, 1)
       constexpr uint32_t idesc_o = make_idesc_bf16(128, D, false, true);
       const uint32_t qaddr = smem_u32(sq), raddr = smem_u32(ring);
       uint32_t qi = 0, qiph = 0, k = 0, qb = 0, items = 0;
-      uint32_t q_ph[2] = {0, 0}, p_ph[kSBufs] = {}, oe_ph[2] = {1, 1};
+      PhaseBits q_ph{0u}, p_ph{0u}, oe_ph{0x3u};
       for (;;) {
         mbar_wait(&ctl->item_full[qi], qiph);
         const ItemDesc it = ctl->items[qi];
@@ -431,7 +431,7 @@ __global__ void __launch_bounds__(kThreadsOf<D>, 1)
             if (k >= kSBufs) mbar_wait(&ctl->pv_done[buf], ((k - kSBufs) / kSBufs) & 1);
             if (j == 0) {
               mbar_wait(&ctl->q_full[qb], q_ph[qb]);
-              q_ph[qb] ^= 1;
+              q_ph.flip(qb);
             }
             const uint32_t kseq = kseq_of(k);
             const uint32_t slot = kseq % C::kRing;
@@ -455,11 +455,11 @@ __global__ void __launch_bounds__(kThreadsOf<D>, 1)
             }
           } else {
             mbar_wait(&ctl->p_full[buf], p_ph[buf]);
-            p_ph[buf] ^= 1;
+            p_ph.flip(buf);
             trace_ev<kTrace>(tracing, p, &ctl->trace_count, 14, buf, j);
             if (j == 0) {
               mbar_wait(&ctl->o_empty[ob], oe_ph[ob]);
-              oe_ph[ob] ^= 1;
+              oe_ph.flip(ob);
             }
             const uint32_t vseq = vseq_of(k);
             const uint32_t slot = vseq % C::kRing;
@@ -508,8 +508,8 @@ __global__ void __launch_bounds__(kThreadsOf<D>, 1)
     uint2 nbits = make_uint2(0xFFFFFFFFu, 0xFFFFFFFFu);  // mask bits of the next tile
     uint32_t nentry = 0;                                // its list entry (dense_binblk)
     bool have_next_bits = false;                        // prefetched for the next item
-    uint32_t s_ph[kSBufs] = {}, qi = 0, qiph = 0, items = 0;
-    uint32_t o_ph[2] = {0, 0};
+    PhaseBits s_ph{0u}, o_ph{0u};
+    uint32_t qi = 0, qiph = 0, items = 0;
     // The epilogue of an item is DEFERRED until the next item's first tile has been handed to
     // the tensor core: the engine never idles while the item's last PV drains (the two items use
     // different O accumulators). At most one epilogue is pending at a time.
@@ -576,7 +576,7 @@ __global__ void __launch_bounds__(kThreadsOf<D>, 1)
       const uint32_t to = to_base + pd.ob * D;
       if (leader) bulk_wait_group_read<0>();  // staging buffers free again
       mbar_wait(&ctl->o_full[pd.ob], o_ph[pd.ob]);
-      o_ph[pd.ob] ^= 1;
+      o_ph.flip(pd.ob);
       tc_fence_after();
       named_bar_sync(1, kEng);
       if (tracer) trace_ev<kTrace>(tracing, p, &ctl->trace_count, 23, 0, it.t);
@@ -727,7 +727,7 @@ __global__ void __launch_bounds__(kThreadsOf<D>, 1)
 
         if (tracer) trace_ev<kTrace>(tracing, p, &ctl->trace_count, 20, buf, j);
         mbar_wait(&ctl->s_full[buf], s_ph[buf]);
-        s_ph[buf] ^= 1;
+        s_ph.flip(buf);
         tc_fence_after();
         if (tracer) trace_ev<kTrace>(tracing, p, &ctl->trace_count, 21, buf, j);
 
@@ -748,9 +748,17 @@ __global__ void __launch_bounds__(kThreadsOf<D>, 1)
         }
 #endif
         uint32_t a0[32], a1[32];
+#ifdef BBM_ABLATE_NO_SLOAD  // timing experiments only: scores are not read from TMEM
+#pragma unroll
+        for (uint32_t i = 0; i < 32; ++i) {
+          a0[i] = __float_as_uint(static_cast<float>(i ^ lane ^ j) * 0.01f);
+          a1[i] = __float_as_uint(static_cast<float>(i ^ lane ^ k) * 0.01f);
+        }
+#else
         tmem_ld32(ts + half * kSC, a0);
         if constexpr (kSC == 64) tmem_ld32(ts + half * kSC + 32, a1);
         tmem_ld_wait();
+#endif
         if (tracer) trace_ev<kTrace>(tracing, p, &ctl->trace_count, 25, buf, j);
         if (masked) {
           apply_mask(a0, bits.x, sentinel);

@@ -343,10 +343,20 @@ __device__ __forceinline__ void exp2_poly2(float x0, float x1, float& e0, float&
   pv = ffma2(pv, fr, f2_pack(0.69511664f, 0.69511664f));
   pv = ffma2(pv, fr, f2_pack(1.0f, 1.0f));
 #endif
-  const uint32_t tl = static_cast<uint32_t>(t), th = static_cast<uint32_t>(t >> 32);
-  e0 = __uint_as_float(static_cast<uint32_t>(pv) + (tl << 23));
-  e1 = __uint_as_float(static_cast<uint32_t>(pv >> 32) + (th << 23));
+  uint32_t tl, th, pl, ph;
+  asm("mov.b64 {%0, %1}, %2;" : "=r"(tl), "=r"(th) : "l"(t));
+  asm("mov.b64 {%0, %1}, %2;" : "=r"(pl), "=r"(ph) : "l"(pv));
+  e0 = __uint_as_float(pl + (tl << 23));  // one IMAD per lane
+  e1 = __uint_as_float(ph + (th << 23));
 }
+
+// Phase bits of a small array of mbarriers in one register: a dynamically indexed uint32_t
+// array would be placed in local memory (an LDL/STL pair on every wait).
+struct PhaseBits {
+  uint32_t bits;
+  __device__ __forceinline__ uint32_t operator[](uint32_t i) const { return (bits >> i) & 1u; }
+  __device__ __forceinline__ void flip(uint32_t i) { bits ^= 1u << i; }
+};
 
 __device__ __forceinline__ float fmax3(float a, float b, float c) {
   float d;

@@ -20,19 +20,25 @@ for v in $VARIANTS; do
     DEG2_6) FL="-DBBM_POLY_DEG2" ;;
     DEG2_8) FL="-DBBM_POLY_DEG2 -DBBM_POLY_PAIRS=0x0F0Fu" ;;
     DEG2_4) FL="-DBBM_POLY_DEG2 -DBBM_POLY_PAIRS=0x0303u" ;;
+    NO_SLOAD) FL="-DBBM_ABLATE_NO_SLOAD" ;;
+    LACC1) FL="-DBBM_LACC=1" ;;
+    LACC2) FL="-DBBM_LACC=2" ;;
+    LACC8) FL="-DBBM_LACC=8" ;;
+    *) FL="${FLAGS_OF_VARIANT:?unknown variant}" ;;
   esac
   rm -rf /tmp/abl_$v && mkdir -p /tmp/abl_$v
   cp -r "$ROOT/paper_2409_15097_b200" "$ROOT/include" /tmp/abl_$v/
   (cd /tmp/abl_$v/paper_2409_15097_b200/csrc && sed -i "s|^NVFLAGS := |NVFLAGS := $FL |; s|^BUILD := .*|BUILD := /tmp/abl_obj_$v|" Makefile && make -j8 >/dev/null)
   cp /tmp/abl_$v/paper_2409_15097_b200/libbbm.so "$ROOT/abl_bin/libbbm_$v.so"
 done
+SPECS_Q=${ABL_SPECS:-'"c2 binblk" "c2 dense" "c4 dense-binblk" "c5 binblk" "c3 binblk"'}
 cat > "$ROOT/abl_bin/run.sh" <<EOS
 #!/bin/bash
 mkdir -p gpurun_out
 cp paper_2409_15097_b200/libbbm.so /tmp/libbbm_real.so
 for v in base $VARIANTS; do
   if [ \$v = base ]; then cp /tmp/libbbm_real.so paper_2409_15097_b200/libbbm.so; else cp abl_bin/libbbm_\$v.so paper_2409_15097_b200/libbbm.so; fi
-  for spec in "c2 binblk" "c2 dense" "c4 dense-binblk"; do set -- \$spec
+  for spec in $SPECS_Q; do set -- \$spec
     echo -n "\$v "; python bench.py --config \$1 --variant \$2 --steps 10 --warmup 3 --no-cpu-baseline --no-e2e 2>&1 | tail -1 | python3 tools/bench_summary.py
   done
 done > gpurun_out/ablate.txt 2>&1
