@@ -216,18 +216,13 @@ constexpr uint32_t kPolyPairs = BBM_POLY_PAIRS;
 // P chunk: 32 scores -> 16 packed bf16x2; accumulates the fp32 sum of the unrounded
 // exponentials into the packed pair `lacc`. Scale/shift and the sum run two lanes per
 // instruction (FFMA2 / FADD2).
-template <bool kMasked>
-__device__ __forceinline__ void chunk_exp(const uint32_t (&r)[32], uint32_t mw, uint64_t sl2x2,
-                                          uint64_t neg_m_x2, uint32_t (&pk)[16], uint64_t& lacc) {
+__device__ __forceinline__ void chunk_exp(const uint32_t (&r)[32], uint64_t sl2x2, uint64_t neg_m_x2,
+                                          uint32_t (&pk)[16], uint64_t& lacc) {
 #pragma unroll
   for (uint32_t i = 0; i < 32; i += 2) {
     const uint64_t x = ffma2(f2_pack(__uint_as_float(r[i]), __uint_as_float(r[i + 1])), sl2x2,
                              neg_m_x2);
-    float x0 = f2_lo(x), x1 = f2_hi(x);
-    if constexpr (kMasked) {
-      x0 = ((mw >> i) & 1u) ? x0 : -INFINITY;
-      x1 = ((mw >> (i + 1)) & 1u) ? x1 : -INFINITY;
-    }
+    const float x0 = f2_lo(x), x1 = f2_hi(x);
     float e0, e1;
     if ((kPolyPairs >> ((i / 2) & 15)) & 1u) {
       exp2_poly2(x0, x1, e0, e1);  // this pair on the FMA pipe
@@ -492,13 +487,11 @@ __global__ void __launch_bounds__(kThreadsOf<D>, 1)
     const bool leader = (warp == 4 && lane == 0);
     const bool tracer = (quad == 0 && lane == 0 && half == 0);
     const bool neg = p.sl2 < 0.0f;
-    const bool zero_scale = p.sl2 == 0.0f;
     const float abs_sl2 = fabsf(p.sl2);
     const bool ragged = (p.n % 128) != 0;
     const uint32_t last_q = p.kcols - 1;
     const uint32_t kv_valid_last = static_cast<uint32_t>(p.n - static_cast<uint64_t>(last_q) * 128);
-    // masked scores: -inf, or +inf with a negative scale; with a zero scale the sentinel only
-    // has to drop out of the max (the exp pass selects explicitly)
+    // masked scores: -inf, or +inf with a negative scale, so that scale * sentinel = -inf
     const uint32_t sentinel = neg ? 0x7F800000u : 0xFF800000u;
     constexpr uint32_t kHalfO = D / kP;  // O columns per part
     const uint32_t to_base = tmem + C::kOCol + lane_off;
@@ -809,22 +802,12 @@ __global__ void __launch_bounds__(kThreadsOf<D>, 1)
         uint64_t lacc = 0;
         const uint64_t sl2x2 = f2_pack(p.sl2, p.sl2), nm2 = f2_pack(-m_use, -m_use);
         // this half's 64 columns -> 32 packed P columns at [32 * half, 32 * half + 32); masked
-        // scores already hold the sentinel, except with a zero scale (inf * 0 = NaN), which
-        // keeps the select inside the exp pass
-        if (masked && zero_scale) {
-          chunk_exp<true>(a0, bits.x, sl2x2, nm2, pk, lacc);
-          tmem_st16(ts + half * (kSC / 2), pk);
-          if constexpr (kSC == 64) {
-            chunk_exp<true>(a1, bits.y, sl2x2, nm2, pk, lacc);
-            tmem_st16(ts + half * (kSC / 2) + 16, pk);
-          }
-        } else {
-          chunk_exp<false>(a0, 0, sl2x2, nm2, pk, lacc);
-          tmem_st16(ts + half * (kSC / 2), pk);
-          if constexpr (kSC == 64) {
-            chunk_exp<false>(a1, 0, sl2x2, nm2, pk, lacc);
-            tmem_st16(ts + half * (kSC / 2) + 16, pk);
-          }
+        // scores already hold the sentinel (the host never passes a zero scale, see launch_impl)
+        chunk_exp(a0, sl2x2, nm2, pk, lacc);
+        tmem_st16(ts + half * (kSC / 2), pk);
+        if constexpr (kSC == 64) {
+          chunk_exp(a1, sl2x2, nm2, pk, lacc);
+          tmem_st16(ts + half * (kSC / 2) + 16, pk);
         }
         l += f2_lo(lacc) + f2_hi(lacc);
         if (tracer) trace_ev<kTrace>(tracing, p, &ctl->trace_count, 27, buf, j);
@@ -1009,6 +992,10 @@ void launch_impl(const Prep& prep, const AttnArgs& a, cudaStream_t s, int num_sm
   p.units = plan.units;
   p.total_items = static_cast<uint32_t>(a.slots * plan.units);
   p.sl2 = a.scale * 1.4426950408889634f;
+  // A zero scale would turn the masked sentinel into inf * 0 = NaN. 2^-100 instead: every
+  // visible score's offset from the row max is then ~1e-28 and exp2 of it rounds to exactly 1.0f
+  // (uniform weights, as with scale 0), while masked keys stay at -inf.
+  if (p.sl2 == 0.0f) p.sl2 = 7.8886090522101181e-31f;
   p.list = km.list;
   p.bitmaps = km.bitmaps;
   p.mask = reinterpret_cast<const uint4*>(km.mask);
