@@ -753,7 +753,9 @@ __global__ void __launch_bounds__(kThreadsOf<D>, 1)
         tmem_ld_wait();
 #endif
         if (tracer) trace_ev<kTrace>(tracing, p, &ctl->trace_count, 25, buf, j);
-        if (masked) {
+        // binblk reads bits for every tile; a warp whose 32 rows see every key of the tile skips
+        // the selects (they would be no-ops)
+        if (masked && !__all_sync(0xffffffffu, (kSC == 64 ? (bits.x & bits.y) : bits.x) == 0xFFFFFFFFu)) {
           apply_mask(a0, bits.x, sentinel);
           if constexpr (kSC == 64) apply_mask(a1, bits.y, sentinel);
         }
