@@ -286,7 +286,7 @@ __global__ void __launch_bounds__(kThreadsOf<D>, 1)
     }
     for (uint32_t r = 0; r < kQueue; ++r) {
       mbar_init(&ctl->item_full[r], 1);
-      mbar_init(&ctl->item_empty[r], 3);  // S issuer + PV issuer + softmax engine
+      mbar_init(&ctl->item_empty[r], 2 + kParts<D> * 4);  // S issuer + PV issuer + engine warps
     }
     fence_barrier_init();
   }
@@ -578,13 +578,16 @@ __global__ void __launch_bounds__(kThreadsOf<D>, 1)
 #ifdef BBM_ABLATE_NO_EPI  // timing experiments only (tools/ablate.sh): O is never written
         if (false)
 #endif
+        {
+          // both 32-column loads in flight before the single wait
+          uint32_t o[kHalfO / 32][32];
 #pragma unroll
-        for (uint32_t c32 = 0; c32 < kHalfO / 32; ++c32) {
-          uint32_t o[32];
-          tmem_ld32(to + half * kHalfO + c32 * 32, o);
+          for (uint32_t c32 = 0; c32 < kHalfO / 32; ++c32) tmem_ld32(to + half * kHalfO + c32 * 32, o[c32]);
           tmem_ld_wait();
-          stage_chunk32(stg_row_of(half * kHalfO + c32 * 32), row, stg_chunk_of(half * kHalfO + c32 * 32),
-                        reinterpret_cast<const float*>(o), inv);
+#pragma unroll
+          for (uint32_t c32 = 0; c32 < kHalfO / 32; ++c32)
+            stage_chunk32(stg_row_of(half * kHalfO + c32 * 32), row, stg_chunk_of(half * kHalfO + c32 * 32),
+                          reinterpret_cast<const float*>(o[c32]), inv);
         }
         tc_fence_before();
         mbar_arrive(&ctl->o_empty[pd.ob]);  // the accumulator may be overwritten from here on
@@ -674,8 +677,8 @@ __global__ void __launch_bounds__(kThreadsOf<D>, 1)
       // ---------------- next item (items without tiles are written as zeros right away)
       mbar_wait(&ctl->item_full[qi], qiph);
       const ItemDesc it = ctl->items[qi];
-      named_bar_sync(1, kEng);  // every engine thread has read the descriptor
-      if (leader) mbar_arrive(&ctl->item_empty[qi]);
+      __syncwarp();  // every lane of this warp has read the descriptor
+      if (lane == 0) mbar_arrive(&ctl->item_empty[qi]);
       if (++qi == kQueue) { qi = 0; qiph ^= 1; }
       if (it.t == kEnd) break;
       if (it.nt == 0) {
