@@ -99,6 +99,21 @@ def main():
                 per["epilogue (O ready -> done)"].append(t - last[(s, 23)])
             if code == 20 and (s, 24) in last:
                 per["epilogue done -> next softmax wait"].append(t - last.pop((s, 24)))
+        # engine time budget: every cycle between consecutive engine events gets one label
+        eng = [e for e in evs if 20 <= e[1] <= 27]
+        lab = {(20, 21): "wait S", (21, 25): "S tmem load", (25, 26): "mask + max + exchange",
+               (26, 27): "exp + P pack", (27, 22): "P store + arrive", (22, 23): "o_full wait + barrier",
+               (23, 24): "epilogue", (24, 20): "after epilogue -> next tile", (22, 20): "tile gap"}
+        budget = collections.Counter()
+        for (ta, ca, _, _), (tb, cb, _, ab) in zip(eng, eng[1:]):
+            name = lab.get((ca, cb), f"{ca}->{cb}")
+            if cb in (20, 21):
+                name += " (item start)" if ab == 0 else " (in item)"
+            budget[name] += tb - ta
+        tot = sum(budget.values())
+        print(f"  engine budget over {tot} cycles:")
+        for name, v in budget.most_common():
+            print(f"     {name:40s} {v / tot:6.1%}")
         span = evs[-1][0] - t0
         n_s = sum(1 for e in evs if e[1] == 10)
         print(f"CTA {c}: span {span} cycles, {n_s} S tiles, {span / max(1, n_s):.0f} cycles/tile (both streams)")
