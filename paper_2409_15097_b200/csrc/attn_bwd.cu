@@ -67,8 +67,8 @@ struct BwdParams {
   uint32_t list_stride;
   const uint32_t* order;      // [tiles] LPT order
   const uint4* bitmaps;       // list-position tile-major bits (row bitmaps | transposed)
-  const float* lse2;          // [slots][rows_pad]
-  const float* delta;         // [slots][rows_pad]
+  const float* lse2;          // [slots][rows_pad], NEGATED (-lse2, rowstats_kernel)
+  const float* delta;         // [slots][rows_pad], NEGATED (-delta)
   uint32_t rows_pad;          // krows * 128
   uint32_t* ctr;              // [2] next item, finished CTAs
   __nv_bfloat16* out0;        // dq | dk
@@ -331,12 +331,14 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (it.t == kEnd) break;
       const uint64_t grow = static_cast<uint64_t>(it.tile) * 128 + row;
       if (it.nt > 0) {
-        float my_lse = 0.0f, my_delta = 0.0f;
+        uint64_t my_nl = 0, my_nd = 0;  // (-lse2, -delta) of this thread's query row, both lanes
         if constexpr (SIDE == kSideDQ) {
           const uint64_t o = static_cast<uint64_t>(it.slot) * p.rows_pad + grow;
-          my_lse = p.lse2[o];
-          my_delta = p.delta[o];
+          const float nl = p.lse2[o], nd = p.delta[o];
+          my_nl = f2_pack(nl, nl);
+          my_nd = f2_pack(nd, nd);
         }
+        const uint64_t sl2x2 = f2_pack(sl2, sl2);
         for (uint32_t j = 0; j < it.nt; ++j) {
           const uint32_t e = bwd_entry(p, it.tile, j);
           const uint32_t u = e & 0x7FFFFFFFu;
@@ -375,22 +377,24 @@ __global__ void __launch_bounds__(kThreads, 1)
             uint32_t pk[16], dk[16];
 #pragma unroll
             for (uint32_t i = 0; i < 32; i += 2) {
-              float l0 = my_lse, l1 = my_lse, d0 = my_delta, d1 = my_delta;
-              if constexpr (SIDE == kSideDKDV) {
-                const float2 lv = *reinterpret_cast<const float2*>(vec + c32 * 32 + i);
-                const float2 dv = *reinterpret_cast<const float2*>(vec + 128 + c32 * 32 + i);
-                l0 = lv.x, l1 = lv.y, d0 = dv.x, d1 = dv.y;
+              uint64_t nl = my_nl, nd = my_nd;
+              if constexpr (SIDE == kSideDKDV) {  // per key pair: the partner query rows' values
+                nl = *reinterpret_cast<const uint64_t*>(vec + c32 * 32 + i);
+                nd = *reinterpret_cast<const uint64_t*>(vec + 128 + c32 * 32 + i);
               }
-              float p0 = fast_exp2(__uint_as_float(s[i]) * sl2 - l0);
-              float p1 = fast_exp2(__uint_as_float(s[i + 1]) * sl2 - l1);
+              // x = S sl2 - lse2, two lanes per instruction
+              const uint64_t x = ffma2(f2_pack(__uint_as_float(s[i]), __uint_as_float(s[i + 1])), sl2x2, nl);
+              float p0 = fast_exp2(f2_lo(x));
+              float p1 = fast_exp2(f2_hi(x));
               if (masked) {
                 p0 = ((mw >> i) & 1u) ? p0 : 0.0f;
                 p1 = ((mw >> (i + 1)) & 1u) ? p1 : 0.0f;
               }
-              const float g0 = p0 * (__uint_as_float(dp[i]) - d0);
-              const float g1 = p1 * (__uint_as_float(dp[i + 1]) - d1);
+              // dS = P (dP - delta)
+              const uint64_t g = fmul2(f2_pack(p0, p1),
+                                       fadd2(f2_pack(__uint_as_float(dp[i]), __uint_as_float(dp[i + 1])), nd));
               pk[i / 2] = pack_bf16x2(p0, p1);
-              dk[i / 2] = pack_bf16x2(g0, g1);
+              dk[i / 2] = pack_bf16x2(f2_lo(g), f2_hi(g));
             }
             tmem_st16(ts + c32 * 16, pk);        // P over this half's own S columns
             tmem_st16(ts + 128 + c32 * 16, dk);  // dS over this half's own dP columns
@@ -454,13 +458,14 @@ __global__ void __launch_bounds__(kThreads, 1)
 }
 
 // delta = rowsum(dO * O) (engine.hpp:366-372), lse2 = (row_max + ln row_sum) * log2(e); rows with
-// row_sum == 0 (fully masked) and rows past n: lse2 = +inf (their P is 0), delta = 0.
+// row_sum == 0 (fully masked) and rows past n: lse2 = +inf (their P is 0), delta = 0. Both are
+// stored NEGATED (nlse2, ndelta) so the engine adds them with packed FFMA2 / FADD2.
 // One warp per row.
 template <typename OT>
 __global__ void rowstats_kernel(const OT* __restrict__ o, const __nv_bfloat16* __restrict__ dout,
                                 const float* __restrict__ row_max, const float* __restrict__ row_sum,
                                 uint64_t slots, uint64_t n, uint32_t d, uint32_t rows_pad,
-                                float* __restrict__ lse2, float* __restrict__ delta) {
+                                float* __restrict__ nlse2, float* __restrict__ ndelta) {
   const uint64_t total = slots * rows_pad;
   const uint32_t lane = threadIdx.x & 31;
   for (uint64_t w = (blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x) >> 5; w < total;
@@ -481,8 +486,8 @@ __global__ void rowstats_kernel(const OT* __restrict__ o, const __nv_bfloat16* _
 #pragma unroll
     for (uint32_t m = 16; m; m >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, m);
     if (lane == 0) {
-      lse2[w] = l;
-      delta[w] = r < n ? acc : 0.0f;
+      nlse2[w] = -l;
+      ndelta[w] = r < n ? -acc : 0.0f;
     }
   }
 }
