@@ -161,7 +161,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (uint32_t r = 0; r < kQueue; ++r) {
       mbar_init(&ctl->item_full[r], 1);
-      mbar_init(&ctl->item_empty[r], 2);
+      mbar_init(&ctl->item_empty[r], 1 + 8);  // MMA issuer + the 8 engine warps
     }
     fence_barrier_init();
   }
@@ -317,7 +317,6 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t quad = warp & 3;
     const uint32_t row = quad * 32 + lane;  // TMEM lane: key (dkdv) or query (dq) in the tile
     const uint32_t lane_off = (quad * 32) << 16;
-    const bool leader = warp == 4 && lane == 0;
     const float sl2 = p.sl2;
     uint32_t qi = 0, qiph = 0, sph = 0, acph = 0, r = 0;
     const uint32_t last = (static_cast<uint32_t>(p.n) + 127) / 128 - 1;
@@ -325,8 +324,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (;;) {
       mbar_wait(&ctl->item_full[qi], qiph);
       const ItemDesc it = ctl->items[qi];
-      named_bar_sync(1, 256);
-      if (leader) mbar_arrive(&ctl->item_empty[qi]);
+      __syncwarp();  // every lane of this warp has read the descriptor
+      if (lane == 0) mbar_arrive(&ctl->item_empty[qi]);
       if (++qi == kQueue) { qi = 0; qiph ^= 1; }
       if (it.t == kEnd) break;
       const uint64_t grow = static_cast<uint64_t>(it.tile) * 128 + row;
