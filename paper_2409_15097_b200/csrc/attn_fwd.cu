@@ -85,8 +85,12 @@ struct FwdParams {
 #endif
 template <int D>
 constexpr uint32_t kParts = D == 128 ? BBM_PARTS128 : 2;
+static_assert(BBM_PARTS128 == 2, "the register split below assumes two engine warpgroups");
+// warpgroup 0: producer / MMA issuers / TMEM allocator; 1..kParts: softmax engine; last: epilogue
 template <int D>
-constexpr uint32_t kThreadsOf = 128 + 128 * kParts<D>;
+constexpr uint32_t kThreadsOf = 256 + 128 * kParts<D>;
+constexpr uint32_t kEngineRegs = 168;  // setmaxnreg: 2 x 128 x 168 + 2 x 128 x 88 = 65536
+constexpr uint32_t kOtherRegs = 88;
 constexpr uint32_t kTraceCap = 8192;  // events per traced CTA
 constexpr uint32_t kQueue = 8;        // item queue depth (items open between the producer and the PV issuer)
 
@@ -128,7 +132,7 @@ template <int D>
 struct Cfg {
   static constexpr uint32_t kBoxes = D / 64;
   static constexpr uint32_t kTileBytes = kBoxes * kBoxBytes;  // one 128 x D bf16 tile
-  static constexpr uint32_t kRing = (D == 64) ? 10 : (BBM_PARTS128 > 2 ? 3 : 4);  // K/V ring slots
+  static constexpr uint32_t kRing = (D == 64) ? 9 : 3;  // K/V ring slots
   static constexpr uint32_t kStageBytes = kBoxBytes;          // epilogue staging (two buffers)
   static constexpr uint32_t kTmemCols = 512;
   static constexpr uint32_t kOCol = kSBufs * 128;
@@ -140,16 +144,27 @@ struct ItemDesc {
 
 // Everything that is not a tile lives behind the tiles in the same dynamic allocation (no static
 // smem, so the dynamic base is the 1024-byte aligned start of the CTA's window).
+// Row statistics of a finished item, handed from the softmax engine to the epilogue warpgroup
+// (one per O accumulator).
+template <uint32_t kXP>
+struct ItemStats {
+  ItemDesc item;
+  float l[kXP][128];  // per-part row sums
+  float m_run[128], m_true[128];
+};
+
 template <uint32_t kRing, uint32_t kXP>
 struct SmemCtl {
   uint64_t q_full[2], q_empty[2], s_full[kSBufs], p_full[kSBufs], o_full[2], o_empty[2], pv_done[kSBufs];
+  uint64_t stats_full[2], stats_empty[2];
   uint64_t ring_full[kRing], ring_empty[kRing];
   uint64_t item_full[kQueue], item_empty[kQueue];
   ItemDesc items[kQueue];
   uint32_t tmem_base;
   uint32_t trace_count;
   uint32_t bcast;
-  float xchg[2][kXP][128];  // [exchange parity][part][row]: partial row max / row sum
+  float xchg[2][kXP][128];  // [exchange parity][part][row]: partial row max
+  ItemStats<kXP> stats[2];
 };
 
 template <int D>
@@ -278,7 +293,9 @@ __global__ void __launch_bounds__(kThreadsOf<D>, 1)
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&ctl->o_full[b], 1);
-      mbar_init(&ctl->o_empty[b], 128 * kParts<D>);
+      mbar_init(&ctl->o_empty[b], 128);                 // the epilogue warpgroup's threads
+      mbar_init(&ctl->stats_full[b], 4 * kParts<D>);    // engine warps
+      mbar_init(&ctl->stats_empty[b], 4);               // epilogue warps
     }
     for (uint32_t r = 0; r < C::kRing; ++r) {
       mbar_init(&ctl->ring_full[r], 1);
@@ -304,7 +321,10 @@ __global__ void __launch_bounds__(kThreadsOf<D>, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = ctl->tmem_base;
+  const bool engine_wg = warp >= 4 && warp < 4 + 4 * kParts<D>;
 
+  if (warp < 4) {
+  setmaxnreg_dec<kOtherRegs>();
   if (warp == 0) {
     // ------------------------------------------------------------------ producer
     // Loads follow the MMA issuers' consumption order (kseq_of / vseq_of): a K cursor runs kSBufs
@@ -475,7 +495,9 @@ __global__ void __launch_bounds__(kThreadsOf<D>, 1)
         }
       }
     }
-  } else if (warp >= 4) {
+  }
+  } else if (engine_wg) {
+    setmaxnreg_inc<kEngineRegs>();
     // ------------------------------------------------------------------ softmax engine
     constexpr uint32_t kP = kParts<D>;
     constexpr uint32_t kSC = 128 / kP;        // score columns per part
@@ -501,20 +523,8 @@ __global__ void __launch_bounds__(kThreadsOf<D>, 1)
     uint2 nbits = make_uint2(0xFFFFFFFFu, 0xFFFFFFFFu);  // mask bits of the next tile
     uint32_t nentry = 0;                                // its list entry (dense_binblk)
     bool have_next_bits = false;                        // prefetched for the next item
-    PhaseBits s_ph{0u}, o_ph{0u};
+    PhaseBits s_ph{0u}, se_ph{0x3u};
     uint32_t qi = 0, qiph = 0, items = 0;
-    // The epilogue of an item is DEFERRED until the next item's first tile has been handed to
-    // the tensor core: the engine never idles while the item's last PV drains (the two items use
-    // different O accumulators). At most one epilogue is pending at a time.
-    struct Pending {
-      ItemDesc it;
-      float l_unit, m_run, m_true;
-      uint32_t ob;
-      bool valid;
-    };
-    Pending pend{};
-    pend.valid = false;
-
     auto write_stats = [&](const ItemDesc& it, float m_true2, float m_run2, float l_tot) {
       const uint64_t grow = static_cast<uint64_t>(it.rt) * 128 + row;
       if (half == 0 && grow < p.n) {
@@ -532,22 +542,6 @@ __global__ void __launch_bounds__(kThreadsOf<D>, 1)
       for (uint32_t v = 0; v < kHalfO / 8; ++v) dst[v] = make_uint4(0, 0, 0, 0);
       write_stats(it, -INFINITY, -INFINITY, 0.0f);
     };
-    // TMA-store the staged O tile of item `it` (called by every engine thread)
-    auto store_staged = [&](const ItemDesc& it) {
-      fence_proxy_async_smem();
-      named_bar_sync(1, kEng);
-      if (leader) {
-        tma_store_3d(&tm_o, stage, 0, it.rt * 128, it.slot);
-        if (D == 128) tma_store_3d(&tm_o, stage + C::kStageBytes, 64, it.rt * 128, it.slot);
-        bulk_commit_group();
-      }
-    };
-    // D=128: half h stages columns [64h, 64h+64) in buffer h; D=64: both halves share buffer 0,
-    // 32 columns (4 chunks) each
-    // staged output column c goes to box c / 64, 16-byte chunk (c % 64) / 8 of the row
-    auto stg_row_of = [&](uint32_t c) { return stage + (c / 64) * C::kStageBytes + row * 128; };
-    auto stg_chunk_of = [&](uint32_t c) { return (c % 64) / 8; };
-
     // mask bits (and, for dense_binblk, the list entry) of tile jj of item `it`; the bitmap
     // address depends only on (row tile, list position), never on a loaded value
     auto load_bits = [&](const ItemDesc& it, uint32_t jj, uint2& bits, uint32_t& entry) {
@@ -561,116 +555,6 @@ __global__ void __launch_bounds__(kThreadsOf<D>, 1)
                          : make_uint2(__ldg(reinterpret_cast<const uint32_t*>(bp) + half), 0u);
       }
       if constexpr (MODE == kModeDenseBinblk) entry = entry_of<MODE>(p, it.rt, jj);
-    };
-
-    auto finish = [&](const Pending& pd) {
-      const ItemDesc& it = pd.it;
-      const float l_unit = pd.l_unit, m_run = pd.m_run, m_true = pd.m_true;
-      const uint32_t to = to_base + pd.ob * D;
-      if (leader) bulk_wait_group_read<0>();  // staging buffers free again
-      mbar_wait(&ctl->o_full[pd.ob], o_ph[pd.ob]);
-      o_ph.flip(pd.ob);
-      tc_fence_after();
-      named_bar_sync(1, kEng);
-      if (tracer) trace_ev<kTrace>(tracing, p, &ctl->trace_count, 23, 0, it.t);
-      if (it.split == kNoSplit) {
-        const float inv = l_unit > 0.0f ? 1.0f / l_unit : 0.0f;
-#ifdef BBM_ABLATE_NO_EPI  // timing experiments only (tools/ablate.sh): O is never written
-        if (false)
-#endif
-        {
-          // both 32-column loads in flight before the single wait
-          uint32_t o[kHalfO / 32][32];
-#pragma unroll
-          for (uint32_t c32 = 0; c32 < kHalfO / 32; ++c32) tmem_ld32(to + half * kHalfO + c32 * 32, o[c32]);
-          tmem_ld_wait();
-#pragma unroll
-          for (uint32_t c32 = 0; c32 < kHalfO / 32; ++c32)
-            stage_chunk32(stg_row_of(half * kHalfO + c32 * 32), row, stg_chunk_of(half * kHalfO + c32 * 32),
-                          reinterpret_cast<const float*>(o[c32]), inv);
-        }
-        tc_fence_before();
-        mbar_arrive(&ctl->o_empty[pd.ob]);  // the accumulator may be overwritten from here on
-#ifndef BBM_ABLATE_NO_EPI
-        store_staged(it);
-#endif
-        write_stats(it, m_true, m_run, l_unit);
-      } else {
-        // ---- split-KV chunk: publish the unnormalized partial, the last chunk combines
-        const uint32_t srow = it.split >> 8, chunk = it.split & 0xFF;
-        const uint2 si = p.split_info[srow];  // {chunks, first workspace chunk}
-        const uint64_t blk = static_cast<uint64_t>(128) * (D + 3);
-        float* wsb = p.ws + (static_cast<uint64_t>(it.slot) * p.split_chunks + si.y + chunk) * blk;
-#pragma unroll
-        for (uint32_t c32 = 0; c32 < kHalfO / 32; ++c32) {
-          uint32_t o[32];
-          tmem_ld32(to + half * kHalfO + c32 * 32, o);
-          tmem_ld_wait();
-          uint4* dst = reinterpret_cast<uint4*>(wsb + row * D + half * kHalfO + c32 * 32);
-#pragma unroll
-          for (uint32_t v = 0; v < 8; ++v)
-            dst[v] = make_uint4(o[v * 4], o[v * 4 + 1], o[v * 4 + 2], o[v * 4 + 3]);
-        }
-        tc_fence_before();
-        mbar_arrive(&ctl->o_empty[pd.ob]);
-        if (half == 0) {
-          wsb[128 * D + row] = m_run;
-          wsb[128 * D + 128 + row] = m_true;
-          wsb[128 * D + 256 + row] = l_unit;
-        }
-        __threadfence();
-        named_bar_sync(1, kEng);
-        uint32_t* ctr = p.split_ctr + static_cast<uint64_t>(it.slot) * p.split_rows + srow;
-        if (leader) ctl->bcast = atomicAdd(ctr, 1u);
-        named_bar_sync(1, kEng);
-        const uint32_t done_before = ctl->bcast;
-        if (done_before + 1 == si.x) {
-          // last chunk: combine every chunk's partial for this row tile
-          __threadfence();
-          const float* base = p.ws + (static_cast<uint64_t>(it.slot) * p.split_chunks + si.y) * blk;
-          float mrun = -INFINITY, mtrue = -INFINITY;
-          for (uint32_t c = 0; c < si.x; ++c) {
-            const float* b = base + c * blk + 128 * D;
-            if (__ldcg(b + 256 + row) > 0.0f) mrun = fmaxf(mrun, __ldcg(b + row));
-            mtrue = fmaxf(mtrue, __ldcg(b + 128 + row));
-          }
-          float ltot = 0.0f;
-          for (uint32_t c = 0; c < si.x; ++c) {
-            const float* b = base + c * blk + 128 * D;
-            const float lc = __ldcg(b + 256 + row);
-            if (lc > 0.0f) ltot += lc * exp2f(__ldcg(b + row) - mrun);
-          }
-          const float inv = ltot > 0.0f ? 1.0f / ltot : 0.0f;
-          named_bar_sync(1, kEng);  // every engine thread has read the count
-          if (leader) *ctr = 0;    // ready for the next launch
-#pragma unroll 1
-          for (uint32_t c32 = 0; c32 < kHalfO / 32; ++c32) {
-            float acc[32];
-#pragma unroll
-            for (uint32_t i = 0; i < 32; ++i) acc[i] = 0.0f;
-            for (uint32_t c = 0; c < si.x; ++c) {
-              const float* b = base + c * blk;
-              const float lc = __ldcg(b + 128 * D + 256 + row);
-              if (!(lc > 0.0f)) continue;
-              const float w = exp2f(__ldcg(b + 128 * D + row) - mrun);
-              const float4* src = reinterpret_cast<const float4*>(b + row * D + half * kHalfO + c32 * 32);
-#pragma unroll
-              for (uint32_t v = 0; v < 8; ++v) {
-                const float4 f = __ldcg(src + v);
-                acc[v * 4 + 0] += w * f.x;
-                acc[v * 4 + 1] += w * f.y;
-                acc[v * 4 + 2] += w * f.z;
-                acc[v * 4 + 3] += w * f.w;
-              }
-            }
-            stage_chunk32(stg_row_of(half * kHalfO + c32 * 32), row, stg_chunk_of(half * kHalfO + c32 * 32), acc, inv);
-          }
-          store_staged(it);
-          write_stats(it, mtrue, mrun, ltot);
-        }
-      }
-      if (tracer) trace_ev<kTrace>(tracing, p, &ctl->trace_count, 24, 0, it.t);
-      pend.valid = false;
     };
 
     for (;;) {
@@ -739,7 +623,6 @@ __global__ void __launch_bounds__(kThreadsOf<D>, 1)
           tmem_st_wait();
           tc_fence_before();
           mbar_arrive(&ctl->p_full[buf]);
-          if (j == 0 && pend.valid) finish(pend);
           continue;
         }
 #endif
@@ -820,23 +703,179 @@ __global__ void __launch_bounds__(kThreadsOf<D>, 1)
         tc_fence_before();
         mbar_arrive(&ctl->p_full[buf]);
         if (tracer) trace_ev<kTrace>(tracing, p, &ctl->trace_count, 22, buf, j);
-        if (j == 0 && pend.valid) finish(pend);  // the previous item's last PV has drained meanwhile
       }
 
-      // ---------------- item end: combine the halves' row sums now; the O readout is deferred
-      ctl->xchg[step & 1][half][row] = l;
-      named_bar_sync(1, kEng);
-      pend.l_unit = l;
-#pragma unroll
-      for (uint32_t o = 1; o < kP; ++o) pend.l_unit += ctl->xchg[step & 1][(half + o) % kP][row];
-      ++step;
-      pend.it = it;
-      pend.m_run = m_run;
-      pend.m_true = m_true;
-      pend.ob = ob;
-      pend.valid = true;
+      // ---------------- item end: hand the row statistics to the epilogue warpgroup, which
+      // combines the parts' row sums, waits for the item's last PV and writes O
+      mbar_wait(&ctl->stats_empty[ob], se_ph[ob]);
+      se_ph.flip(ob);
+      ItemStats<kP>& st = ctl->stats[ob];
+      st.l[half][row] = l;
+      if (half == 0) {
+        st.m_run[row] = m_run;
+        st.m_true[row] = m_true;
+      }
+      if (leader) st.item = it;
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&ctl->stats_full[ob]);
     }
-    if (pend.valid) finish(pend);
+    {  // end marker for the epilogue warpgroup
+      const uint32_t ob = items & 1;
+      mbar_wait(&ctl->stats_empty[ob], se_ph[ob]);
+      if (leader) ctl->stats[ob].item.t = kEnd;
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&ctl->stats_full[ob]);
+    }
+  } else {
+    setmaxnreg_dec<kOtherRegs>();
+    // ------------------------------------------------------------------ epilogue warpgroup
+    // Per item (in O-accumulator order): row statistics from the engine, then the item's last PV
+    // (o_full), then O / l -> bf16 staged in 128B-swizzled shared memory -> TMA store, or, for a
+    // split-KV chunk, the unnormalized partial to the workspace and the last chunk's combine.
+    constexpr uint32_t kEpi = 128;
+    const uint32_t quad = warp & 3;
+    const uint32_t row = quad * 32 + lane;
+    const uint32_t lane_off = (quad * 32) << 16;
+    const bool leader = (quad == 0 && lane == 0);
+    const bool tracer = leader;
+    PhaseBits sf_ph{0u}, o_ph{0u};
+    auto write_stats = [&](const ItemDesc& it, float m_true2, float m_run2, float l_tot) {
+      const uint64_t grow = static_cast<uint64_t>(it.rt) * 128 + row;
+      if (grow < p.n) {
+        const uint64_t si = static_cast<uint64_t>(it.slot) * p.n + grow;
+        if (p.row_max) p.row_max[si] = m_true2 == -INFINITY ? -INFINITY : m_true2 * kLn2;
+        if (p.row_sum) p.row_sum[si] = l_tot > 0.0f ? l_tot * exp2f(m_run2 - m_true2) : 0.0f;
+      }
+    };
+    // TMA-store the staged O tile of item `it` (called by every epilogue thread)
+    auto store_staged = [&](const ItemDesc& it) {
+      fence_proxy_async_smem();
+      named_bar_sync(2, kEpi);
+      if (leader) {
+        tma_store_3d(&tm_o, stage, 0, it.rt * 128, it.slot);
+        if (D == 128) tma_store_3d(&tm_o, stage + C::kStageBytes, 64, it.rt * 128, it.slot);
+        bulk_commit_group();
+      }
+    };
+    // staged output column c goes to box c / 64, 16-byte chunk (c % 64) / 8 of the row
+    auto stg_row_of = [&](uint32_t c) { return stage + (c / 64) * C::kStageBytes + row * 128; };
+    auto stg_chunk_of = [&](uint32_t c) { return (c % 64) / 8; };
+    for (uint32_t ob = 0;; ob ^= 1) {
+      mbar_wait(&ctl->stats_full[ob], sf_ph[ob]);
+      sf_ph.flip(ob);
+      const ItemStats<kParts<D>>& st = ctl->stats[ob];
+      const ItemDesc it = st.item;
+      if (it.t == kEnd) break;
+      float l_unit = 0.0f;
+#pragma unroll
+      for (uint32_t h = 0; h < kParts<D>; ++h) l_unit += st.l[h][row];
+      const float m_run = st.m_run[row], m_true = st.m_true[row];
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&ctl->stats_empty[ob]);
+      const uint32_t to = tmem + C::kOCol + lane_off + ob * D;
+      if (leader) bulk_wait_group_read<0>();  // staging buffers free again
+      mbar_wait(&ctl->o_full[ob], o_ph[ob]);
+      o_ph.flip(ob);
+      tc_fence_after();
+      named_bar_sync(2, kEpi);
+      if (tracer) trace_ev<kTrace>(tracing, p, &ctl->trace_count, 23, 0, it.t);
+      if (it.split == kNoSplit) {
+        const float inv = l_unit > 0.0f ? 1.0f / l_unit : 0.0f;
+#ifdef BBM_ABLATE_NO_EPI  // timing experiments only (tools/ablate.sh): O is never written
+        if (false)
+#endif
+#pragma unroll
+        for (uint32_t c64 = 0; c64 < D / 64; ++c64) {
+          // two 32-column loads in flight per wait
+          uint32_t o[2][32];
+          tmem_ld32(to + c64 * 64, o[0]);
+          tmem_ld32(to + c64 * 64 + 32, o[1]);
+          tmem_ld_wait();
+#pragma unroll
+          for (uint32_t h = 0; h < 2; ++h)
+            stage_chunk32(stg_row_of(c64 * 64 + h * 32), row, stg_chunk_of(c64 * 64 + h * 32),
+                          reinterpret_cast<const float*>(o[h]), inv);
+        }
+        tc_fence_before();
+        mbar_arrive(&ctl->o_empty[ob]);  // the accumulator may be overwritten from here on
+#ifndef BBM_ABLATE_NO_EPI
+        store_staged(it);
+#endif
+        write_stats(it, m_true, m_run, l_unit);
+      } else {
+        // ---- split-KV chunk: publish the unnormalized partial, the last chunk combines
+        const uint32_t srow = it.split >> 8, chunk = it.split & 0xFF;
+        const uint2 si = p.split_info[srow];  // {chunks, first workspace chunk}
+        const uint64_t blk = static_cast<uint64_t>(128) * (D + 3);
+        float* wsb = p.ws + (static_cast<uint64_t>(it.slot) * p.split_chunks + si.y + chunk) * blk;
+#pragma unroll
+        for (uint32_t c32 = 0; c32 < D / 32; ++c32) {
+          uint32_t o[32];
+          tmem_ld32(to + c32 * 32, o);
+          tmem_ld_wait();
+          uint4* dst = reinterpret_cast<uint4*>(wsb + row * D + c32 * 32);
+#pragma unroll
+          for (uint32_t v = 0; v < 8; ++v)
+            dst[v] = make_uint4(o[v * 4], o[v * 4 + 1], o[v * 4 + 2], o[v * 4 + 3]);
+        }
+        tc_fence_before();
+        mbar_arrive(&ctl->o_empty[ob]);
+        wsb[128 * D + row] = m_run;
+        wsb[128 * D + 128 + row] = m_true;
+        wsb[128 * D + 256 + row] = l_unit;
+        __threadfence();
+        named_bar_sync(2, kEpi);
+        uint32_t* ctr = p.split_ctr + static_cast<uint64_t>(it.slot) * p.split_rows + srow;
+        if (leader) ctl->bcast = atomicAdd(ctr, 1u);
+        named_bar_sync(2, kEpi);
+        const uint32_t done_before = ctl->bcast;
+        if (done_before + 1 == si.x) {
+          // last chunk: combine every chunk's partial for this row tile
+          __threadfence();
+          const float* base = p.ws + (static_cast<uint64_t>(it.slot) * p.split_chunks + si.y) * blk;
+          float mrun = -INFINITY, mtrue = -INFINITY;
+          for (uint32_t c = 0; c < si.x; ++c) {
+            const float* b = base + c * blk + 128 * D;
+            if (__ldcg(b + 256 + row) > 0.0f) mrun = fmaxf(mrun, __ldcg(b + row));
+            mtrue = fmaxf(mtrue, __ldcg(b + 128 + row));
+          }
+          float ltot = 0.0f;
+          for (uint32_t c = 0; c < si.x; ++c) {
+            const float* b = base + c * blk + 128 * D;
+            const float lc = __ldcg(b + 256 + row);
+            if (lc > 0.0f) ltot += lc * exp2f(__ldcg(b + row) - mrun);
+          }
+          const float inv = ltot > 0.0f ? 1.0f / ltot : 0.0f;
+          named_bar_sync(2, kEpi);  // every epilogue thread has read the count
+          if (leader) *ctr = 0;    // ready for the next launch
+#pragma unroll 1
+          for (uint32_t c32 = 0; c32 < D / 32; ++c32) {
+            float acc[32];
+#pragma unroll
+            for (uint32_t i = 0; i < 32; ++i) acc[i] = 0.0f;
+            for (uint32_t c = 0; c < si.x; ++c) {
+              const float* b = base + c * blk;
+              const float lc = __ldcg(b + 128 * D + 256 + row);
+              if (!(lc > 0.0f)) continue;
+              const float w = exp2f(__ldcg(b + 128 * D + row) - mrun);
+              const float4* src = reinterpret_cast<const float4*>(b + row * D + c32 * 32);
+#pragma unroll
+              for (uint32_t v = 0; v < 8; ++v) {
+                const float4 f = __ldcg(src + v);
+                acc[v * 4 + 0] += w * f.x;
+                acc[v * 4 + 1] += w * f.y;
+                acc[v * 4 + 2] += w * f.z;
+                acc[v * 4 + 3] += w * f.w;
+              }
+            }
+            stage_chunk32(stg_row_of(c32 * 32), row, stg_chunk_of(c32 * 32), acc, inv);
+          }
+          store_staged(it);
+          write_stats(it, mtrue, mrun, ltot);
+        }
+      }
+      if (tracer) trace_ev<kTrace>(tracing, p, &ctl->trace_count, 24, 0, it.t);
+    }
     if (leader) bulk_wait_group<0>();  // O stores landed
   }
 

@@ -355,6 +355,16 @@ __device__ __forceinline__ void exp2_poly2(float x0, float x1, float& e0, float&
   e1 = __uint_as_float(ph + (th << 23));
 }
 
+// Per-warpgroup register budget (all four warps of the warpgroup execute it).
+template <uint32_t N>
+__device__ __forceinline__ void setmaxnreg_inc() {
+  asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(N));
+}
+template <uint32_t N>
+__device__ __forceinline__ void setmaxnreg_dec() {
+  asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(N));
+}
+
 // Phase bits of a small array of mbarriers in one register: a dynamically indexed uint32_t
 // array would be placed in local memory (an LDL/STL pair on every wait).
 struct PhaseBits {
