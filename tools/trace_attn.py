@@ -100,10 +100,9 @@ def main():
             if code == 20 and (s, 24) in last:
                 per["epilogue done -> next softmax wait"].append(t - last.pop((s, 24)))
         # engine time budget: every cycle between consecutive engine events gets one label
-        eng = [e for e in evs if 20 <= e[1] <= 27]
+        eng = [e for e in evs if e[1] in (20, 21, 22, 25, 26, 27)]  # 23/24: epilogue warpgroup
         lab = {(20, 21): "wait S", (21, 25): "S tmem load", (25, 26): "mask + max + exchange",
-               (26, 27): "exp + P pack", (27, 22): "P store + arrive", (22, 23): "o_full wait + barrier",
-               (23, 24): "epilogue", (24, 20): "after epilogue -> next tile", (22, 20): "tile gap"}
+               (26, 27): "exp + P pack", (27, 22): "P store + arrive", (22, 20): "tile gap"}
         budget = collections.Counter()
         for (ta, ca, _, _), (tb, cb, _, ab) in zip(eng, eng[1:]):
             name = lab.get((ca, cb), f"{ca}->{cb}")
