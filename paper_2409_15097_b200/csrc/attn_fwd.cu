@@ -89,8 +89,11 @@ static_assert(BBM_PARTS128 == 2, "the register split below assumes two engine wa
 // warpgroup 0: producer / MMA issuers / TMEM allocator; 1..kParts: softmax engine; last: epilogue
 template <int D>
 constexpr uint32_t kThreadsOf = 256 + 128 * kParts<D>;
-constexpr uint32_t kEngineRegs = 168;  // setmaxnreg: 2 x 128 x 168 + 2 x 128 x 88 = 65536
-constexpr uint32_t kOtherRegs = 88;
+#ifndef BBM_ENGINE_REGS
+#define BBM_ENGINE_REGS 168
+#endif
+constexpr uint32_t kEngineRegs = BBM_ENGINE_REGS;  // setmaxnreg: 2 x 128 x 168 + 2 x 128 x 88 = 65536
+constexpr uint32_t kOtherRegs = 256 - kEngineRegs;
 constexpr uint32_t kTraceCap = 8192;  // events per traced CTA
 constexpr uint32_t kQueue = 8;        // item queue depth (items open between the producer and the PV issuer)
 
