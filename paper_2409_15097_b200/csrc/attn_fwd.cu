@@ -12,22 +12,25 @@
 // combines them. Items are claimed dynamically (one global atomic per item) in slot-major order,
 // longest units first inside a slot.
 //
-// Structure: one persistent CTA per SM (384 threads), one stream of items (the tile sequence of
-// consecutive items is treated as one sequence k = 0, 1, 2, ...). tcgen05.mma issue is nearly
-// synchronous, so the score accumulator is TRIPLE-BUFFERED in TMEM: S_{k+1} and S_{k+2} are
-// computed while the softmax engine turns S_k into P_k, and the engine never waits on the tensor
-// core in steady state.
+// Structure: one persistent CTA per SM (512 threads = four warpgroups, registers rebalanced with
+// setmaxnreg), one stream of items (the tile sequence of consecutive items is treated as one
+// sequence k = 0, 1, 2, ...). The score accumulator is double-buffered in TMEM, so S_{k+1} is
+// computed while the softmax engine turns S_k into P_k.
 //   warp 0       producer: claims items, publishes them through a shared-memory item queue,
 //                loads Q (double-buffered across items) and K_k, V_k into a K/V ring (TMA,
 //                128B-swizzled 64-column boxes).
 //   warps 1, 3   MMA issuers (one thread each): warp 1 S_k = Q K_k^T (SS, both K-major) into
-//                TMEM buffer k % 3 once PV_{k-3} has completed (S_{k+3} reuses P_k's columns);
+//                TMEM buffer k % 2 once PV_{k-2} has completed (S_{k+2} reuses P_k's columns);
 //                warp 3 O += P_k V_k (TS: P read from TMEM, V MN-major).
-//   warp 2       TMEM allocator (512 columns: S buffers at 0, 128, 256; O at 384).
-//   warps 4-11   softmax engine: warps 4-7 own S columns [0,64) and O columns [0,D/2), warps
-//                8-11 the other halves; the halves exchange their partial row max through shared
-//                memory once per tile. The epilogue stages bf16 O in 128B-swizzled shared memory
-//                for TMA stores.
+//   warp 2       TMEM allocator (512 columns: S buffers at 0 and 128; O accumulators at 256 and
+//                256 + D, alternating between items).
+//   warps 4-11   softmax engine (168 registers): warps 4-7 own S columns [0,64), warps 8-11 the
+//                other half; the halves exchange their partial row max through shared memory
+//                once per tile. At an item's end the engine hands its row statistics to the
+//                epilogue warpgroup through shared memory (ItemStats) and moves on.
+//   warps 12-15  epilogue (88 registers): waits for an item's last PV, writes O / l as bf16
+//                through 128B-swizzled staging and TMA stores (or a split-KV partial) and
+//                releases the accumulator.
 // Numerics: scores are scaled into the log2 domain; the running max is only raised when it grows
 // by more than 2^8 (stale-max trick; exact after the final O/l), P is rounded to bf16 for the
 // MMA and written over S in TMEM, l accumulates in fp32. Partial tiles read 8 B of mask bits per
