@@ -34,6 +34,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstdint>
 #include <numeric>
 #include <vector>
@@ -73,7 +74,26 @@ struct BwdParams {
   uint32_t* ctr;              // [2] next item, finished CTAs
   __nv_bfloat16* out0;        // dq | dk
   __nv_bfloat16* out1;        // -  | dv
+  uint64_t* trace;            // optional event trace (bbm_set_trace), nullptr = off
+  uint32_t trace_ctas;
 };
+
+// Trace event: [63:24] clock64 low 40 bits | [23:16] code | [15] stream (= half) | [14:0] aux.
+// Codes: MMA 40 S/dP of half issued (aux = tile), 41 accumulate of half issued, 42 P/dS of half
+// seen, 43 item start (fixed tiles landed); engine 50 s_full wait begin, 51 s_full wait end,
+// 52 p_full arrive, 53 acc_full wait end, 54 epilogue done, 55 item descriptor read.
+constexpr uint32_t kTraceCap = 8192;
+template <bool kTrace>
+__device__ __forceinline__ void trace_ev(bool on, const BwdParams& p, uint32_t* counter, uint32_t code,
+                                         uint32_t stream, uint32_t aux) {
+  if constexpr (!kTrace) return;
+  if (!on) return;
+  const uint32_t i = atomicAdd(counter, 1u);
+  if (i >= kTraceCap) return;
+  const uint64_t t = static_cast<uint64_t>(clock64()) & ((1ull << 40) - 1);
+  p.trace[static_cast<uint64_t>(blockIdx.x) * kTraceCap + i] =
+      (t << 24) | (static_cast<uint64_t>(code & 0xFF) << 16) | ((stream & 1u) << 15) | (aux & 0x7FFF);
+}
 
 struct ItemDesc {
   uint32_t t, slot, tile, nt;
@@ -97,6 +117,7 @@ struct BwdCtl {
   uint64_t item_full[kQueue], item_empty[kQueue];
   ItemDesc items[kQueue];
   uint32_t tmem_base;
+  uint32_t trace_count;
 };
 
 template <int D, int SIDE>
@@ -131,7 +152,7 @@ __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t b
       : "memory");
 }
 
-template <int D, int SIDE>
+template <int D, int SIDE, bool kTrace>
 __global__ void __launch_bounds__(kThreads, 1)
     attn_bwd_kernel(const __grid_constant__ CUtensorMap tm_f0, const __grid_constant__ CUtensorMap tm_f1,
                     const __grid_constant__ CUtensorMap tm_s0, const __grid_constant__ CUtensorMap tm_s1,
@@ -146,7 +167,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if ((smem_u32(smem) & 1023u) != 0) __trap();
 
+  const bool tracing = kTrace && blockIdx.x < p.trace_ctas;
   if (threadIdx.x == 0) {
+    ctl->trace_count = 0;
     mbar_init(&ctl->fixed_full, 1);
     mbar_init(&ctl->fixed_empty, 1);
     for (int h = 0; h < 2; ++h) {
@@ -280,8 +303,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         fph ^= 1;
         mbar_wait(&ctl->ring_full[r], rph);
         tc_fence_after();
+        trace_ev<kTrace>(tracing, p, &ctl->trace_count, 43, 0, it.t);
         issue_sdp(0, r);
+        trace_ev<kTrace>(tracing, p, &ctl->trace_count, 40, 0, 0);
         issue_sdp(1, r);
+        trace_ev<kTrace>(tracing, p, &ctl->trace_count, 40, 1, 0);
         if (it.nt == 1) tc_commit(&ctl->fixed_empty);
         for (uint32_t j = 0; j < it.nt; ++j) {
           const uint32_t rn = r + 1 == C::kStages ? 0 : r + 1;
@@ -289,12 +315,14 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (uint32_t h = 0; h < 2; ++h) {
             mbar_wait(&ctl->p_full[h], pph[h]);
             pph.flip(h);
+            trace_ev<kTrace>(tracing, p, &ctl->trace_count, 42, h, j);
             if (j == 0 && h == 0) {
               mbar_wait(&ctl->acc_empty, aph);  // previous item's epilogue has read the accumulators
               aph ^= 1;
             }
             tc_fence_after();
             issue_acc(h, r, j);
+            trace_ev<kTrace>(tracing, p, &ctl->trace_count, 41, h, j);
             if (h == 1) tc_commit(&ctl->ring_empty[r]);  // both halves of tile j consumed
             if (j + 1 < it.nt) {
               if (h == 0) {
@@ -302,6 +330,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 tc_fence_after();
               }
               issue_sdp(h, rn);
+              trace_ev<kTrace>(tracing, p, &ctl->trace_count, 40, h, j + 1);
               if (h == 1 && j + 2 == it.nt) tc_commit(&ctl->fixed_empty);
             }
           }
@@ -317,6 +346,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t quad = warp & 3;
     const uint32_t row = quad * 32 + lane;  // TMEM lane: key (dkdv) or query (dq) in the tile
     const uint32_t lane_off = (quad * 32) << 16;
+    const bool tracer = quad == 0 && lane == 0;  // one per half
     const float sl2 = p.sl2;
     uint32_t qi = 0, qiph = 0, sph = 0, acph = 0, r = 0;
     const uint32_t last = (static_cast<uint32_t>(p.n) + 127) / 128 - 1;
@@ -324,6 +354,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (;;) {
       mbar_wait(&ctl->item_full[qi], qiph);
       const ItemDesc it = ctl->items[qi];
+      if (tracer) trace_ev<kTrace>(tracing, p, &ctl->trace_count, 55, half, it.t);
       __syncwarp();  // every lane of this warp has read the descriptor
       if (lane == 0) mbar_arrive(&ctl->item_empty[qi]);
       if (++qi == kQueue) { qi = 0; qiph ^= 1; }
@@ -359,9 +390,11 @@ __global__ void __launch_bounds__(kThreads, 1)
                                 p.bitmaps + (static_cast<uint64_t>(it.tile) * p.list_stride + j) * 128 + row) +
                             half);
           }
+          if (tracer) trace_ev<kTrace>(tracing, p, &ctl->trace_count, 50, half, j);
           mbar_wait(&ctl->s_full[half], sph);
           sph ^= 1;
           tc_fence_after();
+          if (tracer) trace_ev<kTrace>(tracing, p, &ctl->trace_count, 51, half, j);
           const uint32_t ts = tmem + lane_off + half * 64;
           const float* vec = nullptr;
           if constexpr (SIDE == kSideDKDV)
@@ -401,12 +434,14 @@ __global__ void __launch_bounds__(kThreads, 1)
           tmem_st_wait();
           tc_fence_before();
           mbar_arrive(&ctl->p_full[half]);
+          if (tracer) trace_ev<kTrace>(tracing, p, &ctl->trace_count, 52, half, j);
           if (++r == C::kStages) r = 0;
         }
         // epilogue: accumulators -> bf16 rows (dq * scale | dk * scale, dv)
         mbar_wait(&ctl->acc_full, acph);
         acph ^= 1;
         tc_fence_after();
+        if (tracer) trace_ev<kTrace>(tracing, p, &ctl->trace_count, 53, half, it.t);
       }
       constexpr uint32_t kHalf = D / 2;
       const bool in = grow < p.n;
@@ -440,6 +475,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc_fence_before();
         mbar_arrive(&ctl->acc_empty);
       }
+      if (tracer) trace_ev<kTrace>(tracing, p, &ctl->trace_count, 54, half, it.t);
     }
   }
 
@@ -586,14 +622,29 @@ void launch_side(const Prep& prep, const BwdArgs& a, const float* lse2, const fl
   const CUtensorMap tdo = make_tmap_bf16_3d(a.d_out, D, a.n, a.slots, 64, 128);
   static std::atomic<uint64_t> attr_devices{0};
   once_per_device(attr_devices, [] {
-    BBM_CUDA(cudaFuncSetAttribute(attn_bwd_kernel<D, SIDE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    BBM_CUDA(cudaFuncSetAttribute(attn_bwd_kernel<D, SIDE, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  bwd_smem_bytes<D, SIDE>()));
+    BBM_CUDA(cudaFuncSetAttribute(attn_bwd_kernel<D, SIDE, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   bwd_smem_bytes<D, SIDE>()));
   });
   const uint32_t grid = std::min<uint32_t>(p.total_items, static_cast<uint32_t>(num_sms));
-  if (SIDE == kSideDQ)
-    attn_bwd_kernel<D, SIDE><<<grid, kThreads, bwd_smem_bytes<D, SIDE>(), s>>>(tq, tdo, tk, tv, p);
+  // event trace (bbm_set_trace) of one side only, chosen by BBM_TRACE_BWD_SIDE (0 dq, 1 dkdv):
+  // both kernels would otherwise write the same buffer
+  const char* tside = std::getenv("BBM_TRACE_BWD_SIDE");
+  if (g_trace.buffer && tside && std::atoi(tside) == SIDE) {
+    p.trace = static_cast<uint64_t*>(g_trace.buffer);
+    p.trace_ctas = g_trace.ctas;
+  }
+  auto go = [&](auto kernel) {
+    if (SIDE == kSideDQ)
+      kernel<<<grid, kThreads, bwd_smem_bytes<D, SIDE>(), s>>>(tq, tdo, tk, tv, p);
+    else
+      kernel<<<grid, kThreads, bwd_smem_bytes<D, SIDE>(), s>>>(tk, tv, tq, tdo, p);
+  };
+  if (p.trace)
+    go(attn_bwd_kernel<D, SIDE, true>);
   else
-    attn_bwd_kernel<D, SIDE><<<grid, kThreads, bwd_smem_bytes<D, SIDE>(), s>>>(tk, tv, tq, tdo, p);
+    go(attn_bwd_kernel<D, SIDE, false>);
   BBM_CUDA(cudaGetLastError());
 }
 
