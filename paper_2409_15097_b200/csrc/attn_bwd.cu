@@ -107,6 +107,7 @@ struct BCfg {
   static constexpr uint32_t kStageBytes = 2 * kTileBytes + (SIDE == kSideDKDV ? 1024 : 0);
   static constexpr uint32_t kStageAlloc = (kStageBytes + 1023) / 1024 * 1024;
   static constexpr uint32_t kStages = D == 64 ? 4 : 2;
+  static constexpr uint32_t kOutStage = (D / 64) * kBoxBytes;  // epilogue staging: one 128 x D bf16 tile
   static constexpr uint32_t kAcc0 = 256;      // dQ | dK
   static constexpr uint32_t kAcc1 = 256 + D;  // dV
 };
@@ -123,7 +124,7 @@ struct BwdCtl {
 template <int D, int SIDE>
 constexpr uint32_t bwd_smem_bytes() {
   using C = BCfg<D, SIDE>;
-  return 2 * C::kTileBytes + C::kStages * C::kStageAlloc + sizeof(BwdCtl);
+  return 2 * C::kTileBytes + C::kStages * C::kStageAlloc + C::kOutStage + sizeof(BwdCtl);
 }
 
 __device__ __forceinline__ ItemDesc bwd_decode(const BwdParams& p, uint32_t t) {
@@ -156,6 +157,7 @@ template <int D, int SIDE, bool kTrace>
 __global__ void __launch_bounds__(kThreads, 1)
     attn_bwd_kernel(const __grid_constant__ CUtensorMap tm_f0, const __grid_constant__ CUtensorMap tm_f1,
                     const __grid_constant__ CUtensorMap tm_s0, const __grid_constant__ CUtensorMap tm_s1,
+                    const __grid_constant__ CUtensorMap tm_o0, const __grid_constant__ CUtensorMap tm_o1,
                     const BwdParams p) {
   // fixed tiles f0, f1: (Q_i, dO_i) for dq, (K_j, V_j) for dkdv; streamed s0, s1: the partner's
   // (K_j, V_j) for dq, (Q_i, dO_i) for dkdv.
@@ -163,7 +165,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   extern __shared__ __align__(1024) uint8_t smem[];
   uint8_t* fixed = smem;                       // [2][tile]
   uint8_t* ring = smem + 2 * C::kTileBytes;    // [kStages][stage]
-  auto* ctl = reinterpret_cast<BwdCtl*>(ring + C::kStages * C::kStageAlloc);
+  uint8_t* ostage = ring + C::kStages * C::kStageAlloc;  // [D/64][128 x 64 bf16] epilogue staging
+  auto* ctl = reinterpret_cast<BwdCtl*>(ostage + C::kOutStage);
   const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if ((smem_u32(smem) & 1023u) != 0) __trap();
 
@@ -347,6 +350,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t row = quad * 32 + lane;  // TMEM lane: key (dkdv) or query (dq) in the tile
     const uint32_t lane_off = (quad * 32) << 16;
     const bool tracer = quad == 0 && lane == 0;  // one per half
+    const bool leader = warp == 4 && lane == 0;
     const float sl2 = p.sl2;
     uint32_t qi = 0, qiph = 0, sph = 0, acph = 0, r = 0;
     const uint32_t last = (static_cast<uint32_t>(p.n) + 127) / 128 - 1;
@@ -443,13 +447,14 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc_fence_after();
         if (tracer) trace_ev<kTrace>(tracing, p, &ctl->trace_count, 53, half, it.t);
       }
+      // accumulator -> bf16 (x scale for dq / dk) -> 128B-swizzled staging -> TMA store (rows past
+      // n are clipped by the tensor map). Half h stages output columns [D/2 h, D/2 (h+1)).
       constexpr uint32_t kHalf = D / 2;
-      const bool in = grow < p.n;
-      const uint64_t obase = (static_cast<uint64_t>(it.slot) * p.n + grow) * D + half * kHalf;
 #pragma unroll
       for (uint32_t a = 0; a < (SIDE == kSideDKDV ? 2u : 1u); ++a) {
-        __nv_bfloat16* dst = a == 0 ? p.out0 : p.out1;
         const float mul = a == 0 ? p.scale : 1.0f;
+        if (leader) bulk_wait_group_read<0>();  // the previous store has read the staging tile
+        named_bar_sync(1, 256);
 #pragma unroll
         for (uint32_t c32 = 0; c32 < kHalf / 32; ++c32) {
           uint32_t v[32];
@@ -460,15 +465,25 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
             for (uint32_t i = 0; i < 32; ++i) v[i] = 0u;
           }
-          if (in) {
-            uint4* o = reinterpret_cast<uint4*>(dst + obase + c32 * 32);
+          const uint32_t col = half * kHalf + c32 * 32;  // output column of v[0]
+          uint8_t* rowp = ostage + (col / 64) * kBoxBytes + row * 128;
 #pragma unroll
-            for (uint32_t w = 0; w < 4; ++w)
-              o[w] = make_uint4(pack_bf16x2(__uint_as_float(v[w * 8 + 0]) * mul, __uint_as_float(v[w * 8 + 1]) * mul),
-                                pack_bf16x2(__uint_as_float(v[w * 8 + 2]) * mul, __uint_as_float(v[w * 8 + 3]) * mul),
-                                pack_bf16x2(__uint_as_float(v[w * 8 + 4]) * mul, __uint_as_float(v[w * 8 + 5]) * mul),
-                                pack_bf16x2(__uint_as_float(v[w * 8 + 6]) * mul, __uint_as_float(v[w * 8 + 7]) * mul));
+          for (uint32_t c = 0; c < 4; ++c) {
+            uint4 w;
+            w.x = pack_bf16x2(__uint_as_float(v[c * 8 + 0]) * mul, __uint_as_float(v[c * 8 + 1]) * mul);
+            w.y = pack_bf16x2(__uint_as_float(v[c * 8 + 2]) * mul, __uint_as_float(v[c * 8 + 3]) * mul);
+            w.z = pack_bf16x2(__uint_as_float(v[c * 8 + 4]) * mul, __uint_as_float(v[c * 8 + 5]) * mul);
+            w.w = pack_bf16x2(__uint_as_float(v[c * 8 + 6]) * mul, __uint_as_float(v[c * 8 + 7]) * mul);
+            *reinterpret_cast<uint4*>(rowp + ((((col % 64) / 8 + c) ^ (row & 7)) << 4)) = w;
           }
+        }
+        fence_proxy_async_smem();
+        named_bar_sync(1, 256);
+        if (leader) {
+#pragma unroll
+          for (uint32_t b = 0; b < D / 64; ++b)
+            tma_store_3d(a == 0 ? &tm_o0 : &tm_o1, ostage + b * kBoxBytes, b * 64, it.tile * 128, it.slot);
+          bulk_commit_group();
         }
       }
       if (it.nt > 0) {
@@ -477,6 +492,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       if (tracer) trace_ev<kTrace>(tracing, p, &ctl->trace_count, 54, half, it.t);
     }
+    if (leader) bulk_wait_group<0>();  // gradient stores landed
   }
 
   tc_fence_before();
@@ -620,6 +636,8 @@ void launch_side(const Prep& prep, const BwdArgs& a, const float* lse2, const fl
   const CUtensorMap tk = make_tmap_bf16_3d(a.k, D, a.n, a.slots, 64, 128);
   const CUtensorMap tv = make_tmap_bf16_3d(a.v, D, a.n, a.slots, 64, 128);
   const CUtensorMap tdo = make_tmap_bf16_3d(a.d_out, D, a.n, a.slots, 64, 128);
+  const CUtensorMap to0 = make_tmap_bf16_3d(p.out0, D, a.n, a.slots, 64, 128);
+  const CUtensorMap to1 = SIDE == kSideDKDV ? make_tmap_bf16_3d(p.out1, D, a.n, a.slots, 64, 128) : to0;
   static std::atomic<uint64_t> attr_devices{0};
   once_per_device(attr_devices, [] {
     BBM_CUDA(cudaFuncSetAttribute(attn_bwd_kernel<D, SIDE, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -637,9 +655,9 @@ void launch_side(const Prep& prep, const BwdArgs& a, const float* lse2, const fl
   }
   auto go = [&](auto kernel) {
     if (SIDE == kSideDQ)
-      kernel<<<grid, kThreads, bwd_smem_bytes<D, SIDE>(), s>>>(tq, tdo, tk, tv, p);
+      kernel<<<grid, kThreads, bwd_smem_bytes<D, SIDE>(), s>>>(tq, tdo, tk, tv, to0, to1, p);
     else
-      kernel<<<grid, kThreads, bwd_smem_bytes<D, SIDE>(), s>>>(tk, tv, tq, tdo, p);
+      kernel<<<grid, kThreads, bwd_smem_bytes<D, SIDE>(), s>>>(tk, tv, tq, tdo, to0, to1, p);
   };
   if (p.trace)
     go(attn_bwd_kernel<D, SIDE, true>);
