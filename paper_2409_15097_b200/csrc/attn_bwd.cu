@@ -23,8 +23,11 @@
 //               and streams the partner tiles (Q_i, dO_i | K_j, V_j) through a ring (TMA, 128B
 //               swizzle); for dkdv the partner's lse2 / delta vectors ride along (bulk copy).
 //   warp 1      MMA issuer (one thread).
-//   warp 2      TMEM allocator: S at [0,128), dP at [128,256), accumulators at 256 (+D).
-//   warps 4-11  elementwise engine: warp w owns TMEM lanes 32*(w%4).. and column half w/8.
+//   warp 2      TMEM allocator: S at [0,128), dP at [128,256), accumulators at 256 (+D); when a
+//               second accumulator set fits (dq; dkdv at d=64) items alternate between the two
+//               sets and an item's epilogue is deferred until the next item's first tile.
+//   warps 4-11  elementwise engine: warp w owns TMEM lanes 32*(w%4).. and column half w/8;
+//               epilogue: accumulators -> bf16 -> 128B-swizzled staging -> TMA store.
 //               P and dS are written back as packed bf16 into their own half's columns
 //               ([64h, 64h+32) of S / dP), which the TS MMAs read as the A operand.
 // Mask bits: partial tiles only (full tiles skip them), 8 B per row and half from tile-major
@@ -110,10 +113,14 @@ struct BCfg {
   static constexpr uint32_t kOutStage = (D / 64) * kBoxBytes;  // epilogue staging: one 128 x D bf16 tile
   static constexpr uint32_t kAcc0 = 256;      // dQ | dK
   static constexpr uint32_t kAcc1 = 256 + D;  // dV
+  // Two accumulator sets when TMEM has room (dq; dkdv at d=64): items alternate between them and
+  // an item's epilogue is deferred until the next item's first tile is with the tensor core.
+  static constexpr uint32_t kAccSet = SIDE == kSideDQ ? D : 2 * D;  // columns per set
+  static constexpr bool kDefer = 256 + 2 * kAccSet <= 512;
 };
 
 struct BwdCtl {
-  uint64_t fixed_full, fixed_empty, s_full[2], p_full[2], acc_full, acc_empty;
+  uint64_t fixed_full, fixed_empty, s_full[2], p_full[2], acc_full[2], acc_empty[2];
   uint64_t ring_full[4], ring_empty[4];
   uint64_t item_full[kQueue], item_empty[kQueue];
   ItemDesc items[kQueue];
@@ -179,8 +186,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&ctl->s_full[h], 1);
       mbar_init(&ctl->p_full[h], 128);  // the four softmax warps of half h
     }
-    mbar_init(&ctl->acc_full, 1);
-    mbar_init(&ctl->acc_empty, 256);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&ctl->acc_full[b], 1);
+      mbar_init(&ctl->acc_empty[b], 256);
+    }
     for (uint32_t r = 0; r < C::kStages; ++r) {
       mbar_init(&ctl->ring_full[r], 1);
       mbar_init(&ctl->ring_empty[r], 1);
@@ -260,7 +269,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       constexpr uint32_t idesc_acc = make_idesc_bf16(128, D, false, true);
       const uint32_t faddr = smem_u32(fixed), raddr = smem_u32(ring);
       const uint64_t f0 = make_sdesc_sw128(faddr, 16, 1024), f1 = make_sdesc_sw128(faddr + C::kTileBytes, 16, 1024);
-      uint32_t qi = 0, qiph = 0, r = 0, rph = 0, fph = 0, aph = 1;
+      uint32_t qi = 0, qiph = 0, r = 0, rph = 0, fph = 0, items = 0;
+      PhaseBits aph{0x3u};  // acc_empty phases (both sets start free)
       PhaseBits pph{0u};
       // S_h = f0 s0[64h..]^T, dP_h = f1 s1[64h..]^T: both K-major, K = D, N = 64 partner rows
       auto issue_sdp = [&](uint32_t h, uint32_t stage) {
@@ -280,7 +290,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       };
       // accumulate MMAs of half h: K steps 4h..4h+3 (partner rows 64h..64h+63). Packed bf16 A
       // operand: half h's 32 columns at [64h, 64h+32) of its region -> column (kk/4)*64 + (kk%4)*8
-      auto issue_acc = [&](uint32_t h, uint32_t stage, uint32_t j) {
+      auto issue_acc = [&](uint32_t h, uint32_t stage, uint32_t j, uint32_t acc0) {
         const uint32_t sbase = raddr + stage * C::kStageAlloc;
         const uint64_t b0 = make_sdesc_sw128(sbase, kBoxBytes, 1024);
         const uint64_t b1 = make_sdesc_sw128(sbase + C::kTileBytes, kBoxBytes, 1024);
@@ -290,9 +300,9 @@ __global__ void __launch_bounds__(kThreads, 1)
           const uint32_t acol = (kk / 4) * 64 + (kk % 4) * 8;
           const uint32_t acc = (j > 0 || kk > 0) ? 1u : 0u;
           // dQ += dS K_j  |  dK += dS^T Q_i   (B = streamed tile 0, MN-major)
-          umma_ts(tmem + C::kAcc0, tmem + 128 + acol, sdesc_advance(b0, kk * 2048), idesc_acc, acc);
+          umma_ts(tmem + acc0, tmem + 128 + acol, sdesc_advance(b0, kk * 2048), idesc_acc, acc);
           if constexpr (SIDE == kSideDKDV)  // dV += P^T dO_i   (B = streamed tile 1)
-            umma_ts(tmem + C::kAcc1, tmem + acol, sdesc_advance(b1, kk * 2048), idesc_acc, acc);
+            umma_ts(tmem + acc0 + D, tmem + acol, sdesc_advance(b1, kk * 2048), idesc_acc, acc);
         }
       };
       for (;;) {
@@ -312,6 +322,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         issue_sdp(1, r);
         trace_ev<kTrace>(tracing, p, &ctl->trace_count, 40, 1, 0);
         if (it.nt == 1) tc_commit(&ctl->fixed_empty);
+        const uint32_t ab = C::kDefer ? (items++ & 1u) : 0u;  // this item's accumulator set
+        const uint32_t acc0 = C::kAcc0 + ab * C::kAccSet;
         for (uint32_t j = 0; j < it.nt; ++j) {
           const uint32_t rn = r + 1 == C::kStages ? 0 : r + 1;
           const uint32_t rnph = r + 1 == C::kStages ? rph ^ 1 : rph;
@@ -320,11 +332,11 @@ __global__ void __launch_bounds__(kThreads, 1)
             pph.flip(h);
             trace_ev<kTrace>(tracing, p, &ctl->trace_count, 42, h, j);
             if (j == 0 && h == 0) {
-              mbar_wait(&ctl->acc_empty, aph);  // previous item's epilogue has read the accumulators
-              aph ^= 1;
+              mbar_wait(&ctl->acc_empty[ab], aph[ab]);  // this set's last epilogue has read it
+              aph.flip(ab);
             }
             tc_fence_after();
-            issue_acc(h, r, j);
+            issue_acc(h, r, j, acc0);
             trace_ev<kTrace>(tracing, p, &ctl->trace_count, 41, h, j);
             if (h == 1) tc_commit(&ctl->ring_empty[r]);  // both halves of tile j consumed
             if (j + 1 < it.nt) {
@@ -340,7 +352,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           r = rn;
           rph = rnph;
         }
-        tc_commit(&ctl->acc_full);
+        tc_commit(&ctl->acc_full[ab]);
       }
     }
   } else if (warp >= 4) {
@@ -352,9 +364,73 @@ __global__ void __launch_bounds__(kThreads, 1)
     const bool tracer = quad == 0 && lane == 0;  // one per half
     const bool leader = warp == 4 && lane == 0;
     const float sl2 = p.sl2;
-    uint32_t qi = 0, qiph = 0, sph = 0, acph = 0, r = 0;
+    uint32_t qi = 0, qiph = 0, sph = 0, r = 0;
     const uint32_t last = (static_cast<uint32_t>(p.n) + 127) / 128 - 1;
     const int valid_last = static_cast<int>(p.n - static_cast<uint64_t>(last) * 128) - static_cast<int>(half * 64);
+    // Epilogue of item `it` (accumulator set ab; has_acc = false writes zero rows for an item
+    // without partners): waits for the item's last accumulate MMAs, then accumulator -> bf16 ->
+    // staging -> TMA store and releases the set. Called by all 256 engine threads together.
+    PhaseBits afph{0u};
+    auto finish = [&](const ItemDesc& it, uint32_t ab, bool has_acc) {
+      const uint32_t acc0 = C::kAcc0 + ab * C::kAccSet;
+      if (has_acc) {
+        mbar_wait(&ctl->acc_full[ab], afph[ab]);
+        afph.flip(ab);
+        tc_fence_after();
+        if (tracer) trace_ev<kTrace>(tracing, p, &ctl->trace_count, 53, half, it.t);
+      }
+      // accumulator -> bf16 (x scale for dq / dk) -> 128B-swizzled staging -> TMA store (rows past
+      // n are clipped by the tensor map). Half h stages output columns [D/2 h, D/2 (h+1)).
+      constexpr uint32_t kHalf = D / 2;
+#pragma unroll
+      for (uint32_t a = 0; a < (SIDE == kSideDKDV ? 2u : 1u); ++a) {
+        const float mul = a == 0 ? p.scale : 1.0f;
+        if (leader) bulk_wait_group_read<0>();  // the previous store has read the staging tile
+        named_bar_sync(1, 256);
+#pragma unroll
+        for (uint32_t c32 = 0; c32 < kHalf / 32; ++c32) {
+          uint32_t v[32];
+          if (has_acc) {
+            tmem_ld32(tmem + lane_off + acc0 + a * D + half * kHalf + c32 * 32, v);
+            tmem_ld_wait();
+          } else {
+#pragma unroll
+            for (uint32_t i = 0; i < 32; ++i) v[i] = 0u;
+          }
+          const uint32_t col = half * kHalf + c32 * 32;  // output column of v[0]
+          uint8_t* rowp = ostage + (col / 64) * kBoxBytes + row * 128;
+#pragma unroll
+          for (uint32_t c = 0; c < 4; ++c) {
+            uint4 w;
+            w.x = pack_bf16x2(__uint_as_float(v[c * 8 + 0]) * mul, __uint_as_float(v[c * 8 + 1]) * mul);
+            w.y = pack_bf16x2(__uint_as_float(v[c * 8 + 2]) * mul, __uint_as_float(v[c * 8 + 3]) * mul);
+            w.z = pack_bf16x2(__uint_as_float(v[c * 8 + 4]) * mul, __uint_as_float(v[c * 8 + 5]) * mul);
+            w.w = pack_bf16x2(__uint_as_float(v[c * 8 + 6]) * mul, __uint_as_float(v[c * 8 + 7]) * mul);
+            *reinterpret_cast<uint4*>(rowp + ((((col % 64) / 8 + c) ^ (row & 7)) << 4)) = w;
+          }
+        }
+        fence_proxy_async_smem();
+        named_bar_sync(1, 256);
+        if (leader) {
+#pragma unroll
+          for (uint32_t b = 0; b < D / 64; ++b)
+            tma_store_3d(a == 0 ? &tm_o0 : &tm_o1, ostage + b * kBoxBytes, b * 64, it.tile * 128, it.slot);
+          bulk_commit_group();
+        }
+      }
+      if (has_acc) {
+        tc_fence_before();
+        mbar_arrive(&ctl->acc_empty[ab]);
+      }
+      if (tracer) trace_ev<kTrace>(tracing, p, &ctl->trace_count, 54, half, it.t);
+    };
+    struct Pending {
+      ItemDesc it;
+      uint32_t ab;
+      bool valid;
+    };
+    Pending pend{};
+    uint32_t items = 0;
     for (;;) {
       mbar_wait(&ctl->item_full[qi], qiph);
       const ItemDesc it = ctl->items[qi];
@@ -373,6 +449,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           my_nd = f2_pack(nd, nd);
         }
         const uint64_t sl2x2 = f2_pack(sl2, sl2);
+        const uint32_t ab = C::kDefer ? (items++ & 1u) : 0u;  // same sequence as the MMA issuer
         for (uint32_t j = 0; j < it.nt; ++j) {
           const uint32_t e = bwd_entry(p, it.tile, j);
           const uint32_t u = e & 0x7FFFFFFFu;
@@ -440,58 +517,22 @@ __global__ void __launch_bounds__(kThreads, 1)
           mbar_arrive(&ctl->p_full[half]);
           if (tracer) trace_ev<kTrace>(tracing, p, &ctl->trace_count, 52, half, j);
           if (++r == C::kStages) r = 0;
-        }
-        // epilogue: accumulators -> bf16 rows (dq * scale | dk * scale, dv)
-        mbar_wait(&ctl->acc_full, acph);
-        acph ^= 1;
-        tc_fence_after();
-        if (tracer) trace_ev<kTrace>(tracing, p, &ctl->trace_count, 53, half, it.t);
-      }
-      // accumulator -> bf16 (x scale for dq / dk) -> 128B-swizzled staging -> TMA store (rows past
-      // n are clipped by the tensor map). Half h stages output columns [D/2 h, D/2 (h+1)).
-      constexpr uint32_t kHalf = D / 2;
-#pragma unroll
-      for (uint32_t a = 0; a < (SIDE == kSideDKDV ? 2u : 1u); ++a) {
-        const float mul = a == 0 ? p.scale : 1.0f;
-        if (leader) bulk_wait_group_read<0>();  // the previous store has read the staging tile
-        named_bar_sync(1, 256);
-#pragma unroll
-        for (uint32_t c32 = 0; c32 < kHalf / 32; ++c32) {
-          uint32_t v[32];
-          if (it.nt > 0) {
-            tmem_ld32(tmem + lane_off + (a == 0 ? C::kAcc0 : C::kAcc1) + half * kHalf + c32 * 32, v);
-            tmem_ld_wait();
-          } else {
-#pragma unroll
-            for (uint32_t i = 0; i < 32; ++i) v[i] = 0u;
-          }
-          const uint32_t col = half * kHalf + c32 * 32;  // output column of v[0]
-          uint8_t* rowp = ostage + (col / 64) * kBoxBytes + row * 128;
-#pragma unroll
-          for (uint32_t c = 0; c < 4; ++c) {
-            uint4 w;
-            w.x = pack_bf16x2(__uint_as_float(v[c * 8 + 0]) * mul, __uint_as_float(v[c * 8 + 1]) * mul);
-            w.y = pack_bf16x2(__uint_as_float(v[c * 8 + 2]) * mul, __uint_as_float(v[c * 8 + 3]) * mul);
-            w.z = pack_bf16x2(__uint_as_float(v[c * 8 + 4]) * mul, __uint_as_float(v[c * 8 + 5]) * mul);
-            w.w = pack_bf16x2(__uint_as_float(v[c * 8 + 6]) * mul, __uint_as_float(v[c * 8 + 7]) * mul);
-            *reinterpret_cast<uint4*>(rowp + ((((col % 64) / 8 + c) ^ (row & 7)) << 4)) = w;
+          if (C::kDefer && j == 0 && pend.valid) {  // the previous item's accumulate MMAs drained meanwhile
+            finish(pend.it, pend.ab, true);
+            pend.valid = false;
           }
         }
-        fence_proxy_async_smem();
-        named_bar_sync(1, 256);
-        if (leader) {
-#pragma unroll
-          for (uint32_t b = 0; b < D / 64; ++b)
-            tma_store_3d(a == 0 ? &tm_o0 : &tm_o1, ostage + b * kBoxBytes, b * 64, it.tile * 128, it.slot);
-          bulk_commit_group();
+        if constexpr (C::kDefer) {
+          pend = Pending{it, ab, true};  // written after the next item's first tile
+        } else {
+          finish(it, 0, true);
         }
-      }
-      if (it.nt > 0) {
-        tc_fence_before();
-        mbar_arrive(&ctl->acc_empty);
+      } else {
+        finish(it, 0, false);  // no partner: zero rows
       }
       if (tracer) trace_ev<kTrace>(tracing, p, &ctl->trace_count, 54, half, it.t);
     }
+    if (pend.valid) finish(pend.it, pend.ab, true);
     if (leader) bulk_wait_group<0>();  // gradient stores landed
   }
 
