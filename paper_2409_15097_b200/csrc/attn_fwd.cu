@@ -104,7 +104,8 @@ constexpr uint32_t kQueue = 8;        // item queue depth (items open between th
 // Codes: producer 1 Q issued (aux = item), 2 K_k issued, 3 V_k issued;
 //        MMA 10 S_k issued, 11 PV_k issued, 12 V_k landed, 13 K_k landed, 14 P_k seen;
 //        softmax 20 s_full wait begin, 21 s_full wait end, 22 p_full arrive, 23 o_full wait end,
-//        24 epilogue done, 25 S in registers, 26 row max exchanged, 27 P computed.
+//        24 epilogue done, 25 S in registers, 26 row max exchanged, 27 P computed,
+//        28 item statistics handed over, 29 next item's descriptor read.
 template <bool kTrace>
 __device__ __forceinline__ void trace_ev(bool on, const FwdParams& p, uint32_t* counter,
                                          uint32_t code, uint32_t stream, uint32_t aux) {
@@ -575,6 +576,7 @@ __global__ void __launch_bounds__(kThreadsOf<D>, 1)
         zero_item(it);
         continue;
       }
+      if (tracer) trace_ev<kTrace>(tracing, p, &ctl->trace_count, 29, 0, it.t);
       float m_run = -INFINITY, m_true = -INFINITY, l = 0.0f;
       const uint32_t ob = items++ & 1;  // this item's O accumulator (same sequence as the PV issuer)
       const uint32_t to = to_base + ob * D;
@@ -724,6 +726,7 @@ __global__ void __launch_bounds__(kThreadsOf<D>, 1)
       if (leader) st.item = it;
       __syncwarp();
       if (lane == 0) mbar_arrive(&ctl->stats_full[ob]);
+      if (tracer) trace_ev<kTrace>(tracing, p, &ctl->trace_count, 28, 0, it.t);
     }
     {  // end marker for the epilogue warpgroup
       const uint32_t ob = items & 1;

@@ -18,7 +18,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
 NAMES = {1: "P:Q", 2: "P:K", 3: "P:V", 10: "M:S", 11: "M:PV", 12: "M:Vready", 13: "M:Kready", 14: "M:Pseen", 25: "X:sregs", 26: "X:maxed", 27: "X:pcomp", 20: "X:swait", 21: "X:sready",
-         22: "X:pready", 23: "X:oready", 24: "X:epi_done"}
+         22: "X:pready", 23: "X:oready", 24: "X:epi_done", 28: "X:stats", 29: "X:item"}
 
 
 def main():
@@ -100,9 +100,11 @@ def main():
             if code == 20 and (s, 24) in last:
                 per["epilogue done -> next softmax wait"].append(t - last.pop((s, 24)))
         # engine time budget: every cycle between consecutive engine events gets one label
-        eng = [e for e in evs if e[1] in (20, 21, 22, 25, 26, 27)]  # 23/24: epilogue warpgroup
+        eng = [e for e in evs if e[1] in (20, 21, 22, 25, 26, 27, 28, 29)]  # 23/24: epilogue warpgroup
         lab = {(20, 21): "wait S", (21, 25): "S tmem load", (25, 26): "mask + max + exchange",
-               (26, 27): "exp + P pack", (27, 22): "P store + arrive", (22, 20): "tile gap"}
+               (26, 27): "exp + P pack", (27, 22): "P store + arrive", (22, 20): "tile gap",
+               (22, 28): "item end: stats hand-over", (28, 29): "next item descriptor",
+               (29, 20): "item start: first mask bits etc."}
         budget = collections.Counter()
         for (ta, ca, _, _), (tb, cb, _, ab) in zip(eng, eng[1:]):
             name = lab.get((ca, cb), f"{ca}->{cb}")
