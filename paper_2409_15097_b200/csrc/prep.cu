@@ -25,13 +25,18 @@
 namespace bbm {
 namespace {
 
-__device__ __forceinline__ uint32_t bytes_to_bits4(uint32_t w) {
-  // 4 bytes (any nonzero = true) -> 4 bits, byte k -> bit k.
+// 8 bytes that are each 0 or 1 (lo = bytes 0..3, hi = bytes 4..7) -> 8 bits, byte k -> bit k:
+// byte i of lo + (hi << 4) is b_i + 16 b_{i+4}; the multiply gathers sum_i (b_i + 16 b_{i+4}) 2^i
+// into the top byte, and no partial-product byte exceeds 255, so nothing carries across.
+__device__ __forceinline__ uint32_t bits8_of_01(uint32_t lo, uint32_t hi) {
+  return ((lo + (hi << 4)) * 0x01020408u) >> 24;
+}
+// any nonzero byte -> 1 (the slow path of bool inputs that hold other values than 0 / 1)
+__device__ __forceinline__ uint32_t to01(uint32_t w) {
   w |= w >> 4;
   w |= w >> 2;
   w |= w >> 1;
-  w &= 0x01010101u;
-  return (w * 0x01020408u) >> 24;  // distinct partial products: no carries
+  return w & 0x01010101u;
 }
 
 // grid (ceil(kcols/32), krows), 256 threads. Warp w owns column tiles 4*w .. 4*w+3 of the chunk
@@ -51,16 +56,22 @@ __global__ void __launch_bounds__(256) pack_bool_sums128_kernel(
     const uint64_t row = static_cast<uint64_t>(p) * 128 + r;
     uint32_t bits16 = 0;
     if (col_ok && row < n) {
-      const uint4 v = __ldg(reinterpret_cast<const uint4*>(mask + row * stride + col0));
-      bits16 = bytes_to_bits4(v.x) | (bytes_to_bits4(v.y) << 4) | (bytes_to_bits4(v.z) << 8) |
-               (bytes_to_bits4(v.w) << 12);
+      uint4 v = __ldg(reinterpret_cast<const uint4*>(mask + row * stride + col0));
+      if ((v.x | v.y | v.z | v.w) & 0xFEFEFEFEu) {  // bytes other than 0 / 1: nonzero = true
+        v.x = to01(v.x);
+        v.y = to01(v.y);
+        v.z = to01(v.z);
+        v.w = to01(v.w);
+      }
+      bits16 = bits8_of_01(v.x, v.y) | (bits8_of_01(v.z, v.w) << 8);
     }
     count += __popc(bits16);
-    uint64_t part = static_cast<uint64_t>(bits16) << (16 * (lane & 3));
-    part |= __shfl_xor_sync(0xffffffffu, part, 1);
-    part |= __shfl_xor_sync(0xffffffffu, part, 2);
+    // lanes 4m..4m+3 hold the four 16-bit quarters of one 64-bit word
+    const uint32_t pair = bits16 | (__shfl_xor_sync(0xffffffffu, bits16, 1) << 16);
+    const uint32_t other = __shfl_xor_sync(0xffffffffu, pair, 2);
     if ((lane & 3) == 0 && q < kcols)
-      out[row * wpr + static_cast<uint64_t>(q) * 2 + ((lane >> 2) & 1)] = part;
+      out[row * wpr + static_cast<uint64_t>(q) * 2 + ((lane >> 2) & 1)] =
+          static_cast<uint64_t>(pair) | (static_cast<uint64_t>(other) << 32);
   }
   count += __shfl_xor_sync(0xffffffffu, count, 1);
   count += __shfl_xor_sync(0xffffffffu, count, 2);

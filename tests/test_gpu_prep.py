@@ -129,3 +129,33 @@ def test_counters_match_reference_golden(cuda):
         assert got == want, (n, bi, bj, var)
         c3 = prep.counters(bbm.Variant(var), 3)
         assert c3.blocks_visited == 3 * want[0]
+
+
+@pytest.mark.parametrize("n", [4096, 1000])
+def test_uint8_mask_any_nonzero_is_true(cuda, n):
+    """A uint8 mask holding arbitrary nonzero values (not just 0 / 1) means the same as its 0 / 1
+    version: identical metadata and bitwise identical attention output (the fast pack path
+    normalizes 16-byte chunks that contain values > 1)."""
+    import torch
+
+    m = bbm.gen_random_sparse(n, 0.05, 4)
+    ones = torch.from_numpy(m.to_dense()).to(cuda)
+    g = torch.Generator(device=cuda).manual_seed(1)
+    vals = torch.randint(1, 256, (n, n), generator=g, device=cuda, dtype=torch.uint8)
+    # half the rows keep plain 0 / 1 bytes, so both pack paths meet in one launch
+    vals[::2] = 1
+    wild = torch.where(ones, vals, torch.zeros_like(vals))
+    a = bbm.preprocess_mask(ones, bbm.BlockSpec(128, 128))
+    b = bbm.preprocess_mask(wild, bbm.BlockSpec(128, 128))
+    assert np.array_equal(a.sums.values, b.sums.values) and a.runs == b.runs and a.stats == b.stats
+    ca, la, _ = a.kernel_lists()
+    cb, lb, _ = b.kernel_lists()
+    assert np.array_equal(ca, cb)
+    q, k, v = ((torch.rand((2, n, 64), generator=g, device=cuda) * 2 - 1).to(torch.bfloat16) for _ in range(3))
+    outs = []
+    for prep in (a, b):
+        o = torch.empty_like(q)
+        bbm.attn_fwd_device(prep, bbm.Variant.binblk, q, k, v, o, None, None, 0.125)
+        outs.append(o)
+    torch.cuda.synchronize()
+    assert torch.equal(outs[0], outs[1])
