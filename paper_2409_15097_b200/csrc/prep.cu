@@ -51,27 +51,35 @@ __global__ void __launch_bounds__(256) pack_bool_sums128_kernel(
   const bool col_ok = q < kcols && col0 < n;  // n % 16 == 0 on this path
   const uint64_t wpr = static_cast<uint64_t>(kcols) * 2;
   uint32_t count = 0;
-#pragma unroll 4
-  for (uint32_t r = 0; r < 128; ++r) {
-    const uint64_t row = static_cast<uint64_t>(p) * 128 + r;
-    uint32_t bits16 = 0;
-    if (col_ok && row < n) {
-      uint4 v = __ldg(reinterpret_cast<const uint4*>(mask + row * stride + col0));
+  // rows in batches of kBatch: all loads of a batch are in flight before the first is used
+  constexpr uint32_t kBatch = 8;
+  for (uint32_t r0 = 0; r0 < 128; r0 += kBatch) {
+    uint4 vb[kBatch];
+#pragma unroll
+    for (uint32_t b = 0; b < kBatch; ++b) {
+      const uint64_t row = static_cast<uint64_t>(p) * 128 + r0 + b;
+      vb[b] = (col_ok && row < n) ? __ldg(reinterpret_cast<const uint4*>(mask + row * stride + col0))
+                                  : make_uint4(0, 0, 0, 0);
+    }
+#pragma unroll
+    for (uint32_t b = 0; b < kBatch; ++b) {
+      const uint64_t row = static_cast<uint64_t>(p) * 128 + r0 + b;
+      uint4 v = vb[b];
       if ((v.x | v.y | v.z | v.w) & 0xFEFEFEFEu) {  // bytes other than 0 / 1: nonzero = true
         v.x = to01(v.x);
         v.y = to01(v.y);
         v.z = to01(v.z);
         v.w = to01(v.w);
       }
-      bits16 = bits8_of_01(v.x, v.y) | (bits8_of_01(v.z, v.w) << 8);
+      const uint32_t bits16 = bits8_of_01(v.x, v.y) | (bits8_of_01(v.z, v.w) << 8);
+      count += __popc(bits16);
+      // lanes 4m..4m+3 hold the four 16-bit quarters of one 64-bit word
+      const uint32_t pair = bits16 | (__shfl_xor_sync(0xffffffffu, bits16, 1) << 16);
+      const uint32_t other = __shfl_xor_sync(0xffffffffu, pair, 2);
+      if ((lane & 3) == 0 && q < kcols)
+        out[row * wpr + static_cast<uint64_t>(q) * 2 + ((lane >> 2) & 1)] =
+            static_cast<uint64_t>(pair) | (static_cast<uint64_t>(other) << 32);
     }
-    count += __popc(bits16);
-    // lanes 4m..4m+3 hold the four 16-bit quarters of one 64-bit word
-    const uint32_t pair = bits16 | (__shfl_xor_sync(0xffffffffu, bits16, 1) << 16);
-    const uint32_t other = __shfl_xor_sync(0xffffffffu, pair, 2);
-    if ((lane & 3) == 0 && q < kcols)
-      out[row * wpr + static_cast<uint64_t>(q) * 2 + ((lane >> 2) & 1)] =
-          static_cast<uint64_t>(pair) | (static_cast<uint64_t>(other) << 32);
   }
   count += __shfl_xor_sync(0xffffffffu, count, 1);
   count += __shfl_xor_sync(0xffffffffu, count, 2);
