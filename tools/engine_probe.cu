@@ -1,0 +1,172 @@
+// engine_probe.cu — softmax-engine throughput by work organisation (measurement tool, no MMAs).
+//
+// Both layouts run the forward kernel's per-tile math on scores resident in TMEM (scale/shift
+// FFMA2, 6/16 polynomial exp2 pairs, FADD2 row sums, bf16 packing, P written back with tcgen05.st),
+// 8 engine warps per CTA, one CTA per SM:
+//   A "halves": two warps per TMEM lane quadrant split each row's 128 columns (64 each), exchange
+//      the partial row max through shared memory and a named barrier every tile, and all 8 warps
+//      work on the same tile (the current kernel).
+//   B "rows":  one thread per row owns all 128 columns (two passes over TMEM: max, then exp); warps
+//      4-7 and 8-11 are two independent streams on different S buffers, with no barrier between
+//      them (FA4's two-softmax-warpgroup layout).
+// Output: cycles per 128x128 tile (all tiles of both streams / elapsed).
+#include <cstdio>
+
+#include "../paper_2409_15097_b200/csrc/bbm_ptx.cuh"
+
+using namespace bbm::ptx;
+
+constexpr uint32_t kTiles = 512;  // tiles per CTA (layout B: 256 per stream)
+
+__device__ __forceinline__ void exp_chunk(const uint32_t (&r)[32], uint64_t sl2x2, uint64_t nm2, uint32_t (&pk)[16],
+                                          uint64_t& lacc) {
+#pragma unroll
+  for (uint32_t i = 0; i < 32; i += 2) {
+    const uint64_t x = ffma2(f2_pack(__uint_as_float(r[i]), __uint_as_float(r[i + 1])), sl2x2, nm2);
+    float e0, e1;
+    if ((0x0707u >> ((i / 2) & 15)) & 1u) {
+      exp2_poly2(f2_lo(x), f2_hi(x), e0, e1);
+    } else {
+      e0 = fast_exp2(f2_lo(x));
+      e1 = fast_exp2(f2_hi(x));
+    }
+    lacc = fadd2(lacc, f2_pack(e0, e1));
+    pk[i / 2] = pack_bf16x2(e0, e1);
+  }
+}
+
+__device__ __forceinline__ float max32(const uint32_t (&r)[32]) {
+  float m0 = -INFINITY, m1 = -INFINITY;
+#pragma unroll
+  for (uint32_t i = 0; i < 32; i += 4) {
+    m0 = fmax3(m0, __uint_as_float(r[i]), __uint_as_float(r[i + 1]));
+    m1 = fmax3(m1, __uint_as_float(r[i + 2]), __uint_as_float(r[i + 3]));
+  }
+  return fmaxf(m0, m1);
+}
+
+template <int LAYOUT>
+__global__ void __launch_bounds__(384, 1) engine_kernel(unsigned long long* out, float* sink) {
+  __shared__ uint32_t tbase;
+  __shared__ float xchg[2][2][128];
+  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (warp == 0) {
+    tmem_alloc<512>(&tbase);
+    tmem_relinquish();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tbase;
+  const uint32_t quad = warp & 3, row = quad * 32 + lane, lane_off = (quad * 32) << 16;
+  // fill both S buffers (columns 0..255) with scores
+  if (warp >= 4 && warp < 8) {
+#pragma unroll 1
+    for (uint32_t c = 0; c < 256; c += 32) {
+      uint32_t v[32];
+#pragma unroll
+      for (uint32_t i = 0; i < 32; ++i) v[i] = __float_as_uint(0.01f * static_cast<float>((row * 7 + c + i) % 97));
+      tmem_st32(tmem + lane_off + c, v);
+    }
+    tmem_st_wait();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint64_t sl2x2 = f2_pack(0.18f, 0.18f);
+  float l = 0.0f, m_run = 0.0f;
+  long long t0 = clock64();
+  if (warp >= 4) {
+    if (LAYOUT == 0) {
+      const uint32_t half = (warp - 4) >> 2;
+#pragma unroll 1
+      for (uint32_t k = 0; k < kTiles; ++k) {
+        const uint32_t ts = tmem + lane_off + (k & 1) * 128;
+        uint32_t a0[32], a1[32];
+        tmem_ld32(ts + half * 64, a0);
+        tmem_ld32(ts + half * 64 + 32, a1);
+        tmem_ld_wait();
+        float pm = fmaxf(max32(a0), max32(a1));
+        xchg[k & 1][half][row] = pm;
+        named_bar_sync(1, 256);
+        pm = fmaxf(pm, xchg[k & 1][half ^ 1][row]);
+        m_run = fmaxf(m_run, pm * 0.18f);
+        const uint64_t nm2 = f2_pack(-m_run, -m_run);
+        uint32_t pk[16];
+        uint64_t lacc = 0;
+        exp_chunk(a0, sl2x2, nm2, pk, lacc);
+        tmem_st16(ts + 256 + half * 32, pk);  // P to scratch columns (S stays intact)
+        exp_chunk(a1, sl2x2, nm2, pk, lacc);
+        tmem_st16(ts + 256 + half * 32 + 16, pk);
+        l += f2_lo(lacc) + f2_hi(lacc);
+        tmem_st_wait();
+      }
+    } else {
+      const uint32_t stream = (warp - 4) >> 2;  // S buffer of this stream
+#pragma unroll 1
+      for (uint32_t k = 0; k < kTiles / 2; ++k) {
+        const uint32_t ts = tmem + lane_off + stream * 128;
+        float pm = -INFINITY;
+#pragma unroll
+        for (uint32_t c = 0; c < 128; c += 64) {  // pass 1: row max
+          uint32_t a0[32], a1[32];
+          tmem_ld32(ts + c, a0);
+          tmem_ld32(ts + c + 32, a1);
+          tmem_ld_wait();
+          pm = fmaxf(pm, fmaxf(max32(a0), max32(a1)));
+        }
+        m_run = fmaxf(m_run, pm * 0.18f);
+        const uint64_t nm2 = f2_pack(-m_run, -m_run);
+        uint64_t lacc = 0;
+#pragma unroll
+        for (uint32_t c = 0; c < 128; c += 64) {  // pass 2: exponentials, P
+          uint32_t a0[32], a1[32];
+          tmem_ld32(ts + c, a0);
+          tmem_ld32(ts + c + 32, a1);
+          tmem_ld_wait();
+          uint32_t pk[16];
+          exp_chunk(a0, sl2x2, nm2, pk, lacc);
+          tmem_st16(tmem + lane_off + 256 + stream * 64 + c / 2, pk);
+          exp_chunk(a1, sl2x2, nm2, pk, lacc);
+          tmem_st16(tmem + lane_off + 256 + stream * 64 + c / 2 + 16, pk);
+        }
+        l += f2_lo(lacc) + f2_hi(lacc);
+        tmem_st_wait();
+      }
+    }
+  }
+  long long t1 = clock64();
+  __syncthreads();
+  if (warp >= 4) sink[blockIdx.x * 256 + threadIdx.x - 128] = l + m_run;
+  if (threadIdx.x == 128) out[blockIdx.x] = t1 - t0;
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) tmem_dealloc<512>(tmem);
+}
+
+template <int LAYOUT>
+void run(const char* name, int sms) {
+  unsigned long long* d;
+  float* sink;
+  cudaMalloc(&d, sms * 8);
+  cudaMalloc(&sink, sms * 256 * 4);
+  engine_kernel<LAYOUT><<<sms, 384>>>(d, sink);
+  engine_kernel<LAYOUT><<<sms, 384>>>(d, sink);
+  cudaError_t e = cudaDeviceSynchronize();
+  unsigned long long h[256];
+  cudaMemcpy(h, d, sms * 8, cudaMemcpyDeviceToHost);
+  double avg = 0;
+  for (int i = 0; i < sms; ++i) avg += h[i];
+  avg /= sms;
+  std::printf("%-58s %7.0f cycles per 128x128 tile %s\n", name, avg / kTiles, e == cudaSuccess ? "" : cudaGetErrorString(e));
+  cudaFree(d);
+  cudaFree(sink);
+}
+
+int main() {
+  int sms = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  run<0>("A halves: 2 warps per row, max exchange + barrier per tile", sms);
+  run<1>("B rows: 1 thread per row, 2 free-running streams", sms);
+  return 0;
+}
