@@ -421,11 +421,10 @@ __global__ void __launch_bounds__(kThreadsOf<D>, 1)
     }
   } else if (warp == 1 || warp == 3) {
     // ------------------------------------------------------------------ MMA issuers
-    // tcgen05.mma issue is nearly synchronous (~56 cycles per 128x128x16 MMA from an idle pipe,
-    // tools/mma_latency_probe.cu), so one issuing thread competing for issue slots with two
-    // softmax warps on its SMSP cannot keep the tensor pipe fed. Two issuers, each walking the
-    // same tile sequence k = 0, 1, 2, ...:
-    //   warp 1: S_k = Q K_k^T into TMEM buffer k % 3 (SS), once PV_{k-3} (the last reader of
+    // tcgen05.mma issue is nearly synchronous (~56 cycles per 128x128x16 MMA,
+    // tools/mma_issue_probe.cu), and one thread issuing both S and PV queues each behind the other
+    // (measured slower). Two issuers, each walking the same tile sequence k = 0, 1, 2, ...:
+    //   warp 1: S_k = Q K_k^T into TMEM buffer k % 2 (SS), once PV_{k-2} (the last reader of
     //           that buffer's P) has completed;
     //   warp 3: O += P_k V_k (TS, P read from TMEM) once the softmax engine has written P_k.
     // Ring slots follow the load order: K_k at kseq_of(k), V_k at vseq_of(k) (mod kRing).
@@ -444,7 +443,7 @@ __global__ void __launch_bounds__(kThreadsOf<D>, 1)
         if (it.t == kEnd) break;
         if (it.nt == 0) continue;
         // items alternate between the two O accumulators; an item's first PV waits until the
-        // engine has read out the item two back (its deferred epilogue)
+        // epilogue warpgroup has read out the item two back
         const uint32_t ob = items++ & 1;
         const uint32_t tmem_o = tmem + C::kOCol + ob * D;
         for (uint32_t j = 0; j < it.nt; ++j, ++k) {
