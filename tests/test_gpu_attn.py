@@ -374,3 +374,26 @@ def test_rcm_host_pipeline_equals_explicit_permutation(cuda):
     got = (out.astype(np.uint32) << 16).view(np.float32)
     check_against_oracle(shuffled, q, k, v, d ** -0.5, got, rmax.astype(np.float64),
                          rsum.astype(np.float64), bbm.Variant.binblk, slots_to_check=[0, 4])
+
+
+@pytest.mark.parametrize("d", [64, 128])
+def test_mixed_items_in_one_launch(cuda, d):
+    """Every item shape in one multi-slot launch: fully masked row tiles (no tiles), one-tile rows,
+    a long global row that the launch splits (split-KV), a ragged last tile, and both O
+    accumulators / statistics slots in turn — the hand-off between the softmax engine and the
+    epilogue warpgroup must keep each item's statistics with its own accumulator."""
+    n = 2900
+    mask = bbm.gen_longformer_windowed(n, 40)
+    for j in range(n):  # global row and column: row 0 sees everything, everyone sees key 0
+        mask.set(0, j, True)
+        mask.set(j, 0, True)
+    for i in range(1280, 1408):  # a whole row tile with no key
+        for j in range(n):
+            mask.set(i, j, False)
+    q, k, v = problem(31, 3, n, d)
+    scale = 1 / np.sqrt(d)
+    prep = bbm.preprocess_mask(mask, bbm.BlockSpec(128, 128))
+    for var in (bbm.Variant.binblk, bbm.Variant.dense_binblk):
+        out, rmax, rsum, _ = run_gpu(mask, q, k, v, scale, var, cuda, prep=prep)
+        check_against_oracle(mask, q, k, v, scale, out, rmax, rsum, var)
+        assert np.all(out[:, 1280:1408] == 0) and np.all(rmax[:, 1280:1408] == -np.inf)
