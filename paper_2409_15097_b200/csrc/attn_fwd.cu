@@ -14,23 +14,23 @@
 //
 // Structure: one persistent CTA per SM (512 threads = four warpgroups, registers rebalanced with
 // setmaxnreg), one stream of items (the tile sequence of consecutive items is treated as one
-// sequence k = 0, 1, 2, ...). The score accumulator is double-buffered in TMEM, so S_{k+1} is
-// computed while the softmax engine turns S_k into P_k.
+// sequence k = 0, 1, 2, ...). The score accumulator is triple-buffered in TMEM, so S_{k+1} and
+// S_{k+2} are computed while the softmax engine turns S_k into P_k.
 //   warp 0       producer: claims items, publishes them through a shared-memory item queue,
 //                loads Q (double-buffered across items) and K_k, V_k into a K/V ring (TMA,
 //                128B-swizzled 64-column boxes).
 //   warps 1, 3   MMA issuers (one thread each): warp 1 S_k = Q K_k^T (SS, both K-major) into
-//                TMEM buffer k % 2 once PV_{k-2} has completed (S_{k+2} reuses P_k's columns);
+//                TMEM buffer k % 3 once PV_{k-3} has completed (S_{k+3} reuses P_k's columns);
 //                warp 3 O += P_k V_k (TS: P read from TMEM, V MN-major).
-//   warp 2       TMEM allocator (512 columns: S buffers at 0 and 128; O accumulators at 256 and
-//                256 + D, alternating between items).
+//   warp 2       TMEM allocator (512 columns: S buffers at 0, 128, 256; O at 384 — at d=64 two O
+//                accumulators at 384 and 448, alternating between items).
 //   warps 4-11   softmax engine (168 registers): warps 4-7 own S columns [0,64), warps 8-11 the
 //                other half; the halves exchange their partial row max through shared memory
 //                once per tile. At an item's end the engine hands its row statistics to the
 //                epilogue warpgroup through shared memory (ItemStats) and moves on.
-//   warps 12-15  epilogue (88 registers): waits for an item's last PV, writes O / l as bf16
-//                through 128B-swizzled staging and TMA stores (or a split-KV partial) and
-//                releases the accumulator.
+//   warps 12-15  epilogue (88 registers): waits for an item's last PV, reads O out of TMEM and
+//                releases the accumulator, then writes O / l as bf16 one 64-column box at a time
+//                through a 128B-swizzled staging box and TMA stores (or a split-KV partial).
 // Numerics: scores are scaled into the log2 domain; the running max is only raised when it grows
 // by more than 2^8 (stale-max trick; exact after the final O/l), P is rounded to bf16 for the
 // MMA and written over S in TMEM, l accumulates in fp32. Partial tiles read 8 B of mask bits per
@@ -122,8 +122,15 @@ constexpr uint32_t kBoxBytes = 128 * 64 * 2;  // 128 rows x 64 bf16, one 128B-sw
 
 // S buffers in TMEM: S_{k+kSBufs} is issued once PV_k (the last reader of P_k, written over S_k)
 // has completed, so the S issuer runs kSBufs tiles ahead of the PV issuer. TMEM at D = 128:
-// S at 0 and 128, two O accumulators at 256 and 384 (the whole 512-column allocation).
-constexpr uint32_t kSBufs = 2;
+// S at 0, 128 and 256, one O accumulator at 384 (the whole 512-column allocation; the epilogue
+// warpgroup releases it as soon as it has read it out); at D = 64 two O accumulators.
+#ifndef BBM_SBUFS
+#define BBM_SBUFS 3
+#endif
+constexpr uint32_t kSBufs = BBM_SBUFS;
+// O accumulators behind the S buffers: two (items alternate) when they fit, else one
+template <int D>
+constexpr uint32_t kOBufs = 512 - kSBufs * 128 >= 2 * D ? 2 : 1;
 // Ring positions in the load order K_0 .. K_{kSBufs-1}, V_0, K_kSBufs, V_1, ...: the order the
 // two MMA issuers consume them in, so a load only waits for the slot freed kRing positions
 // earlier in that same order.
@@ -139,8 +146,9 @@ template <int D>
 struct Cfg {
   static constexpr uint32_t kBoxes = D / 64;
   static constexpr uint32_t kTileBytes = kBoxes * kBoxBytes;  // one 128 x D bf16 tile
-  static constexpr uint32_t kRing = (D == 64) ? 9 : 3;  // K/V ring slots
-  static constexpr uint32_t kStageBytes = kBoxBytes;          // epilogue staging (two buffers)
+  // K/V ring slots: the K cursor runs kSBufs tiles ahead of the V cursor
+  static constexpr uint32_t kRing = (D == 64) ? 9 : kSBufs + 1;
+  static constexpr uint32_t kStageBytes = kBoxBytes;          // epilogue staging: one 128 x 64 box
   static constexpr uint32_t kTmemCols = 512;
   static constexpr uint32_t kOCol = kSBufs * 128;
 };
@@ -176,7 +184,7 @@ struct SmemCtl {
 
 template <int D>
 constexpr uint32_t smem_bytes() {
-  return Cfg<D>::kTileBytes * (2 + Cfg<D>::kRing) + 2 * Cfg<D>::kStageBytes +
+  return Cfg<D>::kTileBytes * (2 + Cfg<D>::kRing) + Cfg<D>::kStageBytes +
          sizeof(SmemCtl<Cfg<D>::kRing, kParts<D>>);
 }
 
@@ -280,8 +288,8 @@ __global__ void __launch_bounds__(kThreadsOf<D>, 1)
   extern __shared__ __align__(1024) uint8_t smem[];
   uint8_t* sq = smem;                              // [2][tile]          Q, double-buffered
   uint8_t* ring = sq + 2 * C::kTileBytes;          // [kRing][tile]      K/V ring
-  uint8_t* stage = ring + C::kRing * C::kTileBytes;  // [2][128 x 64 bf16] epilogue staging
-  auto* ctl = reinterpret_cast<SmemCtl<C::kRing, kParts<D>>*>(stage + 2 * C::kStageBytes);
+  uint8_t* stage = ring + C::kRing * C::kTileBytes;  // [128 x 64 bf16] epilogue staging box
+  auto* ctl = reinterpret_cast<SmemCtl<C::kRing, kParts<D>>*>(stage + C::kStageBytes);
 
   const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if ((smem_u32(smem) & 1023u) != 0) __trap();  // 128B-swizzle atoms need 1024-byte alignment
@@ -424,7 +432,7 @@ __global__ void __launch_bounds__(kThreadsOf<D>, 1)
     // tcgen05.mma issue is nearly synchronous (~56 cycles per 128x128x16 MMA,
     // tools/mma_issue_probe.cu), and one thread issuing both S and PV queues each behind the other
     // (measured slower). Two issuers, each walking the same tile sequence k = 0, 1, 2, ...:
-    //   warp 1: S_k = Q K_k^T into TMEM buffer k % 2 (SS), once PV_{k-2} (the last reader of
+    //   warp 1: S_k = Q K_k^T into TMEM buffer k % 3 (SS), once PV_{k-3} (the last reader of
     //           that buffer's P) has completed;
     //   warp 3: O += P_k V_k (TS, P read from TMEM) once the softmax engine has written P_k.
     // Ring slots follow the load order: K_k at kseq_of(k), V_k at vseq_of(k) (mod kRing).
@@ -444,7 +452,7 @@ __global__ void __launch_bounds__(kThreadsOf<D>, 1)
         if (it.nt == 0) continue;
         // items alternate between the two O accumulators; an item's first PV waits until the
         // epilogue warpgroup has read out the item two back
-        const uint32_t ob = items++ & 1;
+        const uint32_t ob = kOBufs<D> == 2 ? (items++ & 1) : 0;
         const uint32_t tmem_o = tmem + C::kOCol + ob * D;
         for (uint32_t j = 0; j < it.nt; ++j, ++k) {
           const uint32_t buf = k % kSBufs;
@@ -577,7 +585,8 @@ __global__ void __launch_bounds__(kThreadsOf<D>, 1)
       }
       if (tracer) trace_ev<kTrace>(tracing, p, &ctl->trace_count, 29, 0, it.t);
       float m_run = -INFINITY, m_true = -INFINITY, l = 0.0f;
-      const uint32_t ob = items++ & 1;  // this item's O accumulator (same sequence as the PV issuer)
+      const uint32_t sl = items++ & 1;              // this item's statistics slot
+      const uint32_t ob = kOBufs<D> == 2 ? sl : 0;  // and O accumulator (same sequence as the PV issuer)
       const uint32_t to = to_base + ob * D;
       if (!have_next_bits) load_bits(it, it.j0, nbits, nentry);  // else prefetched last item
       have_next_bits = false;
@@ -714,9 +723,9 @@ __global__ void __launch_bounds__(kThreadsOf<D>, 1)
 
       // ---------------- item end: hand the row statistics to the epilogue warpgroup, which
       // combines the parts' row sums, waits for the item's last PV and writes O
-      mbar_wait(&ctl->stats_empty[ob], se_ph[ob]);
-      se_ph.flip(ob);
-      ItemStats<kP>& st = ctl->stats[ob];
+      mbar_wait(&ctl->stats_empty[sl], se_ph[sl]);
+      se_ph.flip(sl);
+      ItemStats<kP>& st = ctl->stats[sl];
       st.l[half][row] = l;
       if (half == 0) {
         st.m_run[row] = m_run;
@@ -724,15 +733,15 @@ __global__ void __launch_bounds__(kThreadsOf<D>, 1)
       }
       if (leader) st.item = it;
       __syncwarp();
-      if (lane == 0) mbar_arrive(&ctl->stats_full[ob]);
+      if (lane == 0) mbar_arrive(&ctl->stats_full[sl]);
       if (tracer) trace_ev<kTrace>(tracing, p, &ctl->trace_count, 28, 0, it.t);
     }
     {  // end marker for the epilogue warpgroup
-      const uint32_t ob = items & 1;
-      mbar_wait(&ctl->stats_empty[ob], se_ph[ob]);
-      if (leader) ctl->stats[ob].item.t = kEnd;
+      const uint32_t sl = items & 1;
+      mbar_wait(&ctl->stats_empty[sl], se_ph[sl]);
+      if (leader) ctl->stats[sl].item.t = kEnd;
       __syncwarp();
-      if (lane == 0) mbar_arrive(&ctl->stats_full[ob]);
+      if (lane == 0) mbar_arrive(&ctl->stats_full[sl]);
     }
   } else {
     setmaxnreg_dec<kOtherRegs>();
@@ -755,23 +764,29 @@ __global__ void __launch_bounds__(kThreadsOf<D>, 1)
         if (p.row_sum) p.row_sum[si] = l_tot > 0.0f ? l_tot * exp2f(m_run2 - m_true2) : 0.0f;
       }
     };
-    // TMA-store the staged O tile of item `it` (called by every epilogue thread)
-    auto store_staged = [&](const ItemDesc& it) {
+    // The O tile leaves one 64-column box at a time through a single staging box: TMA-store box b
+    // of item `it` once staged (called by every epilogue thread) ...
+    auto store_box = [&](const ItemDesc& it, uint32_t b) {
       fence_proxy_async_smem();
       named_bar_sync(2, kEpi);
       if (leader) {
-        tma_store_3d(&tm_o, stage, 0, it.rt * 128, it.slot);
-        if (D == 128) tma_store_3d(&tm_o, stage + C::kStageBytes, 64, it.rt * 128, it.slot);
+        tma_store_3d(&tm_o, stage, b * 64, it.rt * 128, it.slot);
         bulk_commit_group();
       }
     };
-    // staged output column c goes to box c / 64, 16-byte chunk (c % 64) / 8 of the row
-    auto stg_row_of = [&](uint32_t c) { return stage + (c / 64) * C::kStageBytes + row * 128; };
+    // ... and wait until the previous box's store has read the staging memory
+    auto box_free = [&]() {
+      if (leader) bulk_wait_group_read<0>();
+      named_bar_sync(2, kEpi);
+    };
+    // staged output column c goes to 16-byte chunk (c % 64) / 8 of the row
+    auto stg_row_of = [&](uint32_t) { return stage + row * 128; };
     auto stg_chunk_of = [&](uint32_t c) { return (c % 64) / 8; };
-    for (uint32_t ob = 0;; ob ^= 1) {
-      mbar_wait(&ctl->stats_full[ob], sf_ph[ob]);
-      sf_ph.flip(ob);
-      const ItemStats<kParts<D>>& st = ctl->stats[ob];
+    for (uint32_t sl = 0;; sl ^= 1) {
+      mbar_wait(&ctl->stats_full[sl], sf_ph[sl]);
+      sf_ph.flip(sl);
+      const ItemStats<kParts<D>>& st = ctl->stats[sl];
+      const uint32_t ob = kOBufs<D> == 2 ? sl : 0;
       const ItemDesc it = st.item;
       if (it.t == kEnd) break;
       float l_unit = 0.0f;
@@ -779,7 +794,7 @@ __global__ void __launch_bounds__(kThreadsOf<D>, 1)
       for (uint32_t h = 0; h < kParts<D>; ++h) l_unit += st.l[h][row];
       const float m_run = st.m_run[row], m_true = st.m_true[row];
       __syncwarp();
-      if (lane == 0) mbar_arrive(&ctl->stats_empty[ob]);
+      if (lane == 0) mbar_arrive(&ctl->stats_empty[sl]);
       const uint32_t to = tmem + C::kOCol + lane_off + ob * D;
       if (leader) bulk_wait_group_read<0>();  // staging buffers free again
       mbar_wait(&ctl->o_full[ob], o_ph[ob]);
@@ -799,16 +814,19 @@ __global__ void __launch_bounds__(kThreadsOf<D>, 1)
           tmem_ld32(to + c64 * 64, o[0]);
           tmem_ld32(to + c64 * 64 + 32, o[1]);
           tmem_ld_wait();
+          if (c64 + 1 == D / 64) {
+            tc_fence_before();
+            mbar_arrive(&ctl->o_empty[ob]);  // the accumulator may be overwritten from here on
+          }
+          if (c64 > 0) box_free();
 #pragma unroll
           for (uint32_t h = 0; h < 2; ++h)
             stage_chunk32(stg_row_of(c64 * 64 + h * 32), row, stg_chunk_of(c64 * 64 + h * 32),
                           reinterpret_cast<const float*>(o[h]), inv);
-        }
-        tc_fence_before();
-        mbar_arrive(&ctl->o_empty[ob]);  // the accumulator may be overwritten from here on
 #ifndef BBM_ABLATE_NO_EPI
-        store_staged(it);
+          store_box(it, c64);
 #endif
+        }
         write_stats(it, m_true, m_run, l_unit);
       } else {
         // ---- split-KV chunk: publish the unnormalized partial, the last chunk combines
@@ -858,6 +876,7 @@ __global__ void __launch_bounds__(kThreadsOf<D>, 1)
           if (leader) *ctr = 0;    // ready for the next launch
 #pragma unroll 1
           for (uint32_t c32 = 0; c32 < D / 32; ++c32) {
+            if (c32 > 0 && c32 % 2 == 0) box_free();  // the next 64-column box reuses the staging
             float acc[32];
 #pragma unroll
             for (uint32_t i = 0; i < 32; ++i) acc[i] = 0.0f;
@@ -877,8 +896,8 @@ __global__ void __launch_bounds__(kThreadsOf<D>, 1)
               }
             }
             stage_chunk32(stg_row_of(c32 * 32), row, stg_chunk_of(c32 * 32), acc, inv);
+            if (c32 % 2 == 1) store_box(it, c32 / 2);
           }
-          store_staged(it);
           write_stats(it, mtrue, mrun, ltot);
         }
       }
