@@ -497,10 +497,12 @@ __global__ void __launch_bounds__(kThreadsOf<D>, 1)
             tc_fence_after();
             const uint64_t vdesc = make_sdesc_sw128(raddr + slot * C::kTileBytes, kBoxBytes, 1024);
             const uint32_t pcol = tmem + buf * 128;
+#ifndef BBM_ABLATE_NO_PV  // timing experiments only: O is never accumulated
 #pragma unroll
             for (uint32_t kk = 0; kk < 128 / 16; ++kk)
               umma_ts(tmem_o, pcol + kk * 8, sdesc_advance(vdesc, kk * 2048), idesc_o,
                       (j > 0 || kk > 0) ? 1u : 0u);
+#endif
             tc_commit(&ctl->ring_empty[slot]);
             tc_commit(&ctl->pv_done[buf]);
             trace_ev<kTrace>(tracing, p, &ctl->trace_count, 11, buf, j);
