@@ -1,4 +1,4 @@
-// engine_probe.cu — softmax-engine throughput by work organisation (measurement tool, no MMAs).
+// engine_probe.cu — softmax-engine throughput by work organisation (measurement tool).
 //
 // Both layouts run the forward kernel's per-tile math on scores resident in TMEM (scale/shift
 // FFMA2, 6/16 polynomial exp2 pairs, FADD2 row sums, bf16 packing, P written back with tcgen05.st),
@@ -9,6 +9,8 @@
 //   B "rows":  one thread per row owns all 128 columns (two passes over TMEM: max, then exp); warps
 //      4-7 and 8-11 are two independent streams on different S buffers, with no barrier between
 //      them (FA4's two-softmax-warpgroup layout).
+// With a concurrent MMA stream (one thread issuing 128x128x16 SS MMAs into spare TMEM columns for
+// the whole run) the same loops show how much tensor-core traffic slows the engine.
 // Output: cycles per 128x128 tile (all tiles of both streams / elapsed).
 #include <cstdio>
 
@@ -45,14 +47,22 @@ __device__ __forceinline__ float max32(const uint32_t (&r)[32]) {
   return fmaxf(m0, m1);
 }
 
-template <int LAYOUT>
+template <int LAYOUT, bool kMma>
 __global__ void __launch_bounds__(384, 1) engine_kernel(unsigned long long* out, float* sink) {
+  extern __shared__ __align__(1024) uint8_t dsmem[];  // MMA operands (kMma)
   __shared__ uint32_t tbase;
+  __shared__ uint64_t mbar;
+  __shared__ volatile uint32_t done;
   __shared__ float xchg[2][2][128];
   const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (warp == 0) {
     tmem_alloc<512>(&tbase);
     tmem_relinquish();
+  }
+  if (threadIdx.x == 0) {
+    done = 0;
+    mbar_init(&mbar, 1);
+    fence_barrier_init();
   }
   tc_fence_before();
   __syncthreads();
@@ -76,6 +86,22 @@ __global__ void __launch_bounds__(384, 1) engine_kernel(unsigned long long* out,
   const uint64_t sl2x2 = f2_pack(0.18f, 0.18f);
   float l = 0.0f, m_run = 0.0f;
   long long t0 = clock64();
+  if (kMma && warp == 1 && lane == 0) {
+    // a tensor-core stream beside the engine: 128x128x16 SS MMAs into TMEM columns 384..511
+    const uint32_t a = smem_u32(dsmem), b = a + 32768;
+    constexpr uint32_t idesc = make_idesc_bf16(128, 128, false, false);
+    uint32_t ph = 0;
+    while (!done) {
+#pragma unroll
+      for (uint32_t kk = 0; kk < 8; ++kk) {
+        const uint32_t off = (kk / 4) * 16384 + (kk % 4) * 32;
+        umma_ss(tmem + 384, make_sdesc_sw128(a + off, 16, 1024), make_sdesc_sw128(b + off, 16, 1024), idesc, kk > 0);
+      }
+      tc_commit(&mbar);
+      mbar_wait(&mbar, ph);
+      ph ^= 1;
+    }
+  }
   if (warp >= 4) {
     if (LAYOUT == 0) {
       const uint32_t half = (warp - 4) >> 2;
@@ -136,6 +162,10 @@ __global__ void __launch_bounds__(384, 1) engine_kernel(unsigned long long* out,
     }
   }
   long long t1 = clock64();
+  if (warp >= 4) {
+    named_bar_sync(2, 256);
+    if (threadIdx.x == 128) done = 1;
+  }
   __syncthreads();
   if (warp >= 4) sink[blockIdx.x * 256 + threadIdx.x - 128] = l + m_run;
   if (threadIdx.x == 128) out[blockIdx.x] = t1 - t0;
@@ -144,14 +174,15 @@ __global__ void __launch_bounds__(384, 1) engine_kernel(unsigned long long* out,
   if (warp == 0) tmem_dealloc<512>(tmem);
 }
 
-template <int LAYOUT>
+template <int LAYOUT, bool kMma>
 void run(const char* name, int sms) {
   unsigned long long* d;
   float* sink;
   cudaMalloc(&d, sms * 8);
   cudaMalloc(&sink, sms * 256 * 4);
-  engine_kernel<LAYOUT><<<sms, 384>>>(d, sink);
-  engine_kernel<LAYOUT><<<sms, 384>>>(d, sink);
+  cudaFuncSetAttribute(engine_kernel<LAYOUT, kMma>, cudaFuncAttributeMaxDynamicSharedMemorySize, 66 * 1024);
+  engine_kernel<LAYOUT, kMma><<<sms, 384, 66 * 1024>>>(d, sink);
+  engine_kernel<LAYOUT, kMma><<<sms, 384, 66 * 1024>>>(d, sink);
   cudaError_t e = cudaDeviceSynchronize();
   unsigned long long h[256];
   cudaMemcpy(h, d, sms * 8, cudaMemcpyDeviceToHost);
@@ -166,7 +197,9 @@ void run(const char* name, int sms) {
 int main() {
   int sms = 0;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
-  run<0>("A halves: 2 warps per row, max exchange + barrier per tile", sms);
-  run<1>("B rows: 1 thread per row, 2 free-running streams", sms);
+  run<0, false>("A halves: 2 warps per row, max exchange + barrier per tile", sms);
+  run<1, false>("B rows: 1 thread per row, 2 free-running streams", sms);
+  run<0, true>("A halves + a concurrent 128x128x16 MMA stream", sms);
+  run<1, true>("B rows + a concurrent 128x128x16 MMA stream", sms);
   return 0;
 }
