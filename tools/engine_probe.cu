@@ -47,12 +47,13 @@ __device__ __forceinline__ float max32(const uint32_t (&r)[32]) {
   return fmaxf(m0, m1);
 }
 
-template <int LAYOUT, bool kMma>
+template <int LAYOUT, bool kMma, bool kSync = false>
 __global__ void __launch_bounds__(384, 1) engine_kernel(unsigned long long* out, float* sink) {
   extern __shared__ __align__(1024) uint8_t dsmem[];  // MMA operands (kMma)
   __shared__ uint32_t tbase;
   __shared__ uint64_t mbar;
   __shared__ volatile uint32_t done;
+  __shared__ uint64_t sync_bar[2];  // kSync: the kernel's per-tile s_full wait / p_full arrive
   __shared__ float xchg[2][2][128];
   const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (warp == 0) {
@@ -61,6 +62,8 @@ __global__ void __launch_bounds__(384, 1) engine_kernel(unsigned long long* out,
   }
   if (threadIdx.x == 0) {
     done = 0;
+    mbar_init(&sync_bar[0], 1);  // waited on: completed once below, then always phase 0 done
+    mbar_init(&sync_bar[1], 256);
     mbar_init(&mbar, 1);
     fence_barrier_init();
   }
@@ -80,6 +83,7 @@ __global__ void __launch_bounds__(384, 1) engine_kernel(unsigned long long* out,
     }
     tmem_st_wait();
   }
+  if (threadIdx.x == 0) mbar_arrive(&sync_bar[0]);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -108,6 +112,10 @@ __global__ void __launch_bounds__(384, 1) engine_kernel(unsigned long long* out,
 #pragma unroll 1
       for (uint32_t k = 0; k < kTiles; ++k) {
         const uint32_t ts = tmem + lane_off + (k & 1) * 128;
+        if (kSync) {
+          mbar_wait(&sync_bar[0], 0);  // already complete, as a ready s_full
+          tc_fence_after();
+        }
         uint32_t a0[32], a1[32];
         tmem_ld32(ts + half * 64, a0);
         tmem_ld32(ts + half * 64 + 32, a1);
@@ -126,6 +134,10 @@ __global__ void __launch_bounds__(384, 1) engine_kernel(unsigned long long* out,
         tmem_st16(ts + 256 + half * 32 + 16, pk);
         l += f2_lo(lacc) + f2_hi(lacc);
         tmem_st_wait();
+        if (kSync) {
+          tc_fence_before();
+          mbar_arrive(&sync_bar[1]);  // as p_full (nobody waits)
+        }
       }
     } else {
       const uint32_t stream = (warp - 4) >> 2;  // S buffer of this stream
@@ -174,15 +186,15 @@ __global__ void __launch_bounds__(384, 1) engine_kernel(unsigned long long* out,
   if (warp == 0) tmem_dealloc<512>(tmem);
 }
 
-template <int LAYOUT, bool kMma>
+template <int LAYOUT, bool kMma, bool kSync = false>
 void run(const char* name, int sms) {
   unsigned long long* d;
   float* sink;
   cudaMalloc(&d, sms * 8);
   cudaMalloc(&sink, sms * 256 * 4);
-  cudaFuncSetAttribute(engine_kernel<LAYOUT, kMma>, cudaFuncAttributeMaxDynamicSharedMemorySize, 66 * 1024);
-  engine_kernel<LAYOUT, kMma><<<sms, 384, 66 * 1024>>>(d, sink);
-  engine_kernel<LAYOUT, kMma><<<sms, 384, 66 * 1024>>>(d, sink);
+  cudaFuncSetAttribute(engine_kernel<LAYOUT, kMma, kSync>, cudaFuncAttributeMaxDynamicSharedMemorySize, 66 * 1024);
+  engine_kernel<LAYOUT, kMma, kSync><<<sms, 384, 66 * 1024>>>(d, sink);
+  engine_kernel<LAYOUT, kMma, kSync><<<sms, 384, 66 * 1024>>>(d, sink);
   cudaError_t e = cudaDeviceSynchronize();
   unsigned long long h[256];
   cudaMemcpy(h, d, sms * 8, cudaMemcpyDeviceToHost);
@@ -201,5 +213,6 @@ int main() {
   run<1, false>("B rows: 1 thread per row, 2 free-running streams", sms);
   run<0, true>("A halves + a concurrent 128x128x16 MMA stream", sms);
   run<1, true>("B rows + a concurrent 128x128x16 MMA stream", sms);
+  run<0, true, true>("A halves + MMA stream + per-tile mbarrier wait/arrive, fences", sms);
   return 0;
 }
