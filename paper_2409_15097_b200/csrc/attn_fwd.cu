@@ -645,17 +645,9 @@ __global__ void __launch_bounds__(kThreadsOf<D>, 1)
         }
 #endif
         uint32_t a0[32], a1[32];
-#ifdef BBM_ABLATE_NO_SLOAD  // timing experiments only: scores are not read from TMEM
-#pragma unroll
-        for (uint32_t i = 0; i < 32; ++i) {
-          a0[i] = __float_as_uint(static_cast<float>(i ^ lane ^ j) * 0.01f);
-          a1[i] = __float_as_uint(static_cast<float>(i ^ lane ^ k) * 0.01f);
-        }
-#else
         tmem_ld32(ts + half * kSC, a0);
         if constexpr (kSC == 64) tmem_ld32(ts + half * kSC + 32, a1);
         tmem_ld_wait();
-#endif
         if (tracer) trace_ev<kTrace>(tracing, p, &ctl->trace_count, 25, buf, j);
         // binblk reads bits for every tile; a warp whose 32 rows see every key of the tile skips
         // the selects (they would be no-ops)

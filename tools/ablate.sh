@@ -20,7 +20,6 @@ for v in $VARIANTS; do
     DEG2_6) FL="-DBBM_POLY_DEG2" ;;
     DEG2_8) FL="-DBBM_POLY_DEG2 -DBBM_POLY_PAIRS=0x0F0Fu" ;;
     DEG2_4) FL="-DBBM_POLY_DEG2 -DBBM_POLY_PAIRS=0x0303u" ;;
-    NO_SLOAD) FL="-DBBM_ABLATE_NO_SLOAD" ;;
     NO_PV) FL="-DBBM_ABLATE_NO_PV" ;;
     SUSPEND) FL="-DBBM_SUSPEND_WAIT" ;;
     LACC1) FL="-DBBM_LACC=1" ;;
