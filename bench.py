@@ -1,24 +1,34 @@
 """Benchmark of the B200 masked-attention hot path (BASELINE.json metric).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--variant binblk]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c5] [--variant binblk]
     python bench.py --impl reference ...        # the reference's own CPU engine (oracle/_ref)
 
-One step = one blocked_forward over the whole config (all B*H slots share one mask and one
-MaskPrep, engine.hpp:489-505) with inputs resident in HBM, launched through the C ABI
-(bbm_attn_fwd). Under torchrun each rank runs its own full config on its own GPU (weak scaling,
-disjoint slot ranges of a virtual global batch; no collective on the data path — the only
-collectives are the timing barrier and the max-over-ranks of the elapsed time).
+Default workload: BASELINE config 5 (the metric is quoted "at 1-8 B200", and C5 is the config
+sharded over batch x heads): a 1 % structured graph mask (Longformer band w=164 at N=32768,
+relabelled by std::shuffle(mt19937_64(3)), then RCM-reordered), B=4 H=32 d=128, binblk.
+
+One step = one blocked_forward over this rank's slots of the config (all B*H slots share one mask
+and one MaskPrep, engine.hpp:489-505) with inputs resident in HBM, launched through the C ABI
+(bbm_attn_fwd). Under torchrun the config's B*H slots are sharded contiguously over the ranks
+([r*S/G, (r+1)*S/G), SURVEY §8e, strong scaling); rank 0 builds the mask metadata once and the
+other ranks import it peer to peer (cudaIpc handle + one device-to-device copy over NVLink). No
+collective on the data path: the only collectives are the timing barriers, the metadata handle
+broadcast before the timed region and the max-over-ranks of the elapsed device time.
 
 Printed on rank 0: ONE JSON line with the contract keys plus roofline / cpu_baseline / e2e /
-clocks / dense-run speedup / preprocessor throughput.
+clocks / dense-run speed-up / preprocessor throughput.
+
+--impl reference never imports paper_2409_15097_b200: it builds the same mask through the
+reference's own generators / reorder code (oracle/_ref, compiled from /root/reference headers)
+and times the reference's blocked_forward<float> on the host cores.
 """
 from __future__ import annotations
 
 import argparse
+import importlib.util
 import json
 import os
 import statistics
-import subprocess
 import sys
 import threading
 import time
@@ -27,7 +37,11 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 if ROOT not in sys.path:
     sys.path.insert(0, ROOT)
 
-from paper_2409_15097_b200.rng import MT19937_64, uniform_below  # noqa: E402
+# the pure-Python mt19937_64 (rng.hpp mappings) without importing the package (whose import loads
+# libbbm.so, which the reference arm must never touch)
+_spec = importlib.util.spec_from_file_location("_bbm_rng", os.path.join(ROOT, "paper_2409_15097_b200", "rng.py"))
+_rng = importlib.util.module_from_spec(_spec)
+_spec.loader.exec_module(_rng)
 
 METRIC = "masked-attn fwd TFLOP/s on executed blocks (ms & speedup vs dense-mask reported beside)"
 PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
@@ -36,72 +50,125 @@ PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustain
 def alpaca_lengths(total: int, seed: int = 7, lo: int = 64, span: int = 449):
     """Config 2 segment lengths: L_i = 64 + uniform_below(gen, 449) from mt19937_64(seed), the last
     segment truncated so the lengths fill `total`."""
-    gen = MT19937_64(seed)
+    gen = _rng.MT19937_64(seed)
     out, acc = [], 0
     while acc < total:
-        length = min(lo + uniform_below(gen, span), total - acc)
+        length = min(lo + _rng.uniform_below(gen, span), total - acc)
         out.append(length)
         acc += length
     return out
 
 
-RCM_PERM = {}  # config -> RCM permutation (new -> old) of its reordered mask
+# BASELINE.json configs: (B, H, d, default variant, description, N)
+CONFIGS = {
+    "c1": (1, 4, 64, "binblk", "C1 causal B=1 H=4 N=1024 d=64", 1024),
+    "c2": (8, 32, 128, "binblk",
+           "C2 packed-seq (ALPACA-like lengths U{64..512}, mt19937_64(7)) B=8 H=32 N=4096 d=128", 4096),
+    "c3": (1, 32, 128, "binblk", "C3 causal prefix 2048 + MEDUSA[16;15] tree (N=2304) B=1 H=32 d=128", 2304),
+    "c4": (1, 16, 64, "dense-binblk", "C4 Longformer window 512 + 128 global, N=16384 B=1 H=16 d=64", 16384),
+    "c5": (4, 32, 128, "binblk",
+           "C5 1% band (w=164) relabelled by mt19937_64(3), RCM-reordered, N=32768 B=4 H=32 d=128", 32768),
+}
+VARIANTS = {"dense": 0, "naive": 1, "binblk": 2, "dense-binblk": 3}
 
 
-def make_config(name: str):
-    """BASELINE.json configs -> (mask, B, H, d, description). C2 is the headline workload."""
-    import paper_2409_15097_b200 as bbm
+def mask_words(name: str, generate, relabel, rcm, permute):
+    """The config's mask as reference-layout packed words, composed from four backends so both
+    arms build the identical mask: generate(spec, n) -> words, relabel(words, n, seed),
+    rcm(words, n) -> forward, permute(words, n, forward). Returns (words, rcm forward or None)."""
+    import numpy as np
 
+    n = CONFIGS[name][5]
     if name == "c1":
-        return bbm.gen_causal(1024), 1, 4, 64, "C1 causal B=1 H=4 N=1024 d=64"
+        return generate("causal", n), None
     if name == "c2":
-        return (bbm.gen_packed_sequential(alpaca_lengths(4096, 7)), 8, 32, 128,
-                "C2 packed-seq (ALPACA-like lengths U{64..512}, mt19937_64(7)) B=8 H=32 N=4096 d=128")
+        return generate("packed-seq[" + ";".join(str(x) for x in alpaca_lengths(n, 7)) + "]", 0), None
     if name == "c3":
         # causal prefix P=2048 + MEDUSA [16;15] tree: prefix rows causal, tree rows see the whole
         # prefix plus their ancestors (SURVEY §8d)
-        tree = bbm.gen_medusa([16, 15])
-        t = tree.size()
-        n = 2048 + t
-        m = bbm.Mask(n)
-        dense = m.to_dense()
-        import numpy as np
-
+        tree = generate("medusa[16;15]", 0)
+        t = tree.shape[0]
+        wpr = (n + 63) // 64
+        dense = np.zeros((n, wpr * 64), bool)
         dense[:2048, :2048] = np.tril(np.ones((2048, 2048), bool))
         dense[2048:, :2048] = True
-        dense[2048:, 2048:] = tree.to_dense()
-        return (bbm.Mask.from_dense(dense), 1, 32, 128,
-                f"C3 causal prefix 2048 + MEDUSA[16;15] tree (N={n}) B=1 H=32 d=128")
+        tb = np.unpackbits(tree.view(np.uint8), axis=1, bitorder="little")[:, :t].astype(bool)
+        dense[2048:, 2048:n] = tb
+        return np.packbits(dense, axis=1, bitorder="little").view(np.uint64).reshape(n, wpr), None
     if name == "c4":
-        return (bbm.gen_longformer_global(16384, 512, 128), 1, 16, 64,
-                "C4 Longformer window 512 + 128 global, N=16384 H=16 d=64")
+        return generate("global(w=512;g=128)", n), None
     if name == "c5":
-        base = bbm.gen_longformer_windowed(32768, 164)
-        shuffled = bbm.relabel(base, 3)
-        perm = bbm.rcm_order(shuffled)
-        RCM_PERM["c5"] = perm
-        return (bbm.permute_mask(shuffled, perm), 4, 32, 128,
-                "C5 1% band (w=164) relabelled by mt19937_64(3), RCM-reordered, N=32768 B=4 H=32 d=128")
+        shuffled = relabel(generate("windowed(w=164)", n), n, 3)
+        fwd = rcm(shuffled, n)
+        return permute(shuffled, n, fwd), fwd
     raise SystemExit(f"unknown config {name}")
 
 
-def executed_flops(prep, slots: int, d: int, variant: int) -> float:
-    """F = slots * sum over executed tiles of 4 * rows_in_block * cols_in_block * d,
-    at the kernel's 128x128 tiling (partial tiles count in full)."""
+def bbm_backends(bbm, device: int = 0):
+    """mask_words backends on this framework: host generators / relabel / RCM (libbbm host code)
+    and the device permute_mask kernel (K6)."""
+    def gen(spec, nn):
+        return bbm.generate(spec, nn).words
+
+    def relabel(w, nn, seed):
+        return bbm.relabel(bbm.Mask(nn, w), seed).words
+
+    def rcm(w, nn):
+        return bbm.rcm_order(bbm.Mask(nn, w)).forward
+
+    def permute(w, nn, f):
+        return bbm.permute_mask(bbm.Mask(nn, w), bbm.Permutation.from_forward(f), device=device).words
+
+    return gen, relabel, rcm, permute
+
+
+def make_config(name: str, device: int = 0):
+    """(Mask, B, H, d, description) of a config, built with this framework (tests, tools)."""
+    import paper_2409_15097_b200 as bbm
+
+    B, H, d, _, desc, n = CONFIGS[name]
+    words, _ = mask_words(name, *bbm_backends(bbm, device))
+    return bbm.Mask(n, words), B, H, d, desc
+
+
+def config_dict(name: str, variant: str, world: int, scaling: str) -> dict:
+    """The `config` object of the JSON line, identical in both arms."""
+    B, H, d, _, desc, n = CONFIGS[name]
+    slots = B * H
+    return {"workload": desc, "variant": variant, "batch": B, "heads": H, "seq_len": n, "head_dim": d,
+            "slots": slots, "tiles": "128x128",
+            "parallelism": (f"batch x heads sharded over {world} GPU(s), contiguous slot ranges (strong)"
+                            if scaling == "strong" else f"every GPU runs all {slots} slots (weak)"),
+            "l2": "inputs > 126 MB L2 (no flush)" if 3 * slots * n * d * 2 > 126e6
+            else "inputs < L2: steps back-to-back (L2 warm)"}
+
+
+def executed_area(cnt, lst, n: int, variant: int) -> float:
+    """sum over the kernel's executed 128x128 tiles of rows_in_block * cols_in_block
+    (partial tiles count in full); F = 4 * area * d per slot."""
     import numpy as np
 
-    n = prep.n_tokens
-    cnt, lst, _ = prep.kernel_lists()
     kr = cnt.size
     ext = np.minimum(128, n - np.arange(kr) * 128).astype(np.float64)
     if variant in (0, 1):  # dense / naive: every tile
-        area = float(ext.sum() ** 2)
-    else:
-        area = 0.0
-        for p in range(kr):
-            qs = lst[p, : cnt[p]] & 0x7FFFFFFF
-            area += ext[p] * float(ext[qs].sum())
-    return 4.0 * area * d * slots
+        return float(ext.sum() ** 2)
+    area = 0.0
+    for p in range(kr):
+        qs = lst[p, : cnt[p]] & 0x7FFFFFFF
+        area += ext[p] * float(ext[qs].sum())
+    return area
+
+
+def area_from_words(words, n: int, variant: int) -> float:
+    """The same figure from the mask alone (reference arm: the oracle's block sums)."""
+    import numpy as np
+
+    import oracle
+
+    sums = oracle.block_sums(words, n, 128, 128)
+    ext = np.minimum(128, n - np.arange(sums.shape[0]) * 128).astype(np.float64)
+    occ = sums > 0 if variant >= 2 else np.ones_like(sums, bool)
+    return float((np.outer(ext, ext) * occ).sum())
 
 
 def max_over_ranks(value: float, device=None) -> float:
@@ -123,6 +190,36 @@ def load_peaks():
         with open(path) as f:
             return json.load(f), "measured"
     return PEAKS_FALLBACK, "fallback"
+
+
+def cpu_info() -> dict:
+    """Host CPU model, physical cores and the threads this process may use."""
+    model, cores = None, set()
+    try:
+        phys = core = None
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                k, _, v = line.partition(":")
+                k, v = k.strip(), v.strip()
+                if k == "model name" and model is None:
+                    model = v
+                elif k == "physical id":
+                    phys = v
+                elif k == "core id":
+                    core = v
+                elif not k and phys is not None:
+                    cores.add((phys, core))
+                    phys = core = None
+            if phys is not None:
+                cores.add((phys, core))
+    except OSError:
+        pass
+    try:
+        usable = len(os.sched_getaffinity(0))
+    except AttributeError:
+        usable = os.cpu_count() or 1
+    return {"cpu_model": model, "physical_cores": len(cores) or None, "logical_cpus": os.cpu_count(),
+            "usable_threads": usable}
 
 
 class ClockSampler:
@@ -178,97 +275,121 @@ class ClockSampler:
             bits |= s[2]
         reasons = sorted({name for b, name in self.REASONS.items() if bits & b and name != "gpu_idle"})
         return {"sm_mhz": mhz, "sm_max_mhz": self.max_mhz, "reasons": reasons, "samples": len(inside),
-                "window": "soak + timed region (timed steps are sub-ms)"}
+                "window": "soak + timed region"}
 
 
-def cpu_reference_run(mask, slots_total, d, variant, budget_s, threads, min_slots=1):
-    """The reference's own CPU engine (blocked_forward<float>, engine.hpp:282-341, compiled from
-    the reference headers into oracle/_ref) over a bounded sample of the workload's slots.
-    Returns (seconds per slot, slots timed, preprocess ms)."""
-    import numpy as np
+# ----------------------------------------------------------------------------- reference arm
 
+def ref_mask(name: str):
+    """The config's mask built by the reference's own code (oracle/_ref = /root/reference headers
+    compiled in place): generators.hpp families, the shuffle relabel through reorder.hpp's
+    permute_mask, rcm_order(build_graph) and permute_mask."""
     import oracle
 
-    if not oracle.ref_available():
-        raise RuntimeError("oracle/_ref/libbbm_ref.so not built")
-    L = oracle.ref()
-    n = mask.size()
-    # one slot of make_problem-style inputs (values do not change the work: counters and tile
-    # walk depend on the mask only, engine.hpp:47-48)
-    q, k, v, _ = oracle.ref_make_problem_f32(1, 1, n, d)
-    words = np.ascontiguousarray(mask.words)
-    import ctypes as C
+    return mask_words(name, lambda spec, n: oracle.ref_generate(spec, n), oracle.ref_relabel,
+                      lambda w, n: oracle.ref_rcm(w, n)[0], oracle.ref_permute_mask)
 
-    h = L.ref_engine_create(words.ctypes.data_as(C.POINTER(C.c_uint64)), n, 128, 128,
-                            q.ctypes.data_as(C.POINTER(C.c_float)), k.ctypes.data_as(C.POINTER(C.c_float)),
-                            v.ctypes.data_as(C.POINTER(C.c_float)), 1, d)
-    try:
-        prepro_ms = L.ref_engine_preprocess_ms(h, 1)
-        L.ref_engine_forward(h, variant, threads, 1.0 / d ** 0.5)  # warm
+
+class RefEngine:
+    """The reference's blocked_forward<float> (engine.hpp:282-341) over one slot of make_problem
+    inputs, MaskPrep built once (ref_shim.cpp)."""
+
+    def __init__(self, words, n: int, d: int):
+        import ctypes as C
+
+        import numpy as np
+
+        import oracle
+
+        self.L = oracle.ref()
+        self.words = np.ascontiguousarray(words, dtype=np.uint64)
+        q, k, v, _ = oracle.ref_make_problem_f32(1, 1, n, d)
+        self.h = self.L.ref_engine_create(self.words.ctypes.data_as(C.POINTER(C.c_uint64)), n, 128, 128,
+                                          q.ctypes.data_as(C.POINTER(C.c_float)),
+                                          k.ctypes.data_as(C.POINTER(C.c_float)),
+                                          v.ctypes.data_as(C.POINTER(C.c_float)), 1, d)
+        self.scale = 1.0 / d ** 0.5
+
+    def preprocess_ms(self, reps: int = 1) -> float:
+        return self.L.ref_engine_preprocess_ms(self.h, reps)
+
+    def forward(self, variant: int, threads: int) -> float:
         t0 = time.perf_counter()
-        done = 0
-        while done < slots_total and (done < min_slots or time.perf_counter() - t0 < budget_s):
-            L.ref_engine_forward(h, variant, threads, 1.0 / d ** 0.5)
-            done += 1
-        el = time.perf_counter() - t0
-    finally:
-        L.ref_engine_destroy(h)
-    return el / done, done, prepro_ms
+        self.L.ref_engine_forward(self.h, variant, threads, self.scale)
+        return time.perf_counter() - t0
+
+    def close(self):
+        if self.h:
+            self.L.ref_engine_destroy(self.h)
+            self.h = None
+
+
+def cpu_sample(engine: RefEngine, variant: int, threads: int, budget_s: float, max_slots: int):
+    """Time one-slot forwards until `budget_s` (at least one); returns seconds per slot, slots."""
+    times = []
+    t0 = time.perf_counter()
+    while len(times) < max_slots and (not times or time.perf_counter() - t0 < budget_s):
+        times.append(engine.forward(variant, threads))
+    return statistics.median(times), len(times)
 
 
 def run_reference_arm(args):
-    """--impl reference: the reference CPU implementation on the host cores, rank 0 only."""
+    """--impl reference: the reference CPU implementation on the host cores, rank 0 only. One step
+    = blocked_forward<float> over ONE (batch, head) slot of the config (a bounded sample; the
+    value is a rate, TFLOP/s on the executed tiles, comparable with the GPU arm's)."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    mask, B, H, d, desc = make_config(args.config)
+    B, H, d, dvar, desc, n = CONFIGS[args.config]
+    variant_name = args.variant or dvar
+    variant = VARIANTS[variant_name]
+    t_setup = time.perf_counter()
+    words, _ = ref_mask(args.config)
+    flops_slot = 4.0 * area_from_words(words, n, variant) * d
+    info = cpu_info()
+    threads = info["usable_threads"]
+    eng = RefEngine(words, n, d)
+    setup_s = time.perf_counter() - t_setup
+    try:
+        for _ in range(args.warmup):
+            eng.forward(variant, threads)
+        step_s = [eng.forward(variant, threads) for _ in range(args.steps)]
+        pre_ms = eng.preprocess_ms(1)
+    finally:
+        eng.close()
+    ms_step = statistics.mean(step_s) * 1e3
+    value = flops_slot / (ms_step * 1e-3) / 1e12
     slots = B * H
-    variant = {"dense": 0, "naive": 1, "binblk": 2, "dense-binblk": 3}[args.variant]
-    import numpy as np  # noqa: F401
-
-    import paper_2409_15097_b200 as bbm
-
-    # executed-tile FLOPs from the mask alone (host oracle-free computation of the same figure)
-    sums = __import__("oracle").block_sums(mask.words, mask.size(), 128, 128)
-    n = mask.size()
-    ext = np.minimum(128, n - np.arange(sums.shape[0]) * 128).astype(np.float64)
-    occ = sums > 0 if variant >= 2 else np.ones_like(sums, bool)
-    flops_slot = 4.0 * float((np.outer(ext, ext) * occ).sum()) * d
-    threads = os.cpu_count() or 1
-    per_step_budget = max(2.0, 60.0 / max(1, args.steps + args.warmup))
-    for _ in range(args.warmup):
-        cpu_reference_run(mask, 1, d, variant, 0.0, threads)
-    times = []
-    sample_slots = []
-    for _ in range(args.steps):
-        sec_per_slot, done, _ = cpu_reference_run(mask, slots, d, variant, per_step_budget, threads)
-        times.append(sec_per_slot)
-        sample_slots.append(done)
-    sec_slot = statistics.median(times)
-    value = flops_slot / sec_slot / 1e12
-    ms_step = sec_slot * slots * 1e3
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f32 (fp64 accumulate)", "data": "synthetic",
-        "config": {"workload": desc, "variant": args.variant, "slots": slots, "tiles": "128x128",
-                   "extrapolated_from_slots_per_step": sample_slots},
+        "scaling": args.scaling, "vs_baseline": None, "dtype": "f32 (fp64 accumulate)",
+        "data": "synthetic (make_problem uniform[-1,1) inputs, bench.hpp:320-337)",
+        "config": config_dict(args.config, variant_name, args.gpus, args.scaling),
+        "sample": f"1 of {slots} slots per step (each step = one blocked_forward<float> call; "
+                  f"the whole config would take ~{slots * ms_step / 1e3:.1f} s per step)",
         "cpu_baseline": {"value": value, "unit": "TFLOP/s", "cores": threads, "kind": "reference",
-                         "sample": f"{min(sample_slots)}-{max(sample_slots)} of {slots} slots per step, "
-                                   f"blocked_forward<float> threads={threads}, ms_per_step extrapolated x{slots}"},
+                         "sample": f"1 slot per step x {args.steps} steps, blocked_forward<float> "
+                                   f"{variant_name} threads={threads}, 128x128 tiles", **info,
+                         "preprocess_ms": pre_ms, "setup_s": setup_s},
         "e2e": {"value": value, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
-    del bbm
 
+
+# ----------------------------------------------------------------------------- our arm
 
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "c4", "c5"])
-    ap.add_argument("--variant", default="binblk", choices=["dense", "naive", "binblk", "dense-binblk"])
+    ap.add_argument("--config", default="c5", choices=sorted(CONFIGS))
+    ap.add_argument("--variant", default=None, choices=sorted(VARIANTS),
+                    help="default: the config's own (dense-binblk for c4, binblk otherwise)")
+    ap.add_argument("--scaling", default="strong", choices=["strong", "weak"],
+                    help="strong: the config's B*H slots sharded over the ranks (default); "
+                         "weak: every rank runs all of them")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -296,26 +417,46 @@ def main():
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
 
-    mask, B, H, d, desc = make_config(args.config)
-    slots = B * H
-    n = mask.size()
-    variant = bbm.parse_variant(args.variant)
+    B, H, d, dvar, desc, n = CONFIGS[args.config]
+    variant_name = args.variant or dvar
+    variant = bbm.parse_variant(variant_name)
     scale = 1.0 / d ** 0.5
+    slots_total = B * H
+    if args.scaling == "strong":
+        s0, s1 = bbm.shard_slots(slots_total, world, rank)
+    else:
+        s0, s1 = 0, slots_total
+    slots = s1 - s0
+    stream = torch.cuda.current_stream(dev)
 
-    # metadata: built once per GPU from the dense bool mask on the device (K1+K2+lists+bitmaps),
-    # exactly as shared by every slot (engine.hpp:68-70)
-    dense_mask = torch.from_numpy(mask.to_dense()).to(dev)
-    prep = bbm.preprocess_mask(dense_mask, bbm.BlockSpec(128, 128), device=local)
-    flops = executed_flops(prep, slots, d, int(variant))
-    dense_flops = executed_flops(prep, slots, d, 0)
+    # ---- metadata: rank 0 builds the mask and its prep on its GPU (K1 pack + K2 lists + K3
+    # bitmaps from the dense bool mask), the other ranks import it peer to peer
+    dense_mask = fwd_perm = None
+    t_setup = time.perf_counter()
+    if rank == 0:
+        words, fwd_perm = mask_words(args.config, *bbm_backends(bbm, local))
+        mask = bbm.Mask(n, words)
+        dense_mask = torch.from_numpy(mask.to_dense()).to(dev)
+        prep = bbm.preprocess_mask(dense_mask, bbm.BlockSpec(128, 128), device=local)
+    if world > 1:
+        blob = [prep.export_ipc() if rank == 0 else None]
+        dist.broadcast_object_list(blob, src=0)
+        if rank != 0:
+            prep = bbm.import_prep_ipc(blob[0], local)
+        dist.barrier()  # every importer has copied the arena before rank 0 may touch its prep
+    setup_s = time.perf_counter() - t_setup
+    cnt, lst, _ = prep.kernel_lists()
+    area = executed_area(cnt, lst, n, int(variant))
+    flops = 4.0 * area * d * slots
+    dense_flops = 4.0 * executed_area(cnt, lst, n, 0) * d * slots
+    total_flops = 4.0 * area * d * (slots_total if args.scaling == "strong" else slots_total * world)
 
-    # inputs: this rank's slots of the virtual global batch, uniform[-1,1) bf16, resident in HBM
-    g = torch.Generator(device=dev).manual_seed(1234 + rank)
+    # ---- inputs: this rank's slots, uniform[-1,1) bf16, resident in HBM
+    g = torch.Generator(device=dev).manual_seed(1234 + s0 + (rank if args.scaling == "weak" else 0))
     q, k, v = ((torch.rand((slots, n, d), generator=g, device=dev) * 2 - 1).to(torch.bfloat16) for _ in range(3))
     out = torch.empty_like(q)
     rmax = torch.empty((slots, n), dtype=torch.float32, device=dev)
     rsum = torch.empty((slots, n), dtype=torch.float32, device=dev)
-    stream = torch.cuda.current_stream(dev)
 
     def step(var=variant):
         bbm.attn_fwd_device(prep, var, q, k, v, out, rmax, rsum, scale, stream.cuda_stream)
@@ -333,6 +474,7 @@ def main():
             fwd_outs[var] = (o_, m_, l_)
         flops *= 2.5
         dense_flops *= 2.5
+        total_flops *= 2.5
 
         def step(var=variant):  # noqa: F811
             o_, m_, l_ = fwd_outs[int(var)]
@@ -343,10 +485,10 @@ def main():
     torch.cuda.synchronize()
 
     sampler = ClockSampler(local).start()
-    # soak so the sampled clocks reflect the loaded state (timed steps alone are sub-ms)
+    # soak so the sampled clocks reflect the loaded state (short steps alone are sub-ms)
     t_soak = time.perf_counter()
     while time.perf_counter() - t_soak < (0.05 if args.profile else 0.4):
-        for _ in range(20):
+        for _ in range(5):
             step()
         torch.cuda.synchronize()
 
@@ -368,13 +510,13 @@ def main():
     if world > 1:
         dist.barrier()
     t1 = time.perf_counter()
-    sampler.stop()
     elapsed_ms = start_all.elapsed_time(end_all)
     launch_ms = [a.elapsed_time(b) for a, b in ev]
     elapsed_ms = max_over_ranks(elapsed_ms, dev)
     ms_step = elapsed_ms / args.steps
-    value = world * flops / (ms_step * 1e-3) / 1e12
+    value = total_flops / (ms_step * 1e-3) / 1e12
     if args.profile:
+        sampler.stop()
         if rank == 0:
             print(json.dumps({"profile_run": True, "ms_per_step": ms_step, "value": value}))
         if world > 1:
@@ -382,10 +524,18 @@ def main():
         return
 
     extras = {}
+    # e2e through the reference-facing host-buffer C ABI, every rank on its own shard, max over
+    # ranks (collective timing only)
+    if not args.no_e2e and args.which == "fwd":
+        extras.update(e2e_all(bbm, prep, variant, q, k, v, slots, n, d, scale, total_flops, args,
+                              fwd_perm, dev, world))
+    sampler.stop()
     if rank == 0:
         peaks, peak_kind = load_peaks()
         avg_launch = statistics.mean(launch_ms)
         bytes_alg = 4.0 * slots * n * d * 2  # Q, K, V read + O written once (bf16)
+        if args.which == "bwd":
+            bytes_alg = 8.0 * slots * n * d * 2  # q k v o dO in, dq dk dv out
         t_tensor = flops / (peaks["bf16_tflops"] * 1e12)
         t_hbm = bytes_alg / (peaks["hbm_gbs"] * 1e9)
         if t_hbm > t_tensor:
@@ -396,16 +546,17 @@ def main():
         tpath = os.path.join(ROOT, "profiles", "traffic.json")
         if os.path.exists(tpath):
             with open(tpath) as f:
-                tr = json.load(f).get(f"{args.config}/{args.variant}")
-            if tr:
+                tr = json.load(f).get(f"{args.config}/{variant_name}/{args.which}")
+            if tr and tr.get("slots") == slots:
                 traffic = tr.get("dram_bytes_per_launch")
         extras["roofline"] = {
             "bound": bound, "achieved": achieved, "peak": peak, "unit": unit, "frac": achieved / peak,
             "traffic": traffic, "peak_source": f"{peak_kind} (MEASURED_PEAKS.json burst)",
+            "kernel": "attn_fwd_kernel" if args.which == "fwd" else "attn_bwd_kernel (dq + dkdv)",
             "algorithmic_bytes_per_launch": bytes_alg, "flops_per_launch": flops,
             "tensor_frac": (flops / (avg_launch * 1e-3) / 1e12) / peaks["bf16_tflops"],
             "hbm_frac": (bytes_alg / (avg_launch * 1e-3) / 1e9) / peaks["hbm_gbs"],
-            "avg_launch_ms": avg_launch,
+            "avg_launch_ms": avg_launch, "slots_per_launch": slots,
         }
         # dense-mask run of the same kernel (all tiles, no mask reads)
         for _ in range(2):
@@ -420,58 +571,41 @@ def main():
         torch.cuda.synchronize()
         dense_ms = e0.elapsed_time(e1) / reps
         extras["dense_mask_run"] = {"ms_per_step": dense_ms, "tflops": dense_flops / (dense_ms * 1e-3) / 1e12,
-                                    "speedup_vs_dense": dense_ms / ms_step,
+                                    "speedup_vs_dense": dense_ms / (avg_launch if world > 1 else ms_step),
                                     "ideal_speedup_by_tiles": dense_flops / flops}
-        # preprocessor: per-batch rebuild of the kernel metadata from the dense bool mask
-        if args.which == "bwd":
-            args.no_e2e = args.no_cpu_baseline = True
-        for _ in range(3):
-            prep_update(prep, dense_mask, stream)
-        torch.cuda.synchronize()
-        e0.record(stream)
-        reps = 20
-        for _ in range(reps):
-            prep_update(prep, dense_mask, stream)
-        e1.record(stream)
-        torch.cuda.synchronize()
-        pre_ms = e0.elapsed_time(e1) / reps
-        extras["preprocess"] = {"ms": pre_ms, "input": f"dense bool mask {n}x{n} on device",
-                                "gbs_bool_read": n * n / (pre_ms * 1e-3) / 1e9,
-                                "kernels": "pack_bool_sums128 + rowmeta + compact_bitmaps + finalize"}
-        # e2e: the same forward through the host-buffer C ABI call, H2D + D2H inside the region
-        if not args.no_e2e:
-            extras["e2e"] = e2e_measure(prep, variant, q, k, v, slots, n, d, scale, flops, args.steps)
-            if args.config in RCM_PERM:  # the whole reordered pipeline from original-order buffers
-                extras["e2e_rcm"] = e2e_measure(prep, variant, q, k, v, slots, n, d, scale, flops, args.steps,
-                                                forward=RCM_PERM[args.config].forward)
-        if not args.no_cpu_baseline and world == 1:
+        if args.which == "fwd":
+            extras["preprocess"] = preprocess_measure(bbm, prep, dense_mask, stream, n, step, ms_step)
+        if not args.no_cpu_baseline and world == 1 and args.which == "fwd":
             try:
-                threads = os.cpu_count() or 1
-                sec_slot, done, ref_pre_ms = cpu_reference_run(mask, slots, d, int(variant), 15.0, threads)
-                cpu_val = (flops / slots) / sec_slot / 1e12
+                info = cpu_info()
+                threads = info["usable_threads"]
+                eng = RefEngine(mask.words, n, d)
+                try:
+                    eng.forward(int(variant), threads)  # warm
+                    sec_slot, done = cpu_sample(eng, int(variant), threads, 15.0, slots)
+                    ref_pre_ms = eng.preprocess_ms(1)
+                finally:
+                    eng.close()
                 extras["cpu_baseline"] = {
-                    "value": cpu_val, "unit": "TFLOP/s", "cores": threads, "kind": "reference",
-                    "sample": f"{done} of {slots} slots (one slot's inputs re-run), reference "
-                              f"blocked_forward<float> {args.variant} threads={threads}, 128x128 tiles",
-                    "ms_per_step_extrapolated": sec_slot * slots * 1e3,
-                    "preprocess_ms_reference": ref_pre_ms,
+                    "value": (flops / slots) / sec_slot / 1e12, "unit": "TFLOP/s", "cores": threads,
+                    "kind": "reference",
+                    "sample": f"{done} one-slot blocked_forward<float> calls (~15 s), {variant_name}, "
+                              f"threads={threads}, 128x128 tiles; whole config ~{sec_slot * slots:.1f} s",
+                    **info, "preprocess_ms_reference": ref_pre_ms,
                 }
             except Exception as e:  # noqa: BLE001
                 extras["cpu_baseline"] = {"value": None, "unavailable": str(e)}
         extras["clocks"] = sampler.summary(t_soak, t1)
+        extras["setup_s"] = setup_s
 
     if rank == 0:
         line = {
             "metric": METRIC if args.which == "fwd" else METRIC.replace("fwd", "bwd (5-GEMM FLOPs)"),
             "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": args.scaling,
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic (uniform[-1,1) bf16 inputs)",
-            "config": {"workload": desc, "variant": args.variant, "batch": B, "heads": H, "seq_len": n,
-                       "head_dim": d, "slots_per_gpu": slots, "global_slots": slots * world,
-                       "tiles": "128x128", "parallelism": f"slot shards x{world} (weak)",
-                       "l2": "inputs > 126 MB L2 (no flush)" if 3 * slots * n * d * 2 > 126e6
-                       else "inputs < L2: steps back-to-back (L2 warm)"},
-            "gpu_launches": args.steps,
+            "config": config_dict(args.config, variant_name, world, args.scaling),
+            "gpu_launches": args.steps * (1 if args.which == "fwd" else 3),
         }
         line.update(extras)
         print(json.dumps(line), flush=True)
@@ -479,62 +613,127 @@ def main():
         dist.destroy_process_group()
 
 
-def prep_update(prep, dense_mask, stream):
+def preprocess_measure(bbm, prep, dense_mask, stream, n, step, fwd_ms):
+    """The per-batch path: bbm_prep_update_bool_device rebuilds the prep from a dense bool mask on
+    the device (pack + sums + lists + bitmaps + order, no host round trip); then the same with
+    a forward after every update, alternating two different masks (the forward re-plans on the
+    device for each new mask version)."""
+    import torch
+
+    reps = 20
+    for _ in range(3):
+        prep.update(dense_mask, stream.cuda_stream)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(reps):
+        prep.update(dense_mask, stream.cuda_stream)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    pre_ms = e0.elapsed_time(e1) / reps
+    # a second mask of the same size: the first one's transpose (same density, other lists)
+    other = dense_mask.t().contiguous()
+    masks = [other, dense_mask]
+    prep.update(other, stream.cuda_stream)
+    step()
+    torch.cuda.synchronize()
+    e0.record(stream)
+    for i in range(reps):
+        prep.update(masks[i % 2], stream.cuda_stream)
+        step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    both_ms = e0.elapsed_time(e1) / reps
+    del other
+    return {"ms": pre_ms, "input": f"dense bool mask {n}x{n} on device",
+            "gbs_bool_read": n * n / (pre_ms * 1e-3) / 1e9,
+            "update_plus_forward_ms": both_ms, "forward_ms": fwd_ms,
+            "update_plus_forward_note": "fresh mask every step (alternating the mask and its transpose); "
+                                        "the forward's launch plan is rebuilt on the device each time"}
+
+
+def e2e_all(bbm, prep, variant, q, k, v, slots, n, d, scale, total_flops, args, fwd_perm, dev, world):
+    """e2e through the reference-facing host-buffer C ABI: Q/K/V from pinned host memory, H2D,
+    the kernel and D2H of O and the row statistics inside the timed call, every step.
+
+    e2e      bbm_run_attention_host_f32: the reference's own types (run_attention<float>,
+             engine.hpp:489-505): per-slot Matrix<float> buffers in, float out, double row stats
+    e2e_bf16 bbm_attn_fwd_host_bf16: bf16 host buffers (half the PCIe bytes)
+    e2e_rcm  (C5) the reordered pipeline from ORIGINAL-order bf16 buffers (device gather/scatter)
+    Times are max over ranks."""
     import ctypes as C
 
-    from paper_2409_15097_b200 import _lib
-
-    _lib.check(_lib.lib.bbm_prep_update_bool_device(prep.handle.h, C.c_void_p(dense_mask.data_ptr()),
-                                                     dense_mask.stride(0), C.c_void_p(stream.cuda_stream)))
-
-
-def e2e_measure(prep, variant, q, k, v, slots, n, d, scale, flops, steps, forward=None):
-    """bbm_attn_fwd_host_bf16 with pinned host buffers: H2D of Q/K/V, the kernel, D2H of O and the
-    row statistics, all inside the timed call. With `forward` (an RCM permutation), the
-    reordered pipeline bbm_attn_fwd_rcm_host_bf16 instead: original-order buffers, the device
-    gathers / scatters rows around the kernel."""
-    import ctypes as C
-
+    import numpy as np
     import torch
 
     from paper_2409_15097_b200 import _lib
 
-    hq, hk, hv = (t.cpu().pin_memory() for t in (q, k, v))
-    ho = torch.empty_like(hq).pin_memory()
-    hmax = torch.empty((slots, n), dtype=torch.float32).pin_memory()
-    hsum = torch.empty((slots, n), dtype=torch.float32).pin_memory()
+    reps = max(3, min(args.steps, 5))
+    res = {}
 
-    import numpy as np
-
-    fwd = None if forward is None else np.ascontiguousarray(forward, dtype=np.uint32)
-
-    def call():
-        u16 = C.POINTER(C.c_uint16)
-        f32 = C.POINTER(C.c_float)
-        if fwd is not None:
-            _lib.check(_lib.lib.bbm_attn_fwd_rcm_host_bf16(
-                prep.handle.h, int(variant), fwd.ctypes.data_as(C.POINTER(C.c_uint32)),
-                C.cast(hq.data_ptr(), u16), C.cast(hk.data_ptr(), u16), C.cast(hv.data_ptr(), u16),
-                C.cast(ho.data_ptr(), u16), C.cast(hmax.data_ptr(), f32), C.cast(hsum.data_ptr(), f32),
-                slots, d, scale))
-            return
-        _lib.check(_lib.lib.bbm_attn_fwd_host_bf16(
-            prep.handle.h, int(variant), C.cast(hq.data_ptr(), u16), C.cast(hk.data_ptr(), u16),
-            C.cast(hv.data_ptr(), u16), C.cast(ho.data_ptr(), u16), C.cast(hmax.data_ptr(), f32),
-            C.cast(hsum.data_ptr(), f32), slots, d, scale))
-
-    call()
-    reps = max(3, min(steps, 10))
-    t0 = time.perf_counter()
-    for _ in range(reps):
+    def timed(call):
         call()
-    ms = (time.perf_counter() - t0) / reps * 1e3
-    h2d = 3 * slots * n * d * 2
-    d2h = slots * n * d * 2 + 2 * slots * n * 4
-    return {"value": flops / (ms * 1e-3) / 1e12, "unit": "TFLOP/s", "ms_per_step": ms,
-            "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-            "path": ("bbm_attn_fwd_rcm_host_bf16 (original token order; device gather/scatter)" if fwd is not None
-                     else "bbm_attn_fwd_host_bf16") + " (C ABI, pinned host buffers, synchronous)"}
+        torch.cuda.synchronize()
+        if world > 1:
+            torch.distributed.barrier()
+        t0 = time.perf_counter()
+        for _ in range(reps):
+            call()
+        ms = (time.perf_counter() - t0) / reps * 1e3
+        return max_over_ranks(ms, dev)
+
+    # f32 per-slot (the reference signature)
+    hq, hk, hv = (t.float().cpu().pin_memory() for t in (q, k, v))
+    ho = torch.empty((slots, n, d), dtype=torch.float32).pin_memory()
+    hm = torch.empty((slots, n), dtype=torch.float64).pin_memory()
+    hs = torch.empty((slots, n), dtype=torch.float64).pin_memory()
+    arr = lambda t, per: (C.c_void_p * slots)(*[t.data_ptr() + i * per for i in range(slots)])  # noqa: E731
+    pq, pk, pv, po = (arr(t, n * d * 4) for t in (hq, hk, hv, ho))
+    pm, ps = arr(hm, n * 8), arr(hs, n * 8)
+
+    def call_f32():
+        _lib.check(_lib.lib.bbm_run_attention_host_f32(prep.handle.h, int(variant), pq, pk, pv, po, pm, ps,
+                                                       slots, d, scale))
+
+    ms = timed(call_f32)
+    res["e2e"] = {"value": total_flops / (ms * 1e-3) / 1e12, "unit": "TFLOP/s", "ms_per_step": ms,
+                  "h2d_bytes_per_step": 3 * slots * n * d * 4,
+                  "d2h_bytes_per_step": slots * n * d * 4 + 2 * slots * n * 8,
+                  "path": "bbm_run_attention_host_f32 (C ABI of run_attention<float>: per-slot float host "
+                          "buffers, pinned; f32->bf16 + finiteness check on the device; float out, double "
+                          "row stats; synchronous)"}
+    del hq, hk, hv, ho, hm, hs
+
+    u16 = C.POINTER(C.c_uint16)
+    f32 = C.POINTER(C.c_float)
+    bq, bk, bv = (t.cpu().pin_memory() for t in (q, k, v))
+    bo = torch.empty_like(bq).pin_memory()
+    bm = torch.empty((slots, n), dtype=torch.float32).pin_memory()
+    bs = torch.empty((slots, n), dtype=torch.float32).pin_memory()
+    ptrs = [C.cast(t.data_ptr(), u16) for t in (bq, bk, bv, bo)] + [C.cast(t.data_ptr(), f32) for t in (bm, bs)]
+
+    def call_bf16():
+        _lib.check(_lib.lib.bbm_attn_fwd_host_bf16(prep.handle.h, int(variant), *ptrs, slots, d, scale))
+
+    ms = timed(call_bf16)
+    h2d, d2h = 3 * slots * n * d * 2, slots * n * d * 2 + 2 * slots * n * 4
+    res["e2e_bf16"] = {"value": total_flops / (ms * 1e-3) / 1e12, "unit": "TFLOP/s", "ms_per_step": ms,
+                       "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                       "path": "bbm_attn_fwd_host_bf16 (pinned bf16 host buffers, synchronous)"}
+    if fwd_perm is not None and world == 1:
+        fwd = np.ascontiguousarray(fwd_perm, dtype=np.uint32)
+
+        def call_rcm():
+            _lib.check(_lib.lib.bbm_attn_fwd_rcm_host_bf16(prep.handle.h, int(variant),
+                                                           fwd.ctypes.data_as(C.POINTER(C.c_uint32)), *ptrs,
+                                                           slots, d, scale))
+
+        ms = timed(call_rcm)
+        res["e2e_rcm"] = {"value": total_flops / (ms * 1e-3) / 1e12, "unit": "TFLOP/s", "ms_per_step": ms,
+                          "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                          "path": "bbm_attn_fwd_rcm_host_bf16 (original token order; RCM gather/scatter "
+                                  "on the device)"}
+    return res
 
 
 if __name__ == "__main__":

@@ -25,7 +25,7 @@
 extern "C" {
 #endif
 
-#define BBM_ABI_VERSION 1
+#define BBM_ABI_VERSION 2
 
 typedef enum {
   BBM_OK = 0,
@@ -70,7 +70,11 @@ typedef struct {
 } bbm_prep_info;
 
 /* Opaque MaskPrep (engine.hpp:71-78): host copies of sums/occupancy/runs/stats plus the
- * device-resident kernel metadata (compacted tile lists, tile-major partial bitmaps). */
+ * device-resident kernel metadata (compacted tile lists, tile-major partial bitmaps).
+ * Like the reference's MaskPrep ("built once and shared across heads, runs and both passes",
+ * engine.hpp:68-70) a prep may be used from any number of threads and streams concurrently:
+ * everything a launch mutates (work counters, split-KV workspace, launch plans) is private to the
+ * launching stream. */
 typedef struct bbm_prep_s* bbm_prep;
 
 int bbm_abi_version(void);
@@ -88,10 +92,13 @@ bbm_status bbm_preprocess_packed_device(const uint64_t* d_words, uint64_t n, uin
 bbm_status bbm_preprocess_bool_device(const uint8_t* d_mask, uint64_t n, uint64_t row_stride,
                                       uint64_t block_i, uint64_t block_j, void* stream,
                                       bbm_prep* out);
-/* Rebuild the KERNEL view (128x128 sums, tile lists, LPT order, partial-tile bitmaps) of an
- * existing prep from a new mask of the same n, fully asynchronously on `stream` (no host
- * copies, no allocation): the per-batch path when every batch packs different sequences. The
- * caller-spec host metadata (sums/occupancy/runs/stats getters) is NOT refreshed. */
+/* Rebuild an existing prep for a new mask of the same n (the per-batch path when every batch
+ * packs different sequences), fully asynchronously on `stream`: no host copies, no allocation.
+ * The update is ordered after every launch already queued on the prep (any stream), and every
+ * later launch (any stream) is ordered after the update; launch plans are rebuilt on the device.
+ * The caller-spec metadata (sums/occupancy/runs/stats getters, counters, info) is recomputed on
+ * the next getter call (one synchronization there), and replicas made for the multi-GPU driver
+ * are dropped and re-made from the new mask on their next use. */
 bbm_status bbm_prep_update_bool_device(bbm_prep prep, const uint8_t* d_mask, uint64_t row_stride,
                                        void* stream);
 bbm_status bbm_prep_update_packed_device(bbm_prep prep, const uint64_t* d_words, void* stream);
@@ -119,8 +126,16 @@ bbm_status bbm_sums_metadata(const uint32_t* sums, uint64_t n, uint64_t block_i,
                              int device, uint8_t* occ, uint32_t* offset, uint32_t* total_ones,
                              bbm_block_stats* stats);
 /* Peer-to-peer copy of the device metadata to another GPU (NVLink), for the multi-GPU driver.
- * The result is an independent prep bound to `device`. */
+ * The result is an independent prep bound to `device`. The kernel view is one device arena, so
+ * this is one cudaMemcpyPeerAsync. */
 bbm_status bbm_prep_replicate(bbm_prep prep, int device, void* stream, bbm_prep* out);
+/* The same replication across processes (one process per GPU): export writes a flat blob (the
+ * arena's cudaIpcMemHandle + the host metadata; blob == NULL queries *size), import opens the
+ * handle on `device`, copies the arena peer to peer and returns an independent prep. The exporting
+ * prep must stay alive and un-updated until every importer has returned. */
+bbm_status bbm_prep_export_ipc(bbm_prep prep, void* blob, size_t* size);
+bbm_status bbm_prep_import_ipc(const void* blob, size_t size, int device, void* stream,
+                               bbm_prep* out);
 
 /* ---- blocked_forward (engine.hpp:282-341) over `slots` independent (batch, head) slots that
  *      share one mask (run_attention, engine.hpp:489-505). Device pointers, bf16 [slots][n][d];
@@ -131,7 +146,7 @@ bbm_status bbm_attn_fwd(bbm_prep prep, int variant, const void* q, const void* k
                         uint32_t head_dim, double scale, void* stream);
 
 /* Same, host buffers (bf16 bits as uint16): copies in, runs, copies out, synchronizes.
- * Pinned buffers get full PCIe bandwidth. */
+ * Pinned buffers get full PCIe bandwidth. Validates finiteness (engine.hpp:237-258). */
 bbm_status bbm_attn_fwd_host_bf16(bbm_prep prep, int variant, const uint16_t* q,
                                   const uint16_t* k, const uint16_t* v, uint16_t* out,
                                   float* row_max, float* row_sum, uint64_t slots,
@@ -149,16 +164,25 @@ bbm_status bbm_attn_fwd_rcm_host_bf16(bbm_prep prep, int variant, const uint32_t
 
 /* Same, float host buffers (the reference's Matrix<float> storage, matrix.hpp:14-45); inputs
  * rounded to bf16 (RNE) on the device, output widened back to float; row stats as double.
- * Validates finiteness like validate_forward_args (engine.hpp:244-258). */
+ * Validates finiteness like validate_forward_args (engine.hpp:244-258). Copy/compute pipeline
+ * over slot chunks, like the bf16 form. */
 bbm_status bbm_attn_fwd_host_f32(bbm_prep prep, int variant, const float* q, const float* k,
                                  const float* v, float* out, double* row_max, double* row_sum,
                                  uint64_t slots, uint32_t head_dim, double scale);
+/* run_attention<float> (engine.hpp:489-505) with the reference's per-slot storage: slot i's
+ * Matrix<float> q/k/v (n x d, row-major) at q[i]/k[i]/v[i], ForwardResult<float>::out at out[i]
+ * and its double row_max / row_sum at row_max[i] / row_sum[i] (the arrays may be NULL). */
+bbm_status bbm_run_attention_host_f32(bbm_prep prep, int variant, const float* const* q,
+                                      const float* const* k, const float* const* v,
+                                      float* const* out, double* const* row_max,
+                                      double* const* row_sum, uint64_t slots, uint32_t head_dim,
+                                      double scale);
 
 /* ---- blocked_backward (engine.hpp:346-471): dq, dk, dv of L = sum(out * d_out) from the forward's
  *      saved row statistics (row_max / row_sum as bbm_attn_fwd returns them), over the same tiles
  *      the forward processed. Deterministic (no atomics on gradients). Device pointers, bf16
- *      [slots][n][d]; asynchronous on `stream`. The first call on a prep builds its column view
- *      (column tile lists + transposed partial-tile bitmaps), which needs one host sync. ---- */
+ *      [slots][n][d]; asynchronous on `stream`. The first call after each mask version builds
+ *      the column view (column tile lists + transposed partial-tile bitmaps) on the device. ---- */
 bbm_status bbm_attn_bwd(bbm_prep prep, int variant, const void* q, const void* k, const void* v,
                         const void* out, const float* row_max, const float* row_sum,
                         const void* d_out, void* dq, void* dk, void* dv, uint64_t slots,

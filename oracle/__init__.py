@@ -110,6 +110,7 @@ def ref():
                                          f64p, f64p, f64p, f64p]
         L.ref_rcm.argtypes = [u64p, C.c_uint64, u32p, u64p, u64p]
         L.ref_permute_mask.argtypes = [u64p, C.c_uint64, u32p, u64p]
+        L.ref_relabel.argtypes = [u64p, C.c_uint64, C.c_uint64, u64p]
         L.ref_make_problem_f32.argtypes = [C.c_uint64] * 4 + [f32p] * 4
         _ref = L
     return _ref
@@ -314,3 +315,20 @@ def ref_make_problem_f32(seed, slots, n, d):
     arrs = [np.empty((slots, n, d), np.float32) for _ in range(4)]
     ref().ref_make_problem_f32(seed, slots, n, d, *[_p(a, C.c_float) for a in arrs])
     return tuple(arrs)
+
+
+def ref_permute_mask(words, n, fwd):
+    """The reference's permute_mask (reorder.hpp:156-163): out(a, b) = mask(fwd[a], fwd[b])."""
+    w = np.ascontiguousarray(words, dtype=np.uint64)
+    f = np.ascontiguousarray(fwd, dtype=np.uint32)
+    out = np.zeros_like(w)
+    _check_ref(ref().ref_permute_mask(_p(w, C.c_uint64), n, _p(f, C.c_uint32), _p(out, C.c_uint64)))
+    return out
+
+
+def ref_relabel(words, n, seed):
+    """Config 5's shuffle relabelling through the reference's permute_mask (ref_shim.cpp)."""
+    w = np.ascontiguousarray(words, dtype=np.uint64)
+    out = np.zeros_like(w)
+    _check_ref(ref().ref_relabel(_p(w, C.c_uint64), n, seed, _p(out, C.c_uint64)))
+    return out

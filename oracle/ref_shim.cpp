@@ -236,6 +236,22 @@ int ref_permute_mask(const uint64_t* words, uint64_t n, const uint32_t* forward,
   });
 }
 
+// The bench's config-5 relabelling, expressed with the reference's own permute_mask
+// (reorder.hpp:156-163): labels = std::shuffle(iota, mt19937_64(seed)), out(label[i], label[j]) =
+// mask(i, j), i.e. permute_mask with forward = labels^-1.
+int ref_relabel(const uint64_t* words, uint64_t n, uint64_t seed, uint64_t* out) {
+  return guarded([&] {
+    std::vector<uint32_t> labels(n);
+    for (uint64_t i = 0; i < n; ++i) labels[i] = static_cast<uint32_t>(i);
+    std::mt19937_64 gen(seed);
+    std::shuffle(labels.begin(), labels.end(), gen);
+    std::vector<uint32_t> fwd(n);
+    for (uint64_t i = 0; i < n; ++i) fwd[labels[i]] = static_cast<uint32_t>(i);
+    const Mask m = mask_from_words(words, n);
+    words_from_mask(permute_mask(m, Permutation::from_forward(fwd)), out);
+  });
+}
+
 // make_problem (bench.hpp:320-337) as float, the engine's single-precision inputs.
 void ref_make_problem_f32(uint64_t seed, uint64_t slots, uint64_t n, uint64_t d, float* q,
                           float* k, float* v, float* d_out) {

@@ -70,6 +70,8 @@ SIGNATURES = {
     "bbm_prep_get_kernel_lists": (C.c_int, [vp, u32p, u32p, u32p]),
     "bbm_prep_counters": (C.c_int, [vp, C.c_int, C.c_uint64, C.POINTER(CountersC)]),
     "bbm_prep_replicate": (C.c_int, [vp, C.c_int, vp, C.POINTER(vp)]),
+    "bbm_prep_export_ipc": (C.c_int, [vp, vp, C.POINTER(C.c_size_t)]),
+    "bbm_prep_import_ipc": (C.c_int, [vp, C.c_size_t, C.c_int, vp, C.POINTER(vp)]),
     "bbm_sums_metadata": (C.c_int, [u32p, C.c_uint64, C.c_uint64, C.c_uint64, C.c_int, u8p, u32p, u32p, C.POINTER(BlockStatsC)]),
     "bbm_attn_bwd": (C.c_int, [vp, C.c_int, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, C.c_uint64, C.c_uint32, C.c_double, vp]),
     "bbm_attn_bwd_host_f32": (C.c_int, [vp, C.c_int, f32p, f32p, f32p, f32p, f64p, f64p, f32p, f32p, f32p, f32p, C.c_uint64, C.c_uint32, C.c_double]),
@@ -80,6 +82,8 @@ SIGNATURES = {
     "bbm_attn_fwd_host_bf16": (C.c_int, [vp, C.c_int, u16p, u16p, u16p, u16p, f32p, f32p, C.c_uint64, C.c_uint32, C.c_double]),
     "bbm_attn_fwd_rcm_host_bf16": (C.c_int, [vp, C.c_int, u32p, u16p, u16p, u16p, u16p, f32p, f32p, C.c_uint64, C.c_uint32, C.c_double]),
     "bbm_attn_fwd_host_f32": (C.c_int, [vp, C.c_int, f32p, f32p, f32p, f32p, f64p, f64p, C.c_uint64, C.c_uint32, C.c_double]),
+    "bbm_run_attention_host_f32": (C.c_int, [vp, C.c_int, C.POINTER(vp), C.POINTER(vp), C.POINTER(vp), C.POINTER(vp),
+                                             C.POINTER(vp), C.POINTER(vp), C.c_uint64, C.c_uint32, C.c_double]),
     "bbm_run_attention_multi": (C.c_int, [vp, C.c_int, C.c_int, C.POINTER(C.c_int), u16p, u16p, u16p, u16p, f32p, f32p, C.c_uint64, C.c_uint32, C.c_double, f64p]),
     "bbm_set_trace": (C.c_int, [vp, C.c_uint32]),
     "bbm_rcm_order": (C.c_int, [u64p, C.c_uint64, u32p]),

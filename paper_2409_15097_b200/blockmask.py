@@ -239,16 +239,61 @@ class _PrepHandle:
             self.h = None
 
 
-@dataclass
 class MaskPrep:
-    """engine.hpp:71-78 plus the device-resident kernel metadata (``handle``)."""
-    n_tokens: int
-    spec: BlockSpec
-    sums: BlockSums
-    occupancy: BlockOccupancy
-    runs: DenseRuns
-    stats: BlockStats
-    handle: _PrepHandle = field(repr=False)
+    """engine.hpp:71-78 plus the device-resident kernel metadata (``handle``).
+
+    The host-side fields (``sums``, ``occupancy``, ``runs``, ``stats``) are read from the C ABI,
+    which recomputes them after :meth:`update` (a new mask of the same size, rebuilt on the device
+    without a host round trip); they are cached per update."""
+
+    def __init__(self, handle: _PrepHandle):
+        self.handle = handle
+        self._version = 0
+        self._cache = {}
+        info = self.info()
+        self.n_tokens = int(info.n)
+        self.spec = BlockSpec(int(info.block_i), int(info.block_j))
+
+    def __repr__(self) -> str:
+        return f"MaskPrep(n_tokens={self.n_tokens}, spec={self.spec})"
+
+    def _host(self):
+        got = self._cache.get(self._version)
+        if got is None:
+            h = self.handle.h
+            info = self.info()
+            rows, cols = int(info.rows), int(info.cols)
+            sums = np.zeros((rows, cols), np.uint32)
+            occ = np.zeros((rows, cols), np.uint8)
+            off = np.zeros(rows, np.uint32)
+            tot = np.zeros(rows, np.uint32)
+            st = _lib.BlockStatsC()
+            check(lib.bbm_prep_get_sums(h, ptr(sums, C.c_uint32)))
+            check(lib.bbm_prep_get_occupancy(h, ptr(occ, C.c_uint8)))
+            check(lib.bbm_prep_get_runs(h, ptr(off, C.c_uint32), ptr(tot, C.c_uint32)))
+            check(lib.bbm_prep_get_stats(h, C.byref(st)))
+            got = (BlockSums(self.n_tokens, self.spec, sums), BlockOccupancy(occ),
+                   DenseRuns([int(x) for x in off], [int(x) for x in tot]),
+                   BlockStats(st.blocks_total, st.blocks_nonzero, st.blocks_full, st.block_density,
+                              st.element_density))
+            self._cache = {self._version: got}
+        return got
+
+    @property
+    def sums(self) -> BlockSums:
+        return self._host()[0]
+
+    @property
+    def occupancy(self) -> BlockOccupancy:
+        return self._host()[1]
+
+    @property
+    def runs(self) -> DenseRuns:
+        return self._host()[2]
+
+    @property
+    def stats(self) -> BlockStats:
+        return self._host()[3]
 
     def info(self) -> _lib.PrepInfoC:
         info = _lib.PrepInfoC()
@@ -271,28 +316,52 @@ class MaskPrep:
         return EngineCounters(c.blocks_visited, c.blocks_processed, c.mask_block_reads,
                               c.skipped_by_binblk, c.skipped_mask_reads_by_run)
 
+    def update(self, mask, stream=None) -> None:
+        """Rebuild for a new mask of the same size, asynchronously on ``stream`` (a CUDA
+        ``torch.bool``/``uint8`` n x n tensor, or ``torch.int64`` packed words [n][ceil(n/64)])."""
+        import torch
+
+        if not isinstance(mask, torch.Tensor) or not mask.is_cuda or mask.shape[0] != self.n_tokens:
+            raise ValueError("update needs a CUDA mask tensor of the prep's size")
+        s = stream if stream is not None else torch.cuda.current_stream(mask.device).cuda_stream
+        with torch.cuda.device(mask.device):
+            if mask.dtype in (torch.bool, torch.uint8):
+                m = mask if mask.stride(1) == 1 else mask.contiguous()
+                check(lib.bbm_prep_update_bool_device(self.handle.h, C.c_void_p(m.data_ptr()), m.stride(0),
+                                                      C.c_void_p(s)))
+            elif mask.dtype == torch.int64:
+                m = mask.contiguous()
+                check(lib.bbm_prep_update_packed_device(self.handle.h, C.c_void_p(m.data_ptr()), C.c_void_p(s)))
+            else:
+                raise ValueError("unsupported mask tensor dtype")
+        self._version += 1
+
+    def replicate(self, device: int) -> "MaskPrep":
+        """bbm_prep_replicate: the same metadata on another GPU (peer-to-peer copy)."""
+        h = C.c_void_p()
+        check(lib.bbm_prep_replicate(self.handle.h, int(device), None, C.byref(h)))
+        return MaskPrep(_PrepHandle(h))
+
+    def export_ipc(self) -> bytes:
+        """bbm_prep_export_ipc: a blob another process imports with :func:`import_prep_ipc`."""
+        size = C.c_size_t(0)
+        check(lib.bbm_prep_export_ipc(self.handle.h, None, C.byref(size)))
+        buf = (C.c_uint8 * size.value)()
+        check(lib.bbm_prep_export_ipc(self.handle.h, C.cast(buf, C.c_void_p), C.byref(size)))
+        return bytes(buf)
+
+
+def import_prep_ipc(blob: bytes, device: int = 0) -> MaskPrep:
+    """bbm_prep_import_ipc: copy an exported prep's device metadata (IPC + peer copy) onto
+    ``device`` of this process."""
+    h = C.c_void_p()
+    buf = (C.c_uint8 * len(blob)).from_buffer_copy(blob)
+    check(lib.bbm_prep_import_ipc(C.cast(buf, C.c_void_p), len(blob), int(device), None, C.byref(h)))
+    return MaskPrep(_PrepHandle(h))
+
 
 def _prep_from_handle(h: C.c_void_p) -> MaskPrep:
-    handle = _PrepHandle(h)
-    info = _lib.PrepInfoC()
-    check(lib.bbm_prep_get_info(h, C.byref(info)))
-    rows, cols = int(info.rows), int(info.cols)
-    sums = np.zeros((rows, cols), np.uint32)
-    occ = np.zeros((rows, cols), np.uint8)
-    off = np.zeros(rows, np.uint32)
-    tot = np.zeros(rows, np.uint32)
-    st = _lib.BlockStatsC()
-    check(lib.bbm_prep_get_sums(h, ptr(sums, C.c_uint32)))
-    check(lib.bbm_prep_get_occupancy(h, ptr(occ, C.c_uint8)))
-    check(lib.bbm_prep_get_runs(h, ptr(off, C.c_uint32), ptr(tot, C.c_uint32)))
-    check(lib.bbm_prep_get_stats(h, C.byref(st)))
-    spec = BlockSpec(int(info.block_i), int(info.block_j))
-    return MaskPrep(
-        n_tokens=int(info.n), spec=spec, sums=BlockSums(int(info.n), spec, sums),
-        occupancy=BlockOccupancy(occ), runs=DenseRuns([int(x) for x in off], [int(x) for x in tot]),
-        stats=BlockStats(st.blocks_total, st.blocks_nonzero, st.blocks_full, st.block_density,
-                         st.element_density),
-        handle=handle)
+    return MaskPrep(_PrepHandle(h))
 
 
 def preprocess_mask(mask, spec: BlockSpec = BlockSpec(), device: int = 0, stream=None) -> MaskPrep:
@@ -414,6 +483,12 @@ def attn_fwd_device(prep: MaskPrep, variant: Variant, q, k, v, out, row_max=None
     import torch
 
     slots, n, d = (q.shape if q.dim() == 3 else (1, *q.shape))
+    for t in (k, v, out):
+        if t.shape != q.shape or not t.is_contiguous() or t.dtype != torch.bfloat16:
+            raise ValueError("q, k, v, out must be contiguous bf16 tensors of one shape")
+    for t in (row_max, row_sum):
+        if t is not None and (t.numel() != slots * n or t.dtype != torch.float32):
+            raise ValueError("row statistics must be float32 [slots][n]")
     s = stream if stream is not None else torch.cuda.current_stream(q.device).cuda_stream
     check(lib.bbm_attn_fwd(prep.handle.h, int(variant), C.c_void_p(q.data_ptr()), C.c_void_p(k.data_ptr()),
                            C.c_void_p(v.data_ptr()), C.c_void_p(out.data_ptr()),
@@ -444,6 +519,10 @@ def blocked_forward(q, k, v, scale: float, mask, prep: MaskPrep, variant: Varian
         raise ValueError("v must have a positive head dim")
     if len(shapes) != 1:
         raise ValueError(f"head dims {sorted(shapes)} unsupported: the sm_100a kernel needs d_v == d_k")
+    if not (q.shape == k.shape == v.shape) or q.dim() not in (2, 3):
+        raise ValueError("q, k and v must share one [n, d] or [slots, n, d] shape")
+    if not (q.device == k.device == v.device) or not q.is_cuda:
+        raise ValueError("q, k and v must live on one CUDA device")
     if check_finite:
         for name, t in (("q", q), ("k", k), ("v", v)):
             if not bool(torch.isfinite(t).all()):

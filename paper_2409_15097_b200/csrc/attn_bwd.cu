@@ -636,8 +636,8 @@ __global__ void __launch_bounds__(128) transpose_bitmaps_kernel(const uint4* __r
 }
 
 template <int D, int SIDE>
-void launch_side(const Prep& prep, const BwdArgs& a, const float* lse2, const float* delta, uint32_t rows_pad,
-                 cudaStream_t s, int num_sms) {
+void launch_side(const Prep& prep, StreamCtx& ctx, const BwdArgs& a, const float* lse2, const float* delta,
+                 uint32_t rows_pad, cudaStream_t s, int num_sms) {
   static_assert(bwd_smem_bytes<D, SIDE>() <= 232448, "exceeds the 227 KB opt-in shared memory");
   const KernelMeta& km = prep.kmeta;
   const BwdMeta& bm = prep.bwd;
@@ -658,7 +658,7 @@ void launch_side(const Prep& prep, const BwdArgs& a, const float* lse2, const fl
     p.list_stride = km.kcols;
     p.order = p.all_tiles ? bm.all_order : km.order;
     p.bitmaps = km.bitmaps;
-    p.ctr = bm.ctr;
+    p.ctr = ctx.ctr + 2;
     p.out0 = static_cast<__nv_bfloat16*>(a.dq);
   } else {
     p.tiles = km.kcols;
@@ -668,17 +668,17 @@ void launch_side(const Prep& prep, const BwdArgs& a, const float* lse2, const fl
     p.list_stride = km.krows;
     p.order = p.all_tiles ? bm.all_order : bm.col_order;
     p.bitmaps = bm.tbitmaps;
-    p.ctr = bm.ctr + 2;
+    p.ctr = ctx.ctr + 4;
     p.out0 = static_cast<__nv_bfloat16*>(a.dk);
     p.out1 = static_cast<__nv_bfloat16*>(a.dv);
   }
   p.total_items = static_cast<uint32_t>(a.slots * p.tiles);
-  const CUtensorMap tq = make_tmap_bf16_3d(a.q, D, a.n, a.slots, 64, 128);
-  const CUtensorMap tk = make_tmap_bf16_3d(a.k, D, a.n, a.slots, 64, 128);
-  const CUtensorMap tv = make_tmap_bf16_3d(a.v, D, a.n, a.slots, 64, 128);
-  const CUtensorMap tdo = make_tmap_bf16_3d(a.d_out, D, a.n, a.slots, 64, 128);
-  const CUtensorMap to0 = make_tmap_bf16_3d(p.out0, D, a.n, a.slots, 64, 128);
-  const CUtensorMap to1 = SIDE == kSideDKDV ? make_tmap_bf16_3d(p.out1, D, a.n, a.slots, 64, 128) : to0;
+  const CUtensorMap tq = cached_tmap_bf16_3d(a.q, D, a.n, a.slots, 64, 128);
+  const CUtensorMap tk = cached_tmap_bf16_3d(a.k, D, a.n, a.slots, 64, 128);
+  const CUtensorMap tv = cached_tmap_bf16_3d(a.v, D, a.n, a.slots, 64, 128);
+  const CUtensorMap tdo = cached_tmap_bf16_3d(a.d_out, D, a.n, a.slots, 64, 128);
+  const CUtensorMap to0 = cached_tmap_bf16_3d(p.out0, D, a.n, a.slots, 64, 128);
+  const CUtensorMap to1 = SIDE == kSideDKDV ? cached_tmap_bf16_3d(p.out1, D, a.n, a.slots, 64, 128) : to0;
   static std::atomic<uint64_t> attr_devices{0};
   once_per_device(attr_devices, [] {
     BBM_CUDA(cudaFuncSetAttribute(attn_bwd_kernel<D, SIDE, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -714,6 +714,10 @@ T* bwd_alloc(uint64_t count) {
   return static_cast<T*>(ptr);
 }
 
+__global__ void iota_kernel(uint32_t* __restrict__ out, uint32_t count) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < count; i += gridDim.x * blockDim.x) out[i] = i;
+}
+
 }  // namespace
 
 void free_bwd_meta(BwdMeta& b) {
@@ -722,61 +726,64 @@ void free_bwd_meta(BwdMeta& b) {
   cudaFree(b.col_order);
   cudaFree(b.all_order);
   cudaFree(b.tbitmaps);
-  cudaFree(b.ctr);
-  cudaFree(b.rowws);
+  cudaFree(b.scratch);
+  if (b.ready) cudaEventDestroy(b.ready);
   b = BwdMeta{};
 }
 
-void build_bwd_meta(Prep& prep, cudaStream_t s) {
+// Column view of the current mask version, built on stream s by kernels only (called with
+// prep.mu held). Streams that did not build it wait for `ready`.
+void ensure_bwd_meta(const Prep& prep, cudaStream_t s) {
   BwdMeta& b = prep.bwd;
-  if (b.built) return;
   const KernelMeta& km = prep.kmeta;
   const uint32_t kr = km.krows, kc = km.kcols;
-  if (!b.col_cnt) {
-    b.col_cnt = bwd_alloc<uint32_t>(kc);
-    b.col_list = bwd_alloc<uint32_t>(static_cast<uint64_t>(kc) * kr);
-    b.col_order = bwd_alloc<uint32_t>(kc);
-    b.all_order = bwd_alloc<uint32_t>(std::max(kr, kc));
-    b.tbitmaps = bwd_alloc<uint4>(static_cast<uint64_t>(kc) * kr * 128);
-    b.ctr = bwd_alloc<uint32_t>(4);
-    BBM_CUDA(cudaMemsetAsync(b.ctr, 0, 16, s));
-    std::vector<uint32_t> ident(std::max(kr, kc));
-    std::iota(ident.begin(), ident.end(), 0u);
-    BBM_CUDA(cudaMemcpyAsync(b.all_order, ident.data(), ident.size() * 4, cudaMemcpyHostToDevice, s));
-    BBM_CUDA(cudaStreamSynchronize(s));
+  if (b.version != prep.version) {
+    if (!b.col_cnt) {
+      b.col_cnt = bwd_alloc<uint32_t>(kc);
+      b.col_list = bwd_alloc<uint32_t>(static_cast<uint64_t>(kc) * kr);
+      b.col_order = bwd_alloc<uint32_t>(kc);
+      b.all_order = bwd_alloc<uint32_t>(std::max(kr, kc));
+      b.tbitmaps = bwd_alloc<uint4>(static_cast<uint64_t>(kc) * kr * 128);
+      b.scratch = bwd_alloc<uint32_t>(static_cast<uint64_t>(kr) + kc + 2);
+      BBM_CUDA(cudaEventCreateWithFlags(&b.ready, cudaEventDisableTiming));
+      iota_kernel<<<(std::max(kr, kc) + 255) / 256, 256, 0, s>>>(b.all_order, std::max(kr, kc));
+      BBM_CUDA(cudaGetLastError());
+    }
+    collist_kernel<<<kc, 256, 0, s>>>(km.sums, prep.n, kr, kc, b.col_list, b.col_cnt);
+    BBM_CUDA(cudaGetLastError());
+    transpose_bitmaps_kernel<<<dim3(kr, kc), 128, 0, s>>>(reinterpret_cast<const uint4*>(km.mask), kr, kc,
+                                                           b.col_list, b.col_cnt, b.tbitmaps);
+    BBM_CUDA(cudaGetLastError());
+    // LPT order of the columns (longest list first, ties by index), like the forward's row order
+    launch_lpt_order(b.col_cnt, kc, kr, b.scratch, b.col_order, s);
+    BBM_CUDA(cudaEventRecord(b.ready, s));
+    b.version = prep.version;
+  } else {
+    BBM_CUDA(cudaStreamWaitEvent(s, b.ready, 0));
   }
-  collist_kernel<<<kc, 256, 0, s>>>(km.sums, prep.n, kr, kc, b.col_list, b.col_cnt);
-  BBM_CUDA(cudaGetLastError());
-  transpose_bitmaps_kernel<<<dim3(kr, kc), 128, 0, s>>>(reinterpret_cast<const uint4*>(km.mask), kr, kc,
-                                                         b.col_list, b.col_cnt, b.tbitmaps);
-  BBM_CUDA(cudaGetLastError());
-  // LPT order of the columns (longest list first, ties by index), like the forward's row order
-  std::vector<uint32_t> cnt(kc), order(kc);
-  BBM_CUDA(cudaMemcpyAsync(cnt.data(), b.col_cnt, kc * 4, cudaMemcpyDeviceToHost, s));
-  BBM_CUDA(cudaStreamSynchronize(s));
-  std::iota(order.begin(), order.end(), 0u);
-  std::stable_sort(order.begin(), order.end(), [&](uint32_t x, uint32_t y) { return cnt[x] > cnt[y]; });
-  BBM_CUDA(cudaMemcpyAsync(b.col_order, order.data(), kc * 4, cudaMemcpyHostToDevice, s));
-  BBM_CUDA(cudaStreamSynchronize(s));
-  b.built = true;
 }
 
 void launch_attn_bwd(const Prep& prep, const BwdArgs& a, cudaStream_t s, int num_sms) {
   require(a.slots >= 1, "need at least one batch/head slot");
   require(a.n == prep.n, "mask preprocessing does not match this problem");
-  require(prep.bwd.built, "backward metadata not built");
   if (a.d != 64 && a.d != 128) throw ArgError("head dim must be 64 or 128 on the sm_100a kernel");
+  std::lock_guard<std::recursive_mutex> lk(prep.mu);
+  StreamCtx& ctx = prep.ctx_for(s);
+  ensure_bwd_meta(prep, s);
   const uint32_t rows_pad = prep.kmeta.krows * 128;
   const size_t need = 2 * static_cast<size_t>(a.slots) * rows_pad;
-  const BwdMeta& b = prep.bwd;
-  if (need > b.rowws_floats) {
-    cudaFree(b.rowws);
-    b.rowws = nullptr;
-    BBM_CUDA(cudaMalloc(&b.rowws, need * sizeof(float)));
-    b.rowws_floats = need;
+  if (need > ctx.rowws_floats) {
+    if (ctx.rowws) {
+      BBM_CUDA(cudaStreamSynchronize(s));
+      cudaFree(ctx.rowws);
+    }
+    ctx.rowws = nullptr;
+    ctx.rowws_floats = 0;
+    BBM_CUDA(cudaMalloc(&ctx.rowws, need * sizeof(float)));
+    ctx.rowws_floats = need;
   }
-  float* lse2 = b.rowws;
-  float* delta = b.rowws + static_cast<size_t>(a.slots) * rows_pad;
+  float* lse2 = ctx.rowws;
+  float* delta = ctx.rowws + static_cast<size_t>(a.slots) * rows_pad;
   const uint64_t warps = a.slots * rows_pad;
   const unsigned grid = static_cast<unsigned>(std::min<uint64_t>((warps + 7) / 8, 148ull * 64));
   if (a.o_f32)
@@ -789,12 +796,13 @@ void launch_attn_bwd(const Prep& prep, const BwdArgs& a, cudaStream_t s, int num
         a.row_sum, a.slots, a.n, a.d, rows_pad, lse2, delta);
   BBM_CUDA(cudaGetLastError());
   if (a.d == 64) {
-    launch_side<64, kSideDKDV>(prep, a, lse2, delta, rows_pad, s, num_sms);
-    launch_side<64, kSideDQ>(prep, a, lse2, delta, rows_pad, s, num_sms);
+    launch_side<64, kSideDKDV>(prep, ctx, a, lse2, delta, rows_pad, s, num_sms);
+    launch_side<64, kSideDQ>(prep, ctx, a, lse2, delta, rows_pad, s, num_sms);
   } else {
-    launch_side<128, kSideDKDV>(prep, a, lse2, delta, rows_pad, s, num_sms);
-    launch_side<128, kSideDQ>(prep, a, lse2, delta, rows_pad, s, num_sms);
+    launch_side<128, kSideDKDV>(prep, ctx, a, lse2, delta, rows_pad, s, num_sms);
+    launch_side<128, kSideDQ>(prep, ctx, a, lse2, delta, rows_pad, s, num_sms);
   }
+  mark_launch_done(ctx, s);
 }
 
 }  // namespace bbm

@@ -55,25 +55,22 @@ using namespace ptx;
 
 enum Mode : int { kModeBinblk = 0, kModeDenseBinblk = 1, kModeDense = 2, kModeNaive = 3 };
 
-constexpr uint32_t kNoSplit = 0xFFFFFFFFu;
 constexpr uint32_t kEnd = 0xFFFFFFFFu;
 
 struct FwdParams {
   uint64_t n;
   uint32_t slots;
   uint32_t krows, kcols;
-  uint32_t units;        // row units per slot
-  uint32_t total_items;  // slots * units
+  const PlanHdr* hdr;    // device plan header: row units per slot, split rows / chunks
   float sl2;             // scale * log2(e)
   const uint32_t* list;
   const uint4* bitmaps;
   const uint4* mask;        // padded packed mask, kcols uint4 per row
   const uint4* unit_desc;   // [units] {row tile, j0, tiles, split (kNoSplit | row << 8 | chunk)}
   const uint2* split_info;  // [split rows] {chunks, first workspace chunk}
-  uint32_t split_rows, split_chunks;
   float* ws;             // [slots][split_chunks][128 * (D + 3)] partial O | m_run | m_true | l
   uint32_t* split_ctr;   // [slots][split_rows] finished chunks (reset by the combiner)
-  uint32_t* work_ctr;    // [2] next item, finished CTAs (reset by the last CTA)
+  uint32_t* work_ctr;    // [2] next item, finished CTAs (reset by the last CTA; per stream)
   __nv_bfloat16* out;
   float* row_max;
   float* row_sum;
@@ -176,6 +173,7 @@ struct SmemCtl {
   uint64_t item_full[kQueue], item_empty[kQueue];
   ItemDesc items[kQueue];
   uint32_t tmem_base;
+  uint32_t units, total_items, split_rows, split_chunks;  // this launch's plan (device-built)
   uint32_t trace_count;
   uint32_t bcast;
   float xchg[2][kXP][128];  // [exchange parity][part][row]: partial row max
@@ -194,17 +192,18 @@ __device__ __forceinline__ uint32_t entry_of(const FwdParams& p, uint32_t row_ti
   else return p.list[static_cast<uint64_t>(row_tile) * p.kcols + j];
 }
 
-__device__ __forceinline__ ItemDesc decode_item(const FwdParams& p, uint32_t t) {
+__device__ __forceinline__ ItemDesc decode_item(const FwdParams& p, uint32_t units, uint32_t total,
+                                                uint32_t t) {
   ItemDesc d;
   d.t = t;
-  if (t >= p.total_items) {
+  if (t >= total) {
     d.t = kEnd;
     d.slot = d.rt = d.j0 = d.nt = 0;
     d.split = kNoSplit;
     return d;
   }
-  d.slot = t / p.units;
-  const uint4 u = p.unit_desc[t - d.slot * p.units];
+  d.slot = t / units;
+  const uint4 u = p.unit_desc[t - d.slot * units];
   d.rt = u.x;
   d.j0 = u.y;
   d.nt = u.z;
@@ -297,6 +296,11 @@ __global__ void __launch_bounds__(kThreadsOf<D>, 1)
 
   if (threadIdx.x == 0) {
     ctl->trace_count = 0;
+    const PlanHdr h = *p.hdr;
+    ctl->units = h.units;
+    ctl->total_items = h.units * p.slots;
+    ctl->split_rows = h.split_rows;
+    ctl->split_chunks = h.split_chunks;
     for (int b = 0; b < 2; ++b) {
       mbar_init(&ctl->q_full[b], 1);
       mbar_init(&ctl->q_empty[b], 1);
@@ -369,7 +373,7 @@ __global__ void __launch_bounds__(kThreadsOf<D>, 1)
       auto k_next = [&]() -> bool {
         while (k_need) {
           if (k_done) return false;
-          const ItemDesc d = decode_item(p, atomicAdd(&p.work_ctr[0], 1u));
+          const ItemDesc d = decode_item(p, ctl->units, ctl->total_items, atomicAdd(&p.work_ctr[0], 1u));
           mbar_wait(&ctl->item_empty[qi], qiph);
           ctl->items[qi] = d;
           mbar_arrive(&ctl->item_full[qi]);  // release: the descriptor is visible to waiters
@@ -827,7 +831,7 @@ __global__ void __launch_bounds__(kThreadsOf<D>, 1)
         const uint32_t srow = it.split >> 8, chunk = it.split & 0xFF;
         const uint2 si = p.split_info[srow];  // {chunks, first workspace chunk}
         const uint64_t blk = static_cast<uint64_t>(128) * (D + 3);
-        float* wsb = p.ws + (static_cast<uint64_t>(it.slot) * p.split_chunks + si.y + chunk) * blk;
+        float* wsb = p.ws + (static_cast<uint64_t>(it.slot) * ctl->split_chunks + si.y + chunk) * blk;
 #pragma unroll
         for (uint32_t c32 = 0; c32 < D / 32; ++c32) {
           uint32_t o[32];
@@ -845,14 +849,14 @@ __global__ void __launch_bounds__(kThreadsOf<D>, 1)
         wsb[128 * D + 256 + row] = l_unit;
         __threadfence();
         named_bar_sync(2, kEpi);
-        uint32_t* ctr = p.split_ctr + static_cast<uint64_t>(it.slot) * p.split_rows + srow;
+        uint32_t* ctr = p.split_ctr + static_cast<uint64_t>(it.slot) * ctl->split_rows + srow;
         if (leader) ctl->bcast = atomicAdd(ctr, 1u);
         named_bar_sync(2, kEpi);
         const uint32_t done_before = ctl->bcast;
         if (done_before + 1 == si.x) {
           // last chunk: combine every chunk's partial for this row tile
           __threadfence();
-          const float* base = p.ws + (static_cast<uint64_t>(it.slot) * p.split_chunks + si.y) * blk;
+          const float* base = p.ws + (static_cast<uint64_t>(it.slot) * ctl->split_chunks + si.y) * blk;
           float mrun = -INFINITY, mtrue = -INFINITY;
           for (uint32_t c = 0; c < si.x; ++c) {
             const float* b = base + c * blk + 128 * D;
@@ -914,148 +918,35 @@ __global__ void __launch_bounds__(kThreadsOf<D>, 1)
   }
 }
 
-// Fully masked row tiles (no tile in the list): zero output rows, row_max = -inf, row_sum = 0
-// (engine.hpp:330-332). One CTA per (slot, empty row tile), 128 threads = rows.
-template <int D>
-__global__ void __launch_bounds__(128) zero_rows_kernel(const uint32_t* __restrict__ rows,
-                                                        uint32_t n_rows, uint64_t n,
-                                                        __nv_bfloat16* __restrict__ out,
-                                                        float* __restrict__ row_max,
-                                                        float* __restrict__ row_sum) {
-  const uint32_t slot = blockIdx.x / n_rows;
-  const uint64_t grow = static_cast<uint64_t>(rows[blockIdx.x % n_rows]) * 128 + threadIdx.x;
-  if (grow >= n) return;
-  uint4* dst = reinterpret_cast<uint4*>(out + (static_cast<uint64_t>(slot) * n + grow) * D);
-#pragma unroll
-  for (uint32_t v = 0; v < D / 8; ++v) dst[v] = make_uint4(0, 0, 0, 0);
-  const uint64_t si = static_cast<uint64_t>(slot) * n + grow;
-  if (row_max) row_max[si] = -INFINITY;
-  if (row_sum) row_sum[si] = 0.0f;
-}
-
 // ------------------------------------------------------------------ host side
-
-// Row units for a launch: row tiles longer than L are split into balanced chunks. With dynamic
-// longest-first claiming the makespan is about (average work per CTA + longest unit), so L is
-// half a CTA's average share, and at least 16 tiles: combining partials goes through global
-// memory and costs more than a few tiles (splitting a tiny launch further measured slower).
-//
-// The masked variants split IN KEY SPACE, at boundaries set by the occupied tiles only: chunk c
-// of a row holds the same occupied tiles, in the same order, whether the variant walks the
-// compacted list (binblk, dense_binblk) or every tile of the key range (naive, whose extra tiles
-// are fully masked and change nothing). Their partials and the combine are then identical, so
-// the masked variants agree bit for bit at every size (test_engine.cpp:112-134). The dense
-// variant ignores the mask and splits by position.
-enum PlanClass : int { kPlanDense = 0, kPlanNaive = 1, kPlanList = 2 };
-
-struct UnitBuild {
-  std::vector<uint4> desc;
-  std::vector<uint2> split_info;
-  std::vector<uint32_t> empty_rows;  // row tiles without any tile: zeroed by zero_rows_kernel
-  uint32_t split_chunks = 0;
-};
-
-// cnt[p]: occupied tiles of row tile p; list: their ascending key tiles ([p * kcols + k]).
-UnitBuild build_units(int cls, uint32_t kcols, const std::vector<uint32_t>& cnt,
-                      const std::vector<uint32_t>& list, uint64_t slots, int workers) {
-  const uint32_t krows = static_cast<uint32_t>(cnt.size());
-  uint64_t total = 0;
-  for (uint32_t p = 0; p < krows; ++p) total += cls == kPlanDense ? kcols : cnt[p];
-  total *= slots;
-  const uint64_t w = static_cast<uint64_t>(std::max(1, workers));
-  const uint32_t L = static_cast<uint32_t>(std::max<uint64_t>(16, (total / w + 1) / 2));
-  UnitBuild ub;
-  struct U {
-    uint32_t rt, j0, nt, split;
-  };
-  std::vector<U> units;
-  for (uint32_t p = 0; p < krows; ++p) {
-    const uint32_t occ = cls == kPlanDense ? kcols : cnt[p];
-    const uint32_t walk = cls == kPlanList ? cnt[p] : kcols;  // tiles the kernel walks
-    if (walk == 0) {  // never enters the work queue (every queued item has >= 1 tile)
-      ub.empty_rows.push_back(p);
-      continue;
-    }
-    if (occ <= L) {
-      units.push_back({p, 0, walk, kNoSplit});
-      continue;
-    }
-    const uint32_t k = std::min<uint32_t>((occ + L - 1) / L, 255);
-    const uint32_t srow = static_cast<uint32_t>(ub.split_info.size());
-    ub.split_info.push_back(make_uint2(k, ub.split_chunks));
-    ub.split_chunks += k;
-    // chunk c: occupied tiles [o0, o1) of the row; key range from its first occupied tile up to
-    // the next chunk's (the first chunk from key 0, the last to the end of the row)
-    auto first_occ = [&](uint32_t c) { return (occ / k) * c + std::min(c, occ % k); };
-    auto key_of = [&](uint32_t o) {
-      return cls == kPlanDense ? o : (list[static_cast<uint64_t>(p) * kcols + o] & 0x7FFFFFFFu);
-    };
-    for (uint32_t c = 0; c < k; ++c) {
-      const uint32_t o0 = first_occ(c), o1 = first_occ(c + 1);
-      if (cls == kPlanNaive) {
-        const uint32_t kv0 = c == 0 ? 0 : key_of(o0), kv1 = c + 1 == k ? kcols : key_of(o1);
-        units.push_back({p, kv0, kv1 - kv0, (srow << 8) | c});
-      } else {
-        units.push_back({p, o0, o1 - o0, (srow << 8) | c});  // list positions (dense: positions)
-      }
-    }
-  }
-  std::stable_sort(units.begin(), units.end(), [](const U& a, const U& b) { return a.nt > b.nt; });
-  for (const U& u : units) ub.desc.push_back(make_uint4(u.rt, u.j0, u.nt, u.split));
-  return ub;
-}
 
 template <int D, int MODE>
 void launch_impl(const Prep& prep, const AttnArgs& a, cudaStream_t s, int num_sms) {
   static_assert(smem_bytes<D>() <= 232448, "exceeds the 227 KB opt-in shared memory");
   const KernelMeta& km = prep.kmeta;
   constexpr int kCls = MODE == kModeDense ? kPlanDense : (MODE == kModeNaive ? kPlanNaive : kPlanList);
-  const LaunchPlan& plan = prep.plan_for(kCls, a.slots, static_cast<uint32_t>(num_sms), [&]() {
-    std::vector<uint32_t> list;
-    if (kCls != kPlanDense) {  // the occupied key tiles set the masked variants' split points
-      list.resize(static_cast<size_t>(km.krows) * km.kcols);
-      BBM_CUDA(cudaMemcpy(list.data(), km.list, list.size() * 4, cudaMemcpyDeviceToHost));
-    }
-    const UnitBuild ub = build_units(kCls, km.kcols, prep.h_row_cnt, list, a.slots, num_sms);
-    LaunchPlan lp;
-    lp.units = static_cast<uint32_t>(ub.desc.size());
-    lp.split_rows = static_cast<uint32_t>(ub.split_info.size());
-    lp.split_chunks = ub.split_chunks;
-    lp.slots = a.slots;
-    BBM_CUDA(cudaMalloc(&lp.unit_desc, std::max<size_t>(1, ub.desc.size()) * sizeof(uint4)));
-    BBM_CUDA(cudaMemcpy(lp.unit_desc, ub.desc.data(), ub.desc.size() * sizeof(uint4),
-                        cudaMemcpyHostToDevice));
-    BBM_CUDA(cudaMalloc(&lp.split_info, std::max<size_t>(1, ub.split_info.size()) * sizeof(uint2)));
-    if (!ub.split_info.empty())
-      BBM_CUDA(cudaMemcpy(lp.split_info, ub.split_info.data(),
-                          ub.split_info.size() * sizeof(uint2), cudaMemcpyHostToDevice));
-    lp.empty_rows = static_cast<uint32_t>(ub.empty_rows.size());
-    if (lp.empty_rows) {
-      BBM_CUDA(cudaMalloc(&lp.empty_list, ub.empty_rows.size() * sizeof(uint32_t)));
-      BBM_CUDA(cudaMemcpy(lp.empty_list, ub.empty_rows.data(),
-                          ub.empty_rows.size() * sizeof(uint32_t), cudaMemcpyHostToDevice));
-    }
-    const size_t nctr = std::max<size_t>(1, a.slots * lp.split_rows);
-    BBM_CUDA(cudaMalloc(&lp.split_ctr, nctr * sizeof(uint32_t)));
-    BBM_CUDA(cudaMemset(lp.split_ctr, 0, nctr * sizeof(uint32_t)));
-    return lp;
-  });
-  // one CTA per SM; when work items are scarce, at most one CTA per item
+  std::lock_guard<std::recursive_mutex> lk(prep.mu);
+  StreamCtx& ctx = prep.ctx_for(s);  // ordered after the latest mask version
+  const uint32_t workers = static_cast<uint32_t>(num_sms);
+  const DevPlan& plan = plan_for(prep, ctx, kCls, a.slots, workers, s);
+  // one CTA per SM; when work items are scarce, at most one CTA per item (upper bound: the
+  // plan's unit capacity; CTAs without an item exit after claiming the end marker)
   const uint32_t grid = static_cast<uint32_t>(
-      std::max<uint64_t>(1, std::min<uint64_t>(a.slots * plan.units, static_cast<uint64_t>(num_sms))));
-  float* ws = prep.workspace_for(static_cast<size_t>(a.slots) * plan.split_chunks * 128 * (D + 3));
+      std::max<uint64_t>(1, std::min<uint64_t>(a.slots * plan.cap_units, static_cast<uint64_t>(num_sms))));
+  const bool can_split = plan.cap_units > km.krows;
+  float* ws = can_split ? ctx_workspace(ctx, plan_cap_chunks(a.slots, workers) * 128 * (128 + 3), s) : nullptr;
+  uint32_t* split_ctr = can_split ? ctx_split_ctr(ctx, plan_cap_chunks(a.slots, workers) + a.slots, s) : nullptr;
 
-  const CUtensorMap tq = make_tmap_bf16_3d(a.q, D, a.n, a.slots, 64, 128);
-  const CUtensorMap tk = make_tmap_bf16_3d(a.k, D, a.n, a.slots, 64, 128);
-  const CUtensorMap tv = make_tmap_bf16_3d(a.v, D, a.n, a.slots, 64, 128);
-  const CUtensorMap to = make_tmap_bf16_3d(a.o, D, a.n, a.slots, 64, 128);
+  const CUtensorMap tq = cached_tmap_bf16_3d(a.q, D, a.n, a.slots, 64, 128);
+  const CUtensorMap tk = cached_tmap_bf16_3d(a.k, D, a.n, a.slots, 64, 128);
+  const CUtensorMap tv = cached_tmap_bf16_3d(a.v, D, a.n, a.slots, 64, 128);
+  const CUtensorMap to = cached_tmap_bf16_3d(a.o, D, a.n, a.slots, 64, 128);
   FwdParams p{};
   p.n = a.n;
   p.slots = static_cast<uint32_t>(a.slots);
   p.krows = km.krows;
   p.kcols = km.kcols;
-  p.units = plan.units;
-  p.total_items = static_cast<uint32_t>(a.slots * plan.units);
+  p.hdr = plan.hdr;
   p.sl2 = a.scale * 1.4426950408889634f;
   // A zero scale would turn the masked sentinel into inf * 0 = NaN. 2^-100 instead: every
   // visible score's offset from the row max is then ~1e-28 and exp2 of it rounds to exactly 1.0f
@@ -1066,11 +957,9 @@ void launch_impl(const Prep& prep, const AttnArgs& a, cudaStream_t s, int num_sm
   p.mask = reinterpret_cast<const uint4*>(km.mask);
   p.unit_desc = plan.unit_desc;
   p.split_info = plan.split_info;
-  p.split_rows = plan.split_rows;
-  p.split_chunks = plan.split_chunks;
   p.ws = ws;
-  p.split_ctr = plan.split_ctr;
-  p.work_ctr = prep.work_ctr;
+  p.split_ctr = split_ctr;
+  p.work_ctr = ctx.ctr;
   p.out = static_cast<__nv_bfloat16*>(a.o);
   p.row_max = a.row_max;
   p.row_sum = a.row_sum;
@@ -1083,17 +972,12 @@ void launch_impl(const Prep& prep, const AttnArgs& a, cudaStream_t s, int num_sm
     BBM_CUDA(cudaFuncSetAttribute(attn_fwd_kernel<D, MODE, true>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes<D>()));
   });
-  if (plan.empty_rows) {
-    zero_rows_kernel<D><<<static_cast<unsigned>(a.slots * plan.empty_rows), 128, 0, s>>>(
-        plan.empty_list, plan.empty_rows, a.n, p.out, p.row_max, p.row_sum);
-    BBM_CUDA(cudaGetLastError());
-  }
-  if (p.total_items == 0) return;
   if (p.trace)  // event-tracing build of the same kernel (bbm_set_trace)
     attn_fwd_kernel<D, MODE, true><<<grid, kThreadsOf<D>, smem_bytes<D>(), s>>>(tq, tk, tv, to, p);
   else
     attn_fwd_kernel<D, MODE, false><<<grid, kThreadsOf<D>, smem_bytes<D>(), s>>>(tq, tk, tv, to, p);
   BBM_CUDA(cudaGetLastError());
+  mark_launch_done(ctx, s);
 }
 
 template <int D>
@@ -1114,7 +998,6 @@ void launch_attn_fwd(const Prep& prep, const AttnArgs& a, cudaStream_t s, int nu
   require(a.n == prep.n, "mask preprocessing does not match this problem");
   require(a.slots < (1ull << 24), "too many slots for one launch");
   if (a.slots * prep.kmeta.krows == 0) return;
-  refresh_kernel_view(prep, s);
   if (a.d == 64) launch_d<64>(prep, a, s, num_sms);
   else if (a.d == 128) launch_d<128>(prep, a, s, num_sms);
   else throw ArgError("head dim must be 64 or 128 on the sm_100a kernel");

@@ -5,9 +5,11 @@
 #include <atomic>
 #include <cstdint>
 #include <map>
+#include <mutex>
 #include <stdexcept>
 #include <string>
 #include <tuple>
+#include <type_traits>
 #include <vector>
 
 namespace bbm {
@@ -47,32 +49,38 @@ void once_per_device(std::atomic<uint64_t>& done, Set&& set) {
   done.fetch_or(bit, std::memory_order_release);
 }
 
-// Device metadata at the kernel tile shape (128 x 128). Layouts (all device memory):
+// Device metadata at the kernel tile shape (128 x 128), carved out of ONE device allocation (the
+// arena) so that replication to another GPU is a single peer copy and an IPC export is a single
+// handle. Layouts (all device memory):
 //   mask      : padded bit-packed mask, ktiles*128 rows x kcols*2 u64 words (zero padded)
-//   sums      : u32 [krows][kcols]
-//   row_cnt   : u32 [krows]              occupied tiles per query row tile
-//   list      : u32 [krows][kcols]       ascending occupied column tiles, bit 31 = full tile
-//                                        (never set on a ragged right-edge tile)
-//   order     : u32 [krows]              row tiles by descending row_cnt (LPT), ties by index
 //   bitmaps   : uint4 [krows*kcols][128] tile-major copy of every occupied tile's mask bits at
 //                                        its LIST position: row r of list entry (p,k) at
 //                                        (p*kcols + k)*128 + r (16 bytes), written sparsely
+//   sums      : u32 [krows][kcols]
+//   list      : u32 [krows][kcols]       ascending occupied column tiles, bit 31 = full tile
+//                                        (never set on a ragged right-edge tile)
+//   row_cnt   : u32 [krows]              occupied tiles per query row tile
+//   order     : u32 [krows]              row tiles by descending row_cnt (LPT), ties by index
+//   occ, run_off, run_len, row_stats, totals: the per-row pass's outputs at 128 x 128
 struct KernelMeta {
   uint32_t krows = 0, kcols = 0;
+  uint8_t* arena = nullptr;
+  size_t arena_bytes = 0;
   uint64_t* mask = nullptr;
-  uint32_t* sums = nullptr;
-  uint32_t* row_cnt = nullptr;
-  uint32_t* list = nullptr;
-  uint32_t* order = nullptr;
   uint4* bitmaps = nullptr;
-  uint64_t nnz = 0, full = 0;  // occupied / full tiles at 128x128
-  // persistent scratch of the per-row pass (so rebuilds allocate nothing)
+  uint32_t* sums = nullptr;
+  uint32_t* list = nullptr;
+  uint32_t* row_cnt = nullptr;
+  uint32_t* order = nullptr;
   uint8_t* occ = nullptr;
   uint32_t* run_off = nullptr;
   uint32_t* run_len = nullptr;
   uint64_t* row_stats = nullptr;
   uint64_t* totals = nullptr;
+  uint32_t* scratch = nullptr;  // [krows + kcols + 2] ordering scratch (device LPT sort)
 };
+void carve_kernel_meta(KernelMeta& km, uint64_t n, uint8_t* arena);  // sets pointers + bytes
+size_t kernel_meta_bytes(uint64_t n);
 
 // Per-spec metadata that mirrors the reference's MaskPrep (engine.hpp:71-78), host side.
 struct SpecMeta {
@@ -81,34 +89,55 @@ struct SpecMeta {
   std::vector<uint8_t> occ;
   std::vector<uint32_t> offset, total_ones;
   uint64_t blocks_total = 0, blocks_nonzero = 0, blocks_full = 0, ones = 0;
+  uint64_t knnz = 0, kfull = 0;  // occupied / full tiles of the 128 x 128 kernel view
 };
 
-// Work decomposition of one attention launch shape (plan class x slots x SMs): row units
-// (whole row tiles, or balanced chunks of long ones = split-KV), device-resident.
-struct LaunchPlan {
-  uint32_t units = 0, split_rows = 0, split_chunks = 0;
-  uint64_t slots = 0;
-  uint4* unit_desc = nullptr;    // [units] {row tile, j0, tiles, split | kNoSplit}
-  uint2* split_info = nullptr;   // [split_rows] {chunks, first workspace chunk}
-  uint32_t* split_ctr = nullptr; // [slots][split_rows] finished-chunk counters
-  uint32_t empty_rows = 0;         // row tiles without tiles (zeroed by a small kernel)
-  uint32_t* empty_list = nullptr;
+// Work decomposition of one attention launch (plan class x slots x SMs), BUILT ON THE DEVICE from
+// row_cnt / list (plan.cu), so a mask update never needs the host: row units (whole row tiles, or
+// balanced chunks of long ones = split-KV) in longest-first order. Header + arrays in one buffer.
+struct PlanHdr {
+  uint32_t units, split_rows, split_chunks, unit_len;
+};
+struct DevPlan {
+  uint64_t version = 0;  // mask version the plan was built from
+  uint8_t* mem = nullptr;
+  uint32_t cap_units = 0, cap_split = 0;
+  PlanHdr* hdr = nullptr;
+  uint4* unit_desc = nullptr;   // [cap_units] {row tile, j0, tiles, split | kNoSplit}
+  uint2* split_info = nullptr;  // [cap_split] {chunks, first workspace chunk}
+  uint4* tmp = nullptr;         // [cap_units] units in row order (before the LPT sort)
+  uint32_t* hist = nullptr;     // [kcols + 2] sort scratch
 };
 
-// Backward metadata (built on first backward use, attn_bwd.cu): the column view of the kernel
-// tiles — for key tile q, the ascending occupied query row tiles (bit 31 = full tile), LPT order
-// of the columns, and every occupied tile's mask bits TRANSPOSED (key-major) at its column-list
-// position: key row c of column entry (q, k) at (q*krows + k)*128 + c (16 bytes over queries).
+// Backward metadata (attn_bwd.cu): the column view of the kernel tiles — for key tile q, the
+// ascending occupied query row tiles (bit 31 = full tile), LPT order of the columns, and every
+// occupied tile's mask bits TRANSPOSED (key-major) at its column-list position: key row c of
+// column entry (q, k) at (q*krows + k)*128 + c (16 bytes over queries). Built on the device, on
+// first backward use after each mask version (stream-ordered; no host sync).
 struct BwdMeta {
-  bool built = false;
+  uint64_t version = 0;          // mask version of the column view (0 = never built)
+  cudaEvent_t ready = nullptr;   // recorded after the latest column-view build
   uint32_t* col_cnt = nullptr;   // [kcols]
   uint32_t* col_list = nullptr;  // [kcols][krows]
   uint32_t* col_order = nullptr; // [kcols]
   uint32_t* all_order = nullptr; // [max(krows,kcols)] identity order (dense mode)
   uint4* tbitmaps = nullptr;     // [kcols*krows][128]
-  uint32_t* ctr = nullptr;       // [4] dynamic item counters + finished CTAs (dq / dkdv kernels)
-  mutable float* rowws = nullptr;  // [slots][krows*128] x 2: lse2 | delta
-  mutable size_t rowws_floats = 0;
+  uint32_t* scratch = nullptr;   // [kcols + krows + 2] ordering scratch
+};
+
+// Everything ONE launch mutates lives in a per-(prep, stream) context: launches on one stream
+// are ordered by the stream, launches on different streams never share mutable device state.
+struct StreamCtx {
+  uint64_t seen_version = 0;     // mask version this stream has been ordered after
+  cudaEvent_t done = nullptr;    // recorded after this stream's latest launch on the prep
+  uint32_t* ctr = nullptr;       // device [8]: fwd next item / finished CTAs, bwd dq, bwd dkdv
+  float* ws = nullptr;           // split-KV workspace
+  size_t ws_floats = 0;
+  uint32_t* split_ctr = nullptr; // split-KV finished-chunk counters
+  size_t split_ctr_n = 0;
+  float* rowws = nullptr;        // backward lse2 | delta
+  size_t rowws_floats = 0;
+  std::map<std::tuple<int, uint64_t, uint32_t>, DevPlan> plans;
 };
 
 // Host-buffer pipeline of one prep's device (host_io.cu): persistent device buffers (grow-only)
@@ -119,43 +148,34 @@ struct HostPipe {
   std::vector<cudaEvent_t> ev_in, ev_out;
   uint8_t* buf = nullptr;
   size_t cap = 0;
+  int* bad = nullptr;  // device finiteness flags (q, k, v, d_out)
   ~HostPipe();
 };
 
+// MaskPrep (engine.hpp:71-91): immutable between updates and shareable across threads and
+// streams. The device metadata carries a version; bbm_prep_update_* rebuilds it on the caller's
+// stream, bumps the version and records `ready`; every later launch orders its stream after
+// `ready` (cudaStreamWaitEvent) and rebuilds its device plans, and the host-side caller-spec
+// metadata (sums / occupancy / runs / stats / counters) is recomputed on the next getter call.
 struct Prep {
   int device = 0;
   uint64_t n = 0;
-  SpecMeta spec;     // the caller's BlockSpec
-  KernelMeta kmeta;  // the kernel's 128x128 view
-  mutable std::vector<uint32_t> h_row_cnt;  // host copy of kmeta.row_cnt (scheduling + tests)
-  // set by the asynchronous kernel-view rebuilds (bbm_prep_update_*): the host row counts, the
-  // cached launch plans and the backward's column view are refreshed at the next launch
-  mutable bool kview_stale = false;
-  BwdMeta bwd;                      // column view for the backward (lazy)
-  uint32_t* work_ctr = nullptr;     // device [2]: dynamic item counter, finished CTAs
-  // launch plans and the split-KV workspace are built on first use (not thread-safe: one
-  // launch at a time per prep, like the reference's single-threaded callers)
-  mutable std::map<std::tuple<int, uint64_t, uint32_t>, LaunchPlan> plans;
-  mutable float* workspace = nullptr;
-  mutable size_t workspace_floats = 0;
-  mutable HostPipe* pipe = nullptr;  // host-buffer pipeline (lazy, host_io.cu)
+  uint64_t bi = 0, bj = 0;       // the caller's BlockSpec
+  KernelMeta kmeta;              // the kernel's 128x128 view (device)
+  mutable std::recursive_mutex mu;  // guards everything below
+  mutable uint64_t version = 1;     // bumped by each update
+  cudaEvent_t ready = nullptr;      // recorded after the latest build / update of kmeta
+  mutable SpecMeta spec;            // host metadata at the caller's spec ...
+  mutable uint64_t spec_version = 0;  // ... valid for this version
+  mutable BwdMeta bwd;
+  mutable std::map<cudaStream_t, StreamCtx> streams;
+  mutable std::mutex pipe_mu;       // host-buffer calls on one prep run one at a time
+  mutable HostPipe* pipe = nullptr;
 
-  template <class F>
-  const LaunchPlan& plan_for(int plan_class, uint64_t slots, uint32_t workers, F make) const {
-    const auto key = std::make_tuple(plan_class, slots, workers);
-    auto it = plans.find(key);
-    if (it == plans.end()) it = plans.emplace(key, make()).first;
-    return it->second;
-  }
-  float* workspace_for(size_t floats) const {
-    if (floats > workspace_floats) {
-      cudaFree(workspace);
-      workspace = nullptr;
-      check_cuda(cudaMalloc(&workspace, floats * sizeof(float)), "cudaMalloc(split workspace)");
-      workspace_floats = floats;
-    }
-    return workspace;
-  }
+  // Context of stream `s` (created on first use), ordered after the latest metadata version.
+  StreamCtx& ctx_for(cudaStream_t s) const;
+  // Host-side caller-spec metadata for the current version (synchronous refresh if stale).
+  const SpecMeta& spec_now() const;
   ~Prep();
 };
 
@@ -207,6 +227,26 @@ extern TraceConfig g_trace;
 
 void launch_attn_fwd(const Prep& prep, const AttnArgs& a, cudaStream_t s, int num_sms);
 
+// ---- device launch plans (plan.cu) ----
+enum PlanClass : int { kPlanDense = 0, kPlanNaive = 1, kPlanList = 2 };
+constexpr uint32_t kNoSplit = 0xFFFFFFFFu;
+// upper bound on row units per slot of a plan and on workspace chunk blocks of one launch
+uint32_t plan_cap_units(uint32_t krows, uint32_t kcols, uint64_t slots, uint32_t workers);
+uint64_t plan_cap_chunks(uint64_t slots, uint32_t workers);
+// (re)build `plan` on stream s for the current metadata (kernel, no host sync)
+void build_plan(const KernelMeta& km, int cls, uint64_t slots, uint32_t workers, DevPlan& plan,
+                cudaStream_t s);
+const DevPlan& plan_for(const Prep& prep, StreamCtx& ctx, int cls, uint64_t slots,
+                        uint32_t workers, cudaStream_t s);
+// LPT order of `count` keys (descending key, ties by index) into out[count], one CTA on s
+void launch_lpt_order(const uint32_t* keys, uint32_t count, uint32_t max_key, uint32_t* scratch,
+                      uint32_t* out, cudaStream_t s);
+// record ctx.done after a launch on s (bbm_prep_update_* orders itself after it)
+void mark_launch_done(StreamCtx& ctx, cudaStream_t s);
+// grow-only per-stream scratch
+float* ctx_workspace(StreamCtx& ctx, size_t floats, cudaStream_t s);
+uint32_t* ctx_split_ctr(StreamCtx& ctx, size_t count, cudaStream_t s);
+
 // ---- attention backward (attn_bwd.cu) ----
 struct BwdArgs {
   const void* q;  // bf16 [slots][n][d]
@@ -226,11 +266,10 @@ struct BwdArgs {
   float scale;
   int variant;
 };
-void build_bwd_meta(Prep& prep, cudaStream_t s);  // idempotent
+// column view for the current version, built on stream s if stale (stream-ordered, no host sync)
+void ensure_bwd_meta(const Prep& prep, cudaStream_t s);
 void launch_attn_bwd(const Prep& prep, const BwdArgs& a, cudaStream_t s, int num_sms);
 void free_bwd_meta(BwdMeta& b);
-// refresh host row counts / plans after bbm_prep_update_* (synchronizes `s` once)
-void refresh_kernel_view(const Prep& prep, cudaStream_t s);
 int attn_fwd_kernel_launches_per_call();
 
 // host-buffer forward through the prep's pipeline (host_io.cu): bf16 host q/k/v/out (pinned for
@@ -239,6 +278,12 @@ int attn_fwd_kernel_launches_per_call();
 void run_fwd_host_pipelined(const Prep& prep, int variant, const uint16_t* q, const uint16_t* k,
                             const uint16_t* v, uint16_t* out, float* row_max, float* row_sum,
                             uint64_t slots, uint32_t d, float scale, int num_sms, double* span_ms);
+// the reference's Matrix<float> signature: per-slot float host buffers in, float out, double row
+// statistics (row_max / row_sum arrays, or their entries, may be null); synchronous
+void run_fwd_host_f32(const Prep& prep, int variant, const float* const* q, const float* const* k,
+                      const float* const* v, float* const* out, double* const* row_max,
+                      double* const* row_sum, uint64_t slots, uint32_t d, float scale, int num_sms,
+                      double* span_ms);
 // the RCM path end to end: original-order host buffers, prep built from the permuted mask
 void run_fwd_host_rcm(const Prep& prep, int variant, const uint32_t* forward, const uint16_t* q,
                       const uint16_t* k, const uint16_t* v, uint16_t* out, float* row_max,

@@ -8,6 +8,9 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <map>
+#include <mutex>
+#include <tuple>
 #include <stdexcept>
 #include <string>
 
@@ -46,6 +49,27 @@ inline CUtensorMap make_tmap_bf16_3d(const void* base, uint64_t inner, uint64_t 
                                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS)
     throw std::runtime_error("cuTensorMapEncodeTiled failed with code " + std::to_string(int(r)));
+  return m;
+}
+
+// The same descriptor, cached per (pointer, shape, box): encoding costs a few microseconds, more
+// than a whole small launch. Descriptors are plain values (no device state), so a stale entry for
+// a freed-and-reused address is still exactly the descriptor of that address and shape.
+inline CUtensorMap cached_tmap_bf16_3d(const void* base, uint64_t inner, uint64_t rows,
+                                       uint64_t outer, uint32_t box_inner, uint32_t box_rows) {
+  using Key = std::tuple<const void*, uint64_t, uint64_t, uint64_t, uint32_t, uint32_t>;
+  static std::mutex mu;
+  static std::map<Key, CUtensorMap> cache;
+  const Key key{base, inner, rows, outer, box_inner, box_rows};
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = cache.find(key);
+    if (it != cache.end()) return it->second;
+  }
+  const CUtensorMap m = make_tmap_bf16_3d(base, inner, rows, outer, box_inner, box_rows);
+  std::lock_guard<std::mutex> lk(mu);
+  if (cache.size() >= 4096) cache.clear();  // bounded: callers cycling through many buffers
+  cache.emplace(key, m);
   return m;
 }
 

@@ -68,44 +68,14 @@ T* dmalloc(uint64_t count) {
   return static_cast<T*>(p);
 }
 
-void alloc_kernel_meta(KernelMeta& km, uint64_t n) {
-  km.krows = static_cast<uint32_t>((n + kTile - 1) / kTile);
-  km.kcols = km.krows;
-  const uint64_t tiles = static_cast<uint64_t>(km.krows) * km.kcols;
-  km.mask = dmalloc<uint64_t>(static_cast<uint64_t>(km.krows) * kTile * km.kcols * 2);
-  km.sums = dmalloc<uint32_t>(tiles);
-  km.row_cnt = dmalloc<uint32_t>(km.krows);
-  km.list = dmalloc<uint32_t>(tiles);
-  km.order = dmalloc<uint32_t>(km.krows);
-  km.bitmaps = dmalloc<uint4>(tiles * kTile);
-  km.occ = dmalloc<uint8_t>(tiles);
-  km.run_off = dmalloc<uint32_t>(km.krows);
-  km.run_len = dmalloc<uint32_t>(km.krows);
-  km.row_stats = dmalloc<uint64_t>(static_cast<uint64_t>(km.krows) * 3);
-  km.totals = dmalloc<uint64_t>(3);
-}
-
-// Kernel view from km.sums (already built): lists, bitmaps, LPT order. Async, no allocation.
+// Kernel view from km.sums (already built): lists, bitmaps, totals, LPT row order. Async, no
+// allocation, no host sync.
 void build_kernel_view(const KernelMeta& km, uint64_t n, cudaStream_t s) {
   launch_rowmeta(km.sums, n, kTile, kTile, km.krows, km.kcols, km.occ, km.run_off, km.run_len,
                  km.row_stats, km.list, km.row_cnt, s);
   launch_compact_bitmaps(km, s);
-  launch_finalize(km.row_stats, km.krows, km.row_cnt, km.order, km.totals, s);
-}
-
-void free_kernel_meta(KernelMeta& km) {
-  cudaFree(km.mask);
-  cudaFree(km.sums);
-  cudaFree(km.row_cnt);
-  cudaFree(km.list);
-  cudaFree(km.order);
-  cudaFree(km.bitmaps);
-  cudaFree(km.occ);
-  cudaFree(km.run_off);
-  cudaFree(km.run_len);
-  cudaFree(km.row_stats);
-  cudaFree(km.totals);
-  km = KernelMeta{};
+  launch_finalize(km.row_stats, km.krows, nullptr, nullptr, km.totals, s);
+  launch_lpt_order(km.row_cnt, km.krows, km.kcols, km.scratch, km.order, s);
 }
 
 void validate_spec(uint64_t n, uint64_t bi, uint64_t bj) {
@@ -114,80 +84,17 @@ void validate_spec(uint64_t n, uint64_t bi, uint64_t bj) {
   require(n < (1ull << 31), "mask too large for the device metadata (n >= 2^31)");
 }
 
-// Everything after the padded mask exists: sums at both views, row metadata, lists, bitmaps.
-void build_metadata(Prep& pr, uint64_t bi, uint64_t bj, cudaStream_t s) {
-  KernelMeta& km = pr.kmeta;
-  const uint64_t n = pr.n;
-  SpecMeta& sp = pr.spec;
-  sp.bi = bi;
-  sp.bj = bj;
-  sp.rows = (n + bi - 1) / bi;
-  sp.cols = (n + bj - 1) / bj;
-
-  // kernel view (128 x 128): sums already produced by the pack kernel or the sums kernel
-  build_kernel_view(km, n, s);
-  uint8_t* d_kocc = km.occ;
-  uint32_t* d_koff = km.run_off;
-  uint32_t* d_ktot = km.run_len;
-  uint64_t* d_kstats = km.row_stats;
-  uint64_t* d_ktotals = km.totals;
-
-  // caller's view
-  const bool same = (bi == kTile && bj == kTile);
-  const uint64_t tiles = sp.rows * sp.cols;
-  uint32_t* d_sums = same ? km.sums : dmalloc<uint32_t>(tiles);
-  uint8_t* d_occ = same ? d_kocc : dmalloc<uint8_t>(tiles);
-  uint32_t* d_off = same ? d_koff : dmalloc<uint32_t>(sp.rows);
-  uint32_t* d_tot = same ? d_ktot : dmalloc<uint32_t>(sp.rows);
-  uint64_t* d_stats = same ? d_kstats : dmalloc<uint64_t>(sp.rows * 3);
-  uint64_t* d_totals = same ? d_ktotals : dmalloc<uint64_t>(3);
-  if (!same) {
-    launch_sums_generic(km, n, bi, bj, sp.rows, sp.cols, d_sums, s);
-    launch_rowmeta(d_sums, n, bi, bj, sp.rows, sp.cols, d_occ, d_off, d_tot, d_stats, nullptr,
-                   nullptr, s);
-    launch_finalize(d_stats, sp.rows, nullptr, nullptr, d_totals, s);
-  }
-
-  sp.sums.resize(tiles);
-  sp.occ.resize(tiles);
-  sp.offset.resize(sp.rows);
-  sp.total_ones.resize(sp.rows);
-  uint64_t totals[3] = {0, 0, 0}, ktotals[3] = {0, 0, 0};
-  pr.h_row_cnt.resize(km.krows);
-  BBM_CUDA(cudaMemcpyAsync(sp.sums.data(), d_sums, tiles * 4, cudaMemcpyDeviceToHost, s));
-  BBM_CUDA(cudaMemcpyAsync(sp.occ.data(), d_occ, tiles, cudaMemcpyDeviceToHost, s));
-  BBM_CUDA(cudaMemcpyAsync(sp.offset.data(), d_off, sp.rows * 4, cudaMemcpyDeviceToHost, s));
-  BBM_CUDA(cudaMemcpyAsync(sp.total_ones.data(), d_tot, sp.rows * 4, cudaMemcpyDeviceToHost, s));
-  BBM_CUDA(cudaMemcpyAsync(totals, d_totals, 24, cudaMemcpyDeviceToHost, s));
-  BBM_CUDA(cudaMemcpyAsync(ktotals, d_ktotals, 24, cudaMemcpyDeviceToHost, s));
-  BBM_CUDA(cudaMemcpyAsync(pr.h_row_cnt.data(), km.row_cnt, km.krows * 4, cudaMemcpyDeviceToHost,
-                           s));
-  BBM_CUDA(cudaStreamSynchronize(s));
-  sp.blocks_total = tiles;
-  sp.blocks_nonzero = totals[0];
-  sp.blocks_full = totals[1];
-  sp.ones = totals[2];
-  km.nnz = ktotals[0];
-  km.full = ktotals[1];
-
-  if (!same) {
-    cudaFree(d_sums);
-    cudaFree(d_occ);
-    cudaFree(d_off);
-    cudaFree(d_tot);
-    cudaFree(d_stats);
-    cudaFree(d_totals);
-  }
-}
-
-Prep* new_prep(uint64_t n, int device) {
+Prep* new_prep(uint64_t n, int device, uint64_t bi, uint64_t bj) {
   auto* pr = new Prep;
   pr->device = device;
   pr->n = n;
+  pr->bi = bi;
+  pr->bj = bj;
   try {
-    alloc_kernel_meta(pr->kmeta, n);
-    pr->work_ctr = dmalloc<uint32_t>(2);
-    BBM_CUDA(cudaMemset(pr->work_ctr, 0, 2 * sizeof(uint32_t)));
+    void* arena = nullptr;
+    BBM_CUDA(cudaMalloc(&arena, kernel_meta_bytes(n)));
+    carve_kernel_meta(pr->kmeta, n, static_cast<uint8_t*>(arena));
+    BBM_CUDA(cudaEventCreateWithFlags(&pr->ready, cudaEventDisableTiming));
   } catch (...) {
     delete pr;
     throw;
@@ -195,43 +102,158 @@ Prep* new_prep(uint64_t n, int device) {
   return pr;
 }
 
+// Order stream s after every launch still reading the current metadata (an update must not
+// overwrite lists a queued kernel is walking), then after the latest metadata write.
+void order_update_after_launches(const Prep& pr, cudaStream_t s) {
+  for (auto& kv : pr.streams)
+    if (kv.second.done) BBM_CUDA(cudaStreamWaitEvent(s, kv.second.done, 0));
+  BBM_CUDA(cudaStreamWaitEvent(s, pr.ready, 0));
+}
+
+// A new metadata version is complete on stream s.
+void publish_version(const Prep& pr, cudaStream_t s) {
+  ++pr.version;
+  BBM_CUDA(cudaEventRecord(pr.ready, s));
+}
+
 }  // namespace
+
+size_t kernel_meta_bytes(uint64_t n) {
+  KernelMeta km;
+  carve_kernel_meta(km, n, nullptr);
+  return km.arena_bytes;
+}
+
+void carve_kernel_meta(KernelMeta& km, uint64_t n, uint8_t* arena) {
+  km.krows = static_cast<uint32_t>((n + kTile - 1) / kTile);
+  km.kcols = km.krows;
+  const uint64_t tiles = static_cast<uint64_t>(km.krows) * km.kcols;
+  size_t off = 0;
+  auto take = [&](auto*& ptr, uint64_t count) {
+    using T = std::remove_reference_t<decltype(*ptr)>;
+    ptr = reinterpret_cast<T*>(arena + off);
+    off += (std::max<uint64_t>(1, count) * sizeof(T) + 255) / 256 * 256;
+  };
+  km.arena = arena;
+  take(km.mask, static_cast<uint64_t>(km.krows) * kTile * km.kcols * 2);
+  take(km.bitmaps, tiles * kTile);
+  take(km.sums, tiles);
+  take(km.list, tiles);
+  take(km.row_cnt, km.krows);
+  take(km.order, km.krows);
+  take(km.occ, tiles);
+  take(km.run_off, km.krows);
+  take(km.run_len, km.krows);
+  take(km.row_stats, static_cast<uint64_t>(km.krows) * 3);
+  take(km.totals, 3);
+  take(km.scratch, static_cast<uint64_t>(km.krows) + km.kcols + 2);
+  km.arena_bytes = off;
+}
 
 Prep::~Prep() {
   int prev = -1;
   cudaGetDevice(&prev);
   cudaSetDevice(device);
+  cudaDeviceSynchronize();  // no queued launch may still read what is freed below
   delete pipe;
-  free_kernel_meta(kmeta);
+  cudaFree(kmeta.arena);
   free_bwd_meta(bwd);
-  cudaFree(work_ctr);
-  cudaFree(workspace);
-  for (auto& kv : plans) {
-    cudaFree(kv.second.unit_desc);
-    cudaFree(kv.second.split_info);
-    cudaFree(kv.second.split_ctr);
-    cudaFree(kv.second.empty_list);
+  for (auto& kv : streams) {
+    StreamCtx& c = kv.second;
+    cudaFree(c.ctr);
+    cudaFree(c.ws);
+    cudaFree(c.split_ctr);
+    cudaFree(c.rowws);
+    if (c.done) cudaEventDestroy(c.done);
+    for (auto& pl : c.plans) cudaFree(pl.second.mem);
   }
+  if (ready) cudaEventDestroy(ready);
   if (prev >= 0) cudaSetDevice(prev);
 }
 
-void refresh_kernel_view(const Prep& pr, cudaStream_t s) {
-  if (!pr.kview_stale) return;
-  std::vector<uint32_t> cnt(pr.kmeta.krows);
-  BBM_CUDA(cudaMemcpyAsync(cnt.data(), pr.kmeta.row_cnt, cnt.size() * 4, cudaMemcpyDeviceToHost, s));
-  BBM_CUDA(cudaStreamSynchronize(s));
-  {  // plans depend on the counts and (masked split points) on the lists: rebuild them
-    for (auto& kv : pr.plans) {
-      cudaFree(kv.second.unit_desc);
-      cudaFree(kv.second.split_info);
-      cudaFree(kv.second.split_ctr);
-      cudaFree(kv.second.empty_list);
-    }
-    pr.plans.clear();
-    pr.h_row_cnt = cnt;
+StreamCtx& Prep::ctx_for(cudaStream_t s) const {
+  auto it = streams.find(s);
+  if (it == streams.end()) {
+    StreamCtx c;
+    c.ctr = dmalloc<uint32_t>(8);
+    BBM_CUDA(cudaMemsetAsync(c.ctr, 0, 8 * sizeof(uint32_t), s));
+    BBM_CUDA(cudaEventCreateWithFlags(&c.done, cudaEventDisableTiming));
+    it = streams.emplace(s, c).first;
   }
-  const_cast<Prep&>(pr).bwd.built = false;  // column view follows the new mask on next use
-  pr.kview_stale = false;
+  StreamCtx& c = it->second;
+  if (c.seen_version != version) {
+    BBM_CUDA(cudaStreamWaitEvent(s, ready, 0));
+    c.seen_version = version;
+  }
+  return c;
+}
+
+void mark_launch_done(StreamCtx& ctx, cudaStream_t s) { BBM_CUDA(cudaEventRecord(ctx.done, s)); }
+
+const SpecMeta& Prep::spec_now() const {
+  std::lock_guard<std::recursive_mutex> lk(mu);
+  if (spec_version == version) return spec;
+  DeviceGuard g(device);
+  BBM_CUDA(cudaEventSynchronize(ready));
+  const KernelMeta& km = kmeta;
+  SpecMeta sp;
+  sp.bi = bi;
+  sp.bj = bj;
+  sp.rows = (n + bi - 1) / bi;
+  sp.cols = (n + bj - 1) / bj;
+  const bool same = (bi == kTile && bj == kTile);
+  const uint64_t tiles = sp.rows * sp.cols;
+  cudaStream_t s;
+  BBM_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  uint8_t* tmp = nullptr;
+  auto release = [&] {
+    if (tmp) cudaFree(tmp);
+    cudaStreamDestroy(s);
+  };
+  try {
+    uint32_t *d_sums = km.sums, *d_off = km.run_off, *d_tot = km.run_len;
+    uint8_t* d_occ = km.occ;
+    uint64_t *d_stats = km.row_stats, *d_totals = km.totals;
+    if (!same) {  // the caller's BlockSpec from the padded mask (any spec, mask.hpp:184-247)
+      const size_t b_sums = tiles * 4, b_occ = (tiles + 7) / 8 * 8, b_rows = sp.rows * 4;
+      BBM_CUDA(cudaMalloc(&tmp, b_sums + b_occ + 2 * b_rows + sp.rows * 24 + 24 + 64));
+      d_sums = reinterpret_cast<uint32_t*>(tmp);
+      d_occ = tmp + b_sums;
+      d_off = reinterpret_cast<uint32_t*>(tmp + b_sums + b_occ);
+      d_tot = d_off + sp.rows;
+      d_stats = reinterpret_cast<uint64_t*>((reinterpret_cast<uintptr_t>(d_tot + sp.rows) + 7) / 8 * 8);
+      d_totals = d_stats + sp.rows * 3;
+      launch_sums_generic(km, n, bi, bj, sp.rows, sp.cols, d_sums, s);
+      launch_rowmeta(d_sums, n, bi, bj, sp.rows, sp.cols, d_occ, d_off, d_tot, d_stats, nullptr,
+                     nullptr, s);
+      launch_finalize(d_stats, sp.rows, nullptr, nullptr, d_totals, s);
+    }
+    sp.sums.resize(tiles);
+    sp.occ.resize(tiles);
+    sp.offset.resize(sp.rows);
+    sp.total_ones.resize(sp.rows);
+    uint64_t totals[3] = {0, 0, 0}, ktotals[3] = {0, 0, 0};
+    BBM_CUDA(cudaMemcpyAsync(sp.sums.data(), d_sums, tiles * 4, cudaMemcpyDeviceToHost, s));
+    BBM_CUDA(cudaMemcpyAsync(sp.occ.data(), d_occ, tiles, cudaMemcpyDeviceToHost, s));
+    BBM_CUDA(cudaMemcpyAsync(sp.offset.data(), d_off, sp.rows * 4, cudaMemcpyDeviceToHost, s));
+    BBM_CUDA(cudaMemcpyAsync(sp.total_ones.data(), d_tot, sp.rows * 4, cudaMemcpyDeviceToHost, s));
+    BBM_CUDA(cudaMemcpyAsync(totals, d_totals, 24, cudaMemcpyDeviceToHost, s));
+    BBM_CUDA(cudaMemcpyAsync(ktotals, km.totals, 24, cudaMemcpyDeviceToHost, s));
+    BBM_CUDA(cudaStreamSynchronize(s));
+    sp.blocks_total = tiles;
+    sp.blocks_nonzero = totals[0];
+    sp.blocks_full = totals[1];
+    sp.ones = totals[2];
+    sp.knnz = ktotals[0];
+    sp.kfull = ktotals[1];
+  } catch (...) {
+    release();
+    throw;
+  }
+  release();
+  spec = std::move(sp);
+  spec_version = version;
+  return spec;
 }
 
 }  // namespace bbm
@@ -240,8 +262,9 @@ using namespace bbm;
 
 struct bbm_prep_s {
   std::unique_ptr<Prep> p;
-  // replicas on other devices for the multi-GPU driver, created lazily
-  std::vector<std::unique_ptr<bbm_prep_s>> replicas;
+  // replicas on other devices for the multi-GPU driver, created lazily per mask version; shared
+  // so that a driver call still running on them survives an update that drops the cache
+  std::vector<std::shared_ptr<bbm_prep_s>> replicas;
 };
 
 namespace bbm_capi_detail {
@@ -260,6 +283,9 @@ void check_attn_args(const Prep& pr, int variant, uint64_t slots, uint32_t d, do
   require(variant >= 0 && variant <= 3, "unknown variant");
   require(slots >= 1, "need at least one batch/head slot");  // engine.hpp:493
   require(std::isfinite(scale), "scale must be finite");     // engine.hpp:253
+  // documented narrowing: the kernels scale scores in fp32 log2 units
+  require(std::isfinite(static_cast<float>(scale) * 1.4426950408889634f),
+          "scale outside the fp32 range of the sm_100a kernel");
   if (d != 64 && d != 128)
     throw ArgError("head dim " + std::to_string(d) +
                    " unsupported by the sm_100a kernel (64 or 128; d_v must equal d_k)");
@@ -297,6 +323,49 @@ unsigned grid_of(uint64_t count) {
   return static_cast<unsigned>(std::max<uint64_t>(1, std::min<uint64_t>(g, 148ull * 16)));
 }
 
+// Creation: the padded mask (and 128x128 sums) are on `s`; build the kernel view, publish the
+// first version and compute the caller-spec host metadata (one sync, like the reference's
+// synchronous preprocess_mask).
+bbm_prep finish_prep(std::unique_ptr<Prep> pr, cudaStream_t s) {
+  build_kernel_view(pr->kmeta, pr->n, s);
+  BBM_CUDA(cudaEventRecord(pr->ready, s));
+  pr->spec_now();
+  return wrap(pr.release());
+}
+
+// Updates rebuild the kernel view of the SAME prep for a new mask of the same n, asynchronously
+// on `stream`: ordered after every queued launch that reads the prep, then published as a new
+// version. Later launches on any stream wait for it; getters and counters recompute the
+// caller-spec metadata; replicas made for the multi-GPU driver are dropped (they hold the old
+// mask) and re-made on their next use.
+template <class Fill>
+void update_prep(bbm_prep h, void* stream, Fill&& fill) {
+  Prep& pr = unwrap(h);
+  std::lock_guard<std::recursive_mutex> lk(pr.mu);
+  DeviceGuard g(pr.device);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  order_update_after_launches(pr, s);
+  fill(pr, s);
+  build_kernel_view(pr.kmeta, pr.n, s);
+  publish_version(pr, s);
+  h->replicas.clear();
+}
+
+// IPC form of the replication, for one process per GPU (torchrun): the exporter publishes the
+// arena's cudaIpcMemHandle plus the host metadata as one flat blob, the importer copies the arena
+// peer to peer into its own prep. The exporter's prep must stay alive and un-updated until every
+// importer has returned.
+constexpr uint64_t kIpcMagic = 0x3150494D4D4242ull;  // "BBMMIP1"
+struct IpcHeader {
+  uint64_t magic, abi, n, bi, bj, arena_bytes, rows, cols;
+  uint64_t blocks_total, blocks_nonzero, blocks_full, ones, knnz, kfull;
+  cudaIpcMemHandle_t handle;
+};
+size_t ipc_size(const SpecMeta& sp) {
+  return sizeof(IpcHeader) + sp.sums.size() * 4 + sp.occ.size() + sp.offset.size() * 4 +
+         sp.total_ones.size() * 4;
+}
+
 }  // namespace bbm_capi_detail
 using namespace bbm_capi_detail;
 
@@ -324,19 +393,23 @@ bbm_status bbm_preprocess_packed_host(const uint64_t* words, uint64_t n, uint64_
     validate_spec(n, bi, bj);
     require(words != nullptr && out != nullptr, "null argument");
     DeviceGuard g(device);
-    std::unique_ptr<Prep> pr(new_prep(n, device));
+    std::unique_ptr<Prep> pr(new_prep(n, device, bi, bj));
     const KernelMeta& km = pr->kmeta;
     cudaStream_t s;
     BBM_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
-    const uint64_t wpr = (n + 63) / 64, pad_wpr = static_cast<uint64_t>(km.kcols) * 2;
-    const uint64_t rows_pad = static_cast<uint64_t>(km.krows) * kTile;
-    BBM_CUDA(cudaMemsetAsync(km.mask, 0, rows_pad * pad_wpr * 8, s));
-    BBM_CUDA(cudaMemcpy2DAsync(km.mask, pad_wpr * 8, words, wpr * 8, wpr * 8, n,
-                               cudaMemcpyHostToDevice, s));
-    launch_sums128(km, s);
-    build_metadata(*pr, bi, bj, s);
+    try {
+      const uint64_t wpr = (n + 63) / 64, pad_wpr = static_cast<uint64_t>(km.kcols) * 2;
+      const uint64_t rows_pad = static_cast<uint64_t>(km.krows) * kTile;
+      BBM_CUDA(cudaMemsetAsync(km.mask, 0, rows_pad * pad_wpr * 8, s));
+      BBM_CUDA(cudaMemcpy2DAsync(km.mask, pad_wpr * 8, words, wpr * 8, wpr * 8, n,
+                                 cudaMemcpyHostToDevice, s));
+      launch_sums128(km, s);
+      *out = finish_prep(std::move(pr), s);
+    } catch (...) {
+      cudaStreamDestroy(s);
+      throw;
+    }
     BBM_CUDA(cudaStreamDestroy(s));
-    *out = wrap(pr.release());
   });
 }
 
@@ -347,12 +420,11 @@ bbm_status bbm_preprocess_packed_device(const uint64_t* d_words, uint64_t n, uin
     require(d_words != nullptr && out != nullptr, "null argument");
     int dev = 0;
     BBM_CUDA(cudaGetDevice(&dev));
-    std::unique_ptr<Prep> pr(new_prep(n, dev));
+    std::unique_ptr<Prep> pr(new_prep(n, dev, bi, bj));
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     launch_pad_packed(d_words, n, pr->kmeta, s);
     launch_sums128(pr->kmeta, s);
-    build_metadata(*pr, bi, bj, s);
-    *out = wrap(pr.release());
+    *out = finish_prep(std::move(pr), s);
   });
 }
 
@@ -364,11 +436,10 @@ bbm_status bbm_preprocess_bool_device(const uint8_t* d_mask, uint64_t n, uint64_
     require(row_stride >= n, "row stride must be >= n");
     int dev = 0;
     BBM_CUDA(cudaGetDevice(&dev));
-    std::unique_ptr<Prep> pr(new_prep(n, dev));
+    std::unique_ptr<Prep> pr(new_prep(n, dev, bi, bj));
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     launch_pack_bool(d_mask, n, row_stride, pr->kmeta, s);
-    build_metadata(*pr, bi, bj, s);
-    *out = wrap(pr.release());
+    *out = finish_prep(std::move(pr), s);
   });
 }
 
@@ -377,22 +448,17 @@ bbm_status bbm_prep_update_bool_device(bbm_prep prep, const uint8_t* d_mask, uin
   return guarded([&] {
     Prep& pr = unwrap(prep);
     require(d_mask != nullptr && row_stride >= pr.n, "bad mask argument");
-    cudaStream_t s = static_cast<cudaStream_t>(stream);
-    launch_pack_bool(d_mask, pr.n, row_stride, pr.kmeta, s);
-    build_kernel_view(pr.kmeta, pr.n, s);
-    pr.kview_stale = true;
+    update_prep(prep, stream, [&](Prep& p, cudaStream_t s) { launch_pack_bool(d_mask, p.n, row_stride, p.kmeta, s); });
   });
 }
 
 bbm_status bbm_prep_update_packed_device(bbm_prep prep, const uint64_t* d_words, void* stream) {
   return guarded([&] {
-    Prep& pr = unwrap(prep);
     require(d_words != nullptr, "bad mask argument");
-    cudaStream_t s = static_cast<cudaStream_t>(stream);
-    launch_pad_packed(d_words, pr.n, pr.kmeta, s);
-    launch_sums128(pr.kmeta, s);
-    build_kernel_view(pr.kmeta, pr.n, s);
-    pr.kview_stale = true;
+    update_prep(prep, stream, [&](Prep& p, cudaStream_t s) {
+      launch_pad_packed(d_words, p.n, p.kmeta, s);
+      launch_sums128(p.kmeta, s);
+    });
   });
 }
 
@@ -403,55 +469,56 @@ bbm_status bbm_prep_destroy(bbm_prep prep) {
 bbm_status bbm_prep_get_info(bbm_prep prep, bbm_prep_info* info) {
   return guarded([&] {
     const Prep& pr = unwrap(prep);
+    const SpecMeta& sp = pr.spec_now();
     info->n = pr.n;
-    info->block_i = pr.spec.bi;
-    info->block_j = pr.spec.bj;
-    info->rows = pr.spec.rows;
-    info->cols = pr.spec.cols;
+    info->block_i = sp.bi;
+    info->block_j = sp.bj;
+    info->rows = sp.rows;
+    info->cols = sp.cols;
     info->ktile = kTile;
     info->krows = pr.kmeta.krows;
     info->kcols = pr.kmeta.kcols;
-    info->knnz = pr.kmeta.nnz;
-    info->kfull = pr.kmeta.full;
+    info->knnz = sp.knnz;
+    info->kfull = sp.kfull;
     info->device = pr.device;
   });
 }
 
 bbm_status bbm_prep_get_sums(bbm_prep prep, uint32_t* sums) {
   return guarded([&] {
-    const Prep& pr = unwrap(prep);
-    std::memcpy(sums, pr.spec.sums.data(), pr.spec.sums.size() * 4);
+    const SpecMeta& sp = unwrap(prep).spec_now();
+    std::memcpy(sums, sp.sums.data(), sp.sums.size() * 4);
   });
 }
 
 bbm_status bbm_prep_get_occupancy(bbm_prep prep, uint8_t* occ) {
   return guarded([&] {
-    const Prep& pr = unwrap(prep);
-    std::memcpy(occ, pr.spec.occ.data(), pr.spec.occ.size());
+    const SpecMeta& sp = unwrap(prep).spec_now();
+    std::memcpy(occ, sp.occ.data(), sp.occ.size());
   });
 }
 
 bbm_status bbm_prep_get_runs(bbm_prep prep, uint32_t* offset, uint32_t* total_ones) {
   return guarded([&] {
-    const Prep& pr = unwrap(prep);
-    if (offset) std::memcpy(offset, pr.spec.offset.data(), pr.spec.offset.size() * 4);
-    if (total_ones)
-      std::memcpy(total_ones, pr.spec.total_ones.data(), pr.spec.total_ones.size() * 4);
+    const SpecMeta& sp = unwrap(prep).spec_now();
+    if (offset) std::memcpy(offset, sp.offset.data(), sp.offset.size() * 4);
+    if (total_ones) std::memcpy(total_ones, sp.total_ones.data(), sp.total_ones.size() * 4);
   });
 }
 
 bbm_status bbm_prep_get_stats(bbm_prep prep, bbm_block_stats* st) {
   return guarded([&] {
     const Prep& pr = unwrap(prep);
+    const SpecMeta& sp = pr.spec_now();
     // block_stats (mask.hpp:230-247): same double expressions as the reference
-    st->blocks_total = pr.spec.blocks_total;
-    st->blocks_nonzero = pr.spec.blocks_nonzero;
-    st->blocks_full = pr.spec.blocks_full;
+    st->blocks_total = sp.blocks_total;
+    st->blocks_nonzero = sp.blocks_nonzero;
+    st->blocks_full = sp.blocks_full;
     const double nd = static_cast<double>(pr.n);
     st->block_density = st->blocks_total ? static_cast<double>(st->blocks_nonzero) /
                                                static_cast<double>(st->blocks_total)
                                          : 0.0;
-    st->element_density = nd > 0 ? static_cast<double>(pr.spec.ones) / (nd * nd) : 0.0;
+    st->element_density = nd > 0 ? static_cast<double>(sp.ones) / (nd * nd) : 0.0;
   });
 }
 
@@ -459,7 +526,9 @@ bbm_status bbm_prep_get_kernel_lists(bbm_prep prep, uint32_t* row_cnt, uint32_t*
                                      uint32_t* order) {
   return guarded([&] {
     const Prep& pr = unwrap(prep);
+    std::lock_guard<std::recursive_mutex> lk(pr.mu);
     DeviceGuard g(pr.device);
+    BBM_CUDA(cudaEventSynchronize(pr.ready));
     const KernelMeta& km = pr.kmeta;
     if (row_cnt) BBM_CUDA(cudaMemcpy(row_cnt, km.row_cnt, km.krows * 4, cudaMemcpyDeviceToHost));
     if (list)
@@ -475,7 +544,7 @@ bbm_status bbm_prep_counters(bbm_prep prep, int variant, uint64_t slots, bbm_cou
     require(variant >= 0 && variant <= 3, "unknown variant");
     // classify_tile (engine.hpp:118-153) summed over every tile of the caller's BlockSpec:
     // counts depend on the mask and spec only (engine.hpp:47-48).
-    const SpecMeta& sp = pr.spec;
+    const SpecMeta& sp = pr.spec_now();
     uint64_t run_blocks = 0;
     for (uint32_t t : sp.total_ones) run_blocks += t;
     bbm_counters one{};
@@ -565,14 +634,11 @@ bbm_status bbm_sums_metadata(const uint32_t* sums, uint64_t n, uint64_t bi, uint
 bbm_status bbm_prep_replicate(bbm_prep prep, int device, void* stream, bbm_prep* out) {
   return guarded([&] {
     const Prep& src = unwrap(prep);
+    require(out != nullptr, "null argument");
+    std::lock_guard<std::recursive_mutex> lk(src.mu);
+    const SpecMeta& sp = src.spec_now();  // host metadata of the current version
     DeviceGuard g(device);
-    std::unique_ptr<Prep> dst(new_prep(src.n, device));
-    dst->spec = src.spec;
-    dst->h_row_cnt = src.h_row_cnt;
-    KernelMeta& a = dst->kmeta;
-    const KernelMeta& b = src.kmeta;
-    a.nnz = b.nnz;
-    a.full = b.full;
+    std::unique_ptr<Prep> dst(new_prep(src.n, device, src.bi, src.bj));
     if (device != src.device) {
       int can = 0;
       BBM_CUDA(cudaDeviceCanAccessPeer(&can, device, src.device));
@@ -583,17 +649,110 @@ bbm_status bbm_prep_replicate(bbm_prep prep, int device, void* stream, bbm_prep*
       }
     }
     cudaStream_t s = static_cast<cudaStream_t>(stream);
-    const uint64_t tiles = static_cast<uint64_t>(b.krows) * b.kcols;
-    auto peer = [&](void* d, const void* sp, uint64_t bytes) {
-      BBM_CUDA(cudaMemcpyPeerAsync(d, device, sp, src.device, bytes, s));
-    };
-    peer(a.mask, b.mask, static_cast<uint64_t>(b.krows) * kTile * b.kcols * 16);
-    peer(a.sums, b.sums, tiles * 4);
-    peer(a.row_cnt, b.row_cnt, b.krows * 4);
-    peer(a.list, b.list, tiles * 4);
-    peer(a.order, b.order, b.krows * 4);
-    peer(a.bitmaps, b.bitmaps, tiles * kTile * 16);
+    // the whole kernel view is one arena: a single peer copy over NVLink / NVSwitch, ordered
+    // after the source's latest metadata write
+    BBM_CUDA(cudaStreamWaitEvent(s, src.ready, 0));
+    BBM_CUDA(cudaMemcpyPeerAsync(dst->kmeta.arena, device, src.kmeta.arena, src.device,
+                                 src.kmeta.arena_bytes, s));
+    BBM_CUDA(cudaEventRecord(dst->ready, s));
     BBM_CUDA(cudaStreamSynchronize(s));
+    dst->spec = sp;
+    dst->spec_version = dst->version;
+    *out = wrap(dst.release());
+  });
+}
+
+bbm_status bbm_prep_export_ipc(bbm_prep prep, void* blob, size_t* size) {
+  return guarded([&] {
+    const Prep& pr = unwrap(prep);
+    require(size != nullptr, "null size");
+    std::lock_guard<std::recursive_mutex> lk(pr.mu);
+    const SpecMeta& sp = pr.spec_now();  // synchronizes with the latest metadata version
+    const size_t need = ipc_size(sp);
+    if (blob == nullptr) {
+      *size = need;
+      return;
+    }
+    require(*size >= need, "IPC blob buffer too small");
+    DeviceGuard g(pr.device);
+    IpcHeader h{};
+    h.magic = kIpcMagic;
+    h.abi = BBM_ABI_VERSION;
+    h.n = pr.n;
+    h.bi = pr.bi;
+    h.bj = pr.bj;
+    h.arena_bytes = pr.kmeta.arena_bytes;
+    h.rows = sp.rows;
+    h.cols = sp.cols;
+    h.blocks_total = sp.blocks_total;
+    h.blocks_nonzero = sp.blocks_nonzero;
+    h.blocks_full = sp.blocks_full;
+    h.ones = sp.ones;
+    h.knnz = sp.knnz;
+    h.kfull = sp.kfull;
+    BBM_CUDA(cudaIpcGetMemHandle(&h.handle, pr.kmeta.arena));
+    uint8_t* b = static_cast<uint8_t*>(blob);
+    std::memcpy(b, &h, sizeof(h));
+    b += sizeof(h);
+    auto put = [&](const void* src, size_t bytes) {
+      std::memcpy(b, src, bytes);
+      b += bytes;
+    };
+    put(sp.sums.data(), sp.sums.size() * 4);
+    put(sp.occ.data(), sp.occ.size());
+    put(sp.offset.data(), sp.offset.size() * 4);
+    put(sp.total_ones.data(), sp.total_ones.size() * 4);
+    *size = need;
+  });
+}
+
+bbm_status bbm_prep_import_ipc(const void* blob, size_t size, int device, void* stream,
+                               bbm_prep* out) {
+  return guarded([&] {
+    require(blob != nullptr && out != nullptr && size >= sizeof(IpcHeader), "bad IPC blob");
+    IpcHeader h;
+    std::memcpy(&h, blob, sizeof(h));
+    require(h.magic == kIpcMagic && h.abi == BBM_ABI_VERSION, "not a bbm prep IPC blob");
+    validate_spec(h.n, h.bi, h.bj);
+    SpecMeta sp;
+    sp.bi = h.bi;
+    sp.bj = h.bj;
+    sp.rows = h.rows;
+    sp.cols = h.cols;
+    sp.blocks_total = h.blocks_total;
+    sp.blocks_nonzero = h.blocks_nonzero;
+    sp.blocks_full = h.blocks_full;
+    sp.ones = h.ones;
+    sp.knnz = h.knnz;
+    sp.kfull = h.kfull;
+    const uint64_t tiles = h.rows * h.cols;
+    sp.sums.resize(tiles);
+    sp.occ.resize(tiles);
+    sp.offset.resize(h.rows);
+    sp.total_ones.resize(h.rows);
+    require(size >= ipc_size(sp), "truncated IPC blob");
+    const uint8_t* b = static_cast<const uint8_t*>(blob) + sizeof(h);
+    auto get = [&](void* dst, size_t bytes) {
+      std::memcpy(dst, b, bytes);
+      b += bytes;
+    };
+    get(sp.sums.data(), tiles * 4);
+    get(sp.occ.data(), tiles);
+    get(sp.offset.data(), h.rows * 4);
+    get(sp.total_ones.data(), h.rows * 4);
+    DeviceGuard g(device);
+    std::unique_ptr<Prep> dst(new_prep(h.n, device, h.bi, h.bj));
+    require(dst->kmeta.arena_bytes == h.arena_bytes, "IPC blob from an incompatible build");
+    void* peer = nullptr;
+    BBM_CUDA(cudaIpcOpenMemHandle(&peer, h.handle, cudaIpcMemLazyEnablePeerAccess));
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const cudaError_t e1 = cudaMemcpyAsync(dst->kmeta.arena, peer, h.arena_bytes, cudaMemcpyDeviceToDevice, s);
+    const cudaError_t e2 = e1 == cudaSuccess ? cudaStreamSynchronize(s) : e1;
+    cudaIpcCloseMemHandle(peer);
+    BBM_CUDA(e2);
+    BBM_CUDA(cudaEventRecord(dst->ready, s));
+    dst->spec = std::move(sp);
+    dst->spec_version = dst->version;
     *out = wrap(dst.release());
   });
 }
@@ -649,65 +808,39 @@ bbm_status bbm_attn_fwd_host_f32(bbm_prep prep, int variant, const float* q, con
   return guarded([&] {
     const Prep& pr = unwrap(prep);
     check_attn_args(pr, variant, slots, head_dim, scale);
+    require(q && k && v && out, "null tensor pointer");
+    const uint64_t per = pr.n * head_dim;
+    std::vector<const float*> pq(slots), pk(slots), pv(slots);
+    std::vector<float*> po(slots);
+    std::vector<double*> pm(slots), ps(slots);
+    for (uint64_t i = 0; i < slots; ++i) {
+      pq[i] = q + i * per;
+      pk[i] = k + i * per;
+      pv[i] = v + i * per;
+      po[i] = out + i * per;
+      pm[i] = row_max ? row_max + i * pr.n : nullptr;
+      ps[i] = row_sum ? row_sum + i * pr.n : nullptr;
+    }
     DeviceGuard g(pr.device);
-    cudaStream_t s;
-    BBM_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
-    const uint64_t elems = slots * pr.n * head_dim, rows = slots * pr.n;
-    float* stage;
-    __nv_bfloat16 *dq, *dk, *dv, *dout;
-    float *dmax, *dsum;
-    int* dbad;
-    BBM_CUDA(cudaMallocAsync(&stage, elems * 4, s));
-    BBM_CUDA(cudaMallocAsync(&dq, elems * 2, s));
-    BBM_CUDA(cudaMallocAsync(&dk, elems * 2, s));
-    BBM_CUDA(cudaMallocAsync(&dv, elems * 2, s));
-    BBM_CUDA(cudaMallocAsync(&dout, elems * 2, s));
-    BBM_CUDA(cudaMallocAsync(&dmax, rows * 4, s));
-    BBM_CUDA(cudaMallocAsync(&dsum, rows * 4, s));
-    BBM_CUDA(cudaMallocAsync(&dbad, 4 * 3, s));
-    BBM_CUDA(cudaMemsetAsync(dbad, 0, 12, s));
-    const float* srcs[3] = {q, k, v};
-    __nv_bfloat16* dsts[3] = {dq, dk, dv};
-    for (int t = 0; t < 3; ++t) {
-      BBM_CUDA(cudaMemcpyAsync(stage, srcs[t], elems * 4, cudaMemcpyHostToDevice, s));
-      f32_to_bf16_kernel<<<grid_of(elems), 256, 0, s>>>(stage, dsts[t], elems, dbad + t);
-      BBM_CUDA(cudaGetLastError());
-    }
-    int bad[3] = {0, 0, 0};
-    BBM_CUDA(cudaMemcpyAsync(bad, dbad, 12, cudaMemcpyDeviceToHost, s));
-    BBM_CUDA(cudaStreamSynchronize(s));
-    auto release = [&] {
-      cudaFreeAsync(stage, s);
-      cudaFreeAsync(dq, s);
-      cudaFreeAsync(dk, s);
-      cudaFreeAsync(dv, s);
-      cudaFreeAsync(dout, s);
-      cudaFreeAsync(dmax, s);
-      cudaFreeAsync(dsum, s);
-      cudaFreeAsync(dbad, s);
-      cudaStreamSynchronize(s);
-      cudaStreamDestroy(s);
-    };
-    static const char* names[3] = {"q", "k", "v"};
-    for (int t = 0; t < 3; ++t)
-      if (bad[t]) {  // require_finite (engine.hpp:237-242)
-        release();
-        throw ArgError(std::string(names[t]) + " must hold finite values");
-      }
-    AttnArgs a{dq, dk, dv, dout, dmax, dsum, slots, pr.n, head_dim, static_cast<float>(scale),
-               variant};
-    launch_attn_fwd(pr, a, s, sm_count(pr.device));
-    bf16_to_f32_kernel<<<grid_of(elems), 256, 0, s>>>(dout, stage, elems);
-    BBM_CUDA(cudaGetLastError());
-    BBM_CUDA(cudaMemcpyAsync(out, stage, elems * 4, cudaMemcpyDeviceToHost, s));
-    std::vector<float> hmax(rows), hsum(rows);
-    BBM_CUDA(cudaMemcpyAsync(hmax.data(), dmax, rows * 4, cudaMemcpyDeviceToHost, s));
-    BBM_CUDA(cudaMemcpyAsync(hsum.data(), dsum, rows * 4, cudaMemcpyDeviceToHost, s));
-    release();
-    for (uint64_t i = 0; i < rows; ++i) {
-      if (row_max) row_max[i] = static_cast<double>(hmax[i]);
-      if (row_sum) row_sum[i] = static_cast<double>(hsum[i]);
-    }
+    run_fwd_host_f32(pr, variant, pq.data(), pk.data(), pv.data(), po.data(), pm.data(), ps.data(),
+                     slots, head_dim, static_cast<float>(scale), sm_count(pr.device), nullptr);
+  });
+}
+
+bbm_status bbm_run_attention_host_f32(bbm_prep prep, int variant, const float* const* q,
+                                      const float* const* k, const float* const* v,
+                                      float* const* out, double* const* row_max,
+                                      double* const* row_sum, uint64_t slots, uint32_t head_dim,
+                                      double scale) {
+  return guarded([&] {
+    const Prep& pr = unwrap(prep);
+    check_attn_args(pr, variant, slots, head_dim, scale);
+    require(q && k && v && out, "null slot array");
+    for (uint64_t i = 0; i < slots; ++i)
+      require(q[i] && k[i] && v[i] && out[i], "null tensor pointer in slot " + std::to_string(i));
+    DeviceGuard g(pr.device);
+    run_fwd_host_f32(pr, variant, q, k, v, out, row_max, row_sum, slots, head_dim,
+                     static_cast<float>(scale), sm_count(pr.device), nullptr);
   });
 }
 
@@ -716,15 +849,13 @@ bbm_status bbm_attn_bwd(bbm_prep prep, int variant, const void* q, const void* k
                         const void* d_out, void* dq, void* dk, void* dv, uint64_t slots,
                         uint32_t head_dim, double scale, void* stream) {
   return guarded([&] {
-    Prep& pr = unwrap(prep);
+    const Prep& pr = unwrap(prep);
     check_attn_args(pr, variant, slots, head_dim, scale);
     require(q && k && v && out && row_max && row_sum && d_out && dq && dk && dv, "null tensor pointer");
     int dev = 0;
     BBM_CUDA(cudaGetDevice(&dev));
     require(dev == pr.device, "prep lives on another device; use bbm_prep_replicate");
     cudaStream_t s = static_cast<cudaStream_t>(stream);
-    refresh_kernel_view(pr, s);
-    build_bwd_meta(pr, s);
     BwdArgs a{q, k, v, out, false, row_max, row_sum, d_out, dq, dk, dv, slots, pr.n, head_dim,
               static_cast<float>(scale), variant};
     launch_attn_bwd(pr, a, s, sm_count(dev));
@@ -736,7 +867,7 @@ bbm_status bbm_attn_bwd_host_f32(bbm_prep prep, int variant, const float* q, con
                                  const double* row_sum, const float* d_out, float* dq, float* dk,
                                  float* dv, uint64_t slots, uint32_t head_dim, double scale) {
   return guarded([&] {
-    Prep& pr = unwrap(prep);
+    const Prep& pr = unwrap(prep);
     check_attn_args(pr, variant, slots, head_dim, scale);
     require(q && k && v && out && row_max && row_sum && d_out && dq && dk && dv, "null tensor pointer");
     DeviceGuard g(pr.device);
@@ -786,8 +917,6 @@ bbm_status bbm_attn_bwd_host_f32(bbm_prep prep, int variant, const float* q, con
       static const char* names[4] = {"q", "k", "v", "d_out"};
       for (int t = 0; t < 4; ++t)  // require_finite (engine.hpp:237-242, 358)
         if (hbad[t]) throw ArgError(std::string(names[t]) + " must hold finite values");
-      refresh_kernel_view(pr, s);
-      build_bwd_meta(pr, s);
       BwdArgs a{b[0], b[1], b[2], o32, true, rm, rs, b[3], g3[0], g3[1], g3[2], slots, pr.n, head_dim,
                 static_cast<float>(scale), variant};
       launch_attn_bwd(pr, a, s, sm_count(pr.device));
@@ -815,24 +944,30 @@ bbm_status bbm_run_attention_multi(bbm_prep prep, int variant, int n_devices, co
     check_attn_args(pr, variant, slots, head_dim, scale);
     require(n_devices >= 1 && devices != nullptr, "need at least one device");
     const uint64_t per_slot = pr.n * head_dim;
-    // replicate metadata peer-to-peer once per device (cached on the handle)
+    // replicate metadata peer-to-peer once per device and mask version (cached on the handle;
+    // bbm_prep_update_* drops the cache)
     std::vector<bbm_prep> preps(n_devices);
-    for (int g = 0; g < n_devices; ++g) {
-      if (devices[g] == pr.device) {
-        preps[g] = prep;
-        continue;
+    std::vector<std::shared_ptr<bbm_prep_s>> hold;
+    {
+      std::lock_guard<std::recursive_mutex> lk(pr.mu);
+      for (int g = 0; g < n_devices; ++g) {
+        if (devices[g] == pr.device) {
+          preps[g] = prep;
+          continue;
+        }
+        std::shared_ptr<bbm_prep_s> found;
+        for (auto& r : prep->replicas)
+          if (r->p->device == devices[g]) found = r;
+        if (!found) {
+          bbm_prep rep = nullptr;
+          const bbm_status st = bbm_prep_replicate(prep, devices[g], nullptr, &rep);
+          if (st != BBM_OK) throw CudaError(g_last_error);
+          found.reset(rep);
+          prep->replicas.push_back(found);
+        }
+        hold.push_back(found);
+        preps[g] = found.get();
       }
-      bbm_prep found = nullptr;
-      for (auto& r : prep->replicas)
-        if (r->p->device == devices[g]) found = r.get();
-      if (!found) {
-        bbm_prep rep = nullptr;
-        const bbm_status st = bbm_prep_replicate(prep, devices[g], nullptr, &rep);
-        if (st != BBM_OK) throw CudaError(g_last_error);
-        prep->replicas.emplace_back(rep);
-        found = rep;
-      }
-      preps[g] = found;
     }
     // one host thread per GPU drives that GPU's copy/compute pipeline over its contiguous slot
     // range; shards share nothing (no collective), the span is max over GPUs of each device's

@@ -6,9 +6,11 @@
 // two PCIe directions). Device buffers persist in the prep and only grow, so a steady-state call
 // allocates nothing. With pinned host buffers the call costs about max(H2D, D2H) bytes over PCIe
 // plus one chunk of kernel time, instead of H2D + kernel + D2H.
+#include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <string>
 #include <cstdint>
 
 #include "bbm_internal.h"
@@ -22,6 +24,7 @@ HostPipe::~HostPipe() {
   if (comp) cudaStreamDestroy(comp);
   if (d2h) cudaStreamDestroy(d2h);
   cudaFree(buf);
+  cudaFree(bad);
 }
 
 namespace {
@@ -36,6 +39,7 @@ HostPipe& pipe_of(const Prep& prep) {
       BBM_CUDA(cudaStreamCreateWithFlags(&p->h2d, cudaStreamNonBlocking));
       BBM_CUDA(cudaStreamCreateWithFlags(&p->comp, cudaStreamNonBlocking));
       BBM_CUDA(cudaStreamCreateWithFlags(&p->d2h, cudaStreamNonBlocking));
+      BBM_CUDA(cudaMalloc(&p->bad, 4 * sizeof(int)));
       p->ev_in.resize(kMaxChunks);
       p->ev_out.resize(kMaxChunks);
       for (uint32_t c = 0; c < kMaxChunks; ++c) {
@@ -63,6 +67,81 @@ uint8_t* reserve(HostPipe& p, size_t bytes) {
   return p.buf;
 }
 
+// require_finite (engine.hpp:237-242) over bf16 data: exponent bits all ones = inf / NaN
+__global__ void check_finite_bf16_kernel(const uint16_t* __restrict__ x, uint64_t count,
+                                         int* __restrict__ bad) {
+  const uint64_t vecs = count / 8;
+  bool any = false;
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < vecs;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint4 v = __ldg(reinterpret_cast<const uint4*>(x) + i);
+    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+      any |= ((w[j] & 0x7F80u) == 0x7F80u) | ((w[j] & 0x7F800000u) == 0x7F800000u);
+  }
+  for (uint64_t i = vecs * 8 + blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < count;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
+    any |= (x[i] & 0x7F80u) == 0x7F80u;
+  if (__any_sync(0xffffffffu, any) && (threadIdx.x & 31) == 0) *bad = 1;
+}
+
+// float -> bf16 (RNE) fused with the finiteness check of the float input
+__global__ void f32_to_bf16_check_kernel(const float* __restrict__ in, __nv_bfloat16* __restrict__ out,
+                                         uint64_t count, int* __restrict__ bad) {
+  const uint64_t vecs = count / 4;
+  bool any = false;
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < vecs;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const float4 f = __ldg(reinterpret_cast<const float4*>(in) + i);
+    any |= !(isfinite(f.x) && isfinite(f.y) && isfinite(f.z) && isfinite(f.w));
+    __nv_bfloat162 lo = __floats2bfloat162_rn(f.x, f.y), hi = __floats2bfloat162_rn(f.z, f.w);
+    uint2 w;
+    w.x = *reinterpret_cast<uint32_t*>(&lo);
+    w.y = *reinterpret_cast<uint32_t*>(&hi);
+    reinterpret_cast<uint2*>(out)[i] = w;
+  }
+  for (uint64_t i = vecs * 4 + blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < count;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    any |= !isfinite(in[i]);
+    out[i] = __float2bfloat16_rn(in[i]);
+  }
+  if (__any_sync(0xffffffffu, any) && (threadIdx.x & 31) == 0) *bad = 1;
+}
+
+// bf16 O -> float, fp32 row statistics -> double (ForwardResult<float>, engine.hpp:93-99)
+__global__ void widen_outputs_kernel(const __nv_bfloat16* __restrict__ o, float* __restrict__ of,
+                                     uint64_t o_count, const float* __restrict__ m,
+                                     const float* __restrict__ l, double* __restrict__ md,
+                                     double* __restrict__ ld, uint64_t rows) {
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  const uint64_t t0 = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+  for (uint64_t i = t0; i < o_count / 8; i += stride) {
+    const uint4 v = __ldg(reinterpret_cast<const uint4*>(o) + i);
+    const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&v);
+    float4 a, b;
+    a.x = __low2float(h[0]), a.y = __high2float(h[0]), a.z = __low2float(h[1]), a.w = __high2float(h[1]);
+    b.x = __low2float(h[2]), b.y = __high2float(h[2]), b.z = __low2float(h[3]), b.w = __high2float(h[3]);
+    reinterpret_cast<float4*>(of)[2 * i] = a;
+    reinterpret_cast<float4*>(of)[2 * i + 1] = b;
+  }
+  for (uint64_t i = o_count / 8 * 8 + t0; i < o_count; i += stride) of[i] = __bfloat162float(o[i]);
+  for (uint64_t i = t0; i < rows; i += stride) {
+    if (md) md[i] = static_cast<double>(m[i]);
+    if (ld) ld[i] = static_cast<double>(l[i]);
+  }
+}
+
+unsigned grid_for_elems(uint64_t count) {
+  return static_cast<unsigned>(std::max<uint64_t>(1, std::min<uint64_t>((count / 8 + 255) / 256, 148ull * 16)));
+}
+
+void throw_if_bad(const int* hbad, int count) {
+  static const char* names[4] = {"q", "k", "v", "d_out"};
+  for (int t = 0; t < count; ++t)  // require_finite (engine.hpp:237-242)
+    if (hbad[t]) throw ArgError(std::string(names[t]) + " must hold finite values");
+}
+
 // dst[s][fwd[a]] = src[s][a]: scatter per-row statistics back to the original token order
 __global__ void scatter_rows_f32_kernel(const float* __restrict__ src, float* __restrict__ dst,
                                         const uint32_t* __restrict__ fwd, uint64_t slots, uint64_t n) {
@@ -78,7 +157,9 @@ __global__ void scatter_rows_f32_kernel(const float* __restrict__ src, float* __
 void run_fwd_host_pipelined(const Prep& prep, int variant, const uint16_t* q, const uint16_t* k,
                             const uint16_t* v, uint16_t* out, float* row_max, float* row_sum,
                             uint64_t slots, uint32_t d, float scale, int num_sms, double* span_ms) {
+  std::lock_guard<std::mutex> lk(prep.pipe_mu);
   HostPipe& p = pipe_of(prep);
+  BBM_CUDA(cudaMemsetAsync(p.bad, 0, 4 * sizeof(int), p.comp));
   const uint64_t n = prep.n, per = n * d, tbytes = slots * per * 2, sbytes = slots * n * 4;
   uint8_t* base = reserve(p, 4 * tbytes + 2 * sbytes);
   uint16_t* dq = reinterpret_cast<uint16_t*>(base);
@@ -103,6 +184,10 @@ void run_fwd_host_pipelined(const Prep& prep, int variant, const uint16_t* q, co
     BBM_CUDA(cudaMemcpyAsync(dv + off, v + off, bytes, cudaMemcpyHostToDevice, p.h2d));
     BBM_CUDA(cudaEventRecord(p.ev_in[c], p.h2d));
     BBM_CUDA(cudaStreamWaitEvent(p.comp, p.ev_in[c], 0));
+    const uint16_t* ins[3] = {dq + off, dk + off, dv + off};
+    for (int t = 0; t < 3; ++t)
+      check_finite_bf16_kernel<<<grid_for_elems(ns * per), 256, 0, p.comp>>>(ins[t], ns * per, p.bad + t);
+    BBM_CUDA(cudaGetLastError());
     AttnArgs a{dq + off, dk + off, dv + off, dout + off, row_max ? dmax + s0 * n : nullptr,
                row_sum ? dsum + s0 * n : nullptr, ns, n, d, scale, variant};
     launch_attn_fwd(prep, a, p.comp, num_sms);
@@ -115,6 +200,9 @@ void run_fwd_host_pipelined(const Prep& prep, int variant, const uint16_t* q, co
       BBM_CUDA(cudaMemcpyAsync(row_sum + s0 * n, dsum + s0 * n, ns * n * 4, cudaMemcpyDeviceToHost, p.d2h));
   }
   if (span_ms) BBM_CUDA(cudaEventRecord(t1, p.d2h));
+  int hbad[4] = {0, 0, 0, 0};
+  BBM_CUDA(cudaMemcpyAsync(hbad, p.bad, 3 * sizeof(int), cudaMemcpyDeviceToHost, p.comp));
+  BBM_CUDA(cudaStreamSynchronize(p.comp));
   BBM_CUDA(cudaStreamSynchronize(p.d2h));
   if (span_ms) {
     float ms = 0.0f;
@@ -123,8 +211,87 @@ void run_fwd_host_pipelined(const Prep& prep, int variant, const uint16_t* q, co
     cudaEventDestroy(t0);
     cudaEventDestroy(t1);
   }
+  throw_if_bad(hbad, 3);
 }
 
+// The reference's own signature, Matrix<float> in and out (engine.hpp:282-285, 489-505): per-slot
+// float host buffers (SlotInputs), rounded to bf16 on the device with the finiteness check fused
+// into the conversion, outputs widened back to float and the row statistics to double. Same
+// three-stream chunk pipeline as the bf16 path; the PCIe traffic is twice the bf16 form's.
+void run_fwd_host_f32(const Prep& prep, int variant, const float* const* q, const float* const* k,
+                      const float* const* v, float* const* out, double* const* row_max,
+                      double* const* row_sum, uint64_t slots, uint32_t d, float scale, int num_sms,
+                      double* span_ms) {
+  std::lock_guard<std::mutex> lk(prep.pipe_mu);
+  HostPipe& p = pipe_of(prep);
+  const bool want_max = row_max && row_max[0], want_sum = row_sum && row_sum[0];
+  const uint64_t n = prep.n, per = n * d, elems = slots * per, rows = slots * n;
+  // f32 in x3 | bf16 q k v o | f32 o | f32 max, sum | f64 max, sum
+  const size_t b_in = elems * 4, b_bf = elems * 2;
+  uint8_t* base = reserve(p, 3 * b_in + 4 * b_bf + b_in + rows * 8 + rows * 16 + 256);
+  float* fin[3] = {reinterpret_cast<float*>(base), nullptr, nullptr};
+  fin[1] = fin[0] + elems;
+  fin[2] = fin[1] + elems;
+  __nv_bfloat16* bq = reinterpret_cast<__nv_bfloat16*>(fin[2] + elems);
+  __nv_bfloat16* bk = bq + elems;
+  __nv_bfloat16* bv = bk + elems;
+  __nv_bfloat16* bo = bv + elems;
+  float* fo = reinterpret_cast<float*>(bo + elems);
+  float* fmax = fo + elems;
+  float* fsum = fmax + rows;
+  double* dmax = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(fsum + rows) + 15) / 16 * 16);
+  double* dsum = dmax + rows;
+  BBM_CUDA(cudaMemsetAsync(p.bad, 0, 4 * sizeof(int), p.comp));
+  const uint64_t chunks =
+      std::max<uint64_t>(1, std::min<uint64_t>({slots, kMaxChunks, (3 * b_in) / kChunkBytes}));
+  cudaEvent_t t0 = nullptr, t1 = nullptr;
+  if (span_ms) {
+    BBM_CUDA(cudaEventCreate(&t0));
+    BBM_CUDA(cudaEventCreate(&t1));
+    BBM_CUDA(cudaEventRecord(t0, p.h2d));
+  }
+  const float* const* src[3] = {q, k, v};
+  __nv_bfloat16* dst[3] = {bq, bk, bv};
+  for (uint64_t c = 0; c < chunks; ++c) {
+    const uint64_t s0 = slots * c / chunks, s1 = slots * (c + 1) / chunks, ns = s1 - s0;
+    const uint64_t off = s0 * per;
+    for (uint64_t sl = s0; sl < s1; ++sl)
+      for (int t = 0; t < 3; ++t)
+        BBM_CUDA(cudaMemcpyAsync(fin[t] + sl * per, src[t][sl], per * 4, cudaMemcpyHostToDevice, p.h2d));
+    BBM_CUDA(cudaEventRecord(p.ev_in[c], p.h2d));
+    BBM_CUDA(cudaStreamWaitEvent(p.comp, p.ev_in[c], 0));
+    for (int t = 0; t < 3; ++t)
+      f32_to_bf16_check_kernel<<<grid_for_elems(ns * per), 256, 0, p.comp>>>(fin[t] + off, dst[t] + off,
+                                                                              ns * per, p.bad + t);
+    BBM_CUDA(cudaGetLastError());
+    AttnArgs a{bq + off, bk + off, bv + off, bo + off, fmax + s0 * n, fsum + s0 * n, ns, n, d, scale, variant};
+    launch_attn_fwd(prep, a, p.comp, num_sms);
+    widen_outputs_kernel<<<grid_for_elems(ns * per), 256, 0, p.comp>>>(
+        bo + off, fo + off, ns * per, fmax + s0 * n, fsum + s0 * n, want_max ? dmax + s0 * n : nullptr,
+        want_sum ? dsum + s0 * n : nullptr, ns * n);
+    BBM_CUDA(cudaGetLastError());
+    BBM_CUDA(cudaEventRecord(p.ev_out[c], p.comp));
+    BBM_CUDA(cudaStreamWaitEvent(p.d2h, p.ev_out[c], 0));
+    for (uint64_t sl = s0; sl < s1; ++sl) {
+      BBM_CUDA(cudaMemcpyAsync(out[sl], fo + sl * per, per * 4, cudaMemcpyDeviceToHost, p.d2h));
+      if (want_max) BBM_CUDA(cudaMemcpyAsync(row_max[sl], dmax + sl * n, n * 8, cudaMemcpyDeviceToHost, p.d2h));
+      if (want_sum) BBM_CUDA(cudaMemcpyAsync(row_sum[sl], dsum + sl * n, n * 8, cudaMemcpyDeviceToHost, p.d2h));
+    }
+  }
+  if (span_ms) BBM_CUDA(cudaEventRecord(t1, p.d2h));
+  int hbad[4] = {0, 0, 0, 0};
+  BBM_CUDA(cudaMemcpyAsync(hbad, p.bad, 3 * sizeof(int), cudaMemcpyDeviceToHost, p.comp));
+  BBM_CUDA(cudaStreamSynchronize(p.comp));
+  BBM_CUDA(cudaStreamSynchronize(p.d2h));
+  if (span_ms) {
+    float ms = 0.0f;
+    BBM_CUDA(cudaEventElapsedTime(&ms, t0, t1));
+    *span_ms = ms;
+    cudaEventDestroy(t0);
+    cudaEventDestroy(t1);
+  }
+  throw_if_bad(hbad, 3);
+}
 
 // The RCM path end to end (reorder.hpp:156-189 + bench.hpp:448-467): the caller's Q/K/V are in
 // the ORIGINAL token order, `prep` was built from permute_mask(mask, perm), forward = perm's
@@ -135,6 +302,7 @@ void run_fwd_host_rcm(const Prep& prep, int variant, const uint32_t* forward, co
                       const uint16_t* k, const uint16_t* v, uint16_t* out, float* row_max,
                       float* row_sum, uint64_t slots, uint32_t d, float scale, int num_sms,
                       double* span_ms) {
+  std::lock_guard<std::mutex> lk(prep.pipe_mu);
   HostPipe& p = pipe_of(prep);
   const uint64_t n = prep.n, per = n * d, tbytes = slots * per * 2, sbytes = slots * n * 4;
   uint8_t* base = reserve(p, 7 * tbytes + 4 * sbytes + n * 4 + 256);

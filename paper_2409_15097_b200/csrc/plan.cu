@@ -1,0 +1,311 @@
+// plan.cu — launch plans of the attention kernels, built ON THE DEVICE from the prep's tile lists.
+//
+// The reference schedules row blocks in waves of host threads (run_in_waves, engine.hpp:264-278)
+// and walks each row block's column blocks in ascending order (engine.hpp:311). Here a plan cuts
+// every (slot, query row tile) into work items for the persistent kernel: a row unit is a row
+// tile's whole tile walk, or — for rows much longer than a CTA's fair share — one balanced chunk
+// of it (split-KV; the chunks' partials are combined in chunk order, so results are
+// deterministic). Units are ordered longest first (LPT), ties by row index.
+//
+// Because the plan is computed from row_cnt / list by a kernel, a mask update
+// (bbm_prep_update_*) followed by a launch needs no host round trip: the stale plan is simply
+// rebuilt on the launching stream.
+//
+// Unit length L: with dynamic longest-first claiming the makespan is about (average work per CTA
+// + longest unit), so L is half a CTA's average share, and at least 16 tiles (combining partials
+// goes through global memory and costs more than a few tiles). L is doubled until the launch's
+// chunks fit the per-stream workspace (plan_cap_chunks).
+//
+// The masked variants split IN KEY SPACE, at boundaries set by the occupied tiles only: chunk c
+// of a row holds the same occupied tiles, in the same order, whether the variant walks the
+// compacted list (binblk, dense_binblk) or every tile of the key range (naive, whose extra tiles
+// are fully masked and change nothing). Their partials and the combine are then identical, so the
+// masked variants agree bit for bit at every size (test_engine.cpp:112-134). The dense variant
+// ignores the mask and splits by position.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdint>
+
+#include "bbm_internal.h"
+
+namespace bbm {
+namespace {
+
+constexpr uint32_t kPlanThreads = 512;
+constexpr uint32_t kMinUnit = 16;
+
+// Exclusive prefix sum of one value per thread over the CTA (kPlanThreads threads); returns the
+// thread's exclusive prefix and writes the CTA total to *total.
+template <class T>
+__device__ T block_exscan(T v, T* total) {
+  __shared__ T warp_sums[kPlanThreads / 32];
+  const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  T x = v;
+#pragma unroll
+  for (uint32_t o = 1; o < 32; o <<= 1) {
+    const T y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) warp_sums[warp] = x;
+  __syncthreads();
+  if (warp == 0) {
+    T w = lane < kPlanThreads / 32 ? warp_sums[lane] : T(0);
+#pragma unroll
+    for (uint32_t o = 1; o < 32; o <<= 1) {
+      const T y = __shfl_up_sync(0xffffffffu, w, o);
+      if (lane >= o) w += y;
+    }
+    if (lane < kPlanThreads / 32) warp_sums[lane] = w;  // inclusive warp prefix
+  }
+  __syncthreads();
+  const T before = (warp ? warp_sums[warp - 1] : T(0)) + x - v;
+  *total = warp_sums[kPlanThreads / 32 - 1];
+  __syncthreads();
+  return before;
+}
+
+template <class T>
+__device__ T block_sum(T v) {
+  T total;
+  block_exscan(v, &total);
+  return total;
+}
+
+// Stable LPT order of `count` items with keys in [0, max_key]: out[rank] = value(i), rank = number
+// of items with a larger key plus items with the same key and a smaller index. Counting sort:
+// histogram, descending exclusive scan, then one warp scatters in index order (match_any gives
+// each lane its rank among equal keys of its group of 32).
+template <class KeyFn, class StoreFn>
+__device__ void lpt_sort(KeyFn key, uint32_t count, uint32_t max_key, uint32_t* hist, StoreFn store) {
+  for (uint32_t v = threadIdx.x; v <= max_key; v += kPlanThreads) hist[v] = 0;
+  __syncthreads();
+  for (uint32_t i = threadIdx.x; i < count; i += kPlanThreads) atomicAdd(&hist[min(key(i), max_key)], 1u);
+  __syncthreads();
+  // descending exclusive scan: start[v] = sum of hist[w] for w > v; chunks from the top key down
+  uint32_t carry = 0;
+  for (uint32_t c0 = 0; c0 <= max_key; c0 += kPlanThreads) {
+    const uint32_t idx = c0 + threadIdx.x;  // position from the top
+    const uint32_t v = idx <= max_key ? max_key - idx : 0;
+    const uint32_t h = idx <= max_key ? hist[v] : 0u;
+    uint32_t tot;
+    const uint32_t before = block_exscan(h, &tot);
+    if (idx <= max_key) hist[v] = carry + before;
+    carry += tot;
+    __syncthreads();
+  }
+  if (threadIdx.x < 32) {
+    const uint32_t lane = threadIdx.x;
+    for (uint32_t i0 = 0; i0 < count; i0 += 32) {
+      const uint32_t i = i0 + lane;
+      const bool ok = i < count;
+      const uint32_t v = ok ? min(key(i), max_key) : 0xFFFFFFFFu;
+      const uint32_t peers = __match_any_sync(0xffffffffu, v);
+      const uint32_t rank = __popc(peers & ((1u << lane) - 1u));
+      const uint32_t base = ok ? hist[v] : 0u;
+      __syncwarp();
+      if (ok) store(base + rank, i);
+      if (ok && rank == 0) hist[v] = base + __popc(peers);
+      __syncwarp();
+    }
+  }
+  __syncthreads();
+}
+
+struct PlanArgs {
+  int cls;
+  uint32_t krows, kcols;
+  const uint32_t* row_cnt;
+  const uint32_t* list;
+  uint64_t slots;
+  uint32_t workers;
+  uint64_t cap_chunks;  // bound on slots * split chunks (workspace blocks)
+  uint32_t cap_units, cap_split;
+  PlanHdr* hdr;
+  uint4* desc;
+  uint2* split_info;
+  uint4* tmp;
+  uint32_t* hist;
+};
+
+__device__ __forceinline__ uint32_t chunks_of(uint32_t occ, uint64_t L) {
+  if (occ <= L) return 0u;
+  const uint64_t k = (occ + L - 1) / L;
+  return static_cast<uint32_t>(k < 255 ? k : 255);
+}
+
+__global__ void __launch_bounds__(kPlanThreads) plan_kernel(const PlanArgs a) {
+  __shared__ unsigned long long s_L;
+  auto occ_of = [&](uint32_t p) { return a.cls == kPlanDense ? a.kcols : a.row_cnt[p]; };
+  auto walk_of = [&](uint32_t p) { return a.cls == kPlanList ? a.row_cnt[p] : a.kcols; };
+
+  // ---- unit length
+  unsigned long long my = 0;
+  for (uint32_t p = threadIdx.x; p < a.krows; p += kPlanThreads) my += occ_of(p);
+  const unsigned long long total = block_sum(my) * a.slots;
+  uint64_t L = (total / max(1u, a.workers) + 1) / 2;
+  if (L < kMinUnit) L = kMinUnit;
+  for (;;) {
+    unsigned long long c = 0;
+    for (uint32_t p = threadIdx.x; p < a.krows; p += kPlanThreads) c += chunks_of(occ_of(p), L);
+    const unsigned long long chunks = block_sum(c);
+    if (chunks * a.slots <= a.cap_chunks && a.krows + chunks <= a.cap_units) break;
+    L *= 2;
+  }
+  if (threadIdx.x == 0) s_L = L;
+  __syncthreads();
+  L = s_L;
+
+  // ---- units in row order: offsets by block scans over the rows, chunk by chunk
+  uint32_t u_carry = 0, s_carry = 0, c_carry = 0;
+  for (uint32_t p0 = 0; p0 < a.krows; p0 += kPlanThreads) {
+    const uint32_t p = p0 + threadIdx.x;
+    const bool in = p < a.krows;
+    const uint32_t occ = in ? occ_of(p) : 0u, walk = in ? walk_of(p) : 0u;
+    const uint32_t k = in ? chunks_of(occ, L) : 0u;
+    uint32_t ut, st, ct;
+    const uint32_t ub = u_carry + block_exscan<uint32_t>(in ? (k ? k : 1u) : 0u, &ut);
+    const uint32_t sb = s_carry + block_exscan<uint32_t>(k ? 1u : 0u, &st);
+    const uint32_t cb = c_carry + block_exscan<uint32_t>(k, &ct);
+    if (in) {
+      if (k == 0) {
+        a.tmp[ub] = make_uint4(p, 0, walk, kNoSplit);  // walk == 0: a fully masked row tile
+      } else {
+        a.split_info[sb] = make_uint2(k, cb);
+        auto first_occ = [&](uint32_t c) { return (occ / k) * c + min(c, occ % k); };
+        auto key_of = [&](uint32_t o) {
+          return a.cls == kPlanDense ? o : (a.list[static_cast<uint64_t>(p) * a.kcols + o] & 0x7FFFFFFFu);
+        };
+        for (uint32_t c = 0; c < k; ++c) {
+          const uint32_t o0 = first_occ(c), o1 = first_occ(c + 1);
+          if (a.cls == kPlanNaive) {
+            const uint32_t kv0 = c == 0 ? 0u : key_of(o0), kv1 = c + 1 == k ? a.kcols : key_of(o1);
+            a.tmp[ub + c] = make_uint4(p, kv0, kv1 - kv0, (sb << 8) | c);
+          } else {
+            a.tmp[ub + c] = make_uint4(p, o0, o1 - o0, (sb << 8) | c);  // list positions
+          }
+        }
+      }
+    }
+    u_carry += ut;
+    s_carry += st;
+    c_carry += ct;
+  }
+  __syncthreads();
+
+  // ---- longest first (tiles walked), ties by row order
+  const uint32_t units = u_carry;
+  lpt_sort([&](uint32_t i) { return a.tmp[i].z; }, units, a.kcols, a.hist,
+           [&](uint32_t pos, uint32_t i) { a.desc[pos] = a.tmp[i]; });
+  if (threadIdx.x == 0) *a.hdr = PlanHdr{units, s_carry, c_carry, static_cast<uint32_t>(L < 0xFFFFFFFFull ? L : 0xFFFFFFFFull)};
+}
+
+__global__ void __launch_bounds__(kPlanThreads) lpt_order_kernel(const uint32_t* __restrict__ keys,
+                                                                 uint32_t count, uint32_t max_key,
+                                                                 uint32_t* __restrict__ hist,
+                                                                 uint32_t* __restrict__ out) {
+  lpt_sort([&](uint32_t i) { return keys[i]; }, count, max_key, hist,
+           [&](uint32_t pos, uint32_t i) { out[pos] = i; });
+}
+
+}  // namespace
+
+uint64_t plan_cap_chunks(uint64_t slots, uint32_t workers) {
+  return 4ull * std::max(1u, workers) + 4 + slots;
+}
+
+uint32_t plan_cap_units(uint32_t krows, uint32_t kcols, uint64_t slots, uint32_t workers) {
+  if (kcols <= kMinUnit) return krows;  // L >= 16 tiles: no row can split
+  const uint64_t extra = plan_cap_chunks(slots, workers) / std::max<uint64_t>(1, slots) + 1;
+  return static_cast<uint32_t>(std::min<uint64_t>(krows + extra, static_cast<uint64_t>(krows) * 256));
+}
+
+void build_plan(const KernelMeta& km, int cls, uint64_t slots, uint32_t workers, DevPlan& plan,
+                cudaStream_t s) {
+  PlanArgs a{};
+  a.cls = cls;
+  a.krows = km.krows;
+  a.kcols = km.kcols;
+  a.row_cnt = km.row_cnt;
+  a.list = km.list;
+  a.slots = slots;
+  a.workers = workers;
+  a.cap_chunks = plan_cap_chunks(slots, workers);
+  a.cap_units = plan.cap_units;
+  a.cap_split = plan.cap_split;
+  a.hdr = plan.hdr;
+  a.desc = plan.unit_desc;
+  a.split_info = plan.split_info;
+  a.tmp = plan.tmp;
+  a.hist = plan.hist;
+  plan_kernel<<<1, kPlanThreads, 0, s>>>(a);
+  BBM_CUDA(cudaGetLastError());
+}
+
+void launch_lpt_order(const uint32_t* keys, uint32_t count, uint32_t max_key, uint32_t* scratch,
+                      uint32_t* out, cudaStream_t s) {
+  lpt_order_kernel<<<1, kPlanThreads, 0, s>>>(keys, count, max_key, scratch, out);
+  BBM_CUDA(cudaGetLastError());
+}
+
+const DevPlan& plan_for(const Prep& prep, StreamCtx& ctx, int cls, uint64_t slots, uint32_t workers,
+                        cudaStream_t s) {
+  const KernelMeta& km = prep.kmeta;
+  DevPlan& pl = ctx.plans[std::make_tuple(cls, slots, workers)];
+  if (!pl.mem) {
+    pl.cap_units = plan_cap_units(km.krows, km.kcols, slots, workers);
+    pl.cap_split = std::min<uint32_t>(pl.cap_units, static_cast<uint32_t>(
+                                                        plan_cap_chunks(slots, workers) / std::max<uint64_t>(1, slots) + 1));
+    const size_t off_desc = 256;
+    const size_t off_tmp = off_desc + static_cast<size_t>(pl.cap_units) * 16;
+    const size_t off_split = off_tmp + static_cast<size_t>(pl.cap_units) * 16;
+    const size_t off_hist = off_split + static_cast<size_t>(pl.cap_split) * 8;
+    const size_t bytes = off_hist + (static_cast<size_t>(km.kcols) + 2) * 4;
+    void* mem = nullptr;
+    BBM_CUDA(cudaMalloc(&mem, bytes));
+    pl.mem = static_cast<uint8_t*>(mem);
+    pl.hdr = reinterpret_cast<PlanHdr*>(pl.mem);
+    pl.unit_desc = reinterpret_cast<uint4*>(pl.mem + off_desc);
+    pl.tmp = reinterpret_cast<uint4*>(pl.mem + off_tmp);
+    pl.split_info = reinterpret_cast<uint2*>(pl.mem + off_split);
+    pl.hist = reinterpret_cast<uint32_t*>(pl.mem + off_hist);
+    pl.version = 0;
+  }
+  if (pl.version != prep.version) {
+    build_plan(km, cls, slots, workers, pl, s);
+    pl.version = prep.version;
+  }
+  return pl;
+}
+
+float* ctx_workspace(StreamCtx& ctx, size_t floats, cudaStream_t s) {
+  if (floats > ctx.ws_floats) {
+    // the previous workspace may still be in use by launches queued on this stream
+    if (ctx.ws) {
+      BBM_CUDA(cudaStreamSynchronize(s));
+      cudaFree(ctx.ws);
+    }
+    ctx.ws = nullptr;
+    ctx.ws_floats = 0;
+    BBM_CUDA(cudaMalloc(&ctx.ws, floats * sizeof(float)));
+    ctx.ws_floats = floats;
+  }
+  return ctx.ws;
+}
+
+uint32_t* ctx_split_ctr(StreamCtx& ctx, size_t count, cudaStream_t s) {
+  if (count > ctx.split_ctr_n) {
+    if (ctx.split_ctr) {
+      BBM_CUDA(cudaStreamSynchronize(s));
+      cudaFree(ctx.split_ctr);
+    }
+    ctx.split_ctr = nullptr;
+    ctx.split_ctr_n = 0;
+    BBM_CUDA(cudaMalloc(&ctx.split_ctr, count * sizeof(uint32_t)));
+    BBM_CUDA(cudaMemsetAsync(ctx.split_ctr, 0, count * sizeof(uint32_t), s));
+    ctx.split_ctr_n = count;
+  }
+  return ctx.split_ctr;
+}
+
+}  // namespace bbm

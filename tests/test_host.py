@@ -24,7 +24,7 @@ def test_library_loads_and_exports_every_declared_symbol():
     missing = [s for s in declared if not hasattr(lib, s)]
     assert not missing, f"symbols declared in bbm_capi.h but not exported: {missing}"
     assert declared == set(_lib.SIGNATURES), "ctypes binding out of sync with the header"
-    assert lib.bbm_abi_version() == 1
+    assert lib.bbm_abi_version() == 2
 
 
 def test_device_count_is_safe_without_gpu():
