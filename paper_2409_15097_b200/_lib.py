@@ -10,6 +10,8 @@ import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libbbm.so")
+# A/B timing experiments (tools/ablate.sh) may point at another in-tree build of the same library
+LIB_PATH = os.environ.get("BBM_LIB", LIB_PATH)
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(

@@ -661,13 +661,15 @@ __global__ void __launch_bounds__(kThreadsOf<D>, 1)
         }
         float pmax = neg ? chunk_max<true>(a0) : chunk_max<false>(a0);
         if constexpr (kSC == 64) pmax = fmaxf(pmax, neg ? chunk_max<true>(a1) : chunk_max<false>(a1));
-        // exchange with the other half (double-buffered by parity); after this barrier every S
-        // read of this tile has completed, so P may overwrite S columns [0, 64)
+        // exchange with the other half of the same rows (double-buffered by parity) through a
+        // 64-thread named barrier of the quadrant's two engine warps only: after it both halves
+        // of these 32 rows have read S, so P may overwrite their S columns [0, 64). The four
+        // quadrant pairs run decoupled.
 #ifdef BBM_ABLATE_NO_XCHG  // timing experiments only: wrong results
         float tmax = pmax;
 #else
         ctl->xchg[step & 1][half][row] = pmax;
-        named_bar_sync(1, kEng);
+        named_bar_sync(3 + quad, 64);
         float tmax = pmax;
 #pragma unroll
         for (uint32_t o = 1; o < kP; ++o) tmax = fmaxf(tmax, ctl->xchg[step & 1][(half + o) % kP][row]);

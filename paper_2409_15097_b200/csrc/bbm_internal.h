@@ -78,6 +78,8 @@ struct KernelMeta {
   uint64_t* row_stats = nullptr;
   uint64_t* totals = nullptr;
   uint32_t* scratch = nullptr;  // [krows + kcols + 2] ordering scratch (device LPT sort)
+  uint32_t* partial = nullptr;  // [8][krows][kcols] fused preprocessor's per-slab tile sums
+  uint32_t* ctr = nullptr;      // [krows + 1] fused preprocessor's finish counters (zero at rest)
 };
 void carve_kernel_meta(KernelMeta& km, uint64_t n, uint8_t* arena);  // sets pointers + bytes
 size_t kernel_meta_bytes(uint64_t n);
@@ -183,6 +185,12 @@ struct Prep {
 void launch_pack_bool(const uint8_t* d_bool, uint64_t n, uint64_t row_stride, const KernelMeta& km,
                       cudaStream_t s);
 void launch_pad_packed(const uint64_t* d_words, uint64_t n, const KernelMeta& km, cudaStream_t s);
+// the whole kernel view (padded mask, sums, lists, bitmaps, totals, LPT order) in ONE launch;
+// false when the input does not fit the fused path (the caller falls back to the chain)
+bool launch_prep_fused_bool(const uint8_t* d_bool, uint64_t n, uint64_t stride, const KernelMeta& km,
+                            cudaStream_t s);
+bool launch_prep_fused_words(const uint64_t* d_words, uint64_t in_wpr, uint64_t n, const KernelMeta& km,
+                             cudaStream_t s);
 void launch_sums128(const KernelMeta& km, cudaStream_t s);
 void launch_sums_generic(const KernelMeta& km, uint64_t n, uint64_t bi, uint64_t bj,
                          uint64_t rows, uint64_t cols, uint32_t* d_sums, cudaStream_t s);

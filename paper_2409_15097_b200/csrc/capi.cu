@@ -78,6 +78,22 @@ void build_kernel_view(const KernelMeta& km, uint64_t n, cudaStream_t s) {
   launch_lpt_order(km.row_cnt, km.krows, km.kcols, km.scratch, km.order, s);
 }
 
+// The complete kernel view from a dense bool mask / from packed words (in_wpr words per row; may
+// be the padded mask itself): the fused one-launch preprocessor, or the kernel chain when the
+// input does not fit it (unaligned bool rows, n % 16 != 0).
+void view_from_bool(const KernelMeta& km, const uint8_t* d_bool, uint64_t n, uint64_t stride, cudaStream_t s) {
+  if (launch_prep_fused_bool(d_bool, n, stride, km, s)) return;
+  launch_pack_bool(d_bool, n, stride, km, s);
+  build_kernel_view(km, n, s);
+}
+
+void view_from_words(const KernelMeta& km, const uint64_t* d_words, uint64_t in_wpr, uint64_t n, cudaStream_t s) {
+  if (launch_prep_fused_words(d_words, in_wpr, n, km, s)) return;
+  if (d_words != km.mask) launch_pad_packed(d_words, n, km, s);
+  launch_sums128(km, s);
+  build_kernel_view(km, n, s);
+}
+
 void validate_spec(uint64_t n, uint64_t bi, uint64_t bj) {
   require(bi >= 1 && bj >= 1, "block sizes must be >= 1");  // mask.hpp:61-63
   require(n >= 1, "mask must be non-empty");                 // engine.hpp:82
@@ -94,6 +110,7 @@ Prep* new_prep(uint64_t n, int device, uint64_t bi, uint64_t bj) {
     void* arena = nullptr;
     BBM_CUDA(cudaMalloc(&arena, kernel_meta_bytes(n)));
     carve_kernel_meta(pr->kmeta, n, static_cast<uint8_t*>(arena));
+    BBM_CUDA(cudaMemset(pr->kmeta.ctr, 0, (static_cast<size_t>(pr->kmeta.krows) + 1) * 4));
     BBM_CUDA(cudaEventCreateWithFlags(&pr->ready, cudaEventDisableTiming));
   } catch (...) {
     delete pr;
@@ -147,6 +164,8 @@ void carve_kernel_meta(KernelMeta& km, uint64_t n, uint8_t* arena) {
   take(km.row_stats, static_cast<uint64_t>(km.krows) * 3);
   take(km.totals, 3);
   take(km.scratch, static_cast<uint64_t>(km.krows) + km.kcols + 2);
+  take(km.partial, tiles * 8);
+  take(km.ctr, static_cast<uint64_t>(km.krows) + 1);
   km.arena_bytes = off;
 }
 
@@ -323,11 +342,9 @@ unsigned grid_of(uint64_t count) {
   return static_cast<unsigned>(std::max<uint64_t>(1, std::min<uint64_t>(g, 148ull * 16)));
 }
 
-// Creation: the padded mask (and 128x128 sums) are on `s`; build the kernel view, publish the
-// first version and compute the caller-spec host metadata (one sync, like the reference's
-// synchronous preprocess_mask).
+// Creation: the kernel view is queued on `s`; publish the first version and compute the
+// caller-spec host metadata (one sync, like the reference's synchronous preprocess_mask).
 bbm_prep finish_prep(std::unique_ptr<Prep> pr, cudaStream_t s) {
-  build_kernel_view(pr->kmeta, pr->n, s);
   BBM_CUDA(cudaEventRecord(pr->ready, s));
   pr->spec_now();
   return wrap(pr.release());
@@ -346,7 +363,6 @@ void update_prep(bbm_prep h, void* stream, Fill&& fill) {
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   order_update_after_launches(pr, s);
   fill(pr, s);
-  build_kernel_view(pr.kmeta, pr.n, s);
   publish_version(pr, s);
   h->replicas.clear();
 }
@@ -403,7 +419,7 @@ bbm_status bbm_preprocess_packed_host(const uint64_t* words, uint64_t n, uint64_
       BBM_CUDA(cudaMemsetAsync(km.mask, 0, rows_pad * pad_wpr * 8, s));
       BBM_CUDA(cudaMemcpy2DAsync(km.mask, pad_wpr * 8, words, wpr * 8, wpr * 8, n,
                                  cudaMemcpyHostToDevice, s));
-      launch_sums128(km, s);
+      view_from_words(km, km.mask, pad_wpr, n, s);
       *out = finish_prep(std::move(pr), s);
     } catch (...) {
       cudaStreamDestroy(s);
@@ -422,8 +438,7 @@ bbm_status bbm_preprocess_packed_device(const uint64_t* d_words, uint64_t n, uin
     BBM_CUDA(cudaGetDevice(&dev));
     std::unique_ptr<Prep> pr(new_prep(n, dev, bi, bj));
     cudaStream_t s = static_cast<cudaStream_t>(stream);
-    launch_pad_packed(d_words, n, pr->kmeta, s);
-    launch_sums128(pr->kmeta, s);
+    view_from_words(pr->kmeta, d_words, (n + 63) / 64, n, s);
     *out = finish_prep(std::move(pr), s);
   });
 }
@@ -438,7 +453,7 @@ bbm_status bbm_preprocess_bool_device(const uint8_t* d_mask, uint64_t n, uint64_
     BBM_CUDA(cudaGetDevice(&dev));
     std::unique_ptr<Prep> pr(new_prep(n, dev, bi, bj));
     cudaStream_t s = static_cast<cudaStream_t>(stream);
-    launch_pack_bool(d_mask, n, row_stride, pr->kmeta, s);
+    view_from_bool(pr->kmeta, d_mask, n, row_stride, s);
     *out = finish_prep(std::move(pr), s);
   });
 }
@@ -448,7 +463,7 @@ bbm_status bbm_prep_update_bool_device(bbm_prep prep, const uint8_t* d_mask, uin
   return guarded([&] {
     Prep& pr = unwrap(prep);
     require(d_mask != nullptr && row_stride >= pr.n, "bad mask argument");
-    update_prep(prep, stream, [&](Prep& p, cudaStream_t s) { launch_pack_bool(d_mask, p.n, row_stride, p.kmeta, s); });
+    update_prep(prep, stream, [&](Prep& p, cudaStream_t s) { view_from_bool(p.kmeta, d_mask, p.n, row_stride, s); });
   });
 }
 
@@ -456,8 +471,7 @@ bbm_status bbm_prep_update_packed_device(bbm_prep prep, const uint64_t* d_words,
   return guarded([&] {
     require(d_words != nullptr, "bad mask argument");
     update_prep(prep, stream, [&](Prep& p, cudaStream_t s) {
-      launch_pad_packed(d_words, p.n, p.kmeta, s);
-      launch_sums128(p.kmeta, s);
+      view_from_words(p.kmeta, d_words, (p.n + 63) / 64, p.n, s);
     });
   });
 }

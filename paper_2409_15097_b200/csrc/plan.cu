@@ -28,89 +28,13 @@
 #include <cstdint>
 
 #include "bbm_internal.h"
+#include "bbm_sort.cuh"
 
 namespace bbm {
 namespace {
 
 constexpr uint32_t kPlanThreads = 512;
 constexpr uint32_t kMinUnit = 16;
-
-// Exclusive prefix sum of one value per thread over the CTA (kPlanThreads threads); returns the
-// thread's exclusive prefix and writes the CTA total to *total.
-template <class T>
-__device__ T block_exscan(T v, T* total) {
-  __shared__ T warp_sums[kPlanThreads / 32];
-  const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  T x = v;
-#pragma unroll
-  for (uint32_t o = 1; o < 32; o <<= 1) {
-    const T y = __shfl_up_sync(0xffffffffu, x, o);
-    if (lane >= o) x += y;
-  }
-  if (lane == 31) warp_sums[warp] = x;
-  __syncthreads();
-  if (warp == 0) {
-    T w = lane < kPlanThreads / 32 ? warp_sums[lane] : T(0);
-#pragma unroll
-    for (uint32_t o = 1; o < 32; o <<= 1) {
-      const T y = __shfl_up_sync(0xffffffffu, w, o);
-      if (lane >= o) w += y;
-    }
-    if (lane < kPlanThreads / 32) warp_sums[lane] = w;  // inclusive warp prefix
-  }
-  __syncthreads();
-  const T before = (warp ? warp_sums[warp - 1] : T(0)) + x - v;
-  *total = warp_sums[kPlanThreads / 32 - 1];
-  __syncthreads();
-  return before;
-}
-
-template <class T>
-__device__ T block_sum(T v) {
-  T total;
-  block_exscan(v, &total);
-  return total;
-}
-
-// Stable LPT order of `count` items with keys in [0, max_key]: out[rank] = value(i), rank = number
-// of items with a larger key plus items with the same key and a smaller index. Counting sort:
-// histogram, descending exclusive scan, then one warp scatters in index order (match_any gives
-// each lane its rank among equal keys of its group of 32).
-template <class KeyFn, class StoreFn>
-__device__ void lpt_sort(KeyFn key, uint32_t count, uint32_t max_key, uint32_t* hist, StoreFn store) {
-  for (uint32_t v = threadIdx.x; v <= max_key; v += kPlanThreads) hist[v] = 0;
-  __syncthreads();
-  for (uint32_t i = threadIdx.x; i < count; i += kPlanThreads) atomicAdd(&hist[min(key(i), max_key)], 1u);
-  __syncthreads();
-  // descending exclusive scan: start[v] = sum of hist[w] for w > v; chunks from the top key down
-  uint32_t carry = 0;
-  for (uint32_t c0 = 0; c0 <= max_key; c0 += kPlanThreads) {
-    const uint32_t idx = c0 + threadIdx.x;  // position from the top
-    const uint32_t v = idx <= max_key ? max_key - idx : 0;
-    const uint32_t h = idx <= max_key ? hist[v] : 0u;
-    uint32_t tot;
-    const uint32_t before = block_exscan(h, &tot);
-    if (idx <= max_key) hist[v] = carry + before;
-    carry += tot;
-    __syncthreads();
-  }
-  if (threadIdx.x < 32) {
-    const uint32_t lane = threadIdx.x;
-    for (uint32_t i0 = 0; i0 < count; i0 += 32) {
-      const uint32_t i = i0 + lane;
-      const bool ok = i < count;
-      const uint32_t v = ok ? min(key(i), max_key) : 0xFFFFFFFFu;
-      const uint32_t peers = __match_any_sync(0xffffffffu, v);
-      const uint32_t rank = __popc(peers & ((1u << lane) - 1u));
-      const uint32_t base = ok ? hist[v] : 0u;
-      __syncwarp();
-      if (ok) store(base + rank, i);
-      if (ok && rank == 0) hist[v] = base + __popc(peers);
-      __syncwarp();
-    }
-  }
-  __syncthreads();
-}
 
 struct PlanArgs {
   int cls;
@@ -142,13 +66,13 @@ __global__ void __launch_bounds__(kPlanThreads) plan_kernel(const PlanArgs a) {
   // ---- unit length
   unsigned long long my = 0;
   for (uint32_t p = threadIdx.x; p < a.krows; p += kPlanThreads) my += occ_of(p);
-  const unsigned long long total = block_sum(my) * a.slots;
+  const unsigned long long total = block_sum<kPlanThreads>(my) * a.slots;
   uint64_t L = (total / max(1u, a.workers) + 1) / 2;
   if (L < kMinUnit) L = kMinUnit;
   for (;;) {
     unsigned long long c = 0;
     for (uint32_t p = threadIdx.x; p < a.krows; p += kPlanThreads) c += chunks_of(occ_of(p), L);
-    const unsigned long long chunks = block_sum(c);
+    const unsigned long long chunks = block_sum<kPlanThreads>(c);
     if (chunks * a.slots <= a.cap_chunks && a.krows + chunks <= a.cap_units) break;
     L *= 2;
   }
@@ -164,9 +88,9 @@ __global__ void __launch_bounds__(kPlanThreads) plan_kernel(const PlanArgs a) {
     const uint32_t occ = in ? occ_of(p) : 0u, walk = in ? walk_of(p) : 0u;
     const uint32_t k = in ? chunks_of(occ, L) : 0u;
     uint32_t ut, st, ct;
-    const uint32_t ub = u_carry + block_exscan<uint32_t>(in ? (k ? k : 1u) : 0u, &ut);
-    const uint32_t sb = s_carry + block_exscan<uint32_t>(k ? 1u : 0u, &st);
-    const uint32_t cb = c_carry + block_exscan<uint32_t>(k, &ct);
+    const uint32_t ub = u_carry + block_exscan<kPlanThreads, uint32_t>(in ? (k ? k : 1u) : 0u, &ut);
+    const uint32_t sb = s_carry + block_exscan<kPlanThreads, uint32_t>(k ? 1u : 0u, &st);
+    const uint32_t cb = c_carry + block_exscan<kPlanThreads, uint32_t>(k, &ct);
     if (in) {
       if (k == 0) {
         a.tmp[ub] = make_uint4(p, 0, walk, kNoSplit);  // walk == 0: a fully masked row tile
@@ -195,7 +119,7 @@ __global__ void __launch_bounds__(kPlanThreads) plan_kernel(const PlanArgs a) {
 
   // ---- longest first (tiles walked), ties by row order
   const uint32_t units = u_carry;
-  lpt_sort([&](uint32_t i) { return a.tmp[i].z; }, units, a.kcols, a.hist,
+  lpt_sort<kPlanThreads>([&](uint32_t i) { return a.tmp[i].z; }, units, a.kcols, a.hist,
            [&](uint32_t pos, uint32_t i) { a.desc[pos] = a.tmp[i]; });
   if (threadIdx.x == 0) *a.hdr = PlanHdr{units, s_carry, c_carry, static_cast<uint32_t>(L < 0xFFFFFFFFull ? L : 0xFFFFFFFFull)};
 }
@@ -204,7 +128,7 @@ __global__ void __launch_bounds__(kPlanThreads) lpt_order_kernel(const uint32_t*
                                                                  uint32_t count, uint32_t max_key,
                                                                  uint32_t* __restrict__ hist,
                                                                  uint32_t* __restrict__ out) {
-  lpt_sort([&](uint32_t i) { return keys[i]; }, count, max_key, hist,
+  lpt_sort<kPlanThreads>([&](uint32_t i) { return keys[i]; }, count, max_key, hist,
            [&](uint32_t pos, uint32_t i) { out[pos] = i; });
 }
 

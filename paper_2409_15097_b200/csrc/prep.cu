@@ -21,6 +21,7 @@
 #include <cstdint>
 
 #include "bbm_internal.h"
+#include "bbm_sort.cuh"
 
 namespace bbm {
 namespace {
@@ -175,18 +176,20 @@ __device__ __forceinline__ uint32_t area_of(uint64_t n, uint64_t bi, uint64_t bj
   return static_cast<uint32_t>(ri * cj);
 }
 
-// One CTA (256 threads) per row tile p; the row is walked in chunks of 256 tiles.
-__global__ void __launch_bounds__(256) rowmeta_kernel(
-    const uint32_t* __restrict__ sums, uint64_t n, uint64_t bi, uint64_t bj, uint64_t cols,
-    uint8_t* __restrict__ occ, uint32_t* __restrict__ offset, uint32_t* __restrict__ total,
-    uint64_t* __restrict__ row_stats, uint32_t* __restrict__ list, uint32_t* __restrict__ cnt) {
-  // Kernel view only (list != nullptr): a tile narrower than bj (ragged right edge) is never
-  // flagged full, so the attention kernel always applies its bitmap, whose bits beyond n are 0.
+// The per-row pass of one query row tile p by one CTA of 256 threads: occupancy
+// (mask.hpp:203-209), the first maximal run of full tiles (mask.hpp:213-228), per-row stats
+// partials (mask.hpp:230-247) and the ascending compacted KV-tile list (block-wide ballot scan)
+// with a full/partial flag. Kernel view only (list != nullptr): a tile narrower than bj (ragged
+// right edge) is never flagged full, so the attention kernel always applies its bitmap, whose
+// bits beyond n are 0. Sums are read through L2 (__ldcg): the fused preprocessor calls this on
+// sums written earlier in the same launch.
+__device__ void rowmeta_row(const uint32_t* sums, uint64_t n, uint64_t bi, uint64_t bj, uint64_t cols,
+                            uint64_t p, uint8_t* occ, uint32_t* offset, uint32_t* total,
+                            uint64_t* row_stats, uint32_t* list, uint32_t* cnt) {
   __shared__ uint32_t warp_cnt[8];
   __shared__ uint32_t s_run_start, s_run_end;
   __shared__ unsigned long long s_nz, s_full, s_ones;
   const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint64_t p = blockIdx.x;
   if (threadIdx.x == 0) {
     s_run_start = 0xFFFFFFFFu;
     s_run_end = 0xFFFFFFFFu;
@@ -200,7 +203,7 @@ __global__ void __launch_bounds__(256) rowmeta_kernel(
     uint32_t s = 0, a = 0;
     bool in = q < cols;
     if (in) {
-      s = sums[p * cols + q];
+      s = __ldcg(sums + p * cols + q);
       a = area_of(n, bi, bj, p, q);
       occ[p * cols + q] = s > 0 ? 1 : 0;
       my_nz += s > 0;
@@ -226,7 +229,7 @@ __global__ void __launch_bounds__(256) rowmeta_kernel(
   const uint32_t start = s_run_start;
   if (start != 0xFFFFFFFFu) {
     for (uint64_t q = start + 1 + threadIdx.x; q < cols; q += 256) {
-      if (sums[p * cols + q] != area_of(n, bi, bj, p, q))
+      if (__ldcg(sums + p * cols + q) != area_of(n, bi, bj, p, q))
         atomicMin(&s_run_end, static_cast<uint32_t>(q));
     }
   }
@@ -248,6 +251,14 @@ __global__ void __launch_bounds__(256) rowmeta_kernel(
     row_stats[p * 3 + 2] = s_ones;
     if (cnt) cnt[p] = base;
   }
+  __syncthreads();
+}
+
+// One CTA (256 threads) per row tile p; the row is walked in chunks of 256 tiles.
+__global__ void __launch_bounds__(256) rowmeta_kernel(
+    const uint32_t* sums, uint64_t n, uint64_t bi, uint64_t bj, uint64_t cols, uint8_t* occ,
+    uint32_t* offset, uint32_t* total, uint64_t* row_stats, uint32_t* list, uint32_t* cnt) {
+  rowmeta_row(sums, n, bi, bj, cols, blockIdx.x, occ, offset, total, row_stats, list, cnt);
 }
 
 // grid (kcols, krows), 128 threads: CTA copies the mask bits of list entry (p, k) (if it exists)
@@ -299,6 +310,193 @@ __global__ void __launch_bounds__(1024) finalize_kernel(const uint64_t* __restri
   if (threadIdx.x < 3) totals[threadIdx.x] = acc[threadIdx.x];
 }
 
+// ------------------------------------------------------------------ fused preprocessor
+// ONE launch turns the caller's mask into the whole kernel view. CTA (chunk, p, rs) handles 16 rows
+// (slab rs of kRowSplits) of query tile row p over 32 column tiles (chunk): it packs / copies the
+// rows into the padded mask and writes its per-tile popcounts as partial sums. The last CTA of tile
+// row p to finish (one atomic per CTA, threadfence-reduction pattern) adds the partials into the
+// tile sums and runs the per-row pass (occupancy, first run, stats, compacted list) and the bitmap
+// compaction of that row; the last row to finish sums the row statistics and builds the LPT row
+// order. Counters reset themselves, so the next launch needs no memset.
+constexpr uint32_t kRowSplits = 8;                 // 128 rows / 16 per CTA
+constexpr uint32_t kSlabRows = 128 / kRowSplits;
+constexpr uint32_t kChunkTiles = 32;               // column tiles per CTA
+
+struct FusedArgs {
+  const uint8_t* bools;  // dense bool rows (IN == kInBool)
+  uint64_t stride;
+  const uint64_t* words; // packed rows, in_wpr words each (IN == kInWords); may alias km.mask
+  uint64_t in_wpr;
+  uint64_t n;
+  uint32_t krows, kcols, chunks;
+  uint64_t* mask;
+  uint32_t* partial;     // [kRowSplits][krows][kcols]
+  uint32_t* sums;
+  uint8_t* occ;
+  uint32_t *run_off, *run_len, *row_cnt, *list, *order, *scratch, *ctr;
+  uint64_t* row_stats;
+  unsigned long long* totals;
+  uint4* bitmaps;
+};
+enum : int { kInBool = 0, kInWords = 1 };
+
+template <int IN>
+__global__ void __launch_bounds__(256) prep_fused_kernel(const FusedArgs a) {
+  __shared__ uint32_t s_cnt[kChunkTiles];
+  __shared__ bool s_last;
+  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t chunk = blockIdx.x % a.chunks;
+  const uint32_t p = (blockIdx.x / a.chunks) % a.krows;
+  const uint32_t rs = blockIdx.x / (a.chunks * a.krows);
+  const uint64_t wpr = static_cast<uint64_t>(a.kcols) * 2;
+  const uint64_t row0 = static_cast<uint64_t>(p) * 128 + rs * kSlabRows;
+
+  // ---- stage A: this CTA's 16 rows x 32 column tiles -> padded packed words + partial sums
+  if constexpr (IN == kInBool) {
+    // warp w owns column tiles 4w .. 4w+3 of the chunk, 8 lanes x 16 bools each
+    const uint32_t q = chunk * kChunkTiles + warp * 4 + (lane >> 3);
+    const uint64_t col0 = static_cast<uint64_t>(q) * 128 + (lane & 7) * 16;
+    const bool col_ok = q < a.kcols && col0 < a.n;  // n % 16 == 0 on this path
+    uint32_t count = 0;
+    uint4 vb[kSlabRows];
+#pragma unroll
+    for (uint32_t b = 0; b < kSlabRows; ++b) {  // all 16 loads in flight before the first use
+      const uint64_t row = row0 + b;
+      vb[b] = (col_ok && row < a.n) ? __ldg(reinterpret_cast<const uint4*>(a.bools + row * a.stride + col0))
+                                    : make_uint4(0, 0, 0, 0);
+    }
+#pragma unroll
+    for (uint32_t b = 0; b < kSlabRows; ++b) {
+      uint4 v = vb[b];
+      if ((v.x | v.y | v.z | v.w) & 0xFEFEFEFEu) {  // bytes other than 0 / 1: nonzero = true
+        v.x = to01(v.x);
+        v.y = to01(v.y);
+        v.z = to01(v.z);
+        v.w = to01(v.w);
+      }
+      const uint32_t bits16 = bits8_of_01(v.x, v.y) | (bits8_of_01(v.z, v.w) << 8);
+      count += __popc(bits16);
+      // lanes 4m..4m+3 hold the four 16-bit quarters of one 64-bit word
+      const uint32_t pair = bits16 | (__shfl_xor_sync(0xffffffffu, bits16, 1) << 16);
+      const uint32_t other = __shfl_xor_sync(0xffffffffu, pair, 2);
+      if ((lane & 3) == 0 && q < a.kcols)
+        a.mask[(row0 + b) * wpr + static_cast<uint64_t>(q) * 2 + ((lane >> 2) & 1)] =
+            static_cast<uint64_t>(pair) | (static_cast<uint64_t>(other) << 32);
+    }
+    count += __shfl_xor_sync(0xffffffffu, count, 1);
+    count += __shfl_xor_sync(0xffffffffu, count, 2);
+    count += __shfl_xor_sync(0xffffffffu, count, 4);
+    if ((lane & 7) == 0 && q < a.kcols)
+      a.partial[(static_cast<uint64_t>(rs) * a.krows + p) * a.kcols + q] = count;
+  } else {
+    // thread t: word w = t % 64 of the chunk (tile w / 2), rows t / 64 + 4 i
+    if (threadIdx.x < kChunkTiles) s_cnt[threadIdx.x] = 0;
+    __syncthreads();
+    const uint32_t w = threadIdx.x & 63;
+    const uint64_t word = static_cast<uint64_t>(chunk) * 64 + w;
+    uint32_t count = 0;
+    if (word < wpr) {
+      uint64_t v[kSlabRows / 4];
+#pragma unroll
+      for (uint32_t i = 0; i < kSlabRows / 4; ++i) {
+        const uint64_t row = row0 + (threadIdx.x >> 6) + 4 * i;
+        v[i] = (row < a.n && word < a.in_wpr) ? a.words[row * a.in_wpr + word] : 0ull;
+      }
+#pragma unroll
+      for (uint32_t i = 0; i < kSlabRows / 4; ++i) {
+        const uint64_t row = row0 + (threadIdx.x >> 6) + 4 * i;
+        a.mask[row * wpr + word] = v[i];
+        count += __popcll(v[i]);
+      }
+    }
+    count += __shfl_xor_sync(0xffffffffu, count, 1);  // the tile's two words
+    if ((lane & 1) == 0 && word < wpr) atomicAdd(&s_cnt[w >> 1], count);
+    __syncthreads();
+    const uint32_t q = chunk * kChunkTiles + threadIdx.x;
+    if (threadIdx.x < kChunkTiles && q < a.kcols)
+      a.partial[(static_cast<uint64_t>(rs) * a.krows + p) * a.kcols + q] = s_cnt[threadIdx.x];
+  }
+
+  // ---- stage B: the last CTA of tile row p builds that row's metadata
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) s_last = atomicAdd(&a.ctr[p], 1u) == a.chunks * kRowSplits - 1;
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  for (uint32_t q = threadIdx.x; q < a.kcols; q += 256) {
+    uint32_t sum = 0;
+#pragma unroll
+    for (uint32_t r = 0; r < kRowSplits; ++r)
+      sum += __ldcg(a.partial + (static_cast<uint64_t>(r) * a.krows + p) * a.kcols + q);
+    a.sums[static_cast<uint64_t>(p) * a.kcols + q] = sum;
+  }
+  __syncthreads();
+  rowmeta_row(a.sums, a.n, 128, 128, a.kcols, p, a.occ, a.run_off, a.run_len, a.row_stats, a.list, a.row_cnt);
+  // K3: the row's occupied tiles' mask bits, tile-major at their list positions
+  const uint32_t cnt = __ldcg(a.row_cnt + p);
+  const uint4* m4 = reinterpret_cast<const uint4*>(a.mask);
+  for (uint32_t idx = threadIdx.x; idx < cnt * 128; idx += 256) {
+    const uint32_t k = idx >> 7, r = idx & 127;
+    const uint32_t q = __ldcg(a.list + static_cast<uint64_t>(p) * a.kcols + k) & 0x7FFFFFFFu;
+    a.bitmaps[(static_cast<uint64_t>(p) * a.kcols + k) * 128 + r] =
+        __ldcg(m4 + (static_cast<uint64_t>(p) * 128 + r) * a.kcols + q);
+  }
+  if (threadIdx.x == 0) a.ctr[p] = 0;
+
+  // ---- stage C: the last row to finish: block_stats totals and the LPT row order
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) s_last = atomicAdd(&a.ctr[a.krows], 1u) == a.krows - 1;
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  unsigned long long t0 = 0, t1 = 0, t2 = 0;
+  for (uint32_t r = threadIdx.x; r < a.krows; r += 256) {
+    t0 += __ldcg(a.row_stats + r * 3 + 0);
+    t1 += __ldcg(a.row_stats + r * 3 + 1);
+    t2 += __ldcg(a.row_stats + r * 3 + 2);
+  }
+  t0 = block_sum<256>(t0);
+  t1 = block_sum<256>(t1);
+  t2 = block_sum<256>(t2);
+  if (threadIdx.x == 0) {
+    a.totals[0] = t0;
+    a.totals[1] = t1;
+    a.totals[2] = t2;
+  }
+  lpt_sort<256>([&](uint32_t i) { return __ldcg(a.row_cnt + i); }, a.krows, a.kcols, a.scratch,
+                [&](uint32_t pos, uint32_t i) { a.order[pos] = i; });
+  if (threadIdx.x == 0) a.ctr[a.krows] = 0;
+}
+
+FusedArgs fused_args(const KernelMeta& km, uint64_t n) {
+  FusedArgs a{};
+  a.n = n;
+  a.krows = km.krows;
+  a.kcols = km.kcols;
+  a.chunks = (km.kcols + kChunkTiles - 1) / kChunkTiles;
+  a.mask = km.mask;
+  a.partial = km.partial;
+  a.sums = km.sums;
+  a.occ = km.occ;
+  a.run_off = km.run_off;
+  a.run_len = km.run_len;
+  a.row_cnt = km.row_cnt;
+  a.list = km.list;
+  a.order = km.order;
+  a.scratch = km.scratch;
+  a.ctr = km.ctr;
+  a.row_stats = km.row_stats;
+  a.totals = reinterpret_cast<unsigned long long*>(km.totals);
+  a.bitmaps = km.bitmaps;
+  return a;
+}
+
+uint64_t fused_grid(const FusedArgs& a) {
+  return static_cast<uint64_t>(a.chunks) * a.krows * kRowSplits;
+}
+
 inline unsigned grid_for(uint64_t work, unsigned block) {
   uint64_t g = (work + block - 1) / block;
   if (g > 148ull * 32) g = 148ull * 32;
@@ -321,6 +519,32 @@ void launch_pack_bool(const uint8_t* d_bool, uint64_t n, uint64_t stride, const 
     launch_sums128(km, s);
   }
   BBM_CUDA(cudaGetLastError());
+}
+
+bool launch_prep_fused_bool(const uint8_t* d_bool, uint64_t n, uint64_t stride, const KernelMeta& km,
+                            cudaStream_t s) {
+  const bool fast = (n % 16 == 0) && (stride % 16 == 0) &&
+                    (reinterpret_cast<uintptr_t>(d_bool) % 16 == 0);
+  FusedArgs a = fused_args(km, n);
+  const uint64_t grid = fused_grid(a);
+  if (!fast || grid >= (1ull << 31)) return false;
+  a.bools = d_bool;
+  a.stride = stride;
+  prep_fused_kernel<kInBool><<<static_cast<unsigned>(grid), 256, 0, s>>>(a);
+  BBM_CUDA(cudaGetLastError());
+  return true;
+}
+
+bool launch_prep_fused_words(const uint64_t* d_words, uint64_t in_wpr, uint64_t n, const KernelMeta& km,
+                             cudaStream_t s) {
+  FusedArgs a = fused_args(km, n);
+  const uint64_t grid = fused_grid(a);
+  if (grid >= (1ull << 31)) return false;
+  a.words = d_words;
+  a.in_wpr = in_wpr;
+  prep_fused_kernel<kInWords><<<static_cast<unsigned>(grid), 256, 0, s>>>(a);
+  BBM_CUDA(cudaGetLastError());
+  return true;
 }
 
 void launch_pad_packed(const uint64_t* d_words, uint64_t n, const KernelMeta& km,
