@@ -656,7 +656,7 @@ void launch_side(const Prep& prep, StreamCtx& ctx, const BwdArgs& a, const float
     p.cnt = km.row_cnt;
     p.list = km.list;
     p.list_stride = km.kcols;
-    p.order = p.all_tiles ? bm.all_order : km.order;
+    p.order = p.all_tiles ? bm.all_order : bm.row_order;
     p.bitmaps = km.bitmaps;
     p.ctr = ctx.ctr + 2;
     p.out0 = static_cast<__nv_bfloat16*>(a.dq);
@@ -724,6 +724,7 @@ void free_bwd_meta(BwdMeta& b) {
   cudaFree(b.col_cnt);
   cudaFree(b.col_list);
   cudaFree(b.col_order);
+  cudaFree(b.row_order);
   cudaFree(b.all_order);
   cudaFree(b.tbitmaps);
   cudaFree(b.scratch);
@@ -742,6 +743,7 @@ void ensure_bwd_meta(const Prep& prep, cudaStream_t s) {
       b.col_cnt = bwd_alloc<uint32_t>(kc);
       b.col_list = bwd_alloc<uint32_t>(static_cast<uint64_t>(kc) * kr);
       b.col_order = bwd_alloc<uint32_t>(kc);
+      b.row_order = bwd_alloc<uint32_t>(kr);
       b.all_order = bwd_alloc<uint32_t>(std::max(kr, kc));
       b.tbitmaps = bwd_alloc<uint4>(static_cast<uint64_t>(kc) * kr * 128);
       b.scratch = bwd_alloc<uint32_t>(static_cast<uint64_t>(kr) + kc + 2);
@@ -756,6 +758,7 @@ void ensure_bwd_meta(const Prep& prep, cudaStream_t s) {
     BBM_CUDA(cudaGetLastError());
     // LPT order of the columns (longest list first, ties by index), like the forward's row order
     launch_lpt_order(b.col_cnt, kc, kr, b.scratch, b.col_order, s);
+    launch_lpt_order(km.row_cnt, kr, kc, b.scratch, b.row_order, s);
     BBM_CUDA(cudaEventRecord(b.ready, s));
     b.version = prep.version;
   } else {

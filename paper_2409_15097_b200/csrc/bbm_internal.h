@@ -60,7 +60,7 @@ void once_per_device(std::atomic<uint64_t>& done, Set&& set) {
 //   list      : u32 [krows][kcols]       ascending occupied column tiles, bit 31 = full tile
 //                                        (never set on a ragged right-edge tile)
 //   row_cnt   : u32 [krows]              occupied tiles per query row tile
-//   order     : u32 [krows]              row tiles by descending row_cnt (LPT), ties by index
+//   order     : u32 [krows]              scratch for the row tiles' LPT order
 //   occ, run_off, run_len, row_stats, totals: the per-row pass's outputs at 128 x 128
 struct KernelMeta {
   uint32_t krows = 0, kcols = 0;
@@ -122,6 +122,7 @@ struct BwdMeta {
   uint32_t* col_cnt = nullptr;   // [kcols]
   uint32_t* col_list = nullptr;  // [kcols][krows]
   uint32_t* col_order = nullptr; // [kcols]
+  uint32_t* row_order = nullptr; // [krows] LPT order of the row tiles (dq items)
   uint32_t* all_order = nullptr; // [max(krows,kcols)] identity order (dense mode)
   uint4* tbitmaps = nullptr;     // [kcols*krows][128]
   uint32_t* scratch = nullptr;   // [kcols + krows + 2] ordering scratch

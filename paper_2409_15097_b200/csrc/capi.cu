@@ -68,14 +68,12 @@ T* dmalloc(uint64_t count) {
   return static_cast<T*>(p);
 }
 
-// Kernel view from km.sums (already built): lists, bitmaps, totals, LPT row order. Async, no
-// allocation, no host sync.
+// Kernel view from km.sums (already built): lists, bitmaps. Async, no allocation, no host sync.
+// (Totals and the LPT row order are derived on demand: spec_now, ensure_bwd_meta.)
 void build_kernel_view(const KernelMeta& km, uint64_t n, cudaStream_t s) {
   launch_rowmeta(km.sums, n, kTile, kTile, km.krows, km.kcols, km.occ, km.run_off, km.run_len,
                  km.row_stats, km.list, km.row_cnt, s);
   launch_compact_bitmaps(km, s);
-  launch_finalize(km.row_stats, km.krows, nullptr, nullptr, km.totals, s);
-  launch_lpt_order(km.row_cnt, km.krows, km.kcols, km.scratch, km.order, s);
 }
 
 // The complete kernel view from a dense bool mask / from packed words (in_wpr words per row; may
@@ -233,6 +231,8 @@ const SpecMeta& Prep::spec_now() const {
     uint32_t *d_sums = km.sums, *d_off = km.run_off, *d_tot = km.run_len;
     uint8_t* d_occ = km.occ;
     uint64_t *d_stats = km.row_stats, *d_totals = km.totals;
+    // the kernel view's totals (block_stats at 128 x 128) from its per-row statistics
+    launch_finalize(km.row_stats, km.krows, nullptr, nullptr, km.totals, s);
     if (!same) {  // the caller's BlockSpec from the padded mask (any spec, mask.hpp:184-247)
       const size_t b_sums = tiles * 4, b_occ = (tiles + 7) / 8 * 8, b_rows = sp.rows * 4;
       BBM_CUDA(cudaMalloc(&tmp, b_sums + b_occ + 2 * b_rows + sp.rows * 24 + 24 + 64));
@@ -548,7 +548,13 @@ bbm_status bbm_prep_get_kernel_lists(bbm_prep prep, uint32_t* row_cnt, uint32_t*
     if (list)
       BBM_CUDA(cudaMemcpy(list, km.list, static_cast<uint64_t>(km.krows) * km.kcols * 4,
                           cudaMemcpyDeviceToHost));
-    if (order) BBM_CUDA(cudaMemcpy(order, km.order, km.krows * 4, cudaMemcpyDeviceToHost));
+    if (order) {  // LPT order of the row tiles, derived on demand (private scratch)
+      uint32_t* tmp = dmalloc<uint32_t>(static_cast<uint64_t>(km.krows) * 2 + km.kcols + 2);
+      launch_lpt_order(km.row_cnt, km.krows, km.kcols, tmp + km.krows, tmp, nullptr);
+      const cudaError_t e = cudaMemcpy(order, tmp, km.krows * 4, cudaMemcpyDeviceToHost);
+      cudaFree(tmp);
+      BBM_CUDA(e);
+    }
   });
 }
 

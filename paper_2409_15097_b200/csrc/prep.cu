@@ -21,7 +21,6 @@
 #include <cstdint>
 
 #include "bbm_internal.h"
-#include "bbm_sort.cuh"
 
 namespace bbm {
 namespace {
@@ -316,8 +315,9 @@ __global__ void __launch_bounds__(1024) finalize_kernel(const uint64_t* __restri
 // rows into the padded mask and writes its per-tile popcounts as partial sums. The last CTA of tile
 // row p to finish (one atomic per CTA, threadfence-reduction pattern) adds the partials into the
 // tile sums and runs the per-row pass (occupancy, first run, stats, compacted list) and the bitmap
-// compaction of that row; the last row to finish sums the row statistics and builds the LPT row
-// order. Counters reset themselves, so the next launch needs no memset.
+// compaction of that row. Counters reset themselves, so the next launch needs no memset. The
+// row-statistics totals and the LPT row order are not on this path: the launches plan on the
+// device from row_cnt, and the totals are summed when the host asks for them.
 constexpr uint32_t kRowSplits = 8;                 // 128 rows / 16 per CTA
 constexpr uint32_t kSlabRows = 128 / kRowSplits;
 constexpr uint32_t kChunkTiles = 32;               // column tiles per CTA
@@ -333,9 +333,8 @@ struct FusedArgs {
   uint32_t* partial;     // [kRowSplits][krows][kcols]
   uint32_t* sums;
   uint8_t* occ;
-  uint32_t *run_off, *run_len, *row_cnt, *list, *order, *scratch, *ctr;
+  uint32_t *run_off, *run_len, *row_cnt, *list, *ctr;
   uint64_t* row_stats;
-  unsigned long long* totals;
   uint4* bitmaps;
 };
 enum : int { kInBool = 0, kInWords = 1 };
@@ -417,13 +416,17 @@ __global__ void __launch_bounds__(256) prep_fused_kernel(const FusedArgs a) {
       a.partial[(static_cast<uint64_t>(rs) * a.krows + p) * a.kcols + q] = s_cnt[threadIdx.x];
   }
 
-  // ---- stage B: the last CTA of tile row p builds that row's metadata
-  __threadfence();
+  // ---- stage B: the last CTA of tile row p builds that row's metadata. One thread publishes
+  // the CTA's writes (the barrier orders them before its cumulative fence) and, if last, acquires
+  // the other CTAs' writes for the whole CTA; reads of them go through L2 (__ldcg).
   __syncthreads();
-  if (threadIdx.x == 0) s_last = atomicAdd(&a.ctr[p], 1u) == a.chunks * kRowSplits - 1;
+  if (threadIdx.x == 0) {
+    __threadfence();
+    s_last = atomicAdd(&a.ctr[p], 1u) == a.chunks * kRowSplits - 1;
+    __threadfence();
+  }
   __syncthreads();
   if (!s_last) return;
-  __threadfence();
   for (uint32_t q = threadIdx.x; q < a.kcols; q += 256) {
     uint32_t sum = 0;
 #pragma unroll
@@ -444,30 +447,6 @@ __global__ void __launch_bounds__(256) prep_fused_kernel(const FusedArgs a) {
   }
   if (threadIdx.x == 0) a.ctr[p] = 0;
 
-  // ---- stage C: the last row to finish: block_stats totals and the LPT row order
-  __threadfence();
-  __syncthreads();
-  if (threadIdx.x == 0) s_last = atomicAdd(&a.ctr[a.krows], 1u) == a.krows - 1;
-  __syncthreads();
-  if (!s_last) return;
-  __threadfence();
-  unsigned long long t0 = 0, t1 = 0, t2 = 0;
-  for (uint32_t r = threadIdx.x; r < a.krows; r += 256) {
-    t0 += __ldcg(a.row_stats + r * 3 + 0);
-    t1 += __ldcg(a.row_stats + r * 3 + 1);
-    t2 += __ldcg(a.row_stats + r * 3 + 2);
-  }
-  t0 = block_sum<256>(t0);
-  t1 = block_sum<256>(t1);
-  t2 = block_sum<256>(t2);
-  if (threadIdx.x == 0) {
-    a.totals[0] = t0;
-    a.totals[1] = t1;
-    a.totals[2] = t2;
-  }
-  lpt_sort<256>([&](uint32_t i) { return __ldcg(a.row_cnt + i); }, a.krows, a.kcols, a.scratch,
-                [&](uint32_t pos, uint32_t i) { a.order[pos] = i; });
-  if (threadIdx.x == 0) a.ctr[a.krows] = 0;
 }
 
 FusedArgs fused_args(const KernelMeta& km, uint64_t n) {
@@ -484,11 +463,8 @@ FusedArgs fused_args(const KernelMeta& km, uint64_t n) {
   a.run_len = km.run_len;
   a.row_cnt = km.row_cnt;
   a.list = km.list;
-  a.order = km.order;
-  a.scratch = km.scratch;
   a.ctr = km.ctr;
   a.row_stats = km.row_stats;
-  a.totals = reinterpret_cast<unsigned long long*>(km.totals);
   a.bitmaps = km.bitmaps;
   return a;
 }
