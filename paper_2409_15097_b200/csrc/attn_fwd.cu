@@ -313,8 +313,9 @@ __global__ void __launch_bounds__(kThreadsOf<D>, 1)
     for (int b = 0; b < 2; ++b) {
       mbar_init(&ctl->o_full[b], 1);
       mbar_init(&ctl->o_empty[b], 128);                 // the epilogue warpgroup's threads
-      mbar_init(&ctl->stats_full[b], 4 * kParts<D>);    // engine warps
-      mbar_init(&ctl->stats_empty[b], 4);               // epilogue warps
+      // every thread of the handing-over side arrives, releasing its own writes
+      mbar_init(&ctl->stats_full[b], 128 * kParts<D>);  // engine threads
+      mbar_init(&ctl->stats_empty[b], 128);             // epilogue threads
     }
     for (uint32_t r = 0; r < C::kRing; ++r) {
       mbar_init(&ctl->ring_full[r], 1);
@@ -732,16 +733,14 @@ __global__ void __launch_bounds__(kThreadsOf<D>, 1)
         st.m_true[row] = m_true;
       }
       if (leader) st.item = it;
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&ctl->stats_full[sl]);
+      mbar_arrive(&ctl->stats_full[sl]);
       if (tracer) trace_ev<kTrace>(tracing, p, &ctl->trace_count, 28, 0, it.t);
     }
     {  // end marker for the epilogue warpgroup
       const uint32_t sl = items & 1;
       mbar_wait(&ctl->stats_empty[sl], se_ph[sl]);
       if (leader) ctl->stats[sl].item.t = kEnd;
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&ctl->stats_full[sl]);
+      mbar_arrive(&ctl->stats_full[sl]);
     }
   } else {
     setmaxnreg_dec<kOtherRegs>();
@@ -793,8 +792,7 @@ __global__ void __launch_bounds__(kThreadsOf<D>, 1)
 #pragma unroll
       for (uint32_t h = 0; h < kParts<D>; ++h) l_unit += st.l[h][row];
       const float m_run = st.m_run[row], m_true = st.m_true[row];
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&ctl->stats_empty[sl]);
+      mbar_arrive(&ctl->stats_empty[sl]);
       const uint32_t to = tmem + C::kOCol + lane_off + ob * D;
       if (leader) bulk_wait_group_read<0>();  // staging buffers free again
       mbar_wait(&ctl->o_full[ob], o_ph[ob]);
