@@ -575,6 +575,25 @@ def main():
                                     "ideal_speedup_by_tiles": dense_flops / flops}
         if args.which == "fwd":
             extras["preprocess"] = preprocess_measure(bbm, prep, dense_mask, stream, n, step, ms_step)
+        if args.which == "fwd" and fwd_perm is not None:
+            # f2: the same forward on ORIGINAL-order inputs with the RCM gather / scatter inside the
+            # kernel (TMA tile::gather4 / scatter4), against the pre-permuted forward above
+            rows = torch.from_numpy(np.ascontiguousarray(fwd_perm, dtype=np.int32)).to(dev)
+            og = torch.empty_like(q)
+
+            def gstep():
+                bbm.attn_fwd_device(prep, variant, q, k, v, og, rmax, rsum, scale, stream.cuda_stream, rows=rows)
+
+            for _ in range(3):
+                gstep()
+            g_ms = device_ms(stream, gstep, max(5, args.steps))
+            p_ms = device_ms(stream, step, max(5, args.steps))
+            extras["fwd_in_kernel_rcm_gather"] = {
+                "ms_per_step": g_ms, "pre_permuted_ms_per_step": p_ms, "ratio_vs_pre_permuted": g_ms / p_ms,
+                "tflops": flops / (g_ms * 1e-3) / 1e12,
+                "note": "original-order Q/K/V resident in HBM; rows gathered with TMA tile::gather4, O scattered "
+                        "with tile::scatter4, row stats at the original tokens (no permute passes)"}
+            del og
         if not args.no_cpu_baseline and world == 1 and args.which == "fwd":
             try:
                 info = cpu_info()

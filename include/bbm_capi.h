@@ -145,6 +145,15 @@ bbm_status bbm_attn_fwd(bbm_prep prep, int variant, const void* q, const void* k
                         void* out, float* row_max, float* row_sum, uint64_t slots,
                         uint32_t head_dim, double scale, void* stream);
 
+/* The same forward with the RCM permutation applied INSIDE the kernel (reorder.hpp:156-189
+ * fused into the loads): `prep` was built from permute_mask(mask, perm), d_forward = perm.forward
+ * (new -> old, device u32 [n]), and q/k/v/out/row stats stay in the ORIGINAL token order. The
+ * kernel gathers each tile's Q/K/V rows with TMA tile::gather4 and scatters O rows with
+ * tile::scatter4: no separate permute_rows / unpermute_rows passes. Requires slots * n < 2^31. */
+bbm_status bbm_attn_fwd_gather(bbm_prep prep, int variant, const uint32_t* d_forward, const void* q,
+                               const void* k, const void* v, void* out, float* row_max, float* row_sum,
+                               uint64_t slots, uint32_t head_dim, double scale, void* stream);
+
 /* Same, host buffers (bf16 bits as uint16): copies in, runs, copies out, synchronizes.
  * Pinned buffers get full PCIe bandwidth. Validates finiteness (engine.hpp:237-258). */
 bbm_status bbm_attn_fwd_host_bf16(bbm_prep prep, int variant, const uint16_t* q,

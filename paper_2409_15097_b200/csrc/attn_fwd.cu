@@ -74,6 +74,7 @@ struct FwdParams {
   __nv_bfloat16* out;
   float* row_max;
   float* row_sum;
+  const uint32_t* rows;  // gather mode: token of each (permuted) row position, new -> old [n]
   uint64_t* trace;       // optional event trace (bbm_set_trace), nullptr = off
   uint32_t trace_ctas;   // CTAs that record
 };
@@ -211,6 +212,17 @@ __device__ __forceinline__ ItemDesc decode_item(const FwdParams& p, uint32_t uni
   return d;
 }
 
+// Gather mode: the 2-D [slots * n][D] row of (permuted) position a of `slot`, or a coordinate past
+// the tensor (zero-filled loads, skipped stores) for the padding rows a >= n.
+__device__ __forceinline__ int32_t gather_row(const FwdParams& p, uint32_t slot, uint32_t a) {
+  return a < p.n ? static_cast<int32_t>(static_cast<uint64_t>(slot) * p.n + __ldg(p.rows + a)) : INT32_MAX;
+}
+// Output row of (permuted) row `grow` of `slot` in the caller's [slots][n] layout
+template <bool kGather>
+__device__ __forceinline__ uint64_t out_row(const FwdParams& p, uint32_t slot, uint64_t grow) {
+  return static_cast<uint64_t>(slot) * p.n + (kGather ? __ldg(p.rows + grow) : grow);
+}
+
 // Replace the scores of invisible keys by a sentinel in place: -inf (or +inf when the scale is
 // negative, so that scale * sentinel = -inf). The max and exp passes then need no selects.
 __device__ __forceinline__ void apply_mask(uint32_t (&r)[32], uint32_t mw, uint32_t sentinel) {
@@ -278,7 +290,7 @@ __device__ __forceinline__ void stage_chunk32(uint8_t* rowp, uint32_t row, uint3
   }
 }
 
-template <int D, int MODE, bool kTrace>
+template <int D, int MODE, bool kTrace, bool kGather>
 __global__ void __launch_bounds__(kThreadsOf<D>, 1)
     attn_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                     const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_o,
@@ -350,22 +362,43 @@ __global__ void __launch_bounds__(kThreadsOf<D>, 1)
     // Loads follow the MMA issuers' consumption order (kseq_of / vseq_of): a K cursor runs kSBufs
     // tiles ahead of a V cursor, so a load only ever waits for the ring slot freed kRing
     // positions earlier in that same order.
-    if (lane == 0) {
+    // The whole warp runs the loop (warp-uniform state; lane 0 owns the side effects: the work
+    // counter, the item queue, the expect-tx arrivals). Plain mode: lane 0 issues the tiled TMA
+    // loads. Gather mode (kGather): every lane gathers 4 rows of each 128-row tile
+    // (tile::gather4), so a tile costs 32 instructions per 64-column box spread over the warp.
+    {
       const uint64_t pol_q = policy_evict_first();
       const uint64_t pol_kv = policy_evict_last();
       uint32_t qi = 0, qiph = 1, qb = 0;
       PhaseBits qph{0x3u};
       ItemDesc pit[kQueue];  // items claimed by the K cursor, replayed by the V cursor
       uint32_t pw = 0, pr = 0;
+      // one 128 x D tile (row tile `tile` of `slot`) into dst, completing on `bar` (expect-tx
+      // already posted by lane 0)
+      auto issue_tile = [&](uint8_t* dst, const CUtensorMap* tm, uint64_t* bar, uint32_t tile, uint32_t slot,
+                            uint64_t pol) {
+        if constexpr (kGather) {
+          int32_t r[4];
+#pragma unroll
+          for (uint32_t i = 0; i < 4; ++i) r[i] = gather_row(p, slot, tile * 128 + lane * 4 + i);
+#pragma unroll
+          for (uint32_t b = 0; b < C::kBoxes; ++b)
+            tma_gather4(dst + b * kBoxBytes + lane * 512, tm, bar, b * 64, r[0], r[1], r[2], r[3], pol);
+        } else {
+          if (lane == 0)
+            for (uint32_t b = 0; b < C::kBoxes; ++b)
+              tma_load_3d(dst + b * kBoxBytes, tm, bar, b * 64, tile * 128, slot, pol);
+        }
+      };
       auto load_tile = [&](const CUtensorMap* tm, uint32_t seq, uint32_t q, uint32_t slot, uint32_t code,
                            uint32_t j) {
         const uint32_t r = seq % C::kRing;
         mbar_wait(&ctl->ring_empty[r], ((seq / C::kRing) & 1) ^ 1);
         uint64_t* full = &ctl->ring_full[r];
-        mbar_arrive_expect_tx(full, C::kTileBytes);
-        for (uint32_t b = 0; b < C::kBoxes; ++b)
-          tma_load_3d(ring + r * C::kTileBytes + b * kBoxBytes, tm, full, b * 64, q * 128, slot, pol_kv);
-        trace_ev<kTrace>(tracing, p, &ctl->trace_count, code, 0, j);
+        if (lane == 0) mbar_arrive_expect_tx(full, C::kTileBytes);
+        __syncwarp();
+        issue_tile(ring + r * C::kTileBytes, tm, full, q, slot, pol_kv);
+        if (lane == 0) trace_ev<kTrace>(tracing, p, &ctl->trace_count, code, 0, j);
       };
       // K cursor (claims and publishes items, loads Q)
       ItemDesc kit{};
@@ -374,10 +407,15 @@ __global__ void __launch_bounds__(kThreadsOf<D>, 1)
       auto k_next = [&]() -> bool {
         while (k_need) {
           if (k_done) return false;
-          const ItemDesc d = decode_item(p, ctl->units, ctl->total_items, atomicAdd(&p.work_ctr[0], 1u));
+          uint32_t t = 0;
+          if (lane == 0) t = atomicAdd(&p.work_ctr[0], 1u);
+          t = __shfl_sync(0xffffffffu, t, 0);
+          const ItemDesc d = decode_item(p, ctl->units, ctl->total_items, t);
           mbar_wait(&ctl->item_empty[qi], qiph);
-          ctl->items[qi] = d;
-          mbar_arrive(&ctl->item_full[qi]);  // release: the descriptor is visible to waiters
+          if (lane == 0) {
+            ctl->items[qi] = d;
+            mbar_arrive(&ctl->item_full[qi]);  // release: the descriptor is visible to waiters
+          }
           if (++qi == kQueue) { qi = 0; qiph ^= 1; }
           if (d.t == kEnd) {
             k_done = true;
@@ -388,11 +426,10 @@ __global__ void __launch_bounds__(kThreadsOf<D>, 1)
           kentry = entry_of<MODE>(p, d.rt, d.j0);
           mbar_wait(&ctl->q_empty[qb], qph[qb]);
           qph.flip(qb);
-          mbar_arrive_expect_tx(&ctl->q_full[qb], C::kTileBytes);
-          for (uint32_t b = 0; b < C::kBoxes; ++b)
-            tma_load_3d(sq + qb * C::kTileBytes + b * kBoxBytes, &tm_q, &ctl->q_full[qb], b * 64,
-                        d.rt * 128, d.slot, pol_q);
-          trace_ev<kTrace>(tracing, p, &ctl->trace_count, 1, 0, d.t);
+          if (lane == 0) mbar_arrive_expect_tx(&ctl->q_full[qb], C::kTileBytes);
+          __syncwarp();
+          issue_tile(sq + qb * C::kTileBytes, &tm_q, &ctl->q_full[qb], d.rt, d.slot, pol_q);
+          if (lane == 0) trace_ev<kTrace>(tracing, p, &ctl->trace_count, 1, 0, d.t);
           qb ^= 1;
           kit = d;
           kj = 0;
@@ -549,7 +586,7 @@ __global__ void __launch_bounds__(kThreadsOf<D>, 1)
     auto write_stats = [&](const ItemDesc& it, float m_true2, float m_run2, float l_tot) {
       const uint64_t grow = static_cast<uint64_t>(it.rt) * 128 + row;
       if (half == 0 && grow < p.n) {
-        const uint64_t si = static_cast<uint64_t>(it.slot) * p.n + grow;
+        const uint64_t si = out_row<kGather>(p, it.slot, grow);
         if (p.row_max) p.row_max[si] = m_true2 == -INFINITY ? -INFINITY : m_true2 * kLn2;
         if (p.row_sum) p.row_sum[si] = l_tot > 0.0f ? l_tot * exp2f(m_run2 - m_true2) : 0.0f;
       }
@@ -558,8 +595,7 @@ __global__ void __launch_bounds__(kThreadsOf<D>, 1)
     auto zero_item = [&](const ItemDesc& it) {
       const uint64_t grow = static_cast<uint64_t>(it.rt) * 128 + row;
       if (grow >= p.n) return;
-      uint4* dst = reinterpret_cast<uint4*>(p.out + (static_cast<uint64_t>(it.slot) * p.n + grow) * D +
-                                            half * kHalfO);
+      uint4* dst = reinterpret_cast<uint4*>(p.out + out_row<kGather>(p, it.slot, grow) * D + half * kHalfO);
       for (uint32_t v = 0; v < kHalfO / 8; ++v) dst[v] = make_uint4(0, 0, 0, 0);
       write_stats(it, -INFINITY, -INFINITY, 0.0f);
     };
@@ -758,24 +794,34 @@ __global__ void __launch_bounds__(kThreadsOf<D>, 1)
     auto write_stats = [&](const ItemDesc& it, float m_true2, float m_run2, float l_tot) {
       const uint64_t grow = static_cast<uint64_t>(it.rt) * 128 + row;
       if (grow < p.n) {
-        const uint64_t si = static_cast<uint64_t>(it.slot) * p.n + grow;
+        const uint64_t si = out_row<kGather>(p, it.slot, grow);
         if (p.row_max) p.row_max[si] = m_true2 == -INFINITY ? -INFINITY : m_true2 * kLn2;
         if (p.row_sum) p.row_sum[si] = l_tot > 0.0f ? l_tot * exp2f(m_run2 - m_true2) : 0.0f;
       }
     };
     // The O tile leaves one 64-column box at a time through a single staging box: TMA-store box b
     // of item `it` once staged (called by every epilogue thread) ...
+    // (gather mode: the first epilogue warp scatters the box's rows, 4 per lane, to their tokens)
+    const bool storer = kGather ? quad == 0 : leader;
     auto store_box = [&](const ItemDesc& it, uint32_t b) {
       fence_proxy_async_smem();
       named_bar_sync(2, kEpi);
-      if (leader) {
+      if constexpr (kGather) {
+        if (quad == 0) {
+          int32_t r[4];
+#pragma unroll
+          for (uint32_t i = 0; i < 4; ++i) r[i] = gather_row(p, it.slot, it.rt * 128 + lane * 4 + i);
+          tma_scatter4(&tm_o, stage + lane * 512, b * 64, r[0], r[1], r[2], r[3]);
+          bulk_commit_group();
+        }
+      } else if (leader) {
         tma_store_3d(&tm_o, stage, b * 64, it.rt * 128, it.slot);
         bulk_commit_group();
       }
     };
     // ... and wait until the previous box's store has read the staging memory
     auto box_free = [&]() {
-      if (leader) bulk_wait_group_read<0>();
+      if (storer) bulk_wait_group_read<0>();
       named_bar_sync(2, kEpi);
     };
     // staged output column c goes to 16-byte chunk (c % 64) / 8 of the row
@@ -794,7 +840,7 @@ __global__ void __launch_bounds__(kThreadsOf<D>, 1)
       const float m_run = st.m_run[row], m_true = st.m_true[row];
       mbar_arrive(&ctl->stats_empty[sl]);
       const uint32_t to = tmem + C::kOCol + lane_off + ob * D;
-      if (leader) bulk_wait_group_read<0>();  // staging buffers free again
+      if (storer) bulk_wait_group_read<0>();  // staging buffers free again
       mbar_wait(&ctl->o_full[ob], o_ph[ob]);
       o_ph.flip(ob);
       tc_fence_after();
@@ -901,7 +947,7 @@ __global__ void __launch_bounds__(kThreadsOf<D>, 1)
       }
       if (tracer) trace_ev<kTrace>(tracing, p, &ctl->trace_count, 24, 0, it.t);
     }
-    if (leader) bulk_wait_group<0>();  // O stores landed
+    if (storer) bulk_wait_group<0>();  // O stores landed
   }
 
   tc_fence_before();
@@ -920,7 +966,7 @@ __global__ void __launch_bounds__(kThreadsOf<D>, 1)
 
 // ------------------------------------------------------------------ host side
 
-template <int D, int MODE>
+template <int D, int MODE, bool kGather>
 void launch_impl(const Prep& prep, const AttnArgs& a, cudaStream_t s, int num_sms) {
   static_assert(smem_bytes<D>() <= 232448, "exceeds the 227 KB opt-in shared memory");
   const KernelMeta& km = prep.kmeta;
@@ -937,11 +983,14 @@ void launch_impl(const Prep& prep, const AttnArgs& a, cudaStream_t s, int num_sm
   float* ws = can_split ? ctx_workspace(ctx, plan_cap_chunks(a.slots, workers) * 128 * (128 + 3), s) : nullptr;
   uint32_t* split_ctr = can_split ? ctx_split_ctr(ctx, plan_cap_chunks(a.slots, workers) + a.slots, s) : nullptr;
 
-  const CUtensorMap tq = cached_tmap_bf16_3d(a.q, D, a.n, a.slots, 64, 128);
-  const CUtensorMap tk = cached_tmap_bf16_3d(a.k, D, a.n, a.slots, 64, 128);
-  const CUtensorMap tv = cached_tmap_bf16_3d(a.v, D, a.n, a.slots, 64, 128);
-  const CUtensorMap to = cached_tmap_bf16_3d(a.o, D, a.n, a.slots, 64, 128);
+  // plain: 3-D [slots][n][D] maps with 128-row boxes; gather: 2-D [slots * n][D] row maps
+  auto tmap = [&](const void* base) {
+    return kGather ? make_tmap_bf16_rows(base, D, a.slots * a.n, 64)
+                   : cached_tmap_bf16_3d(base, D, a.n, a.slots, 64, 128);
+  };
+  const CUtensorMap tq = tmap(a.q), tk = tmap(a.k), tv = tmap(a.v), to = tmap(a.o);
   FwdParams p{};
+  p.rows = a.rows;
   p.n = a.n;
   p.slots = static_cast<uint32_t>(a.slots);
   p.krows = km.krows;
@@ -965,28 +1014,34 @@ void launch_impl(const Prep& prep, const AttnArgs& a, cudaStream_t s, int num_sm
   p.row_sum = a.row_sum;
   p.trace = static_cast<uint64_t*>(g_trace.buffer);
   p.trace_ctas = g_trace.ctas;
-  static std::atomic<uint64_t> attr_devices{0};  // per (D, MODE) instantiation
+  static std::atomic<uint64_t> attr_devices{0};  // per (D, MODE, kGather) instantiation
   once_per_device(attr_devices, [] {
-    BBM_CUDA(cudaFuncSetAttribute(attn_fwd_kernel<D, MODE, false>,
+    BBM_CUDA(cudaFuncSetAttribute(attn_fwd_kernel<D, MODE, false, kGather>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes<D>()));
-    BBM_CUDA(cudaFuncSetAttribute(attn_fwd_kernel<D, MODE, true>,
-                                  cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes<D>()));
+    if constexpr (!kGather)
+      BBM_CUDA(cudaFuncSetAttribute(attn_fwd_kernel<D, MODE, true, false>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes<D>()));
   });
-  if (p.trace)  // event-tracing build of the same kernel (bbm_set_trace)
-    attn_fwd_kernel<D, MODE, true><<<grid, kThreadsOf<D>, smem_bytes<D>(), s>>>(tq, tk, tv, to, p);
-  else
-    attn_fwd_kernel<D, MODE, false><<<grid, kThreadsOf<D>, smem_bytes<D>(), s>>>(tq, tk, tv, to, p);
+  if constexpr (!kGather) {
+    if (p.trace) {  // event-tracing build of the same kernel (bbm_set_trace)
+      attn_fwd_kernel<D, MODE, true, false><<<grid, kThreadsOf<D>, smem_bytes<D>(), s>>>(tq, tk, tv, to, p);
+      BBM_CUDA(cudaGetLastError());
+      mark_launch_done(ctx, s);
+      return;
+    }
+  }
+  attn_fwd_kernel<D, MODE, false, kGather><<<grid, kThreadsOf<D>, smem_bytes<D>(), s>>>(tq, tk, tv, to, p);
   BBM_CUDA(cudaGetLastError());
   mark_launch_done(ctx, s);
 }
 
-template <int D>
+template <int D, bool kGather>
 void launch_d(const Prep& prep, const AttnArgs& a, cudaStream_t s, int num_sms) {
   switch (a.variant) {
-    case 0: launch_impl<D, kModeDense>(prep, a, s, num_sms); break;
-    case 1: launch_impl<D, kModeNaive>(prep, a, s, num_sms); break;
-    case 2: launch_impl<D, kModeBinblk>(prep, a, s, num_sms); break;
-    case 3: launch_impl<D, kModeDenseBinblk>(prep, a, s, num_sms); break;
+    case 0: launch_impl<D, kModeDense, kGather>(prep, a, s, num_sms); break;
+    case 1: launch_impl<D, kModeNaive, kGather>(prep, a, s, num_sms); break;
+    case 2: launch_impl<D, kModeBinblk, kGather>(prep, a, s, num_sms); break;
+    case 3: launch_impl<D, kModeDenseBinblk, kGather>(prep, a, s, num_sms); break;
     default: throw ArgError("unknown variant");
   }
 }
@@ -998,9 +1053,15 @@ void launch_attn_fwd(const Prep& prep, const AttnArgs& a, cudaStream_t s, int nu
   require(a.n == prep.n, "mask preprocessing does not match this problem");
   require(a.slots < (1ull << 24), "too many slots for one launch");
   if (a.slots * prep.kmeta.krows == 0) return;
-  if (a.d == 64) launch_d<64>(prep, a, s, num_sms);
-  else if (a.d == 128) launch_d<128>(prep, a, s, num_sms);
-  else throw ArgError("head dim must be 64 or 128 on the sm_100a kernel");
+  if (a.d != 64 && a.d != 128) throw ArgError("head dim must be 64 or 128 on the sm_100a kernel");
+  if (a.rows) {  // in-kernel RCM gather / scatter of token rows (2-D row coordinates are int32)
+    require(a.slots * a.n < (1ull << 31) - 1, "too many rows for the gather path (slots * n >= 2^31)");
+    if (a.d == 64) launch_d<64, true>(prep, a, s, num_sms);
+    else launch_d<128, true>(prep, a, s, num_sms);
+  } else {
+    if (a.d == 64) launch_d<64, false>(prep, a, s, num_sms);
+    else launch_d<128, false>(prep, a, s, num_sms);
+  }
 }
 
 int attn_fwd_kernel_launches_per_call() { return 1; }

@@ -226,6 +226,10 @@ struct AttnArgs {
   uint32_t d;
   float scale;
   int variant;
+  // optional in-kernel RCM application (reorder.hpp:156-189): device u32 [n], forward map new ->
+  // old. q/k/v/o and the row statistics are then in the ORIGINAL token order while the prep holds
+  // the permuted mask: rows are gathered / scattered by TMA inside the kernel.
+  const uint32_t* rows = nullptr;
 };
 // Process-wide kernel event trace (bbm_set_trace): device buffer of ctas * 8192 u64 events.
 struct TraceConfig {

@@ -135,6 +135,30 @@ __device__ __forceinline__ void tma_store_3d(const void* tmap, const void* smem_
       "r"(smem_u32(smem_src)), "r"(c0), "r"(c1), "r"(c2)
       : "memory");
 }
+// Row gather (TMA tile::gather4): 4 rows r0..r3 of a 2-D tensor map whose box is {64 elements, 1
+// row}, at column c0, into 4 consecutive 128-byte rows of shared memory (the 128B swizzle follows
+// the shared-memory address, so 32 gathers fill a 128-row box exactly like one tiled load).
+// Rows beyond the tensor are zero-filled.
+__device__ __forceinline__ void tma_gather4(void* smem_dst, const void* tmap, uint64_t* bar, int32_t c0,
+                                            int32_t r0, int32_t r1, int32_t r2, int32_t r3,
+                                            uint64_t cache_policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%3, %4, %5, %6, %7}], [%2], %8;" ::"r"(smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(tmap)), "r"(smem_u32(bar)), "r"(c0), "r"(r0), "r"(r1), "r"(r2),
+      "r"(r3), "l"(cache_policy)
+      : "memory");
+}
+// Row scatter (TMA tile::scatter4): 4 consecutive 128-byte shared-memory rows to rows r0..r3 of a
+// 2-D tensor map at column c0 (bulk async group). Rows beyond the tensor are skipped.
+__device__ __forceinline__ void tma_scatter4(const void* tmap, const void* smem_src, int32_t c0, int32_t r0,
+                                             int32_t r1, int32_t r2, int32_t r3) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.global.shared::cta.tile::scatter4.bulk_group [%0, {%2, %3, %4, %5, %6}], [%1];" ::"l"(
+          reinterpret_cast<uint64_t>(tmap)),
+      "r"(smem_u32(smem_src)), "r"(c0), "r"(r0), "r"(r1), "r"(r2), "r"(r3)
+      : "memory");
+}
 __device__ __forceinline__ void bulk_commit_group() {
   asm volatile("cp.async.bulk.commit_group;" ::: "memory");
 }

@@ -52,6 +52,23 @@ inline CUtensorMap make_tmap_bf16_3d(const void* base, uint64_t inner, uint64_t 
   return m;
 }
 
+// bf16 matrix [rows][inner] as a 2-D map with a {box_inner, 1} box and 128-byte swizzle: the form
+// TMA tile::gather4 / tile::scatter4 address rows through.
+inline CUtensorMap make_tmap_bf16_rows(const void* base, uint64_t inner, uint64_t rows, uint32_t box_inner) {
+  CUtensorMap m{};
+  cuuint64_t dims[2] = {inner, rows};
+  cuuint64_t strides[1] = {inner * 2};
+  cuuint32_t box[2] = {box_inner, 1};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = get_encode_tiled()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims,
+                                  strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                  CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    throw std::runtime_error("cuTensorMapEncodeTiled (rows) failed with code " + std::to_string(int(r)));
+  return m;
+}
+
 // The same descriptor, cached per (pointer, shape, box): encoding costs a few microseconds, more
 // than a whole small launch. Descriptors are plain values (no device state), so a stale entry for
 // a freed-and-reused address is still exactly the descriptor of that address and shape.

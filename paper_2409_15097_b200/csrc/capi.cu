@@ -793,6 +793,22 @@ bbm_status bbm_attn_fwd(bbm_prep prep, int variant, const void* q, const void* k
   });
 }
 
+bbm_status bbm_attn_fwd_gather(bbm_prep prep, int variant, const uint32_t* d_forward, const void* q,
+                               const void* k, const void* v, void* out, float* row_max, float* row_sum,
+                               uint64_t slots, uint32_t head_dim, double scale, void* stream) {
+  return guarded([&] {
+    const Prep& pr = unwrap(prep);
+    check_attn_args(pr, variant, slots, head_dim, scale);
+    require(q && k && v && out && d_forward, "null pointer");
+    AttnArgs a{q, k, v, out, row_max, row_sum, slots, pr.n, head_dim, static_cast<float>(scale),
+               variant, d_forward};
+    int dev = 0;
+    BBM_CUDA(cudaGetDevice(&dev));
+    require(dev == pr.device, "prep lives on another device; use bbm_prep_replicate");
+    launch_attn_fwd(pr, a, static_cast<cudaStream_t>(stream), sm_count(dev));
+  });
+}
+
 bbm_status bbm_attn_fwd_host_bf16(bbm_prep prep, int variant, const uint16_t* q, const uint16_t* k,
                                   const uint16_t* v, uint16_t* out, float* row_max,
                                   float* row_sum, uint64_t slots, uint32_t head_dim,

@@ -397,3 +397,41 @@ def test_mixed_items_in_one_launch(cuda, d):
         out, rmax, rsum, _ = run_gpu(mask, q, k, v, scale, var, cuda, prep=prep)
         check_against_oracle(mask, q, k, v, scale, out, rmax, rsum, var)
         assert np.all(out[:, 1280:1408] == 0) and np.all(rmax[:, 1280:1408] == -np.inf)
+
+
+@pytest.mark.parametrize("n,d,slots,spec", [(1000, 64, 3, "windowed(w=40)"), (2304, 128, 2, "global(w=90;g=70)"),
+                                            (640, 128, 5, "causal")])
+def test_in_kernel_rcm_gather_equals_explicit_permutation(cuda, n, d, slots, spec):
+    """bbm_attn_fwd_gather (f2): original-order Q/K/V, the prep of the RCM-permuted mask, rows
+    gathered / O scattered by TMA inside the kernel == permute_rows + forward + unpermute_rows,
+    bit for bit, for every variant (incl. ragged n and split-KV rows)."""
+    import torch
+
+    base = bbm.generate(spec, n)
+    shuffled = bbm.relabel(base, 5)
+    perm = bbm.rcm_order(shuffled)
+    pm = bbm.permute_mask(shuffled, perm)
+    prep = bbm.preprocess_mask(pm, bbm.BlockSpec(128, 128))
+    g = torch.Generator(device=cuda).manual_seed(n + d)
+    q, k, v = ((torch.rand((slots, n, d), generator=g, device=cuda) * 2 - 1).to(torch.bfloat16) for _ in range(3))
+    rows = torch.from_numpy(perm.forward.astype(np.int32)).to(cuda)
+    fwd = torch.from_numpy(perm.forward.astype(np.int64)).to(cuda)
+    for var in bbm.Variant:
+        out = torch.empty_like(q)
+        m = torch.empty((slots, n), dtype=torch.float32, device=cuda)
+        l = torch.empty_like(m)
+        bbm.attn_fwd_device(prep, var, q, k, v, out, m, l, d ** -0.5, rows=rows)
+        qp, kp, vp = (bbm.permute_rows(t, perm) for t in (q, k, v))
+        op = torch.empty_like(qp)
+        mp = torch.empty_like(m)
+        lp = torch.empty_like(m)
+        bbm.attn_fwd_device(prep, var, qp, kp, vp, op, mp, lp, d ** -0.5)
+        want_o = bbm.unpermute_rows(op, perm)
+        want_m = torch.empty_like(mp)
+        want_l = torch.empty_like(lp)
+        want_m[:, fwd] = mp
+        want_l[:, fwd] = lp
+        torch.cuda.synchronize()
+        assert torch.equal(out.view(torch.int16), want_o.view(torch.int16)), var
+        assert torch.equal(m.view(torch.int32), want_m.view(torch.int32)), var
+        assert torch.equal(l.view(torch.int32), want_l.view(torch.int32)), var
