@@ -266,6 +266,13 @@ bbm_status bbm_preprocess_mask_file(const char* path, uint64_t block_i, uint64_t
 /* ---- generators.hpp (host fixtures): MaskSpec grammar (generators.hpp:364-438); families with
  *      a free n take n_free. Call with words == NULL to query n. ---- */
 bbm_status bbm_generate(const char* spec, uint64_t n_free, uint64_t* n_out, uint64_t* words);
+/* The same, generated straight into DEVICE memory (d_words: n * ceil(n/64) u64 on the current
+ * device, NULL to query n), asynchronously on `stream`: causal, all-ones, windowed, dilated,
+ * global and random (one mt19937_64 stream over the n^2 entries, as generators.hpp:171-183) run
+ * as kernels, bit-identical to the reference; the other families are built on the host and
+ * uploaded. */
+bbm_status bbm_generate_device(const char* spec, uint64_t n_free, uint64_t* n_out, uint64_t* d_words,
+                               void* stream);
 /* make_problem's input stream (bench.hpp:320-337, rng.hpp:15-42): per slot q, k, v, d_out
  * (n x d each, uniform [-1,1) from one mt19937_64(seed), drawn in that order), as float. Host. */
 bbm_status bbm_make_problem(uint64_t seed, uint64_t slots, uint64_t n, uint64_t d, float* q,

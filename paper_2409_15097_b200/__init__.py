@@ -15,7 +15,7 @@ from .blockmask import (BlockOccupancy, BlockSpec, BlockStats, BlockSums, DenseR
                         Variant, attn_fwd_device, bandwidth, block_stats, block_sums,
                         blocked_forward, build_block_occupancy, build_dense_runs, generate,
                         parse_variant, permute_mask, permute_rows, preprocess_mask, rcm_order,
-                        import_prep_ipc, relabel, run_attention, run_attention_multi, shard_slots, to_string,
+                        generate_device, import_prep_ipc, relabel, run_attention, run_attention_multi, shard_slots, to_string,
                         unpermute_rows)
 
 LIB_PATH = _lib.LIB_PATH

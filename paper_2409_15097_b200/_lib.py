@@ -94,6 +94,7 @@ SIGNATURES = {
     "bbm_permute_rows_device": (C.c_int, [vp, vp, vp, C.c_uint64, C.c_uint64, C.c_uint64, C.c_int, vp]),
     "bbm_permute_mask_device": (C.c_int, [vp, vp, vp, C.c_uint64, vp]),
     "bbm_generate": (C.c_int, [C.c_char_p, C.c_uint64, u64p, u64p]),
+    "bbm_generate_device": (C.c_int, [C.c_char_p, C.c_uint64, u64p, vp, vp]),
     "bbm_relabel": (C.c_int, [u64p, C.c_uint64, C.c_uint64, u64p]),
     "bbm_write_mask_file": (C.c_int, [C.c_char_p, u64p, C.c_uint64]),
     "bbm_read_mask_file": (C.c_int, [C.c_char_p, u64p, u64p]),

@@ -804,6 +804,22 @@ def generate(spec: str, n: int = 0) -> Mask:
     return m
 
 
+def generate_device(spec: str, n: int = 0, device: int = 0, stream=None):
+    """generate() straight into device memory: a CUDA int64 tensor [n][ceil(n/64)] holding the
+    reference's packed words (bbm_generate_device; random / band families run on the GPU)."""
+    import torch
+
+    n_out = C.c_uint64(0)
+    check(lib.bbm_generate_device(spec.encode(), n, C.byref(n_out), None, None))
+    m = int(n_out.value)
+    dev = torch.device("cuda", device)
+    words = torch.empty((m, (m + 63) // 64), dtype=torch.int64, device=dev)
+    with torch.cuda.device(dev):
+        s = stream if stream is not None else torch.cuda.current_stream(dev).cuda_stream
+        check(lib.bbm_generate_device(spec.encode(), n, C.byref(n_out), C.c_void_p(words.data_ptr()), C.c_void_p(s)))
+    return words
+
+
 def _join(xs: Iterable[int]) -> str:
     return ";".join(str(int(x)) for x in xs)
 

@@ -203,6 +203,18 @@ void launch_compact_bitmaps(const KernelMeta& km, cudaStream_t s);
 void launch_finalize(const uint64_t* d_row_stats, uint64_t rows, const uint32_t* d_cnt,
                      uint32_t* d_order, uint64_t* d_totals /* 3 */, cudaStream_t s);
 
+// ---- device mask generators (gen.cu; spec parsing in host_generators.cpp) ----
+enum GenFamily : int { kGenCausal = 0, kGenAllOnes, kGenWindowed, kGenDilated, kGenGlobal, kGenRandom };
+struct GenSpec {
+  int family = 0;
+  uint64_t n = 0, w = 0, d = 1, g = 0, seed = 0;
+  double p = 0.0;
+  bool causal = false, diag = true;
+};
+// true (and `out` filled, validated like the reference) for the families generated on the device
+bool parse_device_family(const std::string& spec, uint64_t n_free, GenSpec& out);
+void launch_generate(const GenSpec& g, uint64_t* d_words, cudaStream_t s);
+
 // ---- mask files (mask_io.cu) ----
 void launch_bbmk_unpack(const uint8_t* d_payload, uint64_t n, uint64_t* d_words, uint64_t wpr,
                         uint64_t rows_out, cudaStream_t s);

@@ -287,6 +287,57 @@ Bits parse_and_generate(const std::string& text, uint64_t n_free) {
   throw ArgError("unknown mask family: '" + name + "'");
 }
 
+}  // namespace
+
+// The families gen.cu builds on the device, with the host parser's validation (same messages).
+bool bbm::parse_device_family(const std::string& text, uint64_t n_free, bbm::GenSpec& g) {
+  std::string name = text, body;
+  const size_t open = text.find_first_of("[(");
+  if (open != std::string::npos) {
+    const char close = text[open] == '[' ? ']' : ')';
+    require(text.back() == close, "unbalanced bracket in mask spec: '" + text + "'");
+    name = text.substr(0, open);
+    body = text.substr(open + 1, text.size() - open - 2);
+  }
+  g = bbm::GenSpec{};
+  g.n = n_free;
+  if (name == "causal" || name == "all-ones") {
+    require(n_free >= 1, "n must be positive");
+    g.family = name == "causal" ? bbm::kGenCausal : bbm::kGenAllOnes;
+    return true;
+  }
+  if (name == "windowed" || name == "dilated" || name == "global") {
+    for (const auto& [k, v] : kv(body)) {
+      if (k == "w") g.w = to_size(v);
+      else if (name == "windowed" && k == "causal") g.causal = to_size(v) != 0;
+      else if (name == "dilated" && k == "d") g.d = to_size(v);
+      else if (name == "global" && k == "g") g.g = to_size(v);
+      else throw ArgError("unknown " + name + " parameter: " + k);
+    }
+    g.family = name == "windowed" ? bbm::kGenWindowed : name == "dilated" ? bbm::kGenDilated : bbm::kGenGlobal;
+    if (g.family == bbm::kGenGlobal) require(g.g <= n_free, "global token count must be <= n");
+    require(n_free >= 1, "n must be positive");
+    require(g.w < n_free, "window must be < n");
+    if (g.family == bbm::kGenDilated) require(g.d >= 1, "dilation must be >= 1");
+    return true;
+  }
+  if (name == "random") {
+    for (const auto& [k, v] : kv(body)) {
+      if (k == "p") g.p = to_double(v);
+      else if (k == "seed") g.seed = to_size(v);
+      else if (k == "diag") g.diag = to_size(v) != 0;
+      else throw ArgError("unknown random parameter: " + k);
+    }
+    require(n_free >= 1, "n must be positive");
+    require(g.p >= 0.0 && g.p <= 1.0, "density must be in [0, 1]");
+    g.family = bbm::kGenRandom;
+    return true;
+  }
+  return false;
+}
+
+namespace {
+
 template <class F>
 bbm_status guard(F&& f) {
   try {
@@ -310,6 +361,29 @@ extern "C" bbm_status bbm_generate(const char* spec, uint64_t n_free, uint64_t* 
     const Bits m = parse_and_generate(spec, n_free);
     *n_out = m.n;
     if (words) std::memcpy(words, m.w.data(), m.w.size() * 8);
+  });
+}
+
+// generate (generators.hpp:233-438) straight into device memory (d_words: n * ceil(n/64) u64 on
+// the current device; NULL queries n). The families of gen.cu run on the device; the others are
+// built on the host and uploaded.
+extern "C" bbm_status bbm_generate_device(const char* spec, uint64_t n_free, uint64_t* n_out,
+                                          uint64_t* d_words, void* stream) {
+  return guard([&] {
+    require(spec != nullptr && n_out != nullptr, "null argument");
+    bbm::GenSpec g;
+    const cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (bbm::parse_device_family(spec, n_free, g)) {
+      *n_out = g.n;
+      if (d_words) bbm::launch_generate(g, d_words, s);
+      return;
+    }
+    const Bits m = parse_and_generate(spec, n_free);
+    *n_out = m.n;
+    if (d_words) {
+      BBM_CUDA(cudaMemcpyAsync(d_words, m.w.data(), m.w.size() * 8, cudaMemcpyHostToDevice, s));
+      BBM_CUDA(cudaStreamSynchronize(s));
+    }
   });
 }
 
