@@ -55,21 +55,22 @@ enum Side : int { kSideDQ = 0, kSideDKDV = 1 };
 
 constexpr uint32_t kThreads = 384;
 constexpr uint32_t kQueue = 4;
-constexpr uint32_t kEnd = 0xFFFFFFFFu;
+constexpr uint32_t kEnd = 0xFFFFFFFFu;  // kNoSplit: bbm_internal.h
 constexpr uint32_t kBoxBytes = 128 * 64 * 2;
 constexpr float kLog2e = 1.4426950408889634f;
 
 struct BwdParams {
   uint64_t n;
-  uint32_t slots, tiles;      // items = slots * tiles (tiles = key tiles | query row tiles)
-  uint32_t partners;          // dense mode: every tile has this many partners
-  uint32_t total_items;
+  uint32_t slots;
   float sl2, scale;
   bool all_tiles;             // dense variant: every partner, no mask
-  const uint32_t* cnt;        // [tiles] list lengths (list mode)
+  const PlanHdr* hdr;         // device-built plan (plan.cu): units per slot, split rows / chunks
+  const uint4* unit_desc;     // [units] {tile, j0, partners walked, split | kNoSplit}, longest first
+  const uint2* split_info;    // [split tiles] {chunks, first workspace chunk}
+  float* ws;                  // split partials: [slots][split_chunks][128][accumulator columns]
+  uint32_t* split_ctr;        // [slots][split rows] finished chunks (reset by the combiner)
   const uint32_t* list;       // [tiles][stride] partner entries, bit 31 = full
   uint32_t list_stride;
-  const uint32_t* order;      // [tiles] LPT order
   const uint4* bitmaps;       // list-position tile-major bits (row bitmaps | transposed)
   const float* lse2;          // [slots][rows_pad], NEGATED (-lse2, rowstats_kernel)
   const float* delta;         // [slots][rows_pad], NEGATED (-delta)
@@ -99,7 +100,7 @@ __device__ __forceinline__ void trace_ev(bool on, const BwdParams& p, uint32_t* 
 }
 
 struct ItemDesc {
-  uint32_t t, slot, tile, nt;
+  uint32_t t, slot, tile, j0, nt, split;
 };
 
 template <int D, int SIDE>
@@ -125,6 +126,8 @@ struct BwdCtl {
   uint64_t item_full[kQueue], item_empty[kQueue];
   ItemDesc items[kQueue];
   uint32_t tmem_base;
+  uint32_t units, total_items, split_rows, split_chunks;  // this launch's plan
+  uint32_t bcast;
   uint32_t trace_count;
 };
 
@@ -134,16 +137,19 @@ constexpr uint32_t bwd_smem_bytes() {
   return 2 * C::kTileBytes + C::kStages * C::kStageAlloc + C::kOutStage + sizeof(BwdCtl);
 }
 
-__device__ __forceinline__ ItemDesc bwd_decode(const BwdParams& p, uint32_t t) {
+__device__ __forceinline__ ItemDesc bwd_decode(const BwdParams& p, uint32_t units, uint32_t total, uint32_t t) {
   ItemDesc d{};
-  if (t >= p.total_items) {
+  if (t >= total) {
     d.t = kEnd;
     return d;
   }
   d.t = t;
-  d.slot = t / p.tiles;
-  d.tile = p.order[t - d.slot * p.tiles];
-  d.nt = p.all_tiles ? p.partners : p.cnt[d.tile];
+  d.slot = t / units;
+  const uint4 u = p.unit_desc[t - d.slot * units];
+  d.tile = u.x;
+  d.j0 = u.y;
+  d.nt = u.z;
+  d.split = u.w;
   return d;
 }
 
@@ -180,6 +186,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   const bool tracing = kTrace && blockIdx.x < p.trace_ctas;
   if (threadIdx.x == 0) {
     ctl->trace_count = 0;
+    const PlanHdr h = *p.hdr;
+    ctl->units = h.units;
+    ctl->total_items = h.units * p.slots;
+    ctl->split_rows = h.split_rows;
+    ctl->split_chunks = h.split_chunks;
     mbar_init(&ctl->fixed_full, 1);
     mbar_init(&ctl->fixed_empty, 1);
     for (int h = 0; h < 2; ++h) {
@@ -222,7 +233,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint64_t pol_stream = policy_evict_last();
       uint32_t r = 0, rph = 1, qi = 0, qiph = 1, fph = 1;
       for (;;) {
-        const ItemDesc d = bwd_decode(p, atomicAdd(&p.ctr[0], 1u));
+        const ItemDesc d = bwd_decode(p, ctl->units, ctl->total_items, atomicAdd(&p.ctr[0], 1u));
         mbar_wait(&ctl->item_empty[qi], qiph);
         ctl->items[qi] = d;
         mbar_arrive(&ctl->item_full[qi]);
@@ -238,7 +249,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                       d.tile * 128, d.slot, pol_fixed);
         }
         for (uint32_t j = 0; j < d.nt; ++j) {
-          const uint32_t u = bwd_entry(p, d.tile, j) & 0x7FFFFFFFu;
+          const uint32_t u = bwd_entry(p, d.tile, d.j0 + j) & 0x7FFFFFFFu;
           mbar_wait(&ctl->ring_empty[r], rph);
           uint64_t* full = &ctl->ring_full[r];
           uint8_t* st = ring + r * C::kStageAlloc;
@@ -379,25 +390,80 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc_fence_after();
         if (tracer) trace_ev<kTrace>(tracing, p, &ctl->trace_count, 53, half, it.t);
       }
-      // accumulator -> bf16 (x scale for dq / dk) -> 128B-swizzled staging -> TMA store (rows past
-      // n are clipped by the tensor map). Half h stages output columns [D/2 h, D/2 (h+1)).
       constexpr uint32_t kHalf = D / 2;
+      constexpr uint32_t kAccs = SIDE == kSideDKDV ? 2u : 1u;
+      constexpr uint32_t kBlk = 128 * kAccs * D;  // floats per split-chunk partial block
+      // Split tile (a long list cut into chunks by the plan): publish this chunk's fp32 partial
+      // accumulators; the last chunk to finish adds every chunk's partial IN CHUNK ORDER
+      // (deterministic, no atomics on gradients) and writes the gradients.
+      const float* sum_base = nullptr;
+      uint32_t sum_chunks = 0;
+      if (it.split != kNoSplit) {
+        const uint32_t srow = it.split >> 8, chunk = it.split & 0xFF;
+        const uint2 si = p.split_info[srow];  // {chunks, first workspace chunk}
+        float* wsb = p.ws + (static_cast<uint64_t>(it.slot) * ctl->split_chunks + si.y + chunk) * kBlk;
 #pragma unroll
-      for (uint32_t a = 0; a < (SIDE == kSideDKDV ? 2u : 1u); ++a) {
+        for (uint32_t a = 0; a < kAccs; ++a)
+#pragma unroll
+          for (uint32_t c32 = 0; c32 < kHalf / 32; ++c32) {
+            uint32_t v[32];
+            tmem_ld32(tmem + lane_off + acc0 + a * D + half * kHalf + c32 * 32, v);
+            tmem_ld_wait();
+            uint4* dst = reinterpret_cast<uint4*>(wsb + row * (kAccs * D) + a * D + half * kHalf + c32 * 32);
+#pragma unroll
+            for (uint32_t q = 0; q < 8; ++q) dst[q] = make_uint4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+          }
+        tc_fence_before();
+        mbar_arrive(&ctl->acc_empty[ab]);
+        __threadfence();
+        named_bar_sync(1, 256);
+        uint32_t* ctr = p.split_ctr + static_cast<uint64_t>(it.slot) * ctl->split_rows + srow;
+        if (leader) ctl->bcast = atomicAdd(ctr, 1u);
+        named_bar_sync(1, 256);
+        const bool last = ctl->bcast + 1 == si.x;
+        named_bar_sync(1, 256);  // every thread has read the count
+        if (!last) return;
+        __threadfence();
+        if (leader) *ctr = 0;  // ready for the next launch
+        sum_base = p.ws + (static_cast<uint64_t>(it.slot) * ctl->split_chunks + si.y) * kBlk;
+        sum_chunks = si.x;
+      }
+      // accumulator (TMEM, or the chunks' sum) -> bf16 (x scale for dq / dk) -> 128B-swizzled
+      // staging -> TMA store (rows past n are clipped by the tensor map). Half h stages output
+      // columns [D/2 h, D/2 (h+1)).
+#pragma unroll
+      for (uint32_t a = 0; a < kAccs; ++a) {
         const float mul = a == 0 ? p.scale : 1.0f;
         if (leader) bulk_wait_group_read<0>();  // the previous store has read the staging tile
         named_bar_sync(1, 256);
 #pragma unroll
         for (uint32_t c32 = 0; c32 < kHalf / 32; ++c32) {
           uint32_t v[32];
-          if (has_acc) {
-            tmem_ld32(tmem + lane_off + acc0 + a * D + half * kHalf + c32 * 32, v);
+          const uint32_t col = half * kHalf + c32 * 32;  // output column of v[0]
+          if (sum_base) {
+            float acc[32];
+#pragma unroll
+            for (uint32_t i2 = 0; i2 < 32; ++i2) acc[i2] = 0.0f;
+            for (uint32_t c = 0; c < sum_chunks; ++c) {
+              const float4* src = reinterpret_cast<const float4*>(sum_base + c * kBlk + row * (kAccs * D) + a * D + col);
+#pragma unroll
+              for (uint32_t q = 0; q < 8; ++q) {
+                const float4 f = __ldcg(src + q);
+                acc[4 * q] += f.x;
+                acc[4 * q + 1] += f.y;
+                acc[4 * q + 2] += f.z;
+                acc[4 * q + 3] += f.w;
+              }
+            }
+#pragma unroll
+            for (uint32_t i2 = 0; i2 < 32; ++i2) v[i2] = __float_as_uint(acc[i2]);
+          } else if (has_acc) {
+            tmem_ld32(tmem + lane_off + acc0 + a * D + col, v);
             tmem_ld_wait();
           } else {
 #pragma unroll
-            for (uint32_t i = 0; i < 32; ++i) v[i] = 0u;
+            for (uint32_t i2 = 0; i2 < 32; ++i2) v[i2] = 0u;
           }
-          const uint32_t col = half * kHalf + c32 * 32;  // output column of v[0]
           uint8_t* rowp = ostage + (col / 64) * kBoxBytes + row * 128;
 #pragma unroll
           for (uint32_t c = 0; c < 4; ++c) {
@@ -418,7 +484,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           bulk_commit_group();
         }
       }
-      if (has_acc) {
+      if (has_acc && !sum_base) {
         tc_fence_before();
         mbar_arrive(&ctl->acc_empty[ab]);
       }
@@ -451,7 +517,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint64_t sl2x2 = f2_pack(sl2, sl2);
         const uint32_t ab = C::kDefer ? (items++ & 1u) : 0u;  // same sequence as the MMA issuer
         for (uint32_t j = 0; j < it.nt; ++j) {
-          const uint32_t e = bwd_entry(p, it.tile, j);
+          const uint32_t e = bwd_entry(p, it.tile, it.j0 + j);
           const uint32_t u = e & 0x7FFFFFFFu;
           bool masked;
           uint2 bits = make_uint2(0xFFFFFFFFu, 0xFFFFFFFFu);
@@ -468,7 +534,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             masked = (e & 0x80000000u) == 0;
             if (masked)
               bits = __ldg(reinterpret_cast<const uint2*>(
-                                p.bitmaps + (static_cast<uint64_t>(it.tile) * p.list_stride + j) * 128 + row) +
+                                p.bitmaps + (static_cast<uint64_t>(it.tile) * p.list_stride + it.j0 + j) * 128 + row) +
                             half);
           }
           if (tracer) trace_ev<kTrace>(tracing, p, &ctl->trace_count, 50, half, j);
@@ -650,29 +716,31 @@ void launch_side(const Prep& prep, StreamCtx& ctx, const BwdArgs& a, const float
   p.lse2 = lse2;
   p.delta = delta;
   p.rows_pad = rows_pad;
+  // work units from the device-built plan over the row view (dq) or the column view (dkdv):
+  // whole tiles, or balanced chunks of long lists (global tokens) combined deterministically
+  const TileView view = SIDE == kSideDQ ? row_view(km) : TileView{bm.col_cnt, bm.col_list, km.kcols, km.krows, 1};
+  const uint32_t workers = static_cast<uint32_t>(num_sms);
+  const DevPlan& plan = plan_for(prep, ctx, view, p.all_tiles ? kPlanDense : kPlanList, a.slots, workers, s);
+  const bool can_split = plan.cap_units > view.tiles;
+  p.hdr = plan.hdr;
+  p.unit_desc = plan.unit_desc;
+  p.split_info = plan.split_info;
+  p.ws = can_split ? ctx_workspace(ctx, plan_cap_chunks(a.slots, workers) * 128 * 256, s) : nullptr;
+  p.split_ctr = can_split ? ctx_split_ctr(ctx, plan_cap_chunks(a.slots, workers) + a.slots, s) : nullptr;
   if (SIDE == kSideDQ) {
-    p.tiles = km.krows;
-    p.partners = km.kcols;
-    p.cnt = km.row_cnt;
     p.list = km.list;
     p.list_stride = km.kcols;
-    p.order = p.all_tiles ? bm.all_order : bm.row_order;
     p.bitmaps = km.bitmaps;
     p.ctr = ctx.ctr + 2;
     p.out0 = static_cast<__nv_bfloat16*>(a.dq);
   } else {
-    p.tiles = km.kcols;
-    p.partners = km.krows;
-    p.cnt = bm.col_cnt;
     p.list = bm.col_list;
     p.list_stride = km.krows;
-    p.order = p.all_tiles ? bm.all_order : bm.col_order;
     p.bitmaps = bm.tbitmaps;
     p.ctr = ctx.ctr + 4;
     p.out0 = static_cast<__nv_bfloat16*>(a.dk);
     p.out1 = static_cast<__nv_bfloat16*>(a.dv);
   }
-  p.total_items = static_cast<uint32_t>(a.slots * p.tiles);
   const CUtensorMap tq = cached_tmap_bf16_3d(a.q, D, a.n, a.slots, 64, 128);
   const CUtensorMap tk = cached_tmap_bf16_3d(a.k, D, a.n, a.slots, 64, 128);
   const CUtensorMap tv = cached_tmap_bf16_3d(a.v, D, a.n, a.slots, 64, 128);
@@ -686,7 +754,8 @@ void launch_side(const Prep& prep, StreamCtx& ctx, const BwdArgs& a, const float
     BBM_CUDA(cudaFuncSetAttribute(attn_bwd_kernel<D, SIDE, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   bwd_smem_bytes<D, SIDE>()));
   });
-  const uint32_t grid = std::min<uint32_t>(p.total_items, static_cast<uint32_t>(num_sms));
+  const uint32_t grid = static_cast<uint32_t>(
+      std::max<uint64_t>(1, std::min<uint64_t>(a.slots * plan.cap_units, static_cast<uint64_t>(num_sms))));
   // event trace (bbm_set_trace) of one side only, chosen by BBM_TRACE_BWD_SIDE (0 dq, 1 dkdv):
   // both kernels would otherwise write the same buffer
   const char* tside = std::getenv("BBM_TRACE_BWD_SIDE");
@@ -714,18 +783,12 @@ T* bwd_alloc(uint64_t count) {
   return static_cast<T*>(ptr);
 }
 
-__global__ void iota_kernel(uint32_t* __restrict__ out, uint32_t count) {
-  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < count; i += gridDim.x * blockDim.x) out[i] = i;
-}
 
 }  // namespace
 
 void free_bwd_meta(BwdMeta& b) {
   cudaFree(b.col_cnt);
   cudaFree(b.col_list);
-  cudaFree(b.col_order);
-  cudaFree(b.row_order);
-  cudaFree(b.all_order);
   cudaFree(b.tbitmaps);
   cudaFree(b.scratch);
   if (b.ready) cudaEventDestroy(b.ready);
@@ -742,23 +805,15 @@ void ensure_bwd_meta(const Prep& prep, cudaStream_t s) {
     if (!b.col_cnt) {
       b.col_cnt = bwd_alloc<uint32_t>(kc);
       b.col_list = bwd_alloc<uint32_t>(static_cast<uint64_t>(kc) * kr);
-      b.col_order = bwd_alloc<uint32_t>(kc);
-      b.row_order = bwd_alloc<uint32_t>(kr);
-      b.all_order = bwd_alloc<uint32_t>(std::max(kr, kc));
       b.tbitmaps = bwd_alloc<uint4>(static_cast<uint64_t>(kc) * kr * 128);
       b.scratch = bwd_alloc<uint32_t>(static_cast<uint64_t>(kr) + kc + 2);
       BBM_CUDA(cudaEventCreateWithFlags(&b.ready, cudaEventDisableTiming));
-      iota_kernel<<<(std::max(kr, kc) + 255) / 256, 256, 0, s>>>(b.all_order, std::max(kr, kc));
-      BBM_CUDA(cudaGetLastError());
     }
     collist_kernel<<<kc, 256, 0, s>>>(km.sums, prep.n, kr, kc, b.col_list, b.col_cnt);
     BBM_CUDA(cudaGetLastError());
     transpose_bitmaps_kernel<<<dim3(kr, kc), 128, 0, s>>>(reinterpret_cast<const uint4*>(km.mask), kr, kc,
                                                            b.col_list, b.col_cnt, b.tbitmaps);
     BBM_CUDA(cudaGetLastError());
-    // LPT order of the columns (longest list first, ties by index), like the forward's row order
-    launch_lpt_order(b.col_cnt, kc, kr, b.scratch, b.col_order, s);
-    launch_lpt_order(km.row_cnt, kr, kc, b.scratch, b.row_order, s);
     BBM_CUDA(cudaEventRecord(b.ready, s));
     b.version = prep.version;
   } else {

@@ -974,7 +974,7 @@ void launch_impl(const Prep& prep, const AttnArgs& a, cudaStream_t s, int num_sm
   std::lock_guard<std::recursive_mutex> lk(prep.mu);
   StreamCtx& ctx = prep.ctx_for(s);  // ordered after the latest mask version
   const uint32_t workers = static_cast<uint32_t>(num_sms);
-  const DevPlan& plan = plan_for(prep, ctx, kCls, a.slots, workers, s);
+  const DevPlan& plan = plan_for(prep, ctx, row_view(km), kCls, a.slots, workers, s);
   // one CTA per SM; when work items are scarce, at most one CTA per item (upper bound: the
   // plan's unit capacity; CTAs without an item exit after claiming the end marker)
   const uint32_t grid = static_cast<uint32_t>(

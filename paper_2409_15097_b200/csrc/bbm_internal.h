@@ -112,7 +112,7 @@ struct DevPlan {
 };
 
 // Backward metadata (attn_bwd.cu): the column view of the kernel tiles — for key tile q, the
-// ascending occupied query row tiles (bit 31 = full tile), LPT order of the columns, and every
+// ascending occupied query row tiles (bit 31 = full tile), and every
 // occupied tile's mask bits TRANSPOSED (key-major) at its column-list position: key row c of
 // column entry (q, k) at (q*krows + k)*128 + c (16 bytes over queries). Built on the device, on
 // first backward use after each mask version (stream-ordered; no host sync).
@@ -121,9 +121,6 @@ struct BwdMeta {
   cudaEvent_t ready = nullptr;   // recorded after the latest column-view build
   uint32_t* col_cnt = nullptr;   // [kcols]
   uint32_t* col_list = nullptr;  // [kcols][krows]
-  uint32_t* col_order = nullptr; // [kcols]
-  uint32_t* row_order = nullptr; // [krows] LPT order of the row tiles (dq items)
-  uint32_t* all_order = nullptr; // [max(krows,kcols)] identity order (dense mode)
   uint4* tbitmaps = nullptr;     // [kcols*krows][128]
   uint32_t* scratch = nullptr;   // [kcols + krows + 2] ordering scratch
 };
@@ -258,10 +255,19 @@ constexpr uint32_t kNoSplit = 0xFFFFFFFFu;
 // upper bound on row units per slot of a plan and on workspace chunk blocks of one launch
 uint32_t plan_cap_units(uint32_t krows, uint32_t kcols, uint64_t slots, uint32_t workers);
 uint64_t plan_cap_chunks(uint64_t slots, uint32_t workers);
+// The tile lists a plan cuts into units: the forward / dq walk the row view (row_cnt, list),
+// dkdv the column view (col_cnt, col_list).
+struct TileView {
+  const uint32_t* cnt;
+  const uint32_t* list;  // [tiles][partners]
+  uint32_t tiles, partners;
+  int id;  // plan-cache key: 0 rows, 1 columns
+};
+inline TileView row_view(const KernelMeta& km) { return {km.row_cnt, km.list, km.krows, km.kcols, 0}; }
 // (re)build `plan` on stream s for the current metadata (kernel, no host sync)
-void build_plan(const KernelMeta& km, int cls, uint64_t slots, uint32_t workers, DevPlan& plan,
+void build_plan(const TileView& v, int cls, uint64_t slots, uint32_t workers, DevPlan& plan,
                 cudaStream_t s);
-const DevPlan& plan_for(const Prep& prep, StreamCtx& ctx, int cls, uint64_t slots,
+const DevPlan& plan_for(const Prep& prep, StreamCtx& ctx, const TileView& v, int cls, uint64_t slots,
                         uint32_t workers, cudaStream_t s);
 // LPT order of `count` keys (descending key, ties by index) into out[count], one CTA on s
 void launch_lpt_order(const uint32_t* keys, uint32_t count, uint32_t max_key, uint32_t* scratch,

@@ -144,14 +144,14 @@ uint32_t plan_cap_units(uint32_t krows, uint32_t kcols, uint64_t slots, uint32_t
   return static_cast<uint32_t>(std::min<uint64_t>(krows + extra, static_cast<uint64_t>(krows) * 256));
 }
 
-void build_plan(const KernelMeta& km, int cls, uint64_t slots, uint32_t workers, DevPlan& plan,
+void build_plan(const TileView& v, int cls, uint64_t slots, uint32_t workers, DevPlan& plan,
                 cudaStream_t s) {
   PlanArgs a{};
   a.cls = cls;
-  a.krows = km.krows;
-  a.kcols = km.kcols;
-  a.row_cnt = km.row_cnt;
-  a.list = km.list;
+  a.krows = v.tiles;
+  a.kcols = v.partners;
+  a.row_cnt = v.cnt;
+  a.list = v.list;
   a.slots = slots;
   a.workers = workers;
   a.cap_chunks = plan_cap_chunks(slots, workers);
@@ -172,19 +172,18 @@ void launch_lpt_order(const uint32_t* keys, uint32_t count, uint32_t max_key, ui
   BBM_CUDA(cudaGetLastError());
 }
 
-const DevPlan& plan_for(const Prep& prep, StreamCtx& ctx, int cls, uint64_t slots, uint32_t workers,
-                        cudaStream_t s) {
-  const KernelMeta& km = prep.kmeta;
-  DevPlan& pl = ctx.plans[std::make_tuple(cls, slots, workers)];
+const DevPlan& plan_for(const Prep& prep, StreamCtx& ctx, const TileView& v, int cls, uint64_t slots,
+                        uint32_t workers, cudaStream_t s) {
+  DevPlan& pl = ctx.plans[std::make_tuple(cls + 8 * v.id, slots, workers)];
   if (!pl.mem) {
-    pl.cap_units = plan_cap_units(km.krows, km.kcols, slots, workers);
+    pl.cap_units = plan_cap_units(v.tiles, v.partners, slots, workers);
     pl.cap_split = std::min<uint32_t>(pl.cap_units, static_cast<uint32_t>(
                                                         plan_cap_chunks(slots, workers) / std::max<uint64_t>(1, slots) + 1));
     const size_t off_desc = 256;
     const size_t off_tmp = off_desc + static_cast<size_t>(pl.cap_units) * 16;
     const size_t off_split = off_tmp + static_cast<size_t>(pl.cap_units) * 16;
     const size_t off_hist = off_split + static_cast<size_t>(pl.cap_split) * 8;
-    const size_t bytes = off_hist + (static_cast<size_t>(km.kcols) + 2) * 4;
+    const size_t bytes = off_hist + (static_cast<size_t>(v.partners) + 2) * 4;
     void* mem = nullptr;
     BBM_CUDA(cudaMalloc(&mem, bytes));
     pl.mem = static_cast<uint8_t*>(mem);
@@ -196,7 +195,7 @@ const DevPlan& plan_for(const Prep& prep, StreamCtx& ctx, int cls, uint64_t slot
     pl.version = 0;
   }
   if (pl.version != prep.version) {
-    build_plan(km, cls, slots, workers, pl, s);
+    build_plan(v, cls, slots, workers, pl, s);
     pl.version = prep.version;
   }
   return pl;

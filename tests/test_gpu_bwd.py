@@ -171,3 +171,24 @@ def test_prep_update_refreshes_backward_view(cuda):
                                                     C.c_void_p(torch.cuda.current_stream().cuda_stream)))
     f, b = fwd_bwd(m2, q, k, v, g, 0.125, bbm.Variant.binblk, cuda, prep)
     check(m2, q, k, v, g, 0.125, bbm.Variant.binblk, f, b)
+
+
+@pytest.mark.parametrize("spec,n,d", [("global(w=64;g=100)", 4096, 64), ("global(w=100;g=130)", 3000, 128),
+                                      ("all-ones", 2560, 128)])
+def test_split_long_lists_match_oracle_and_stay_deterministic(cuda, spec, n, d):
+    """One slot + long row / column lists (global tokens, all-ones): the device plan cuts them into
+    chunks whose fp32 partial gradients the last chunk adds in chunk order; the result matches
+    the oracle, is bitwise deterministic and identical across the masked variants."""
+    mask = bbm.generate(spec, n)
+    q, k, v, g = problem(13, 1, n, d)
+    scale = d ** -0.5
+    prep = bbm.preprocess_mask(mask, bbm.BlockSpec(128, 128))
+    f, b = fwd_bwd(mask, q, k, v, g, scale, bbm.Variant.binblk, cuda, prep=prep)
+    check(mask, q, k, v, g, scale, bbm.Variant.binblk, f, b)
+    ref = [t.float().cpu().numpy() for t in (b.dq, b.dk, b.dv)]
+    for var in MASKED:
+        f2, b2 = fwd_bwd(mask, q, k, v, g, scale, var, cuda, prep=prep)
+        for got, want in zip((b2.dq, b2.dk, b2.dv), ref):
+            assert np.array_equal(got.float().cpu().numpy(), want), var
+    fd, bd = fwd_bwd(mask, q, k, v, g, scale, bbm.Variant.dense, cuda, prep=prep)
+    check(mask, q, k, v, g, scale, bbm.Variant.dense, fd, bd)
