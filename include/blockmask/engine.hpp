@@ -5,7 +5,8 @@
 //                                              MaskPrep keeps the device metadata alive)
 //   blocked_forward (engine.hpp:282-341)    -> bbm_attn_fwd_host_f32 (sm_100a tcgen05 kernel)
 //   blocked_backward (engine.hpp:346-471)   -> bbm_attn_bwd_host_f32
-//   run_attention (engine.hpp:489-505)      -> one bbm_attn_fwd_host_f32 launch over all slots
+//   run_attention (engine.hpp:489-505)      -> bbm_run_attention_host_f32 over all slots (each
+//                                              slot's Matrix<float> storage used in place)
 //
 // Numerics: Q/K/V are rounded to bf16 (RNE) on the device and the kernel accumulates in fp32, so
 // outputs agree with the reference to a bf16 tolerance (max-abs <= 2e-2; tests/), not bit for
@@ -184,26 +185,47 @@ void forward_slots(const std::vector<const SlotInputs<T>*>& in, double scale, co
                    Variant variant, std::vector<ForwardResult<T>>& out) {
     static_assert(std::is_floating_point_v<T>, "Matrix<T> of float or double");
     const std::size_t slots = in.size(), n = prep.n_tokens, d = in.front()->q.cols();
-    std::vector<float> q, k, v;
-    q.reserve(slots * n * d), k.reserve(slots * n * d), v.reserve(slots * n * d);
-    for (const SlotInputs<T>* s : in) append_f32(q, s->q), append_f32(k, s->k), append_f32(v, s->v);
     if (in.front()->v.cols() != d)
         throw std::invalid_argument("d_v != d_k is not supported by the sm_100a kernel");
-    std::vector<float> o(slots * n * d);
-    std::vector<double> rmax(slots * n), rsum(slots * n);
-    device::check(bbm_attn_fwd_host_f32(prep.device->get(), static_cast<int>(variant), q.data(),
-                                        k.data(), v.data(), o.data(), rmax.data(), rsum.data(),
-                                        slots, static_cast<std::uint32_t>(d), scale),
-                  "blocked_forward");
     const EngineCounters per_slot = counters_for(prep, variant, 1);
     out.resize(slots);
-    for (std::size_t s = 0; s < slots; ++s) {
-        ForwardResult<T>& r = out[s];
+    for (ForwardResult<T>& r : out) {
         r.out = Matrix<T>(n, d);
-        for (std::size_t i = 0; i < n * d; ++i) r.out.data()[i] = static_cast<T>(o[s * n * d + i]);
-        r.row_max.assign(rmax.begin() + s * n, rmax.begin() + (s + 1) * n);
-        r.row_sum.assign(rsum.begin() + s * n, rsum.begin() + (s + 1) * n);
+        r.row_max.assign(n, 0.0);
+        r.row_sum.assign(n, 0.0);
         r.counters = per_slot;
+    }
+    if constexpr (std::is_same_v<T, float>) {
+        // run_attention<float> (engine.hpp:489-505): every slot's own Matrix<float> storage goes
+        // to the device as is (bbm_run_attention_host_f32: chunked H2D / kernel / D2H pipeline),
+        // results land in the ForwardResults directly
+        std::vector<const float*> q(slots), k(slots), v(slots);
+        std::vector<float*> o(slots);
+        std::vector<double*> m(slots), l(slots);
+        for (std::size_t s = 0; s < slots; ++s) {
+            q[s] = in[s]->q.data(), k[s] = in[s]->k.data(), v[s] = in[s]->v.data();
+            o[s] = out[s].out.data(), m[s] = out[s].row_max.data(), l[s] = out[s].row_sum.data();
+        }
+        device::check(bbm_run_attention_host_f32(prep.device->get(), static_cast<int>(variant), q.data(),
+                                                 k.data(), v.data(), o.data(), m.data(), l.data(), slots,
+                                                 static_cast<std::uint32_t>(d), scale),
+                      "blocked_forward");
+    } else {  // Matrix<double>: narrowed to float for the upload (the kernel computes in bf16)
+        std::vector<float> q, k, v;
+        q.reserve(slots * n * d), k.reserve(slots * n * d), v.reserve(slots * n * d);
+        for (const SlotInputs<T>* s : in) append_f32(q, s->q), append_f32(k, s->k), append_f32(v, s->v);
+        std::vector<float> o(slots * n * d);
+        std::vector<double> rmax(slots * n), rsum(slots * n);
+        device::check(bbm_attn_fwd_host_f32(prep.device->get(), static_cast<int>(variant), q.data(),
+                                            k.data(), v.data(), o.data(), rmax.data(), rsum.data(),
+                                            slots, static_cast<std::uint32_t>(d), scale),
+                      "blocked_forward");
+        for (std::size_t s = 0; s < slots; ++s) {
+            ForwardResult<T>& r = out[s];
+            for (std::size_t i = 0; i < n * d; ++i) r.out.data()[i] = static_cast<T>(o[s * n * d + i]);
+            r.row_max.assign(rmax.begin() + s * n, rmax.begin() + (s + 1) * n);
+            r.row_sum.assign(rsum.begin() + s * n, rsum.begin() + (s + 1) * n);
+        }
     }
 }
 

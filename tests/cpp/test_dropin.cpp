@@ -310,6 +310,31 @@ int main() {
   });
 
   // ---------------------------------------------------------------- reorder
+  // ---------------------------------------------------------------- generators (MaskSpec)
+  run("Generators.SpecStringsRoundTrip (test_generators.cpp:180-198)", [] {
+    const char* cases[] = {"causal", "all-ones", "medusa[4;4;4;4]", "packed-seq[128;256;128]",
+                           "packed-bidir[32:16;64:8]", "windowed(w=256)", "windowed(w=16;causal=1)",
+                           "dilated(w=8;d=2)", "global(w=8;g=4)", "random(p=0.25;seed=7)",
+                           "random(p=0.5;seed=9;diag=0)", "file:/some/path.bbmk"};
+    for (const char* text : cases) EXPECT(MaskSpec::parse(text).to_string() == text);
+  });
+  run("Generators.SpecDispatchMatchesDirectCalls (test_generators.cpp:200-210)", [] {
+    EXPECT(generate(MaskSpec::parse("causal").with_n(12)) == gen_causal(12));
+    EXPECT(generate(MaskSpec::parse("medusa[3;3;3]")) == gen_medusa(std::vector<std::size_t>{3, 3, 3}));
+    EXPECT(generate(MaskSpec::parse("windowed(w=3;causal=1)").with_n(9)) == gen_longformer_windowed(9, 3, true));
+    EXPECT(generate(MaskSpec::parse("random(p=0.2;seed=11)").with_n(20)) == gen_random_sparse(20, 0.2, 11));
+    EXPECT(!MaskSpec::parse("medusa[2;2]").has_free_n());
+    EXPECT(MaskSpec::parse("dilated(w=2;d=2)").has_free_n());
+  });
+  run("Generators.SpecParseErrors (test_generators.cpp:212-220)", [] {
+    EXPECT_THROW_INVALID(MaskSpec::parse("triangular"));
+    EXPECT_THROW_INVALID(MaskSpec::parse("medusa[4;x]"));
+    EXPECT_THROW_INVALID(MaskSpec::parse("windowed(w=2"));
+    EXPECT_THROW_INVALID(MaskSpec::parse("windowed(q=2)"));
+    EXPECT_THROW_INVALID(MaskSpec::parse("packed-bidir[4]"));
+    EXPECT_THROW_INVALID(MaskSpec::parse("random(p=abc)"));
+    EXPECT_THROW_INVALID(generate(MaskSpec::parse("causal")));
+  });
   run("Reorder.EdgelessGraphReversesIdentity (test_reorder.cpp:174-186)", [] {
     Mask mask(5);
     for (std::size_t i = 0; i < 5; ++i) mask.set(i, i, true);
