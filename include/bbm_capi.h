@@ -220,6 +220,11 @@ bbm_status bbm_run_attention_multi(bbm_prep prep, int variant, int n_devices,
  *      d_buffer (device, ctas * 8192 u64). NULL disables. Format in attn_fwd.cu (trace_ev). ---- */
 bbm_status bbm_set_trace(void* d_buffer, uint32_t ctas);
 
+/* ---- forward engine builds (diagnostics, no reference counterpart): how many forward launches
+ *      of this process ran the plain softmax engine build and how many the build that skips
+ *      empty score halves (chosen per launch plan from its occupied/full tile counts). ---- */
+bbm_status bbm_fwd_build_counts(uint64_t* plain, uint64_t* skipping);
+
 /* ---- reorder.hpp ---- */
 /* rcm_order(build_graph(mask)) (reorder.hpp:28-133): forward[new] = old. Host. */
 bbm_status bbm_rcm_order(const uint64_t* words, uint64_t n, uint32_t* forward);

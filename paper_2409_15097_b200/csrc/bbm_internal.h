@@ -99,6 +99,7 @@ struct SpecMeta {
 // balanced chunks of long ones = split-KV) in longest-first order. Header + arrays in one buffer.
 struct PlanHdr {
   uint32_t units, split_rows, split_chunks, unit_len;
+  uint32_t occupied, full;  // list plans: occupied tiles of the view and how many are full (bit 31)
 };
 struct DevPlan {
   uint64_t version = 0;  // mask version the plan was built from
@@ -109,6 +110,12 @@ struct DevPlan {
   uint2* split_info = nullptr;  // [cap_split] {chunks, first workspace chunk}
   uint4* tmp = nullptr;         // [cap_units] units in row order (before the LPT sort)
   uint32_t* hist = nullptr;     // [kcols + 2] sort scratch
+  // {occupied, full} of the header, read back without blocking (pinned copy + event): the
+  // forward picks its engine build from it once it has arrived (results do not depend on it)
+  uint32_t* host_hdr = nullptr;
+  cudaEvent_t hdr_ev = nullptr;
+  uint64_t known_version = 0;
+  bool partial_heavy = false;
 };
 
 // Backward metadata (attn_bwd.cu): the column view of the kernel tiles — for key tile q, the
@@ -246,6 +253,8 @@ struct TraceConfig {
   uint32_t ctas = 0;
 };
 extern TraceConfig g_trace;
+// forward launches so far per softmax engine build (plain, empty-half skipping)
+void fwd_build_counts(uint64_t& plain, uint64_t& skipping);
 
 void launch_attn_fwd(const Prep& prep, const AttnArgs& a, cudaStream_t s, int num_sms);
 

@@ -182,7 +182,11 @@ Prep::~Prep() {
     cudaFree(c.split_ctr);
     cudaFree(c.rowws);
     if (c.done) cudaEventDestroy(c.done);
-    for (auto& pl : c.plans) cudaFree(pl.second.mem);
+    for (auto& pl : c.plans) {
+      cudaFree(pl.second.mem);
+      if (pl.second.host_hdr) cudaFreeHost(pl.second.host_hdr);
+      if (pl.second.hdr_ev) cudaEventDestroy(pl.second.hdr_ev);
+    }
   }
   if (ready) cudaEventDestroy(ready);
   if (prev >= 0) cudaSetDevice(prev);
@@ -1038,6 +1042,13 @@ bbm_status bbm_set_trace(void* d_buffer, uint32_t ctas) {
   return guarded([&] {
     g_trace.buffer = d_buffer;
     g_trace.ctas = d_buffer ? ctas : 0;
+  });
+}
+
+bbm_status bbm_fwd_build_counts(uint64_t* plain, uint64_t* skipping) {
+  return guarded([&] {
+    require(plain && skipping, "null argument");
+    fwd_build_counts(*plain, *skipping);
   });
 }
 

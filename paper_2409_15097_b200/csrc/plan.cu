@@ -69,6 +69,12 @@ __global__ void __launch_bounds__(kPlanThreads) plan_kernel(const PlanArgs a) {
   const unsigned long long total = block_sum<kPlanThreads>(my) * a.slots;
   uint64_t L = (total / max(1u, a.workers) + 1) / 2;
   if (L < kMinUnit) L = kMinUnit;
+  // full tiles (list entries with bit 31): the forward's choice of softmax engine build
+  unsigned long long fl = 0;
+  if (a.cls == kPlanList)
+    for (uint32_t p = threadIdx.x; p < a.krows; p += kPlanThreads)
+      for (uint32_t o = 0; o < a.row_cnt[p]; ++o) fl += a.list[static_cast<uint64_t>(p) * a.kcols + o] >> 31;
+  const unsigned long long full = block_sum<kPlanThreads>(fl);
   for (;;) {
     unsigned long long c = 0;
     for (uint32_t p = threadIdx.x; p < a.krows; p += kPlanThreads) c += chunks_of(occ_of(p), L);
@@ -121,7 +127,10 @@ __global__ void __launch_bounds__(kPlanThreads) plan_kernel(const PlanArgs a) {
   const uint32_t units = u_carry;
   lpt_sort<kPlanThreads>([&](uint32_t i) { return a.tmp[i].z; }, units, a.kcols, a.hist,
            [&](uint32_t pos, uint32_t i) { a.desc[pos] = a.tmp[i]; });
-  if (threadIdx.x == 0) *a.hdr = PlanHdr{units, s_carry, c_carry, static_cast<uint32_t>(L < 0xFFFFFFFFull ? L : 0xFFFFFFFFull)};
+  if (threadIdx.x == 0)
+    *a.hdr = PlanHdr{units, s_carry, c_carry, static_cast<uint32_t>(L < 0xFFFFFFFFull ? L : 0xFFFFFFFFull),
+                     static_cast<uint32_t>(total / max(1ull, static_cast<unsigned long long>(a.slots))),
+                     static_cast<uint32_t>(full)};
 }
 
 __global__ void __launch_bounds__(kPlanThreads) lpt_order_kernel(const uint32_t* __restrict__ keys,
@@ -197,6 +206,22 @@ const DevPlan& plan_for(const Prep& prep, StreamCtx& ctx, const TileView& v, int
   if (pl.version != prep.version) {
     build_plan(v, cls, slots, workers, pl, s);
     pl.version = prep.version;
+    if (!pl.host_hdr) {
+      BBM_CUDA(cudaMallocHost(&pl.host_hdr, 8));
+      BBM_CUDA(cudaEventCreateWithFlags(&pl.hdr_ev, cudaEventDisableTiming));
+    }
+    BBM_CUDA(cudaMemcpyAsync(pl.host_hdr, &pl.hdr->occupied, 8, cudaMemcpyDeviceToHost, s));
+    BBM_CUDA(cudaEventRecord(pl.hdr_ev, s));
+  } else if (pl.known_version != pl.version) {
+    const cudaError_t q = cudaEventQuery(pl.hdr_ev);
+    if (q == cudaSuccess) {
+      pl.partial_heavy = (pl.host_hdr[0] - pl.host_hdr[1]) * 2ull > pl.host_hdr[0];
+      pl.known_version = pl.version;
+    } else if (q == cudaErrorNotReady) {
+      (void)cudaGetLastError();  // not an error: the header has not arrived yet
+    } else {
+      BBM_CUDA(q);
+    }
   }
   return pl;
 }

@@ -435,3 +435,48 @@ def test_in_kernel_rcm_gather_equals_explicit_permutation(cuda, n, d, slots, spe
         assert torch.equal(out.view(torch.int16), want_o.view(torch.int16)), var
         assert torch.equal(m.view(torch.int32), want_m.view(torch.int32)), var
         assert torch.equal(l.view(torch.int32), want_l.view(torch.int32)), var
+
+
+@pytest.mark.parametrize("d", [64, 128])
+@pytest.mark.parametrize("scale_sign", [1.0, -1.0])
+def test_empty_half_skip_build_is_bitwise_identical(cuda, d, scale_sign):
+    """Masks whose occupied tiles are mostly partial run the engine build that skips a warp's
+    empty 32 x 64 score halves (the plan header's occupied/full counts select it once they have
+    reached the host, one launch after a new prep). The first launch runs the plain build, later
+    ones the skipping build: outputs and statistics must be bitwise equal, and match the oracle."""
+    import torch
+
+    n = 2900
+    mask = bbm.gen_longformer_windowed(n, 40)  # a band: ~all occupied tiles partial
+    q, k, v = problem(5, 2, n, d)
+    scale = scale_sign / np.sqrt(d)
+    import ctypes as C
+
+    from paper_2409_15097_b200 import _lib
+
+    def builds():
+        a, b = C.c_uint64(), C.c_uint64()
+        _lib.check(_lib.lib.bbm_fwd_build_counts(C.byref(a), C.byref(b)))
+        return a.value, b.value
+
+    for var in (bbm.Variant.binblk, bbm.Variant.dense_binblk):
+        prep = bbm.preprocess_mask(mask, bbm.BlockSpec(128, 128))
+        c0 = builds()
+        first = run_gpu(mask, q, k, v, scale, var, cuda, prep=prep)
+        c1 = builds()
+        assert c1[0] == c0[0] + 1 and c1[1] == c0[1], "a fresh plan runs the plain build"
+        torch.cuda.synchronize()
+        for _ in range(2):
+            again = run_gpu(mask, q, k, v, scale, var, cuda, prep=prep)
+            for a, b in zip(first[:3], again[:3]):
+                assert np.array_equal(a, b), var
+        assert builds()[1] == c1[1] + 2, "the band mask runs the skipping build once known"
+        check_against_oracle(mask, q, k, v, scale, *again[:3], var, slots_to_check=[1])
+    # a mask of mostly full tiles keeps the plain build
+    causal = bbm.gen_causal(n)
+    prep = bbm.preprocess_mask(causal, bbm.BlockSpec(128, 128))
+    run_gpu(causal, q, k, v, scale, bbm.Variant.binblk, cuda, prep=prep)
+    torch.cuda.synchronize()
+    c2 = builds()
+    run_gpu(causal, q, k, v, scale, bbm.Variant.binblk, cuda, prep=prep)
+    assert builds() == (c2[0] + 1, c2[1])
