@@ -253,6 +253,11 @@ struct TraceConfig {
   uint32_t ctas = 0;
 };
 extern TraceConfig g_trace;
+// the fused preprocessor splits a tile row's 128 rows over this many CTAs (KernelMeta.partial)
+#ifndef BBM_PREP_SPLITS
+#define BBM_PREP_SPLITS 8
+#endif
+constexpr uint32_t kPrepRowSplits = BBM_PREP_SPLITS;
 // forward launches so far per softmax engine build (plain, empty-half skipping)
 void fwd_build_counts(uint64_t& plain, uint64_t& skipping);
 

@@ -162,7 +162,7 @@ void carve_kernel_meta(KernelMeta& km, uint64_t n, uint8_t* arena) {
   take(km.row_stats, static_cast<uint64_t>(km.krows) * 3);
   take(km.totals, 3);
   take(km.scratch, static_cast<uint64_t>(km.krows) + km.kcols + 2);
-  take(km.partial, tiles * 8);
+  take(km.partial, tiles * kPrepRowSplits);
   take(km.ctr, static_cast<uint64_t>(km.krows) + 1);
   km.arena_bytes = off;
 }

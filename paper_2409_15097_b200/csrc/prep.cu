@@ -182,9 +182,12 @@ __device__ __forceinline__ uint32_t area_of(uint64_t n, uint64_t bi, uint64_t bj
 // right edge) is never flagged full, so the attention kernel always applies its bitmap, whose
 // bits beyond n are 0. Sums are read through L2 (__ldcg): the fused preprocessor calls this on
 // sums written earlier in the same launch.
-__device__ void rowmeta_row(const uint32_t* sums, uint64_t n, uint64_t bi, uint64_t bj, uint64_t cols,
-                            uint64_t p, uint8_t* occ, uint32_t* offset, uint32_t* total,
-                            uint64_t* row_stats, uint32_t* list, uint32_t* cnt) {
+// sum_at(q): the tile sum of (p, q); s_list (optional, shared memory): a copy of the row's list;
+// returns the row's list length.
+template <class SumAt>
+__device__ uint32_t rowmeta_row_t(SumAt sum_at, uint64_t n, uint64_t bi, uint64_t bj, uint64_t cols,
+                                  uint64_t p, uint8_t* occ, uint32_t* offset, uint32_t* total,
+                                  uint64_t* row_stats, uint32_t* list, uint32_t* cnt, uint32_t* s_list) {
   __shared__ uint32_t warp_cnt[8];
   __shared__ uint32_t s_run_start, s_run_end;
   __shared__ unsigned long long s_nz, s_full, s_ones;
@@ -202,7 +205,7 @@ __device__ void rowmeta_row(const uint32_t* sums, uint64_t n, uint64_t bi, uint6
     uint32_t s = 0, a = 0;
     bool in = q < cols;
     if (in) {
-      s = __ldcg(sums + p * cols + q);
+      s = sum_at(q);
       a = area_of(n, bi, bj, p, q);
       occ[p * cols + q] = s > 0 ? 1 : 0;
       my_nz += s > 0;
@@ -218,7 +221,11 @@ __device__ void rowmeta_row(const uint32_t* sums, uint64_t n, uint64_t bi, uint6
     for (uint32_t w = 0; w < warp; ++w) before += warp_cnt[w];
     before += __popc(ballot & ((1u << lane) - 1u));
     const bool flag_full = s == a && (q + 1) * bj <= n;
-    if (list && o) list[p * cols + before] = static_cast<uint32_t>(q) | (flag_full ? 0x80000000u : 0u);
+    if (list && o) {
+      const uint32_t e = static_cast<uint32_t>(q) | (flag_full ? 0x80000000u : 0u);
+      list[p * cols + before] = e;
+      if (s_list) s_list[before] = e;
+    }
     uint32_t chunk = 0;
     for (uint32_t w = 0; w < 8; ++w) chunk += warp_cnt[w];
     base += chunk;
@@ -228,8 +235,7 @@ __device__ void rowmeta_row(const uint32_t* sums, uint64_t n, uint64_t bi, uint6
   const uint32_t start = s_run_start;
   if (start != 0xFFFFFFFFu) {
     for (uint64_t q = start + 1 + threadIdx.x; q < cols; q += 256) {
-      if (__ldcg(sums + p * cols + q) != area_of(n, bi, bj, p, q))
-        atomicMin(&s_run_end, static_cast<uint32_t>(q));
+      if (sum_at(q) != area_of(n, bi, bj, p, q)) atomicMin(&s_run_end, static_cast<uint32_t>(q));
     }
   }
   atomicAdd(&s_nz, my_nz);
@@ -251,6 +257,14 @@ __device__ void rowmeta_row(const uint32_t* sums, uint64_t n, uint64_t bi, uint6
     if (cnt) cnt[p] = base;
   }
   __syncthreads();
+  return base;
+}
+
+__device__ void rowmeta_row(const uint32_t* sums, uint64_t n, uint64_t bi, uint64_t bj, uint64_t cols,
+                            uint64_t p, uint8_t* occ, uint32_t* offset, uint32_t* total,
+                            uint64_t* row_stats, uint32_t* list, uint32_t* cnt) {
+  rowmeta_row_t([&](uint64_t q) { return __ldcg(sums + p * cols + q); }, n, bi, bj, cols, p, occ, offset,
+                total, row_stats, list, cnt, nullptr);
 }
 
 // One CTA (256 threads) per row tile p; the row is walked in chunks of 256 tiles.
@@ -318,9 +332,10 @@ __global__ void __launch_bounds__(1024) finalize_kernel(const uint64_t* __restri
 // compaction of that row. Counters reset themselves, so the next launch needs no memset. The
 // row-statistics totals and the LPT row order are not on this path: the launches plan on the
 // device from row_cnt, and the totals are summed when the host asks for them.
-constexpr uint32_t kRowSplits = 8;                 // 128 rows / 16 per CTA
+constexpr uint32_t kRowSplits = kPrepRowSplits;    // 128 rows / 16 per CTA
 constexpr uint32_t kSlabRows = 128 / kRowSplits;
 constexpr uint32_t kChunkTiles = 32;               // column tiles per CTA
+constexpr uint32_t kStageCols = 512;               // stage B in shared memory up to N = 65536
 
 struct FusedArgs {
   const uint8_t* bools;  // dense bool rows (IN == kInBool)
@@ -343,10 +358,14 @@ template <int IN>
 __global__ void __launch_bounds__(256) prep_fused_kernel(const FusedArgs a) {
   __shared__ uint32_t s_cnt[kChunkTiles];
   __shared__ bool s_last;
+  __shared__ uint32_t s_sums[kStageCols], s_list[kStageCols];
   const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint32_t chunk = blockIdx.x % a.chunks;
-  const uint32_t p = (blockIdx.x / a.chunks) % a.krows;
-  const uint32_t rs = blockIdx.x / (a.chunks * a.krows);
+  // a tile row's chunks x kRowSplits CTAs are consecutive, so its stage B runs while later rows
+  // are still in stage A (only the last row's is a tail)
+  const uint32_t per_row = a.chunks * kRowSplits;
+  const uint32_t p = blockIdx.x / per_row;
+  const uint32_t chunk = (blockIdx.x % per_row) % a.chunks;
+  const uint32_t rs = (blockIdx.x % per_row) / a.chunks;
   const uint64_t wpr = static_cast<uint64_t>(a.kcols) * 2;
   const uint64_t row0 = static_cast<uint64_t>(p) * 128 + rs * kSlabRows;
 
@@ -422,11 +441,50 @@ __global__ void __launch_bounds__(256) prep_fused_kernel(const FusedArgs a) {
   __syncthreads();
   if (threadIdx.x == 0) {
     __threadfence();
-    s_last = atomicAdd(&a.ctr[p], 1u) == a.chunks * kRowSplits - 1;
+    s_last = atomicAdd(&a.ctr[p], 1u) == per_row - 1;
     __threadfence();
   }
   __syncthreads();
   if (!s_last) return;
+  // Stage B keeps the row's sums and list in shared memory (rows up to kStageCols tiles), so its
+  // only L2 round trips are the partial sums in and the mask words of the bitmaps.
+  if (a.kcols <= kStageCols) {
+    for (uint32_t q = threadIdx.x; q < a.kcols; q += 256) {
+      uint32_t v[kRowSplits];
+#pragma unroll
+      for (uint32_t r = 0; r < kRowSplits; ++r)
+        v[r] = __ldcg(a.partial + (static_cast<uint64_t>(r) * a.krows + p) * a.kcols + q);
+      uint32_t sum = 0;
+#pragma unroll
+      for (uint32_t r = 0; r < kRowSplits; ++r) sum += v[r];
+      s_sums[q] = sum;
+      a.sums[static_cast<uint64_t>(p) * a.kcols + q] = sum;
+    }
+    __syncthreads();
+    const uint32_t cnt = rowmeta_row_t([&](uint64_t q) { return s_sums[q]; }, a.n, 128, 128, a.kcols, p, a.occ,
+                                       a.run_off, a.run_len, a.row_stats, a.list, a.row_cnt, s_list);
+    const uint4* m4 = reinterpret_cast<const uint4*>(a.mask);
+    constexpr uint32_t kU = 4;  // independent mask loads in flight per thread
+    for (uint32_t i0 = threadIdx.x; i0 < cnt * 128; i0 += 256 * kU) {
+      uint4 w[kU];
+#pragma unroll
+      for (uint32_t u = 0; u < kU; ++u) {
+        const uint32_t idx = i0 + u * 256;
+        if (idx < cnt * 128) {
+          const uint32_t q = s_list[idx >> 7] & 0x7FFFFFFFu;
+          w[u] = __ldcg(m4 + (static_cast<uint64_t>(p) * 128 + (idx & 127)) * a.kcols + q);
+        }
+      }
+#pragma unroll
+      for (uint32_t u = 0; u < kU; ++u) {
+        const uint32_t idx = i0 + u * 256;
+        if (idx < cnt * 128)
+          a.bitmaps[(static_cast<uint64_t>(p) * a.kcols + (idx >> 7)) * 128 + (idx & 127)] = w[u];
+      }
+    }
+    if (threadIdx.x == 0) a.ctr[p] = 0;
+    return;
+  }
   for (uint32_t q = threadIdx.x; q < a.kcols; q += 256) {
     uint32_t sum = 0;
 #pragma unroll
