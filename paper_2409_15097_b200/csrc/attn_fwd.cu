@@ -395,6 +395,20 @@ __global__ void __launch_bounds__(kThreadsOf<D>, 1)
         const uint32_t r = seq % C::kRing;
         mbar_wait(&ctl->ring_empty[r], ((seq / C::kRing) & 1) ^ 1);
         uint64_t* full = &ctl->ring_full[r];
+#if defined(BBM_ABLATE_NO_KVLOAD) || defined(BBM_ABLATE_HALF_KVLOAD)
+        // timing experiments only (wrong results): the ring keeps stale tiles after its first
+        // fill (NO_KVLOAD) or every second K/V pair reuses them (HALF_KVLOAD)
+#ifdef BBM_ABLATE_NO_KVLOAD
+        const bool skip_load = seq >= C::kRing;
+#else
+        const bool skip_load = seq >= C::kRing && ((seq / 2) & 1);
+#endif
+        if (skip_load) {
+          __syncwarp();
+          if (lane == 0) mbar_arrive(full);
+          return;
+        }
+#endif
         if (lane == 0) mbar_arrive_expect_tx(full, C::kTileBytes);
         __syncwarp();
         issue_tile(ring + r * C::kTileBytes, tm, full, q, slot, pol_kv);

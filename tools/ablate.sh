@@ -21,6 +21,9 @@ for v in $VARIANTS; do
     DEG2_8) FL="-DBBM_POLY_DEG2 -DBBM_POLY_PAIRS=0x0F0Fu" ;;
     DEG2_4) FL="-DBBM_POLY_DEG2 -DBBM_POLY_PAIRS=0x0303u" ;;
     NO_PV) FL="-DBBM_ABLATE_NO_PV" ;;
+    NO_KVLOAD) FL="-DBBM_ABLATE_NO_KVLOAD" ;;
+    HALF_KVLOAD) FL="-DBBM_ABLATE_HALF_KVLOAD" ;;
+    FAST_NOKV) FL="-DBBM_ABLATE_FAST_ENGINE -DBBM_ABLATE_NO_KVLOAD" ;;
     SUSPEND) FL="-DBBM_SUSPEND_WAIT" ;;
     LACC1) FL="-DBBM_LACC=1" ;;
     LACC2) FL="-DBBM_LACC=2" ;;
