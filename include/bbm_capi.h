@@ -145,14 +145,20 @@ bbm_status bbm_attn_fwd(bbm_prep prep, int variant, const void* q, const void* k
                         void* out, float* row_max, float* row_sum, uint64_t slots,
                         uint32_t head_dim, double scale, void* stream);
 
-/* The same forward with the RCM permutation applied INSIDE the kernel (reorder.hpp:156-189
- * fused into the loads): `prep` was built from permute_mask(mask, perm), d_forward = perm.forward
- * (new -> old, device u32 [n]), and q/k/v/out/row stats stay in the ORIGINAL token order. The
- * kernel gathers each tile's Q/K/V rows with TMA tile::gather4 and scatters O rows with
- * tile::scatter4: no separate permute_rows / unpermute_rows passes. Requires slots * n < 2^31. */
+/* The same forward with the RCM permutation applied on the device (reorder.hpp:156-189):
+ * `prep` was built from permute_mask(mask, perm), d_forward = perm.forward (new -> old, device
+ * u32 [n]), and q/k/v/out/row stats stay in the ORIGINAL token order. Two implementations, equal
+ * results: mode 1 permutes Q/K/V into per-stream scratch (4 x slots*n*d bf16 + 2 x slots*n fp32),
+ * runs the plain kernel and scatters O / row stats back (HBM-bound passes); mode 2 gathers each
+ * tile's rows inside the kernel with TMA tile::gather4 and scatters O with tile::scatter4 (no
+ * scratch; bound by the TMA instruction rate; requires slots * n < 2^31). bbm_attn_fwd_gather =
+ * mode 0 = the faster one on B200 (mode 1; env BBM_GATHER=tma selects mode 2). */
 bbm_status bbm_attn_fwd_gather(bbm_prep prep, int variant, const uint32_t* d_forward, const void* q,
                                const void* k, const void* v, void* out, float* row_max, float* row_sum,
                                uint64_t slots, uint32_t head_dim, double scale, void* stream);
+bbm_status bbm_attn_fwd_gather_ex(bbm_prep prep, int variant, const uint32_t* d_forward, const void* q,
+                                  const void* k, const void* v, void* out, float* row_max, float* row_sum,
+                                  uint64_t slots, uint32_t head_dim, double scale, void* stream, int mode);
 
 /* Same, host buffers (bf16 bits as uint16): copies in, runs, copies out, synchronizes.
  * Pinned buffers get full PCIe bandwidth. Validates finiteness (engine.hpp:237-258). */

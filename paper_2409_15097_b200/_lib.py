@@ -82,6 +82,8 @@ SIGNATURES = {
     "bbm_graph_csr": (C.c_int, [u64p, C.c_uint64, u64p, u32p]),
     "bbm_attn_fwd": (C.c_int, [vp, C.c_int, vp, vp, vp, vp, vp, vp, C.c_uint64, C.c_uint32, C.c_double, vp]),
     "bbm_attn_fwd_gather": (C.c_int, [vp, C.c_int, vp, vp, vp, vp, vp, vp, vp, C.c_uint64, C.c_uint32, C.c_double, vp]),
+    "bbm_attn_fwd_gather_ex": (C.c_int, [vp, C.c_int, vp, vp, vp, vp, vp, vp, vp, C.c_uint64, C.c_uint32, C.c_double, vp,
+                                         C.c_int]),
     "bbm_attn_fwd_host_bf16": (C.c_int, [vp, C.c_int, u16p, u16p, u16p, u16p, f32p, f32p, C.c_uint64, C.c_uint32, C.c_double]),
     "bbm_attn_fwd_rcm_host_bf16": (C.c_int, [vp, C.c_int, u32p, u16p, u16p, u16p, u16p, f32p, f32p, C.c_uint64, C.c_uint32, C.c_double]),
     "bbm_attn_fwd_host_f32": (C.c_int, [vp, C.c_int, f32p, f32p, f32p, f32p, f64p, f64p, C.c_uint64, C.c_uint32, C.c_double]),

@@ -477,13 +477,15 @@ def _validate_common(prep: MaskPrep, mask, scale: float, threads: int) -> None:
 
 
 def attn_fwd_device(prep: MaskPrep, variant: Variant, q, k, v, out, row_max=None, row_sum=None,
-                    scale: float = 1.0, stream=None, rows=None) -> None:
+                    scale: float = 1.0, stream=None, rows=None, gather_mode: int = 0) -> None:
     """Raw launch on device tensors (bf16 [slots][n][d], contiguous). No validation beyond
     shapes; this is the timed entry point. row_max / row_sum: float32 [slots][n] or None.
 
     ``rows``: optional CUDA int32/uint32 tensor [n], an RCM permutation's forward map (new -> old)
     for a prep built from ``permute_mask(mask, perm)``: the tensors then stay in the ORIGINAL
-    token order and the kernel gathers / scatters rows itself (bbm_attn_fwd_gather)."""
+    token order and the RCM permutation is applied on the device (bbm_attn_fwd_gather_ex):
+    ``gather_mode`` 0 = the faster implementation (1), 1 = permute / unpermute passes around the
+    plain kernel, 2 = in-kernel TMA tile::gather4 / scatter4."""
     import torch
 
     slots, n, d = (q.shape if q.dim() == 3 else (1, *q.shape))
@@ -497,12 +499,12 @@ def attn_fwd_device(prep: MaskPrep, variant: Variant, q, k, v, out, row_max=None
     if rows is not None:
         if rows.numel() != n or rows.element_size() != 4 or not rows.is_cuda or not rows.is_contiguous():
             raise ValueError("rows must be a contiguous CUDA 32-bit tensor of n entries")
-        check(lib.bbm_attn_fwd_gather(prep.handle.h, int(variant), C.c_void_p(rows.data_ptr()),
+        check(lib.bbm_attn_fwd_gather_ex(prep.handle.h, int(variant), C.c_void_p(rows.data_ptr()),
                                       C.c_void_p(q.data_ptr()), C.c_void_p(k.data_ptr()), C.c_void_p(v.data_ptr()),
                                       C.c_void_p(out.data_ptr()),
                                       C.c_void_p(row_max.data_ptr() if row_max is not None else 0),
                                       C.c_void_p(row_sum.data_ptr() if row_sum is not None else 0),
-                                      int(slots), int(d), float(scale), C.c_void_p(s)))
+                                      int(slots), int(d), float(scale), C.c_void_p(s), int(gather_mode)))
         return
     check(lib.bbm_attn_fwd(prep.handle.h, int(variant), C.c_void_p(q.data_ptr()), C.c_void_p(k.data_ptr()),
                            C.c_void_p(v.data_ptr()), C.c_void_p(out.data_ptr()),

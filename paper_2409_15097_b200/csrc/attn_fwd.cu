@@ -42,6 +42,8 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <cstdlib>
+#include <string>
 #include <vector>
 
 #include "bbm_internal.h"
@@ -1091,7 +1093,52 @@ void launch_d(const Prep& prep, const AttnArgs& a, cudaStream_t s, int num_sms) 
   }
 }
 
+// Which RCM application a gather launch uses: BBM_GATHER=tma|passes overrides (measurement), the
+// default is the faster one on B200 — the passes: tile::gather4 moves 4 rows (512 B) per TMA
+// instruction and the TMA unit issues one every ~60 cycles, so the in-kernel gather is bound by
+// the TMA instruction rate (C5: 6.4 ms vs 1.5 ms pre-permuted), while the passes are plain
+// HBM-bound copies (Q, K, V in, O and the row statistics out).
+int gather_mode_of(int requested) {
+  if (requested != kGatherAuto) return requested;
+  static const int env = [] {
+    const char* e = std::getenv("BBM_GATHER");
+    if (e && std::string(e) == "tma") return static_cast<int>(kGatherTma);
+    return static_cast<int>(kGatherPasses);
+  }();
+  return env;
+}
+
 }  // namespace
+
+void launch_attn_fwd(const Prep& prep, const AttnArgs& a, cudaStream_t s, int num_sms);
+
+// RCM application by passes around the plain kernel (permute_rows / unpermute_rows,
+// reorder.hpp:156-189): Q, K, V permuted into per-stream scratch, the forward over the permuted
+// mask, O and the row statistics scattered back to the original tokens. Same results as the
+// in-kernel gather (the kernel sees the same bf16 rows in the same positions).
+static void launch_gather_passes(const Prep& prep, const AttnArgs& a, cudaStream_t s, int num_sms) {
+  std::lock_guard<std::recursive_mutex> lk(prep.mu);  // the scratch belongs to this stream's context
+  const uint64_t rowb = static_cast<uint64_t>(a.d) * 2;
+  const uint64_t tb = (a.slots * a.n * rowb + 255) / 256 * 256;
+  const uint64_t sb = (a.slots * a.n * 4 + 255) / 256 * 256;
+  StreamCtx& ctx = prep.ctx_for(s);
+  uint8_t* base = ctx_perm_scratch(ctx, 4 * tb + 2 * sb, s);
+  AttnArgs b = a;
+  b.rows = nullptr;
+  b.q = base;
+  b.k = base + tb;
+  b.v = base + 2 * tb;
+  b.o = base + 3 * tb;
+  b.row_max = a.row_max ? reinterpret_cast<float*>(base + 4 * tb) : nullptr;
+  b.row_sum = a.row_sum ? reinterpret_cast<float*>(base + 4 * tb + sb) : nullptr;
+  launch_permute_rows(a.q, const_cast<void*>(b.q), a.rows, a.slots, a.n, rowb, false, s);
+  launch_permute_rows(a.k, const_cast<void*>(b.k), a.rows, a.slots, a.n, rowb, false, s);
+  launch_permute_rows(a.v, const_cast<void*>(b.v), a.rows, a.slots, a.n, rowb, false, s);
+  launch_attn_fwd(prep, b, s, num_sms);
+  launch_permute_rows(b.o, a.o, a.rows, a.slots, a.n, rowb, true, s);
+  if (a.row_max) launch_permute_rows(b.row_max, a.row_max, a.rows, a.slots, a.n, 4, true, s);
+  if (a.row_sum) launch_permute_rows(b.row_sum, a.row_sum, a.rows, a.slots, a.n, 4, true, s);
+}
 
 void launch_attn_fwd(const Prep& prep, const AttnArgs& a, cudaStream_t s, int num_sms) {
   require(a.slots >= 1, "need at least one batch/head slot");
@@ -1099,7 +1146,9 @@ void launch_attn_fwd(const Prep& prep, const AttnArgs& a, cudaStream_t s, int nu
   require(a.slots < (1ull << 24), "too many slots for one launch");
   if (a.slots * prep.kmeta.krows == 0) return;
   if (a.d != 64 && a.d != 128) throw ArgError("head dim must be 64 or 128 on the sm_100a kernel");
-  if (a.rows) {  // in-kernel RCM gather / scatter of token rows (2-D row coordinates are int32)
+  if (a.rows && gather_mode_of(a.gather_mode) == kGatherPasses) {
+    launch_gather_passes(prep, a, s, num_sms);
+  } else if (a.rows) {  // in-kernel RCM gather / scatter of token rows (2-D row coordinates are int32)
     require(a.slots * a.n < (1ull << 31) - 1, "too many rows for the gather path (slots * n >= 2^31)");
     if (a.d == 64) launch_d<64, true>(prep, a, s, num_sms);
     else launch_d<128, true>(prep, a, s, num_sms);

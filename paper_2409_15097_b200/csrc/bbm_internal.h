@@ -144,6 +144,8 @@ struct StreamCtx {
   size_t split_ctr_n = 0;
   float* rowws = nullptr;        // backward lse2 | delta
   size_t rowws_floats = 0;
+  uint8_t* perm = nullptr;       // RCM pass-mode scratch: permuted Q/K/V/O + row statistics
+  size_t perm_bytes = 0;
   std::map<std::tuple<int, uint64_t, uint32_t>, DevPlan> plans;
 };
 
@@ -244,9 +246,12 @@ struct AttnArgs {
   int variant;
   // optional in-kernel RCM application (reorder.hpp:156-189): device u32 [n], forward map new ->
   // old. q/k/v/o and the row statistics are then in the ORIGINAL token order while the prep holds
-  // the permuted mask: rows are gathered / scattered by TMA inside the kernel.
+  // the permuted mask: rows are gathered / scattered by TMA inside the kernel (kGatherTma), or
+  // permuted into per-stream scratch by HBM-bound passes around the plain kernel (kGatherPasses).
   const uint32_t* rows = nullptr;
+  int gather_mode = 0;
 };
+enum GatherMode : int { kGatherAuto = 0, kGatherPasses = 1, kGatherTma = 2 };
 // Process-wide kernel event trace (bbm_set_trace): device buffer of ctas * 8192 u64 events.
 struct TraceConfig {
   void* buffer = nullptr;
@@ -291,6 +296,7 @@ void mark_launch_done(StreamCtx& ctx, cudaStream_t s);
 // grow-only per-stream scratch
 float* ctx_workspace(StreamCtx& ctx, size_t floats, cudaStream_t s);
 uint32_t* ctx_split_ctr(StreamCtx& ctx, size_t count, cudaStream_t s);
+uint8_t* ctx_perm_scratch(StreamCtx& ctx, size_t bytes, cudaStream_t s);
 
 // ---- attention backward (attn_bwd.cu) ----
 struct BwdArgs {

@@ -181,6 +181,7 @@ Prep::~Prep() {
     cudaFree(c.ws);
     cudaFree(c.split_ctr);
     cudaFree(c.rowws);
+    cudaFree(c.perm);
     if (c.done) cudaEventDestroy(c.done);
     for (auto& pl : c.plans) {
       cudaFree(pl.second.mem);
@@ -800,12 +801,20 @@ bbm_status bbm_attn_fwd(bbm_prep prep, int variant, const void* q, const void* k
 bbm_status bbm_attn_fwd_gather(bbm_prep prep, int variant, const uint32_t* d_forward, const void* q,
                                const void* k, const void* v, void* out, float* row_max, float* row_sum,
                                uint64_t slots, uint32_t head_dim, double scale, void* stream) {
+  return bbm_attn_fwd_gather_ex(prep, variant, d_forward, q, k, v, out, row_max, row_sum, slots, head_dim,
+                                scale, stream, 0);
+}
+
+bbm_status bbm_attn_fwd_gather_ex(bbm_prep prep, int variant, const uint32_t* d_forward, const void* q,
+                                  const void* k, const void* v, void* out, float* row_max, float* row_sum,
+                                  uint64_t slots, uint32_t head_dim, double scale, void* stream, int mode) {
   return guarded([&] {
     const Prep& pr = unwrap(prep);
     check_attn_args(pr, variant, slots, head_dim, scale);
     require(q && k && v && out && d_forward, "null pointer");
+    require(mode >= 0 && mode <= 2, "gather mode must be 0 (auto), 1 (passes) or 2 (in-kernel TMA)");
     AttnArgs a{q, k, v, out, row_max, row_sum, slots, pr.n, head_dim, static_cast<float>(scale),
-               variant, d_forward};
+               variant, d_forward, mode};
     int dev = 0;
     BBM_CUDA(cudaGetDevice(&dev));
     require(dev == pr.device, "prep lives on another device; use bbm_prep_replicate");

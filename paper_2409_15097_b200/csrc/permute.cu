@@ -1,6 +1,7 @@
 // permute.cu — device side of the RCM path (reorder.hpp:156-189).
 //   permute_rows_kernel  K5: X'[a] = X[fwd[a]] (permute_rows) or X'[fwd[a]] = X[a]
-//                        (unpermute_rows) over [slots][n][row_bytes], 16-byte vectors.
+//                        (unpermute_rows) over [slots][n][row_bytes], 16-byte vectors (4-byte
+//                        ones for rows that are not 16-byte multiples, e.g. row statistics).
 //   permute_mask_kernel  K6: mask'(a,b) = mask(fwd[a], fwd[b]) (permute_mask). One CTA per output
 //                        row: the source row is staged in shared memory, each warp builds one
 //                        64-bit output word from two 32-lane ballots (fwd reads coalesced).
@@ -13,7 +14,8 @@
 namespace bbm {
 namespace {
 
-__global__ void permute_rows_kernel(const uint4* __restrict__ src, uint4* __restrict__ dst,
+template <typename V>
+__global__ void permute_rows_kernel(const V* __restrict__ src, V* __restrict__ dst,
                                     const uint32_t* __restrict__ fwd, uint64_t slots, uint64_t n,
                                     uint64_t vec_per_row, bool inverse) {
   const uint64_t total = slots * n * vec_per_row;
@@ -66,13 +68,19 @@ __global__ void __launch_bounds__(256) permute_mask_kernel(const uint64_t* __res
 
 void launch_permute_rows(const void* src, void* dst, const uint32_t* d_fwd, uint64_t slots,
                          uint64_t n, uint64_t row_bytes, bool inverse, cudaStream_t s) {
-  const uint64_t vec = row_bytes / 16;
+  // 16-byte vectors for rows of 16-byte multiples (Q/K/V/O), 4-byte ones otherwise (row stats)
+  const bool wide = row_bytes % 16 == 0;
+  const uint64_t vec = wide ? row_bytes / 16 : row_bytes / 4;
   const uint64_t total = slots * n * vec;
   if (total == 0) return;
   uint64_t grid = (total + 255) / 256;
   if (grid > 148ull * 32) grid = 148ull * 32;
-  permute_rows_kernel<<<static_cast<unsigned>(grid), 256, 0, s>>>(
-      static_cast<const uint4*>(src), static_cast<uint4*>(dst), d_fwd, slots, n, vec, inverse);
+  if (wide)
+    permute_rows_kernel<uint4><<<static_cast<unsigned>(grid), 256, 0, s>>>(
+        static_cast<const uint4*>(src), static_cast<uint4*>(dst), d_fwd, slots, n, vec, inverse);
+  else
+    permute_rows_kernel<uint32_t><<<static_cast<unsigned>(grid), 256, 0, s>>>(
+        static_cast<const uint32_t*>(src), static_cast<uint32_t*>(dst), d_fwd, slots, n, vec, inverse);
   BBM_CUDA(cudaGetLastError());
 }
 

@@ -241,6 +241,20 @@ float* ctx_workspace(StreamCtx& ctx, size_t floats, cudaStream_t s) {
   return ctx.ws;
 }
 
+uint8_t* ctx_perm_scratch(StreamCtx& ctx, size_t bytes, cudaStream_t s) {
+  if (bytes > ctx.perm_bytes) {
+    if (ctx.perm) {
+      BBM_CUDA(cudaStreamSynchronize(s));
+      cudaFree(ctx.perm);
+    }
+    ctx.perm = nullptr;
+    ctx.perm_bytes = 0;
+    BBM_CUDA(cudaMalloc(&ctx.perm, bytes));
+    ctx.perm_bytes = bytes;
+  }
+  return ctx.perm;
+}
+
 uint32_t* ctx_split_ctr(StreamCtx& ctx, size_t count, cudaStream_t s) {
   if (count > ctx.split_ctr_n) {
     if (ctx.split_ctr) {

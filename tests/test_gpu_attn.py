@@ -401,10 +401,12 @@ def test_mixed_items_in_one_launch(cuda, d):
 
 @pytest.mark.parametrize("n,d,slots,spec", [(1000, 64, 3, "windowed(w=40)"), (2304, 128, 2, "global(w=90;g=70)"),
                                             (640, 128, 5, "causal")])
-def test_in_kernel_rcm_gather_equals_explicit_permutation(cuda, n, d, slots, spec):
-    """bbm_attn_fwd_gather (f2): original-order Q/K/V, the prep of the RCM-permuted mask, rows
-    gathered / O scattered by TMA inside the kernel == permute_rows + forward + unpermute_rows,
-    bit for bit, for every variant (incl. ragged n and split-KV rows)."""
+@pytest.mark.parametrize("mode", [0, 1, 2])
+def test_in_kernel_rcm_gather_equals_explicit_permutation(cuda, n, d, slots, spec, mode):
+    """bbm_attn_fwd_gather_ex (f2): original-order Q/K/V, the prep of the RCM-permuted mask, the
+    permutation applied on the device — by permute passes around the plain kernel (mode 1, the
+    default 0) or by TMA tile::gather4 / scatter4 inside the kernel (mode 2) — == permute_rows +
+    forward + unpermute_rows, bit for bit, for every variant (incl. ragged n and split-KV rows)."""
     import torch
 
     base = bbm.generate(spec, n)
@@ -420,7 +422,7 @@ def test_in_kernel_rcm_gather_equals_explicit_permutation(cuda, n, d, slots, spe
         out = torch.empty_like(q)
         m = torch.empty((slots, n), dtype=torch.float32, device=cuda)
         l = torch.empty_like(m)
-        bbm.attn_fwd_device(prep, var, q, k, v, out, m, l, d ** -0.5, rows=rows)
+        bbm.attn_fwd_device(prep, var, q, k, v, out, m, l, d ** -0.5, rows=rows, gather_mode=mode)
         qp, kp, vp = (bbm.permute_rows(t, perm) for t in (q, k, v))
         op = torch.empty_like(qp)
         mp = torch.empty_like(m)
