@@ -231,6 +231,14 @@ bbm_status bbm_set_trace(void* d_buffer, uint32_t ctas);
  *      empty score halves (chosen per launch plan from its occupied/full tile counts). ---- */
 bbm_status bbm_fwd_build_counts(uint64_t* plain, uint64_t* skipping);
 
+/* ---- forward kernel selection (diagnostics and tests, no reference counterpart): 0 = default
+ *      (attn_fwd.cu, one query tile per item with the softmax split over two warpgroups),
+ *      1 = the same, 2 = the two-stream kernel attn_fwd_pair.cu wherever it can run (two query
+ *      tiles per CTA sharing K/V loads, one softmax thread per row; bit-identical results where
+ *      attn_fwd.cu splits no row, measured slower on B200). Process-wide; the environment
+ *      variable BBM_FWD_KERNEL=single|pair sets the initial value. ---- */
+bbm_status bbm_set_fwd_kernel(int mode);
+
 /* ---- reorder.hpp ---- */
 /* rcm_order(build_graph(mask)) (reorder.hpp:28-133): forward[new] = old. Host. */
 bbm_status bbm_rcm_order(const uint64_t* words, uint64_t n, uint32_t* forward);

@@ -91,6 +91,7 @@ SIGNATURES = {
                                              C.POINTER(vp), C.POINTER(vp), C.c_uint64, C.c_uint32, C.c_double]),
     "bbm_run_attention_multi": (C.c_int, [vp, C.c_int, C.c_int, C.POINTER(C.c_int), u16p, u16p, u16p, u16p, f32p, f32p, C.c_uint64, C.c_uint32, C.c_double, f64p]),
     "bbm_set_trace": (C.c_int, [vp, C.c_uint32]),
+    "bbm_set_fwd_kernel": (C.c_int, [C.c_int]),
     "bbm_fwd_build_counts": (C.c_int, [C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]),
     "bbm_rcm_order": (C.c_int, [u64p, C.c_uint64, u32p]),
     "bbm_bandwidth": (C.c_int, [u64p, C.c_uint64, u64p]),

@@ -513,6 +513,15 @@ def attn_fwd_device(prep: MaskPrep, variant: Variant, q, k, v, out, row_max=None
                            int(slots), int(d), float(scale), C.c_void_p(s)))
 
 
+def set_fwd_kernel(mode: str) -> None:
+    """Forward kernel selection (bbm_set_fwd_kernel): "auto" / "single" (attn_fwd.cu, the default)
+    or "pair" (attn_fwd_pair.cu wherever it can run; measured slower, kept for comparison)."""
+    modes = {"auto": 0, "single": 1, "pair": 2}
+    if mode not in modes:
+        raise ValueError(f"unknown forward kernel mode {mode!r}")
+    check(lib.bbm_set_fwd_kernel(modes[mode]))
+
+
 def blocked_forward(q, k, v, scale: float, mask, prep: MaskPrep, variant: Variant,
                     threads: int = 1, check_finite: bool = True) -> ForwardResult:
     """blocked_forward (engine.hpp:282-341) on the sm_100a kernel.

@@ -48,12 +48,14 @@
 
 #include "bbm_internal.h"
 #include "bbm_ptx.cuh"
+#include "bbm_softmax.cuh"
 #include "bbm_tmap.h"
 
 namespace bbm {
 namespace {
 
 using namespace ptx;
+using namespace softmax;
 
 enum Mode : int { kModeBinblk = 0, kModeDenseBinblk = 1, kModeDense = 2, kModeNaive = 3 };
 
@@ -139,15 +141,16 @@ __host__ __device__ constexpr uint32_t kseq_of(uint32_t k) {
 }
 __host__ __device__ constexpr uint32_t vseq_of(uint32_t k) { return 2 * k + kSBufs; }
 static_assert(kseq_of(kSBufs) == vseq_of(0) + 1 && vseq_of(1) == kseq_of(kSBufs) + 1, "interleave");
-constexpr float kRescaleThreshold = 8.0f;     // log2 units
-constexpr float kLn2 = 0.69314718055994530942f;
 
 template <int D>
 struct Cfg {
   static constexpr uint32_t kBoxes = D / 64;
   static constexpr uint32_t kTileBytes = kBoxes * kBoxBytes;  // one 128 x D bf16 tile
   // K/V ring slots: the K cursor runs kSBufs tiles ahead of the V cursor
-  static constexpr uint32_t kRing = (D == 64) ? 9 : kSBufs + 1;
+#ifndef BBM_RING128
+#define BBM_RING128 (BBM_SBUFS + 1)
+#endif
+  static constexpr uint32_t kRing = (D == 64) ? 9 : BBM_RING128;
   static constexpr uint32_t kStageBytes = kBoxBytes;          // epilogue staging: one 128 x 64 box
   static constexpr uint32_t kTmemCols = 512;
   static constexpr uint32_t kOCol = kSBufs * 128;
@@ -223,73 +226,6 @@ __device__ __forceinline__ int32_t gather_row(const FwdParams& p, uint32_t slot,
 template <bool kGather>
 __device__ __forceinline__ uint64_t out_row(const FwdParams& p, uint32_t slot, uint64_t grow) {
   return static_cast<uint64_t>(slot) * p.n + (kGather ? __ldg(p.rows + grow) : grow);
-}
-
-// Replace the scores of invisible keys by a sentinel in place: -inf (or +inf when the scale is
-// negative, so that scale * sentinel = -inf). The max and exp passes then need no selects.
-__device__ __forceinline__ void apply_mask(uint32_t (&r)[32], uint32_t mw, uint32_t sentinel) {
-#pragma unroll
-  for (uint32_t i = 0; i < 32; ++i) r[i] = ((mw >> i) & 1u) ? r[i] : sentinel;
-}
-
-// Max of 32 (already masked) raw scores of one row chunk; of the negated scores when the scale
-// is negative (FMNMX takes negated operands for free).
-template <bool kNeg>
-__device__ __forceinline__ float chunk_max(const uint32_t (&r)[32]) {
-  float m0 = -INFINITY, m1 = -INFINITY;
-#pragma unroll
-  for (uint32_t i = 0; i < 32; i += 4) {
-    float a = __uint_as_float(r[i]), b = __uint_as_float(r[i + 1]);
-    float c = __uint_as_float(r[i + 2]), d = __uint_as_float(r[i + 3]);
-    if constexpr (kNeg) { a = -a; b = -b; c = -c; d = -d; }
-    m0 = fmax3(m0, a, b);
-    m1 = fmax3(m1, c, d);
-  }
-  return fmaxf(m0, m1);
-}
-
-// Which of the 16 exponential pairs of a chunk run as a polynomial on the FMA pipe instead of
-// MUFU ex2 (bit i = pair i): 6 of 16 balances the XU pipe (8 cycles per warp instruction) against
-// the extra issue slots of the polynomial (~10 instructions per pair).
-#ifndef BBM_POLY_PAIRS
-#define BBM_POLY_PAIRS 0x0707u
-#endif
-constexpr uint32_t kPolyPairs = BBM_POLY_PAIRS;
-
-// P chunk: 32 scores -> 16 packed bf16x2; accumulates the fp32 sum of the unrounded
-// exponentials into the packed pair `lacc`. Scale/shift and the sum run two lanes per
-// instruction (FFMA2 / FADD2).
-__device__ __forceinline__ void chunk_exp(const uint32_t (&r)[32], uint64_t sl2x2, uint64_t neg_m_x2,
-                                          uint32_t (&pk)[16], uint64_t& lacc) {
-#pragma unroll
-  for (uint32_t i = 0; i < 32; i += 2) {
-    const uint64_t x = ffma2(f2_pack(__uint_as_float(r[i]), __uint_as_float(r[i + 1])), sl2x2,
-                             neg_m_x2);
-    const float x0 = f2_lo(x), x1 = f2_hi(x);
-    float e0, e1;
-    if ((kPolyPairs >> ((i / 2) & 15)) & 1u) {
-      exp2_poly2(x0, x1, e0, e1);  // this pair on the FMA pipe
-    } else {
-      e0 = fast_exp2(x0);  // MUFU
-      e1 = fast_exp2(x1);
-    }
-    lacc = fadd2(lacc, f2_pack(e0, e1));
-    pk[i / 2] = pack_bf16x2(e0, e1);
-  }
-}
-
-// 32 fp32 -> 4 x 16 B of bf16 into a 128B-swizzled staging row
-__device__ __forceinline__ void stage_chunk32(uint8_t* rowp, uint32_t row, uint32_t chunk0,
-                                              const float* v, float inv) {
-#pragma unroll
-  for (uint32_t c = 0; c < 4; ++c) {
-    uint4 w;
-    w.x = pack_bf16x2(v[c * 8 + 0] * inv, v[c * 8 + 1] * inv);
-    w.y = pack_bf16x2(v[c * 8 + 2] * inv, v[c * 8 + 3] * inv);
-    w.z = pack_bf16x2(v[c * 8 + 4] * inv, v[c * 8 + 5] * inv);
-    w.w = pack_bf16x2(v[c * 8 + 6] * inv, v[c * 8 + 7] * inv);
-    *reinterpret_cast<uint4*>(rowp + (((chunk0 + c) ^ (row & 7)) << 4)) = w;
-  }
 }
 
 template <int D, int MODE, bool kTrace, bool kGather, bool kSkip>
@@ -1146,6 +1082,7 @@ void launch_attn_fwd(const Prep& prep, const AttnArgs& a, cudaStream_t s, int nu
   require(a.slots < (1ull << 24), "too many slots for one launch");
   if (a.slots * prep.kmeta.krows == 0) return;
   if (a.d != 64 && a.d != 128) throw ArgError("head dim must be 64 or 128 on the sm_100a kernel");
+  if (launch_attn_fwd_pair(prep, a, s, num_sms)) return;  // only when selected (bbm_set_fwd_kernel)
   if (a.rows && gather_mode_of(a.gather_mode) == kGatherPasses) {
     launch_gather_passes(prep, a, s, num_sms);
   } else if (a.rows) {  // in-kernel RCM gather / scatter of token rows (2-D row coordinates are int32)

@@ -267,6 +267,10 @@ constexpr uint32_t kPrepRowSplits = BBM_PREP_SPLITS;
 void fwd_build_counts(uint64_t& plain, uint64_t& skipping);
 
 void launch_attn_fwd(const Prep& prep, const AttnArgs& a, cudaStream_t s, int num_sms);
+// the two-stream forward (attn_fwd_pair.cu) when selected with set_fwd_kernel(2); false = not
+// selected or not applicable (the caller runs attn_fwd.cu)
+bool launch_attn_fwd_pair(const Prep& prep, const AttnArgs& a, cudaStream_t s, int num_sms);
+void set_fwd_kernel(int mode);  // 0 default (single-stream), 1 single-stream, 2 pair wherever it can run
 
 // ---- device launch plans (plan.cu) ----
 enum PlanClass : int { kPlanDense = 0, kPlanNaive = 1, kPlanList = 2 };

@@ -1054,6 +1054,13 @@ bbm_status bbm_set_trace(void* d_buffer, uint32_t ctas) {
   });
 }
 
+bbm_status bbm_set_fwd_kernel(int mode) {
+  return guarded([&] {
+    require(mode >= 0 && mode <= 2, "forward kernel mode must be 0 (auto), 1 (single) or 2 (pair)");
+    set_fwd_kernel(mode);
+  });
+}
+
 bbm_status bbm_fwd_build_counts(uint64_t* plain, uint64_t* skipping) {
   return guarded([&] {
     require(plain && skipping, "null argument");

@@ -22,6 +22,8 @@ for v in $VARIANTS; do
     DEG2_4) FL="-DBBM_POLY_DEG2 -DBBM_POLY_PAIRS=0x0303u" ;;
     NO_PV) FL="-DBBM_ABLATE_NO_PV" ;;
     NO_KVLOAD) FL="-DBBM_ABLATE_NO_KVLOAD" ;;
+    S2R3) FL="-DBBM_SBUFS=2" ;;
+    S2R4) FL="-DBBM_SBUFS=2 -DBBM_RING128=4" ;;
     HALF_KVLOAD) FL="-DBBM_ABLATE_HALF_KVLOAD" ;;
     FAST_NOKV) FL="-DBBM_ABLATE_FAST_ENGINE -DBBM_ABLATE_NO_KVLOAD" ;;
     SUSPEND) FL="-DBBM_SUSPEND_WAIT" ;;
