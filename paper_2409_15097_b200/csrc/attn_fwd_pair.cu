@@ -11,8 +11,9 @@
 // while the other reduces maxima (FA4-style ping-pong).
 //
 // Status: selected only on request (bbm_set_fwd_kernel(2)). Measured on B200 it is 15-25 % slower
-// than attn_fwd.cu even with the softmax removed: S_s(t+1) must wait for PV_s(t)
-// to COMPLETE, so at most two MMA groups are in flight and the completion round trips show.
+// than attn_fwd.cu, its MMA side alone included: one thread issues every MMA of
+// both streams (tcgen05 issue takes ~56 cycles per 128x128x16 MMA, so S + PV of a tile are ~900
+// issue cycles for 1024 tensor cycles) and S_s(t+1) waits for PV_s(t) to complete.
 //
 // K/V sharing: the producer merges the two lists into one load schedule. A tile both rows visit
 // is loaded once and feeds both streams' MMAs (adjacent row tiles of banded, causal and packed
@@ -685,10 +686,8 @@ int fwd_kernel_override() {
 void set_fwd_kernel(int mode) { g_fwd_kernel.store(mode, std::memory_order_relaxed); }
 
 bool launch_attn_fwd_pair(const Prep& prep, const AttnArgs& a, cudaStream_t s, int num_sms) {
-  // Selected explicitly only (bbm_set_fwd_kernel(2) / BBM_FWD_KERNEL=pair): on B200 it measured
-  // 15-25 % slower than attn_fwd.cu, because S_s(t+1) may only be issued once
-  // PV_s(t) has COMPLETED (P lives in S's columns and tcgen05 orders MMAs only on the same
-  // accumulator), which leaves at most two MMA groups in flight.
+  // Selected explicitly only (bbm_set_fwd_kernel(2) / BBM_FWD_KERNEL=pair): measured slower than
+  // attn_fwd.cu on B200.
   if (fwd_kernel_override() != 2 || a.rows) return false;
   if (a.d != 128 && a.d != 64) return false;
   const KernelMeta& km = prep.kmeta;
