@@ -27,7 +27,7 @@ import numpy as np
 
 from . import _lib
 from .blockmask import (BlockSpec, EngineCounters, Variant, attn_bwd_device, attn_fwd_device, bandwidth,
-                        generate, parse_variant, permute_mask, preprocess_mask, rcm_order, to_string)
+                        generate, parse_variant, permute_mask, permute_rows, preprocess_mask, rcm_order, to_string)
 
 CSV_HEADER = ("variant,mask,n,block_i,block_j,batch,heads,runs,precision,prepro_ms,fwd_ms_mean,"
               "fwd_ms_std,bwd_ms_mean,bwd_ms_std,total_ms_mean,blocks_visited,blocks_processed,"
@@ -308,8 +308,8 @@ def run_bench(cfg: BenchConfig, sink: Optional[Callable[[BenchRecord], None]] = 
         pmask = permute_mask(mask, perm, device=device)
         pprep = preprocess_mask(pmask, spec, device=device)
         rcm_ms = (time.perf_counter() - t0) * 1e3
-        fwd_idx = torch.from_numpy(perm.forward.astype(np.int64)).to(dev)
-        ptensors = [t.index_select(1, fwd_idx).contiguous() for t in tensors]
+        # permute_rows (reorder.hpp:167-176) with the device kernel (K5), as bench.hpp:456-458
+        ptensors = [permute_rows(t, perm) for t in tensors]
         bw0, bw1 = bandwidth(mask), bandwidth(pmask)
         for v in cfg.variants:
             rec = _bench_variant(cfg, ptensors, pmask, pprep, rcm_ms, v, label + "+rcm", dev)
