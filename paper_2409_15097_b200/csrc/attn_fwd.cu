@@ -90,15 +90,22 @@ struct FwdParams {
 #endif
 template <int D>
 constexpr uint32_t kParts = D == 128 ? BBM_PARTS128 : 2;
-static_assert(BBM_PARTS128 == 2, "the register split below assumes two engine warpgroups");
 // warpgroup 0: producer / MMA issuers / TMEM allocator; 1..kParts: softmax engine; last: epilogue
 template <int D>
 constexpr uint32_t kThreadsOf = 256 + 128 * kParts<D>;
 #ifndef BBM_ENGINE_REGS
 #define BBM_ENGINE_REGS 168
 #endif
-constexpr uint32_t kEngineRegs = BBM_ENGINE_REGS;  // setmaxnreg: 2 x 128 x 168 + 2 x 128 x 88 = 65536
-constexpr uint32_t kOtherRegs = 256 - kEngineRegs;
+// setmaxnreg moves registers between the warpgroups of the CTA's launch allocation (the launch
+// register count x threads): 2 parts: 512 threads x 128 = 2 x 128 x 168 (engine) + 2 x 128 x 88;
+// 4 parts: 768 threads x 80 = 4 x 128 x 88 + 2 x 128 x 64.
+template <int D>
+constexpr uint32_t kLaunchRegs = (65536 / kThreadsOf<D>) / 8 * 8;
+template <int D>
+constexpr uint32_t kEngineRegs = kParts<D> == 2 ? BBM_ENGINE_REGS : 88;
+template <int D>
+constexpr uint32_t kOtherRegs = (kLaunchRegs<D> * (2 + kParts<D>) - kParts<D> * kEngineRegs<D>) / 2;
+static_assert(kOtherRegs<128> % 8 == 0 && kOtherRegs<128> >= 56, "register split");
 constexpr uint32_t kTraceCap = 8192;  // events per traced CTA
 constexpr uint32_t kQueue = 8;        // item queue depth (items open between the producer and the PV issuer)
 
@@ -294,7 +301,7 @@ __global__ void __launch_bounds__(kThreadsOf<D>, 1)
   const bool engine_wg = warp >= 4 && warp < 4 + 4 * kParts<D>;
 
   if (warp < 4) {
-  setmaxnreg_dec<kOtherRegs>();
+  setmaxnreg_dec<kOtherRegs<D>>();
   if (warp == 0) {
     // ------------------------------------------------------------------ producer
     // Loads follow the MMA issuers' consumption order (kseq_of / vseq_of): a K cursor runs kSBufs
@@ -507,7 +514,7 @@ __global__ void __launch_bounds__(kThreadsOf<D>, 1)
     }
   }
   } else if (engine_wg) {
-    setmaxnreg_inc<kEngineRegs>();
+    setmaxnreg_inc<kEngineRegs<D>>();
     // ------------------------------------------------------------------ softmax engine
     constexpr uint32_t kP = kParts<D>;
     constexpr uint32_t kSC = 128 / kP;        // score columns per part
@@ -668,7 +675,7 @@ __global__ void __launch_bounds__(kThreadsOf<D>, 1)
         float tmax = pmax;
 #else
         ctl->xchg[step & 1][half][row] = pmax;
-        named_bar_sync(3 + quad, 64);
+        named_bar_sync(3 + quad, 32 * kP);
         float tmax = pmax;
 #pragma unroll
         for (uint32_t o = 1; o < kP; ++o) tmax = fmaxf(tmax, ctl->xchg[step & 1][(half + o) % kP][row]);
@@ -748,7 +755,7 @@ __global__ void __launch_bounds__(kThreadsOf<D>, 1)
       mbar_arrive(&ctl->stats_full[sl]);
     }
   } else {
-    setmaxnreg_dec<kOtherRegs>();
+    setmaxnreg_dec<kOtherRegs<D>>();
     // ------------------------------------------------------------------ epilogue warpgroup
     // Per item (in O-accumulator order): row statistics from the engine, then the item's last PV
     // (o_full), then O / l -> bf16 staged in 128B-swizzled shared memory -> TMA store, or, for a
