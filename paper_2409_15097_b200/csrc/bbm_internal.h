@@ -152,12 +152,18 @@ struct StreamCtx {
 // Host-buffer pipeline of one prep's device (host_io.cu): persistent device buffers (grow-only)
 // and three streams, so a host-buffer call overlaps H2D of slot chunk c+1, the kernel on chunk c
 // and D2H of chunk c-1 instead of running copy -> kernel -> copy serially.
+class HostPool;  // host_io.cu: persistent host threads for float -> bf16 conversion
 struct HostPipe {
   cudaStream_t h2d = nullptr, comp = nullptr, d2h = nullptr;
   std::vector<cudaEvent_t> ev_in, ev_out;
   uint8_t* buf = nullptr;
   size_t cap = 0;
   int* bad = nullptr;  // device finiteness flags (q, k, v, d_out)
+  // float host path: slots converted to bf16 on the host go through two pinned staging buffers
+  uint8_t* stage = nullptr;
+  size_t stage_cap = 0;  // bytes per staging buffer
+  cudaEvent_t ev_stage[2] = {nullptr, nullptr};
+  HostPool* pool = nullptr;
   ~HostPipe();
 };
 

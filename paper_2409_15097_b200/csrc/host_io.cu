@@ -10,14 +10,90 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
-#include <string>
+#include <atomic>
+#include <condition_variable>
 #include <cstdint>
+#include <cstdlib>
+#include <cstring>
+#include <functional>
+#include <mutex>
+#include <string>
+#include <thread>
+#include <vector>
 
 #include "bbm_internal.h"
 
 namespace bbm {
 
+// Persistent host threads for the float host path's float -> bf16 conversion: run(n, fn) calls
+// fn(0..n-1) on the workers and the calling thread and returns when all calls are done.
+class HostPool {
+ public:
+  explicit HostPool(unsigned workers) {
+    for (unsigned i = 0; i < workers; ++i) threads_.emplace_back([this] { loop(); });
+  }
+  ~HostPool() {
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      stop_ = true;
+    }
+    cv_.notify_all();
+    for (auto& t : threads_) t.join();
+  }
+  void run(uint32_t tasks, std::function<void(uint32_t)> fn) {
+    if (tasks == 0) return;
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      fn_ = std::move(fn);
+      next_.store(0);
+      done_.store(0);
+      tasks_.store(tasks);
+      ++gen_;
+    }
+    cv_.notify_all();
+    work();
+    std::unique_lock<std::mutex> lk(mu_);
+    done_cv_.wait(lk, [&] { return done_.load() == tasks_.load(); });
+  }
+
+ private:
+  void work() {
+    for (;;) {
+      const uint32_t i = next_.fetch_add(1);
+      if (i >= tasks_.load()) return;
+      fn_(i);
+      if (done_.fetch_add(1) + 1 == tasks_.load()) {
+        std::lock_guard<std::mutex> lk(mu_);
+        done_cv_.notify_all();
+      }
+    }
+  }
+  void loop() {
+    uint64_t seen = 0;
+    for (;;) {
+      {
+        std::unique_lock<std::mutex> lk(mu_);
+        cv_.wait(lk, [&] { return stop_ || gen_ != seen; });
+        if (stop_) return;
+        seen = gen_;
+      }
+      work();
+    }
+  }
+  std::vector<std::thread> threads_;
+  std::mutex mu_;
+  std::condition_variable cv_, done_cv_;
+  std::function<void(uint32_t)> fn_;
+  std::atomic<uint32_t> next_{0}, done_{0}, tasks_{0};
+  uint64_t gen_ = 0;
+  bool stop_ = false;
+};
+
 HostPipe::~HostPipe() {
+  delete pool;
+  for (cudaEvent_t e : ev_stage)
+    if (e) cudaEventDestroy(e);
+  if (stage) cudaFreeHost(stage);
   for (cudaEvent_t e : ev_in) cudaEventDestroy(e);
   for (cudaEvent_t e : ev_out) cudaEventDestroy(e);
   if (h2d) cudaStreamDestroy(h2d);
@@ -40,6 +116,8 @@ HostPipe& pipe_of(const Prep& prep) {
       BBM_CUDA(cudaStreamCreateWithFlags(&p->comp, cudaStreamNonBlocking));
       BBM_CUDA(cudaStreamCreateWithFlags(&p->d2h, cudaStreamNonBlocking));
       BBM_CUDA(cudaMalloc(&p->bad, 4 * sizeof(int)));
+      BBM_CUDA(cudaEventCreateWithFlags(&p->ev_stage[0], cudaEventDisableTiming));
+      BBM_CUDA(cudaEventCreateWithFlags(&p->ev_stage[1], cudaEventDisableTiming));
       p->ev_in.resize(kMaxChunks);
       p->ev_out.resize(kMaxChunks);
       for (uint32_t c = 0; c < kMaxChunks; ++c) {
@@ -134,6 +212,35 @@ __global__ void widen_outputs_kernel(const __nv_bfloat16* __restrict__ o, float*
 
 unsigned grid_for_elems(uint64_t count) {
   return static_cast<unsigned>(std::max<uint64_t>(1, std::min<uint64_t>((count / 8 + 255) / 256, 148ull * 16)));
+}
+
+// float -> bf16, round to nearest even (the device kernel's __float2bfloat16_rn on finite values),
+// fused with require_finite's test; returns true if any value is inf / NaN
+bool f32_to_bf16_host(const float* in, uint16_t* out, uint64_t count) {
+  uint32_t bad = 0;
+  for (uint64_t i = 0; i < count; ++i) {
+    uint32_t u;
+    std::memcpy(&u, in + i, 4);
+    bad |= static_cast<uint32_t>((u & 0x7F800000u) == 0x7F800000u);
+    out[i] = static_cast<uint16_t>((u + 0x7FFFu + ((u >> 16) & 1u)) >> 16);
+  }
+  return bad != 0;
+}
+
+// Fraction of a chunk's slots the float path converts on the host. Pageable inputs: all (the
+// copy engine would stage pageable memory through driver buffers anyway, so converting into our
+// pinned staging costs no extra pass). Pinned inputs: the host converts ~67 GB/s of float with 16
+// threads while PCIe moves ~54 GB/s, so converting ~70 % of the slots on the host and sending the
+// rest as float balances the two (BBM_HOST_CONVERT overrides, 0..1).
+double host_convert_fraction(const void* sample) {
+  const char* e = std::getenv("BBM_HOST_CONVERT");
+  if (e) return std::min(1.0, std::max(0.0, std::atof(e)));
+  cudaPointerAttributes at{};
+  if (cudaPointerGetAttributes(&at, sample) != cudaSuccess) {
+    (void)cudaGetLastError();
+    return 1.0;
+  }
+  return at.type == cudaMemoryTypeHost ? 0.7 : 1.0;
 }
 
 void throw_if_bad(const int* hbad, int count) {
@@ -242,18 +349,60 @@ void run_fwd_host_f32(const Prep& prep, int variant, const float* const* q, cons
   }
   const float* const* src[3] = {q, k, v};
   __nv_bfloat16* dst[3] = {bq, bk, bv};
+  // Per chunk, the first nh slots are converted to bf16 by host threads into a pinned staging
+  // buffer (half the PCIe bytes), the rest cross PCIe as float and are converted on the device.
+  // The host converts chunk c while the copy engines and the SMs work on chunks c-1, c-2.
+  const double frac = host_convert_fraction(q[0]);
+  const uint64_t max_ns = (slots + chunks - 1) / chunks;
+  const uint64_t max_nh = std::min<uint64_t>(max_ns, static_cast<uint64_t>(frac * static_cast<double>(max_ns) + 0.5));
+  if (max_nh > 0) {
+    const size_t need = 3 * max_nh * per * 2;
+    if (need > p.stage_cap) {
+      BBM_CUDA(cudaStreamSynchronize(p.h2d));
+      if (p.stage) cudaFreeHost(p.stage);
+      p.stage = nullptr;
+      p.stage_cap = 0;
+      BBM_CUDA(cudaMallocHost(&p.stage, 2 * need));
+      p.stage_cap = need;
+    }
+    if (!p.pool) {
+      const unsigned hw = std::max(2u, std::thread::hardware_concurrency());
+      p.pool = new HostPool(std::min(hw, 16u) - 1);
+    }
+  }
+  std::atomic<int> host_bad[3];
+  for (auto& hb : host_bad) hb.store(0);
+  constexpr uint64_t kPiece = 1ull << 21;  // elements per host conversion task
+  const uint64_t pieces = (per + kPiece - 1) / kPiece;
   for (uint64_t c = 0; c < chunks; ++c) {
     const uint64_t s0 = slots * c / chunks, s1 = slots * (c + 1) / chunks, ns = s1 - s0;
     const uint64_t off = s0 * per;
-    for (uint64_t sl = s0; sl < s1; ++sl)
+    const uint64_t nh = std::min<uint64_t>(ns, static_cast<uint64_t>(frac * static_cast<double>(ns) + 0.5));
+    if (nh > 0) {
+      uint16_t* st = reinterpret_cast<uint16_t*>(p.stage + (c & 1) * p.stage_cap);
+      if (c >= 2) BBM_CUDA(cudaEventSynchronize(p.ev_stage[c & 1]));  // its H2D two chunks ago is done
+      p.pool->run(static_cast<uint32_t>(3 * nh * pieces), [&](uint32_t task) {
+        const uint64_t t = task / (nh * pieces), rem = task % (nh * pieces);
+        const uint64_t sl = rem / pieces, e0 = (rem % pieces) * kPiece, e1 = std::min(per, e0 + kPiece);
+        if (f32_to_bf16_host(src[t][s0 + sl] + e0, st + (t * nh + sl) * per + e0, e1 - e0))
+          host_bad[t].store(1, std::memory_order_relaxed);
+      });
+      for (int t = 0; t < 3; ++t)
+        BBM_CUDA(cudaMemcpyAsync(dst[t] + off, st + t * nh * per, nh * per * 2, cudaMemcpyHostToDevice, p.h2d));
+      BBM_CUDA(cudaEventRecord(p.ev_stage[c & 1], p.h2d));
+    }
+    for (uint64_t sl = s0 + nh; sl < s1; ++sl)
       for (int t = 0; t < 3; ++t)
         BBM_CUDA(cudaMemcpyAsync(fin[t] + sl * per, src[t][sl], per * 4, cudaMemcpyHostToDevice, p.h2d));
     BBM_CUDA(cudaEventRecord(p.ev_in[c], p.h2d));
     BBM_CUDA(cudaStreamWaitEvent(p.comp, p.ev_in[c], 0));
-    for (int t = 0; t < 3; ++t)
-      f32_to_bf16_check_kernel<<<grid_for_elems(ns * per), 256, 0, p.comp>>>(fin[t] + off, dst[t] + off,
-                                                                              ns * per, p.bad + t);
-    BBM_CUDA(cudaGetLastError());
+    if (ns > nh) {
+      const uint64_t doff = (s0 + nh) * per;
+      for (int t = 0; t < 3; ++t)
+        f32_to_bf16_check_kernel<<<grid_for_elems((ns - nh) * per), 256, 0, p.comp>>>(
+            fin[t] + doff, dst[t] + doff, (ns - nh) * per, p.bad + t);
+      BBM_CUDA(cudaGetLastError());
+    }
     AttnArgs a{bq + off, bk + off, bv + off, bo + off, fmax + s0 * n, fsum + s0 * n, ns, n, d, scale, variant};
     launch_attn_fwd(prep, a, p.comp, num_sms);
     widen_outputs_kernel<<<grid_for_elems(ns * per), 256, 0, p.comp>>>(
@@ -280,6 +429,7 @@ void run_fwd_host_f32(const Prep& prep, int variant, const float* const* q, cons
     cudaEventDestroy(t0);
     cudaEventDestroy(t1);
   }
+  for (int t = 0; t < 3; ++t) hbad[t] |= host_bad[t].load();
   throw_if_bad(hbad, 3);
 }
 

@@ -30,13 +30,14 @@ def dev_inputs(cuda, slots, n, d, seed=1):
     return [(torch.rand((slots, n, d), generator=g, device=cuda) * 2 - 1).to(torch.bfloat16) for _ in range(3)]
 
 
-def fwd(prep, variant, q, k, v, stream=None):
+def fwd(prep, variant, q, k, v, stream=None, scale=None):
     import torch
 
     out = torch.empty_like(q)
     m = torch.empty(q.shape[:2], dtype=torch.float32, device=q.device)
     l = torch.empty_like(m)
-    bbm.attn_fwd_device(prep, variant, q, k, v, out, m, l, 1 / np.sqrt(q.shape[-1]), stream)
+    bbm.attn_fwd_device(prep, variant, q, k, v, out, m, l,
+                        1 / np.sqrt(q.shape[-1]) if scale is None else scale, stream)
     return out, m, l
 
 
@@ -306,3 +307,33 @@ def test_device_entry_rejects_mismatched_shapes(cuda):
         bbm.attn_fwd_device(prep, bbm.Variant.binblk, q, k.expand(3, n, d), q, torch.empty_like(q))
     with pytest.raises(ValueError, match="scale"):
         bbm.blocked_forward(q, q, q, 1e39, mask, prep, bbm.Variant.binblk)
+
+
+@pytest.mark.parametrize("pinned", [False, True])
+def test_float_host_path_rounding_equals_device(cuda, pinned):
+    """The float host path converts part of the slots on the host (all of them for pageable
+    buffers, ~70 % for pinned ones) and the rest on the device: both must round to nearest even
+    exactly like torch's device conversion, on values that are NOT bf16-representable."""
+    import torch
+
+    n, d, slots = 900, 128, 7
+    mask = bbm.gen_longformer_windowed(n, 60)
+    prep = bbm.preprocess_mask(mask, bbm.BlockSpec(128, 128))
+    g = torch.Generator().manual_seed(5)
+    host = [torch.rand((slots, n, d), generator=g) * 6 - 3 for _ in range(3)]
+    if pinned:
+        host = [t.pin_memory() for t in host]
+    outs = torch.empty((slots, n, d), dtype=torch.float32)
+    rms = torch.empty((slots, n), dtype=torch.float64)
+    rss = torch.empty((slots, n), dtype=torch.float64)
+    if pinned:
+        outs, rms, rss = outs.pin_memory(), rms.pin_memory(), rss.pin_memory()
+    arr = lambda t: (C.c_void_p * slots)(*[t[s].data_ptr() for s in range(slots)])  # noqa: E731
+    _lib.check(_lib.lib.bbm_run_attention_host_f32(prep.handle.h, int(bbm.Variant.binblk), arr(host[0]),
+                                                   arr(host[1]), arr(host[2]), arr(outs), arr(rms), arr(rss),
+                                                   slots, d, 0.07))
+    dev = [t.to(cuda).to(torch.bfloat16) for t in host]
+    o, m, l = fwd(prep, bbm.Variant.binblk, *dev, scale=0.07)
+    torch.cuda.synchronize()
+    assert torch.equal(outs, o.float().cpu())
+    assert torch.equal(rms, m.double().cpu()) and torch.equal(rss, l.double().cpu())
