@@ -20,6 +20,9 @@
 #include <string>
 #include <thread>
 #include <vector>
+#if defined(__SSE2__)
+#include <emmintrin.h>
+#endif
 
 #include "bbm_internal.h"
 
@@ -215,10 +218,36 @@ unsigned grid_for_elems(uint64_t count) {
 }
 
 // float -> bf16, round to nearest even (the device kernel's __float2bfloat16_rn on finite values),
-// fused with require_finite's test; returns true if any value is inf / NaN
+// fused with require_finite's test; returns true if any value is inf / NaN. SSE2 (the x86-64
+// baseline) with non-temporal stores: the pinned staging is only read again by the copy engine,
+// so streaming stores save the read-for-ownership pass over it (host memory bandwidth, shared
+// with the PCIe DMA, is what bounds this path).
 bool f32_to_bf16_host(const float* in, uint16_t* out, uint64_t count) {
   uint32_t bad = 0;
-  for (uint64_t i = 0; i < count; ++i) {
+  uint64_t i = 0;
+#if defined(__SSE2__)
+  if ((reinterpret_cast<uintptr_t>(out) & 15u) == 0) {
+    const __m128i exp_mask = _mm_set1_epi32(0x7F800000);
+    const __m128i bias = _mm_set1_epi32(0x7FFF), one = _mm_set1_epi32(1), flip = _mm_set1_epi32(0x8000);
+    const __m128i flip16 = _mm_set1_epi16(static_cast<short>(0x8000));
+    __m128i badv = _mm_setzero_si128();
+    for (; i + 8 <= count; i += 8) {
+      const __m128i a = _mm_loadu_si128(reinterpret_cast<const __m128i*>(in + i));
+      const __m128i b = _mm_loadu_si128(reinterpret_cast<const __m128i*>(in + i + 4));
+      badv = _mm_or_si128(badv, _mm_cmpeq_epi32(_mm_and_si128(a, exp_mask), exp_mask));
+      badv = _mm_or_si128(badv, _mm_cmpeq_epi32(_mm_and_si128(b, exp_mask), exp_mask));
+      // (u + 0x7FFF + ((u >> 16) & 1)) >> 16, shifted into signed 16-bit range for the pack
+      const __m128i ra = _mm_sub_epi32(
+          _mm_srli_epi32(_mm_add_epi32(_mm_add_epi32(a, bias), _mm_and_si128(_mm_srli_epi32(a, 16), one)), 16), flip);
+      const __m128i rb = _mm_sub_epi32(
+          _mm_srli_epi32(_mm_add_epi32(_mm_add_epi32(b, bias), _mm_and_si128(_mm_srli_epi32(b, 16), one)), 16), flip);
+      _mm_stream_si128(reinterpret_cast<__m128i*>(out + i), _mm_xor_si128(_mm_packs_epi32(ra, rb), flip16));
+    }
+    _mm_sfence();  // the streamed stores are visible before the copy engine reads the staging
+    bad |= static_cast<uint32_t>(_mm_movemask_epi8(badv) != 0);
+  }
+#endif
+  for (; i < count; ++i) {
     uint32_t u;
     std::memcpy(&u, in + i, 4);
     bad |= static_cast<uint32_t>((u & 0x7F800000u) == 0x7F800000u);
