@@ -748,8 +748,9 @@ def e2e_all(bbm, prep, variant, q, k, v, slots, n, d, scale, total_flops, args, 
                   "h2d_bytes_per_step": 3 * slots * n * d * 4,
                   "d2h_bytes_per_step": slots * n * d * 4 + 2 * slots * n * 8,
                   "path": "bbm_run_attention_host_f32 (C ABI of run_attention<float>: per-slot float host "
-                          "buffers, pinned; f32->bf16 + finiteness check on the device; float out, double "
-                          "row stats; synchronous)"}
+                          "buffers, pinned; ~70% of each chunk's slots rounded to bf16 by host threads into "
+                          "pinned staging, the rest converted on the device, finiteness checked on both; "
+                          "float out, double row stats; synchronous)"}
     del hq, hk, hv, ho, hm, hs
 
     u16 = C.POINTER(C.c_uint16)
