@@ -1087,6 +1087,10 @@ void launch_attn_fwd(const Prep& prep, const AttnArgs& a, cudaStream_t s, int nu
   require(a.slots >= 1, "need at least one batch/head slot");
   require(a.n == prep.n, "mask preprocessing does not match this problem");
   require(a.slots < (1ull << 24), "too many slots for one launch");
+  // work items (slot x row unit) are counted in 32 bits inside the kernels
+  require(a.slots * (static_cast<uint64_t>(prep.kmeta.krows) + 1) + plan_cap_chunks(a.slots, static_cast<uint32_t>(num_sms)) <
+              (1ull << 32),
+          "too many slots x row tiles for one launch");
   if (a.slots * prep.kmeta.krows == 0) return;
   if (a.d != 64 && a.d != 128) throw ArgError("head dim must be 64 or 128 on the sm_100a kernel");
   if (launch_attn_fwd_pair(prep, a, s, num_sms)) return;  // only when selected (bbm_set_fwd_kernel)

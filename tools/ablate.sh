@@ -24,6 +24,8 @@ for v in $VARIANTS; do
     NO_KVLOAD) FL="-DBBM_ABLATE_NO_KVLOAD" ;;
     S2R3) FL="-DBBM_SBUFS=2" ;;
     LOCKSTEP) FL="-DBBM_SPLIT_ENGINE=0" ;;
+    PREP16) FL="-DBBM_PREP_SPLITS=16" ;;
+    PREP32) FL="-DBBM_PREP_SPLITS=32" ;;
     S2R4) FL="-DBBM_SBUFS=2 -DBBM_RING128=4" ;;
     HALF_KVLOAD) FL="-DBBM_ABLATE_HALF_KVLOAD" ;;
     FAST_NOKV) FL="-DBBM_ABLATE_FAST_ENGINE -DBBM_ABLATE_NO_KVLOAD" ;;
