@@ -464,9 +464,9 @@ void run_fwd_host_f32(const Prep& prep, int variant, const float* const* q, cons
 
 // The RCM path end to end (reorder.hpp:156-189 + bench.hpp:448-467): the caller's Q/K/V are in
 // the ORIGINAL token order, `prep` was built from permute_mask(mask, perm), forward = perm's
-// new -> old map. Per slot chunk: H2D, the attention kernel in gather mode (it loads each tile's
-// rows through TMA tile::gather4 and stores O rows and row statistics at their original tokens —
-// no permute_rows / unpermute_rows passes), D2H.
+// new -> old map. Per slot chunk: H2D, the forward with the permutation applied on the device
+// (launch_attn_fwd with AttnArgs::rows: by default permute passes into per-stream scratch around
+// the plain kernel, O and row statistics scattered back to their original tokens), D2H.
 void run_fwd_host_rcm(const Prep& prep, int variant, const uint32_t* forward, const uint16_t* q,
                       const uint16_t* k, const uint16_t* v, uint16_t* out, float* row_max,
                       float* row_sum, uint64_t slots, uint32_t d, float scale, int num_sms,
