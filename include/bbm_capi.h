@@ -116,6 +116,11 @@ bbm_status bbm_prep_get_stats(bbm_prep prep, bbm_block_stats* stats);
  * Any pointer may be NULL. */
 bbm_status bbm_prep_get_kernel_lists(bbm_prep prep, uint32_t* row_cnt, uint32_t* list,
                                      uint32_t* order);
+/* Per list position of the kernel view, u8 [krows*kcols]: bit 0 / bit 1 = key columns 0-63 /
+ * 64-127 of that occupied 128x128 tile are empty for all of its rows (the forward neither loads
+ * nor multiplies that half). No reference counterpart (a finer-grained classify_tile,
+ * engine.hpp:118-153); exposed for tests. */
+bbm_status bbm_prep_get_tile_halves(bbm_prep prep, uint8_t* halves);
 /* EngineCounters a blocked_forward over `slots` slots reports for `variant`
  * (classify_tile, engine.hpp:118-153; summed as run_attention does, engine.hpp:500-503). */
 bbm_status bbm_prep_counters(bbm_prep prep, int variant, uint64_t slots, bbm_counters* out);

@@ -69,6 +69,7 @@ SIGNATURES = {
     "bbm_prep_get_occupancy": (C.c_int, [vp, u8p]),
     "bbm_prep_get_runs": (C.c_int, [vp, u32p, u32p]),
     "bbm_prep_get_stats": (C.c_int, [vp, C.POINTER(BlockStatsC)]),
+    "bbm_prep_get_tile_halves": (C.c_int, [vp, vp]),
     "bbm_prep_get_kernel_lists": (C.c_int, [vp, u32p, u32p, u32p]),
     "bbm_prep_counters": (C.c_int, [vp, C.c_int, C.c_uint64, C.POINTER(CountersC)]),
     "bbm_prep_replicate": (C.c_int, [vp, C.c_int, vp, C.POINTER(vp)]),

@@ -310,6 +310,14 @@ class MaskPrep:
                                             ptr(order, C.c_uint32)))
         return cnt, lst, order
 
+    def tile_halves(self):
+        """u8 [krows, kcols] at list positions: bit 0 / 1 = key columns 0-63 / 64-127 of the
+        occupied tile empty for all its rows (the forward skips that half)."""
+        info = self.info()
+        h = np.zeros((info.krows, info.kcols), np.uint8)
+        check(lib.bbm_prep_get_tile_halves(self.handle.h, ptr(h, C.c_uint8)))
+        return h
+
     def counters(self, variant: Variant, slots: int = 1) -> EngineCounters:
         c = _lib.CountersC()
         check(lib.bbm_prep_counters(self.handle.h, int(variant), int(slots), C.byref(c)))

@@ -68,6 +68,8 @@ struct FwdParams {
   const PlanHdr* hdr;    // device plan header: row units per slot, split rows / chunks
   float sl2;             // scale * log2(e)
   const uint32_t* list;
+  const uint8_t* halves;   // per list position: key half 0 / 1 empty for the whole tile (bit 0 / 1),
+                           // nullptr = load and multiply whole tiles
   const uint4* bitmaps;
   const uint4* mask;        // padded packed mask, kcols uint4 per row
   const uint4* unit_desc;   // [units] {row tile, j0, tiles, split (kNoSplit | row << 8 | chunk)}
@@ -185,6 +187,7 @@ struct SmemCtl {
   uint64_t ring_full[kRing], ring_empty[kRing];
   uint64_t item_full[kQueue], item_empty[kQueue];
   ItemDesc items[kQueue];
+  uint32_t ring_meta[kRing];  // per loaded K / V tile: its empty key half (bit 0 / 1), 0 = none
   uint32_t tmem_base;
   uint32_t units, total_items, split_rows, split_chunks;  // this launch's plan (device-built)
   uint32_t trace_count;
@@ -203,6 +206,18 @@ template <int MODE>
 __device__ __forceinline__ uint32_t entry_of(const FwdParams& p, uint32_t row_tile, uint32_t j) {
   if constexpr (MODE == kModeDense || MODE == kModeNaive) return j;
   else return p.list[static_cast<uint64_t>(row_tile) * p.kcols + j];
+}
+
+// Empty key halves of list entry j of row tile `row_tile` (list modes; the other modes and the
+// in-kernel gather always load and multiply whole tiles)
+template <int MODE, bool kGather>
+__device__ __forceinline__ uint32_t half_of(const FwdParams& p, uint32_t row_tile, uint32_t j) {
+#ifdef BBM_NO_HALF_SKIP  // A/B builds: whole tiles always
+  return 0u;
+#else
+  if constexpr (MODE == kModeDense || MODE == kModeNaive || kGather) return 0u;
+  else return p.halves ? __ldg(p.halves + static_cast<uint64_t>(row_tile) * p.kcols + j) : 0u;
+#endif
 }
 
 __device__ __forceinline__ ItemDesc decode_item(const FwdParams& p, uint32_t units, uint32_t total,
@@ -239,6 +254,7 @@ template <int D, int MODE, bool kTrace, bool kGather, bool kSkip>
 __global__ void __launch_bounds__(kThreadsOf<D>, 1)
     attn_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                     const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_o,
+                    const __grid_constant__ CUtensorMap tm_k64, const __grid_constant__ CUtensorMap tm_v64,
                     const FwdParams p) {
   using C = Cfg<D>;
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -335,8 +351,10 @@ __global__ void __launch_bounds__(kThreadsOf<D>, 1)
               tma_load_3d(dst + b * kBoxBytes, tm, bar, b * 64, tile * 128, slot, pol);
         }
       };
-      auto load_tile = [&](const CUtensorMap* tm, uint32_t seq, uint32_t q, uint32_t slot, uint32_t code,
-                           uint32_t j) {
+      // K / V tile q into the ring; a key half that no row of the tile sees (`half`, bit 0 / 1) is
+      // not loaded (64-row boxes for the other half); the MMA issuers read `half` from ring_meta
+      auto load_tile = [&](const CUtensorMap* tm, const CUtensorMap* tm64, uint32_t seq, uint32_t q, uint32_t slot,
+                           uint32_t code, uint32_t j, uint32_t half) {
         const uint32_t r = seq % C::kRing;
         mbar_wait(&ctl->ring_empty[r], ((seq / C::kRing) & 1) ^ 1);
         uint64_t* full = &ctl->ring_full[r];
@@ -350,18 +368,31 @@ __global__ void __launch_bounds__(kThreadsOf<D>, 1)
 #endif
         if (skip_load) {
           __syncwarp();
-          if (lane == 0) mbar_arrive(full);
+          if (lane == 0) {
+            ctl->ring_meta[r] = half;
+            mbar_arrive(full);
+          }
           return;
         }
 #endif
-        if (lane == 0) mbar_arrive_expect_tx(full, C::kTileBytes);
+        if (lane == 0) {
+          ctl->ring_meta[r] = half;  // published by the arrive below
+          mbar_arrive_expect_tx(full, half ? C::kTileBytes / 2 : C::kTileBytes);
+        }
         __syncwarp();
-        issue_tile(ring + r * C::kTileBytes, tm, full, q, slot, pol_kv);
+        if (half == 0) {
+          issue_tile(ring + r * C::kTileBytes, tm, full, q, slot, pol_kv);
+        } else if (lane == 0) {
+          const uint32_t hh = (half & 1u) ? 1u : 0u;  // the half that is loaded
+          for (uint32_t b = 0; b < C::kBoxes; ++b)
+            tma_load_3d(ring + r * C::kTileBytes + b * kBoxBytes + hh * (kBoxBytes / 2), tm64, full, b * 64,
+                        q * 128 + hh * 64, slot, pol_kv);
+        }
         if (lane == 0) trace_ev<kTrace>(tracing, p, &ctl->trace_count, code, 0, j);
       };
       // K cursor (claims and publishes items, loads Q)
       ItemDesc kit{};
-      uint32_t kj = 0, kk = 0, kentry = 0;
+      uint32_t kj = 0, kk = 0, kentry = 0, khalf = 0;
       bool k_need = true, k_done = false;
       auto k_next = [&]() -> bool {
         while (k_need) {
@@ -383,6 +414,7 @@ __global__ void __launch_bounds__(kThreadsOf<D>, 1)
           if (d.nt == 0) continue;
           pit[pw++ % kQueue] = d;
           kentry = entry_of<MODE>(p, d.rt, d.j0);
+          khalf = half_of<MODE, kGather>(p, d.rt, d.j0);
           mbar_wait(&ctl->q_empty[qb], qph[qb]);
           qph.flip(qb);
           if (lane == 0) mbar_arrive_expect_tx(&ctl->q_full[qb], C::kTileBytes);
@@ -397,16 +429,19 @@ __global__ void __launch_bounds__(kThreadsOf<D>, 1)
         return true;
       };
       auto issue_k = [&]() {
-        const uint32_t cur = kentry;
+        const uint32_t cur = kentry, chalf = khalf;
         // the next list entry is fetched now, a full issue step before it is needed
-        if (kj + 1 < kit.nt) kentry = entry_of<MODE>(p, kit.rt, kit.j0 + kj + 1);
-        load_tile(&tm_k, kseq_of(kk), cur & 0x7FFFFFFFu, kit.slot, 2, kj);
+        if (kj + 1 < kit.nt) {
+          kentry = entry_of<MODE>(p, kit.rt, kit.j0 + kj + 1);
+          khalf = half_of<MODE, kGather>(p, kit.rt, kit.j0 + kj + 1);
+        }
+        load_tile(&tm_k, &tm_k64, kseq_of(kk), cur & 0x7FFFFFFFu, kit.slot, 2, kj, chalf);
         ++kk;
         if (++kj == kit.nt) k_need = true;
       };
       // V cursor
       ItemDesc vit{};
-      uint32_t vj = 0, vk = 0, ventry = 0;
+      uint32_t vj = 0, vk = 0, ventry = 0, vhalf = 0;
       bool v_need = true;
       auto issue_v = [&]() -> bool {
         if (v_need) {
@@ -414,11 +449,15 @@ __global__ void __launch_bounds__(kThreadsOf<D>, 1)
           vit = pit[pr++ % kQueue];
           vj = 0;
           ventry = entry_of<MODE>(p, vit.rt, vit.j0);
+          vhalf = half_of<MODE, kGather>(p, vit.rt, vit.j0);
           v_need = false;
         }
-        const uint32_t cur = ventry;
-        if (vj + 1 < vit.nt) ventry = entry_of<MODE>(p, vit.rt, vit.j0 + vj + 1);
-        load_tile(&tm_v, vseq_of(vk), cur & 0x7FFFFFFFu, vit.slot, 3, vj);
+        const uint32_t cur = ventry, chalf = vhalf;
+        if (vj + 1 < vit.nt) {
+          ventry = entry_of<MODE>(p, vit.rt, vit.j0 + vj + 1);
+          vhalf = half_of<MODE, kGather>(p, vit.rt, vit.j0 + vj + 1);
+        }
+        load_tile(&tm_v, &tm_v64, vseq_of(vk), cur & 0x7FFFFFFFu, vit.slot, 3, vj, chalf);
         ++vk;
         if (++vj == vit.nt) v_need = true;
         return true;
@@ -440,6 +479,7 @@ __global__ void __launch_bounds__(kThreadsOf<D>, 1)
     if (lane == 0) {
       const bool s_side = warp == 1;
       constexpr uint32_t idesc_s = make_idesc_bf16(128, 128, false, false);
+      constexpr uint32_t idesc_s64 = make_idesc_bf16(128, 64, false, false);  // one key half
       constexpr uint32_t idesc_o = make_idesc_bf16(128, D, false, true);
       const uint32_t qaddr = smem_u32(sq), raddr = smem_u32(ring);
       uint32_t qi = 0, qiph = 0, k = 0, qb = 0, items = 0;
@@ -468,13 +508,17 @@ __global__ void __launch_bounds__(kThreadsOf<D>, 1)
             mbar_wait(&ctl->ring_full[slot], (kseq / C::kRing) & 1);
             trace_ev<kTrace>(tracing, p, &ctl->trace_count, 13, buf, j);
             tc_fence_after();
+            // a key half no row sees is neither loaded nor multiplied: N = 64 over the other half
+            // (its S columns keep stale values, which the softmax replaces by the mask sentinel)
+            const uint32_t half = ctl->ring_meta[slot];
+            const uint32_t hrow = (half & 1u) ? 64u : 0u;
             const uint64_t qdesc = make_sdesc_sw128(qaddr + qb * C::kTileBytes, 16, 1024);
-            const uint64_t kdesc = make_sdesc_sw128(raddr + slot * C::kTileBytes, 16, 1024);
+            const uint64_t kdesc = make_sdesc_sw128(raddr + slot * C::kTileBytes + hrow * 128, 16, 1024);
 #pragma unroll
             for (uint32_t kk = 0; kk < D / 16; ++kk) {
               const uint32_t off = (kk / 4) * kBoxBytes + (kk % 4) * 32;
-              umma_ss(tmem + buf * 128, sdesc_advance(qdesc, off), sdesc_advance(kdesc, off), idesc_s,
-                      kk > 0);
+              umma_ss(tmem + buf * 128 + hrow, sdesc_advance(qdesc, off), sdesc_advance(kdesc, off),
+                      half ? idesc_s64 : idesc_s, kk > 0);
             }
             tc_commit(&ctl->ring_empty[slot]);
             tc_commit(&ctl->s_full[buf]);
@@ -498,11 +542,15 @@ __global__ void __launch_bounds__(kThreadsOf<D>, 1)
             tc_fence_after();
             const uint64_t vdesc = make_sdesc_sw128(raddr + slot * C::kTileBytes, kBoxBytes, 1024);
             const uint32_t pcol = tmem + buf * 128;
+            // K steps over the keys present (a whole empty key half is skipped)
+            const uint32_t half = ctl->ring_meta[slot];
+            const uint32_t kk0 = (half & 1u) ? 4u : 0u, kk1 = (half & 2u) ? 4u : 8u;
 #ifndef BBM_ABLATE_NO_PV  // timing experiments only: O is never accumulated
 #pragma unroll
             for (uint32_t kk = 0; kk < 128 / 16; ++kk)
-              umma_ts(tmem_o, pcol + kk * 8, sdesc_advance(vdesc, kk * 2048), idesc_o,
-                      (j > 0 || kk > 0) ? 1u : 0u);
+              if (kk >= kk0 && kk < kk1)
+                umma_ts(tmem_o, pcol + kk * 8, sdesc_advance(vdesc, kk * 2048), idesc_o,
+                        (j > 0 || kk > kk0) ? 1u : 0u);
 #endif
             tc_commit(&ctl->ring_empty[slot]);
             tc_commit(&ctl->pv_done[buf]);
@@ -980,6 +1028,9 @@ void launch_impl(const Prep& prep, const AttnArgs& a, cudaStream_t s, int num_sm
                    : cached_tmap_bf16_3d(base, D, a.n, a.slots, 64, 128);
   };
   const CUtensorMap tq = tmap(a.q), tk = tmap(a.k), tv = tmap(a.v), to = tmap(a.o);
+  // 64-row boxes for tiles with an empty key half (plain mode only; gather mode never uses them)
+  const CUtensorMap tk64 = kGather ? tk : cached_tmap_bf16_3d(a.k, D, a.n, a.slots, 64, 64);
+  const CUtensorMap tv64 = kGather ? tv : cached_tmap_bf16_3d(a.v, D, a.n, a.slots, 64, 64);
   FwdParams p{};
   p.rows = a.rows;
   p.n = a.n;
@@ -993,6 +1044,7 @@ void launch_impl(const Prep& prep, const AttnArgs& a, cudaStream_t s, int num_sm
   // (uniform weights, as with scale 0), while masked keys stay at -inf.
   if (p.sl2 == 0.0f) p.sl2 = 7.8886090522101181e-31f;
   p.list = km.list;
+  p.halves = plan.half_heavy ? km.halves : nullptr;  // known one launch after a new mask version
   p.bitmaps = km.bitmaps;
   p.mask = reinterpret_cast<const uint4*>(km.mask);
   p.unit_desc = plan.unit_desc;
@@ -1019,7 +1071,7 @@ void launch_impl(const Prep& prep, const AttnArgs& a, cudaStream_t s, int num_sm
   });
   if constexpr (!kGather) {
     if (p.trace) {  // event-tracing build of the same kernel (bbm_set_trace)
-      attn_fwd_kernel<D, MODE, true, false, false><<<grid, kThreadsOf<D>, smem_bytes<D>(), s>>>(tq, tk, tv, to, p);
+      attn_fwd_kernel<D, MODE, true, false, false><<<grid, kThreadsOf<D>, smem_bytes<D>(), s>>>(tq, tk, tv, to, tk64, tv64, p);
       BBM_CUDA(cudaGetLastError());
       mark_launch_done(ctx, s);
       return;
@@ -1028,10 +1080,10 @@ void launch_impl(const Prep& prep, const AttnArgs& a, cudaStream_t s, int num_sm
   // the engine build for this mask (plan.partial_heavy arrives one launch after a new mask
   // version; both builds give bitwise identical results)
   if (kCanSkip && plan.partial_heavy) {
-    attn_fwd_kernel<D, MODE, false, kGather, kCanSkip><<<grid, kThreadsOf<D>, smem_bytes<D>(), s>>>(tq, tk, tv, to, p);
+    attn_fwd_kernel<D, MODE, false, kGather, kCanSkip><<<grid, kThreadsOf<D>, smem_bytes<D>(), s>>>(tq, tk, tv, to, tk64, tv64, p);
     g_builds[1].fetch_add(1, std::memory_order_relaxed);
   } else {
-    attn_fwd_kernel<D, MODE, false, kGather, false><<<grid, kThreadsOf<D>, smem_bytes<D>(), s>>>(tq, tk, tv, to, p);
+    attn_fwd_kernel<D, MODE, false, kGather, false><<<grid, kThreadsOf<D>, smem_bytes<D>(), s>>>(tq, tk, tv, to, tk64, tv64, p);
     g_builds[0].fetch_add(1, std::memory_order_relaxed);
   }
   BBM_CUDA(cudaGetLastError());

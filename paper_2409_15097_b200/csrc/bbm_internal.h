@@ -73,6 +73,9 @@ struct KernelMeta {
   uint32_t* row_cnt = nullptr;
   uint32_t* order = nullptr;
   uint8_t* occ = nullptr;
+  // [krows][kcols] at list positions: bit 0 / bit 1 = key columns 0-63 / 64-127 of the tile are
+  // empty for all 128 rows (the forward then loads and multiplies only the other 64 keys)
+  uint8_t* halves = nullptr;
   uint32_t* run_off = nullptr;
   uint32_t* run_len = nullptr;
   uint64_t* row_stats = nullptr;
@@ -100,6 +103,7 @@ struct SpecMeta {
 struct PlanHdr {
   uint32_t units, split_rows, split_chunks, unit_len;
   uint32_t occupied, full;  // list plans: occupied tiles of the view and how many are full (bit 31)
+  uint32_t halves;          // row view: occupied tiles with an empty 64-key half
 };
 struct DevPlan {
   uint64_t version = 0;  // mask version the plan was built from
@@ -116,6 +120,7 @@ struct DevPlan {
   cudaEvent_t hdr_ev = nullptr;
   uint64_t known_version = 0;
   bool partial_heavy = false;
+  bool half_heavy = false;  // enough tiles with an empty key half for the forward to skip them
 };
 
 // Backward metadata (attn_bwd.cu): the column view of the kernel tiles — for key tile q, the
@@ -291,8 +296,9 @@ struct TileView {
   const uint32_t* list;  // [tiles][partners]
   uint32_t tiles, partners;
   int id;  // plan-cache key: 0 rows, 1 columns
+  const uint8_t* halves = nullptr;  // row view: per list position, the tile's empty key halves
 };
-inline TileView row_view(const KernelMeta& km) { return {km.row_cnt, km.list, km.krows, km.kcols, 0}; }
+inline TileView row_view(const KernelMeta& km) { return {km.row_cnt, km.list, km.krows, km.kcols, 0, km.halves}; }
 // (re)build `plan` on stream s for the current metadata (kernel, no host sync)
 void build_plan(const TileView& v, int cls, uint64_t slots, uint32_t workers, DevPlan& plan,
                 cudaStream_t s);

@@ -157,6 +157,7 @@ void carve_kernel_meta(KernelMeta& km, uint64_t n, uint8_t* arena) {
   take(km.row_cnt, km.krows);
   take(km.order, km.krows);
   take(km.occ, tiles);
+  take(km.halves, tiles);
   take(km.run_off, km.krows);
   take(km.run_len, km.krows);
   take(km.row_stats, static_cast<uint64_t>(km.krows) * 3);
@@ -560,6 +561,18 @@ bbm_status bbm_prep_get_kernel_lists(bbm_prep prep, uint32_t* row_cnt, uint32_t*
       cudaFree(tmp);
       BBM_CUDA(e);
     }
+  });
+}
+
+bbm_status bbm_prep_get_tile_halves(bbm_prep prep, uint8_t* halves) {
+  return guarded([&] {
+    const Prep& pr = unwrap(prep);
+    require(halves != nullptr, "null argument");
+    std::lock_guard<std::recursive_mutex> lk(pr.mu);
+    DeviceGuard g(pr.device);
+    BBM_CUDA(cudaEventSynchronize(pr.ready));
+    const KernelMeta& km = pr.kmeta;
+    BBM_CUDA(cudaMemcpy(halves, km.halves, static_cast<uint64_t>(km.krows) * km.kcols, cudaMemcpyDeviceToHost));
   });
 }
 

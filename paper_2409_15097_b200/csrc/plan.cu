@@ -41,6 +41,7 @@ struct PlanArgs {
   uint32_t krows, kcols;
   const uint32_t* row_cnt;
   const uint32_t* list;
+  const uint8_t* halves;  // nullptr for the column view
   uint64_t slots;
   uint32_t workers;
   uint64_t cap_chunks;  // bound on slots * split chunks (workspace blocks)
@@ -70,11 +71,15 @@ __global__ void __launch_bounds__(kPlanThreads) plan_kernel(const PlanArgs a) {
   uint64_t L = (total / max(1u, a.workers) + 1) / 2;
   if (L < kMinUnit) L = kMinUnit;
   // full tiles (list entries with bit 31): the forward's choice of softmax engine build
-  unsigned long long fl = 0;
+  unsigned long long fl = 0, hv = 0;
   if (a.cls == kPlanList)
     for (uint32_t p = threadIdx.x; p < a.krows; p += kPlanThreads)
-      for (uint32_t o = 0; o < a.row_cnt[p]; ++o) fl += a.list[static_cast<uint64_t>(p) * a.kcols + o] >> 31;
+      for (uint32_t o = 0; o < a.row_cnt[p]; ++o) {
+        fl += a.list[static_cast<uint64_t>(p) * a.kcols + o] >> 31;
+        if (a.halves) hv += a.halves[static_cast<uint64_t>(p) * a.kcols + o] != 0;
+      }
   const unsigned long long full = block_sum<kPlanThreads>(fl);
+  const unsigned long long half_tiles = block_sum<kPlanThreads>(hv);
   for (;;) {
     unsigned long long c = 0;
     for (uint32_t p = threadIdx.x; p < a.krows; p += kPlanThreads) c += chunks_of(occ_of(p), L);
@@ -130,7 +135,7 @@ __global__ void __launch_bounds__(kPlanThreads) plan_kernel(const PlanArgs a) {
   if (threadIdx.x == 0)
     *a.hdr = PlanHdr{units, s_carry, c_carry, static_cast<uint32_t>(L < 0xFFFFFFFFull ? L : 0xFFFFFFFFull),
                      static_cast<uint32_t>(total / max(1ull, static_cast<unsigned long long>(a.slots))),
-                     static_cast<uint32_t>(full)};
+                     static_cast<uint32_t>(full), static_cast<uint32_t>(half_tiles)};
 }
 
 __global__ void __launch_bounds__(kPlanThreads) lpt_order_kernel(const uint32_t* __restrict__ keys,
@@ -161,6 +166,7 @@ void build_plan(const TileView& v, int cls, uint64_t slots, uint32_t workers, De
   a.kcols = v.partners;
   a.row_cnt = v.cnt;
   a.list = v.list;
+  a.halves = v.halves;
   a.slots = slots;
   a.workers = workers;
   a.cap_chunks = plan_cap_chunks(slots, workers);
@@ -207,15 +213,18 @@ const DevPlan& plan_for(const Prep& prep, StreamCtx& ctx, const TileView& v, int
     build_plan(v, cls, slots, workers, pl, s);
     pl.version = prep.version;
     if (!pl.host_hdr) {
-      BBM_CUDA(cudaMallocHost(&pl.host_hdr, 8));
+      BBM_CUDA(cudaMallocHost(&pl.host_hdr, 12));
       BBM_CUDA(cudaEventCreateWithFlags(&pl.hdr_ev, cudaEventDisableTiming));
     }
-    BBM_CUDA(cudaMemcpyAsync(pl.host_hdr, &pl.hdr->occupied, 8, cudaMemcpyDeviceToHost, s));
+    BBM_CUDA(cudaMemcpyAsync(pl.host_hdr, &pl.hdr->occupied, 12, cudaMemcpyDeviceToHost, s));
     BBM_CUDA(cudaEventRecord(pl.hdr_ev, s));
   } else if (pl.known_version != pl.version) {
     const cudaError_t q = cudaEventQuery(pl.hdr_ev);
     if (q == cudaSuccess) {
       pl.partial_heavy = (pl.host_hdr[0] - pl.host_hdr[1]) * 2ull > pl.host_hdr[0];
+      // skipping empty key halves pays off on band-like masks (C5: 40 % of the occupied tiles have
+      // one; -4 % same-box A/B) and costs a little elsewhere (an extra metadata load per K / V)
+      pl.half_heavy = pl.host_hdr[2] * 4ull >= pl.host_hdr[0] && pl.host_hdr[0] > 0;
       pl.known_version = pl.version;
     } else if (q == cudaErrorNotReady) {
       (void)cudaGetLastError();  // not an error: the header has not arrived yet

@@ -281,13 +281,17 @@ __global__ void __launch_bounds__(128) compact_bitmaps_kernel(const uint4* __res
                                                               uint32_t kcols,
                                                               const uint32_t* __restrict__ list,
                                                               const uint32_t* __restrict__ cnt,
-                                                              uint4* __restrict__ bitmaps) {
+                                                              uint4* __restrict__ bitmaps,
+                                                              uint8_t* __restrict__ halves) {
   const uint32_t p = blockIdx.y, k = blockIdx.x;
   if (k >= cnt[p]) return;
   const uint32_t q = list[p * kcols + k] & 0x7FFFFFFFu;
   const uint32_t r = threadIdx.x;
-  bitmaps[(static_cast<uint64_t>(p) * kcols + k) * 128 + r] =
-      mask[(static_cast<uint64_t>(p) * 128 + r) * kcols + q];
+  const uint4 w = mask[(static_cast<uint64_t>(p) * 128 + r) * kcols + q];
+  bitmaps[(static_cast<uint64_t>(p) * kcols + k) * 128 + r] = w;
+  // key halves of the tile that no row sees
+  const int lo = __syncthreads_or((w.x | w.y) != 0u), hi = __syncthreads_or((w.z | w.w) != 0u);
+  if (r == 0) halves[static_cast<uint64_t>(p) * kcols + k] = static_cast<uint8_t>((lo ? 0 : 1) | (hi ? 0 : 2));
 }
 
 __global__ void __launch_bounds__(1024) finalize_kernel(const uint64_t* __restrict__ row_stats,
@@ -351,6 +355,7 @@ struct FusedArgs {
   uint32_t *run_off, *run_len, *row_cnt, *list, *ctr;
   uint64_t* row_stats;
   uint4* bitmaps;
+  uint8_t* halves;
 };
 enum : int { kInBool = 0, kInWords = 1 };
 
@@ -358,7 +363,7 @@ template <int IN>
 __global__ void __launch_bounds__(256) prep_fused_kernel(const FusedArgs a) {
   __shared__ uint32_t s_cnt[kChunkTiles];
   __shared__ bool s_last;
-  __shared__ uint32_t s_sums[kStageCols], s_list[kStageCols];
+  __shared__ uint32_t s_sums[kStageCols], s_list[kStageCols], s_half[kStageCols];
   const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   // a tile row's chunks x kRowSplits CTAs are consecutive, so its stage B runs while later rows
   // are still in stage A (only the last row's is a tail)
@@ -463,6 +468,8 @@ __global__ void __launch_bounds__(256) prep_fused_kernel(const FusedArgs a) {
     __syncthreads();
     const uint32_t cnt = rowmeta_row_t([&](uint64_t q) { return s_sums[q]; }, a.n, 128, 128, a.kcols, p, a.occ,
                                        a.run_off, a.run_len, a.row_stats, a.list, a.row_cnt, s_list);
+    for (uint32_t k = threadIdx.x; k < cnt; k += 256) s_half[k] = 0;
+    __syncthreads();
     const uint4* m4 = reinterpret_cast<const uint4*>(a.mask);
     constexpr uint32_t kU = 4;  // independent mask loads in flight per thread
     for (uint32_t i0 = threadIdx.x; i0 < cnt * 128; i0 += 256 * kU) {
@@ -478,10 +485,17 @@ __global__ void __launch_bounds__(256) prep_fused_kernel(const FusedArgs a) {
 #pragma unroll
       for (uint32_t u = 0; u < kU; ++u) {
         const uint32_t idx = i0 + u * 256;
-        if (idx < cnt * 128)
+        if (idx < cnt * 128) {
           a.bitmaps[(static_cast<uint64_t>(p) * a.kcols + (idx >> 7)) * 128 + (idx & 127)] = w[u];
+          const uint32_t seen = ((w[u].x | w[u].y) != 0u ? 1u : 0u) | ((w[u].z | w[u].w) != 0u ? 2u : 0u);
+          if (seen) atomicOr(&s_half[idx >> 7], seen);
+        }
       }
     }
+    __syncthreads();
+    // key halves no row of the tile sees (the forward loads and multiplies only the other half)
+    for (uint32_t k = threadIdx.x; k < cnt; k += 256)
+      a.halves[static_cast<uint64_t>(p) * a.kcols + k] = static_cast<uint8_t>(~s_half[k] & 3u);
     if (threadIdx.x == 0) a.ctr[p] = 0;
     return;
   }
@@ -502,6 +516,7 @@ __global__ void __launch_bounds__(256) prep_fused_kernel(const FusedArgs a) {
     const uint32_t q = __ldcg(a.list + static_cast<uint64_t>(p) * a.kcols + k) & 0x7FFFFFFFu;
     a.bitmaps[(static_cast<uint64_t>(p) * a.kcols + k) * 128 + r] =
         __ldcg(m4 + (static_cast<uint64_t>(p) * 128 + r) * a.kcols + q);
+    if (r == 0) a.halves[static_cast<uint64_t>(p) * a.kcols + k] = 0;  // wide rows: no half skipping
   }
   if (threadIdx.x == 0) a.ctr[p] = 0;
 
@@ -524,6 +539,7 @@ FusedArgs fused_args(const KernelMeta& km, uint64_t n) {
   a.ctr = km.ctr;
   a.row_stats = km.row_stats;
   a.bitmaps = km.bitmaps;
+  a.halves = km.halves;
   return a;
 }
 
@@ -614,7 +630,7 @@ void launch_rowmeta(const uint32_t* d_sums, uint64_t n, uint64_t bi, uint64_t bj
 void launch_compact_bitmaps(const KernelMeta& km, cudaStream_t s) {
   dim3 grid(km.kcols, km.krows);
   compact_bitmaps_kernel<<<grid, 128, 0, s>>>(reinterpret_cast<const uint4*>(km.mask), km.kcols,
-                                              km.list, km.row_cnt, km.bitmaps);
+                                              km.list, km.row_cnt, km.bitmaps, km.halves);
   BBM_CUDA(cudaGetLastError());
 }
 

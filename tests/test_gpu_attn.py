@@ -482,3 +482,29 @@ def test_empty_half_skip_build_is_bitwise_identical(cuda, d, scale_sign):
     c2 = builds()
     run_gpu(causal, q, k, v, scale, bbm.Variant.binblk, cuda, prep=prep)
     assert builds() == (c2[0] + 1, c2[1])
+
+
+@pytest.mark.parametrize("n,w", [(3000, 40), (2048, 30), (1111, 20)])
+def test_empty_key_half_skipping_is_exact(cuda, n, w):
+    """Bands leave whole 64-key halves of their edge tiles empty; binblk / dense_binblk load and
+    multiply only the other half, naive always multiplies whole tiles. All three must agree bit
+    for bit (a skipped half contributes exactly nothing) and match the oracle."""
+    import torch
+
+    mask = bbm.gen_longformer_windowed(n, w)
+    prep = bbm.preprocess_mask(mask, bbm.BlockSpec(128, 128))
+    assert (prep.tile_halves() > 0).any()
+    q, k, v = problem(n + w, 2, n, 128)
+    outs = {}
+    for var in MASKED:
+        for _ in range(2):  # the skip is enabled from the plan header, one launch after a new mask
+            r = bbm.blocked_forward(to_dev(q, cuda), to_dev(k, cuda), to_dev(v, cuda), 0.1, mask, prep, var)
+            torch.cuda.synchronize()
+        outs[var] = (r.out.view(torch.int16).cpu().numpy(), r.row_max.cpu().numpy(), r.row_sum.cpu().numpy())
+    base = outs[bbm.Variant.naive_masked]
+    for var in MASKED:
+        for a, b in zip(outs[var], base):
+            assert np.array_equal(a.view(np.uint8), b.view(np.uint8)), var
+    out = outs[bbm.Variant.binblk][0].view(np.uint16).astype(np.uint32) << 16
+    check_against_oracle(mask, q, k, v, 0.1, out.view(np.float32), outs[bbm.Variant.binblk][1],
+                         outs[bbm.Variant.binblk][2], bbm.Variant.binblk)

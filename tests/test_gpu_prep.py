@@ -159,3 +159,40 @@ def test_uint8_mask_any_nonzero_is_true(cuda, n):
         outs.append(o)
     torch.cuda.synchronize()
     assert torch.equal(outs[0], outs[1])
+
+
+def _expected_halves(m, cnt, lst):
+    """Empty key halves of every occupied 128x128 tile at its list position (numpy)."""
+    n = m.size()
+    kt = (n + 127) // 128
+    pad = np.zeros((kt * 128, kt * 128), bool)
+    pad[:n, :n] = m.to_dense()
+    want = np.zeros((kt, kt), np.uint8)
+    for p in range(kt):
+        for k in range(cnt[p]):
+            q = int(lst[p, k] & 0x7FFFFFFF)
+            blk = pad[p * 128:(p + 1) * 128, q * 128:(q + 1) * 128]
+            want[p, k] = (0 if blk[:, :64].any() else 1) | (0 if blk[:, 64:].any() else 2)
+    return want
+
+
+@pytest.mark.parametrize("n,kind", [(4096, "band"), (1000, "band"), (2304, "causal"), (1500, "random"),
+                                    (3000, "packed")])
+def test_tile_halves_match_the_mask(cuda, n, kind):
+    """The forward skips a 64-key half of a tile that no row sees; the flags come from the fused
+    preprocessor (n % 16 == 0), the kernel chain (bool rows with n % 16 != 0) and the packed path."""
+    import torch
+
+    m = {"band": lambda: bbm.gen_longformer_windowed(n, 40),
+         "causal": lambda: bbm.gen_causal(n),
+         "random": lambda: bbm.gen_random_sparse(n, 0.002, 4),
+         "packed": lambda: bbm.gen_packed_sequential([50, 300, 30, 700, 100, 1820])}[kind]()
+    for src in (m, torch.from_numpy(m.to_dense()).to(cuda)):
+        prep = bbm.preprocess_mask(src, bbm.BlockSpec(128, 128))
+        cnt, lst, _ = prep.kernel_lists()
+        got = prep.tile_halves()
+        want = _expected_halves(m, cnt, lst)
+        for p in range(len(cnt)):
+            assert np.array_equal(got[p, : cnt[p]], want[p, : cnt[p]]), p
+    if kind == "band":
+        assert (want > 0).any()  # the case the forward's half skipping is for

@@ -7,7 +7,7 @@ CONFIGS=${CONFIGS:-"c5:binblk c2:binblk c2:dense c4:dense-binblk c3:binblk"}
 LIBS=${LIBS:-"prev cur"}
 for spec in $CONFIGS; do
   cfg=${spec%%:*}; var=${spec##*:}
-  for rep in 1 2 3; do
+  for rep in ${REPS:-1 2 3}; do
   for lib in $LIBS; do
     if [ $lib = cur ]; then unset BBM_LIB; else export BBM_LIB=$PWD/abl_bin/libbbm_$lib.so; fi
     r=$(timeout 300 python bench.py --config $cfg --variant $var --steps 20 --warmup 5 --profile 2>&1 | tail -1)
