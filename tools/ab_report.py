@@ -9,6 +9,10 @@ for line in open("gpurun_out/ab.log"):
         d = json.loads(parts[3])
     except Exception:
         continue
-    res[(parts[0], parts[1], parts[2])].append(d["ms_per_step"])
+    mhz = (d.get("clocks") or {}).get("sm_mhz")
+    res[(parts[0], parts[1], parts[2])].append((d["ms_per_step"], mhz))
 for k, v in sorted(res.items()):
-    print(k, ["%.4f" % x for x in v], "mean %.4f" % (sum(v) / len(v)))
+    ms = [x for x, _ in v]
+    clk = [c for _, c in v if c]
+    print(k, ["%.4f" % x for x in ms], "mean %.4f" % (sum(ms) / len(ms)),
+          ("MHz %s" % clk) if clk else "")
