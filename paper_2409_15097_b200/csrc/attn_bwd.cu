@@ -72,6 +72,7 @@ struct BwdParams {
   const uint32_t* list;       // [tiles][stride] partner entries, bit 31 = full
   uint32_t list_stride;
   const uint4* bitmaps;       // list-position tile-major bits (row bitmaps | transposed)
+  const uint8_t* halves;      // dq: per list position, the tile's empty 64-key halves (nullptr = none)
   const float* lse2;          // [slots][rows_pad], NEGATED (-lse2, rowstats_kernel)
   const float* delta;         // [slots][rows_pad], NEGATED (-delta)
   uint32_t rows_pad;          // krows * 128
@@ -125,6 +126,7 @@ struct BwdCtl {
   uint64_t ring_full[4], ring_empty[4];
   uint64_t item_full[kQueue], item_empty[kQueue];
   ItemDesc items[kQueue];
+  uint32_t stage_halves[4];  // per ring stage: the streamed tile's empty partner halves (bit h)
   uint32_t tmem_base;
   uint32_t units, total_items, split_rows, split_chunks;  // this launch's plan
   uint32_t bcast;
@@ -250,9 +252,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         for (uint32_t j = 0; j < d.nt; ++j) {
           const uint32_t u = bwd_entry(p, d.tile, d.j0 + j) & 0x7FFFFFFFu;
+          uint32_t hv = 0;
+          if constexpr (SIDE == kSideDQ)
+            if (p.halves) hv = __ldg(p.halves + static_cast<uint64_t>(d.tile) * p.list_stride + d.j0 + j);
           mbar_wait(&ctl->ring_empty[r], rph);
           uint64_t* full = &ctl->ring_full[r];
           uint8_t* st = ring + r * C::kStageAlloc;
+          ctl->stage_halves[r] = hv;  // published by the arrive below
           mbar_arrive_expect_tx(full, C::kStageBytes);
           for (uint32_t b = 0; b < C::kBoxes; ++b) {
             tma_load_3d(st + b * kBoxBytes, &tm_s0, full, b * 64, u * 128, d.slot, pol_stream);
@@ -284,7 +290,13 @@ __global__ void __launch_bounds__(kThreads, 1)
       PhaseBits aph{0x3u};  // acc_empty phases (both sets start free)
       PhaseBits pph{0u};
       // S_h = f0 s0[64h..]^T, dP_h = f1 s1[64h..]^T: both K-major, K = D, N = 64 partner rows
+      // a partner half that no row of the tile sees (dq: an empty 64-key half) is not multiplied:
+      // its S / dP columns keep stale values whose P / dS no accumulate MMA reads
       auto issue_sdp = [&](uint32_t h, uint32_t stage) {
+        if ((ctl->stage_halves[stage] >> h) & 1u) {
+          tc_commit(&ctl->s_full[h]);
+          return;
+        }
         const uint32_t sbase = raddr + stage * C::kStageAlloc + h * 8192;
         const uint64_t s0 = make_sdesc_sw128(sbase, 16, 1024), s1 = make_sdesc_sw128(sbase + C::kTileBytes, 16, 1024);
 #pragma unroll
@@ -301,7 +313,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       };
       // accumulate MMAs of half h: K steps 4h..4h+3 (partner rows 64h..64h+63). Packed bf16 A
       // operand: half h's 32 columns at [64h, 64h+32) of its region -> column (kk/4)*64 + (kk%4)*8
-      auto issue_acc = [&](uint32_t h, uint32_t stage, uint32_t j, uint32_t acc0) {
+      bool started = false;  // the item's first accumulate MMA overwrites, the others accumulate
+      auto issue_acc = [&](uint32_t h, uint32_t stage, uint32_t acc0) {
+        if ((ctl->stage_halves[stage] >> h) & 1u) return;
         const uint32_t sbase = raddr + stage * C::kStageAlloc;
         const uint64_t b0 = make_sdesc_sw128(sbase, kBoxBytes, 1024);
         const uint64_t b1 = make_sdesc_sw128(sbase + C::kTileBytes, kBoxBytes, 1024);
@@ -309,11 +323,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (uint32_t q = 0; q < 4; ++q) {
           const uint32_t kk = 4 * h + q;
           const uint32_t acol = (kk / 4) * 64 + (kk % 4) * 8;
-          const uint32_t acc = (j > 0 || kk > 0) ? 1u : 0u;
+          const uint32_t acc = started ? 1u : 0u;
           // dQ += dS K_j  |  dK += dS^T Q_i   (B = streamed tile 0, MN-major)
           umma_ts(tmem + acc0, tmem + 128 + acol, sdesc_advance(b0, kk * 2048), idesc_acc, acc);
           if constexpr (SIDE == kSideDKDV)  // dV += P^T dO_i   (B = streamed tile 1)
             umma_ts(tmem + acc0 + D, tmem + acol, sdesc_advance(b1, kk * 2048), idesc_acc, acc);
+          started = true;
         }
       };
       for (;;) {
@@ -334,6 +349,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         trace_ev<kTrace>(tracing, p, &ctl->trace_count, 40, 1, 0);
         if (it.nt == 1) tc_commit(&ctl->fixed_empty);
         const uint32_t ab = C::kDefer ? (items++ & 1u) : 0u;  // this item's accumulator set
+        started = false;
         const uint32_t acc0 = C::kAcc0 + ab * C::kAccSet;
         for (uint32_t j = 0; j < it.nt; ++j) {
           const uint32_t rn = r + 1 == C::kStages ? 0 : r + 1;
@@ -347,7 +363,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               aph.flip(ab);
             }
             tc_fence_after();
-            issue_acc(h, r, j, acc0);
+            issue_acc(h, r, acc0);
             trace_ev<kTrace>(tracing, p, &ctl->trace_count, 41, h, j);
             if (h == 1) tc_commit(&ctl->ring_empty[r]);  // both halves of tile j consumed
             if (j + 1 < it.nt) {
@@ -731,6 +747,11 @@ void launch_side(const Prep& prep, StreamCtx& ctx, const BwdArgs& a, const float
     p.list = km.list;
     p.list_stride = km.kcols;
     p.bitmaps = km.bitmaps;
+#ifdef BBM_NO_HALF_SKIP  // A/B builds: whole tiles always
+    p.halves = nullptr;
+#else
+    p.halves = plan.half_heavy ? km.halves : nullptr;  // known one launch after a new mask version
+#endif
     p.ctr = ctx.ctr + 2;
     p.out0 = static_cast<__nv_bfloat16*>(a.dq);
   } else {

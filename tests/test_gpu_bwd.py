@@ -192,3 +192,27 @@ def test_split_long_lists_match_oracle_and_stay_deterministic(cuda, spec, n, d):
             assert np.array_equal(got.float().cpu().numpy(), want), var
     fd, bd = fwd_bwd(mask, q, k, v, g, scale, bbm.Variant.dense, cuda, prep=prep)
     check(mask, q, k, v, g, scale, bbm.Variant.dense, fd, bd)
+
+
+@pytest.mark.parametrize("n,w,d", [(3000, 40, 128), (1111, 20, 64)])
+def test_dq_empty_key_half_skipping_is_exact(cuda, n, w, d):
+    """dq skips the S / dP and accumulate MMAs of a 64-key half that no row of the tile sees,
+    from the launch after the plan header reached the host: the first backward (no skipping)
+    and later ones (skipping) must agree bit for bit, and match the oracle."""
+    import torch
+
+    mask = bbm.gen_longformer_windowed(n, w)
+    prep = bbm.preprocess_mask(mask, bbm.BlockSpec(128, 128))
+    cnt, _, _ = prep.kernel_lists()
+    h = prep.tile_halves()
+    occ = sum(int(c) for c in cnt)
+    assert sum(int((h[p, :c] > 0).sum()) for p, c in enumerate(cnt)) * 4 >= occ  # skip enabled
+    q, k, v, g = problem(n, 2, n, d)
+    tq, tk, tv, tg = (to_dev(a, cuda) for a in (q, k, v, g))
+    f = bbm.blocked_forward(tq, tk, tv, 0.09, mask, prep, bbm.Variant.binblk)
+    runs = [bbm.blocked_backward(tq, tk, tv, 0.09, mask, prep, bbm.Variant.binblk, f, tg) for _ in range(3)]
+    torch.cuda.synchronize()
+    for b in runs[1:]:
+        for a, c in zip((runs[0].dq, runs[0].dk, runs[0].dv), (b.dq, b.dk, b.dv)):
+            assert torch.equal(a, c)
+    check(mask, q, k, v, g, 0.09, bbm.Variant.binblk, f, runs[-1], slots=[1])

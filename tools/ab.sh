@@ -10,7 +10,7 @@ for spec in $CONFIGS; do
   for rep in ${REPS:-1 2 3}; do
   for lib in $LIBS; do
     if [ $lib = cur ]; then unset BBM_LIB; else export BBM_LIB=$PWD/abl_bin/libbbm_$lib.so; fi
-    r=$(timeout 300 python bench.py --config $cfg --variant $var --steps 20 --warmup 5 ${ABMODE:---profile} 2>&1 | tail -1)
+    r=$(timeout 300 python bench.py --config $cfg --variant $var --steps 20 --warmup 5 ${ABPASS:+--pass $ABPASS} ${ABMODE:---profile} 2>&1 | tail -1)
     echo "$cfg $var $lib $r" | tee -a gpurun_out/ab.log
   done
   done
