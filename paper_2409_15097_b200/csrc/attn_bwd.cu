@@ -72,7 +72,8 @@ struct BwdParams {
   const uint32_t* list;       // [tiles][stride] partner entries, bit 31 = full
   uint32_t list_stride;
   const uint4* bitmaps;       // list-position tile-major bits (row bitmaps | transposed)
-  const uint8_t* halves;      // dq: per list position, the tile's empty 64-key halves (nullptr = none)
+  const uint8_t* halves;      // per list position: the tile's empty 64-row partner halves (dq: keys,
+                              // dkdv: queries; nullptr = multiply whole tiles)
   const float* lse2;          // [slots][rows_pad], NEGATED (-lse2, rowstats_kernel)
   const float* delta;         // [slots][rows_pad], NEGATED (-delta)
   uint32_t rows_pad;          // krows * 128
@@ -252,9 +253,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         for (uint32_t j = 0; j < d.nt; ++j) {
           const uint32_t u = bwd_entry(p, d.tile, d.j0 + j) & 0x7FFFFFFFu;
-          uint32_t hv = 0;
-          if constexpr (SIDE == kSideDQ)
-            if (p.halves) hv = __ldg(p.halves + static_cast<uint64_t>(d.tile) * p.list_stride + d.j0 + j);
+          const uint32_t hv =
+              p.halves ? __ldg(p.halves + static_cast<uint64_t>(d.tile) * p.list_stride + d.j0 + j) : 0u;
           mbar_wait(&ctl->ring_empty[r], rph);
           uint64_t* full = &ctl->ring_full[r];
           uint8_t* st = ring + r * C::kStageAlloc;
@@ -700,12 +700,18 @@ __global__ void __launch_bounds__(128) transpose_bitmaps_kernel(const uint4* __r
                                                                 uint32_t krows, uint32_t kcols,
                                                                 const uint32_t* __restrict__ col_list,
                                                                 const uint32_t* __restrict__ col_cnt,
-                                                                uint4* __restrict__ tbits) {
+                                                                uint4* __restrict__ tbits,
+                                                                uint8_t* __restrict__ col_halves) {
   const uint32_t q = blockIdx.y, k = blockIdx.x;
   if (k >= col_cnt[q]) return;
   const uint32_t pr = col_list[static_cast<uint64_t>(q) * krows + k] & 0x7FFFFFFFu;
   const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint4 rowbits = mask[(static_cast<uint64_t>(pr) * 128 + warp * 32 + lane) * kcols + q];
+  // query halves of the tile that see no key of it
+  const bool seen = (rowbits.x | rowbits.y | rowbits.z | rowbits.w) != 0u;
+  const int lo = __syncthreads_or(warp < 2 && seen), hi = __syncthreads_or(warp >= 2 && seen);
+  if (threadIdx.x == 0)
+    col_halves[static_cast<uint64_t>(q) * krows + k] = static_cast<uint8_t>((lo ? 0 : 1) | (hi ? 0 : 2));
   uint32_t* out = reinterpret_cast<uint32_t*>(tbits + (static_cast<uint64_t>(q) * krows + k) * 128);
   const uint32_t words[4] = {rowbits.x, rowbits.y, rowbits.z, rowbits.w};
 #pragma unroll
@@ -734,7 +740,8 @@ void launch_side(const Prep& prep, StreamCtx& ctx, const BwdArgs& a, const float
   p.rows_pad = rows_pad;
   // work units from the device-built plan over the row view (dq) or the column view (dkdv):
   // whole tiles, or balanced chunks of long lists (global tokens) combined deterministically
-  const TileView view = SIDE == kSideDQ ? row_view(km) : TileView{bm.col_cnt, bm.col_list, km.kcols, km.krows, 1};
+  const TileView view =
+      SIDE == kSideDQ ? row_view(km) : TileView{bm.col_cnt, bm.col_list, km.kcols, km.krows, 1, bm.col_halves};
   const uint32_t workers = static_cast<uint32_t>(num_sms);
   const DevPlan& plan = plan_for(prep, ctx, view, p.all_tiles ? kPlanDense : kPlanList, a.slots, workers, s);
   const bool can_split = plan.cap_units > view.tiles;
@@ -758,6 +765,11 @@ void launch_side(const Prep& prep, StreamCtx& ctx, const BwdArgs& a, const float
     p.list = bm.col_list;
     p.list_stride = km.krows;
     p.bitmaps = bm.tbitmaps;
+#ifdef BBM_NO_HALF_SKIP  // A/B builds: whole tiles always
+    p.halves = nullptr;
+#else
+    p.halves = plan.half_heavy ? bm.col_halves : nullptr;  // partner (query) halves of the column view
+#endif
     p.ctr = ctx.ctr + 4;
     p.out0 = static_cast<__nv_bfloat16*>(a.dk);
     p.out1 = static_cast<__nv_bfloat16*>(a.dv);
@@ -811,6 +823,7 @@ void free_bwd_meta(BwdMeta& b) {
   cudaFree(b.col_cnt);
   cudaFree(b.col_list);
   cudaFree(b.tbitmaps);
+  cudaFree(b.col_halves);
   cudaFree(b.scratch);
   if (b.ready) cudaEventDestroy(b.ready);
   b = BwdMeta{};
@@ -827,13 +840,14 @@ void ensure_bwd_meta(const Prep& prep, cudaStream_t s) {
       b.col_cnt = bwd_alloc<uint32_t>(kc);
       b.col_list = bwd_alloc<uint32_t>(static_cast<uint64_t>(kc) * kr);
       b.tbitmaps = bwd_alloc<uint4>(static_cast<uint64_t>(kc) * kr * 128);
+      b.col_halves = bwd_alloc<uint8_t>(static_cast<uint64_t>(kc) * kr);
       b.scratch = bwd_alloc<uint32_t>(static_cast<uint64_t>(kr) + kc + 2);
       BBM_CUDA(cudaEventCreateWithFlags(&b.ready, cudaEventDisableTiming));
     }
     collist_kernel<<<kc, 256, 0, s>>>(km.sums, prep.n, kr, kc, b.col_list, b.col_cnt);
     BBM_CUDA(cudaGetLastError());
     transpose_bitmaps_kernel<<<dim3(kr, kc), 128, 0, s>>>(reinterpret_cast<const uint4*>(km.mask), kr, kc,
-                                                           b.col_list, b.col_cnt, b.tbitmaps);
+                                                           b.col_list, b.col_cnt, b.tbitmaps, b.col_halves);
     BBM_CUDA(cudaGetLastError());
     BBM_CUDA(cudaEventRecord(b.ready, s));
     b.version = prep.version;

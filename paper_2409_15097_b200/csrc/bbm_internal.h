@@ -134,6 +134,8 @@ struct BwdMeta {
   uint32_t* col_cnt = nullptr;   // [kcols]
   uint32_t* col_list = nullptr;  // [kcols][krows]
   uint4* tbitmaps = nullptr;     // [kcols*krows][128]
+  uint8_t* col_halves = nullptr; // [kcols*krows] per column-list position: bit h = query rows
+                                 // 64h..64h+63 of the tile see no key (dkdv skips that half)
   uint32_t* scratch = nullptr;   // [kcols + krows + 2] ordering scratch
 };
 

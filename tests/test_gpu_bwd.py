@@ -195,10 +195,11 @@ def test_split_long_lists_match_oracle_and_stay_deterministic(cuda, spec, n, d):
 
 
 @pytest.mark.parametrize("n,w,d", [(3000, 40, 128), (1111, 20, 64)])
-def test_dq_empty_key_half_skipping_is_exact(cuda, n, w, d):
-    """dq skips the S / dP and accumulate MMAs of a 64-key half that no row of the tile sees,
-    from the launch after the plan header reached the host: the first backward (no skipping)
-    and later ones (skipping) must agree bit for bit, and match the oracle."""
+def test_backward_empty_half_skipping_is_exact(cuda, n, w, d):
+    """dq (dkdv) skips the S / dP and accumulate MMAs of a 64-key (64-query) half of a tile that
+    no partner row sees, from the launch after the plan header reached the host: the first
+    backward (no skipping) and later ones (skipping) must agree bit for bit, and match the
+    oracle."""
     import torch
 
     mask = bbm.gen_longformer_windowed(n, w)
