@@ -222,9 +222,14 @@ const DevPlan& plan_for(const Prep& prep, StreamCtx& ctx, const TileView& v, int
     const cudaError_t q = cudaEventQuery(pl.hdr_ev);
     if (q == cudaSuccess) {
       pl.partial_heavy = (pl.host_hdr[0] - pl.host_hdr[1]) * 2ull > pl.host_hdr[0];
-      // skipping empty key halves pays off on band-like masks (C5: 40 % of the occupied tiles have
-      // one; -4 % same-box A/B) and costs a little elsewhere (an extra metadata load per K / V)
-      pl.half_heavy = pl.host_hdr[2] * 4ull >= pl.host_hdr[0] && pl.host_hdr[0] > 0;
+      // skipping empty 64-row partner halves (an extra metadata load per K / V tile, N = 64 score
+      // MMAs) pays off once at least ~10 % of the occupied tiles have one: same-box A/B, forward
+      // C5 (40 %) -6 %, C2 (16.5 %) -1.5 %, backward C5 -7 %, C2 -1.7 %
+#ifndef BBM_HALF_GATE_PCT
+#define BBM_HALF_GATE_PCT 10
+#endif
+      pl.half_heavy = pl.host_hdr[2] * 100ull >= pl.host_hdr[0] * static_cast<uint64_t>(BBM_HALF_GATE_PCT) &&
+                      pl.host_hdr[0] > 0;
       pl.known_version = pl.version;
     } else if (q == cudaErrorNotReady) {
       (void)cudaGetLastError();  // not an error: the header has not arrived yet

@@ -26,6 +26,7 @@ for v in $VARIANTS; do
     LOCKSTEP) FL="-DBBM_SPLIT_ENGINE=0" ;;
     PREP16) FL="-DBBM_PREP_SPLITS=16" ;;
     NOHALF) FL="-DBBM_NO_HALF_SKIP" ;;
+    GATE10) FL="-DBBM_HALF_GATE_PCT=10" ;;
     PREP32) FL="-DBBM_PREP_SPLITS=32" ;;
     S2R4) FL="-DBBM_SBUFS=2 -DBBM_RING128=4" ;;
     HALF_KVLOAD) FL="-DBBM_ABLATE_HALF_KVLOAD" ;;
