@@ -562,8 +562,19 @@ __global__ void __launch_bounds__(kThreads, 1)
           const float* vec = nullptr;
           if constexpr (SIDE == kSideDKDV)
             vec = reinterpret_cast<const float*>(ring + r * C::kStageAlloc + 2 * C::kTileBytes) + half * 64;
+          // a warp whose 32 rows pair with none of this half's 64 partners: P = dS = 0 without
+          // loading S / dP or computing anything (exactly what the masked path writes)
+          const bool empty = masked && __all_sync(0xffffffffu, (bits.x | bits.y) == 0u);
 #pragma unroll
           for (uint32_t c32 = 0; c32 < 2; ++c32) {
+            if (empty) {
+              uint32_t z[16];
+#pragma unroll
+              for (uint32_t i = 0; i < 16; ++i) z[i] = 0u;
+              tmem_st16(ts + c32 * 16, z);
+              tmem_st16(ts + 128 + c32 * 16, z);
+              continue;
+            }
             uint32_t s[32], dp[32];
             tmem_ld32(ts + c32 * 32, s);
             tmem_ld32(ts + 128 + c32 * 32, dp);
