@@ -456,6 +456,14 @@ def main():
     cnt, lst, _ = prep.kernel_lists()
     area = executed_area(cnt, lst, n, int(variant))
     flops = 4.0 * area * d * slots
+    # tensor-core work the kernel actually issues: tiles with an empty 64-key half (skipped when at
+    # least 10 % of the occupied tiles have one, plan.cu) multiply only the other half
+    mma_flops = flops
+    if int(variant) in (2, 3):
+        hv = prep.tile_halves()
+        nhalf = sum(int((hv[p, :c] > 0).sum()) for p, c in enumerate(cnt))
+        if nhalf * 10 >= int(cnt.sum()):
+            mma_flops = flops - 4.0 * 128 * 64 * d * nhalf * slots  # half of each such tile
     dense_flops = 4.0 * executed_area(cnt, lst, n, 0) * d * slots
     total_flops = 4.0 * area * d * (slots_total if args.scaling == "strong" else slots_total * world)
 
@@ -562,6 +570,10 @@ def main():
             "traffic": traffic, "peak_source": f"{peak_kind} (MEASURED_PEAKS.json burst)",
             "kernel": "attn_fwd_kernel" if args.which == "fwd" else "attn_bwd_kernel (dq + dkdv)",
             "algorithmic_bytes_per_launch": bytes_alg, "flops_per_launch": flops,
+            "mma_flops_per_launch": mma_flops,
+            "flops_note": "flops_per_launch counts every executed 128x128 tile in full (SURVEY 8d); "
+                          "mma_flops_per_launch is the tensor work issued (64-key halves no row sees are "
+                          "skipped)",
             "tensor_frac": (flops / (avg_launch * 1e-3) / 1e12) / peaks["bf16_tflops"],
             "hbm_frac": (bytes_alg / (avg_launch * 1e-3) / 1e9) / peaks["hbm_gbs"],
             "avg_launch_ms": avg_launch, "slots_per_launch": slots,
