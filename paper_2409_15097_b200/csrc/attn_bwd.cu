@@ -174,6 +174,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     attn_bwd_kernel(const __grid_constant__ CUtensorMap tm_f0, const __grid_constant__ CUtensorMap tm_f1,
                     const __grid_constant__ CUtensorMap tm_s0, const __grid_constant__ CUtensorMap tm_s1,
                     const __grid_constant__ CUtensorMap tm_o0, const __grid_constant__ CUtensorMap tm_o1,
+                    const __grid_constant__ CUtensorMap tm_s0h, const __grid_constant__ CUtensorMap tm_s1h,
                     const BwdParams p) {
   // fixed tiles f0, f1: (Q_i, dO_i) for dq, (K_j, V_j) for dkdv; streamed s0, s1: the partner's
   // (K_j, V_j) for dq, (Q_i, dO_i) for dkdv.
@@ -259,11 +260,23 @@ __global__ void __launch_bounds__(kThreads, 1)
           uint64_t* full = &ctl->ring_full[r];
           uint8_t* st = ring + r * C::kStageAlloc;
           ctl->stage_halves[r] = hv;  // published by the arrive below
-          mbar_arrive_expect_tx(full, C::kStageBytes);
-          for (uint32_t b = 0; b < C::kBoxes; ++b) {
-            tma_load_3d(st + b * kBoxBytes, &tm_s0, full, b * 64, u * 128, d.slot, pol_stream);
-            tma_load_3d(st + C::kTileBytes + b * kBoxBytes, &tm_s1, full, b * 64, u * 128, d.slot,
-                        pol_stream);
+          if (hv == 0) {
+            mbar_arrive_expect_tx(full, C::kStageBytes);
+            for (uint32_t b = 0; b < C::kBoxes; ++b) {
+              tma_load_3d(st + b * kBoxBytes, &tm_s0, full, b * 64, u * 128, d.slot, pol_stream);
+              tma_load_3d(st + C::kTileBytes + b * kBoxBytes, &tm_s1, full, b * 64, u * 128, d.slot,
+                          pol_stream);
+            }
+          } else {
+            // one partner half is never paired: only the other half's 64 rows are loaded (64-row boxes)
+            const uint32_t hh = (hv & 1u) ? 1u : 0u;
+            mbar_arrive_expect_tx(full, C::kStageBytes - C::kTileBytes);
+            for (uint32_t b = 0; b < C::kBoxes; ++b) {
+              tma_load_3d(st + b * kBoxBytes + hh * (kBoxBytes / 2), &tm_s0h, full, b * 64, u * 128 + hh * 64,
+                          d.slot, pol_stream);
+              tma_load_3d(st + C::kTileBytes + b * kBoxBytes + hh * (kBoxBytes / 2), &tm_s1h, full, b * 64,
+                          u * 128 + hh * 64, d.slot, pol_stream);
+            }
           }
           if constexpr (SIDE == kSideDKDV) {
             const uint64_t off = static_cast<uint64_t>(d.slot) * p.rows_pad + u * 128;
@@ -791,6 +804,11 @@ void launch_side(const Prep& prep, StreamCtx& ctx, const BwdArgs& a, const float
   const CUtensorMap tdo = cached_tmap_bf16_3d(a.d_out, D, a.n, a.slots, 64, 128);
   const CUtensorMap to0 = cached_tmap_bf16_3d(p.out0, D, a.n, a.slots, 64, 128);
   const CUtensorMap to1 = SIDE == kSideDKDV ? cached_tmap_bf16_3d(p.out1, D, a.n, a.slots, 64, 128) : to0;
+  // streamed tiles with an empty partner half: 64-row boxes of the other half
+  const CUtensorMap tk64 = cached_tmap_bf16_3d(a.k, D, a.n, a.slots, 64, 64);
+  const CUtensorMap tv64 = cached_tmap_bf16_3d(a.v, D, a.n, a.slots, 64, 64);
+  const CUtensorMap tq64 = cached_tmap_bf16_3d(a.q, D, a.n, a.slots, 64, 64);
+  const CUtensorMap tdo64 = cached_tmap_bf16_3d(a.d_out, D, a.n, a.slots, 64, 64);
   static std::atomic<uint64_t> attr_devices{0};
   once_per_device(attr_devices, [] {
     BBM_CUDA(cudaFuncSetAttribute(attn_bwd_kernel<D, SIDE, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -809,9 +827,9 @@ void launch_side(const Prep& prep, StreamCtx& ctx, const BwdArgs& a, const float
   }
   auto go = [&](auto kernel) {
     if (SIDE == kSideDQ)
-      kernel<<<grid, kThreads, bwd_smem_bytes<D, SIDE>(), s>>>(tq, tdo, tk, tv, to0, to1, p);
+      kernel<<<grid, kThreads, bwd_smem_bytes<D, SIDE>(), s>>>(tq, tdo, tk, tv, to0, to1, tk64, tv64, p);
     else
-      kernel<<<grid, kThreads, bwd_smem_bytes<D, SIDE>(), s>>>(tk, tv, tq, tdo, to0, to1, p);
+      kernel<<<grid, kThreads, bwd_smem_bytes<D, SIDE>(), s>>>(tk, tv, tq, tdo, to0, to1, tq64, tdo64, p);
   };
   if (p.trace)
     go(attn_bwd_kernel<D, SIDE, true>);
