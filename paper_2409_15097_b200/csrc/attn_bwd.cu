@@ -169,7 +169,9 @@ __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t b
       : "memory");
 }
 
-template <int D, int SIDE, bool kTrace>
+// kHalves: this launch skips empty 64-row partner halves (p.halves set). A separate build, so the
+// launches without it run exactly the plain issue loop (at d = 64 its issue rate bounds the kernel).
+template <int D, int SIDE, bool kTrace, bool kHalves>
 __global__ void __launch_bounds__(kThreads, 1)
     attn_bwd_kernel(const __grid_constant__ CUtensorMap tm_f0, const __grid_constant__ CUtensorMap tm_f1,
                     const __grid_constant__ CUtensorMap tm_s0, const __grid_constant__ CUtensorMap tm_s1,
@@ -254,13 +256,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         for (uint32_t j = 0; j < d.nt; ++j) {
           const uint32_t u = bwd_entry(p, d.tile, d.j0 + j) & 0x7FFFFFFFu;
-          const uint32_t hv =
-              p.halves ? __ldg(p.halves + static_cast<uint64_t>(d.tile) * p.list_stride + d.j0 + j) : 0u;
+          uint32_t hv = 0;
+          if constexpr (kHalves) hv = __ldg(p.halves + static_cast<uint64_t>(d.tile) * p.list_stride + d.j0 + j);
           mbar_wait(&ctl->ring_empty[r], rph);
           uint64_t* full = &ctl->ring_full[r];
           uint8_t* st = ring + r * C::kStageAlloc;
-          ctl->stage_halves[r] = hv;  // published by the arrive below
-          if (hv == 0) {
+          if constexpr (kHalves) ctl->stage_halves[r] = hv;  // published by the arrive below
+          if (!kHalves || hv == 0) {
             mbar_arrive_expect_tx(full, C::kStageBytes);
             for (uint32_t b = 0; b < C::kBoxes; ++b) {
               tma_load_3d(st + b * kBoxBytes, &tm_s0, full, b * 64, u * 128, d.slot, pol_stream);
@@ -305,8 +307,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       // S_h = f0 s0[64h..]^T, dP_h = f1 s1[64h..]^T: both K-major, K = D, N = 64 partner rows
       // a partner half that no row of the tile sees (dq: an empty 64-key half) is not multiplied:
       // its S / dP columns keep stale values whose P / dS no accumulate MMA reads
-      auto issue_sdp = [&](uint32_t h, uint32_t stage) {
-        if ((ctl->stage_halves[stage] >> h) & 1u) {
+      // (the stage's flags are read once per tile, and only when the launch skips halves: at
+      // d = 64 this thread's issue rate bounds the kernel)
+      constexpr bool skips = kHalves;
+      auto issue_sdp = [&](uint32_t h, uint32_t stage, uint32_t hv) {
+        if (kHalves && ((hv >> h) & 1u)) {
           tc_commit(&ctl->s_full[h]);
           return;
         }
@@ -326,9 +331,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       };
       // accumulate MMAs of half h: K steps 4h..4h+3 (partner rows 64h..64h+63). Packed bf16 A
       // operand: half h's 32 columns at [64h, 64h+32) of its region -> column (kk/4)*64 + (kk%4)*8
-      bool started = false;  // the item's first accumulate MMA overwrites, the others accumulate
-      auto issue_acc = [&](uint32_t h, uint32_t stage, uint32_t acc0) {
-        if ((ctl->stage_halves[stage] >> h) & 1u) return;
+      // the item's first accumulate MMA overwrites, the others accumulate: the first is K step 0 of
+      // tile 0's first non-empty half h0 (no mutable state in this loop: at d = 64 the issue rate
+      // bounds the kernel)
+      auto issue_acc = [&](uint32_t h, uint32_t stage, uint32_t j, uint32_t h0, uint32_t acc0, uint32_t hv) {
+        if (kHalves && ((hv >> h) & 1u)) return;
         const uint32_t sbase = raddr + stage * C::kStageAlloc;
         const uint64_t b0 = make_sdesc_sw128(sbase, kBoxBytes, 1024);
         const uint64_t b1 = make_sdesc_sw128(sbase + C::kTileBytes, kBoxBytes, 1024);
@@ -336,12 +343,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (uint32_t q = 0; q < 4; ++q) {
           const uint32_t kk = 4 * h + q;
           const uint32_t acol = (kk / 4) * 64 + (kk % 4) * 8;
-          const uint32_t acc = started ? 1u : 0u;
+          const uint32_t acc = (j > 0 || h != h0 || q > 0) ? 1u : 0u;
           // dQ += dS K_j  |  dK += dS^T Q_i   (B = streamed tile 0, MN-major)
           umma_ts(tmem + acc0, tmem + 128 + acol, sdesc_advance(b0, kk * 2048), idesc_acc, acc);
           if constexpr (SIDE == kSideDKDV)  // dV += P^T dO_i   (B = streamed tile 1)
             umma_ts(tmem + acc0 + D, tmem + acol, sdesc_advance(b1, kk * 2048), idesc_acc, acc);
-          started = true;
         }
       };
       for (;;) {
@@ -356,17 +362,19 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_wait(&ctl->ring_full[r], rph);
         tc_fence_after();
         trace_ev<kTrace>(tracing, p, &ctl->trace_count, 43, 0, it.t);
-        issue_sdp(0, r);
+        uint32_t hv_cur = skips ? ctl->stage_halves[r] : 0u;
+        issue_sdp(0, r, hv_cur);
         trace_ev<kTrace>(tracing, p, &ctl->trace_count, 40, 0, 0);
-        issue_sdp(1, r);
+        issue_sdp(1, r, hv_cur);
         trace_ev<kTrace>(tracing, p, &ctl->trace_count, 40, 1, 0);
         if (it.nt == 1) tc_commit(&ctl->fixed_empty);
         const uint32_t ab = C::kDefer ? (items++ & 1u) : 0u;  // this item's accumulator set
-        started = false;
+        const uint32_t h0 = (hv_cur & 1u) ? 1u : 0u;  // tile 0's first non-empty half
         const uint32_t acc0 = C::kAcc0 + ab * C::kAccSet;
         for (uint32_t j = 0; j < it.nt; ++j) {
           const uint32_t rn = r + 1 == C::kStages ? 0 : r + 1;
           const uint32_t rnph = r + 1 == C::kStages ? rph ^ 1 : rph;
+          uint32_t hv_next = 0;
           for (uint32_t h = 0; h < 2; ++h) {
             mbar_wait(&ctl->p_full[h], pph[h]);
             pph.flip(h);
@@ -376,21 +384,23 @@ __global__ void __launch_bounds__(kThreads, 1)
               aph.flip(ab);
             }
             tc_fence_after();
-            issue_acc(h, r, acc0);
+            issue_acc(h, r, j, h0, acc0, hv_cur);
             trace_ev<kTrace>(tracing, p, &ctl->trace_count, 41, h, j);
             if (h == 1) tc_commit(&ctl->ring_empty[r]);  // both halves of tile j consumed
             if (j + 1 < it.nt) {
               if (h == 0) {
                 mbar_wait(&ctl->ring_full[rn], rnph);
                 tc_fence_after();
+                hv_next = skips ? ctl->stage_halves[rn] : 0u;
               }
-              issue_sdp(h, rn);
+              issue_sdp(h, rn, hv_next);
               trace_ev<kTrace>(tracing, p, &ctl->trace_count, 40, h, j + 1);
               if (h == 1 && j + 2 == it.nt) tc_commit(&ctl->fixed_empty);
             }
           }
           r = rn;
           rph = rnph;
+          hv_cur = hv_next;
         }
         tc_commit(&ctl->acc_full[ab]);
       }
@@ -811,9 +821,11 @@ void launch_side(const Prep& prep, StreamCtx& ctx, const BwdArgs& a, const float
   const CUtensorMap tdo64 = cached_tmap_bf16_3d(a.d_out, D, a.n, a.slots, 64, 64);
   static std::atomic<uint64_t> attr_devices{0};
   once_per_device(attr_devices, [] {
-    BBM_CUDA(cudaFuncSetAttribute(attn_bwd_kernel<D, SIDE, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    BBM_CUDA(cudaFuncSetAttribute(attn_bwd_kernel<D, SIDE, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   bwd_smem_bytes<D, SIDE>()));
-    BBM_CUDA(cudaFuncSetAttribute(attn_bwd_kernel<D, SIDE, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    BBM_CUDA(cudaFuncSetAttribute(attn_bwd_kernel<D, SIDE, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  bwd_smem_bytes<D, SIDE>()));
+    BBM_CUDA(cudaFuncSetAttribute(attn_bwd_kernel<D, SIDE, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   bwd_smem_bytes<D, SIDE>()));
   });
   const uint32_t grid = static_cast<uint32_t>(
@@ -832,9 +844,11 @@ void launch_side(const Prep& prep, StreamCtx& ctx, const BwdArgs& a, const float
       kernel<<<grid, kThreads, bwd_smem_bytes<D, SIDE>(), s>>>(tk, tv, tq, tdo, to0, to1, tq64, tdo64, p);
   };
   if (p.trace)
-    go(attn_bwd_kernel<D, SIDE, true>);
+    go(attn_bwd_kernel<D, SIDE, true, false>);
+  else if (p.halves)
+    go(attn_bwd_kernel<D, SIDE, false, true>);
   else
-    go(attn_bwd_kernel<D, SIDE, false>);
+    go(attn_bwd_kernel<D, SIDE, false, false>);
   BBM_CUDA(cudaGetLastError());
 }
 
