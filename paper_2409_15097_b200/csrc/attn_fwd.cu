@@ -210,12 +210,14 @@ __device__ __forceinline__ uint32_t entry_of(const FwdParams& p, uint32_t row_ti
 
 // Empty key halves of list entry j of row tile `row_tile` (list modes; the other modes and the
 // in-kernel gather always load and multiply whole tiles)
-template <int MODE, bool kGather>
+// Only the engine build for partial-heavy masks (kSkip) carries the half-skipping code, so the
+// plain build's issue loops are exactly those without it.
+template <int MODE, bool kGather, bool kSkip>
 __device__ __forceinline__ uint32_t half_of(const FwdParams& p, uint32_t row_tile, uint32_t j) {
 #ifdef BBM_NO_HALF_SKIP  // A/B builds: whole tiles always
   return 0u;
 #else
-  if constexpr (MODE == kModeDense || MODE == kModeNaive || kGather) return 0u;
+  if constexpr (MODE == kModeDense || MODE == kModeNaive || kGather || !kSkip) return 0u;
   else return p.halves ? __ldg(p.halves + static_cast<uint64_t>(row_tile) * p.kcols + j) : 0u;
 #endif
 }
@@ -414,7 +416,7 @@ __global__ void __launch_bounds__(kThreadsOf<D>, 1)
           if (d.nt == 0) continue;
           pit[pw++ % kQueue] = d;
           kentry = entry_of<MODE>(p, d.rt, d.j0);
-          khalf = half_of<MODE, kGather>(p, d.rt, d.j0);
+          khalf = half_of<MODE, kGather, kSkip>(p, d.rt, d.j0);
           mbar_wait(&ctl->q_empty[qb], qph[qb]);
           qph.flip(qb);
           if (lane == 0) mbar_arrive_expect_tx(&ctl->q_full[qb], C::kTileBytes);
@@ -433,7 +435,7 @@ __global__ void __launch_bounds__(kThreadsOf<D>, 1)
         // the next list entry is fetched now, a full issue step before it is needed
         if (kj + 1 < kit.nt) {
           kentry = entry_of<MODE>(p, kit.rt, kit.j0 + kj + 1);
-          khalf = half_of<MODE, kGather>(p, kit.rt, kit.j0 + kj + 1);
+          khalf = half_of<MODE, kGather, kSkip>(p, kit.rt, kit.j0 + kj + 1);
         }
         load_tile(&tm_k, &tm_k64, kseq_of(kk), cur & 0x7FFFFFFFu, kit.slot, 2, kj, chalf);
         ++kk;
@@ -449,13 +451,13 @@ __global__ void __launch_bounds__(kThreadsOf<D>, 1)
           vit = pit[pr++ % kQueue];
           vj = 0;
           ventry = entry_of<MODE>(p, vit.rt, vit.j0);
-          vhalf = half_of<MODE, kGather>(p, vit.rt, vit.j0);
+          vhalf = half_of<MODE, kGather, kSkip>(p, vit.rt, vit.j0);
           v_need = false;
         }
         const uint32_t cur = ventry, chalf = vhalf;
         if (vj + 1 < vit.nt) {
           ventry = entry_of<MODE>(p, vit.rt, vit.j0 + vj + 1);
-          vhalf = half_of<MODE, kGather>(p, vit.rt, vit.j0 + vj + 1);
+          vhalf = half_of<MODE, kGather, kSkip>(p, vit.rt, vit.j0 + vj + 1);
         }
         load_tile(&tm_v, &tm_v64, vseq_of(vk), cur & 0x7FFFFFFFu, vit.slot, 3, vj, chalf);
         ++vk;
@@ -510,7 +512,7 @@ __global__ void __launch_bounds__(kThreadsOf<D>, 1)
             tc_fence_after();
             // a key half no row sees is neither loaded nor multiplied: N = 64 over the other half
             // (its S columns keep stale values, which the softmax replaces by the mask sentinel)
-            const uint32_t half = ctl->ring_meta[slot];
+            const uint32_t half = kSkip ? ctl->ring_meta[slot] : 0u;
             const uint32_t hrow = (half & 1u) ? 64u : 0u;
             const uint64_t qdesc = make_sdesc_sw128(qaddr + qb * C::kTileBytes, 16, 1024);
             const uint64_t kdesc = make_sdesc_sw128(raddr + slot * C::kTileBytes + hrow * 128, 16, 1024);
@@ -543,7 +545,7 @@ __global__ void __launch_bounds__(kThreadsOf<D>, 1)
             const uint64_t vdesc = make_sdesc_sw128(raddr + slot * C::kTileBytes, kBoxBytes, 1024);
             const uint32_t pcol = tmem + buf * 128;
             // K steps over the keys present (a whole empty key half is skipped)
-            const uint32_t half = ctl->ring_meta[slot];
+            const uint32_t half = kSkip ? ctl->ring_meta[slot] : 0u;
             const uint32_t kk0 = (half & 1u) ? 4u : 0u, kk1 = (half & 2u) ? 4u : 8u;
 #ifndef BBM_ABLATE_NO_PV  // timing experiments only: O is never accumulated
 #pragma unroll
