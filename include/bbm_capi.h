@@ -185,7 +185,9 @@ bbm_status bbm_attn_fwd_rcm_host_bf16(bbm_prep prep, int variant, const uint32_t
 /* Same, float host buffers (the reference's Matrix<float> storage, matrix.hpp:14-45); inputs
  * rounded to bf16 (RNE) on the device, output widened back to float; row stats as double.
  * Validates finiteness like validate_forward_args (engine.hpp:244-258). Copy/compute pipeline
- * over slot chunks, like the bf16 form. */
+ * over slot chunks, like the bf16 form. The float host-buffer entries take any head dim in
+ * [1, 128] (the device-pointer entries: 64 or 128): the device copy is zero-padded to 64 or 128
+ * columns, which leaves every score and output unchanged. */
 bbm_status bbm_attn_fwd_host_f32(bbm_prep prep, int variant, const float* q, const float* k,
                                  const float* v, float* out, double* row_max, double* row_sum,
                                  uint64_t slots, uint32_t head_dim, double scale);
@@ -197,6 +199,14 @@ bbm_status bbm_run_attention_host_f32(bbm_prep prep, int variant, const float* c
                                       float* const* out, double* const* row_max,
                                       double* const* row_sum, uint64_t slots, uint32_t head_dim,
                                       double scale);
+/* The same with the value head dim independent of the key head dim
+ * (EngineForward.ValueHeadDimMayDifferFromKeyDim, test_engine.cpp:198-209): q/k are n x d_k,
+ * v/out n x d_v; 1 <= d_k, d_v <= 128. */
+bbm_status bbm_run_attention_host_f32_dims(bbm_prep prep, int variant, const float* const* q,
+                                           const float* const* k, const float* const* v,
+                                           float* const* out, double* const* row_max,
+                                           double* const* row_sum, uint64_t slots, uint32_t d_k,
+                                           uint32_t d_v, double scale);
 
 /* ---- blocked_backward (engine.hpp:346-471): dq, dk, dv of L = sum(out * d_out) from the forward's
  *      saved row statistics (row_max / row_sum as bbm_attn_fwd returns them), over the same tiles
@@ -214,6 +224,11 @@ bbm_status bbm_attn_bwd_host_f32(bbm_prep prep, int variant, const float* q, con
                                  const float* v, const float* out, const double* row_max,
                                  const double* row_sum, const float* d_out, float* dq, float* dk,
                                  float* dv, uint64_t slots, uint32_t head_dim, double scale);
+/* The same with d_v != d_k allowed: q, k, dq, dk are n x d_k; v, out, d_out, dv are n x d_v. */
+bbm_status bbm_attn_bwd_host_f32_dims(bbm_prep prep, int variant, const float* q, const float* k,
+                                      const float* v, const float* out, const double* row_max,
+                                      const double* row_sum, const float* d_out, float* dq, float* dk,
+                                      float* dv, uint64_t slots, uint32_t d_k, uint32_t d_v, double scale);
 
 /* Multi-GPU run_attention: slots sharded contiguously over `n_devices` GPUs
  * ([g*S/G, (g+1)*S/G)), metadata replicated peer-to-peer from prep's device, one stream per

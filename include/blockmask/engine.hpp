@@ -3,15 +3,16 @@
 //
 //   preprocess_mask (engine.hpp:80-91)      -> bbm_preprocess_packed_host (GPU preprocessor; the
 //                                              MaskPrep keeps the device metadata alive)
-//   blocked_forward (engine.hpp:282-341)    -> bbm_attn_fwd_host_f32 (sm_100a tcgen05 kernel)
-//   blocked_backward (engine.hpp:346-471)   -> bbm_attn_bwd_host_f32
-//   run_attention (engine.hpp:489-505)      -> bbm_run_attention_host_f32 over all slots (each
+//   blocked_forward (engine.hpp:282-341)    -> bbm_run_attention_host_f32_dims (sm_100a kernel)
+//   blocked_backward (engine.hpp:346-471)   -> bbm_attn_bwd_host_f32_dims
+//   run_attention (engine.hpp:489-505)      -> bbm_run_attention_host_f32_dims over all slots (each
 //                                              slot's Matrix<float> storage used in place)
 //
 // Numerics: Q/K/V are rounded to bf16 (RNE) on the device and the kernel accumulates in fp32, so
 // outputs agree with the reference to a bf16 tolerance (max-abs <= 2e-2; tests/), not bit for
 // bit. Counters (engine.hpp:47-66) are exact: they depend on the mask and spec only.
-// New rejections (std::invalid_argument): head dims other than 64 / 128, d_v != d_k.
+// New rejection (std::invalid_argument): head dims d_k or d_v above 128 (the kernels hold one
+// 128-column head-dim tile; smaller or unequal dims are zero-padded on the device to 64 / 128).
 // `threads` is validated (>= 1) like the reference and otherwise ignored.
 #pragma once
 
@@ -166,7 +167,7 @@ void validate_shapes(const Matrix<T>& q, const Matrix<T>& k, const Matrix<T>& v,
     require(prep.n_tokens == n, "mask preprocessing does not match this mask");
     require(prep.device != nullptr, "MaskPrep was not built by preprocess_mask");
     require(q.rows() == n && k.rows() == n && v.rows() == n, "q, k, v need one row per token");
-    require(q.cols() == k.cols(), "q and k must share the head dimension");
+    require(q.cols() == k.cols() && q.cols() >= 1, "q and k must share a positive head dim");
     require(v.cols() >= 1, "v needs at least one column");
     require(std::isfinite(scale), "scale must be finite");
     require(threads >= 1, "threads must be >= 1");
@@ -184,49 +185,46 @@ template <typename T>
 void forward_slots(const std::vector<const SlotInputs<T>*>& in, double scale, const MaskPrep& prep,
                    Variant variant, std::vector<ForwardResult<T>>& out) {
     static_assert(std::is_floating_point_v<T>, "Matrix<T> of float or double");
-    const std::size_t slots = in.size(), n = prep.n_tokens, d = in.front()->q.cols();
-    if (in.front()->v.cols() != d)
-        throw std::invalid_argument("d_v != d_k is not supported by the sm_100a kernel");
+    const std::size_t slots = in.size(), n = prep.n_tokens;
+    const std::size_t dk = in.front()->q.cols(), dv = in.front()->v.cols();
     const EngineCounters per_slot = counters_for(prep, variant, 1);
     out.resize(slots);
     for (ForwardResult<T>& r : out) {
-        r.out = Matrix<T>(n, d);
+        r.out = Matrix<T>(n, dv);
         r.row_max.assign(n, 0.0);
         r.row_sum.assign(n, 0.0);
         r.counters = per_slot;
     }
-    if constexpr (std::is_same_v<T, float>) {
-        // run_attention<float> (engine.hpp:489-505): every slot's own Matrix<float> storage goes
-        // to the device as is (bbm_run_attention_host_f32: chunked H2D / kernel / D2H pipeline),
-        // results land in the ForwardResults directly
-        std::vector<const float*> q(slots), k(slots), v(slots);
-        std::vector<float*> o(slots);
-        std::vector<double*> m(slots), l(slots);
-        for (std::size_t s = 0; s < slots; ++s) {
-            q[s] = in[s]->q.data(), k[s] = in[s]->k.data(), v[s] = in[s]->v.data();
-            o[s] = out[s].out.data(), m[s] = out[s].row_max.data(), l[s] = out[s].row_sum.data();
-        }
-        device::check(bbm_run_attention_host_f32(prep.device->get(), static_cast<int>(variant), q.data(),
-                                                 k.data(), v.data(), o.data(), m.data(), l.data(), slots,
-                                                 static_cast<std::uint32_t>(d), scale),
-                      "blocked_forward");
-    } else {  // Matrix<double>: narrowed to float for the upload (the kernel computes in bf16)
-        std::vector<float> q, k, v;
-        q.reserve(slots * n * d), k.reserve(slots * n * d), v.reserve(slots * n * d);
-        for (const SlotInputs<T>* s : in) append_f32(q, s->q), append_f32(k, s->k), append_f32(v, s->v);
-        std::vector<float> o(slots * n * d);
-        std::vector<double> rmax(slots * n), rsum(slots * n);
-        device::check(bbm_attn_fwd_host_f32(prep.device->get(), static_cast<int>(variant), q.data(),
-                                            k.data(), v.data(), o.data(), rmax.data(), rsum.data(),
-                                            slots, static_cast<std::uint32_t>(d), scale),
-                      "blocked_forward");
-        for (std::size_t s = 0; s < slots; ++s) {
-            ForwardResult<T>& r = out[s];
-            for (std::size_t i = 0; i < n * d; ++i) r.out.data()[i] = static_cast<T>(o[s * n * d + i]);
-            r.row_max.assign(rmax.begin() + s * n, rmax.begin() + (s + 1) * n);
-            r.row_sum.assign(rsum.begin() + s * n, rsum.begin() + (s + 1) * n);
-        }
+    std::vector<const float*> q(slots), k(slots), v(slots);
+    std::vector<float*> o(slots);
+    std::vector<double*> m(slots), l(slots);
+    std::vector<float> fq, fk, fv, fo;  // Matrix<double>: narrowed to float for the upload
+    if constexpr (!std::is_same_v<T, float>) {
+        fq.reserve(slots * n * dk), fk.reserve(slots * n * dk), fv.reserve(slots * n * dv);
+        for (const SlotInputs<T>* s : in) append_f32(fq, s->q), append_f32(fk, s->k), append_f32(fv, s->v);
+        fo.resize(slots * n * dv);
     }
+    for (std::size_t s = 0; s < slots; ++s) {
+        if constexpr (std::is_same_v<T, float>) {
+            // run_attention<float> (engine.hpp:489-505): every slot's own Matrix<float> storage goes
+            // to the device as is (chunked H2D / kernel / D2H pipeline), results land in the
+            // ForwardResults directly
+            q[s] = in[s]->q.data(), k[s] = in[s]->k.data(), v[s] = in[s]->v.data();
+            o[s] = out[s].out.data();
+        } else {
+            q[s] = fq.data() + s * n * dk, k[s] = fk.data() + s * n * dk, v[s] = fv.data() + s * n * dv;
+            o[s] = fo.data() + s * n * dv;
+        }
+        m[s] = out[s].row_max.data(), l[s] = out[s].row_sum.data();
+    }
+    device::check(bbm_run_attention_host_f32_dims(prep.device->get(), static_cast<int>(variant), q.data(),
+                                                  k.data(), v.data(), o.data(), m.data(), l.data(), slots,
+                                                  static_cast<std::uint32_t>(dk), static_cast<std::uint32_t>(dv),
+                                                  scale),
+                  "blocked_forward");
+    if constexpr (!std::is_same_v<T, float>)
+        for (std::size_t s = 0; s < slots; ++s)
+            for (std::size_t i = 0; i < n * dv; ++i) out[s].out.data()[i] = static_cast<T>(fo[s * n * dv + i]);
 }
 
 }  // namespace detail
@@ -248,27 +246,27 @@ BackwardResult<T> blocked_backward(const Matrix<T>& q, const Matrix<T>& k, const
                                    Variant variant, const ForwardResult<T>& fwd,
                                    const Matrix<T>& d_out, unsigned threads = 1) {
     detail::validate_shapes(q, k, v, scale, mask, prep, threads);
-    const std::size_t n = mask.size(), d = q.cols();
-    require(fwd.out.rows() == n && fwd.out.cols() == v.cols(), "forward output shape mismatch");
+    const std::size_t n = mask.size(), dk = q.cols(), dv = v.cols();
+    require(fwd.out.rows() == n && fwd.out.cols() == dv, "forward output shape mismatch");
     require(fwd.row_max.size() == n && fwd.row_sum.size() == n, "forward row stats missing");
-    require(d_out.rows() == n && d_out.cols() == v.cols(), "d_out shape must match the output");
-    if (v.cols() != d) throw std::invalid_argument("d_v != d_k is not supported by the sm_100a kernel");
+    require(d_out.rows() == n && d_out.cols() == dv, "d_out shape must match the output");
     std::vector<float> hq, hk, hv, ho, hdo;
     detail::append_f32(hq, q), detail::append_f32(hk, k), detail::append_f32(hv, v);
     detail::append_f32(ho, fwd.out), detail::append_f32(hdo, d_out);
-    std::vector<float> dq(n * d), dk(n * d), dv(n * d);
-    device::check(bbm_attn_bwd_host_f32(prep.device->get(), static_cast<int>(variant), hq.data(),
-                                        hk.data(), hv.data(), ho.data(), fwd.row_max.data(),
-                                        fwd.row_sum.data(), hdo.data(), dq.data(), dk.data(),
-                                        dv.data(), 1, static_cast<std::uint32_t>(d), scale),
+    std::vector<float> dq(n * dk), dkg(n * dk), dvg(n * dv);
+    device::check(bbm_attn_bwd_host_f32_dims(prep.device->get(), static_cast<int>(variant), hq.data(),
+                                             hk.data(), hv.data(), ho.data(), fwd.row_max.data(),
+                                             fwd.row_sum.data(), hdo.data(), dq.data(), dkg.data(),
+                                             dvg.data(), 1, static_cast<std::uint32_t>(dk),
+                                             static_cast<std::uint32_t>(dv), scale),
                   "blocked_backward");
     BackwardResult<T> r;
-    r.dq = Matrix<T>(n, d), r.dk = Matrix<T>(n, d), r.dv = Matrix<T>(n, d);
-    for (std::size_t i = 0; i < n * d; ++i) {
+    r.dq = Matrix<T>(n, dk), r.dk = Matrix<T>(n, dk), r.dv = Matrix<T>(n, dv);
+    for (std::size_t i = 0; i < n * dk; ++i) {
         r.dq.data()[i] = static_cast<T>(dq[i]);
-        r.dk.data()[i] = static_cast<T>(dk[i]);
-        r.dv.data()[i] = static_cast<T>(dv[i]);
+        r.dk.data()[i] = static_cast<T>(dkg[i]);
     }
+    for (std::size_t i = 0; i < n * dv; ++i) r.dv.data()[i] = static_cast<T>(dvg[i]);
     r.counters = detail::counters_for(prep, variant, 1);
     return r;
 }

@@ -78,6 +78,8 @@ SIGNATURES = {
     "bbm_sums_metadata": (C.c_int, [u32p, C.c_uint64, C.c_uint64, C.c_uint64, C.c_int, u8p, u32p, u32p, C.POINTER(BlockStatsC)]),
     "bbm_attn_bwd": (C.c_int, [vp, C.c_int, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, C.c_uint64, C.c_uint32, C.c_double, vp]),
     "bbm_attn_bwd_host_f32": (C.c_int, [vp, C.c_int, f32p, f32p, f32p, f32p, f64p, f64p, f32p, f32p, f32p, f32p, C.c_uint64, C.c_uint32, C.c_double]),
+    "bbm_attn_bwd_host_f32_dims": (C.c_int, [vp, C.c_int, f32p, f32p, f32p, f32p, f64p, f64p, f32p, f32p, f32p, f32p,
+                                             C.c_uint64, C.c_uint32, C.c_uint32, C.c_double]),
     "bbm_permute_rows_host": (C.c_int, [vp, vp, u32p, C.c_uint64, C.c_uint64, C.c_uint64, C.c_int, C.c_int]),
     "bbm_permute_mask_host": (C.c_int, [u64p, u64p, u32p, C.c_uint64, C.c_int]),
     "bbm_graph_csr": (C.c_int, [u64p, C.c_uint64, u64p, u32p]),
@@ -90,6 +92,9 @@ SIGNATURES = {
     "bbm_attn_fwd_host_f32": (C.c_int, [vp, C.c_int, f32p, f32p, f32p, f32p, f64p, f64p, C.c_uint64, C.c_uint32, C.c_double]),
     "bbm_run_attention_host_f32": (C.c_int, [vp, C.c_int, C.POINTER(vp), C.POINTER(vp), C.POINTER(vp), C.POINTER(vp),
                                              C.POINTER(vp), C.POINTER(vp), C.c_uint64, C.c_uint32, C.c_double]),
+    "bbm_run_attention_host_f32_dims": (C.c_int, [vp, C.c_int, C.POINTER(vp), C.POINTER(vp), C.POINTER(vp),
+                                                  C.POINTER(vp), C.POINTER(vp), C.POINTER(vp), C.c_uint64,
+                                                  C.c_uint32, C.c_uint32, C.c_double]),
     "bbm_run_attention_multi": (C.c_int, [vp, C.c_int, C.c_int, C.POINTER(C.c_int), u16p, u16p, u16p, u16p, f32p, f32p, C.c_uint64, C.c_uint32, C.c_double, f64p]),
     "bbm_set_trace": (C.c_int, [vp, C.c_uint32]),
     "bbm_set_fwd_kernel": (C.c_int, [C.c_int]),

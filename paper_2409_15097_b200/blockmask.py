@@ -530,30 +530,53 @@ def set_fwd_kernel(mode: str) -> None:
     check(lib.bbm_set_fwd_kernel(modes[mode]))
 
 
+def _check_head_dims(dk: int, dv: int) -> None:
+    """validate_forward_args (engine.hpp:249-251) plus the documented narrowing d <= 128."""
+    if dk < 1:
+        raise ValueError("q and k must share a positive head dim")
+    if dv < 1:
+        raise ValueError("v must have a positive head dim")
+    if dk > 128 or dv > 128:
+        raise ValueError(f"head dims {dk} / {dv} unsupported by the sm_100a kernel (at most 128)")
+
+
+def _kernel_dim(dk: int, dv: int) -> int:
+    """The kernels' head dim for caller dims d_k, d_v (bbm_internal.h kernel_dim)."""
+    return 128 if max(dk, dv) > 64 else 64
+
+
+def _pad_cols(t, D: int):
+    """Zero-pad the last dim to D: zero Q/K columns add exact zeros to every score, zero V / dO
+    columns give output columns that are cropped away."""
+    if t.shape[-1] == D:
+        return t
+    import torch.nn.functional as F
+    return F.pad(t, (0, D - t.shape[-1]))
+
+
 def blocked_forward(q, k, v, scale: float, mask, prep: MaskPrep, variant: Variant,
                     threads: int = 1, check_finite: bool = True) -> ForwardResult:
     """blocked_forward (engine.hpp:282-341) on the sm_100a kernel.
 
     q, k, v: CUDA bf16 tensors [n, d] or [slots, n, d] (device path, result stays on device), or
     numpy float arrays [n, d] (host path, like Matrix<float>; rounded to bf16 on the device).
-    d must be 64 or 128 and d_v == d_k (documented narrowing of the reference)."""
+    Head dims d_k (q, k) and d_v (v, out) may differ; both at most 128 (documented narrowing: the
+    kernels hold one 128-column head-dim tile). Dims other than 64 / 128 run zero-padded."""
     _validate_common(prep, mask, scale, threads)
     n = prep.n_tokens
     if isinstance(q, np.ndarray):
         return _blocked_forward_host(q, k, v, scale, prep, variant)
     import torch
 
-    shapes = {tuple(t.shape[-2:]) for t in (q, k, v)}
     if q.shape[-2] != n or k.shape[-2] != n or v.shape[-2] != n:
         raise ValueError("q/k/v row count must match mask size")
     if q.shape[-1] != k.shape[-1] or q.shape[-1] < 1:
         raise ValueError("q and k must share a positive head dim")
     if v.shape[-1] < 1:
         raise ValueError("v must have a positive head dim")
-    if len(shapes) != 1:
-        raise ValueError(f"head dims {sorted(shapes)} unsupported: the sm_100a kernel needs d_v == d_k")
-    if not (q.shape == k.shape == v.shape) or q.dim() not in (2, 3):
-        raise ValueError("q, k and v must share one [n, d] or [slots, n, d] shape")
+    if q.shape != k.shape or q.shape[:-1] != v.shape[:-1] or q.dim() not in (2, 3):
+        raise ValueError("q, k and v must share one [n, d] or [slots, n, d] shape (v may differ in d)")
+    _check_head_dims(q.shape[-1], v.shape[-1])
     if not (q.device == k.device == v.device) or not q.is_cuda:
         raise ValueError("q, k and v must live on one CUDA device")
     if check_finite:
@@ -562,13 +585,17 @@ def blocked_forward(q, k, v, scale: float, mask, prep: MaskPrep, variant: Varian
                 raise ValueError(f"{name} must hold finite values")
     squeeze = q.dim() == 2
     q3, k3, v3 = (t.unsqueeze(0) if squeeze else t for t in (q, k, v))
-    q3, k3, v3 = (t.to(torch.bfloat16).contiguous() for t in (q3, k3, v3))
-    slots, _, d = q3.shape
-    out = torch.empty_like(q3)
+    dv = v3.shape[-1]
+    D = _kernel_dim(q3.shape[-1], dv)
+    q3, k3, v3 = (_pad_cols(t.to(torch.bfloat16), D).contiguous() for t in (q3, k3, v3))
+    slots = q3.shape[0]
+    out = torch.empty_like(v3)
     rmax = torch.empty((slots, n), dtype=torch.float32, device=q3.device)
     rsum = torch.empty((slots, n), dtype=torch.float32, device=q3.device)
     with torch.cuda.device(q3.device):
         attn_fwd_device(prep, variant, q3, k3, v3, out, rmax, rsum, scale)
+    if dv != D:
+        out = out[..., :dv].contiguous()
     counters = prep.counters(variant, slots)
     if squeeze:
         out, rmax, rsum = out[0], rmax[0], rsum[0]
@@ -584,17 +611,23 @@ def _blocked_forward_host(q, k, v, scale, prep, variant) -> ForwardResult:
     qa, ka, va = arrs
     if qa.shape[1] != n or ka.shape[1] != n or va.shape[1] != n:
         raise ValueError("q/k/v row count must match mask size")
-    if qa.shape[2] != ka.shape[2]:
+    if qa.shape[2] != ka.shape[2] or qa.shape[2] < 1:
         raise ValueError("q and k must share a positive head dim")
-    if va.shape[2] != qa.shape[2]:
-        raise ValueError("head dims unsupported: the sm_100a kernel needs d_v == d_k")
-    slots, _, d = qa.shape
-    out = np.empty_like(qa)
+    if va.shape[2] < 1:
+        raise ValueError("v must have a positive head dim")
+    if not (qa.shape[0] == ka.shape[0] == va.shape[0]):
+        raise ValueError("q, k and v must hold the same number of slots")
+    slots, _, dk = qa.shape
+    dv = va.shape[2]
+    _check_head_dims(dk, dv)
+    out = np.empty((slots, n, dv), np.float32)
     rmax = np.empty((slots, n), np.float64)
     rsum = np.empty((slots, n), np.float64)
-    check(lib.bbm_attn_fwd_host_f32(prep.handle.h, int(variant), ptr(qa, C.c_float), ptr(ka, C.c_float),
-                                    ptr(va, C.c_float), ptr(out, C.c_float), ptr(rmax, C.c_double),
-                                    ptr(rsum, C.c_double), slots, d, float(scale)))
+    # per-slot pointers (run_attention's storage, engine.hpp:489-505)
+    vpa = lambda a, w: (C.c_void_p * slots)(*[a.ctypes.data + i * n * w * a.itemsize for i in range(slots)])  # noqa: E731
+    check(lib.bbm_run_attention_host_f32_dims(prep.handle.h, int(variant), vpa(qa, dk), vpa(ka, dk), vpa(va, dv),
+                                              vpa(out, dv), vpa(rmax, 1), vpa(rsum, 1), slots, dk, dv,
+                                              float(scale)))
     counters = prep.counters(variant, slots)
     if squeeze:
         out, rmax, rsum = out[0], rmax[0], rsum[0]
@@ -637,38 +670,47 @@ def blocked_backward(q, k, v, scale: float, mask, prep: MaskPrep, variant: Varia
         if squeeze:
             arrs = [a[None] for a in arrs]
         qa, ka, va, oa, ga = arrs
-        slots, _, d = qa.shape
-        for a in (ka, va, oa, ga):
-            if a.shape != qa.shape:
-                raise ValueError("q, k, v, out, d_out must share one shape (d_v == d_k on the sm_100a kernel)")
+        slots, _, dk = qa.shape
+        dv = va.shape[2]
+        if ka.shape != qa.shape or oa.shape != va.shape or ga.shape != va.shape or va.shape[:2] != qa.shape[:2]:
+            raise ValueError("q, k must share [slots][n][d_k]; v, out, d_out [slots][n][d_v]")
         if qa.shape[1] != n:
             raise ValueError("q/k/v row count must match mask size")
+        _check_head_dims(dk, dv)
         rm = np.ascontiguousarray(np.asarray(fwd.row_max, np.float64).reshape(slots, n))
         rs = np.ascontiguousarray(np.asarray(fwd.row_sum, np.float64).reshape(slots, n))
-        dq, dk, dv = (np.empty_like(qa) for _ in range(3))
-        check(lib.bbm_attn_bwd_host_f32(prep.handle.h, int(variant), ptr(qa, C.c_float), ptr(ka, C.c_float),
-                                        ptr(va, C.c_float), ptr(oa, C.c_float), ptr(rm, C.c_double),
-                                        ptr(rs, C.c_double), ptr(ga, C.c_float), ptr(dq, C.c_float),
-                                        ptr(dk, C.c_float), ptr(dv, C.c_float), slots, d, float(scale)))
+        gq, gk, gv = np.empty_like(qa), np.empty_like(ka), np.empty_like(va)
+        check(lib.bbm_attn_bwd_host_f32_dims(prep.handle.h, int(variant), ptr(qa, C.c_float), ptr(ka, C.c_float),
+                                             ptr(va, C.c_float), ptr(oa, C.c_float), ptr(rm, C.c_double),
+                                             ptr(rs, C.c_double), ptr(ga, C.c_float), ptr(gq, C.c_float),
+                                             ptr(gk, C.c_float), ptr(gv, C.c_float), slots, dk, dv, float(scale)))
         if squeeze:
-            dq, dk, dv = dq[0], dk[0], dv[0]
-        return BackwardResult(dq, dk, dv, prep.counters(variant, slots))
+            gq, gk, gv = gq[0], gk[0], gv[0]
+        return BackwardResult(gq, gk, gv, prep.counters(variant, slots))
     import torch
 
     squeeze = q.dim() == 2
     ts = [t.unsqueeze(0) if squeeze else t for t in (q, k, v, fwd.out, d_out)]
-    if len({tuple(t.shape) for t in ts}) != 1 or ts[0].shape[1] != n:
-        raise ValueError("q, k, v, out, d_out must share one [slots][n][d] shape (d_v == d_k)")
+    if (ts[0].shape != ts[1].shape or len({tuple(t.shape) for t in ts[2:]}) != 1
+            or ts[2].shape[:2] != ts[0].shape[:2] or ts[0].shape[1] != n):
+        raise ValueError("q, k must share [slots][n][d_k]; v, out, d_out [slots][n][d_v]")
+    dk_, dv_ = ts[0].shape[-1], ts[2].shape[-1]
+    _check_head_dims(dk_, dv_)
+    D = _kernel_dim(dk_, dv_)
     for name, t in (("q", q), ("k", k), ("v", v), ("d_out", d_out)):
         if not bool(torch.isfinite(t).all()):
             raise ValueError(f"{name} must hold finite values")
-    q3, k3, v3, o3, g3 = (t.to(torch.bfloat16).contiguous() for t in ts)
-    slots, _, d = q3.shape
+    q3, k3, v3, o3, g3 = (_pad_cols(t.to(torch.bfloat16), D).contiguous() for t in ts)
+    slots = q3.shape[0]
     rm = torch.as_tensor(fwd.row_max, device=q3.device).reshape(slots, n).float().contiguous()
     rs = torch.as_tensor(fwd.row_sum, device=q3.device).reshape(slots, n).float().contiguous()
     dq, dk, dv = (torch.empty_like(q3) for _ in range(3))
     with torch.cuda.device(q3.device):
         attn_bwd_device(prep, variant, q3, k3, v3, o3, rm, rs, g3, dq, dk, dv, scale)
+    if D != dk_:
+        dq, dk = dq[..., :dk_].contiguous(), dk[..., :dk_].contiguous()
+    if D != dv_:
+        dv = dv[..., :dv_].contiguous()
     if squeeze:
         dq, dk, dv = dq[0], dk[0], dv[0]
     return BackwardResult(dq, dk, dv, prep.counters(variant, slots))

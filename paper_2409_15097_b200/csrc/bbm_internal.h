@@ -348,11 +348,23 @@ void run_fwd_host_pipelined(const Prep& prep, int variant, const uint16_t* q, co
                             const uint16_t* v, uint16_t* out, float* row_max, float* row_sum,
                             uint64_t slots, uint32_t d, float scale, int num_sms, double* span_ms);
 // the reference's Matrix<float> signature: per-slot float host buffers in, float out, double row
-// statistics (row_max / row_sum arrays, or their entries, may be null); synchronous
+// statistics (row_max / row_sum arrays, or their entries, may be null); synchronous. Any head dims
+// d_k, d_v <= 128: the kernel runs at kernel_dim(d_k, d_v) with the inputs zero-padded on the
+// device (zero Q/K columns add exact zeros to every score, zero V columns give output columns
+// that are dropped).
 void run_fwd_host_f32(const Prep& prep, int variant, const float* const* q, const float* const* k,
                       const float* const* v, float* const* out, double* const* row_max,
-                      double* const* row_sum, uint64_t slots, uint32_t d, float scale, int num_sms,
-                      double* span_ms);
+                      double* const* row_sum, uint64_t slots, uint32_t d_k, uint32_t d_v, float scale,
+                      int num_sms, double* span_ms);
+// the kernels' head dim for caller dims d_k, d_v in [1, 128]
+inline uint32_t kernel_dim(uint32_t d_k, uint32_t d_v) { return (d_k > 64 || d_v > 64) ? 128u : 64u; }
+// row-pitch changes between the caller's dims and the kernel's (host_io.cu), on stream s:
+// float [rows][w] -> bf16 [rows][D] (zero columns w..D-1; RNE; any inf / NaN sets *bad if non-null),
+// float [rows][w] -> float [rows][D] (zero-padded), bf16 [rows][D] -> float [rows][w] (cropped)
+void launch_pad_to_bf16(const float* in, void* out, uint64_t rows, uint32_t w, uint32_t D, int* bad,
+                        cudaStream_t s);
+void launch_pad_f32(const float* in, float* out, uint64_t rows, uint32_t w, uint32_t D, cudaStream_t s);
+void launch_crop_to_f32(const void* in, float* out, uint64_t rows, uint32_t D, uint32_t w, cudaStream_t s);
 // the RCM path end to end: original-order host buffers, prep built from the permuted mask
 void run_fwd_host_rcm(const Prep& prep, int variant, const uint32_t* forward, const uint16_t* q,
                       const uint16_t* k, const uint16_t* v, uint16_t* out, float* row_max,

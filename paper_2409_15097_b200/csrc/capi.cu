@@ -304,17 +304,35 @@ bbm_prep wrap(Prep* p) {
   return h;
 }
 
-void check_attn_args(const Prep& pr, int variant, uint64_t slots, uint32_t d, double scale) {
+void check_common_args(int variant, uint64_t slots, double scale) {
   require(variant >= 0 && variant <= 3, "unknown variant");
   require(slots >= 1, "need at least one batch/head slot");  // engine.hpp:493
   require(std::isfinite(scale), "scale must be finite");     // engine.hpp:253
   // documented narrowing: the kernels scale scores in fp32 log2 units
   require(std::isfinite(static_cast<float>(scale) * 1.4426950408889634f),
           "scale outside the fp32 range of the sm_100a kernel");
+}
+
+// device-pointer entries: the caller's layout is the kernel's, [slots][n][64 | 128]
+void check_attn_args(const Prep& pr, int variant, uint64_t slots, uint32_t d, double scale) {
+  check_common_args(variant, slots, scale);
   if (d != 64 && d != 128)
     throw ArgError("head dim " + std::to_string(d) +
-                   " unsupported by the sm_100a kernel (64 or 128; d_v must equal d_k)");
+                   " unsupported by the device-pointer entries (64 or 128; the float host-buffer"
+                   " entries take any d_k, d_v <= 128)");
   (void)pr;
+}
+
+// float host-buffer entries (validate_forward_args, engine.hpp:244-258): any positive d_k, d_v up
+// to 128 (documented narrowing: the kernels hold one 128-column head-dim tile); the device copy is
+// zero-padded to kernel_dim(d_k, d_v)
+void check_host_dims(int variant, uint64_t slots, uint32_t d_k, uint32_t d_v, double scale) {
+  check_common_args(variant, slots, scale);
+  require(d_k >= 1, "q and k must share a positive head dim");
+  require(d_v >= 1, "v must have a positive head dim");
+  if (d_k > 128 || d_v > 128)
+    throw ArgError("head dims " + std::to_string(d_k) + " / " + std::to_string(d_v) +
+                   " unsupported by the sm_100a kernel (at most 128)");
 }
 
 __global__ void f32_to_bf16_kernel(const float* __restrict__ in, __nv_bfloat16* __restrict__ out,
@@ -325,13 +343,6 @@ __global__ void f32_to_bf16_kernel(const float* __restrict__ in, __nv_bfloat16* 
     if (!isfinite(x)) *bad = 1;
     out[i] = __float2bfloat16_rn(x);
   }
-}
-
-__global__ void bf16_to_f32_kernel(const __nv_bfloat16* __restrict__ in, float* __restrict__ out,
-                                   uint64_t count) {
-  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < count;
-       i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
-    out[i] = __bfloat162float(in[i]);
 }
 
 // Permutation::from_forward (reorder.hpp:57-68): forward must be a bijection on [0, n)
@@ -869,7 +880,7 @@ bbm_status bbm_attn_fwd_host_f32(bbm_prep prep, int variant, const float* q, con
                                  uint64_t slots, uint32_t head_dim, double scale) {
   return guarded([&] {
     const Prep& pr = unwrap(prep);
-    check_attn_args(pr, variant, slots, head_dim, scale);
+    check_host_dims(variant, slots, head_dim, head_dim, scale);
     require(q && k && v && out, "null tensor pointer");
     const uint64_t per = pr.n * head_dim;
     std::vector<const float*> pq(slots), pk(slots), pv(slots);
@@ -885,7 +896,24 @@ bbm_status bbm_attn_fwd_host_f32(bbm_prep prep, int variant, const float* q, con
     }
     DeviceGuard g(pr.device);
     run_fwd_host_f32(pr, variant, pq.data(), pk.data(), pv.data(), po.data(), pm.data(), ps.data(),
-                     slots, head_dim, static_cast<float>(scale), sm_count(pr.device), nullptr);
+                     slots, head_dim, head_dim, static_cast<float>(scale), sm_count(pr.device), nullptr);
+  });
+}
+
+bbm_status bbm_run_attention_host_f32_dims(bbm_prep prep, int variant, const float* const* q,
+                                           const float* const* k, const float* const* v,
+                                           float* const* out, double* const* row_max,
+                                           double* const* row_sum, uint64_t slots, uint32_t d_k,
+                                           uint32_t d_v, double scale) {
+  return guarded([&] {
+    const Prep& pr = unwrap(prep);
+    check_host_dims(variant, slots, d_k, d_v, scale);
+    require(q && k && v && out, "null slot array");
+    for (uint64_t i = 0; i < slots; ++i)
+      require(q[i] && k[i] && v[i] && out[i], "null tensor pointer in slot " + std::to_string(i));
+    DeviceGuard g(pr.device);
+    run_fwd_host_f32(pr, variant, q, k, v, out, row_max, row_sum, slots, d_k, d_v,
+                     static_cast<float>(scale), sm_count(pr.device), nullptr);
   });
 }
 
@@ -894,16 +922,8 @@ bbm_status bbm_run_attention_host_f32(bbm_prep prep, int variant, const float* c
                                       float* const* out, double* const* row_max,
                                       double* const* row_sum, uint64_t slots, uint32_t head_dim,
                                       double scale) {
-  return guarded([&] {
-    const Prep& pr = unwrap(prep);
-    check_attn_args(pr, variant, slots, head_dim, scale);
-    require(q && k && v && out, "null slot array");
-    for (uint64_t i = 0; i < slots; ++i)
-      require(q[i] && k[i] && v[i] && out[i], "null tensor pointer in slot " + std::to_string(i));
-    DeviceGuard g(pr.device);
-    run_fwd_host_f32(pr, variant, q, k, v, out, row_max, row_sum, slots, head_dim,
-                     static_cast<float>(scale), sm_count(pr.device), nullptr);
-  });
+  return bbm_run_attention_host_f32_dims(prep, variant, q, k, v, out, row_max, row_sum, slots, head_dim,
+                                         head_dim, scale);
 }
 
 bbm_status bbm_attn_bwd(bbm_prep prep, int variant, const void* q, const void* k, const void* v,
@@ -924,18 +944,20 @@ bbm_status bbm_attn_bwd(bbm_prep prep, int variant, const void* q, const void* k
   });
 }
 
-bbm_status bbm_attn_bwd_host_f32(bbm_prep prep, int variant, const float* q, const float* k,
-                                 const float* v, const float* out, const double* row_max,
-                                 const double* row_sum, const float* d_out, float* dq, float* dk,
-                                 float* dv, uint64_t slots, uint32_t head_dim, double scale) {
+bbm_status bbm_attn_bwd_host_f32_dims(bbm_prep prep, int variant, const float* q, const float* k,
+                                      const float* v, const float* out, const double* row_max,
+                                      const double* row_sum, const float* d_out, float* dq, float* dk,
+                                      float* dv, uint64_t slots, uint32_t d_k, uint32_t d_v, double scale) {
   return guarded([&] {
     const Prep& pr = unwrap(prep);
-    check_attn_args(pr, variant, slots, head_dim, scale);
+    check_host_dims(variant, slots, d_k, d_v, scale);
     require(q && k && v && out && row_max && row_sum && d_out && dq && dk && dv, "null tensor pointer");
     DeviceGuard g(pr.device);
     cudaStream_t s;
     BBM_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
-    const uint64_t elems = slots * pr.n * head_dim, rows = slots * pr.n;
+    // D: the kernels' head dim; q, k, dq, dk are d_k wide, v, out, d_out, dv are d_v wide
+    const uint32_t D = kernel_dim(d_k, d_v);
+    const uint64_t rows = slots * pr.n, elems = rows * D;
     std::vector<void*> owned;
     auto alloc = [&](uint64_t bytes) {
       void* p = nullptr;
@@ -960,12 +982,22 @@ bbm_status bbm_attn_bwd_host_f32(bbm_prep prep, int variant, const float* q, con
       int* bad = static_cast<int*>(alloc(16));
       BBM_CUDA(cudaMemsetAsync(bad, 0, 16, s));
       const float* srcs[4] = {q, k, v, d_out};
+      const uint32_t w_in[4] = {d_k, d_k, d_v, d_v};
       for (int t = 0; t < 4; ++t) {
-        BBM_CUDA(cudaMemcpyAsync(stage, srcs[t], elems * 4, cudaMemcpyHostToDevice, s));
-        f32_to_bf16_kernel<<<grid_of(elems), 256, 0, s>>>(stage, b[t], elems, bad + t);
-        BBM_CUDA(cudaGetLastError());
+        BBM_CUDA(cudaMemcpyAsync(stage, srcs[t], rows * w_in[t] * 4, cudaMemcpyHostToDevice, s));
+        if (w_in[t] == D) {
+          f32_to_bf16_kernel<<<grid_of(elems), 256, 0, s>>>(stage, b[t], elems, bad + t);
+          BBM_CUDA(cudaGetLastError());
+        } else {
+          launch_pad_to_bf16(stage, b[t], rows, w_in[t], D, bad + t, s);
+        }
       }
-      BBM_CUDA(cudaMemcpyAsync(o32, out, elems * 4, cudaMemcpyHostToDevice, s));
+      if (d_v == D) {
+        BBM_CUDA(cudaMemcpyAsync(o32, out, elems * 4, cudaMemcpyHostToDevice, s));
+      } else {
+        BBM_CUDA(cudaMemcpyAsync(stage, out, rows * d_v * 4, cudaMemcpyHostToDevice, s));
+        launch_pad_f32(stage, o32, rows, d_v, D, s);
+      }
       std::vector<float> hm(rows), hs(rows);
       for (uint64_t i = 0; i < rows; ++i) {
         hm[i] = static_cast<float>(row_max[i]);
@@ -979,14 +1011,14 @@ bbm_status bbm_attn_bwd_host_f32(bbm_prep prep, int variant, const float* q, con
       static const char* names[4] = {"q", "k", "v", "d_out"};
       for (int t = 0; t < 4; ++t)  // require_finite (engine.hpp:237-242, 358)
         if (hbad[t]) throw ArgError(std::string(names[t]) + " must hold finite values");
-      BwdArgs a{b[0], b[1], b[2], o32, true, rm, rs, b[3], g3[0], g3[1], g3[2], slots, pr.n, head_dim,
+      BwdArgs a{b[0], b[1], b[2], o32, true, rm, rs, b[3], g3[0], g3[1], g3[2], slots, pr.n, D,
                 static_cast<float>(scale), variant};
       launch_attn_bwd(pr, a, s, sm_count(pr.device));
       float* dsts[3] = {dq, dk, dv};
+      const uint32_t w_out[3] = {d_k, d_k, d_v};
       for (int t = 0; t < 3; ++t) {
-        bf16_to_f32_kernel<<<grid_of(elems), 256, 0, s>>>(g3[t], stage, elems);
-        BBM_CUDA(cudaGetLastError());
-        BBM_CUDA(cudaMemcpyAsync(dsts[t], stage, elems * 4, cudaMemcpyDeviceToHost, s));
+        launch_crop_to_f32(g3[t], stage, rows, D, w_out[t], s);
+        BBM_CUDA(cudaMemcpyAsync(dsts[t], stage, rows * w_out[t] * 4, cudaMemcpyDeviceToHost, s));
         BBM_CUDA(cudaStreamSynchronize(s));
       }
     } catch (...) {
@@ -995,6 +1027,14 @@ bbm_status bbm_attn_bwd_host_f32(bbm_prep prep, int variant, const float* q, con
     }
     release();
   });
+}
+
+bbm_status bbm_attn_bwd_host_f32(bbm_prep prep, int variant, const float* q, const float* k,
+                                 const float* v, const float* out, const double* row_max,
+                                 const double* row_sum, const float* d_out, float* dq, float* dk,
+                                 float* dv, uint64_t slots, uint32_t head_dim, double scale) {
+  return bbm_attn_bwd_host_f32_dims(prep, variant, q, k, v, out, row_max, row_sum, d_out, dq, dk, dv, slots,
+                                    head_dim, head_dim, scale);
 }
 
 bbm_status bbm_run_attention_multi(bbm_prep prep, int variant, int n_devices, const int* devices,

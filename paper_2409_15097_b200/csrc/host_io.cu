@@ -213,6 +213,51 @@ __global__ void widen_outputs_kernel(const __nv_bfloat16* __restrict__ o, float*
   }
 }
 
+// Row-pitch changes for head dims the kernels do not tile natively (d_k / d_v below 64, between 64
+// and 128, or unequal): one thread per destination element, off the hot path.
+__global__ void pad_to_bf16_kernel(const float* __restrict__ in, __nv_bfloat16* __restrict__ out,
+                                   uint64_t rows, uint32_t w, uint32_t D, int* __restrict__ bad) {
+  bool any = false;
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < rows * D;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint64_t r = i / D;
+    const uint32_t c = static_cast<uint32_t>(i - r * D);
+    const float x = c < w ? in[r * w + c] : 0.0f;
+    any |= !isfinite(x);
+    out[i] = __float2bfloat16_rn(x);
+  }
+  if (bad && __any_sync(0xffffffffu, any) && (threadIdx.x & 31) == 0) *bad = 1;
+}
+
+__global__ void pad_f32_kernel(const float* __restrict__ in, float* __restrict__ out, uint64_t rows,
+                               uint32_t w, uint32_t D) {
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < rows * D;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint64_t r = i / D;
+    const uint32_t c = static_cast<uint32_t>(i - r * D);
+    out[i] = c < w ? in[r * w + c] : 0.0f;
+  }
+}
+
+__global__ void crop_to_f32_kernel(const __nv_bfloat16* __restrict__ in, float* __restrict__ out,
+                                   uint64_t rows, uint32_t D, uint32_t w) {
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < rows * w;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint64_t r = i / w;
+    out[i] = __bfloat162float(in[r * D + (i - r * w)]);
+  }
+}
+
+// fp32 row statistics -> double
+__global__ void widen_stats_kernel(const float* __restrict__ m, const float* __restrict__ l,
+                                   double* __restrict__ md, double* __restrict__ ld, uint64_t rows) {
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < rows;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    if (md) md[i] = static_cast<double>(m[i]);
+    if (ld) ld[i] = static_cast<double>(l[i]);
+  }
+}
+
 unsigned grid_for_elems(uint64_t count) {
   return static_cast<unsigned>(std::max<uint64_t>(1, std::min<uint64_t>((count / 8 + 255) / 256, 148ull * 16)));
 }
@@ -280,6 +325,24 @@ void throw_if_bad(const int* hbad, int count) {
 
 }  // namespace
 
+void launch_pad_to_bf16(const float* in, void* out, uint64_t rows, uint32_t w, uint32_t D, int* bad,
+                        cudaStream_t s) {
+  pad_to_bf16_kernel<<<grid_for_elems(rows * D), 256, 0, s>>>(in, static_cast<__nv_bfloat16*>(out), rows,
+                                                              w, D, bad);
+  BBM_CUDA(cudaGetLastError());
+}
+
+void launch_pad_f32(const float* in, float* out, uint64_t rows, uint32_t w, uint32_t D, cudaStream_t s) {
+  pad_f32_kernel<<<grid_for_elems(rows * D), 256, 0, s>>>(in, out, rows, w, D);
+  BBM_CUDA(cudaGetLastError());
+}
+
+void launch_crop_to_f32(const void* in, float* out, uint64_t rows, uint32_t D, uint32_t w, cudaStream_t s) {
+  crop_to_f32_kernel<<<grid_for_elems(rows * w), 256, 0, s>>>(static_cast<const __nv_bfloat16*>(in), out,
+                                                              rows, D, w);
+  BBM_CUDA(cudaGetLastError());
+}
+
 void run_fwd_host_pipelined(const Prep& prep, int variant, const uint16_t* q, const uint16_t* k,
                             const uint16_t* v, uint16_t* out, float* row_max, float* row_sum,
                             uint64_t slots, uint32_t d, float scale, int num_sms, double* span_ms) {
@@ -346,30 +409,42 @@ void run_fwd_host_pipelined(const Prep& prep, int variant, const uint16_t* q, co
 // three-stream chunk pipeline as the bf16 path; the PCIe traffic is twice the bf16 form's.
 void run_fwd_host_f32(const Prep& prep, int variant, const float* const* q, const float* const* k,
                       const float* const* v, float* const* out, double* const* row_max,
-                      double* const* row_sum, uint64_t slots, uint32_t d, float scale, int num_sms,
-                      double* span_ms) {
+                      double* const* row_sum, uint64_t slots, uint32_t d_k, uint32_t d_v, float scale,
+                      int num_sms, double* span_ms) {
   std::lock_guard<std::mutex> lk(prep.pipe_mu);
   HostPipe& p = pipe_of(prep);
   const bool want_max = row_max && row_max[0], want_sum = row_sum && row_sum[0];
-  const uint64_t n = prep.n, per = n * d, elems = slots * per, rows = slots * n;
-  // f32 in x3 | bf16 q k v o | f32 o | f32 max, sum | f64 max, sum
-  const size_t b_in = elems * 4, b_bf = elems * 2;
-  uint8_t* base = reserve(p, 3 * b_in + 4 * b_bf + b_in + rows * 8 + rows * 16 + 256);
-  float* fin[3] = {reinterpret_cast<float*>(base), nullptr, nullptr};
-  fin[1] = fin[0] + elems;
-  fin[2] = fin[1] + elems;
-  __nv_bfloat16* bq = reinterpret_cast<__nv_bfloat16*>(fin[2] + elems);
-  __nv_bfloat16* bk = bq + elems;
-  __nv_bfloat16* bv = bk + elems;
-  __nv_bfloat16* bo = bv + elems;
-  float* fo = reinterpret_cast<float*>(bo + elems);
-  float* fmax = fo + elems;
-  float* fsum = fmax + rows;
-  double* dmax = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(fsum + rows) + 15) / 16 * 16);
+  // D: the kernel's head dim; w[t]: the caller's row width of q, k, v (and d_v of out)
+  const uint32_t D = kernel_dim(d_k, d_v), w[3] = {d_k, d_k, d_v};
+  const bool padded = d_k != D || d_v != D;
+  const uint64_t n = prep.n, per = n * D, elems = slots * per, rows = slots * n;
+  // f32 in q k v | bf16 q k v o | f32 o | f32 max, sum | f64 max, sum; every piece 256-B aligned
+  // (the TMA descriptors need 16-B aligned bases; caller widths need not be multiples of 4)
+  const size_t b_in[3] = {rows * w[0] * 4, rows * w[1] * 4, rows * w[2] * 4}, b_bf = elems * 2;
+  auto al = [](size_t b) { return (b + 255) / 256 * 256; };
+  const size_t sizes[11] = {b_in[0], b_in[1], b_in[2], b_bf, b_bf, b_bf, b_bf, b_in[2], rows * 4, rows * 4, rows * 16};
+  size_t total = 0;
+  for (size_t z : sizes) total += al(z);
+  uint8_t* cur = reserve(p, total);
+  auto take = [&](size_t b) {
+    uint8_t* r = cur;
+    cur += al(b);
+    return r;
+  };
+  float* fin[3];
+  for (int t = 0; t < 3; ++t) fin[t] = reinterpret_cast<float*>(take(b_in[t]));
+  __nv_bfloat16* bq = reinterpret_cast<__nv_bfloat16*>(take(b_bf));
+  __nv_bfloat16* bk = reinterpret_cast<__nv_bfloat16*>(take(b_bf));
+  __nv_bfloat16* bv = reinterpret_cast<__nv_bfloat16*>(take(b_bf));
+  __nv_bfloat16* bo = reinterpret_cast<__nv_bfloat16*>(take(b_bf));
+  float* fo = reinterpret_cast<float*>(take(b_in[2]));
+  float* fmax = reinterpret_cast<float*>(take(rows * 4));
+  float* fsum = reinterpret_cast<float*>(take(rows * 4));
+  double* dmax = reinterpret_cast<double*>(take(rows * 16));
   double* dsum = dmax + rows;
   BBM_CUDA(cudaMemsetAsync(p.bad, 0, 4 * sizeof(int), p.comp));
   const uint64_t chunks =
-      std::max<uint64_t>(1, std::min<uint64_t>({slots, kMaxChunks, (3 * b_in) / kChunkBytes}));
+      std::max<uint64_t>(1, std::min<uint64_t>({slots, kMaxChunks, (b_in[0] + b_in[1] + b_in[2]) / kChunkBytes}));
   cudaEvent_t t0 = nullptr, t1 = nullptr;
   if (span_ms) {
     BBM_CUDA(cudaEventCreate(&t0));
@@ -380,8 +455,9 @@ void run_fwd_host_f32(const Prep& prep, int variant, const float* const* q, cons
   __nv_bfloat16* dst[3] = {bq, bk, bv};
   // Per chunk, the first nh slots are converted to bf16 by host threads into a pinned staging
   // buffer (half the PCIe bytes), the rest cross PCIe as float and are converted on the device.
-  // The host converts chunk c while the copy engines and the SMs work on chunks c-1, c-2.
-  const double frac = host_convert_fraction(q[0]);
+  // The host converts chunk c while the copy engines and the SMs work on chunks c-1, c-2. Padded
+  // head dims convert everything on the device (the row-pitch change rides on the conversion).
+  const double frac = padded ? 0.0 : host_convert_fraction(q[0]);
   const uint64_t max_ns = (slots + chunks - 1) / chunks;
   const uint64_t max_nh = std::min<uint64_t>(max_ns, static_cast<uint64_t>(frac * static_cast<double>(max_ns) + 0.5));
   if (max_nh > 0) {
@@ -422,26 +498,37 @@ void run_fwd_host_f32(const Prep& prep, int variant, const float* const* q, cons
     }
     for (uint64_t sl = s0 + nh; sl < s1; ++sl)
       for (int t = 0; t < 3; ++t)
-        BBM_CUDA(cudaMemcpyAsync(fin[t] + sl * per, src[t][sl], per * 4, cudaMemcpyHostToDevice, p.h2d));
+        BBM_CUDA(cudaMemcpyAsync(fin[t] + sl * n * w[t], src[t][sl], n * w[t] * 4, cudaMemcpyHostToDevice, p.h2d));
     BBM_CUDA(cudaEventRecord(p.ev_in[c], p.h2d));
     BBM_CUDA(cudaStreamWaitEvent(p.comp, p.ev_in[c], 0));
     if (ns > nh) {
-      const uint64_t doff = (s0 + nh) * per;
-      for (int t = 0; t < 3; ++t)
-        f32_to_bf16_check_kernel<<<grid_for_elems((ns - nh) * per), 256, 0, p.comp>>>(
-            fin[t] + doff, dst[t] + doff, (ns - nh) * per, p.bad + t);
+      const uint64_t r0 = (s0 + nh) * n, nr = (ns - nh) * n;
+      for (int t = 0; t < 3; ++t) {
+        if (padded)
+          launch_pad_to_bf16(fin[t] + r0 * w[t], dst[t] + r0 * D, nr, w[t], D, p.bad + t, p.comp);
+        else
+          f32_to_bf16_check_kernel<<<grid_for_elems(nr * D), 256, 0, p.comp>>>(fin[t] + r0 * D, dst[t] + r0 * D,
+                                                                               nr * D, p.bad + t);
+      }
       BBM_CUDA(cudaGetLastError());
     }
-    AttnArgs a{bq + off, bk + off, bv + off, bo + off, fmax + s0 * n, fsum + s0 * n, ns, n, d, scale, variant};
+    AttnArgs a{bq + off, bk + off, bv + off, bo + off, fmax + s0 * n, fsum + s0 * n, ns, n, D, scale, variant};
     launch_attn_fwd(prep, a, p.comp, num_sms);
-    widen_outputs_kernel<<<grid_for_elems(ns * per), 256, 0, p.comp>>>(
-        bo + off, fo + off, ns * per, fmax + s0 * n, fsum + s0 * n, want_max ? dmax + s0 * n : nullptr,
-        want_sum ? dsum + s0 * n : nullptr, ns * n);
+    if (padded) {
+      launch_crop_to_f32(bo + off, fo + s0 * n * d_v, ns * n, D, d_v, p.comp);
+      widen_stats_kernel<<<grid_for_elems(ns * n), 256, 0, p.comp>>>(
+          fmax + s0 * n, fsum + s0 * n, want_max ? dmax + s0 * n : nullptr, want_sum ? dsum + s0 * n : nullptr,
+          ns * n);
+    } else {
+      widen_outputs_kernel<<<grid_for_elems(ns * per), 256, 0, p.comp>>>(
+          bo + off, fo + off, ns * per, fmax + s0 * n, fsum + s0 * n, want_max ? dmax + s0 * n : nullptr,
+          want_sum ? dsum + s0 * n : nullptr, ns * n);
+    }
     BBM_CUDA(cudaGetLastError());
     BBM_CUDA(cudaEventRecord(p.ev_out[c], p.comp));
     BBM_CUDA(cudaStreamWaitEvent(p.d2h, p.ev_out[c], 0));
     for (uint64_t sl = s0; sl < s1; ++sl) {
-      BBM_CUDA(cudaMemcpyAsync(out[sl], fo + sl * per, per * 4, cudaMemcpyDeviceToHost, p.d2h));
+      BBM_CUDA(cudaMemcpyAsync(out[sl], fo + sl * n * d_v, n * d_v * 4, cudaMemcpyDeviceToHost, p.d2h));
       if (want_max) BBM_CUDA(cudaMemcpyAsync(row_max[sl], dmax + sl * n, n * 8, cudaMemcpyDeviceToHost, p.d2h));
       if (want_sum) BBM_CUDA(cudaMemcpyAsync(row_sum[sl], dsum + sl * n, n * 8, cudaMemcpyDeviceToHost, p.d2h));
     }

@@ -2,9 +2,9 @@
 // (include/blockmask/*.hpp), which call libbbm's C ABI and run on the B200.
 //
 // Mirrors proj/tests/test_mask_model.cpp, test_engine.cpp and test_reorder.cpp case by case
-// (file:line beside each). Differences, by design of the sm_100a engine: head dims are 64 / 128
-// (the reference's tests use 3..8), and outputs are compared with a double-precision naive
-// attention at the bf16 tolerance (2e-2) instead of 1e-12.
+// (file:line beside each). Differences, by design of the sm_100a engine: head dims are at most
+// 128 (zero-padded on the device to 64 / 128), and outputs are compared with a double-precision
+// naive attention at the bf16 tolerance (2e-2) instead of 1e-12.
 //
 //   g++ -std=c++20 -O1 -Iinclude tests/cpp/test_dropin.cpp -Lpaper_2409_15097_b200 -lbbm
 //       -Wl,-rpath,$PWD/paper_2409_15097_b200 -o build/test_dropin && build/test_dropin
@@ -58,13 +58,14 @@ struct Problem {
 
 // bf16-exact inputs (multiples of 1/64 in [-1, 1)), so the device's bf16 rounding is lossless and
 // the double naive oracle sees exactly what the kernel sees
-Problem make_problem(std::size_t n, std::size_t d, uint64_t seed) {
+Problem make_problem(std::size_t n, std::size_t d, uint64_t seed, std::size_t dv = 0) {
+  if (dv == 0) dv = d;
   uint64_t s = seed * 0x9E3779B97F4A7C15ull + 1;
   auto next = [&] {
     s = s * 6364136223846793005ull + 1442695040888963407ull;
     return static_cast<float>(static_cast<int>((s >> 33) % 128) - 64) / 64.0f;
   };
-  Problem p{Matrix<float>(n, d), Matrix<float>(n, d), Matrix<float>(n, d), Matrix<float>(n, d),
+  Problem p{Matrix<float>(n, d), Matrix<float>(n, d), Matrix<float>(n, dv), Matrix<float>(n, dv),
             1.0 / std::sqrt(static_cast<double>(d))};
   for (Matrix<float>* m : {&p.q, &p.k, &p.v, &p.g})
     for (std::size_t i = 0; i < m->size(); ++i) m->data()[i] = next();
@@ -77,8 +78,8 @@ struct Naive {
   std::vector<double> m, l;
 };
 Naive naive(const Problem& p, const Mask& mask, bool dense) {
-  const std::size_t n = mask.size(), d = p.q.cols();
-  Naive r{Matrix<double>(n, d), Matrix<double>(n, d), Matrix<double>(n, d), Matrix<double>(n, d),
+  const std::size_t n = mask.size(), d = p.q.cols(), dv = p.v.cols();
+  Naive r{Matrix<double>(n, dv), Matrix<double>(n, d), Matrix<double>(n, d), Matrix<double>(n, dv),
           std::vector<double>(n), std::vector<double>(n)};
   std::vector<double> s(n), pr(n), dp(n);
   for (std::size_t i = 0; i < n; ++i) {
@@ -101,7 +102,7 @@ Naive naive(const Problem& p, const Mask& mask, bool dense) {
       if (!dense && !mask.get(i, j)) continue;
       pr[j] /= l;
       double t = 0;
-      for (std::size_t c = 0; c < d; ++c) {
+      for (std::size_t c = 0; c < dv; ++c) {
         r.out(i, c) += pr[j] * p.v(j, c);
         t += double(p.g(i, c)) * p.v(j, c);
       }
@@ -114,8 +115,8 @@ Naive naive(const Problem& p, const Mask& mask, bool dense) {
       for (std::size_t c = 0; c < d; ++c) {
         r.dq(i, c) += p.scale * ds * p.k(j, c);
         r.dk(j, c) += p.scale * ds * p.q(i, c);
-        r.dv(j, c) += pr[j] * p.g(i, c);
       }
+      for (std::size_t c = 0; c < dv; ++c) r.dv(j, c) += pr[j] * p.g(i, c);
     }
   }
   return r;
@@ -277,6 +278,28 @@ int main() {
       for (std::size_t c = 0; c < 64; ++c) EXPECT(f.out(i, c) == 0.0f);
     }
   });
+  run("EngineForward.ValueHeadDimMayDifferFromKeyDim (test_engine.cpp:198-209) + other head dims", [] {
+    struct Dims { std::size_t n, dk, dv; };
+    for (Dims dm : {Dims{21, 5, 3}, Dims{130, 3, 100}, Dims{200, 96, 96}, Dims{77, 128, 7}}) {
+      const Mask mask = gen_causal(dm.n);
+      const MaskPrep prep = preprocess_mask(mask, BlockSpec{8, 8});
+      Problem p = make_problem(dm.n, dm.dk, 13 + dm.dk, dm.dv);
+      p.scale = 0.4;
+      const Naive want = naive(p, mask, false);
+      const auto f = blocked_forward(p.q, p.k, p.v, p.scale, mask, prep, Variant::binblk);
+      EXPECT(f.out.rows() == dm.n && f.out.cols() == dm.dv);
+      EXPECT(rel(f.out, want.out) <= 2e-2);
+      const auto b = blocked_backward(p.q, p.k, p.v, p.scale, mask, prep, Variant::binblk, f, p.g);
+      EXPECT(b.dq.cols() == dm.dk && b.dk.cols() == dm.dk && b.dv.cols() == dm.dv);
+      EXPECT(rel(b.dq, want.dq) <= 2e-2 && rel(b.dk, want.dk) <= 2e-2 && rel(b.dv, want.dv) <= 2e-2);
+      // Matrix<double> goes through the same entry
+      Matrix<double> qd(dm.n, dm.dk), kd(dm.n, dm.dk), vd(dm.n, dm.dv);
+      for (std::size_t i = 0; i < qd.size(); ++i) qd.data()[i] = p.q.data()[i], kd.data()[i] = p.k.data()[i];
+      for (std::size_t i = 0; i < vd.size(); ++i) vd.data()[i] = p.v.data()[i];
+      const auto fd = blocked_forward(qd, kd, vd, p.scale, mask, prep, Variant::binblk);
+      for (std::size_t i = 0; i < vd.size(); ++i) EXPECT(fd.out.data()[i] == static_cast<double>(f.out.data()[i]));
+    }
+  });
   run("Engine.MultiSlotMatchesPerSlot (test_engine.cpp:323-347)", [] {
     const Mask mask = gen_longformer_global(300, 20, 3);
     const MaskPrep prep = preprocess_mask(mask, BlockSpec{64, 64});
@@ -301,8 +324,9 @@ int main() {
     EXPECT_THROW_INVALID(blocked_forward(p.q, p.k, p.v, std::nan(""), mask, prep, Variant::binblk));
     EXPECT_THROW_INVALID(blocked_forward(p.q, p.k, p.v, 0.1, mask, prep, Variant::binblk, 0));
     EXPECT_THROW_INVALID(blocked_forward(p.q, p.k, p.v, 0.1, gen_causal(64), prep, Variant::binblk));
-    Matrix<float> small(128, 5);
-    EXPECT_THROW_INVALID(blocked_forward(small, small, small, 0.1, mask, prep, Variant::binblk));
+    Matrix<float> wide(128, 129), empty(128, 0);  // above the kernels' 128-column head-dim tile; zero
+    EXPECT_THROW_INVALID(blocked_forward(wide, wide, wide, 0.1, mask, prep, Variant::binblk));
+    EXPECT_THROW_INVALID(blocked_forward(empty, empty, p.v, 0.1, mask, prep, Variant::binblk));
     p.k(3, 4) = std::numeric_limits<float>::infinity();
     EXPECT_THROW_INVALID(blocked_forward(p.q, p.k, p.v, 0.1, mask, prep, Variant::binblk));
     EXPECT_THROW_INVALID(parse_variant("sparse"));

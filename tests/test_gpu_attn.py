@@ -193,8 +193,8 @@ def test_validation_errors(cuda):  # test_engine.cpp:349-385
         bbm.blocked_forward(q, k, v, 0.1, mask, wrong, bbm.Variant.binblk)
     with pytest.raises(ValueError):
         bbm.blocked_forward(q[:, :-1], k, v, 0.1, mask, prep, bbm.Variant.binblk)
-    with pytest.raises(ValueError):  # documented narrowing: d in {64,128}
-        z = torch.zeros((1, n, 32), dtype=torch.bfloat16, device=cuda)
+    with pytest.raises(ValueError):  # documented narrowing: d <= 128 (smaller dims run padded)
+        z = torch.zeros((1, n, 160), dtype=torch.bfloat16, device=cuda)
         bbm.blocked_forward(z, z, z, 0.1, mask, prep, bbm.Variant.binblk)
     with pytest.raises(ValueError):
         bbm.run_attention([], 0.1, mask, prep, bbm.Variant.binblk)
