@@ -26,6 +26,7 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <cstdlib>
 
 #include "bbm_internal.h"
 #include "bbm_sort.cuh"
@@ -36,6 +37,16 @@ namespace {
 constexpr uint32_t kPlanThreads = 512;
 constexpr uint32_t kMinUnit = 16;
 
+// minimum split unit in tiles (BBM_MIN_UNIT overrides, for experiments)
+uint32_t min_unit() {
+  static const uint32_t v = [] {
+    const char* e = std::getenv("BBM_MIN_UNIT");
+    const long x = e ? std::atol(e) : 0;
+    return x >= 1 && x <= 1024 ? static_cast<uint32_t>(x) : kMinUnit;
+  }();
+  return v;
+}
+
 struct PlanArgs {
   int cls;
   uint32_t krows, kcols;
@@ -43,7 +54,7 @@ struct PlanArgs {
   const uint32_t* list;
   const uint8_t* halves;  // nullptr for the column view
   uint64_t slots;
-  uint32_t workers;
+  uint32_t workers, min_unit;
   uint64_t cap_chunks;  // bound on slots * split chunks (workspace blocks)
   uint32_t cap_units, cap_split;
   PlanHdr* hdr;
@@ -69,7 +80,7 @@ __global__ void __launch_bounds__(kPlanThreads) plan_kernel(const PlanArgs a) {
   for (uint32_t p = threadIdx.x; p < a.krows; p += kPlanThreads) my += occ_of(p);
   const unsigned long long total = block_sum<kPlanThreads>(my) * a.slots;
   uint64_t L = (total / max(1u, a.workers) + 1) / 2;
-  if (L < kMinUnit) L = kMinUnit;
+  if (L < a.min_unit) L = a.min_unit;
   // full tiles (list entries with bit 31): the forward's choice of softmax engine build
   unsigned long long fl = 0, hv = 0;
   if (a.cls == kPlanList)
@@ -153,7 +164,7 @@ uint64_t plan_cap_chunks(uint64_t slots, uint32_t workers) {
 }
 
 uint32_t plan_cap_units(uint32_t krows, uint32_t kcols, uint64_t slots, uint32_t workers) {
-  if (kcols <= kMinUnit) return krows;  // L >= 16 tiles: no row can split
+  if (kcols <= min_unit()) return krows;  // L >= min_unit tiles: no row can split
   const uint64_t extra = plan_cap_chunks(slots, workers) / std::max<uint64_t>(1, slots) + 1;
   return static_cast<uint32_t>(std::min<uint64_t>(krows + extra, static_cast<uint64_t>(krows) * 256));
 }
@@ -169,6 +180,7 @@ void build_plan(const TileView& v, int cls, uint64_t slots, uint32_t workers, De
   a.halves = v.halves;
   a.slots = slots;
   a.workers = workers;
+  a.min_unit = min_unit();
   a.cap_chunks = plan_cap_chunks(slots, workers);
   a.cap_units = plan.cap_units;
   a.cap_split = plan.cap_split;
