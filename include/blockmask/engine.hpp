@@ -250,23 +250,31 @@ BackwardResult<T> blocked_backward(const Matrix<T>& q, const Matrix<T>& k, const
     require(fwd.out.rows() == n && fwd.out.cols() == dv, "forward output shape mismatch");
     require(fwd.row_max.size() == n && fwd.row_sum.size() == n, "forward row stats missing");
     require(d_out.rows() == n && d_out.cols() == dv, "d_out shape must match the output");
-    std::vector<float> hq, hk, hv, ho, hdo;
-    detail::append_f32(hq, q), detail::append_f32(hk, k), detail::append_f32(hv, v);
-    detail::append_f32(ho, fwd.out), detail::append_f32(hdo, d_out);
-    std::vector<float> dq(n * dk), dkg(n * dk), dvg(n * dv);
-    device::check(bbm_attn_bwd_host_f32_dims(prep.device->get(), static_cast<int>(variant), hq.data(),
-                                             hk.data(), hv.data(), ho.data(), fwd.row_max.data(),
-                                             fwd.row_sum.data(), hdo.data(), dq.data(), dkg.data(),
-                                             dvg.data(), 1, static_cast<std::uint32_t>(dk),
-                                             static_cast<std::uint32_t>(dv), scale),
-                  "blocked_backward");
     BackwardResult<T> r;
     r.dq = Matrix<T>(n, dk), r.dk = Matrix<T>(n, dk), r.dv = Matrix<T>(n, dv);
-    for (std::size_t i = 0; i < n * dk; ++i) {
-        r.dq.data()[i] = static_cast<T>(dq[i]);
-        r.dk.data()[i] = static_cast<T>(dkg[i]);
+    const auto run = [&](const float* hq, const float* hk, const float* hv, const float* ho, const float* hdo,
+                         float* gq, float* gk, float* gv) {
+        device::check(bbm_attn_bwd_host_f32_dims(prep.device->get(), static_cast<int>(variant), hq, hk, hv, ho,
+                                                 fwd.row_max.data(), fwd.row_sum.data(), hdo, gq, gk, gv, 1,
+                                                 static_cast<std::uint32_t>(dk), static_cast<std::uint32_t>(dv),
+                                                 scale),
+                      "blocked_backward");
+    };
+    if constexpr (std::is_same_v<T, float>) {
+        // Matrix<float>: the caller's storage in, the BackwardResult's storage out, no copies
+        run(q.data(), k.data(), v.data(), fwd.out.data(), d_out.data(), r.dq.data(), r.dk.data(), r.dv.data());
+    } else {  // Matrix<double>: narrowed to float for the upload
+        std::vector<float> hq, hk, hv, ho, hdo;
+        detail::append_f32(hq, q), detail::append_f32(hk, k), detail::append_f32(hv, v);
+        detail::append_f32(ho, fwd.out), detail::append_f32(hdo, d_out);
+        std::vector<float> gq(n * dk), gk(n * dk), gv(n * dv);
+        run(hq.data(), hk.data(), hv.data(), ho.data(), hdo.data(), gq.data(), gk.data(), gv.data());
+        for (std::size_t i = 0; i < n * dk; ++i) {
+            r.dq.data()[i] = static_cast<T>(gq[i]);
+            r.dk.data()[i] = static_cast<T>(gk[i]);
+        }
+        for (std::size_t i = 0; i < n * dv; ++i) r.dv.data()[i] = static_cast<T>(gv[i]);
     }
-    for (std::size_t i = 0; i < n * dv; ++i) r.dv.data()[i] = static_cast<T>(dvg[i]);
     r.counters = detail::counters_for(prep, variant, 1);
     return r;
 }

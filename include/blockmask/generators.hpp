@@ -6,6 +6,7 @@
 
 #include <cstdint>
 #include <cstdio>
+#include <random>  // the reference's header brings std::mt19937_64 along (callers rely on it)
 #include <sstream>
 #include <span>
 #include <string>
@@ -143,6 +144,11 @@ inline double spec_double(const std::string& t) {
     require(used == t.size(), "bad number in mask spec: '" + t + "'");
     return v;
 }
+// the reference's names for the same helpers (generators.hpp:276-308; its bench.hpp parses CSV
+// rows with them)
+inline std::vector<std::string> split(const std::string& text, char sep) { return split_on(text, sep); }
+inline std::size_t parse_size(const std::string& text) { return spec_size(text); }
+inline double parse_double(const std::string& text) { return spec_double(text); }
 // key=value;key=value -> visits (key, value), rejecting items without '='
 template <class F>
 void spec_params(const std::string& body, F&& on) {

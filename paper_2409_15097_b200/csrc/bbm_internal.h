@@ -356,6 +356,12 @@ void run_fwd_host_f32(const Prep& prep, int variant, const float* const* q, cons
                       const float* const* v, float* const* out, double* const* row_max,
                       double* const* row_sum, uint64_t slots, uint32_t d_k, uint32_t d_v, float scale,
                       int num_sms, double* span_ms);
+// blocked_backward over float host buffers (q, k, dq, dk: d_k wide; v, out, d_out, dv: d_v wide),
+// double row statistics; synchronous, on the prep's pipeline stream and buffers
+void run_bwd_host_f32(const Prep& prep, int variant, const float* q, const float* k, const float* v,
+                      const float* out, const double* row_max, const double* row_sum, const float* d_out,
+                      float* dq, float* dk, float* dv, uint64_t slots, uint32_t d_k, uint32_t d_v,
+                      float scale, int num_sms);
 // the kernels' head dim for caller dims d_k, d_v in [1, 128]
 inline uint32_t kernel_dim(uint32_t d_k, uint32_t d_v) { return (d_k > 64 || d_v > 64) ? 128u : 64u; }
 // row-pitch changes between the caller's dims and the kernel's (host_io.cu), on stream s:

@@ -335,16 +335,6 @@ void check_host_dims(int variant, uint64_t slots, uint32_t d_k, uint32_t d_v, do
                    " unsupported by the sm_100a kernel (at most 128)");
 }
 
-__global__ void f32_to_bf16_kernel(const float* __restrict__ in, __nv_bfloat16* __restrict__ out,
-                                   uint64_t count, int* __restrict__ bad) {
-  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < count;
-       i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
-    const float x = in[i];
-    if (!isfinite(x)) *bad = 1;
-    out[i] = __float2bfloat16_rn(x);
-  }
-}
-
 // Permutation::from_forward (reorder.hpp:57-68): forward must be a bijection on [0, n)
 void check_bijection(const uint32_t* fwd, uint64_t n) {
   std::vector<char> seen(n, 0);
@@ -352,11 +342,6 @@ void check_bijection(const uint32_t* fwd, uint64_t n) {
     require(fwd[a] < n && !seen[fwd[a]], "forward map is not a bijection");
     seen[fwd[a]] = 1;
   }
-}
-
-unsigned grid_of(uint64_t count) {
-  uint64_t g = (count + 255) / 256;
-  return static_cast<unsigned>(std::max<uint64_t>(1, std::min<uint64_t>(g, 148ull * 16)));
 }
 
 // Creation: the kernel view is queued on `s`; publish the first version and compute the
@@ -953,79 +938,8 @@ bbm_status bbm_attn_bwd_host_f32_dims(bbm_prep prep, int variant, const float* q
     check_host_dims(variant, slots, d_k, d_v, scale);
     require(q && k && v && out && row_max && row_sum && d_out && dq && dk && dv, "null tensor pointer");
     DeviceGuard g(pr.device);
-    cudaStream_t s;
-    BBM_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
-    // D: the kernels' head dim; q, k, dq, dk are d_k wide, v, out, d_out, dv are d_v wide
-    const uint32_t D = kernel_dim(d_k, d_v);
-    const uint64_t rows = slots * pr.n, elems = rows * D;
-    std::vector<void*> owned;
-    auto alloc = [&](uint64_t bytes) {
-      void* p = nullptr;
-      BBM_CUDA(cudaMallocAsync(&p, std::max<uint64_t>(bytes, 16), s));
-      owned.push_back(p);
-      return p;
-    };
-    auto release = [&] {
-      for (void* p : owned) cudaFreeAsync(p, s);
-      cudaStreamSynchronize(s);
-      cudaStreamDestroy(s);
-    };
-    try {
-      float* stage = static_cast<float*>(alloc(elems * 4));
-      float* o32 = static_cast<float*>(alloc(elems * 4));
-      __nv_bfloat16* b[4];
-      for (auto& x : b) x = static_cast<__nv_bfloat16*>(alloc(elems * 2));  // q k v dO
-      __nv_bfloat16* g3[3];
-      for (auto& x : g3) x = static_cast<__nv_bfloat16*>(alloc(elems * 2));  // dq dk dv
-      float* rm = static_cast<float*>(alloc(rows * 4));
-      float* rs = static_cast<float*>(alloc(rows * 4));
-      int* bad = static_cast<int*>(alloc(16));
-      BBM_CUDA(cudaMemsetAsync(bad, 0, 16, s));
-      const float* srcs[4] = {q, k, v, d_out};
-      const uint32_t w_in[4] = {d_k, d_k, d_v, d_v};
-      for (int t = 0; t < 4; ++t) {
-        BBM_CUDA(cudaMemcpyAsync(stage, srcs[t], rows * w_in[t] * 4, cudaMemcpyHostToDevice, s));
-        if (w_in[t] == D) {
-          f32_to_bf16_kernel<<<grid_of(elems), 256, 0, s>>>(stage, b[t], elems, bad + t);
-          BBM_CUDA(cudaGetLastError());
-        } else {
-          launch_pad_to_bf16(stage, b[t], rows, w_in[t], D, bad + t, s);
-        }
-      }
-      if (d_v == D) {
-        BBM_CUDA(cudaMemcpyAsync(o32, out, elems * 4, cudaMemcpyHostToDevice, s));
-      } else {
-        BBM_CUDA(cudaMemcpyAsync(stage, out, rows * d_v * 4, cudaMemcpyHostToDevice, s));
-        launch_pad_f32(stage, o32, rows, d_v, D, s);
-      }
-      std::vector<float> hm(rows), hs(rows);
-      for (uint64_t i = 0; i < rows; ++i) {
-        hm[i] = static_cast<float>(row_max[i]);
-        hs[i] = static_cast<float>(row_sum[i]);
-      }
-      BBM_CUDA(cudaMemcpyAsync(rm, hm.data(), rows * 4, cudaMemcpyHostToDevice, s));
-      BBM_CUDA(cudaMemcpyAsync(rs, hs.data(), rows * 4, cudaMemcpyHostToDevice, s));
-      int hbad[4] = {0, 0, 0, 0};
-      BBM_CUDA(cudaMemcpyAsync(hbad, bad, 16, cudaMemcpyDeviceToHost, s));
-      BBM_CUDA(cudaStreamSynchronize(s));
-      static const char* names[4] = {"q", "k", "v", "d_out"};
-      for (int t = 0; t < 4; ++t)  // require_finite (engine.hpp:237-242, 358)
-        if (hbad[t]) throw ArgError(std::string(names[t]) + " must hold finite values");
-      BwdArgs a{b[0], b[1], b[2], o32, true, rm, rs, b[3], g3[0], g3[1], g3[2], slots, pr.n, D,
-                static_cast<float>(scale), variant};
-      launch_attn_bwd(pr, a, s, sm_count(pr.device));
-      float* dsts[3] = {dq, dk, dv};
-      const uint32_t w_out[3] = {d_k, d_k, d_v};
-      for (int t = 0; t < 3; ++t) {
-        launch_crop_to_f32(g3[t], stage, rows, D, w_out[t], s);
-        BBM_CUDA(cudaMemcpyAsync(dsts[t], stage, rows * w_out[t] * 4, cudaMemcpyDeviceToHost, s));
-        BBM_CUDA(cudaStreamSynchronize(s));
-      }
-    } catch (...) {
-      release();
-      throw;
-    }
-    release();
+    run_bwd_host_f32(pr, variant, q, k, v, out, row_max, row_sum, d_out, dq, dk, dv, slots, d_k, d_v,
+                     static_cast<float>(scale), sm_count(pr.device));
   });
 }
 

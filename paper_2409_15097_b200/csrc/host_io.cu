@@ -549,6 +549,75 @@ void run_fwd_host_f32(const Prep& prep, int variant, const float* const* q, cons
   throw_if_bad(hbad, 3);
 }
 
+// blocked_backward with the reference's storage (engine.hpp:346-471): float host q, k, v, out,
+// d_out, double row statistics, float gradients out. Runs on the prep's persistent pipeline
+// stream and buffers (no per-call stream, allocation or launch-context setup); q, k, v, d_out are
+// rounded to bf16 on the device with the finiteness check fused, out stays fp32 for
+// delta = rowsum(d_out * out); head dims other than the kernel's are zero-padded / cropped.
+void run_bwd_host_f32(const Prep& prep, int variant, const float* q, const float* k, const float* v,
+                      const float* out, const double* row_max, const double* row_sum, const float* d_out,
+                      float* dq, float* dk, float* dv, uint64_t slots, uint32_t d_k, uint32_t d_v,
+                      float scale, int num_sms) {
+  std::lock_guard<std::mutex> lk(prep.pipe_mu);
+  HostPipe& p = pipe_of(prep);
+  cudaStream_t s = p.comp;
+  const uint32_t D = kernel_dim(d_k, d_v);
+  const uint64_t rows = slots * prep.n, elems = rows * D;
+  auto al = [](size_t b) { return (b + 255) / 256 * 256; };
+  uint8_t* cur = reserve(p, 2 * al(elems * 4) + 7 * al(elems * 2) + 2 * al(rows * 4));
+  auto take = [&](size_t b) {
+    uint8_t* r = cur;
+    cur += al(b);
+    return r;
+  };
+  float* stage = reinterpret_cast<float*>(take(elems * 4));
+  float* o32 = reinterpret_cast<float*>(take(elems * 4));
+  __nv_bfloat16* b[4];  // q k v dO
+  for (auto& x : b) x = reinterpret_cast<__nv_bfloat16*>(take(elems * 2));
+  __nv_bfloat16* g3[3];  // dq dk dv
+  for (auto& x : g3) x = reinterpret_cast<__nv_bfloat16*>(take(elems * 2));
+  float* rm = reinterpret_cast<float*>(take(rows * 4));
+  float* rs = reinterpret_cast<float*>(take(rows * 4));
+  BBM_CUDA(cudaMemsetAsync(p.bad, 0, 4 * sizeof(int), s));
+  const float* srcs[4] = {q, k, v, d_out};
+  const uint32_t w_in[4] = {d_k, d_k, d_v, d_v};
+  for (int t = 0; t < 4; ++t) {
+    BBM_CUDA(cudaMemcpyAsync(stage, srcs[t], rows * w_in[t] * 4, cudaMemcpyHostToDevice, s));
+    if (w_in[t] == D) {
+      f32_to_bf16_check_kernel<<<grid_for_elems(elems), 256, 0, s>>>(stage, b[t], elems, p.bad + t);
+      BBM_CUDA(cudaGetLastError());
+    } else {
+      launch_pad_to_bf16(stage, b[t], rows, w_in[t], D, p.bad + t, s);
+    }
+  }
+  if (d_v == D) {
+    BBM_CUDA(cudaMemcpyAsync(o32, out, elems * 4, cudaMemcpyHostToDevice, s));
+  } else {
+    BBM_CUDA(cudaMemcpyAsync(stage, out, rows * d_v * 4, cudaMemcpyHostToDevice, s));
+    launch_pad_f32(stage, o32, rows, d_v, D, s);
+  }
+  std::vector<float> hst(2 * rows);
+  for (uint64_t i = 0; i < rows; ++i) {
+    hst[i] = static_cast<float>(row_max[i]);
+    hst[rows + i] = static_cast<float>(row_sum[i]);
+  }
+  BBM_CUDA(cudaMemcpyAsync(rm, hst.data(), rows * 4, cudaMemcpyHostToDevice, s));
+  BBM_CUDA(cudaMemcpyAsync(rs, hst.data() + rows, rows * 4, cudaMemcpyHostToDevice, s));
+  int hbad[4] = {0, 0, 0, 0};
+  BBM_CUDA(cudaMemcpyAsync(hbad, p.bad, 4 * sizeof(int), cudaMemcpyDeviceToHost, s));
+  BBM_CUDA(cudaStreamSynchronize(s));  // hst, hbad
+  throw_if_bad(hbad, 4);  // require_finite (engine.hpp:237-242, 358)
+  BwdArgs a{b[0], b[1], b[2], o32, true, rm, rs, b[3], g3[0], g3[1], g3[2], slots, prep.n, D, scale, variant};
+  launch_attn_bwd(prep, a, s, num_sms);
+  float* dsts[3] = {dq, dk, dv};
+  const uint32_t w_out[3] = {d_k, d_k, d_v};
+  for (int t = 0; t < 3; ++t) {  // stream order: each widening follows the previous download
+    launch_crop_to_f32(g3[t], stage, rows, D, w_out[t], s);
+    BBM_CUDA(cudaMemcpyAsync(dsts[t], stage, rows * w_out[t] * 4, cudaMemcpyDeviceToHost, s));
+  }
+  BBM_CUDA(cudaStreamSynchronize(s));
+}
+
 // The RCM path end to end (reorder.hpp:156-189 + bench.hpp:448-467): the caller's Q/K/V are in
 // the ORIGINAL token order, `prep` was built from permute_mask(mask, perm), forward = perm's
 // new -> old map. Per slot chunk: H2D, the forward with the permutation applied on the device
