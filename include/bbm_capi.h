@@ -156,8 +156,10 @@ bbm_status bbm_attn_fwd(bbm_prep prep, int variant, const void* q, const void* k
  * results: mode 1 permutes Q/K/V into per-stream scratch (4 x slots*n*d bf16 + 2 x slots*n fp32),
  * runs the plain kernel and scatters O / row stats back (HBM-bound passes); mode 2 gathers each
  * tile's rows inside the kernel with TMA tile::gather4 and scatters O with tile::scatter4 (no
- * scratch; bound by the TMA instruction rate; requires slots * n < 2^31). bbm_attn_fwd_gather =
- * mode 0 = the faster one on B200 (mode 1; env BBM_GATHER=tma selects mode 2). */
+ * scratch; bound by the TMA instruction rate; requires slots * n < 2^31); mode 3 permutes only K
+ * and V into scratch (2 x slots*n*d bf16) and gathers Q / scatters O inside the kernel.
+ * bbm_attn_fwd_gather = mode 0 = the default, the fastest on B200: mode 3 (env
+ * BBM_GATHER=passes|tma|hybrid overrides). */
 bbm_status bbm_attn_fwd_gather(bbm_prep prep, int variant, const uint32_t* d_forward, const void* q,
                                const void* k, const void* v, void* out, float* row_max, float* row_sum,
                                uint64_t slots, uint32_t head_dim, double scale, void* stream);

@@ -44,6 +44,7 @@
 #include <cstdint>
 #include <cstdlib>
 #include <string>
+#include <type_traits>
 #include <vector>
 
 #include "bbm_internal.h"
@@ -252,12 +253,15 @@ __device__ __forceinline__ uint64_t out_row(const FwdParams& p, uint32_t slot, u
   return static_cast<uint64_t>(slot) * p.n + (kGather ? __ldg(p.rows + grow) : grow);
 }
 
-template <int D, int MODE, bool kTrace, bool kGather, bool kSkip>
+template <int D, int MODE, bool kTrace, int kGather, bool kSkip>
 __global__ void __launch_bounds__(kThreadsOf<D>, 1)
     attn_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                     const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_o,
                     const __grid_constant__ CUtensorMap tm_k64, const __grid_constant__ CUtensorMap tm_v64,
                     const FwdParams p) {
+  // kGather: 0 plain tiles; 1 every Q / K / V row gathered and O scattered in the kernel
+  // (tile::gather4 / scatter4); 2 only Q gathered and O scattered, K / V from permuted copies
+  constexpr bool kGQ = kGather != 0, kGKV = kGather == 1;
   using C = Cfg<D>;
   extern __shared__ __align__(1024) uint8_t smem[];
   uint8_t* sq = smem;                              // [2][tile]          Q, double-buffered
@@ -339,8 +343,8 @@ __global__ void __launch_bounds__(kThreadsOf<D>, 1)
       // one 128 x D tile (row tile `tile` of `slot`) into dst, completing on `bar` (expect-tx
       // already posted by lane 0)
       auto issue_tile = [&](uint8_t* dst, const CUtensorMap* tm, uint64_t* bar, uint32_t tile, uint32_t slot,
-                            uint64_t pol) {
-        if constexpr (kGather) {
+                            uint64_t pol, auto gather) {
+        if constexpr (decltype(gather)::value) {
           int32_t r[4];
 #pragma unroll
           for (uint32_t i = 0; i < 4; ++i) r[i] = gather_row(p, slot, tile * 128 + lane * 4 + i);
@@ -383,7 +387,7 @@ __global__ void __launch_bounds__(kThreadsOf<D>, 1)
         }
         __syncwarp();
         if (half == 0) {
-          issue_tile(ring + r * C::kTileBytes, tm, full, q, slot, pol_kv);
+          issue_tile(ring + r * C::kTileBytes, tm, full, q, slot, pol_kv, std::bool_constant<kGKV>{});
         } else if (lane == 0) {
           const uint32_t hh = (half & 1u) ? 1u : 0u;  // the half that is loaded
           for (uint32_t b = 0; b < C::kBoxes; ++b)
@@ -416,12 +420,12 @@ __global__ void __launch_bounds__(kThreadsOf<D>, 1)
           if (d.nt == 0) continue;
           pit[pw++ % kQueue] = d;
           kentry = entry_of<MODE>(p, d.rt, d.j0);
-          khalf = half_of<MODE, kGather, kSkip>(p, d.rt, d.j0);
+          khalf = half_of<MODE, kGKV, kSkip>(p, d.rt, d.j0);
           mbar_wait(&ctl->q_empty[qb], qph[qb]);
           qph.flip(qb);
           if (lane == 0) mbar_arrive_expect_tx(&ctl->q_full[qb], C::kTileBytes);
           __syncwarp();
-          issue_tile(sq + qb * C::kTileBytes, &tm_q, &ctl->q_full[qb], d.rt, d.slot, pol_q);
+          issue_tile(sq + qb * C::kTileBytes, &tm_q, &ctl->q_full[qb], d.rt, d.slot, pol_q, std::bool_constant<kGQ>{});
           if (lane == 0) trace_ev<kTrace>(tracing, p, &ctl->trace_count, 1, 0, d.t);
           qb ^= 1;
           kit = d;
@@ -435,7 +439,7 @@ __global__ void __launch_bounds__(kThreadsOf<D>, 1)
         // the next list entry is fetched now, a full issue step before it is needed
         if (kj + 1 < kit.nt) {
           kentry = entry_of<MODE>(p, kit.rt, kit.j0 + kj + 1);
-          khalf = half_of<MODE, kGather, kSkip>(p, kit.rt, kit.j0 + kj + 1);
+          khalf = half_of<MODE, kGKV, kSkip>(p, kit.rt, kit.j0 + kj + 1);
         }
         load_tile(&tm_k, &tm_k64, kseq_of(kk), cur & 0x7FFFFFFFu, kit.slot, 2, kj, chalf);
         ++kk;
@@ -451,13 +455,13 @@ __global__ void __launch_bounds__(kThreadsOf<D>, 1)
           vit = pit[pr++ % kQueue];
           vj = 0;
           ventry = entry_of<MODE>(p, vit.rt, vit.j0);
-          vhalf = half_of<MODE, kGather, kSkip>(p, vit.rt, vit.j0);
+          vhalf = half_of<MODE, kGKV, kSkip>(p, vit.rt, vit.j0);
           v_need = false;
         }
         const uint32_t cur = ventry, chalf = vhalf;
         if (vj + 1 < vit.nt) {
           ventry = entry_of<MODE>(p, vit.rt, vit.j0 + vj + 1);
-          vhalf = half_of<MODE, kGather, kSkip>(p, vit.rt, vit.j0 + vj + 1);
+          vhalf = half_of<MODE, kGKV, kSkip>(p, vit.rt, vit.j0 + vj + 1);
         }
         load_tile(&tm_v, &tm_v64, vseq_of(vk), cur & 0x7FFFFFFFu, vit.slot, 3, vj, chalf);
         ++vk;
@@ -595,7 +599,7 @@ __global__ void __launch_bounds__(kThreadsOf<D>, 1)
     auto write_stats = [&](const ItemDesc& it, float m_true2, float m_run2, float l_tot) {
       const uint64_t grow = static_cast<uint64_t>(it.rt) * 128 + row;
       if (half == 0 && grow < p.n) {
-        const uint64_t si = out_row<kGather>(p, it.slot, grow);
+        const uint64_t si = out_row<kGQ>(p, it.slot, grow);
         if (p.row_max) p.row_max[si] = m_true2 == -INFINITY ? -INFINITY : m_true2 * kLn2;
         if (p.row_sum) p.row_sum[si] = l_tot > 0.0f ? l_tot * exp2f(m_run2 - m_true2) : 0.0f;
       }
@@ -604,7 +608,7 @@ __global__ void __launch_bounds__(kThreadsOf<D>, 1)
     auto zero_item = [&](const ItemDesc& it) {
       const uint64_t grow = static_cast<uint64_t>(it.rt) * 128 + row;
       if (grow >= p.n) return;
-      uint4* dst = reinterpret_cast<uint4*>(p.out + out_row<kGather>(p, it.slot, grow) * D + half * kHalfO);
+      uint4* dst = reinterpret_cast<uint4*>(p.out + out_row<kGQ>(p, it.slot, grow) * D + half * kHalfO);
       for (uint32_t v = 0; v < kHalfO / 8; ++v) dst[v] = make_uint4(0, 0, 0, 0);
       write_stats(it, -INFINITY, -INFINITY, 0.0f);
     };
@@ -833,7 +837,7 @@ __global__ void __launch_bounds__(kThreadsOf<D>, 1)
     auto write_stats = [&](const ItemDesc& it, float m_true2, float m_run2, float l_tot) {
       const uint64_t grow = static_cast<uint64_t>(it.rt) * 128 + row;
       if (grow < p.n) {
-        const uint64_t si = out_row<kGather>(p, it.slot, grow);
+        const uint64_t si = out_row<kGQ>(p, it.slot, grow);
         if (p.row_max) p.row_max[si] = m_true2 == -INFINITY ? -INFINITY : m_true2 * kLn2;
         if (p.row_sum) p.row_sum[si] = l_tot > 0.0f ? l_tot * exp2f(m_run2 - m_true2) : 0.0f;
       }
@@ -841,11 +845,11 @@ __global__ void __launch_bounds__(kThreadsOf<D>, 1)
     // The O tile leaves one 64-column box at a time through a single staging box: TMA-store box b
     // of item `it` once staged (called by every epilogue thread) ...
     // (gather mode: the first epilogue warp scatters the box's rows, 4 per lane, to their tokens)
-    const bool storer = kGather ? quad == 0 : leader;
+    const bool storer = kGQ ? quad == 0 : leader;
     auto store_box = [&](const ItemDesc& it, uint32_t b) {
       fence_proxy_async_smem();
       named_bar_sync(2, kEpi);
-      if constexpr (kGather) {
+      if constexpr (kGQ) {
         if (quad == 0) {
           int32_t r[4];
 #pragma unroll
@@ -1007,7 +1011,7 @@ __global__ void __launch_bounds__(kThreadsOf<D>, 1)
 
 std::atomic<uint64_t> g_builds[2];  // forward launches per engine build (plain, skipping)
 
-template <int D, int MODE, bool kGather>
+template <int D, int MODE, int kGather>
 void launch_impl(const Prep& prep, const AttnArgs& a, cudaStream_t s, int num_sms) {
   static_assert(smem_bytes<D>() <= 232448, "exceeds the 227 KB opt-in shared memory");
   const KernelMeta& km = prep.kmeta;
@@ -1024,15 +1028,17 @@ void launch_impl(const Prep& prep, const AttnArgs& a, cudaStream_t s, int num_sm
   float* ws = can_split ? ctx_workspace(ctx, plan_cap_chunks(a.slots, workers) * 128 * (128 + 3), s) : nullptr;
   uint32_t* split_ctr = can_split ? ctx_split_ctr(ctx, plan_cap_chunks(a.slots, workers) + a.slots, s) : nullptr;
 
-  // plain: 3-D [slots][n][D] maps with 128-row boxes; gather: 2-D [slots * n][D] row maps
-  auto tmap = [&](const void* base) {
-    return kGather ? make_tmap_bf16_rows(base, D, a.slots * a.n, 64)
-                   : cached_tmap_bf16_3d(base, D, a.n, a.slots, 64, 128);
+  // plain: 3-D [slots][n][D] maps with 128-row boxes; gathered tensors: 2-D [slots * n][D] row maps
+  // (Q and O in both gather modes, K and V only when kGather == 1)
+  constexpr bool kGQ = kGather != 0, kGKV = kGather == 1;
+  auto tmap = [&](const void* base, bool gathered) {
+    return gathered ? make_tmap_bf16_rows(base, D, a.slots * a.n, 64)
+                    : cached_tmap_bf16_3d(base, D, a.n, a.slots, 64, 128);
   };
-  const CUtensorMap tq = tmap(a.q), tk = tmap(a.k), tv = tmap(a.v), to = tmap(a.o);
-  // 64-row boxes for tiles with an empty key half (plain mode only; gather mode never uses them)
-  const CUtensorMap tk64 = kGather ? tk : cached_tmap_bf16_3d(a.k, D, a.n, a.slots, 64, 64);
-  const CUtensorMap tv64 = kGather ? tv : cached_tmap_bf16_3d(a.v, D, a.n, a.slots, 64, 64);
+  const CUtensorMap tq = tmap(a.q, kGQ), tk = tmap(a.k, kGKV), tv = tmap(a.v, kGKV), to = tmap(a.o, kGQ);
+  // 64-row boxes for tiles with an empty key half (plain K / V only)
+  const CUtensorMap tk64 = kGKV ? tk : cached_tmap_bf16_3d(a.k, D, a.n, a.slots, 64, 64);
+  const CUtensorMap tv64 = kGKV ? tv : cached_tmap_bf16_3d(a.v, D, a.n, a.slots, 64, 64);
   FwdParams p{};
   p.rows = a.rows;
   p.n = a.n;
@@ -1067,13 +1073,13 @@ void launch_impl(const Prep& prep, const AttnArgs& a, cudaStream_t s, int num_sm
     if constexpr (kCanSkip)
       BBM_CUDA(cudaFuncSetAttribute(attn_fwd_kernel<D, MODE, false, kGather, true>,
                                     cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes<D>()));
-    if constexpr (!kGather)
-      BBM_CUDA(cudaFuncSetAttribute(attn_fwd_kernel<D, MODE, true, false, false>,
+    if constexpr (kGather == 0)
+      BBM_CUDA(cudaFuncSetAttribute(attn_fwd_kernel<D, MODE, true, 0, false>,
                                     cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes<D>()));
   });
-  if constexpr (!kGather) {
+  if constexpr (kGather == 0) {
     if (p.trace) {  // event-tracing build of the same kernel (bbm_set_trace)
-      attn_fwd_kernel<D, MODE, true, false, false><<<grid, kThreadsOf<D>, smem_bytes<D>(), s>>>(tq, tk, tv, to, tk64, tv64, p);
+      attn_fwd_kernel<D, MODE, true, 0, false><<<grid, kThreadsOf<D>, smem_bytes<D>(), s>>>(tq, tk, tv, to, tk64, tv64, p);
       BBM_CUDA(cudaGetLastError());
       mark_launch_done(ctx, s);
       return;
@@ -1092,7 +1098,7 @@ void launch_impl(const Prep& prep, const AttnArgs& a, cudaStream_t s, int num_sm
   mark_launch_done(ctx, s);
 }
 
-template <int D, bool kGather>
+template <int D, int kGather>
 void launch_d(const Prep& prep, const AttnArgs& a, cudaStream_t s, int num_sms) {
   switch (a.variant) {
     case 0: launch_impl<D, kModeDense, kGather>(prep, a, s, num_sms); break;
@@ -1103,17 +1109,20 @@ void launch_d(const Prep& prep, const AttnArgs& a, cudaStream_t s, int num_sms) 
   }
 }
 
-// Which RCM application a gather launch uses: BBM_GATHER=tma|passes overrides (measurement), the
-// default is the faster one on B200 — the passes: tile::gather4 moves 4 rows (512 B) per TMA
-// instruction and the TMA unit issues one every ~60 cycles, so the in-kernel gather is bound by
-// the TMA instruction rate (C5: 6.4 ms vs 1.5 ms pre-permuted), while the passes are plain
-// HBM-bound copies (Q, K, V in, O and the row statistics out).
+// Which RCM application a gather launch uses: BBM_GATHER=tma|passes|hybrid overrides (measurement).
+// The default is the fastest on B200, the hybrid: K and V are each re-read by several row tiles, so
+// one HBM-bound permute pass each is cheaper than gathering them per tile (tile::gather4 moves 4
+// rows, 512 B, per TMA instruction and the TMA unit issues one every ~60 cycles: the all-in-kernel
+// gather runs C5 in 6.4 ms against 1.4 ms pre-permuted), while Q and O, touched once per item,
+// are gathered / scattered in the kernel instead of costing a pass each (C5: 2.70 ms against
+// 2.84 ms for passes over Q, K, V, O and the row statistics).
 int gather_mode_of(int requested) {
   if (requested != kGatherAuto) return requested;
   static const int env = [] {
     const char* e = std::getenv("BBM_GATHER");
     if (e && std::string(e) == "tma") return static_cast<int>(kGatherTma);
-    return static_cast<int>(kGatherPasses);
+    if (e && std::string(e) == "passes") return static_cast<int>(kGatherPasses);
+    return static_cast<int>(kGatherHybrid);
   }();
   return env;
 }
@@ -1150,6 +1159,25 @@ static void launch_gather_passes(const Prep& prep, const AttnArgs& a, cudaStream
   if (a.row_sum) launch_permute_rows(b.row_sum, a.row_sum, a.rows, a.slots, a.n, 4, true, s);
 }
 
+// Hybrid RCM application: K and V (each tile re-read by several row tiles) permuted into per-stream
+// scratch by one pass each; Q rows gathered (tile::gather4, once per item) and O rows scattered
+// (tile::scatter4) inside the kernel, row statistics written to their original tokens. Same
+// results as the other two modes.
+static void launch_gather_hybrid(const Prep& prep, const AttnArgs& a, cudaStream_t s, int num_sms) {
+  std::lock_guard<std::recursive_mutex> lk(prep.mu);  // the scratch belongs to this stream's context
+  const uint64_t rowb = static_cast<uint64_t>(a.d) * 2;
+  const uint64_t tb = (a.slots * a.n * rowb + 255) / 256 * 256;
+  StreamCtx& ctx = prep.ctx_for(s);
+  uint8_t* base = ctx_perm_scratch(ctx, 2 * tb, s);
+  AttnArgs b = a;
+  b.k = base;
+  b.v = base + tb;
+  launch_permute_rows(a.k, const_cast<void*>(b.k), a.rows, a.slots, a.n, rowb, false, s);
+  launch_permute_rows(a.v, const_cast<void*>(b.v), a.rows, a.slots, a.n, rowb, false, s);
+  if (a.d == 64) launch_d<64, 2>(prep, b, s, num_sms);
+  else launch_d<128, 2>(prep, b, s, num_sms);
+}
+
 void launch_attn_fwd(const Prep& prep, const AttnArgs& a, cudaStream_t s, int num_sms) {
   require(a.slots >= 1, "need at least one batch/head slot");
   require(a.n == prep.n, "mask preprocessing does not match this problem");
@@ -1163,13 +1191,16 @@ void launch_attn_fwd(const Prep& prep, const AttnArgs& a, cudaStream_t s, int nu
   if (launch_attn_fwd_pair(prep, a, s, num_sms)) return;  // only when selected (bbm_set_fwd_kernel)
   if (a.rows && gather_mode_of(a.gather_mode) == kGatherPasses) {
     launch_gather_passes(prep, a, s, num_sms);
+  } else if (a.rows && gather_mode_of(a.gather_mode) == kGatherHybrid) {
+    require(a.slots * a.n < (1ull << 31) - 1, "too many rows for the gather path (slots * n >= 2^31)");
+    launch_gather_hybrid(prep, a, s, num_sms);
   } else if (a.rows) {  // in-kernel RCM gather / scatter of token rows (2-D row coordinates are int32)
     require(a.slots * a.n < (1ull << 31) - 1, "too many rows for the gather path (slots * n >= 2^31)");
-    if (a.d == 64) launch_d<64, true>(prep, a, s, num_sms);
-    else launch_d<128, true>(prep, a, s, num_sms);
+    if (a.d == 64) launch_d<64, 1>(prep, a, s, num_sms);
+    else launch_d<128, 1>(prep, a, s, num_sms);
   } else {
-    if (a.d == 64) launch_d<64, false>(prep, a, s, num_sms);
-    else launch_d<128, false>(prep, a, s, num_sms);
+    if (a.d == 64) launch_d<64, 0>(prep, a, s, num_sms);
+    else launch_d<128, 0>(prep, a, s, num_sms);
   }
 }
 

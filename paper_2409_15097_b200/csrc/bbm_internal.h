@@ -260,11 +260,13 @@ struct AttnArgs {
   // optional in-kernel RCM application (reorder.hpp:156-189): device u32 [n], forward map new ->
   // old. q/k/v/o and the row statistics are then in the ORIGINAL token order while the prep holds
   // the permuted mask: rows are gathered / scattered by TMA inside the kernel (kGatherTma), or
-  // permuted into per-stream scratch by HBM-bound passes around the plain kernel (kGatherPasses).
+  // permuted into per-stream scratch by HBM-bound passes around the plain kernel (kGatherPasses),
+  // or K / V permuted by passes while Q / O rows are gathered / scattered in the kernel
+  // (kGatherHybrid).
   const uint32_t* rows = nullptr;
   int gather_mode = 0;
 };
-enum GatherMode : int { kGatherAuto = 0, kGatherPasses = 1, kGatherTma = 2 };
+enum GatherMode : int { kGatherAuto = 0, kGatherPasses = 1, kGatherTma = 2, kGatherHybrid = 3 };
 // Process-wide kernel event trace (bbm_set_trace): device buffer of ctas * 8192 u64 events.
 struct TraceConfig {
   void* buffer = nullptr;
