@@ -598,12 +598,13 @@ def main():
         if args.which == "fwd" and fwd_perm is not None:
             # f2: the same forward on ORIGINAL-order inputs with the RCM permutation applied on the
             # device (bbm_attn_fwd_gather_ex): permute passes around the plain kernel (mode 1), the
-            # in-kernel TMA tile::gather4 / scatter4 (mode 2) and the default hybrid (mode 3: K/V
-            # passes, Q/O in the kernel), against the pre-permuted forward above
+            # in-kernel TMA tile::gather4 (mode 2), the hybrid (mode 3: K/V passes, Q/O in the
+            # kernel) and the default in-kernel LSU gather (mode 4), against the pre-permuted
+            # forward above
             rows = torch.from_numpy(np.ascontiguousarray(fwd_perm, dtype=np.int32)).to(dev)
             og = torch.empty_like(q)
             rcm = {}
-            for mode, key in ((1, "passes"), (2, "in_kernel_tma"), (3, "hybrid")):
+            for mode, key in ((1, "passes"), (2, "in_kernel_tma"), (3, "hybrid"), (4, "in_kernel_lsu")):
                 def gstep(mode=mode):
                     bbm.attn_fwd_device(prep, variant, q, k, v, og, rmax, rsum, scale, stream.cuda_stream,
                                         rows=rows, gather_mode=mode)
@@ -613,15 +614,17 @@ def main():
                 rcm[key] = device_ms(stream, gstep, max(5, args.steps))
             p_ms = device_ms(stream, step, max(5, args.steps))
             extras["fwd_device_rcm"] = {
-                "ms_per_step": rcm["hybrid"], "pre_permuted_ms_per_step": p_ms,
-                "ratio_vs_pre_permuted": rcm["hybrid"] / p_ms, "tflops": flops / (rcm["hybrid"] * 1e-3) / 1e12,
-                "passes_ms_per_step": rcm["passes"],
+                "ms_per_step": rcm["in_kernel_lsu"], "pre_permuted_ms_per_step": p_ms,
+                "ratio_vs_pre_permuted": rcm["in_kernel_lsu"] / p_ms,
+                "tflops": flops / (rcm["in_kernel_lsu"] * 1e-3) / 1e12,
+                "hybrid_ms_per_step": rcm["hybrid"], "passes_ms_per_step": rcm["passes"],
                 "in_kernel_tma_ms_per_step": rcm["in_kernel_tma"],
-                "note": "original-order Q/K/V resident in HBM; default path (bbm_attn_fwd_gather, mode 3): K/V "
-                        "permuted into scratch by HBM-bound passes, Q rows gathered (TMA tile::gather4) and O rows "
-                        "scattered (tile::scatter4) inside the kernel; passes: Q/K/V permuted, plain kernel, O "
-                        "and row stats scattered back; in_kernel_tma: every row gathered inside the kernel "
-                        "(bound by the TMA instruction rate, 512 B per instruction)"}
+                "note": "original-order Q/K/V resident in HBM; default path (bbm_attn_fwd_gather, mode 4): every "
+                        "Q/K/V row gathered inside the kernel by LSU cp.async (two producer warps), O rows "
+                        "written to their tokens by the epilogue threads, no scratch; hybrid (mode 3): K/V "
+                        "permuted by passes, Q gathered / O scattered with TMA tile::gather4 / scatter4; passes "
+                        "(mode 1): Q/K/V permuted, plain kernel, O and row stats scattered back; in_kernel_tma "
+                        "(mode 2): every row gathered with tile::gather4 (bound by the TMA instruction rate)"}
             del og
         if not args.no_cpu_baseline and world == 1 and args.which == "fwd":
             try:

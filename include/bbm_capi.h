@@ -152,14 +152,14 @@ bbm_status bbm_attn_fwd(bbm_prep prep, int variant, const void* q, const void* k
 
 /* The same forward with the RCM permutation applied on the device (reorder.hpp:156-189):
  * `prep` was built from permute_mask(mask, perm), d_forward = perm.forward (new -> old, device
- * u32 [n]), and q/k/v/out/row stats stay in the ORIGINAL token order. Two implementations, equal
- * results: mode 1 permutes Q/K/V into per-stream scratch (4 x slots*n*d bf16 + 2 x slots*n fp32),
- * runs the plain kernel and scatters O / row stats back (HBM-bound passes); mode 2 gathers each
- * tile's rows inside the kernel with TMA tile::gather4 and scatters O with tile::scatter4 (no
- * scratch; bound by the TMA instruction rate; requires slots * n < 2^31); mode 3 permutes only K
- * and V into scratch (2 x slots*n*d bf16) and gathers Q / scatters O inside the kernel.
- * bbm_attn_fwd_gather = mode 0 = the default, the fastest on B200: mode 3 (env
- * BBM_GATHER=passes|tma|hybrid overrides). */
+ * u32 [n]), and q/k/v/out/row stats stay in the ORIGINAL token order. Four implementations, equal
+ * results bit for bit: mode 4 (the default) gathers every Q / K / V row inside the kernel with LSU
+ * cp.async and writes O rows / row stats to their tokens (no scratch); mode 3 permutes K and V into
+ * per-stream scratch (2 x slots*n*d bf16) and gathers Q / scatters O with TMA tile::gather4 /
+ * scatter4; mode 1 permutes Q/K/V into scratch (4 x slots*n*d bf16 + 2 x slots*n fp32), runs the
+ * plain kernel and scatters O / row stats back; mode 2 gathers every row with tile::gather4 (bound
+ * by the TMA instruction rate). Modes 2-4 require slots * n < 2^31. bbm_attn_fwd_gather = mode 0 =
+ * the default (env BBM_GATHER=passes|tma|hybrid|lsu overrides). */
 bbm_status bbm_attn_fwd_gather(bbm_prep prep, int variant, const uint32_t* d_forward, const void* q,
                                const void* k, const void* v, void* out, float* row_max, float* row_sum,
                                uint64_t slots, uint32_t head_dim, double scale, void* stream);

@@ -492,9 +492,10 @@ def attn_fwd_device(prep: MaskPrep, variant: Variant, q, k, v, out, row_max=None
     ``rows``: optional CUDA int32/uint32 tensor [n], an RCM permutation's forward map (new -> old)
     for a prep built from ``permute_mask(mask, perm)``: the tensors then stay in the ORIGINAL
     token order and the RCM permutation is applied on the device (bbm_attn_fwd_gather_ex):
-    ``gather_mode`` 0 = the default, the fastest on B200 (3), 1 = permute / unpermute passes around the
+    ``gather_mode`` 0 = the default, the fastest on B200 (4), 1 = permute / unpermute passes around the
     plain kernel, 2 = in-kernel TMA tile::gather4 / scatter4, 3 = K / V permuted by passes with
-    Q rows gathered and O rows scattered in the kernel."""
+    Q rows gathered and O rows scattered in the kernel, 4 = every row gathered in the kernel by
+    LSU cp.async (no scratch)."""
     import torch
 
     slots, n, d = (q.shape if q.dim() == 3 else (1, *q.shape))

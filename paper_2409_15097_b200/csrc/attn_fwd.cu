@@ -82,6 +82,9 @@ struct FwdParams {
   float* row_max;
   float* row_sum;
   const uint32_t* rows;  // gather mode: token of each (permuted) row position, new -> old [n]
+  const __nv_bfloat16* qg;  // LSU gather mode (kGather == 3): Q / K / V in the caller's token order
+  const __nv_bfloat16* kg;
+  const __nv_bfloat16* vg;
   uint64_t* trace;       // optional event trace (bbm_set_trace), nullptr = off
   uint32_t trace_ctas;   // CTAs that record
 };
@@ -260,8 +263,9 @@ __global__ void __launch_bounds__(kThreadsOf<D>, 1)
                     const __grid_constant__ CUtensorMap tm_k64, const __grid_constant__ CUtensorMap tm_v64,
                     const FwdParams p) {
   // kGather: 0 plain tiles; 1 every Q / K / V row gathered and O scattered in the kernel
-  // (tile::gather4 / scatter4); 2 only Q gathered and O scattered, K / V from permuted copies
-  constexpr bool kGQ = kGather != 0, kGKV = kGather == 1;
+  // (tile::gather4 / scatter4); 2 only Q gathered and O scattered, K / V from permuted copies;
+  // 3 Q / K / V rows gathered by LSU cp.async (16 B per lane, the TMA unit left to the O scatter)
+  constexpr bool kGQ = kGather != 0, kGKV = kGather == 1 || kGather == 3, kLsu = kGather == 3;
   using C = Cfg<D>;
   extern __shared__ __align__(1024) uint8_t smem[];
   uint8_t* sq = smem;                              // [2][tile]          Q, double-buffered
@@ -281,7 +285,7 @@ __global__ void __launch_bounds__(kThreadsOf<D>, 1)
     ctl->split_rows = h.split_rows;
     ctl->split_chunks = h.split_chunks;
     for (int b = 0; b < 2; ++b) {
-      mbar_init(&ctl->q_full[b], 1);
+      mbar_init(&ctl->q_full[b], kLsu ? 64 : 1);  // LSU gather: every producer lane's cp.async arrive
       mbar_init(&ctl->q_empty[b], 1);
     }
     for (uint32_t b = 0; b < kSBufs; ++b) {
@@ -297,12 +301,13 @@ __global__ void __launch_bounds__(kThreadsOf<D>, 1)
       mbar_init(&ctl->stats_empty[b], 128);             // epilogue threads
     }
     for (uint32_t r = 0; r < C::kRing; ++r) {
-      mbar_init(&ctl->ring_full[r], 1);
+      mbar_init(&ctl->ring_full[r], kLsu ? 64 : 1);
       mbar_init(&ctl->ring_empty[r], 1);
     }
     for (uint32_t r = 0; r < kQueue; ++r) {
       mbar_init(&ctl->item_full[r], 1);
-      mbar_init(&ctl->item_empty[r], 2 + kParts<D> * 4);  // S issuer + PV issuer + engine warps
+      // S issuer + PV issuer + engine warps (+ the V-cursor warp of the LSU gather mode)
+      mbar_init(&ctl->item_empty[r], 2 + kParts<D> * 4 + (kLsu ? 1 : 0));
     }
     fence_barrier_init();
   }
@@ -324,8 +329,11 @@ __global__ void __launch_bounds__(kThreadsOf<D>, 1)
 
   if (warp < 4) {
   setmaxnreg_dec<kOtherRegs<D>>();
-  if (warp == 0) {
+  if (warp == 0 || (kLsu && warp == 2)) {
     // ------------------------------------------------------------------ producer
+    // (LSU gather mode: the cp.async gathers cost a warp instruction per 512 bytes, so warps 0
+    // and 2 both run the producer, each copying 64 rows of every tile; warp 2 takes the items
+    // warp 0 claims from the item queue, as one more consumer)
     // Loads follow the MMA issuers' consumption order (kseq_of / vseq_of): a K cursor runs kSBufs
     // tiles ahead of a V cursor, so a load only ever waits for the ring slot freed kRing
     // positions earlier in that same order.
@@ -344,7 +352,33 @@ __global__ void __launch_bounds__(kThreadsOf<D>, 1)
       // already posted by lane 0)
       auto issue_tile = [&](uint8_t* dst, const CUtensorMap* tm, uint64_t* bar, uint32_t tile, uint32_t slot,
                             uint64_t pol, auto gather) {
-        if constexpr (decltype(gather)::value) {
+        if constexpr (kLsu) {
+          // Coalesced: lane l copies 16-byte chunk l % 8 of rows 4g + l / 8, g = 0..31, so one warp
+          // instruction moves four whole 128-byte box rows. The chunk lands where TMA's 128B
+          // swizzle puts it (chunk c of row r at ((c ^ (r % 8)) * 16) within the row's 128 bytes).
+          // Row tokens: lane l looks up rows l, l + 32, l + 64, l + 96; the others come by shuffle.
+          const __nv_bfloat16* base = tm == &tm_q ? p.qg : (tm == &tm_k ? p.kg : p.vg);
+          const uint32_t d0 = smem_u32(dst), c = lane & 7, rr = lane >> 3, i0 = warp == 0 ? 0u : 2u;
+          int32_t tok[2];
+#pragma unroll
+          for (uint32_t ii = 0; ii < 2; ++ii) tok[ii] = gather_row(p, slot, tile * 128 + (i0 + ii) * 32 + lane);
+#pragma unroll
+          for (uint32_t ii = 0; ii < 2; ++ii) {
+            const uint32_t i = i0 + ii;
+#pragma unroll
+            for (uint32_t g8 = 0; g8 < 8; ++g8) {
+              const uint32_t r = i * 32 + g8 * 4 + rr;  // row of the tile; its token is in lane r % 32
+              const int32_t gr = __shfl_sync(0xffffffffu, tok[ii], g8 * 4 + rr);
+              const bool in = gr != INT32_MAX;
+              const __nv_bfloat16* src = base + (in ? static_cast<uint64_t>(gr) * D : 0) + c * 8;
+#pragma unroll
+              for (uint32_t b = 0; b < C::kBoxes; ++b)
+                cp_async16(d0 + b * kBoxBytes + r * 128 + ((c ^ (r & 7)) << 4), src + b * 64, in ? 16 : 0);
+            }
+          }
+          cp_async_mbar_arrive(bar);
+          (void)pol;
+        } else if constexpr (decltype(gather)::value) {
           int32_t r[4];
 #pragma unroll
           for (uint32_t i = 0; i < 4; ++i) r[i] = gather_row(p, slot, tile * 128 + lane * 4 + i);
@@ -383,7 +417,7 @@ __global__ void __launch_bounds__(kThreadsOf<D>, 1)
 #endif
         if (lane == 0) {
           ctl->ring_meta[r] = half;  // published by the arrive below
-          mbar_arrive_expect_tx(full, half ? C::kTileBytes / 2 : C::kTileBytes);
+          if (!kLsu) mbar_arrive_expect_tx(full, half ? C::kTileBytes / 2 : C::kTileBytes);
         }
         __syncwarp();
         if (half == 0) {
@@ -403,14 +437,22 @@ __global__ void __launch_bounds__(kThreadsOf<D>, 1)
       auto k_next = [&]() -> bool {
         while (k_need) {
           if (k_done) return false;
-          uint32_t t = 0;
-          if (lane == 0) t = atomicAdd(&p.work_ctr[0], 1u);
-          t = __shfl_sync(0xffffffffu, t, 0);
-          const ItemDesc d = decode_item(p, ctl->units, ctl->total_items, t);
-          mbar_wait(&ctl->item_empty[qi], qiph);
-          if (lane == 0) {
-            ctl->items[qi] = d;
-            mbar_arrive(&ctl->item_full[qi]);  // release: the descriptor is visible to waiters
+          ItemDesc d;
+          if (kLsu && warp == 2) {  // the second gather warp follows warp 0's claims
+            mbar_wait(&ctl->item_full[qi], qiph ^ 1);
+            d = ctl->items[qi];
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&ctl->item_empty[qi]);
+          } else {
+            uint32_t t = 0;
+            if (lane == 0) t = atomicAdd(&p.work_ctr[0], 1u);
+            t = __shfl_sync(0xffffffffu, t, 0);
+            d = decode_item(p, ctl->units, ctl->total_items, t);
+            mbar_wait(&ctl->item_empty[qi], qiph);
+            if (lane == 0) {
+              ctl->items[qi] = d;
+              mbar_arrive(&ctl->item_full[qi]);  // release: the descriptor is visible to waiters
+            }
           }
           if (++qi == kQueue) { qi = 0; qiph ^= 1; }
           if (d.t == kEnd) {
@@ -423,7 +465,7 @@ __global__ void __launch_bounds__(kThreadsOf<D>, 1)
           khalf = half_of<MODE, kGKV, kSkip>(p, d.rt, d.j0);
           mbar_wait(&ctl->q_empty[qb], qph[qb]);
           qph.flip(qb);
-          if (lane == 0) mbar_arrive_expect_tx(&ctl->q_full[qb], C::kTileBytes);
+          if (lane == 0 && !kLsu) mbar_arrive_expect_tx(&ctl->q_full[qb], C::kTileBytes);
           __syncwarp();
           issue_tile(sq + qb * C::kTileBytes, &tm_q, &ctl->q_full[qb], d.rt, d.slot, pol_q, std::bool_constant<kGQ>{});
           if (lane == 0) trace_ev<kTrace>(tracing, p, &ctl->trace_count, 1, 0, d.t);
@@ -513,6 +555,7 @@ __global__ void __launch_bounds__(kThreadsOf<D>, 1)
             const uint32_t slot = kseq % C::kRing;
             mbar_wait(&ctl->ring_full[slot], (kseq / C::kRing) & 1);
             trace_ev<kTrace>(tracing, p, &ctl->trace_count, 13, buf, j);
+            if constexpr (kLsu) fence_proxy_async_smem();  // cp.async (generic proxy) -> tcgen05 reads
             tc_fence_after();
             // a key half no row sees is neither loaded nor multiplied: N = 64 over the other half
             // (its S columns keep stale values, which the softmax replaces by the mask sentinel)
@@ -545,6 +588,7 @@ __global__ void __launch_bounds__(kThreadsOf<D>, 1)
             const uint32_t slot = vseq % C::kRing;
             mbar_wait(&ctl->ring_full[slot], (vseq / C::kRing) & 1);
             trace_ev<kTrace>(tracing, p, &ctl->trace_count, 12, buf, j);
+            if constexpr (kLsu) fence_proxy_async_smem();
             tc_fence_after();
             const uint64_t vdesc = make_sdesc_sw128(raddr + slot * C::kTileBytes, kBoxBytes, 1024);
             const uint32_t pcol = tmem + buf * 128;
@@ -889,7 +933,41 @@ __global__ void __launch_bounds__(kThreadsOf<D>, 1)
       tc_fence_after();
       named_bar_sync(2, kEpi);
       if (tracer) trace_ev<kTrace>(tracing, p, &ctl->trace_count, 23, 0, it.t);
-      if (it.split == kNoSplit) {
+      if (it.split == kNoSplit && kGQ) {
+        // gathered rows: each epilogue thread writes its own O row straight to its token (whole
+        // 32-byte sectors per thread), no staging box and no TMA scatter
+        const float inv = l_unit > 0.0f ? 1.0f / l_unit : 0.0f;
+        const uint64_t grow = static_cast<uint64_t>(it.rt) * 128 + row;
+        __nv_bfloat16* dst = p.out + (grow < p.n ? out_row<kGQ>(p, it.slot, grow) * D : 0);
+#pragma unroll
+        for (uint32_t c64 = 0; c64 < D / 64; ++c64) {
+          uint32_t o[2][32];
+          tmem_ld32(to + c64 * 64, o[0]);
+          tmem_ld32(to + c64 * 64 + 32, o[1]);
+          tmem_ld_wait();
+          if (c64 + 1 == D / 64) {
+            tc_fence_before();
+            mbar_arrive(&ctl->o_empty[ob]);
+          }
+          if (grow < p.n) {
+#pragma unroll
+            for (uint32_t h = 0; h < 2; ++h) {
+              const float* v = reinterpret_cast<const float*>(o[h]);
+              uint4* d4 = reinterpret_cast<uint4*>(dst + c64 * 64 + h * 32);
+#pragma unroll
+              for (uint32_t q4 = 0; q4 < 4; ++q4) {
+                uint4 w;
+                w.x = pack_bf16x2(v[q4 * 8 + 0] * inv, v[q4 * 8 + 1] * inv);
+                w.y = pack_bf16x2(v[q4 * 8 + 2] * inv, v[q4 * 8 + 3] * inv);
+                w.z = pack_bf16x2(v[q4 * 8 + 4] * inv, v[q4 * 8 + 5] * inv);
+                w.w = pack_bf16x2(v[q4 * 8 + 6] * inv, v[q4 * 8 + 7] * inv);
+                d4[q4] = w;
+              }
+            }
+          }
+        }
+        write_stats(it, m_true, m_run, l_unit);
+      } else if (it.split == kNoSplit) {
         const float inv = l_unit > 0.0f ? 1.0f / l_unit : 0.0f;
 #ifdef BBM_ABLATE_NO_EPI  // timing experiments only (tools/ablate.sh): O is never written
         if (false)
@@ -1030,7 +1108,7 @@ void launch_impl(const Prep& prep, const AttnArgs& a, cudaStream_t s, int num_sm
 
   // plain: 3-D [slots][n][D] maps with 128-row boxes; gathered tensors: 2-D [slots * n][D] row maps
   // (Q and O in both gather modes, K and V only when kGather == 1)
-  constexpr bool kGQ = kGather != 0, kGKV = kGather == 1;
+  constexpr bool kGQ = kGather != 0, kGKV = kGather == 1 || kGather == 3;
   auto tmap = [&](const void* base, bool gathered) {
     return gathered ? make_tmap_bf16_rows(base, D, a.slots * a.n, 64)
                     : cached_tmap_bf16_3d(base, D, a.n, a.slots, 64, 128);
@@ -1041,6 +1119,9 @@ void launch_impl(const Prep& prep, const AttnArgs& a, cudaStream_t s, int num_sm
   const CUtensorMap tv64 = kGKV ? tv : cached_tmap_bf16_3d(a.v, D, a.n, a.slots, 64, 64);
   FwdParams p{};
   p.rows = a.rows;
+  p.qg = static_cast<const __nv_bfloat16*>(a.q);
+  p.kg = static_cast<const __nv_bfloat16*>(a.k);
+  p.vg = static_cast<const __nv_bfloat16*>(a.v);
   p.n = a.n;
   p.slots = static_cast<uint32_t>(a.slots);
   p.krows = km.krows;
@@ -1109,20 +1190,21 @@ void launch_d(const Prep& prep, const AttnArgs& a, cudaStream_t s, int num_sms) 
   }
 }
 
-// Which RCM application a gather launch uses: BBM_GATHER=tma|passes|hybrid overrides (measurement).
-// The default is the fastest on B200, the hybrid: K and V are each re-read by several row tiles, so
-// one HBM-bound permute pass each is cheaper than gathering them per tile (tile::gather4 moves 4
-// rows, 512 B, per TMA instruction and the TMA unit issues one every ~60 cycles: the all-in-kernel
-// gather runs C5 in 6.4 ms against 1.4 ms pre-permuted), while Q and O, touched once per item,
-// are gathered / scattered in the kernel instead of costing a pass each (C5: 2.70 ms against
-// 2.84 ms for passes over Q, K, V, O and the row statistics).
+// Which RCM application a gather launch uses: BBM_GATHER=tma|passes|hybrid|lsu overrides
+// (measurement). The default is the fastest on B200 and needs no scratch: every Q / K / V row
+// gathered inside the kernel by LSU cp.async (two producer warps, 16 B per lane, four whole
+// 128-byte box rows per warp instruction; C5 2.39 ms against 1.43 ms pre-permuted). The TMA
+// tile::gather4 variant moves 4 rows (512 B) per TMA instruction and the TMA unit issues one
+// every ~60 cycles (6.4 ms); the hybrid permutes K / V by passes and gathers Q / O with TMA
+// (2.65 ms); passes over Q, K, V, O and the statistics around the plain kernel take 2.85 ms.
 int gather_mode_of(int requested) {
   if (requested != kGatherAuto) return requested;
   static const int env = [] {
     const char* e = std::getenv("BBM_GATHER");
     if (e && std::string(e) == "tma") return static_cast<int>(kGatherTma);
     if (e && std::string(e) == "passes") return static_cast<int>(kGatherPasses);
-    return static_cast<int>(kGatherHybrid);
+    if (e && std::string(e) == "hybrid") return static_cast<int>(kGatherHybrid);
+    return static_cast<int>(kGatherLsu);
   }();
   return env;
 }
@@ -1194,6 +1276,10 @@ void launch_attn_fwd(const Prep& prep, const AttnArgs& a, cudaStream_t s, int nu
   } else if (a.rows && gather_mode_of(a.gather_mode) == kGatherHybrid) {
     require(a.slots * a.n < (1ull << 31) - 1, "too many rows for the gather path (slots * n >= 2^31)");
     launch_gather_hybrid(prep, a, s, num_sms);
+  } else if (a.rows && gather_mode_of(a.gather_mode) == kGatherLsu) {
+    require(a.slots * a.n < (1ull << 31) - 1, "too many rows for the gather path (slots * n >= 2^31)");
+    if (a.d == 64) launch_d<64, 3>(prep, a, s, num_sms);
+    else launch_d<128, 3>(prep, a, s, num_sms);
   } else if (a.rows) {  // in-kernel RCM gather / scatter of token rows (2-D row coordinates are int32)
     require(a.slots * a.n < (1ull << 31) - 1, "too many rows for the gather path (slots * n >= 2^31)");
     if (a.d == 64) launch_d<64, 1>(prep, a, s, num_sms);

@@ -266,7 +266,7 @@ struct AttnArgs {
   const uint32_t* rows = nullptr;
   int gather_mode = 0;
 };
-enum GatherMode : int { kGatherAuto = 0, kGatherPasses = 1, kGatherTma = 2, kGatherHybrid = 3 };
+enum GatherMode : int { kGatherAuto = 0, kGatherPasses = 1, kGatherTma = 2, kGatherHybrid = 3, kGatherLsu = 4 };
 // Process-wide kernel event trace (bbm_set_trace): device buffer of ctas * 8192 u64 events.
 struct TraceConfig {
   void* buffer = nullptr;

@@ -821,8 +821,9 @@ bbm_status bbm_attn_fwd_gather_ex(bbm_prep prep, int variant, const uint32_t* d_
     const Prep& pr = unwrap(prep);
     check_attn_args(pr, variant, slots, head_dim, scale);
     require(q && k && v && out && d_forward, "null pointer");
-    require(mode >= 0 && mode <= 3,
-            "gather mode must be 0 (auto), 1 (passes), 2 (in-kernel TMA) or 3 (K/V passes, Q/O in-kernel)");
+    require(mode >= 0 && mode <= 4,
+            "gather mode must be 0 (auto), 1 (passes), 2 (in-kernel TMA), 3 (K/V passes, Q/O in-kernel) or "
+            "4 (in-kernel LSU gather)");
     AttnArgs a{q, k, v, out, row_max, row_sum, slots, pr.n, head_dim, static_cast<float>(scale),
                variant, d_forward, mode};
     int dev = 0;

@@ -401,7 +401,7 @@ def test_mixed_items_in_one_launch(cuda, d):
 
 @pytest.mark.parametrize("n,d,slots,spec", [(1000, 64, 3, "windowed(w=40)"), (2304, 128, 2, "global(w=90;g=70)"),
                                             (640, 128, 5, "causal")])
-@pytest.mark.parametrize("mode", [0, 1, 2, 3])
+@pytest.mark.parametrize("mode", [0, 1, 2, 3, 4])
 def test_in_kernel_rcm_gather_equals_explicit_permutation(cuda, n, d, slots, spec, mode):
     """bbm_attn_fwd_gather_ex (f2): original-order Q/K/V, the prep of the RCM-permuted mask, the
     permutation applied on the device — by permute passes around the plain kernel (mode 1, the

@@ -118,3 +118,37 @@ def test_backward_full_size_rows_and_identities(cuda, cfg):
         sdk = host(dk[s]).sum(0)
         assert float(np.abs(sdk).max()) <= TOL * max(float(np.abs(host(dk[s])).sum(0).max()) / np.sqrt(n), 1.0), \
             f"{cfg} sum dK slot {s}"
+
+
+@pytest.mark.parametrize("mode", [2, 3, 4])
+def test_full_c5_rcm_gather_modes_bitwise(cuda, mode):
+    """f2 at the headline size: the C5 forward (bench.py's RCM-reordered mask and its permutation)
+    on ORIGINAL-order inputs with the RCM permutation
+    applied on the device (in-kernel TMA gather, hybrid, in-kernel LSU gather) equals the forward
+    on pre-permuted inputs scattered back, bit for bit, on every slot — three launches each (the
+    LSU mode's cp.async gathers hand shared memory to tcgen05 through mbarrier + proxy fence; a
+    missing ordering would show here as sporadic differences)."""
+    import torch
+
+    words, fwd_perm = bench.mask_words("c5", *bench.bbm_backends(bbm, 0))  # the RCM-reordered mask
+    _, _, d, _, _, n = bench.CONFIGS["c5"]
+    prep = bbm.preprocess_mask(bbm.Mask(n, words), bbm.BlockSpec(128, 128))
+    slots = 16  # 16 of C5's 128 slots: the full per-slot size, a bounded test time
+    q, k, v, _ = inputs(slots, n, d, cuda, 7)
+    fwd = torch.from_numpy(np.ascontiguousarray(fwd_perm, dtype=np.int64)).to(cuda)
+    rows = fwd.to(torch.int32)
+    qp, kp, vp = (t[:, fwd].contiguous() for t in (q, k, v))  # row a <- token forward[a]
+    op = torch.empty_like(qp)
+    mp = torch.empty((slots, n), dtype=torch.float32, device=cuda)
+    bbm.attn_fwd_device(prep, bbm.Variant.binblk, qp, kp, vp, op, mp, None, d ** -0.5)
+    want_o = torch.empty_like(op)
+    want_o[:, fwd] = op
+    want_m = torch.empty_like(mp)
+    want_m[:, fwd] = mp
+    for _ in range(3):
+        out = torch.empty_like(q)
+        m = torch.empty_like(mp)
+        bbm.attn_fwd_device(prep, bbm.Variant.binblk, q, k, v, out, m, None, d ** -0.5, rows=rows, gather_mode=mode)
+        torch.cuda.synchronize()
+        assert torch.equal(out.view(torch.int16), want_o.view(torch.int16))
+        assert torch.equal(m.view(torch.int32), want_m.view(torch.int32))
