@@ -1270,6 +1270,9 @@ void launch_attn_fwd(const Prep& prep, const AttnArgs& a, cudaStream_t s, int nu
           "too many slots x row tiles for one launch");
   if (a.slots * prep.kmeta.krows == 0) return;
   if (a.d != 64 && a.d != 128) throw ArgError("head dim must be 64 or 128 on the sm_100a kernel");
+  // TMA descriptors and the 16-byte cp.async / vector row accesses need 16-byte aligned tensors
+  for (const void* t : {a.q, a.k, a.v, static_cast<const void*>(a.o)})
+    require((reinterpret_cast<uintptr_t>(t) & 15u) == 0, "q, k, v and out must be 16-byte aligned");
   if (launch_attn_fwd_pair(prep, a, s, num_sms)) return;  // only when selected (bbm_set_fwd_kernel)
   if (a.rows && gather_mode_of(a.gather_mode) == kGatherPasses) {
     launch_gather_passes(prep, a, s, num_sms);

@@ -307,6 +307,13 @@ def test_device_entry_rejects_mismatched_shapes(cuda):
         bbm.attn_fwd_device(prep, bbm.Variant.binblk, q, k.expand(3, n, d), q, torch.empty_like(q))
     with pytest.raises(ValueError, match="scale"):
         bbm.blocked_forward(q, q, q, 1e39, mask, prep, bbm.Variant.binblk)
+    # a contiguous view 2 bytes into its storage: rejected before any TMA descriptor / cp.async
+    buf = torch.zeros(3 * n * d + 8, dtype=torch.bfloat16, device=cuda)
+    mis = buf[1:1 + 3 * n * d].view(3, n, d)
+    rows = torch.arange(n, dtype=torch.int32, device=cuda)
+    for kw in ({}, {"rows": rows, "gather_mode": 4}, {"rows": rows, "gather_mode": 2}):
+        with pytest.raises(ValueError, match="aligned"):
+            bbm.attn_fwd_device(prep, bbm.Variant.binblk, mis, q, q, torch.empty_like(q), **kw)
 
 
 @pytest.mark.parametrize("pinned", [False, True])
