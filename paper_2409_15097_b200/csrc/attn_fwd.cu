@@ -198,7 +198,11 @@ struct SmemCtl {
   uint32_t bcast;
   float xchg[2][kXP][128];  // [exchange parity][part][row]: partial row max
   ItemStats<kXP> stats[2];
+  // LSU gather: the row tokens of the last 8 K tiles, per producer warp (64 rows each), so the V
+  // load of the same key tile (kSBufs tiles later) needs no second lookup
+  int32_t lsu_tok[2][8][64];
 };
+static_assert(kSBufs < 8, "the V cursor trails the K cursor by kSBufs tiles: lsu_tok keeps 8");
 
 template <int D>
 constexpr uint32_t smem_bytes() {
@@ -350,8 +354,10 @@ __global__ void __launch_bounds__(kThreadsOf<D>, 1)
       uint32_t pw = 0, pr = 0;
       // one 128 x D tile (row tile `tile` of `slot`) into dst, completing on `bar` (expect-tx
       // already posted by lane 0)
+      // `pre` / `save` (LSU gather only): take this lane's row tokens from / leave them in shared
+      // memory (slot [ii * 32 + lane] of a 64-entry row of lsu_tok)
       auto issue_tile = [&](uint8_t* dst, const CUtensorMap* tm, uint64_t* bar, uint32_t tile, uint32_t slot,
-                            uint64_t pol, auto gather) {
+                            uint64_t pol, auto gather, const int32_t* pre = nullptr, int32_t* save = nullptr) {
         if constexpr (kLsu) {
           // Coalesced: lane l copies 16-byte chunk l % 8 of rows 4g + l / 8, g = 0..31, so one warp
           // instruction moves four whole 128-byte box rows. The chunk lands where TMA's 128B
@@ -361,7 +367,12 @@ __global__ void __launch_bounds__(kThreadsOf<D>, 1)
           const uint32_t d0 = smem_u32(dst), c = lane & 7, rr = lane >> 3, i0 = warp == 0 ? 0u : 2u;
           int32_t tok[2];
 #pragma unroll
-          for (uint32_t ii = 0; ii < 2; ++ii) tok[ii] = gather_row(p, slot, tile * 128 + (i0 + ii) * 32 + lane);
+          for (uint32_t ii = 0; ii < 2; ++ii)
+            tok[ii] = pre ? pre[ii * 32 + lane] : gather_row(p, slot, tile * 128 + (i0 + ii) * 32 + lane);
+          if (save) {
+            save[lane] = tok[0];
+            save[32 + lane] = tok[1];
+          }
 #pragma unroll
           for (uint32_t ii = 0; ii < 2; ++ii) {
             const uint32_t i = i0 + ii;
@@ -394,7 +405,7 @@ __global__ void __launch_bounds__(kThreadsOf<D>, 1)
       // K / V tile q into the ring; a key half that no row of the tile sees (`half`, bit 0 / 1) is
       // not loaded (64-row boxes for the other half); the MMA issuers read `half` from ring_meta
       auto load_tile = [&](const CUtensorMap* tm, const CUtensorMap* tm64, uint32_t seq, uint32_t q, uint32_t slot,
-                           uint32_t code, uint32_t j, uint32_t half) {
+                           uint32_t code, uint32_t j, uint32_t half, const int32_t* pre, int32_t* save) {
         const uint32_t r = seq % C::kRing;
         mbar_wait(&ctl->ring_empty[r], ((seq / C::kRing) & 1) ^ 1);
         uint64_t* full = &ctl->ring_full[r];
@@ -421,7 +432,7 @@ __global__ void __launch_bounds__(kThreadsOf<D>, 1)
         }
         __syncwarp();
         if (half == 0) {
-          issue_tile(ring + r * C::kTileBytes, tm, full, q, slot, pol_kv, std::bool_constant<kGKV>{});
+          issue_tile(ring + r * C::kTileBytes, tm, full, q, slot, pol_kv, std::bool_constant<kGKV>{}, pre, save);
         } else if (lane == 0) {
           const uint32_t hh = (half & 1u) ? 1u : 0u;  // the half that is loaded
           for (uint32_t b = 0; b < C::kBoxes; ++b)
@@ -483,7 +494,8 @@ __global__ void __launch_bounds__(kThreadsOf<D>, 1)
           kentry = entry_of<MODE>(p, kit.rt, kit.j0 + kj + 1);
           khalf = half_of<MODE, kGKV, kSkip>(p, kit.rt, kit.j0 + kj + 1);
         }
-        load_tile(&tm_k, &tm_k64, kseq_of(kk), cur & 0x7FFFFFFFu, kit.slot, 2, kj, chalf);
+        load_tile(&tm_k, &tm_k64, kseq_of(kk), cur & 0x7FFFFFFFu, kit.slot, 2, kj, chalf, nullptr,
+                  kLsu ? ctl->lsu_tok[warp == 0 ? 0 : 1][kk % 8] : nullptr);
         ++kk;
         if (++kj == kit.nt) k_need = true;
       };
@@ -505,7 +517,9 @@ __global__ void __launch_bounds__(kThreadsOf<D>, 1)
           ventry = entry_of<MODE>(p, vit.rt, vit.j0 + vj + 1);
           vhalf = half_of<MODE, kGKV, kSkip>(p, vit.rt, vit.j0 + vj + 1);
         }
-        load_tile(&tm_v, &tm_v64, vseq_of(vk), cur & 0x7FFFFFFFu, vit.slot, 3, vj, chalf);
+        // K tile vk's tokens (saved kSBufs tiles ago by this same lane)
+        load_tile(&tm_v, &tm_v64, vseq_of(vk), cur & 0x7FFFFFFFu, vit.slot, 3, vj, chalf,
+                  kLsu ? ctl->lsu_tok[warp == 0 ? 0 : 1][vk % 8] : nullptr, nullptr);
         ++vk;
         if (++vj == vit.nt) v_need = true;
         return true;
@@ -1193,7 +1207,8 @@ void launch_d(const Prep& prep, const AttnArgs& a, cudaStream_t s, int num_sms) 
 // Which RCM application a gather launch uses: BBM_GATHER=tma|passes|hybrid|lsu overrides
 // (measurement). The default is the fastest on B200 and needs no scratch: every Q / K / V row
 // gathered inside the kernel by LSU cp.async (two producer warps, 16 B per lane, four whole
-// 128-byte box rows per warp instruction; C5 2.39 ms against 1.43 ms pre-permuted). The TMA
+// 128-byte box rows per warp instruction, row tokens looked up once per key tile; C5 2.10 ms
+// against 1.43 ms pre-permuted). The TMA
 // tile::gather4 variant moves 4 rows (512 B) per TMA instruction and the TMA unit issues one
 // every ~60 cycles (6.4 ms); the hybrid permutes K / V by passes and gathers Q / O with TMA
 // (2.65 ms); passes over Q, K, V, O and the statistics around the plain kernel take 2.85 ms.
