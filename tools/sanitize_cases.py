@@ -1,7 +1,7 @@
 """Small launches for compute-sanitizer (racecheck / synccheck / memcheck): every forward variant
 on C1/C3-shaped problems incl. ragged n, multi-slot and split-KV rows, the backward, and the
 fused preprocessor update path; band masks whose repeated launches skip empty 64-row halves
-(forward and backward), the device RCM application in both modes, and the opt-in two-stream
+(forward and backward), the device RCM application in all four modes, and the opt-in two-stream
 forward.
 
     compute-sanitizer --tool racecheck python tools/sanitize_cases.py
@@ -43,7 +43,7 @@ def main():
         bbm.blocked_forward(q, k, v, d ** -0.5, mask, prep, bbm.Variant.binblk)
         torch.cuda.synchronize()
         print(f"ok {spec} n={n} d={d} slots={slots}", flush=True)
-    # device RCM application (permute passes / in-kernel TMA gather) and the two-stream forward
+    # device RCM application (passes / TMA gather4 / hybrid / LSU gather) and the two-stream forward
     base = bbm.relabel(bbm.generate("windowed(w=40)", 1000), 5)
     perm = bbm.rcm_order(base)
     prep = bbm.preprocess_mask(bbm.permute_mask(base, perm), bbm.BlockSpec(128, 128))
@@ -52,8 +52,9 @@ def main():
     out = torch.empty_like(q)
     m = torch.empty((2, 1000), dtype=torch.float32, device=dev)
     l = torch.empty_like(m)
-    for mode in (1, 2):
-        bbm.attn_fwd_device(prep, bbm.Variant.binblk, q, k, v, out, m, l, 0.08, rows=rows, gather_mode=mode)
+    for mode in (1, 2, 3, 4):  # passes, TMA gather4, hybrid, LSU cp.async gather
+        for var in bbm.Variant:
+            bbm.attn_fwd_device(prep, var, q, k, v, out, m, l, 0.08, rows=rows, gather_mode=mode)
     bbm.set_fwd_kernel("pair")
     bbm.attn_fwd_device(prep, bbm.Variant.binblk, q, k, v, out, m, l, 0.08)
     bbm.set_fwd_kernel("auto")
