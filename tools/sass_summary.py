@@ -14,7 +14,7 @@ import subprocess
 import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-KEYS = ["UTCHMMA", "UTCQMMA", "UTCBAR", "UTMALDG", "UTMASTG", "UTMAPF", "LDTM", "STTM", "HMMA", "MUFU.EX2",
+KEYS = ["UTCHMMA", "UTCQMMA", "UTCBAR", "UTMALDG", "UTMASTG", "LDGSTS", "UTMAPF", "LDTM", "STTM", "HMMA", "MUFU.EX2",
         "FFMA2", "FADD2", "FMUL2", "F2FP", "FMNMX", "SYNCS", "BAR", "LDS", "STS", "LDG", "STG", "STL", "LDL",
         "NANOSLEEP", "ELECT"]
 
