@@ -203,7 +203,8 @@ bbm_status bbm_run_attention_host_f32(bbm_prep prep, int variant, const float* c
                                       double scale);
 /* The same with the value head dim independent of the key head dim
  * (EngineForward.ValueHeadDimMayDifferFromKeyDim, test_engine.cpp:198-209): q/k are n x d_k,
- * v/out n x d_v; 1 <= d_k, d_v <= 128. */
+ * v/out n x d_v; 1 <= d_k <= 128, d_v >= 1 (d_v above 128 runs as column passes over V, each
+ * recomputing the same softmax). */
 bbm_status bbm_run_attention_host_f32_dims(bbm_prep prep, int variant, const float* const* q,
                                            const float* const* k, const float* const* v,
                                            float* const* out, double* const* row_max,
@@ -226,7 +227,8 @@ bbm_status bbm_attn_bwd_host_f32(bbm_prep prep, int variant, const float* q, con
                                  const float* v, const float* out, const double* row_max,
                                  const double* row_sum, const float* d_out, float* dq, float* dk,
                                  float* dv, uint64_t slots, uint32_t head_dim, double scale);
-/* The same with d_v != d_k allowed: q, k, dq, dk are n x d_k; v, out, d_out, dv are n x d_v. */
+/* The same with d_v != d_k allowed: q, k, dq, dk are n x d_k; v, out, d_out, dv are n x d_v
+ * (d_v above 128: column passes over V, dq / dk summed over the passes in order). */
 bbm_status bbm_attn_bwd_host_f32_dims(bbm_prep prep, int variant, const float* q, const float* k,
                                       const float* v, const float* out, const double* row_max,
                                       const double* row_sum, const float* d_out, float* dq, float* dk,

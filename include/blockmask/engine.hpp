@@ -11,8 +11,9 @@
 // Numerics: Q/K/V are rounded to bf16 (RNE) on the device and the kernel accumulates in fp32, so
 // outputs agree with the reference to a bf16 tolerance (max-abs <= 2e-2; tests/), not bit for
 // bit. Counters (engine.hpp:47-66) are exact: they depend on the mask and spec only.
-// New rejection (std::invalid_argument): head dims d_k or d_v above 128 (the kernels hold one
-// 128-column head-dim tile; smaller or unequal dims are zero-padded on the device to 64 / 128).
+// New rejection (std::invalid_argument): key head dim d_k above 128 (the kernels hold one
+// 128-column head-dim tile of Q / K; smaller or unequal dims are zero-padded on the device to
+// 64 / 128, and d_v above 128 runs as column passes over V).
 // `threads` is validated (>= 1) like the reference and otherwise ignored.
 #pragma once
 

@@ -533,13 +533,13 @@ def set_fwd_kernel(mode: str) -> None:
 
 
 def _check_head_dims(dk: int, dv: int) -> None:
-    """validate_forward_args (engine.hpp:249-251) plus the documented narrowing d <= 128."""
+    """validate_forward_args (engine.hpp:249-251) plus the documented narrowing d_k <= 128."""
     if dk < 1:
         raise ValueError("q and k must share a positive head dim")
     if dv < 1:
         raise ValueError("v must have a positive head dim")
-    if dk > 128 or dv > 128:
-        raise ValueError(f"head dims {dk} / {dv} unsupported by the sm_100a kernel (at most 128)")
+    if dk > 128:
+        raise ValueError(f"head dim d_k = {dk} unsupported by the sm_100a kernel (at most 128)")
 
 
 def _kernel_dim(dk: int, dv: int) -> int:
@@ -562,8 +562,9 @@ def blocked_forward(q, k, v, scale: float, mask, prep: MaskPrep, variant: Varian
 
     q, k, v: CUDA bf16 tensors [n, d] or [slots, n, d] (device path, result stays on device), or
     numpy float arrays [n, d] (host path, like Matrix<float>; rounded to bf16 on the device).
-    Head dims d_k (q, k) and d_v (v, out) may differ; both at most 128 (documented narrowing: the
-    kernels hold one 128-column head-dim tile). Dims other than 64 / 128 run zero-padded."""
+    Head dims d_k (q, k) and d_v (v, out) may differ; d_k at most 128 (documented narrowing: the
+    kernels hold one 128-column head-dim tile). Dims other than 64 / 128 run zero-padded, d_v above
+    128 as column passes over V."""
     _validate_common(prep, mask, scale, threads)
     n = prep.n_tokens
     if isinstance(q, np.ndarray):
@@ -588,16 +589,19 @@ def blocked_forward(q, k, v, scale: float, mask, prep: MaskPrep, variant: Varian
     squeeze = q.dim() == 2
     q3, k3, v3 = (t.unsqueeze(0) if squeeze else t for t in (q, k, v))
     dv = v3.shape[-1]
-    D = _kernel_dim(q3.shape[-1], dv)
-    q3, k3, v3 = (_pad_cols(t.to(torch.bfloat16), D).contiguous() for t in (q3, k3, v3))
     slots = q3.shape[0]
-    out = torch.empty_like(v3)
     rmax = torch.empty((slots, n), dtype=torch.float32, device=q3.device)
     rsum = torch.empty((slots, n), dtype=torch.float32, device=q3.device)
-    with torch.cuda.device(q3.device):
-        attn_fwd_device(prep, variant, q3, k3, v3, out, rmax, rsum, scale)
-    if dv != D:
-        out = out[..., :dv].contiguous()
+    parts = []
+    for c0 in range(0, dv, 128):  # d_v > 128: column passes over V (capi.cu v_slices)
+        w = min(128, dv - c0)
+        D = _kernel_dim(q3.shape[-1], w)
+        qp, kp, vp = (_pad_cols(t.to(torch.bfloat16), D).contiguous() for t in (q3, k3, v3[..., c0:c0 + w]))
+        o = torch.empty_like(vp)
+        with torch.cuda.device(q3.device):
+            attn_fwd_device(prep, variant, qp, kp, vp, o, rmax, rsum, scale)
+        parts.append(o[..., :w])
+    out = parts[0].contiguous() if len(parts) == 1 else torch.cat(parts, dim=-1)
     counters = prep.counters(variant, slots)
     if squeeze:
         out, rmax, rsum = out[0], rmax[0], rsum[0]
@@ -698,6 +702,19 @@ def blocked_backward(q, k, v, scale: float, mask, prep: MaskPrep, variant: Varia
         raise ValueError("q, k must share [slots][n][d_k]; v, out, d_out [slots][n][d_v]")
     dk_, dv_ = ts[0].shape[-1], ts[2].shape[-1]
     _check_head_dims(dk_, dv_)
+    if dv_ > 128:  # column passes over V: dq, dk summed over the slices, dv concatenated
+        fq, fk, fv = None, None, []
+        for c0 in range(0, dv_, 128):
+            w = min(128, dv_ - c0)
+            sl = lambda t: t[..., c0:c0 + w]  # noqa: E731
+            part = blocked_backward(q, k, sl(v), scale, mask, prep, variant,
+                                    ForwardResult(sl(fwd.out), fwd.row_max, fwd.row_sum, fwd.counters), sl(d_out),
+                                    threads)
+            fq = part.dq.float() if fq is None else fq + part.dq.float()
+            fk = part.dk.float() if fk is None else fk + part.dk.float()
+            fv.append(part.dv)
+        return BackwardResult(fq.to(torch.bfloat16), fk.to(torch.bfloat16), torch.cat(fv, dim=-1),
+                              prep.counters(variant, ts[0].shape[0]))
     D = _kernel_dim(dk_, dv_)
     for name, t in (("q", q), ("k", k), ("v", v), ("d_out", d_out)):
         if not bool(torch.isfinite(t).all()):

@@ -323,16 +323,36 @@ void check_attn_args(const Prep& pr, int variant, uint64_t slots, uint32_t d, do
   (void)pr;
 }
 
-// float host-buffer entries (validate_forward_args, engine.hpp:244-258): any positive d_k, d_v up
-// to 128 (documented narrowing: the kernels hold one 128-column head-dim tile); the device copy is
-// zero-padded to kernel_dim(d_k, d_v)
+// float host-buffer entries (validate_forward_args, engine.hpp:244-258): any positive d_k up to 128
+// (documented narrowing: the kernels hold one 128-column head-dim tile of Q / K) and any positive
+// d_v; the device copy is zero-padded to kernel_dim(d_k, d_v), and d_v above 128 runs as column
+// passes over V (v_column_passes below)
 void check_host_dims(int variant, uint64_t slots, uint32_t d_k, uint32_t d_v, double scale) {
   check_common_args(variant, slots, scale);
   require(d_k >= 1, "q and k must share a positive head dim");
   require(d_v >= 1, "v must have a positive head dim");
-  if (d_k > 128 || d_v > 128)
-    throw ArgError("head dims " + std::to_string(d_k) + " / " + std::to_string(d_v) +
-                   " unsupported by the sm_100a kernel (at most 128)");
+  if (d_k > 128)
+    throw ArgError("head dim d_k = " + std::to_string(d_k) + " unsupported by the sm_100a kernel (at most 128)");
+}
+
+// d_v > 128: the output columns are independent given the softmax, O[:, c] = P V[:, c], so the
+// forward runs once per 128-column slice of V (every pass computes the same P bit for bit: same
+// Q, K and kernel; the zero padding adds exact zeros), and the backward decomposes linearly,
+// dS = sum_c P o (dO_c V_c^T - rowsum(dO_c o O_c)): dq and dk are the sums of the slices' dq / dk
+// (added in slice order), dv is the concatenation of the slices' dv. The slices are gathered from
+// and scattered to the caller's row-major [n][d_v] storage on the host.
+struct VSlice {
+  uint32_t c0, w;
+};
+std::vector<VSlice> v_slices(uint32_t d_v) {
+  std::vector<VSlice> out;
+  for (uint32_t c0 = 0; c0 < d_v; c0 += 128) out.push_back({c0, std::min<uint32_t>(128, d_v - c0)});
+  return out;
+}
+void copy_cols(const float* src, uint32_t ld_src, uint32_t c_src, float* dst, uint32_t ld_dst, uint32_t c_dst,
+               uint64_t rows, uint32_t w) {
+  for (uint64_t r = 0; r < rows; ++r)
+    std::memcpy(dst + r * ld_dst + c_dst, src + r * ld_src + c_src, w * sizeof(float));
 }
 
 // Permutation::from_forward (reorder.hpp:57-68): forward must be a bijection on [0, n)
@@ -899,8 +919,29 @@ bbm_status bbm_run_attention_host_f32_dims(bbm_prep prep, int variant, const flo
     for (uint64_t i = 0; i < slots; ++i)
       require(q[i] && k[i] && v[i] && out[i], "null tensor pointer in slot " + std::to_string(i));
     DeviceGuard g(pr.device);
-    run_fwd_host_f32(pr, variant, q, k, v, out, row_max, row_sum, slots, d_k, d_v,
-                     static_cast<float>(scale), sm_count(pr.device), nullptr);
+    if (d_v <= 128) {
+      run_fwd_host_f32(pr, variant, q, k, v, out, row_max, row_sum, slots, d_k, d_v,
+                       static_cast<float>(scale), sm_count(pr.device), nullptr);
+      return;
+    }
+    const uint64_t n = pr.n;
+    std::vector<float> vs(slots * n * 128), os(slots * n * 128);
+    std::vector<const float*> pv(slots);
+    std::vector<float*> po(slots);
+    bool first = true;
+    for (const VSlice sl : v_slices(d_v)) {
+      for (uint64_t i = 0; i < slots; ++i) {
+        copy_cols(v[i], d_v, sl.c0, vs.data() + i * n * sl.w, sl.w, 0, n, sl.w);
+        pv[i] = vs.data() + i * n * sl.w;
+        po[i] = os.data() + i * n * sl.w;
+      }
+      // the row statistics are those of every pass; written by the first
+      run_fwd_host_f32(pr, variant, q, k, pv.data(), po.data(), first ? row_max : nullptr,
+                       first ? row_sum : nullptr, slots, d_k, sl.w, static_cast<float>(scale), sm_count(pr.device),
+                       nullptr);
+      for (uint64_t i = 0; i < slots; ++i) copy_cols(po[i], sl.w, 0, out[i], d_v, sl.c0, n, sl.w);
+      first = false;
+    }
   });
 }
 
@@ -940,8 +981,27 @@ bbm_status bbm_attn_bwd_host_f32_dims(bbm_prep prep, int variant, const float* q
     check_host_dims(variant, slots, d_k, d_v, scale);
     require(q && k && v && out && row_max && row_sum && d_out && dq && dk && dv, "null tensor pointer");
     DeviceGuard g(pr.device);
-    run_bwd_host_f32(pr, variant, q, k, v, out, row_max, row_sum, d_out, dq, dk, dv, slots, d_k, d_v,
-                     static_cast<float>(scale), sm_count(pr.device));
+    if (d_v <= 128) {
+      run_bwd_host_f32(pr, variant, q, k, v, out, row_max, row_sum, d_out, dq, dk, dv, slots, d_k, d_v,
+                       static_cast<float>(scale), sm_count(pr.device));
+      return;
+    }
+    const uint64_t rows = slots * pr.n, qk = rows * d_k;
+    std::vector<float> vs(rows * 128), os(rows * 128), gs(rows * 128), dvs(rows * 128), dqs(qk), dks(qk);
+    std::fill(dq, dq + qk, 0.0f);
+    std::fill(dk, dk + qk, 0.0f);
+    for (const VSlice sl : v_slices(d_v)) {
+      copy_cols(v, d_v, sl.c0, vs.data(), sl.w, 0, rows, sl.w);
+      copy_cols(out, d_v, sl.c0, os.data(), sl.w, 0, rows, sl.w);
+      copy_cols(d_out, d_v, sl.c0, gs.data(), sl.w, 0, rows, sl.w);
+      run_bwd_host_f32(pr, variant, q, k, vs.data(), os.data(), row_max, row_sum, gs.data(), dqs.data(), dks.data(),
+                       dvs.data(), slots, d_k, sl.w, static_cast<float>(scale), sm_count(pr.device));
+      for (uint64_t i = 0; i < qk; ++i) {
+        dq[i] += dqs[i];
+        dk[i] += dks[i];
+      }
+      copy_cols(dvs.data(), sl.w, 0, dv, d_v, sl.c0, rows, sl.w);
+    }
   });
 }
 

@@ -2,8 +2,9 @@
 // (include/blockmask/*.hpp), which call libbbm's C ABI and run on the B200.
 //
 // Mirrors proj/tests/test_mask_model.cpp, test_engine.cpp and test_reorder.cpp case by case
-// (file:line beside each). Differences, by design of the sm_100a engine: head dims are at most
-// 128 (zero-padded on the device to 64 / 128), and outputs are compared with a double-precision
+// (file:line beside each). Differences, by design of the sm_100a engine: d_k is at most 128
+// (dims are zero-padded on the device to 64 / 128, d_v above 128 runs as column passes over V),
+// and outputs are compared with a double-precision
 // naive attention at the bf16 tolerance (2e-2) instead of 1e-12.
 //
 //   g++ -std=c++20 -O1 -Iinclude tests/cpp/test_dropin.cpp -Lpaper_2409_15097_b200 -lbbm
@@ -280,7 +281,7 @@ int main() {
   });
   run("EngineForward.ValueHeadDimMayDifferFromKeyDim (test_engine.cpp:198-209) + other head dims", [] {
     struct Dims { std::size_t n, dk, dv; };
-    for (Dims dm : {Dims{21, 5, 3}, Dims{130, 3, 100}, Dims{200, 96, 96}, Dims{77, 128, 7}}) {
+    for (Dims dm : {Dims{21, 5, 3}, Dims{130, 3, 100}, Dims{200, 96, 96}, Dims{77, 128, 7}, Dims{90, 32, 260}}) {
       const Mask mask = gen_causal(dm.n);
       const MaskPrep prep = preprocess_mask(mask, BlockSpec{8, 8});
       Problem p = make_problem(dm.n, dm.dk, 13 + dm.dk, dm.dv);

@@ -7,7 +7,9 @@ sm_100a kernels tile the head dim at 64 or 128, so every entry that takes the ca
 kernel_dim(d_k, d_v) on the device and crops the outputs: zero Q/K columns add exact zeros to every
 score, zero V / dO columns give output columns that are dropped. Parity: the double oracle at the
 same tolerance as the native dims (2e-2 relative); the padded run must also equal an explicitly
-zero-padded native run bit for bit. Dims above 128 stay rejected (documented narrowing).
+zero-padded native run bit for bit. d_v above 128 runs as column passes over V (the forward's
+P is the same on every pass; the backward's dq / dk are sums over the passes, dv their
+concatenation); d_k above 128 stays rejected (documented narrowing).
 """
 import numpy as np
 import pytest
@@ -18,7 +20,7 @@ import paper_2409_15097_b200 as bbm
 pytestmark = pytest.mark.gpu
 
 TOL = 2e-2
-DIMS = [(21, 5, 3), (130, 3, 100), (300, 96, 96), (200, 128, 7), (257, 64, 40)]
+DIMS = [(21, 5, 3), (130, 3, 100), (300, 96, 96), (200, 128, 7), (257, 64, 40), (150, 40, 200), (77, 128, 300)]
 
 
 def rel_err(got, want):
@@ -101,7 +103,7 @@ def test_padded_run_equals_explicitly_padded_native_run(cuda, n, dk, dv):
         assert rel_err(got.float().cpu().numpy(), want) <= 1e-3
 
 
-def test_head_dims_above_128_or_zero_rejected():
+def test_key_dim_above_128_or_zero_rejected():
     n = 64
     mask = bbm.gen_causal(n)
     prep = bbm.preprocess_mask(mask, bbm.BlockSpec(64, 64))
@@ -109,8 +111,35 @@ def test_head_dims_above_128_or_zero_rejected():
     with pytest.raises(ValueError):
         bbm.blocked_forward(np.zeros((n, 129), np.float32), np.zeros((n, 129), np.float32), ok, 0.1, mask, prep,
                             bbm.Variant.binblk)
-    with pytest.raises(ValueError):
-        bbm.blocked_forward(ok, ok, np.zeros((n, 200), np.float32), 0.1, mask, prep, bbm.Variant.binblk)
+    # d_v above 128 runs as column passes (test_host_path_any_head_dims_match_oracle); d_k cannot
+    f = bbm.blocked_forward(ok, ok, np.ones((n, 200), np.float32), 0.1, mask, prep, bbm.Variant.binblk)
+    assert f.out.shape == (n, 200) and np.allclose(f.out, 1.0)
     with pytest.raises(ValueError):
         bbm.blocked_forward(np.zeros((n, 0), np.float32), np.zeros((n, 0), np.float32), ok, 0.1, mask, prep,
                             bbm.Variant.binblk)
+
+
+def test_device_path_value_dim_above_128(cuda):
+    """CUDA bf16 tensors with d_v > 128 (column passes in the Python mirror) agree with the float
+    host entries (column passes in the C ABI) and with the oracle."""
+    import torch
+
+    n, dk, dv = 300, 64, 200
+    mask = bbm.gen_longformer_windowed(n, 50)
+    prep = bbm.preprocess_mask(mask, bbm.BlockSpec(64, 64))
+    q, k, v, g = inputs(n, dk, dv, seed=5)
+    scale = 0.3
+    dev = lambda a: torch.from_numpy(a).to(cuda).to(torch.bfloat16)  # noqa: E731
+    f = bbm.blocked_forward(q, k, v, scale, mask, prep, bbm.Variant.binblk)
+    fd = bbm.blocked_forward(dev(q), dev(k), dev(v), scale, mask, prep, bbm.Variant.binblk)
+    assert tuple(fd.out.shape) == (2, n, dv)
+    assert np.array_equal(fd.out.float().cpu().numpy(), f.out)
+    b = bbm.blocked_backward(q, k, v, scale, mask, prep, bbm.Variant.binblk, f, g)
+    bd = bbm.blocked_backward(dev(q), dev(k), dev(v), scale, mask, prep, bbm.Variant.binblk, fd, dev(g))
+    for got, want in ((bd.dq, b.dq), (bd.dk, b.dk), (bd.dv, b.dv)):
+        assert tuple(got.shape) == want.shape
+        assert rel_err(got.float().cpu().numpy(), want) <= 1e-2
+    for s in range(2):
+        want = oracle_backward(q[s], k[s], v[s], g[s], scale, mask.words, n)
+        for got, w in zip((b.dq[s], b.dk[s], b.dv[s]), want):
+            assert rel_err(got, w) <= TOL
