@@ -621,8 +621,8 @@ void run_bwd_host_f32(const Prep& prep, int variant, const float* q, const float
 // The RCM path end to end (reorder.hpp:156-189 + bench.hpp:448-467): the caller's Q/K/V are in
 // the ORIGINAL token order, `prep` was built from permute_mask(mask, perm), forward = perm's
 // new -> old map. Per slot chunk: H2D, the forward with the permutation applied on the device
-// (launch_attn_fwd with AttnArgs::rows: by default K / V permuted into per-stream scratch, Q rows
-// gathered and O rows / row statistics scattered to their original tokens inside the kernel), D2H.
+// (launch_attn_fwd with AttnArgs::rows: by default every Q / K / V row gathered inside the kernel
+// by LSU cp.async, O rows and row statistics written to their original tokens), D2H.
 void run_fwd_host_rcm(const Prep& prep, int variant, const uint32_t* forward, const uint16_t* q,
                       const uint16_t* k, const uint16_t* v, uint16_t* out, float* row_max,
                       float* row_sum, uint64_t slots, uint32_t d, float scale, int num_sms,
