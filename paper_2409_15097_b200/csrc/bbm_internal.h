@@ -262,7 +262,8 @@ struct AttnArgs {
   // the permuted mask: rows are gathered / scattered by TMA inside the kernel (kGatherTma), or
   // permuted into per-stream scratch by HBM-bound passes around the plain kernel (kGatherPasses),
   // or K / V permuted by passes while Q / O rows are gathered / scattered in the kernel
-  // (kGatherHybrid).
+  // (kGatherHybrid), or every row gathered inside the kernel by LSU cp.async (kGatherLsu, the
+  // default: gather_mode_of in attn_fwd.cu).
   const uint32_t* rows = nullptr;
   int gather_mode = 0;
 };
