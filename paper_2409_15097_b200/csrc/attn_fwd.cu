@@ -444,6 +444,20 @@ __global__ void __launch_bounds__(kThreadsOf<D>, 1)
       // K cursor (claims and publishes items, loads Q)
       ItemDesc kit{};
       uint32_t kj = 0, kk = 0, kentry = 0, khalf = 0;
+      uint32_t kentry2 = 0;             // LSU gather: the list entry two K tiles ahead
+      uint32_t ktok[2] = {0u, 0u};      // LSU gather: the next K tile's raw rows[] values (in flight)
+      // this warp's rows[] values of key tile `tile` (rows (i0 + ii) * 32 + lane, i0 = 0 / 2),
+      // 0xFFFFFFFF past n; predicated loads, nothing consumes them until the tile is issued
+      auto lsu_tokens = [&](uint32_t, uint32_t tile, uint32_t (&t)[2]) {
+        const uint32_t i0 = warp == 0 ? 0u : 2u;
+#pragma unroll
+        for (uint32_t ii = 0; ii < 2; ++ii) {
+          const uint64_t a = static_cast<uint64_t>(tile) * 128 + (i0 + ii) * 32 + lane;
+          uint32_t v = 0xFFFFFFFFu;
+          if (a < p.n) v = __ldg(p.rows + a);
+          t[ii] = v;
+        }
+      };
       bool k_need = true, k_done = false;
       auto k_next = [&]() -> bool {
         while (k_need) {
@@ -474,6 +488,10 @@ __global__ void __launch_bounds__(kThreadsOf<D>, 1)
           pit[pw++ % kQueue] = d;
           kentry = entry_of<MODE>(p, d.rt, d.j0);
           khalf = half_of<MODE, kGKV, kSkip>(p, d.rt, d.j0);
+          if constexpr (kLsu) {  // entries run two tiles ahead, row tokens one (issue_k)
+            kentry2 = d.nt > 1 ? entry_of<MODE>(p, d.rt, d.j0 + 1) : 0u;
+            lsu_tokens(d.slot, kentry & 0x7FFFFFFFu, ktok);
+          }
           mbar_wait(&ctl->q_empty[qb], qph[qb]);
           qph.flip(qb);
           if (lane == 0 && !kLsu) mbar_arrive_expect_tx(&ctl->q_full[qb], C::kTileBytes);
@@ -489,13 +507,31 @@ __global__ void __launch_bounds__(kThreadsOf<D>, 1)
       };
       auto issue_k = [&]() {
         const uint32_t cur = kentry, chalf = khalf;
-        // the next list entry is fetched now, a full issue step before it is needed
-        if (kj + 1 < kit.nt) {
-          kentry = entry_of<MODE>(p, kit.rt, kit.j0 + kj + 1);
-          khalf = half_of<MODE, kGKV, kSkip>(p, kit.rt, kit.j0 + kj + 1);
+        if constexpr (kLsu) {
+          // LSU gather: this tile's tokens were looked up a step ago (ktok); the next tile's entry
+          // (fetched two steps ago) gives its tokens now, and the entry after that is fetched
+          const uint32_t r0 = ktok[0], r1 = ktok[1];
+          if (kj + 1 < kit.nt) {
+            kentry = kentry2;
+            if (kj + 2 < kit.nt) kentry2 = entry_of<MODE>(p, kit.rt, kit.j0 + kj + 2);
+            lsu_tokens(kit.slot, kentry & 0x7FFFFFFFu, ktok);
+          }
+          auto tok_of = [&](uint32_t raw) {
+            return raw == 0xFFFFFFFFu ? INT32_MAX
+                                      : static_cast<int32_t>(static_cast<uint64_t>(kit.slot) * p.n + raw);
+          };
+          int32_t* save = ctl->lsu_tok[warp == 0 ? 0 : 1][kk % 8];
+          save[lane] = tok_of(r0);
+          save[32 + lane] = tok_of(r1);
+          load_tile(&tm_k, &tm_k64, kseq_of(kk), cur & 0x7FFFFFFFu, kit.slot, 2, kj, chalf, save, nullptr);
+        } else {
+          // the next list entry is fetched now, a full issue step before it is needed
+          if (kj + 1 < kit.nt) {
+            kentry = entry_of<MODE>(p, kit.rt, kit.j0 + kj + 1);
+            khalf = half_of<MODE, kGKV, kSkip>(p, kit.rt, kit.j0 + kj + 1);
+          }
+          load_tile(&tm_k, &tm_k64, kseq_of(kk), cur & 0x7FFFFFFFu, kit.slot, 2, kj, chalf, nullptr, nullptr);
         }
-        load_tile(&tm_k, &tm_k64, kseq_of(kk), cur & 0x7FFFFFFFu, kit.slot, 2, kj, chalf, nullptr,
-                  kLsu ? ctl->lsu_tok[warp == 0 ? 0 : 1][kk % 8] : nullptr);
         ++kk;
         if (++kj == kit.nt) k_need = true;
       };
@@ -1207,8 +1243,8 @@ void launch_d(const Prep& prep, const AttnArgs& a, cudaStream_t s, int num_sms) 
 // Which RCM application a gather launch uses: BBM_GATHER=tma|passes|hybrid|lsu overrides
 // (measurement). The default is the fastest on B200 and needs no scratch: every Q / K / V row
 // gathered inside the kernel by LSU cp.async (two producer warps, 16 B per lane, four whole
-// 128-byte box rows per warp instruction, row tokens looked up once per key tile; C5 2.10 ms
-// against 1.43 ms pre-permuted). The TMA
+// 128-byte box rows per warp instruction, row tokens looked up once per key tile, one tile
+// ahead; C5 1.98 ms against 1.42 ms pre-permuted). The TMA
 // tile::gather4 variant moves 4 rows (512 B) per TMA instruction and the TMA unit issues one
 // every ~60 cycles (6.4 ms); the hybrid permutes K / V by passes and gathers Q / O with TMA
 // (2.65 ms); passes over Q, K, V, O and the statistics around the plain kernel take 2.85 ms.
